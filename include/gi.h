@@ -1,0 +1,188 @@
+/*
+ * gi.h — C ABI of the B200-native edgeset.apply library (GraphIt hot path).
+ *
+ * The library implements the paper's edge-traversal operator
+ *     edges.from(frontier).to(filter).apply(f)
+ * in its pull (DensePull, CSC gather), push (SparsePush / DensePush, CSR
+ * scatter with atomics) and direction-optimising hybrid (DensePull-SparsePush,
+ * P:661-675) forms, instantiated for fixed-iteration PageRank (P:855-856,
+ * P:2286, vertex update P:3242-3253 [draft]) and BFS (parent vector
+ * initialised to -1; applyModified without dedup).
+ *
+ * Conventions for every function:
+ *   - returns gi_status; never throws, never exits, never prints;
+ *   - on error, a thread-local message is available from gi_last_error()
+ *     until the next call from the same thread; outputs are unspecified and
+ *     any graph passed in stays valid;
+ *   - calls are stream-ordered on the context's CUDA stream and RETURN AFTER
+ *     COMPLETION (the stream is synchronised before returning); asynchronous
+ *     CUDA faults surface at that synchronisation as GI_ERR_CUDA;
+ *   - pointer arguments may be host or device memory unless stated; the
+ *     library detects which with cudaPointerGetAttributes and copies as needed;
+ *   - input arrays are borrowed for the duration of the call (copied);
+ *     outputs are caller-allocated with the stated length.
+ * There is no CPU fallback: without a usable CUDA device every call that
+ * needs one fails with GI_ERR_CUDA.
+ */
+#ifndef GI_H_
+#define GI_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GI_ABI_VERSION 1
+
+typedef enum {
+  GI_OK = 0,
+  GI_ERR_INVALID_ARGUMENT = 1,  /* null pointer, negative size, bad flag/option */
+  GI_ERR_VERTEX_OUT_OF_RANGE = 2, /* an endpoint or source not in [0, n) */
+  GI_ERR_OUT_OF_MEMORY = 3,     /* device or host allocation failed */
+  GI_ERR_CUDA = 4,              /* CUDA runtime error (incl. async faults) */
+  GI_ERR_NCCL = 5,              /* NCCL missing or a collective failed */
+  GI_ERR_UNSUPPORTED = 6,       /* valid request this build cannot serve */
+  GI_ERR_INTERNAL = 7           /* invariant violated inside the library */
+} gi_status;
+
+typedef struct gi_context_s* gi_context; /* device, CUDA stream, optional NCCL comm */
+typedef struct gi_graph_s* gi_graph;     /* device CSR + CSC + degrees (+ partition) */
+
+/* ---------------------------------------------------------------- context */
+
+/* device: CUDA ordinal. cuda_stream: a cudaStream_t to order all work on, or
+ * NULL for a stream owned by the context. */
+gi_status gi_context_create(int device, void* cuda_stream, gi_context* out);
+
+/* Multi-GPU (one process per GPU): rank 0 calls
+ * gi_nccl_unique_id, broadcasts the 128 bytes (e.g. with torch.distributed),
+ * then every rank calls gi_context_create_dist. NCCL is loaded at run time
+ * (dlopen "libnccl.so.2"); GI_ERR_NCCL if it cannot be. */
+gi_status gi_nccl_unique_id(unsigned char id[128]);
+gi_status gi_context_create_dist(int device, void* cuda_stream, int rank, int nranks,
+                                 const unsigned char id[128], gi_context* out);
+gi_status gi_context_destroy(gi_context ctx);
+gi_status gi_context_rank(gi_context ctx, int* rank, int* nranks);
+
+/* ---------------------------------------------------------------- graph */
+
+/* flags for gi_graph_create */
+enum {
+  GI_EDGES_ON_DEVICE = 1u << 0,   /* hint: src/dst are device pointers (checked) */
+  GI_REMOVE_SELF_LOOPS = 1u << 1, /* drop (u,u) pairs (reading R5) */
+  GI_DEDUP = 1u << 2,             /* keep one copy of repeated (u,v) (R5) */
+  GI_SYMMETRIZE = 1u << 3,        /* add (v,u) for every (u,v): "an undirected
+                                     graph would be represented by duplicating
+                                     the directed edges" P:3183 [draft] */
+  GI_NO_RELABEL = 1u << 4         /* keep input vertex order internally (the
+                                     default relabels by out-degree; results are
+                                     always reported in input ids) */
+};
+
+/* Builds the edgeset from an edge list ("edges = load(...)"):
+ *   num_vertices n: V = {0..n-1}; isolated ids are vertices (reading R4);
+ *                   0 <= n <= 2^31-1.
+ *   num_edges m0:   length of src/dst (int32 vertex ids), 0 <= m0 < 2^40.
+ *   flags:          GI_* above; unknown bits -> GI_ERR_INVALID_ARGUMENT.
+ * Any endpoint outside [0, n) -> GI_ERR_VERTEX_OUT_OF_RANGE.
+ * Device work: validate, clean (self-loops, symmetrise, dedup) by radix sort
+ * of 64-bit keys, CSR by source, CSC by destination, out-degrees, pull-kernel
+ * tiling metadata.
+ * Multi-GPU context: every rank passes ANY share of the edge list; the graph
+ * is the union. The graph owns its device memory until gi_graph_destroy. */
+gi_status gi_graph_create(gi_context ctx, int64_t num_vertices, int64_t num_edges,
+                          const int32_t* src, const int32_t* dst, uint32_t flags,
+                          gi_graph* out);
+gi_status gi_graph_destroy(gi_graph g);
+gi_status gi_graph_num_vertices(gi_graph g, int64_t* n);
+gi_status gi_graph_num_edges(gi_graph g, int64_t* m); /* global m after cleanup */
+
+/* Test hooks (length n, input ids; host or device pointers). */
+gi_status gi_graph_out_degrees(gi_graph g, int32_t* outdeg);
+gi_status gi_graph_in_degrees(gi_graph g, int32_t* indeg);
+/* Cleaned CSR in input ids: off[n+1] (int64), idx[m] (int32, ascending per row).
+ * Single-GPU graphs only. */
+gi_status gi_graph_csr(gi_graph g, int64_t* off, int32_t* idx);
+
+/* ---------------------------------------------------------------- PageRank */
+
+/* Fixed-iteration Jacobi PageRank, fp32 storage (reading R10):
+ *   r_0[v] = 1/n                                                  (R2)
+ *   r_{k+1}[v] = (1-d)/n + d * ( sum_{(u,v) in E} r_k[u]/outdeg(u) + D_k/n )
+ *   D_k = sum over dangling u (outdeg 0) of r_k[u]      (uniform rule, R3)
+ * P:3242-3253 [draft], base score P:856, fixed MaxIter P:514-517.
+ *   iters >= 0 (iters = 0 gives 1/n), damping in [0, 1].
+ *   out: float[n] in input ids (host or device).
+ * n = 0 -> GI_OK, nothing written. */
+gi_status gi_pagerank(gi_graph g, int32_t iters, double damping, float* out);
+
+enum { GI_PR_PULL = 0, GI_PR_PUSH = 1, GI_PR_PULL_DIRECT = 2, GI_PR_PULL_SEGMENTED = 3 };
+enum { GI_DANGLING_UNIFORM = 0, GI_DANGLING_DROP = 1 };
+typedef struct {
+  int32_t direction; /* GI_PR_PULL (auto-selected pull kernel), GI_PR_PUSH
+                        (DensePush with atomics, the parity form),
+                        GI_PR_PULL_DIRECT (CSC gather via L1/L2),
+                        GI_PR_PULL_SEGMENTED (shared-memory source segments) */
+  int32_t dangling;  /* GI_DANGLING_UNIFORM (default) or GI_DANGLING_DROP
+                        (paper-literal: no D term) */
+  int32_t profile;   /* 1: fill gi_pr_stats kernel timings (CUDA events on the
+                        context stream around every edge-pass launch) */
+  int32_t reserved;
+} gi_pr_opts;
+
+typedef struct {
+  int32_t edge_launches;   /* edge-pass kernel launches (one per iteration) */
+  int32_t aux_launches;    /* other kernel launches in the call */
+  float edge_ms;           /* sum of edge-pass kernel durations (profile=1) */
+  float total_ms;          /* whole call on the stream (profile=1) */
+  int32_t kernel;          /* GI_PR_* kernel actually used */
+  int32_t reserved;
+  int64_t bytes_alg_per_iter; /* 4m + (o+12)n for pull */
+} gi_pr_stats;
+
+gi_status gi_pagerank_ex(gi_graph g, int32_t iters, double damping, const gi_pr_opts* opts,
+                         float* out, gi_pr_stats* stats /* may be NULL */);
+
+/* ---------------------------------------------------------------- BFS */
+
+/* Breadth-first search from `source` along out-edges (R9), direction-
+ * optimising by default: pull (DensePull + bitmap frontier + early exit) iff
+ * |F| + sum_{v in F} outdeg(v) > m / threshold_div, else push (SparsePush +
+ * queue frontier + CAS claim) (Ligra's m/20 P:3074 [punt], R7).
+ *   parent_out: int32[n] in input ids; parent[source] = source, parent[v] = -1
+ *   when unreachable, otherwise an in-neighbour one level closer to the source
+ *   (any valid one, R8). */
+gi_status gi_bfs(gi_graph g, int32_t source, int32_t* parent_out);
+
+enum { GI_BFS_AUTO = 0, GI_BFS_PUSH_ONLY = 1, GI_BFS_PULL_ONLY = 2 };
+typedef struct {
+  int32_t policy;        /* GI_BFS_AUTO / PUSH_ONLY / PULL_ONLY (pull-only runs
+                            the first level as push: a 1-vertex frontier) */
+  int32_t threshold_div; /* 0 -> 20 */
+  int32_t profile;       /* 1: fill timing fields of gi_bfs_stats */
+  int32_t reserved;
+} gi_bfs_opts;
+
+typedef struct {
+  int32_t levels;          /* frontier rounds executed */
+  int32_t pull_levels;     /* rounds run in the pull direction */
+  int64_t reached;         /* vertices with parent != -1 */
+  int64_t edges_traversed; /* R16: sum of outdeg over reached vertices */
+  float total_ms;          /* profile=1 */
+  int32_t launches;        /* kernel launches in the call */
+  int32_t reserved;
+} gi_bfs_stats;
+
+gi_status gi_bfs_ex(gi_graph g, int32_t source, const gi_bfs_opts* opts, int32_t* parent_out,
+                    gi_bfs_stats* stats /* may be NULL */);
+
+/* ---------------------------------------------------------------- misc */
+const char* gi_status_string(gi_status s);
+const char* gi_last_error(void); /* thread-local; valid until the next call */
+int gi_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GI_H_ */

@@ -1,0 +1,223 @@
+/*
+ * gi_oracle.c — the CPU ORACLE for the edgeset.apply hot path (PageRank, BFS).
+ *
+ * TEST INFRASTRUCTURE ONLY. Only tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline / --impl reference legs may load this library.
+ * It shares no code, header, table or constant generator with the CUDA
+ * library (paper_1805_00923_b200/csrc, include/gi.h); neither includes the
+ * other. It is plain, slow and written to be checked against the paper by eye.
+ *
+ * What it computes (PAPER.md = P, SPEC.md = S, readings = R):
+ *
+ *  Graph (or_build)   P:853-858 "edges = load(...)", "vertices =
+ *      edges.getVertices()", "OutDegree = edges.getOutDegrees()"; edgeset as
+ *      CSR/CSC P:3183 [draft]. V = {0..n-1} with n given explicitly (R4);
+ *      self-loops removed and duplicates removed on request (R5); optional
+ *      symmetrisation "duplicating the directed edges" P:3183 [draft].
+ *      Sort = qsort of 64-bit (u<<32|v) keys (a library primitive).
+ *
+ *  PageRank (or_pagerank), fp64, Jacobi, fixed iteration count:
+ *      edge update  new_rank[dst] += old_rank[src] / out_degree[src]
+ *                                                    P:3242-3244 [draft]
+ *      vertex update new_rank = beta_score + damp * new_rank  P:3249 [draft]
+ *      beta_score = (1 - damp) / |V|                         P:856 (R1)
+ *      r_0 = 1/|V|                                           (R2)
+ *      dangling mass D_k = sum_{outdeg(u)=0} r_k[u], redistributed as D_k/n
+ *      inside the damped term ("uniform", default) or dropped ("drop",
+ *      the paper-literal rule)                                (R3)
+ *      r_{k+1}[v] = (1-d)/n + d * ( sum_{(u,v) in E} r_k[u]/outdeg(u) + D_k/n )
+ *      fixed MaxIter, no convergence test
+ *    Rows are summed in ascending source order (CSC rows sorted), one
+ *    destination at a time; the OpenMP loop over destinations does not change
+ *    any rounding, so results are bit-identical for every thread count.
+ *
+ *  BFS (or_bfs_depth): depth(s) = 0, depth(v) = length of the shortest
+ *      directed path s ->* v along out-edges, -1 if unreachable; FIFO queue.
+ *      Parent vector semantics: parent = -1 initially P:2093-2099; each vertex
+ *      inserted once P:1021-1025; parent[source] = source S:509 (R8, R9).
+ *
+ *  Validator (or_validate_bfs): Graph500-style. A parent vector is valid iff
+ *      parent[s] = s; parent[v] = -1 <=> depth(v) = -1; otherwise
+ *      (parent[v], v) in E (binary search in the CSR row of parent[v]) and
+ *      depth(parent[v]) = depth(v) - 1. Several parent vectors are valid; they
+ *      are validated, never compared (R8).
+ */
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+typedef struct {
+  int64_t n, m;
+  int64_t* csr_off; /* n+1 */
+  int32_t* csr_idx; /* m, ascending within each row */
+  int64_t* csc_off; /* n+1 */
+  int32_t* csc_idx; /* m, ascending within each row */
+} or_graph;
+
+static int cmp_u64(const void* a, const void* b) {
+  const uint64_t x = *(const uint64_t*)a, y = *(const uint64_t*)b;
+  return x < y ? -1 : (x > y ? 1 : 0);
+}
+
+/* Returns m >= 0 and *out, or -1 (bad argument) / -2 (vertex out of range) /
+ * -3 (out of memory). */
+int64_t or_build(int64_t n, int64_t m0, const int32_t* src, const int32_t* dst,
+                 int remove_self_loops, int dedup, int symmetrize, or_graph** out) {
+  *out = NULL;
+  if (n < 0 || m0 < 0 || n > 2147483647LL) return -1;
+  for (int64_t i = 0; i < m0; ++i)
+    if (src[i] < 0 || src[i] >= n || dst[i] < 0 || dst[i] >= n) return -2;
+  const int64_t cap = symmetrize ? 2 * m0 : m0;
+  uint64_t* key = (uint64_t*)malloc((size_t)(cap > 0 ? cap : 1) * sizeof(uint64_t));
+  if (!key) return -3;
+  int64_t k = 0;
+  for (int64_t i = 0; i < m0; ++i) {
+    const uint32_t u = (uint32_t)src[i], v = (uint32_t)dst[i];
+    if (remove_self_loops && u == v) continue;
+    key[k++] = ((uint64_t)u << 32) | v;
+    if (symmetrize) key[k++] = ((uint64_t)v << 32) | u;
+  }
+  qsort(key, (size_t)k, sizeof(uint64_t), cmp_u64);
+  int64_t m = 0;
+  for (int64_t i = 0; i < k; ++i) {
+    if (dedup && m > 0 && key[m - 1] == key[i]) continue;
+    key[m++] = key[i];
+  }
+  or_graph* g = (or_graph*)calloc(1, sizeof(or_graph));
+  g->n = n;
+  g->m = m;
+  g->csr_off = (int64_t*)calloc((size_t)n + 1, sizeof(int64_t));
+  g->csc_off = (int64_t*)calloc((size_t)n + 1, sizeof(int64_t));
+  g->csr_idx = (int32_t*)malloc((size_t)(m > 0 ? m : 1) * sizeof(int32_t));
+  g->csc_idx = (int32_t*)malloc((size_t)(m > 0 ? m : 1) * sizeof(int32_t));
+  /* CSR: keys are sorted by (u, v). */
+  for (int64_t i = 0; i < m; ++i) {
+    g->csr_off[(key[i] >> 32) + 1]++;
+    g->csr_idx[i] = (int32_t)(key[i] & 0xFFFFFFFFu);
+  }
+  for (int64_t v = 0; v < n; ++v) g->csr_off[v + 1] += g->csr_off[v];
+  /* CSC: re-key as (v, u) and sort again. */
+  for (int64_t i = 0; i < m; ++i) key[i] = (key[i] << 32) | (key[i] >> 32);
+  qsort(key, (size_t)m, sizeof(uint64_t), cmp_u64);
+  for (int64_t i = 0; i < m; ++i) {
+    g->csc_off[(key[i] >> 32) + 1]++;
+    g->csc_idx[i] = (int32_t)(key[i] & 0xFFFFFFFFu);
+  }
+  for (int64_t v = 0; v < n; ++v) g->csc_off[v + 1] += g->csc_off[v];
+  free(key);
+  *out = g;
+  return m;
+}
+
+void or_graph_arrays(const or_graph* g, int64_t* csr_off, int32_t* csr_idx, int64_t* csc_off,
+                     int32_t* csc_idx) {
+  memcpy(csr_off, g->csr_off, (size_t)(g->n + 1) * sizeof(int64_t));
+  memcpy(csc_off, g->csc_off, (size_t)(g->n + 1) * sizeof(int64_t));
+  memcpy(csr_idx, g->csr_idx, (size_t)g->m * sizeof(int32_t));
+  memcpy(csc_idx, g->csc_idx, (size_t)g->m * sizeof(int32_t));
+}
+
+void or_graph_free(or_graph* g) {
+  if (!g) return;
+  free(g->csr_off);
+  free(g->csr_idx);
+  free(g->csc_off);
+  free(g->csc_idx);
+  free(g);
+}
+
+/* dangling_rule: 0 = uniform redistribution (R3 default), 1 = drop. */
+int or_pagerank(const or_graph* g, int iters, double damp, int dangling_rule, double* rank) {
+  const int64_t n = g->n;
+  if (iters < 0 || damp < 0.0 || damp > 1.0) return -1;
+  if (n == 0) return 0;
+  double* r = rank;
+  double* nr = (double*)malloc((size_t)n * sizeof(double));
+  double* outdeg = (double*)malloc((size_t)n * sizeof(double));
+  if (!nr || !outdeg) { free(nr); free(outdeg); return -3; }
+  for (int64_t u = 0; u < n; ++u) outdeg[u] = (double)(g->csr_off[u + 1] - g->csr_off[u]);
+  for (int64_t v = 0; v < n; ++v) r[v] = 1.0 / (double)n;
+  const double base = (1.0 - damp) / (double)n;
+  for (int it = 0; it < iters; ++it) {
+    double D = 0.0;
+    for (int64_t u = 0; u < n; ++u)
+      if (outdeg[u] == 0.0) D += r[u];
+    const double spread = dangling_rule == 0 ? D / (double)n : 0.0;
+#pragma omp parallel for schedule(dynamic, 4096)
+    for (int64_t v = 0; v < n; ++v) {
+      double s = 0.0;
+      for (int64_t j = g->csc_off[v]; j < g->csc_off[v + 1]; ++j) {
+        const int32_t u = g->csc_idx[j];
+        s += r[u] / outdeg[u];
+      }
+      nr[v] = base + damp * (s + spread);
+    }
+    memcpy(r, nr, (size_t)n * sizeof(double));
+  }
+  free(nr);
+  free(outdeg);
+  return 0;
+}
+
+/* FIFO BFS over out-edges; depth[v] = -1 when unreachable. */
+int or_bfs_depth(const or_graph* g, int32_t source, int32_t* depth) {
+  const int64_t n = g->n;
+  if (source < 0 || source >= n) return -2;
+  int32_t* q = (int32_t*)malloc((size_t)n * sizeof(int32_t));
+  if (!q) return -3;
+  for (int64_t v = 0; v < n; ++v) depth[v] = -1;
+  int64_t head = 0, tail = 0;
+  depth[source] = 0;
+  q[tail++] = source;
+  while (head < tail) {
+    const int32_t u = q[head++];
+    for (int64_t j = g->csr_off[u]; j < g->csr_off[u + 1]; ++j) {
+      const int32_t v = g->csr_idx[j];
+      if (depth[v] < 0) {
+        depth[v] = depth[u] + 1;
+        q[tail++] = v;
+      }
+    }
+  }
+  free(q);
+  return 0;
+}
+
+static int has_edge(const or_graph* g, int32_t u, int32_t v) {
+  int64_t lo = g->csr_off[u], hi = g->csr_off[u + 1];
+  while (lo < hi) {
+    const int64_t mid = lo + (hi - lo) / 2;
+    if (g->csr_idx[mid] < v) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo < g->csr_off[u + 1] && g->csr_idx[lo] == v;
+}
+
+/* Returns 0 if valid; otherwise 1 + the index of the failed rule and sets
+ * *bad_vertex:  1 root not self-parent, 2 reachability mismatch,
+ * 3 parent out of range, 4 parent edge missing, 5 depth(parent) != depth-1. */
+int or_validate_bfs(const or_graph* g, int32_t source, const int32_t* depth,
+                    const int32_t* parent, int64_t* bad_vertex) {
+  const int64_t n = g->n;
+  *bad_vertex = -1;
+  if (parent[source] != source) { *bad_vertex = source; return 1; }
+  for (int64_t v = 0; v < n; ++v) {
+    if (v == source) continue;
+    const int32_t p = parent[v];
+    if ((p == -1) != (depth[v] == -1)) { *bad_vertex = v; return 2; }
+    if (p == -1) continue;
+    if (p < 0 || p >= n) { *bad_vertex = v; return 3; }
+    if (!has_edge(g, p, (int32_t)v)) { *bad_vertex = v; return 4; }
+    if (depth[p] != depth[v] - 1) { *bad_vertex = v; return 5; }
+  }
+  return 0;
+}
+
+/* Edge count examined by a BFS tree in TEPS terms (R16): sum of outdeg over
+ * reached vertices. */
+int64_t or_reached_out_edges(const or_graph* g, const int32_t* depth) {
+  int64_t s = 0;
+  for (int64_t v = 0; v < g->n; ++v)
+    if (depth[v] >= 0) s += g->csr_off[v + 1] - g->csr_off[v];
+  return s;
+}
