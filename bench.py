@@ -1,0 +1,366 @@
+#!/usr/bin/env python3
+"""bench.py — GTEPS of the edgeset.apply hot path (PageRank 20 iters + BFS) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl ours|reference]
+
+One step = the whole hot path over the workload
+BASELINE.json's metric is quoted on at N=1 (configs[1] = RMAT s22 ef16,
+"config 2"): fixed-iteration PageRank (20 iterations, d = 0.85, pull) plus
+BFS from 64 seeded random sources (direction-optimising). The graph build
+(a1) runs once before timing and is reported separately (`build_ms`), as the
+paper's Table 4 times the algorithms, not loading.
+
+value  = (20 m + sum over sources of edges traversed) / device time, all ranks
+         (GTEPS), inputs resident in HBM, CUDA events on the library's stream.
+e2e    = the same edges over the time of the public C-ABI calls with HOST
+         buffers: gi_graph_create from pinned host edges (H2D inside),
+         gi_pagerank into host memory, gi_bfs x 64 into host memory.
+roofline: the pull-PageRank edge kernel (dominant), algorithmic bytes
+         4m + (o+12)n per launch / its CUDA-event duration.
+cpu_baseline: the oracle (oracle/, plain C, OpenMP) on a bounded sample of
+         the same graph (2 PR iterations + 2 BFS sources).
+
+Multi-GPU (torchrun, one process per GPU): the units of this workload are
+independent problems, so N > 1 runs N replicas (weak scaling, no data-path
+collective); see DESIGN.md "Multi-GPU".
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "GTEPS for PageRank iteration and BFS; achieved fraction of HBM roofline"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--pr-direction", default="pull", choices=["pull", "push", "direct", "segmented"])
+    return ap.parse_args()
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def load_traffic():
+    """Per-launch DRAM bytes of the pull kernel from the committed ncu summary (or None)."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if not os.path.exists(p):
+        return None
+    try:
+        d = json.load(open(p))
+        return d.get("pr_pull", {}).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(2)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def workload(cfg_idx):
+    import graphgen
+
+    cfg = graphgen.CONFIGS[cfg_idx]
+    t = time.perf_counter()
+    s, d = cfg.edges()
+    sources = cfg.sources(s, d)
+    return cfg, s, d, sources, time.perf_counter() - t
+
+
+# ---------------------------------------------------------------------------------------------- reference arm
+def run_reference(args):
+    """The oracle (plain C, fp64 PR, FIFO BFS), as it stands, on this host's cores."""
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    import oracle
+
+    cfg, s, d, sources, _ = workload(args.config)
+    t = time.perf_counter()
+    g = oracle.build_graph(cfg.n, s, d, symmetrize=cfg.symmetrize)
+    build_s = time.perf_counter() - t
+    pr_iters, nsrc = 2, 2
+    cores = os.cpu_count()
+
+    def step():
+        t0 = time.perf_counter()
+        oracle.pagerank(g, pr_iters, cfg.damping)
+        edges = g.m * pr_iters
+        for src in sources[:nsrc]:
+            dep = oracle.bfs_depth(g, int(src))
+            edges += oracle.reached_out_edges(g, dep)
+        return edges, time.perf_counter() - t0
+
+    for _ in range(args.warmup):
+        step()
+    tot_e, tot_t = 0, 0.0
+    for _ in range(args.steps):
+        e, dt = step()
+        tot_e += e
+        tot_t += dt
+    gteps = tot_e / tot_t / 1e9
+    sample = (f"{cfg.name}: oracle PageRank {pr_iters} iterations + FIFO BFS from {nsrc} of the {len(sources)} "
+              f"sources per step (graph build {build_s:.1f} s untimed)")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": gteps, "unit": "GTEPS", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot_t / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded RMAT/grid generators; paper datasets not available)",
+        "config": {"workload": cfg.name, "n": cfg.n, "m": g.m},
+        "cpu_baseline": {"value": gteps, "unit": "GTEPS", "cores": cores, "kind": "oracle", "sample": sample},
+        "e2e": {"value": gteps, "unit": "GTEPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------------------------- our arm
+def cpu_baseline(cfg, s, d, sources):
+    import oracle
+
+    t = time.perf_counter()
+    g = oracle.build_graph(cfg.n, s, d, symmetrize=cfg.symmetrize)
+    build_s = time.perf_counter() - t
+    t0 = time.perf_counter()
+    oracle.pagerank(g, 2, cfg.damping)
+    edges = 2 * g.m
+    for src in sources[:2]:
+        edges += oracle.reached_out_edges(g, oracle.bfs_depth(g, int(src)))
+    dt = time.perf_counter() - t0
+    return {"value": edges / dt / 1e9, "unit": "GTEPS", "cores": os.cpu_count(), "kind": "oracle",
+            "sample": f"{cfg.name}: oracle PageRank 2 iterations + FIFO BFS from 2 sources ({dt:.1f} s; "
+                      f"oracle graph build {build_s:.1f} s untimed)"}
+
+
+def run_ours(args):
+    import torch
+
+    rank, world, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.cuda.current_device()
+    from paper_1805_00923_b200 import gi
+
+    stream = torch.cuda.Stream()
+    ctx = gi.Context(dev, stream.cuda_stream)
+    cfg, s, d, sources, gen_s = workload(args.config)
+    flags = gi.GI_DEFAULT_FLAGS | (gi.GI_SYMMETRIZE if cfg.symmetrize else 0)
+    direction = {"pull": gi.GI_PR_PULL, "push": gi.GI_PR_PUSH, "direct": gi.GI_PR_PULL_DIRECT,
+                 "segmented": gi.GI_PR_PULL_SEGMENTED}[args.pr_direction]
+
+    # device-resident inputs; build (a1) timed separately
+    ts = torch.from_numpy(s).to(dev)
+    td = torch.from_numpy(d).to(dev)
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    g = gi.Graph(ctx, cfg.n, ts, td, flags | gi.GI_EDGES_ON_DEVICE)
+    build_ms = (time.perf_counter() - t) * 1e3
+    del ts, td
+    n, m = g.n, g.m
+    pr_out = torch.empty(n, dtype=torch.float32, device=dev)
+    bfs_out = torch.empty(n, dtype=torch.int32, device=dev)
+    srcs = [int(x) for x in sources]
+
+    def step():
+        _, ps = g.pagerank(cfg.pr_iters, cfg.damping, out=pr_out, direction=direction)
+        bfs_edges, launches = 0, ps.edge_launches + ps.aux_launches
+        for src in srcs:
+            _, bs = g.bfs(src, out=bfs_out)
+            bfs_edges += bs.edges_traversed
+            launches += bs.launches
+        return cfg.pr_iters * m, bfs_edges, launches
+
+    for _ in range(max(args.warmup, 0)):
+        step()
+    # phase timings (PR vs BFS), outside the main timed region
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    torch.cuda.synchronize()
+    ev[0].record(stream)
+    g.pagerank(cfg.pr_iters, cfg.damping, out=pr_out, direction=direction)
+    ev[1].record(stream)
+    for src in srcs:
+        g.bfs(src, out=bfs_out)
+    ev[2].record(stream)
+    torch.cuda.synchronize()
+    pr_ms, bfs_ms = ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2])
+
+    # timed region
+    sampler = ClockSampler(dev)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    sampler.start()
+    time.sleep(0.3)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    tot_pr = tot_bfs = launches = 0
+    for _ in range(args.steps):
+        a, b, l = step()
+        tot_pr += a
+        tot_bfs += b
+        launches += l
+    e1.record(stream)
+    torch.cuda.synchronize()
+    clocks = sampler.stop()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        tt = torch.tensor([ms, tot_pr + tot_bfs], dtype=torch.float64, device=dev)
+        mx = tt.clone()
+        torch.distributed.all_reduce(mx[:1], op=torch.distributed.ReduceOp.MAX)
+        torch.distributed.all_reduce(tt[1:], op=torch.distributed.ReduceOp.SUM)
+        ms_max, edges_all = float(mx[0]), float(tt[1])
+    else:
+        ms_max, edges_all = ms, float(tot_pr + tot_bfs)
+    value = edges_all / (ms_max * 1e-3) / 1e9
+
+    # roofline of the dominant kernel (pull PR edge pass): CUDA events around each launch
+    _, ps = g.pagerank(cfg.pr_iters, cfg.damping, out=pr_out, direction=direction, profile=True)
+    kern_ms = ps.edge_ms / max(ps.edge_launches, 1)
+    peak, peak_src = load_peaks()
+    achieved = ps.bytes_alg_per_iter / (kern_ms * 1e-3) / 1e9
+    traffic = load_traffic()
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": traffic, "kernel": "k_pr_pull (pull PageRank edge pass + fused vertex update)",
+                "bytes_alg_per_launch": ps.bytes_alg_per_iter, "launch_ms": kern_ms, "peak_source": peak_src}
+
+    # e2e through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        hs = torch.from_numpy(s).pin_memory()
+        hd = torch.from_numpy(d).pin_memory()
+        hpr = torch.empty(n, dtype=torch.float32).pin_memory()
+        hbfs = torch.empty(n, dtype=torch.int32).pin_memory()
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        e2e_steps = max(1, min(args.steps, 2))
+        e_edges = 0
+        for _ in range(e2e_steps):
+            g2 = gi.Graph(ctx, cfg.n, hs, hd, flags)
+            _, ps2 = g2.pagerank(cfg.pr_iters, cfg.damping, out=hpr, direction=direction)
+            e_edges += cfg.pr_iters * g2.m
+            for src in srcs:
+                _, bs = g2.bfs(src, out=hbfs)
+                e_edges += bs.edges_traversed
+            g2.close()
+        torch.cuda.synchronize()
+        e2e_s = time.perf_counter() - t
+        e2e = {"value": e_edges / e2e_s / 1e9 * world, "unit": "GTEPS", "h2d_bytes_per_step": int(8 * len(s)),
+               "d2h_bytes_per_step": int(4 * n * (1 + len(srcs))), "steps": e2e_steps,
+               "includes": "gi_graph_create from pinned host edges + gi_pagerank + gi_bfs x sources, host outputs"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(cfg, s, d, sources)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "GTEPS", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded counter-based RMAT; stands in for LiveJournal, paper datasets unavailable)",
+            "config": {"workload": f"{cfg.name} (BASELINE configs[{cfg.idx - 1}])", "n": n, "m": m,
+                       "pr_iters": cfg.pr_iters, "damping": cfg.damping, "bfs_sources": len(srcs),
+                       "pr_direction": args.pr_direction, "bfs_policy": "auto (m/20)",
+                       "l2": "inputs larger than L2 (CSR+CSC ~ 8m bytes > 126 MB), no flush",
+                       "parallelism": f"replicas x{world}" if world > 1 else "single"},
+            "e2e": e2e, "gpu_launches": launches, "roofline": roofline, "cpu_baseline": cpu, "clocks": clocks,
+            "pr_gteps": cfg.pr_iters * m / (pr_ms * 1e-3) / 1e9, "pr_ms": pr_ms,
+            "bfs_gteps": (tot_bfs / args.steps) / (bfs_ms * 1e-3) / 1e9 if bfs_ms > 0 else None,
+            "bfs_ms_per_source": bfs_ms / max(len(srcs), 1), "build_ms": build_ms, "gen_s": gen_s,
+        }
+        print(json.dumps(line), flush=True)
+    g.close()
+    ctx.close()
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

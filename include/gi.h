@@ -35,6 +35,12 @@ extern "C" {
 
 #define GI_ABI_VERSION 1
 
+#if defined(__GNUC__)
+#define GI_API __attribute__((visibility("default")))
+#else
+#define GI_API
+#endif
+
 typedef enum {
   GI_OK = 0,
   GI_ERR_INVALID_ARGUMENT = 1,  /* null pointer, negative size, bad flag/option */
@@ -53,17 +59,17 @@ typedef struct gi_graph_s* gi_graph;     /* device CSR + CSC + degrees (+ partit
 
 /* device: CUDA ordinal. cuda_stream: a cudaStream_t to order all work on, or
  * NULL for a stream owned by the context. */
-gi_status gi_context_create(int device, void* cuda_stream, gi_context* out);
+GI_API gi_status gi_context_create(int device, void* cuda_stream, gi_context* out);
 
 /* Multi-GPU (one process per GPU): rank 0 calls
  * gi_nccl_unique_id, broadcasts the 128 bytes (e.g. with torch.distributed),
  * then every rank calls gi_context_create_dist. NCCL is loaded at run time
  * (dlopen "libnccl.so.2"); GI_ERR_NCCL if it cannot be. */
-gi_status gi_nccl_unique_id(unsigned char id[128]);
-gi_status gi_context_create_dist(int device, void* cuda_stream, int rank, int nranks,
+GI_API gi_status gi_nccl_unique_id(unsigned char id[128]);
+GI_API gi_status gi_context_create_dist(int device, void* cuda_stream, int rank, int nranks,
                                  const unsigned char id[128], gi_context* out);
-gi_status gi_context_destroy(gi_context ctx);
-gi_status gi_context_rank(gi_context ctx, int* rank, int* nranks);
+GI_API gi_status gi_context_destroy(gi_context ctx);
+GI_API gi_status gi_context_rank(gi_context ctx, int* rank, int* nranks);
 
 /* ---------------------------------------------------------------- graph */
 
@@ -91,19 +97,19 @@ enum {
  * tiling metadata.
  * Multi-GPU context: every rank passes ANY share of the edge list; the graph
  * is the union. The graph owns its device memory until gi_graph_destroy. */
-gi_status gi_graph_create(gi_context ctx, int64_t num_vertices, int64_t num_edges,
+GI_API gi_status gi_graph_create(gi_context ctx, int64_t num_vertices, int64_t num_edges,
                           const int32_t* src, const int32_t* dst, uint32_t flags,
                           gi_graph* out);
-gi_status gi_graph_destroy(gi_graph g);
-gi_status gi_graph_num_vertices(gi_graph g, int64_t* n);
-gi_status gi_graph_num_edges(gi_graph g, int64_t* m); /* global m after cleanup */
+GI_API gi_status gi_graph_destroy(gi_graph g);
+GI_API gi_status gi_graph_num_vertices(gi_graph g, int64_t* n);
+GI_API gi_status gi_graph_num_edges(gi_graph g, int64_t* m); /* global m after cleanup */
 
 /* Test hooks (length n, input ids; host or device pointers). */
-gi_status gi_graph_out_degrees(gi_graph g, int32_t* outdeg);
-gi_status gi_graph_in_degrees(gi_graph g, int32_t* indeg);
+GI_API gi_status gi_graph_out_degrees(gi_graph g, int32_t* outdeg);
+GI_API gi_status gi_graph_in_degrees(gi_graph g, int32_t* indeg);
 /* Cleaned CSR in input ids: off[n+1] (int64), idx[m] (int32, ascending per row).
  * Single-GPU graphs only. */
-gi_status gi_graph_csr(gi_graph g, int64_t* off, int32_t* idx);
+GI_API gi_status gi_graph_csr(gi_graph g, int64_t* off, int32_t* idx);
 
 /* ---------------------------------------------------------------- PageRank */
 
@@ -115,7 +121,7 @@ gi_status gi_graph_csr(gi_graph g, int64_t* off, int32_t* idx);
  *   iters >= 0 (iters = 0 gives 1/n), damping in [0, 1].
  *   out: float[n] in input ids (host or device).
  * n = 0 -> GI_OK, nothing written. */
-gi_status gi_pagerank(gi_graph g, int32_t iters, double damping, float* out);
+GI_API gi_status gi_pagerank(gi_graph g, int32_t iters, double damping, float* out);
 
 enum { GI_PR_PULL = 0, GI_PR_PUSH = 1, GI_PR_PULL_DIRECT = 2, GI_PR_PULL_SEGMENTED = 3 };
 enum { GI_DANGLING_UNIFORM = 0, GI_DANGLING_DROP = 1 };
@@ -141,7 +147,7 @@ typedef struct {
   int64_t bytes_alg_per_iter; /* 4m + (o+12)n for pull */
 } gi_pr_stats;
 
-gi_status gi_pagerank_ex(gi_graph g, int32_t iters, double damping, const gi_pr_opts* opts,
+GI_API gi_status gi_pagerank_ex(gi_graph g, int32_t iters, double damping, const gi_pr_opts* opts,
                          float* out, gi_pr_stats* stats /* may be NULL */);
 
 /* ---------------------------------------------------------------- BFS */
@@ -153,7 +159,7 @@ gi_status gi_pagerank_ex(gi_graph g, int32_t iters, double damping, const gi_pr_
  *   parent_out: int32[n] in input ids; parent[source] = source, parent[v] = -1
  *   when unreachable, otherwise an in-neighbour one level closer to the source
  *   (any valid one, R8). */
-gi_status gi_bfs(gi_graph g, int32_t source, int32_t* parent_out);
+GI_API gi_status gi_bfs(gi_graph g, int32_t source, int32_t* parent_out);
 
 enum { GI_BFS_AUTO = 0, GI_BFS_PUSH_ONLY = 1, GI_BFS_PULL_ONLY = 2 };
 typedef struct {
@@ -174,13 +180,13 @@ typedef struct {
   int32_t reserved;
 } gi_bfs_stats;
 
-gi_status gi_bfs_ex(gi_graph g, int32_t source, const gi_bfs_opts* opts, int32_t* parent_out,
+GI_API gi_status gi_bfs_ex(gi_graph g, int32_t source, const gi_bfs_opts* opts, int32_t* parent_out,
                     gi_bfs_stats* stats /* may be NULL */);
 
 /* ---------------------------------------------------------------- misc */
-const char* gi_status_string(gi_status s);
-const char* gi_last_error(void); /* thread-local; valid until the next call */
-int gi_abi_version(void);
+GI_API const char* gi_status_string(gi_status s);
+GI_API const char* gi_last_error(void); /* thread-local; valid until the next call */
+GI_API int gi_abi_version(void);
 
 #ifdef __cplusplus
 }

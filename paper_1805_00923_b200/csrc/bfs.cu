@@ -1,0 +1,306 @@
+// bfs.cu — direction-optimising BFS through edgeset.apply (SURVEY §8(a) rows
+// a6-a9, §2.7 K6-K9).
+//
+//  push level (SparsePush + to(unvisited) + applyModified without dedup,
+//    PAPER.md P:1779-1808): for u in the sparse queue, for
+//    v in out(u): if parent[v] == -1 and CAS(parent[v], -1, u) wins, append v.
+//    The CAS is the claim that makes "each vertex inserted once" hold without
+//    a dedup pass. Load balance: per-CTA exclusive scan of frontier degrees,
+//    then the CTA walks the flattened edge list (the paper's edge-aware
+//    chunking, at CTA granularity).
+//  pull level (DensePull + bitvector frontier + early exit, P:600-601,
+//    P:1812-1817): each warp owns 32 consecutive vertices = one
+//    bitmap word; an unvisited vertex scans its in-edges until it finds a
+//    frontier member; the next-frontier word is the warp ballot (no atomics).
+//  direction (DensePull-SparsePush): pull iff
+//    |F| + sum_{v in F} outdeg(v) > m / threshold_div (Ligra's m/20,
+//    P:3074 [punt]; reading R7). Both counts are produced by the level
+//    kernels themselves (warp-aggregated atomics), so the only host read per
+//    level is two int64.
+//  conversion: queue -> bitmap (atomicOr per id);
+//    bitmap -> queue (popc + warp scan + one atomicAdd per warp).
+#include <algorithm>
+#include <cub/block/block_scan.cuh>
+
+#include "gi_internal.cuh"
+
+namespace gi {
+namespace {
+
+constexpr int kRing = 4;  // counter slots ring: slot(l) = cnt + 2*(l % kRing): {|F_l|, sum outdeg F_l}
+
+__global__ void k_bfs_init(int32_t s_in, const int32_t* __restrict__ inv, const int32_t* __restrict__ outdeg,
+                           int32_t* __restrict__ parent, int32_t* __restrict__ q, int64_t* __restrict__ cnt) {
+  const int32_t s = inv ? inv[s_in] : s_in;
+  parent[s] = s;
+  q[0] = s;
+  cnt[0] = 1;
+  cnt[1] = outdeg[s];
+}
+
+template <typename OffT>
+__global__ void __launch_bounds__(256) k_bfs_push(const int32_t* __restrict__ q, int64_t qlen,
+                                                  const OffT* __restrict__ off, const int32_t* __restrict__ idx,
+                                                  const int32_t* __restrict__ outdeg, int32_t* parent,
+                                                  int32_t* __restrict__ qnext, int64_t* __restrict__ cnext) {
+  constexpr int NT = 256;
+  using Scan = cub::BlockScan<long long, NT>;
+  __shared__ typename Scan::TempStorage scan_tmp;
+  __shared__ long long s_pre[NT + 1];
+  __shared__ long long s_beg[NT];
+  __shared__ int32_t s_u[NT];
+  const int tid = threadIdx.x, lane = tid & 31;
+  for (int64_t c0 = (int64_t)blockIdx.x * NT; c0 < qlen; c0 += (int64_t)gridDim.x * NT) {
+    const int64_t i = c0 + tid;
+    long long deg = 0, beg = 0;
+    int32_t u = -1;
+    if (i < qlen) {
+      u = q[i];
+      beg = (long long)off[u];
+      deg = (long long)off[u + 1] - beg;
+    }
+    long long pre, total;
+    Scan(scan_tmp).ExclusiveSum(deg, pre, total);
+    s_pre[tid] = pre;
+    s_beg[tid] = beg;
+    s_u[tid] = u;
+    if (tid == 0) s_pre[NT] = total;
+    __syncthreads();
+    for (long long base = 0; base < total; base += NT) {
+      const long long f = base + tid;
+      bool won = false;
+      int32_t v = 0;
+      if (f < total) {
+        int lo = 0, hi = NT - 1;  // owner = last k with s_pre[k] <= f
+        while (lo < hi) {
+          int mid = (lo + hi + 1) >> 1;
+          if (s_pre[mid] <= f) lo = mid;
+          else hi = mid - 1;
+        }
+        const int32_t uu = s_u[lo];
+        v = __ldg(&idx[s_beg[lo] + (f - s_pre[lo])]);
+        if (*(volatile int32_t*)&parent[v] == -1) won = atomicCAS(&parent[v], -1, uu) == -1;
+      }
+      const unsigned mask = __ballot_sync(0xffffffffu, won);
+      long long od = won ? (long long)__ldg(&outdeg[v]) : 0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) od += __shfl_xor_sync(0xffffffffu, od, o);
+      if (mask) {
+        long long pos = 0;
+        if (lane == 0) {
+          pos = atomicAdd((unsigned long long*)&cnext[0], (unsigned long long)__popc(mask));
+          atomicAdd((unsigned long long*)&cnext[1], (unsigned long long)od);
+        }
+        pos = __shfl_sync(0xffffffffu, pos, 0);
+        if (won) qnext[pos + __popc(mask & ((1u << lane) - 1))] = v;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+template <typename OffT>
+__global__ void __launch_bounds__(256) k_bfs_pull(const uint32_t* __restrict__ fcur, uint32_t* __restrict__ fnext,
+                                                  int32_t* __restrict__ parent, const OffT* __restrict__ off,
+                                                  const int32_t* __restrict__ idx, const int32_t* __restrict__ outdeg,
+                                                  int64_t n, int64_t* __restrict__ cnext) {
+  const int lane = threadIdx.x & 31;
+  const int64_t words = (n + 31) >> 5;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  long long cnt = 0, sdeg = 0;
+  for (int64_t w = warp; w < words; w += nwarps) {
+    const int64_t v = (w << 5) + lane;
+    bool found = false;
+    if (v < n && parent[v] == -1) {
+      const int64_t e1 = (int64_t)off[v + 1];
+      for (int64_t e = (int64_t)off[v]; e < e1; ++e) {
+        const int32_t u = __ldg(&idx[e]);
+        if ((__ldg(&fcur[u >> 5]) >> (u & 31)) & 1u) {
+          parent[v] = u;
+          found = true;
+          break;
+        }
+      }
+    }
+    const unsigned mask = __ballot_sync(0xffffffffu, found);
+    if (lane == 0) fnext[w] = mask;
+    if (found) {
+      cnt += 1;
+      sdeg += __ldg(&outdeg[v]);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    sdeg += __shfl_xor_sync(0xffffffffu, sdeg, o);
+  }
+  if (lane == 0 && cnt) {
+    atomicAdd((unsigned long long*)&cnext[0], (unsigned long long)cnt);
+    atomicAdd((unsigned long long*)&cnext[1], (unsigned long long)sdeg);
+  }
+}
+
+__global__ void k_q2b(const int32_t* __restrict__ q, int64_t qlen, uint32_t* __restrict__ bm) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < qlen; i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t u = q[i];
+    atomicOr(&bm[u >> 5], 1u << (u & 31));
+  }
+}
+
+__global__ void k_b2q(const uint32_t* __restrict__ bm, int64_t words, int32_t* __restrict__ q,
+                      unsigned long long* __restrict__ tail) {
+  const int lane = threadIdx.x & 31;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;  // multiple of 32: warps stay aligned
+  for (int64_t wb = blockIdx.x * (int64_t)blockDim.x + threadIdx.x - lane; wb < words; wb += stride) {
+    const int64_t w = wb + lane;
+    uint32_t bits = w < words ? bm[w] : 0u;
+    int c = __popc(bits), inc = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int t = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += t;
+    }
+    const int total = __shfl_sync(0xffffffffu, inc, 31);
+    unsigned long long base = 0;
+    if (lane == 0 && total) base = atomicAdd(tail, (unsigned long long)total);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    long long pos = (long long)base + inc - c;
+    while (bits) {
+      const int b = __ffs(bits) - 1;
+      bits &= bits - 1;
+      q[pos++] = (int32_t)((w << 5) + b);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) k_bfs_finish(const int32_t* __restrict__ parent, int64_t n,
+                                                    const int32_t* __restrict__ perm, const int32_t* __restrict__ outdeg,
+                                                    int32_t* __restrict__ out, unsigned long long* __restrict__ red) {
+  long long reached = 0, edges = 0;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t p = parent[v];
+    const int32_t vin = perm ? perm[v] : (int32_t)v;
+    out[vin] = p < 0 ? -1 : (perm ? perm[p] : p);
+    if (p >= 0) {
+      reached += 1;
+      edges += outdeg[v];
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    reached += __shfl_xor_sync(0xffffffffu, reached, o);
+    edges += __shfl_xor_sync(0xffffffffu, edges, o);
+  }
+  if ((threadIdx.x & 31) == 0 && reached) {
+    atomicAdd(&red[0], (unsigned long long)reached);
+    atomicAdd(&red[1], (unsigned long long)edges);
+  }
+}
+
+}  // namespace
+
+template <typename OffT>
+static gi_status bfs_impl(gi_graph g, int32_t source, const gi_bfs_opts& o, int32_t* d_out, gi_bfs_stats* stats) {
+  gi_context ctx = g->ctx;
+  cudaStream_t st = ctx->stream;
+  const int sms = ctx->num_sms;
+  const int64_t n = g->n, m = g->m;
+  const int64_t words = (n + 31) >> 5;
+  const int div = o.threshold_div > 0 ? o.threshold_div : 20;
+  if (!g->parent.p) {
+    GI_TRY(g->parent.alloc(n * sizeof(int32_t)));
+    for (int k = 0; k < 2; ++k) {
+      GI_TRY(g->queue[k].alloc(n * sizeof(int32_t)));
+      GI_TRY(g->bitmap[k].alloc(words * sizeof(uint32_t)));
+    }
+    GI_TRY(g->counters.alloc((2 * kRing + 4) * sizeof(int64_t)));
+  }
+  int64_t* cnt = g->counters.as<int64_t>();
+  unsigned long long* aux = reinterpret_cast<unsigned long long*>(cnt + 2 * kRing);  // [0]=tail [1..2]=finish
+  int64_t* h = ctx->h_scratch;
+  int32_t* parent = g->parent.as<int32_t>();
+  const OffT* csr_off = g->csr_off.as<OffT>();
+  const OffT* csc_off = g->csc_off.as<OffT>();
+  const int32_t* outdeg = g->outdeg.as<int32_t>();
+  gi_bfs_stats S{};
+
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (o.profile) {
+    GI_CUDA(cudaEventCreate(&e0));
+    GI_CUDA(cudaEventCreate(&e1));
+    GI_CUDA(cudaEventRecord(e0, st));
+  }
+  GI_CUDA(cudaMemsetAsync(parent, 0xFF, n * sizeof(int32_t), st));
+  GI_CUDA(cudaMemsetAsync(cnt, 0, (2 * kRing + 4) * sizeof(int64_t), st));
+  k_bfs_init<<<1, 1, 0, st>>>(source, g->relabeled ? g->inv.as<int32_t>() : nullptr, outdeg, parent,
+                              g->queue[0].as<int32_t>(), cnt);
+  S.launches = 1;
+  int qc = 0, bc = 0;     // current queue / bitmap buffers
+  bool in_bitmap = false;  // representation of the current frontier
+  for (int64_t level = 0;; ++level) {
+    int64_t* cur = cnt + 2 * (level % kRing);
+    int64_t* nxt = cnt + 2 * ((level + 1) % kRing);
+    GI_CUDA(cudaMemcpyAsync(h, cur, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    GI_CUDA(cudaStreamSynchronize(st));
+    const int64_t nf = h[0], sdeg = h[1];
+    if (nf == 0) break;
+    bool pull;
+    if (o.policy == GI_BFS_PUSH_ONLY) pull = false;
+    else if (o.policy == GI_BFS_PULL_ONLY) pull = level > 0;
+    else pull = (nf + sdeg) > m / div;
+    GI_CUDA(cudaMemsetAsync(nxt, 0, 2 * sizeof(int64_t), st));
+    if (pull) {
+      if (!in_bitmap) {
+        GI_CUDA(cudaMemsetAsync(g->bitmap[bc].p, 0, words * sizeof(uint32_t), st));
+        k_q2b<<<grid_for(nf, 256, sms), 256, 0, st>>>(g->queue[qc].as<int32_t>(), nf, g->bitmap[bc].as<uint32_t>());
+        S.launches++;
+      }
+      k_bfs_pull<OffT><<<grid_for(words * 32, 256, sms, 8), 256, 0, st>>>(
+          g->bitmap[bc].as<uint32_t>(), g->bitmap[bc ^ 1].as<uint32_t>(), parent, csc_off, g->csc_idx.as<int32_t>(),
+          outdeg, n, nxt);
+      bc ^= 1;
+      in_bitmap = true;
+      S.pull_levels++;
+    } else {
+      if (in_bitmap) {
+        GI_CUDA(cudaMemsetAsync(aux, 0, sizeof(unsigned long long), st));
+        k_b2q<<<grid_for(words, 256, sms), 256, 0, st>>>(g->bitmap[bc].as<uint32_t>(), words,
+                                                         g->queue[qc].as<int32_t>(), aux);
+        S.launches++;
+      }
+      const int grid = (int)std::min<int64_t>(ceil_div(nf, 256), (int64_t)sms * 8);
+      k_bfs_push<OffT><<<grid, 256, 0, st>>>(g->queue[qc].as<int32_t>(), nf, csr_off, g->csr_idx.as<int32_t>(), outdeg,
+                                             parent, g->queue[qc ^ 1].as<int32_t>(), nxt);
+      qc ^= 1;
+      in_bitmap = false;
+    }
+    GI_CUDA(cudaGetLastError());
+    S.launches++;
+    S.levels++;
+  }
+  GI_CUDA(cudaMemsetAsync(aux + 1, 0, 2 * sizeof(unsigned long long), st));
+  k_bfs_finish<<<grid_for(n, 256, sms), 256, 0, st>>>(parent, n, g->relabeled ? g->perm.as<int32_t>() : nullptr,
+                                                      outdeg, d_out, aux + 1);
+  S.launches++;
+  GI_CUDA(cudaGetLastError());
+  GI_CUDA(cudaMemcpyAsync(h, aux + 1, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  if (o.profile) GI_CUDA(cudaEventRecord(e1, st));
+  GI_CUDA(cudaStreamSynchronize(st));
+  S.reached = h[0];
+  S.edges_traversed = h[1];
+  if (o.profile) {
+    GI_CUDA(cudaEventElapsedTime(&S.total_ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+  }
+  if (stats) *stats = S;
+  return GI_OK;
+}
+
+gi_status bfs_run(gi_graph g, int32_t source, const gi_bfs_opts& o, int32_t* d_out, gi_bfs_stats* stats) {
+  if (g->off64) return bfs_impl<int64_t>(g, source, o, d_out, stats);
+  return bfs_impl<int32_t>(g, source, o, d_out, stats);
+}
+
+}  // namespace gi

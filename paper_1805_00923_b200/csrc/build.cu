@@ -1,0 +1,291 @@
+// build.cu — device graph builder.
+//
+// edge list (int32 src, dst) -> validate -> 64-bit keys (u << b | v), self-loops
+// dropped, optional symmetrisation ("an undirected graph would be represented
+// by duplicating the directed edges", PAPER.md P:3183 [draft]) -> radix sort ->
+// unique (dedup) -> CSR offsets by binary search per vertex -> out-degrees ->
+// relabel by out-degree (descending, stable) -> CSR and CSC in internal ids ->
+// merge-path tile metadata for the pull kernel.
+//
+// The sort and select primitives are CUB (CUDA toolkit, header-only): library
+// primitives in the sense of a cuBLAS call; every graph-specific step is a
+// kernel below.
+#include <cub/cub.cuh>
+
+#include "gi_internal.cuh"
+
+namespace gi {
+namespace {
+
+constexpr uint64_t kSentinel = ~0ull;
+
+__global__ void k_validate(const int32_t* __restrict__ src, const int32_t* __restrict__ dst, int64_t m0,
+                           int64_t n, int* __restrict__ bad) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m0; i += (int64_t)gridDim.x * blockDim.x) {
+    int32_t u = src[i], v = dst[i];
+    if (u < 0 || u >= n || v < 0 || v >= n) atomicExch(bad, 1);
+  }
+}
+
+__global__ void k_make_keys(const int32_t* __restrict__ src, const int32_t* __restrict__ dst, int64_t m0,
+                            int bits, int rm_self, int sym, uint64_t* __restrict__ keys) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m0; i += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t u = (uint32_t)src[i], v = (uint32_t)dst[i];
+    bool drop = rm_self && u == v;
+    if (sym) {
+      keys[2 * i] = drop ? kSentinel : (u << bits) | v;
+      keys[2 * i + 1] = drop ? kSentinel : (v << bits) | u;
+    } else {
+      keys[i] = drop ? kSentinel : (u << bits) | v;
+    }
+  }
+}
+
+struct NotSentinel {
+  __host__ __device__ bool operator()(const uint64_t& k) const { return k != kSentinel; }
+};
+
+// off[u] = first position of row u in the sorted key array (lower bound of u << bits).
+template <typename OffT>
+__global__ void k_offsets(const uint64_t* __restrict__ keys, int64_t m, int64_t n, int bits, OffT* __restrict__ off) {
+  for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u <= n; u += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t target = (uint64_t)u << bits;
+    int64_t lo = 0, hi = m;
+    while (lo < hi) {
+      int64_t mid = lo + ((hi - lo) >> 1);
+      if (keys[mid] < target) lo = mid + 1;
+      else hi = mid;
+    }
+    off[u] = (OffT)lo;
+  }
+}
+
+template <typename OffT>
+__global__ void k_degrees(const OffT* __restrict__ off, int64_t n, int32_t* __restrict__ deg) {
+  for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n; u += (int64_t)gridDim.x * blockDim.x)
+    deg[u] = (int32_t)(off[u + 1] - off[u]);
+}
+
+__global__ void k_low_bits(const uint64_t* __restrict__ keys, int64_t m, int bits, int32_t* __restrict__ idx) {
+  const uint64_t mask = (1ull << bits) - 1;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+    idx[i] = (int32_t)(keys[i] & mask);
+}
+
+// sort key for relabelling: descending out-degree, stable on input id
+__global__ void k_relabel_keys(const int32_t* __restrict__ deg, int64_t n, uint32_t* __restrict__ k,
+                               int32_t* __restrict__ ids) {
+  for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n; u += (int64_t)gridDim.x * blockDim.x) {
+    k[u] = 0x7FFFFFFFu - (uint32_t)deg[u];
+    ids[u] = (int32_t)u;
+  }
+}
+
+__global__ void k_invert(const int32_t* __restrict__ perm, int64_t n, int32_t* __restrict__ inv) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    inv[perm[i]] = (int32_t)i;
+}
+
+// re-key sorted input-id edges (u << b | v) into internal ids; transpose => (v', u')
+__global__ void k_rekey(const uint64_t* __restrict__ in, int64_t m, int bits, const int32_t* __restrict__ inv,
+                        int transpose, uint64_t* __restrict__ out) {
+  const uint64_t mask = (1ull << bits) - 1;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t u = in[i] >> bits, v = in[i] & mask;
+    if (inv) {
+      u = (uint32_t)inv[u];
+      v = (uint32_t)inv[v];
+    }
+    out[i] = transpose ? ((v << bits) | u) : ((u << bits) | v);
+  }
+}
+
+// Merge-path tiling of the CSC (items = rows' end markers + edges, n + m in
+// total; row r occupies merge positions [r + off[r], r + off[r+1]]).
+// rows[2b] = row containing position b*T, rows[2b+1] = row containing the
+// tile's last position. "Row containing p" = min r with r + off[r+1] >= p.
+template <typename OffT>
+__global__ void k_tile_rows(const OffT* __restrict__ off, int64_t n, int64_t m, int64_t ntiles, int T,
+                            int32_t* __restrict__ rows) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < 2 * ntiles;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t b = t >> 1;
+    int64_t p = (t & 1) ? min((b + 1) * (int64_t)T, n + m) - 1 : b * (int64_t)T;
+    int64_t lo = 0, hi = n - 1;
+    while (lo < hi) {
+      int64_t mid = lo + ((hi - lo) >> 1);
+      if (mid + (int64_t)off[mid + 1] >= p) hi = mid;
+      else lo = mid + 1;
+    }
+    rows[t] = (int32_t)lo;
+  }
+}
+
+int bits_for(int64_t n) {
+  int b = 1;
+  while ((1ll << b) < n) ++b;
+  return b;
+}
+
+struct Temp {
+  DevBuf buf;
+  gi_status ensure(size_t bytes) {
+    if (buf.bytes >= bytes && buf.p) return GI_OK;
+    return buf.alloc(bytes);
+  }
+};
+
+}  // namespace
+
+template <typename OffT>
+static gi_status csr_from_sorted(gi_graph g, const uint64_t* keys, int64_t m, int bits, DevBuf& off, DevBuf& idx) {
+  cudaStream_t st = g->ctx->stream;
+  const int sms = g->ctx->num_sms;
+  GI_TRY(off.alloc((g->n + 1) * sizeof(OffT)));
+  GI_TRY(idx.alloc(m * sizeof(int32_t)));
+  k_offsets<OffT><<<grid_for(g->n + 1, 256, sms), 256, 0, st>>>(keys, m, g->n, bits, off.as<OffT>());
+  k_low_bits<<<grid_for(m, 256, sms), 256, 0, st>>>(keys, m, bits, idx.as<int32_t>());
+  GI_CUDA(cudaGetLastError());
+  return GI_OK;
+}
+
+gi_status build_graph(gi_context ctx, int64_t n, int64_t m0, const int32_t* d_src, const int32_t* d_dst,
+                      uint32_t flags, gi_graph g) {
+  cudaStream_t st = ctx->stream;
+  const int sms = ctx->num_sms;
+  g->ctx = ctx;
+  g->n = n;
+  const bool rm_self = flags & GI_REMOVE_SELF_LOOPS;
+  const bool dedup = flags & GI_DEDUP;
+  const bool sym = flags & GI_SYMMETRIZE;
+  g->relabeled = !(flags & GI_NO_RELABEL) && n > 1;
+
+  // 1. validate endpoints
+  DevBuf bad;
+  GI_TRY(bad.alloc(sizeof(int)));
+  GI_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), st));
+  if (m0 > 0) k_validate<<<grid_for(m0, 256, sms), 256, 0, st>>>(d_src, d_dst, m0, n, bad.as<int>());
+  int h_bad = 0;
+  GI_CUDA(cudaMemcpyAsync(&h_bad, bad.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  GI_CUDA(cudaStreamSynchronize(st));
+  if (h_bad) return fail(GI_ERR_VERTEX_OUT_OF_RANGE, "gi_graph_create: an edge endpoint is outside [0, n)");
+
+  // 2. keys, 3. select non-sentinel, 4. sort, 5. unique
+  const int bits = bits_for(n > 1 ? n : 2);
+  const int64_t mk = sym ? 2 * m0 : m0;
+  DevBuf kA, kB, nsel;
+  GI_TRY(kA.alloc(mk * sizeof(uint64_t)));
+  GI_TRY(kB.alloc(mk * sizeof(uint64_t)));
+  GI_TRY(nsel.alloc(sizeof(int64_t)));
+  Temp tmp;
+  size_t tb = 0;
+  int64_t m = 0;
+  if (mk > 0) {
+    k_make_keys<<<grid_for(m0, 256, sms), 256, 0, st>>>(d_src, d_dst, m0, bits, rm_self, sym, kA.as<uint64_t>());
+    GI_CUDA(cub::DeviceSelect::If(nullptr, tb, kA.as<uint64_t>(), kB.as<uint64_t>(), nsel.as<int64_t>(), mk,
+                                  NotSentinel(), st));
+    GI_TRY(tmp.ensure(tb));
+    GI_CUDA(cub::DeviceSelect::If(tmp.buf.p, tb, kA.as<uint64_t>(), kB.as<uint64_t>(), nsel.as<int64_t>(), mk,
+                                  NotSentinel(), st));
+    GI_CUDA(cudaMemcpyAsync(&m, nsel.p, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    GI_CUDA(cudaStreamSynchronize(st));
+  }
+  // sorted keys end up in `cur`
+  DevBuf* cur = &kB;
+  DevBuf* alt = &kA;
+  auto sort_keys = [&](int64_t count) -> gi_status {
+    if (count <= 1) return GI_OK;
+    cub::DoubleBuffer<uint64_t> db(cur->as<uint64_t>(), alt->as<uint64_t>());
+    size_t b = 0;
+    GI_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, b, db, count, 0, 2 * bits, st));
+    GI_TRY(tmp.ensure(b));
+    GI_CUDA(cub::DeviceRadixSort::SortKeys(tmp.buf.p, b, db, count, 0, 2 * bits, st));
+    if (db.Current() != cur->as<uint64_t>()) std::swap(cur, alt);
+    return GI_OK;
+  };
+  GI_TRY(sort_keys(m));
+  if (dedup && m > 1) {
+    size_t b = 0;
+    GI_CUDA(cub::DeviceSelect::Unique(nullptr, b, cur->as<uint64_t>(), alt->as<uint64_t>(), nsel.as<int64_t>(), m, st));
+    GI_TRY(tmp.ensure(b));
+    GI_CUDA(cub::DeviceSelect::Unique(tmp.buf.p, b, cur->as<uint64_t>(), alt->as<uint64_t>(), nsel.as<int64_t>(), m,
+                                      st));
+    GI_CUDA(cudaMemcpyAsync(&m, nsel.p, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    GI_CUDA(cudaStreamSynchronize(st));
+    std::swap(cur, alt);
+  }
+  g->m = m;
+  g->off64 = m >= (int64_t)INT32_MAX;
+
+  // 6. out-degrees in input ids (from the input-id CSR)
+  DevBuf off_in;
+  GI_TRY(off_in.alloc((n + 1) * sizeof(int64_t)));
+  GI_TRY(g->outdeg.alloc(n * sizeof(int32_t)));
+  k_offsets<int64_t><<<grid_for(n + 1, 256, sms), 256, 0, st>>>(cur->as<uint64_t>(), m, n, bits, off_in.as<int64_t>());
+  k_degrees<int64_t><<<grid_for(n, 256, sms), 256, 0, st>>>(off_in.as<int64_t>(), n, g->outdeg.as<int32_t>());
+  GI_CUDA(cudaGetLastError());
+
+  // 7. relabel by out-degree (descending, stable)
+  const int32_t* inv = nullptr;
+  if (g->relabeled) {
+    DevBuf rk, rk2, ids;
+    GI_TRY(rk.alloc(n * sizeof(uint32_t)));
+    GI_TRY(rk2.alloc(n * sizeof(uint32_t)));
+    GI_TRY(ids.alloc(n * sizeof(int32_t)));
+    GI_TRY(g->perm.alloc(n * sizeof(int32_t)));
+    GI_TRY(g->inv.alloc(n * sizeof(int32_t)));
+    k_relabel_keys<<<grid_for(n, 256, sms), 256, 0, st>>>(g->outdeg.as<int32_t>(), n, rk.as<uint32_t>(), ids.as<int32_t>());
+    size_t b = 0;
+    GI_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, b, rk.as<uint32_t>(), rk2.as<uint32_t>(), ids.as<int32_t>(),
+                                            g->perm.as<int32_t>(), n, 0, 32, st));
+    GI_TRY(tmp.ensure(b));
+    GI_CUDA(cub::DeviceRadixSort::SortPairs(tmp.buf.p, b, rk.as<uint32_t>(), rk2.as<uint32_t>(), ids.as<int32_t>(),
+                                            g->perm.as<int32_t>(), n, 0, 32, st));
+    k_invert<<<grid_for(n, 256, sms), 256, 0, st>>>(g->perm.as<int32_t>(), n, g->inv.as<int32_t>());
+    GI_CUDA(cudaGetLastError());
+    inv = g->inv.as<int32_t>();
+  }
+
+  // 8. CSR in internal ids. Input keys are sorted by (u, v); after relabelling
+  // re-key and sort again.
+  DevBuf edges_in;  // keep the input-id sorted keys for the CSC pass
+  if (m > 0) {
+    GI_TRY(edges_in.alloc(m * sizeof(uint64_t)));
+    GI_CUDA(cudaMemcpyAsync(edges_in.p, cur->p, m * sizeof(uint64_t), cudaMemcpyDeviceToDevice, st));
+    if (inv) {
+      k_rekey<<<grid_for(m, 256, sms), 256, 0, st>>>(edges_in.as<uint64_t>(), m, bits, inv, 0, cur->as<uint64_t>());
+      GI_TRY(sort_keys(m));
+    }
+  }
+  if (g->off64) GI_TRY(csr_from_sorted<int64_t>(g, cur->as<uint64_t>(), m, bits, g->csr_off, g->csr_idx));
+  else GI_TRY(csr_from_sorted<int32_t>(g, cur->as<uint64_t>(), m, bits, g->csr_off, g->csr_idx));
+  if (inv) {  // out-degrees in internal ids
+    if (g->off64) k_degrees<int64_t><<<grid_for(n, 256, sms), 256, 0, st>>>(g->csr_off.as<int64_t>(), n, g->outdeg.as<int32_t>());
+    else k_degrees<int32_t><<<grid_for(n, 256, sms), 256, 0, st>>>(g->csr_off.as<int32_t>(), n, g->outdeg.as<int32_t>());
+  }
+
+  // 9. CSC in internal ids: transpose keys and sort
+  if (m > 0) {
+    k_rekey<<<grid_for(m, 256, sms), 256, 0, st>>>(edges_in.as<uint64_t>(), m, bits, inv, 1, cur->as<uint64_t>());
+    GI_TRY(sort_keys(m));
+  }
+  if (g->off64) GI_TRY(csr_from_sorted<int64_t>(g, cur->as<uint64_t>(), m, bits, g->csc_off, g->csc_idx));
+  else GI_TRY(csr_from_sorted<int32_t>(g, cur->as<uint64_t>(), m, bits, g->csc_off, g->csc_idx));
+
+  // 10. pull tiling metadata
+  g->ntiles = n > 0 ? ceil_div(n + m, kPullTile) : 0;
+  GI_TRY(g->tile_rows.alloc(2 * (g->ntiles > 0 ? g->ntiles : 1) * sizeof(int32_t)));
+  if (g->ntiles > 0) {
+    if (g->off64)
+      k_tile_rows<int64_t><<<grid_for(2 * g->ntiles, 256, sms), 256, 0, st>>>(g->csc_off.as<int64_t>(), n, m, g->ntiles,
+                                                                            kPullTile, g->tile_rows.as<int32_t>());
+    else
+      k_tile_rows<int32_t><<<grid_for(2 * g->ntiles, 256, sms), 256, 0, st>>>(g->csc_off.as<int32_t>(), n, m, g->ntiles,
+                                                                            kPullTile, g->tile_rows.as<int32_t>());
+  }
+  GI_CUDA(cudaGetLastError());
+  GI_CUDA(cudaStreamSynchronize(st));
+  return GI_OK;
+}
+
+}  // namespace gi

@@ -1,0 +1,410 @@
+// gi_api.cu — the extern "C" boundary declared in include/gi.h: argument
+// validation, host/device pointer handling, error reporting, orchestration.
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+
+#include "gi_internal.cuh"
+#include "nccl_dyn.cuh"
+
+namespace gi {
+
+static thread_local std::string t_last_error;
+
+void set_error(const std::string& msg) { t_last_error = msg; }
+
+gi_status fail(gi_status s, const std::string& msg) {
+  t_last_error = msg;
+  return s;
+}
+
+gi_status cuda_fail(cudaError_t e, const char* what, const char* file, int line) {
+  char buf[512];
+  snprintf(buf, sizeof buf, "CUDA error %s (%d) in %s at %s:%d", cudaGetErrorString(e), (int)e, what, file, line);
+  t_last_error = buf;
+  if (e == cudaErrorMemoryAllocation) return GI_ERR_OUT_OF_MEMORY;
+  return GI_ERR_CUDA;
+}
+
+static bool is_device_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes a{};
+  cudaError_t e = cudaPointerGetAttributes(&a, p);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+// Makes `p` (n elements of T, host or device) available on the device.
+template <typename T>
+static gi_status to_device(gi_context ctx, const T* p, int64_t n, DevBuf& hold, const T** out) {
+  if (n == 0 || is_device_ptr(p)) {
+    *out = p;
+    return GI_OK;
+  }
+  GI_TRY(hold.alloc(n * sizeof(T)));
+  GI_CUDA(cudaMemcpyAsync(hold.p, p, n * sizeof(T), cudaMemcpyHostToDevice, ctx->stream));
+  *out = hold.as<T>();
+  return GI_OK;
+}
+
+// Output helper: device pointer -> write in place; host pointer -> stage + D2H copy.
+template <typename T>
+struct OutBuf {
+  T* user;
+  int64_t n;
+  bool dev;
+  DevBuf* stage;
+  gi_status prepare(gi_graph g, T** d) {
+    dev = is_device_ptr(user);
+    if (dev) {
+      *d = user;
+      return GI_OK;
+    }
+    if (!stage->p || stage->bytes < (size_t)n * sizeof(T)) GI_TRY(stage->alloc(n * sizeof(T)));
+    *d = stage->as<T>();
+    return GI_OK;
+  }
+  gi_status finish(gi_context ctx) {
+    if (!dev && n > 0) GI_CUDA(cudaMemcpyAsync(user, stage->p, n * sizeof(T), cudaMemcpyDeviceToHost, ctx->stream));
+    return GI_OK;
+  }
+};
+
+static gi_status sync(gi_context ctx) {
+  GI_CUDA(cudaStreamSynchronize(ctx->stream));
+  GI_CUDA(cudaGetLastError());
+  return GI_OK;
+}
+
+}  // namespace gi
+
+using namespace gi;
+
+#define GI_GUARD_BEGIN try {
+#define GI_GUARD_END                                                    \
+  }                                                                     \
+  catch (const std::bad_alloc&) {                                       \
+    return fail(GI_ERR_OUT_OF_MEMORY, "host allocation failed");        \
+  }                                                                     \
+  catch (...) {                                                         \
+    return fail(GI_ERR_INTERNAL, "unexpected C++ exception");           \
+  }
+
+extern "C" {
+
+int gi_abi_version(void) { return GI_ABI_VERSION; }
+
+const char* gi_status_string(gi_status s) {
+  switch (s) {
+    case GI_OK: return "GI_OK";
+    case GI_ERR_INVALID_ARGUMENT: return "GI_ERR_INVALID_ARGUMENT";
+    case GI_ERR_VERTEX_OUT_OF_RANGE: return "GI_ERR_VERTEX_OUT_OF_RANGE";
+    case GI_ERR_OUT_OF_MEMORY: return "GI_ERR_OUT_OF_MEMORY";
+    case GI_ERR_CUDA: return "GI_ERR_CUDA";
+    case GI_ERR_NCCL: return "GI_ERR_NCCL";
+    case GI_ERR_UNSUPPORTED: return "GI_ERR_UNSUPPORTED";
+    case GI_ERR_INTERNAL: return "GI_ERR_INTERNAL";
+  }
+  return "GI_ERR_UNKNOWN";
+}
+
+const char* gi_last_error(void) { return t_last_error.c_str(); }
+
+gi_status gi_context_create(int device, void* cuda_stream, gi_context* out) {
+  GI_GUARD_BEGIN
+  if (!out) return fail(GI_ERR_INVALID_ARGUMENT, "gi_context_create: out is NULL");
+  *out = nullptr;
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    return fail(GI_ERR_CUDA, std::string("gi_context_create: no CUDA device (") + cudaGetErrorString(e) + ")");
+  }
+  if (device < 0 || device >= ndev) return fail(GI_ERR_INVALID_ARGUMENT, "gi_context_create: bad device ordinal");
+  GI_CUDA(cudaSetDevice(device));
+  gi_context c = new gi_context_s();
+  c->device = device;
+  cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
+  if (cuda_stream) {
+    c->stream = static_cast<cudaStream_t>(cuda_stream);
+  } else {
+    cudaError_t se = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+    if (se != cudaSuccess) {
+      delete c;
+      return cuda_fail(se, "cudaStreamCreate", __FILE__, __LINE__);
+    }
+    c->own_stream = true;
+  }
+  cudaError_t he = cudaMallocHost(&c->h_scratch, 64 * sizeof(int64_t));
+  if (he != cudaSuccess) {
+    if (c->own_stream) cudaStreamDestroy(c->stream);
+    delete c;
+    return cuda_fail(he, "cudaMallocHost", __FILE__, __LINE__);
+  }
+  *out = c;
+  return GI_OK;
+  GI_GUARD_END
+}
+
+gi_status gi_context_destroy(gi_context ctx) {
+  if (!ctx) return fail(GI_ERR_INVALID_ARGUMENT, "gi_context_destroy: NULL context");
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  if (ctx->nccl_comm) {
+    const NcclApi* a = nccl_api();
+    if (a) a->commDestroy(static_cast<ncclComm_t>(ctx->nccl_comm));
+    ctx->nccl_comm = nullptr;
+  }
+  if (ctx->h_scratch) cudaFreeHost(ctx->h_scratch);
+  if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+  return GI_OK;
+}
+
+gi_status gi_context_rank(gi_context ctx, int* rank, int* nranks) {
+  if (!ctx || !rank || !nranks) return fail(GI_ERR_INVALID_ARGUMENT, "gi_context_rank: NULL argument");
+  *rank = ctx->rank;
+  *nranks = ctx->nranks;
+  return GI_OK;
+}
+
+gi_status gi_graph_create(gi_context ctx, int64_t n, int64_t m0, const int32_t* src, const int32_t* dst,
+                          uint32_t flags, gi_graph* out) {
+  GI_GUARD_BEGIN
+  if (!out) return fail(GI_ERR_INVALID_ARGUMENT, "gi_graph_create: out is NULL");
+  *out = nullptr;
+  if (!ctx) return fail(GI_ERR_INVALID_ARGUMENT, "gi_graph_create: NULL context");
+  if (n < 0 || n > INT32_MAX) return fail(GI_ERR_INVALID_ARGUMENT, "gi_graph_create: n must be in [0, 2^31-1]");
+  if (m0 < 0 || m0 >= (1ll << 40)) return fail(GI_ERR_INVALID_ARGUMENT, "gi_graph_create: bad edge count");
+  if (m0 > 0 && (!src || !dst)) return fail(GI_ERR_INVALID_ARGUMENT, "gi_graph_create: NULL edge array");
+  const uint32_t known = GI_EDGES_ON_DEVICE | GI_REMOVE_SELF_LOOPS | GI_DEDUP | GI_SYMMETRIZE | GI_NO_RELABEL;
+  if (flags & ~known) return fail(GI_ERR_INVALID_ARGUMENT, "gi_graph_create: unknown flag bits");
+  if (n == 0 && m0 > 0) return fail(GI_ERR_VERTEX_OUT_OF_RANGE, "gi_graph_create: edges given but n = 0");
+  if (ctx->nranks > 1) return fail(GI_ERR_UNSUPPORTED, "gi_graph_create: multi-GPU graphs not built yet");
+  GI_CUDA(cudaSetDevice(ctx->device));
+  if ((flags & GI_EDGES_ON_DEVICE) && m0 > 0 && !(is_device_ptr(src) && is_device_ptr(dst)))
+    return fail(GI_ERR_INVALID_ARGUMENT, "gi_graph_create: GI_EDGES_ON_DEVICE but edges are host memory");
+  DevBuf hs, hd;
+  const int32_t *ds = nullptr, *dd = nullptr;
+  GI_TRY(to_device(ctx, src, m0, hs, &ds));
+  GI_TRY(to_device(ctx, dst, m0, hd, &dd));
+  gi_graph g = new gi_graph_s();
+  gi_status s = build_graph(ctx, n, m0, ds, dd, flags, g);
+  if (s == GI_OK) s = sync(ctx);
+  if (s != GI_OK) {
+    delete g;
+    return s;
+  }
+  *out = g;
+  return GI_OK;
+  GI_GUARD_END
+}
+
+gi_status gi_graph_destroy(gi_graph g) {
+  if (!g) return fail(GI_ERR_INVALID_ARGUMENT, "gi_graph_destroy: NULL graph");
+  cudaSetDevice(g->ctx->device);
+  cudaStreamSynchronize(g->ctx->stream);
+  delete g;
+  return GI_OK;
+}
+
+gi_status gi_graph_num_vertices(gi_graph g, int64_t* n) {
+  if (!g || !n) return fail(GI_ERR_INVALID_ARGUMENT, "gi_graph_num_vertices: NULL argument");
+  *n = g->n;
+  return GI_OK;
+}
+
+gi_status gi_graph_num_edges(gi_graph g, int64_t* m) {
+  if (!g || !m) return fail(GI_ERR_INVALID_ARGUMENT, "gi_graph_num_edges: NULL argument");
+  *m = g->m;
+  return GI_OK;
+}
+
+}  // extern "C"
+
+namespace gi {
+namespace {
+__global__ void k_degree_out(const int32_t* __restrict__ deg_int, const int32_t* __restrict__ perm, int64_t n,
+                             int32_t* __restrict__ out) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x)
+    out[perm ? perm[v] : v] = deg_int[v];
+}
+
+template <typename OffT>
+__global__ void k_indeg(const OffT* __restrict__ off, const int32_t* __restrict__ perm, int64_t n,
+                        int32_t* __restrict__ out) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x)
+    out[perm ? perm[v] : v] = (int32_t)(off[v + 1] - off[v]);
+}
+
+// CSR in input ids: row lengths first (scan on host side of the caller), then
+// rows copied with ids mapped back and sorted per row.
+template <typename OffT>
+__global__ void k_csr_export(const OffT* __restrict__ off, const int32_t* __restrict__ idx,
+                             const int32_t* __restrict__ perm, const int32_t* __restrict__ inv, int64_t n,
+                             const int64_t* __restrict__ out_off, int32_t* __restrict__ out_idx) {
+  // one warp per input-id row
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t u_in = warp; u_in < n; u_in += nw) {
+    const int64_t u = inv ? inv[u_in] : u_in;
+    const int64_t b = off[u], e = off[u + 1], o = out_off[u_in];
+    for (int64_t j = b + lane; j < e; j += 32) out_idx[o + (j - b)] = perm ? perm[idx[j]] : idx[j];
+  }
+}
+}  // namespace
+}  // namespace gi
+
+#include <cub/device/device_scan.cuh>
+#include <cub/device/device_segmented_radix_sort.cuh>
+
+extern "C" {
+
+gi_status gi_graph_out_degrees(gi_graph g, int32_t* outdeg) {
+  GI_GUARD_BEGIN
+  if (!g || (!outdeg && g->n > 0)) return fail(GI_ERR_INVALID_ARGUMENT, "gi_graph_out_degrees: NULL argument");
+  gi_context ctx = g->ctx;
+  GI_CUDA(cudaSetDevice(ctx->device));
+  if (g->n == 0) return GI_OK;
+  OutBuf<int32_t> ob{outdeg, g->n, false, &g->out_stage};
+  int32_t* d = nullptr;
+  GI_TRY(ob.prepare(g, &d));
+  k_degree_out<<<grid_for(g->n, 256, ctx->num_sms), 256, 0, ctx->stream>>>(
+      g->outdeg.as<int32_t>(), g->relabeled ? g->perm.as<int32_t>() : nullptr, g->n, d);
+  GI_CUDA(cudaGetLastError());
+  GI_TRY(ob.finish(ctx));
+  return sync(ctx);
+  GI_GUARD_END
+}
+
+gi_status gi_graph_in_degrees(gi_graph g, int32_t* indeg) {
+  GI_GUARD_BEGIN
+  if (!g || (!indeg && g->n > 0)) return fail(GI_ERR_INVALID_ARGUMENT, "gi_graph_in_degrees: NULL argument");
+  gi_context ctx = g->ctx;
+  GI_CUDA(cudaSetDevice(ctx->device));
+  if (g->n == 0) return GI_OK;
+  OutBuf<int32_t> ob{indeg, g->n, false, &g->out_stage};
+  int32_t* d = nullptr;
+  GI_TRY(ob.prepare(g, &d));
+  const int32_t* perm = g->relabeled ? g->perm.as<int32_t>() : nullptr;
+  if (g->off64)
+    k_indeg<int64_t><<<grid_for(g->n, 256, ctx->num_sms), 256, 0, ctx->stream>>>(g->csc_off.as<int64_t>(), perm, g->n, d);
+  else
+    k_indeg<int32_t><<<grid_for(g->n, 256, ctx->num_sms), 256, 0, ctx->stream>>>(g->csc_off.as<int32_t>(), perm, g->n, d);
+  GI_CUDA(cudaGetLastError());
+  GI_TRY(ob.finish(ctx));
+  return sync(ctx);
+  GI_GUARD_END
+}
+
+gi_status gi_graph_csr(gi_graph g, int64_t* off, int32_t* idx) {
+  GI_GUARD_BEGIN
+  if (!g || !off || (!idx && g->m > 0)) return fail(GI_ERR_INVALID_ARGUMENT, "gi_graph_csr: NULL argument");
+  gi_context ctx = g->ctx;
+  cudaStream_t st = ctx->stream;
+  GI_CUDA(cudaSetDevice(ctx->device));
+  const int64_t n = g->n, m = g->m;
+  const int sms = ctx->num_sms;
+  DevBuf deg, doff, didx, didx2, tmp;
+  GI_TRY(deg.alloc((n + 1) * sizeof(int32_t)));
+  GI_TRY(doff.alloc((n + 1) * sizeof(int64_t)));
+  GI_TRY(didx.alloc(m * sizeof(int32_t)));
+  GI_TRY(didx2.alloc(m * sizeof(int32_t)));
+  const int32_t* perm = g->relabeled ? g->perm.as<int32_t>() : nullptr;
+  const int32_t* inv = g->relabeled ? g->inv.as<int32_t>() : nullptr;
+  GI_CUDA(cudaMemsetAsync(deg.p, 0, (n + 1) * sizeof(int32_t), st));
+  if (n > 0)
+    k_degree_out<<<grid_for(n, 256, sms), 256, 0, st>>>(g->outdeg.as<int32_t>(), perm, n, deg.as<int32_t>());
+  size_t tb = 0;
+  GI_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, deg.as<int32_t>(), doff.as<int64_t>(), n + 1, st));
+  GI_TRY(tmp.alloc(tb));
+  GI_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb, deg.as<int32_t>(), doff.as<int64_t>(), n + 1, st));
+  if (n > 0 && m > 0) {
+    if (g->off64)
+      k_csr_export<int64_t><<<grid_for(n * 32, 256, sms), 256, 0, st>>>(g->csr_off.as<int64_t>(), g->csr_idx.as<int32_t>(),
+                                                                     perm, inv, n, doff.as<int64_t>(), didx.as<int32_t>());
+    else
+      k_csr_export<int32_t><<<grid_for(n * 32, 256, sms), 256, 0, st>>>(g->csr_off.as<int32_t>(), g->csr_idx.as<int32_t>(),
+                                                                     perm, inv, n, doff.as<int64_t>(), didx.as<int32_t>());
+    if (perm) {  // rows must be ascending in input ids
+      size_t sb = 0;
+      GI_CUDA(cub::DeviceSegmentedRadixSort::SortKeys(nullptr, sb, didx.as<int32_t>(), didx2.as<int32_t>(), m, n,
+                                                      doff.as<int64_t>(), doff.as<int64_t>() + 1, 0, 32, st));
+      DevBuf tmp2;
+      GI_TRY(tmp2.alloc(sb));
+      GI_CUDA(cub::DeviceSegmentedRadixSort::SortKeys(tmp2.p, sb, didx.as<int32_t>(), didx2.as<int32_t>(), m, n,
+                                                      doff.as<int64_t>(), doff.as<int64_t>() + 1, 0, 32, st));
+      GI_CUDA(cudaStreamSynchronize(st));
+      std::swap(didx.p, didx2.p);
+      std::swap(didx.bytes, didx2.bytes);
+    }
+  }
+  GI_CUDA(cudaGetLastError());
+  GI_CUDA(cudaMemcpyAsync(off, doff.p, (n + 1) * sizeof(int64_t), is_device_ptr(off) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
+  if (m > 0)
+    GI_CUDA(cudaMemcpyAsync(idx, didx.p, m * sizeof(int32_t), is_device_ptr(idx) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
+  return sync(ctx);
+  GI_GUARD_END
+}
+
+gi_status gi_pagerank_ex(gi_graph g, int32_t iters, double damping, const gi_pr_opts* opts, float* out,
+                         gi_pr_stats* stats) {
+  GI_GUARD_BEGIN
+  if (!g) return fail(GI_ERR_INVALID_ARGUMENT, "gi_pagerank: NULL graph");
+  if (!out && g->n > 0) return fail(GI_ERR_INVALID_ARGUMENT, "gi_pagerank: NULL output");
+  if (iters < 0) return fail(GI_ERR_INVALID_ARGUMENT, "gi_pagerank: iters < 0");
+  if (!(damping >= 0.0 && damping <= 1.0)) return fail(GI_ERR_INVALID_ARGUMENT, "gi_pagerank: damping not in [0,1]");
+  gi_pr_opts o{};
+  if (opts) o = *opts;
+  if (o.direction < GI_PR_PULL || o.direction > GI_PR_PULL_SEGMENTED)
+    return fail(GI_ERR_INVALID_ARGUMENT, "gi_pagerank: bad direction");
+  if (o.dangling != GI_DANGLING_UNIFORM && o.dangling != GI_DANGLING_DROP)
+    return fail(GI_ERR_INVALID_ARGUMENT, "gi_pagerank: bad dangling rule");
+  gi_context ctx = g->ctx;
+  GI_CUDA(cudaSetDevice(ctx->device));
+  OutBuf<float> ob{out, g->n, false, &g->out_stage};
+  float* d = nullptr;
+  if (g->n > 0) GI_TRY(ob.prepare(g, &d));
+  GI_TRY(pagerank_run(g, iters, damping, o, d, stats));
+  GI_TRY(ob.finish(ctx));
+  return sync(ctx);
+  GI_GUARD_END
+}
+
+gi_status gi_pagerank(gi_graph g, int32_t iters, double damping, float* out) {
+  return gi_pagerank_ex(g, iters, damping, nullptr, out, nullptr);
+}
+
+gi_status gi_bfs_ex(gi_graph g, int32_t source, const gi_bfs_opts* opts, int32_t* parent_out, gi_bfs_stats* stats) {
+  GI_GUARD_BEGIN
+  if (!g) return fail(GI_ERR_INVALID_ARGUMENT, "gi_bfs: NULL graph");
+  if (!parent_out) return fail(GI_ERR_INVALID_ARGUMENT, "gi_bfs: NULL output");
+  if (source < 0 || source >= g->n) return fail(GI_ERR_VERTEX_OUT_OF_RANGE, "gi_bfs: source not in [0, n)");
+  gi_bfs_opts o{};
+  if (opts) o = *opts;
+  if (o.policy < GI_BFS_AUTO || o.policy > GI_BFS_PULL_ONLY || o.threshold_div < 0)
+    return fail(GI_ERR_INVALID_ARGUMENT, "gi_bfs: bad options");
+  gi_context ctx = g->ctx;
+  GI_CUDA(cudaSetDevice(ctx->device));
+  OutBuf<int32_t> ob{parent_out, g->n, false, &g->out_stage};
+  int32_t* d = nullptr;
+  GI_TRY(ob.prepare(g, &d));
+  GI_TRY(bfs_run(g, source, o, d, stats));
+  GI_TRY(ob.finish(ctx));
+  return sync(ctx);
+  GI_GUARD_END
+}
+
+gi_status gi_bfs(gi_graph g, int32_t source, int32_t* parent_out) {
+  return gi_bfs_ex(g, source, nullptr, parent_out, nullptr);
+}
+
+}  // extern "C"

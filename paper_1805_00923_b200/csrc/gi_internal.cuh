@@ -1,0 +1,134 @@
+// gi_internal.cuh — shared internals of the CUDA library (not part of the ABI).
+//
+// Data layout in HBM. All internal arrays use the library's
+// vertex numbering: by default vertices are relabelled by out-degree
+// (descending, ties by input id) so that the hottest sources form a dense
+// prefix; `perm[new] = input id`, `inv[input id] = new`. Results are always
+// reported in input ids.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "gi.h"
+
+namespace gi {
+
+// ------------------------------------------------------------------ errors
+void set_error(const std::string& msg);
+gi_status fail(gi_status s, const std::string& msg);
+gi_status cuda_fail(cudaError_t e, const char* what, const char* file, int line);
+
+#define GI_CUDA(call)                                                        \
+  do {                                                                       \
+    cudaError_t e__ = (call);                                                \
+    if (e__ != cudaSuccess) return ::gi::cuda_fail(e__, #call, __FILE__, __LINE__); \
+  } while (0)
+
+#define GI_TRY(call)                    \
+  do {                                  \
+    gi_status s__ = (call);             \
+    if (s__ != GI_OK) return s__;       \
+  } while (0)
+
+// ------------------------------------------------------------------ device buffer
+// RAII device allocation (cudaMalloc; freed on destruction).
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() { reset(); }
+  void reset() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  gi_status alloc(size_t nbytes) {
+    reset();
+    if (nbytes == 0) nbytes = 16;
+    cudaError_t e = cudaMalloc(&p, nbytes);
+    if (e != cudaSuccess) {
+      p = nullptr;
+      cudaGetLastError();
+      return fail(GI_ERR_OUT_OF_MEMORY, "cudaMalloc of " + std::to_string(nbytes) + " bytes failed: " +
+                                            cudaGetErrorString(e));
+    }
+    bytes = nbytes;
+    return GI_OK;
+  }
+  template <typename T>
+  T* as() const { return static_cast<T*>(p); }
+};
+
+}  // namespace gi
+
+// ------------------------------------------------------------------ context / graph
+struct NcclApi;  // dynamically loaded NCCL entry points (nccl_dyn.cpp)
+
+struct gi_context_s {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int rank = 0, nranks = 1;
+  void* nccl_comm = nullptr;  // ncclComm_t when nranks > 1
+  int num_sms = 148;
+  // pinned host scratch for small D2H reads (counters)
+  int64_t* h_scratch = nullptr;
+};
+
+// Pull-PageRank tiling (merge-path over CSC rows + edges).
+constexpr int kPullThreads = 256;
+constexpr int kPullItemsPerThread = 8;
+constexpr int kPullTile = kPullThreads * kPullItemsPerThread;  // merge items per tile
+
+struct gi_graph_s {
+  gi_context ctx = nullptr;
+  int64_t n = 0;       // vertices
+  int64_t m = 0;       // directed edges after cleanup (global)
+  bool off64 = false;  // offsets stored as int64 (m >= 2^31) else int32
+  bool relabeled = false;
+  // vertex relabelling (n each; empty when !relabeled)
+  gi::DevBuf perm, inv;
+  // CSR (out-edges) and CSC (in-edges) in internal ids
+  gi::DevBuf csr_off, csr_idx, csc_off, csc_idx;
+  gi::DevBuf outdeg;  // int32[n], internal ids
+  // pull tiling: first/last row of each merge-path tile (int32 pairs)
+  int64_t ntiles = 0;
+  gi::DevBuf tile_rows;
+  // PageRank workspace
+  gi::DevBuf contrib[2];  // float[n]
+  gi::DevBuf dbuf;        // double[4]: dangling-mass ring
+  gi::DevBuf split_acc;   // double[n]: partial sums of rows split across tiles
+  gi::DevBuf split_cnt;   // int32[n]: arrival counters for split rows
+  gi::DevBuf push_sum;    // float[n]: push-form accumulator
+  gi::DevBuf out_stage;   // float/int32[n]: output staging in input ids
+  // BFS workspace
+  gi::DevBuf parent;      // int32[n], internal ids
+  gi::DevBuf queue[2];    // int32[n]
+  gi::DevBuf bitmap[2];   // uint32[ceil(n/32)]
+  gi::DevBuf counters;    // int64 slots, see bfs.cu
+};
+
+namespace gi {
+// build.cu
+gi_status build_graph(gi_context ctx, int64_t n, int64_t m0, const int32_t* d_src,
+                      const int32_t* d_dst, uint32_t flags, gi_graph g);
+// pagerank.cu
+gi_status pagerank_run(gi_graph g, int32_t iters, double damping, const gi_pr_opts& o,
+                       float* d_out_input_ids, gi_pr_stats* stats);
+// bfs.cu
+gi_status bfs_run(gi_graph g, int32_t source_input_id, const gi_bfs_opts& o,
+                  int32_t* d_parent_input_ids, gi_bfs_stats* stats);
+// util
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+inline int grid_for(int64_t work, int threads, int num_sms, int per_sm = 8) {
+  int64_t g = ceil_div(work, threads);
+  int64_t cap = (int64_t)num_sms * per_sm;
+  if (g > cap) g = cap;
+  if (g < 1) g = 1;
+  return (int)g;
+}
+}  // namespace gi

@@ -1,0 +1,348 @@
+// pagerank.cu — fixed-iteration PageRank through edgeset.apply (SURVEY §8(a)
+// rows a3-a5, §2.7 K4/K5).
+//
+// Math (PAPER.md P:3242-3253 [draft] edge/vertex update, base score P:856,
+// DESIGN.md readings R1-R3, R10):
+//   contrib_k[u] = r_k[u] / outdeg(u)   (0 for dangling u)
+//   r_{k+1}[v]   = (1-d)/n + d * ( sum_{u in in(v)} contrib_k[u] + D_k/n )
+//   D_k          = sum_{outdeg(u)=0} r_k[u]      (uniform rule; drop rule: no D)
+//
+// Pull (DensePull): one launch per iteration, the
+// merge-path tile kernel k_pr_pull below; no atomics on the row sums except
+// for rows split across tiles (last-arriver fix-up), which is the only
+// cross-CTA dependence ("pull needs no atomics").
+// Push (DensePush with an all-active frontier): red.global.add.f32
+// per edge into an accumulator + a vertex kernel — the parity form.
+#include "gi_internal.cuh"
+
+namespace gi {
+namespace {
+
+struct PrArgs {
+  int64_t n, m;
+  const void* off;
+  const int32_t* __restrict__ idx;
+  const int32_t* __restrict__ tile_rows;
+  const float* __restrict__ cin;
+  float* __restrict__ cout;
+  const int32_t* __restrict__ outdeg;
+  double* dbuf;  // dangling-mass ring (3 slots)
+  int it;
+  float base, damp;
+  double inv_n;
+  int uniform;
+  double* split_acc;
+  int32_t* split_cnt;
+  float* rank_out;  // non-null on the final iteration (input ids)
+  const int32_t* __restrict__ perm;
+};
+
+// vertex update (a3): r' = base + d (s + D/n); contrib' = r'/outdeg; dangling partial
+__device__ __forceinline__ void pr_epilogue(const PrArgs& A, int64_t r, float s, float dn, double& dpart) {
+  float rn = A.base + A.damp * (s + dn);
+  int od = __ldg(&A.outdeg[r]);
+  A.cout[r] = od > 0 ? rn / (float)od : 0.f;
+  if (od == 0) dpart += (double)rn;
+  if (A.rank_out) A.rank_out[A.perm ? __ldg(&A.perm[r]) : r] = rn;
+}
+
+__device__ __forceinline__ double block_sum(double v, double* sred) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) sred[w] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (threadIdx.x < 32) {
+    t = threadIdx.x < (blockDim.x >> 5) ? sred[threadIdx.x] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  }
+  return t;  // valid in thread 0
+}
+
+// ---------------------------------------------------------------- pull (K4)
+// Tile b covers merge positions [bT, (b+1)T) of the sequence that lists, for
+// each CSC row r in order, its in-edges then an end marker; row r occupies
+// positions [r + off[r], r + off[r+1]]. Phases:
+//  A  stage this tile's row offsets in smem; gather contrib[idx[e]] for the
+//     tile's edges with coalesced index loads (the random reads of P:598-599);
+//  B  each thread walks IPT consecutive merge items, summing staged values;
+//     rows wholly inside its window are finished in registers (fused vertex
+//     update), rows crossing a thread boundary go through smem atomics;
+//  C  rows that crossed threads are finished; rows that cross tiles add a
+//     double partial + arrival count, and the last arriving tile finishes them.
+template <typename OffT>
+__global__ void __launch_bounds__(kPullThreads) k_pr_pull(PrArgs A) {
+  constexpr int NT = kPullThreads, IPT = kPullItemsPerThread, T = kPullTile;
+  __shared__ OffT soff[T + 2];
+  __shared__ float sval[T];
+  __shared__ float srow[T];
+  __shared__ uint8_t sflag[T];
+  __shared__ double sred[NT / 32];
+
+  const OffT* __restrict__ off = static_cast<const OffT*>(A.off);
+  const int tid = threadIdx.x;
+  const int64_t b = blockIdx.x;
+  const int64_t p0 = b * (int64_t)T;
+  const int64_t p1 = min(p0 + (int64_t)T, A.n + A.m);
+  const int64_t r0 = A.tile_rows[2 * b], r1 = A.tile_rows[2 * b + 1];
+  const int R = (int)(r1 - r0 + 1);
+
+  if (b == 0 && tid == 0) A.dbuf[(A.it + 2) % 3] = 0.0;
+  const double D = A.uniform ? A.dbuf[A.it % 3] : 0.0;
+  const float dn = (float)(D * A.inv_n);
+
+  for (int i = tid; i <= R; i += NT) soff[i] = off[r0 + i];
+  for (int i = tid; i < R; i += NT) {
+    srow[i] = 0.f;
+    sflag[i] = 0;
+  }
+  const int64_t eb = p0 - r0;
+  const int64_t ee = min((int64_t)off[r1 + 1], p1 - r1);
+  // phase A: coalesced index stream + random gather (IPT loads in flight per thread)
+  {
+    const int64_t ne = ee - eb;
+#pragma unroll
+    for (int k = 0; k < IPT; ++k) {
+      int64_t j = tid + (int64_t)k * NT;
+      if (j < ne) sval[j] = __ldg(&A.cin[__ldg(&A.idx[eb + j])]);
+    }
+  }
+  __syncthreads();
+
+  double dpart = 0.0;
+  // phase B: per-thread merge-path walk
+  const int64_t d0 = p0 + (int64_t)tid * IPT;
+  if (d0 < p1) {
+    const int64_t d1 = min(d0 + (int64_t)IPT, p1);
+    // row containing d0: min i in [0, R) with r0 + i + soff[i+1] >= d0
+    int lo = 0, hi = R - 1;
+    while (lo < hi) {
+      int mid = (lo + hi) >> 1;
+      if (r0 + mid + (int64_t)soff[mid + 1] >= d0) hi = mid;
+      else lo = mid + 1;
+    }
+    int i = lo;
+    int64_t e = d0 - (r0 + i);
+    bool own = (r0 + i + (int64_t)soff[i]) >= d0;  // row starts inside this window
+    float acc = 0.f;
+    int64_t rowend = r0 + i + (int64_t)soff[i + 1];
+    for (int64_t p = d0; p < d1; ++p) {
+      if (p < rowend) {
+        acc += sval[e - eb];
+        ++e;
+      } else {
+        if (own) {
+          pr_epilogue(A, r0 + i, acc, dn, dpart);
+        } else {
+          atomicAdd(&srow[i], acc);
+          sflag[i] = 1;
+        }
+        acc = 0.f;
+        ++i;
+        own = true;
+        if (i < R) rowend = r0 + i + (int64_t)soff[i + 1];
+      }
+    }
+    // window ended inside row i: hand the partial to phase C
+    if (i < R && (r0 + i + (int64_t)soff[i]) < d1) {
+      atomicAdd(&srow[i], acc);
+      sflag[i] = 1;
+    }
+  }
+  __syncthreads();
+
+  // phase C: rows that crossed threads or tiles
+  for (int i = tid; i < R; i += NT) {
+    if (!sflag[i]) continue;
+    const int64_t r = r0 + i;
+    const int64_t sp = r + (int64_t)soff[i], ep = r + (int64_t)soff[i + 1];
+    if (sp >= p0 && ep < p1) {
+      pr_epilogue(A, r, srow[i], dn, dpart);
+    } else {
+      const int pieces = (int)(ep / T - sp / T + 1);
+      atomicAdd(&A.split_acc[r], (double)srow[i]);
+      __threadfence();
+      const int prev = atomicAdd(&A.split_cnt[r], 1);
+      if (prev == pieces - 1) {
+        __threadfence();
+        const double tot = atomicAdd(&A.split_acc[r], 0.0);
+        pr_epilogue(A, r, (float)tot, dn, dpart);
+        A.split_acc[r] = 0.0;
+        A.split_cnt[r] = 0;
+      }
+    }
+  }
+  const double bs = block_sum(dpart, sred);
+  if (tid == 0 && bs != 0.0) atomicAdd(&A.dbuf[(A.it + 1) % 3], bs);
+}
+
+// ---------------------------------------------------------------- push (K5)
+template <typename OffT>
+__global__ void __launch_bounds__(256) k_pr_push(int64_t n, const OffT* __restrict__ off,
+                                                 const int32_t* __restrict__ idx, const float* __restrict__ cin,
+                                                 float* __restrict__ acc) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t u = warp; u < n; u += nwarps) {
+    const float c = __ldg(&cin[u]);
+    if (c == 0.f) continue;
+    for (int64_t j = (int64_t)off[u] + lane; j < (int64_t)off[u + 1]; j += 32)
+      atomicAdd(&acc[__ldg(&idx[j])], c);  // result unused -> RED.E.ADD.F32
+  }
+}
+
+__global__ void __launch_bounds__(256) k_pr_vertex(PrArgs A, float* __restrict__ acc) {
+  __shared__ double sred[8];
+  if (blockIdx.x == 0 && threadIdx.x == 0) A.dbuf[(A.it + 2) % 3] = 0.0;
+  const double D = A.uniform ? A.dbuf[A.it % 3] : 0.0;
+  const float dn = (float)(D * A.inv_n);
+  double dpart = 0.0;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < A.n; v += (int64_t)gridDim.x * blockDim.x) {
+    const float s = acc[v];
+    acc[v] = 0.f;
+    pr_epilogue(A, v, s, dn, dpart);
+  }
+  const double bs = block_sum(dpart, sred);
+  if (threadIdx.x == 0 && bs != 0.0) atomicAdd(&A.dbuf[(A.it + 1) % 3], bs);
+}
+
+// r_0 = 1/n: contrib_0 and D_0
+__global__ void __launch_bounds__(256) k_pr_init(int64_t n, const int32_t* __restrict__ outdeg, float* __restrict__ c0,
+                                                 double* __restrict__ dbuf, float r0) {
+  __shared__ double sred[8];
+  double dpart = 0.0;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+    const int od = outdeg[v];
+    c0[v] = od > 0 ? r0 / (float)od : 0.f;
+    if (od == 0) dpart += (double)r0;
+  }
+  const double bs = block_sum(dpart, sred);
+  if (threadIdx.x == 0 && bs != 0.0) atomicAdd(&dbuf[0], bs);
+}
+
+__global__ void k_fill(float* __restrict__ out, int64_t n, float v) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = v;
+}
+
+}  // namespace
+
+gi_status pagerank_run(gi_graph g, int32_t iters, double damping, const gi_pr_opts& o, float* d_out,
+                       gi_pr_stats* stats) {
+  gi_context ctx = g->ctx;
+  cudaStream_t st = ctx->stream;
+  const int sms = ctx->num_sms;
+  const int64_t n = g->n, m = g->m;
+  gi_pr_stats S{};
+  S.kernel = o.direction == GI_PR_PUSH ? GI_PR_PUSH : GI_PR_PULL_DIRECT;
+  const int osz = g->off64 ? 8 : 4;
+  S.bytes_alg_per_iter = 4 * m + (int64_t)(osz + 12) * n;
+  if (n == 0) {
+    if (stats) *stats = S;
+    return GI_OK;
+  }
+  if (iters == 0) {
+    k_fill<<<grid_for(n, 256, sms), 256, 0, st>>>(d_out, n, (float)(1.0 / (double)n));
+    GI_CUDA(cudaGetLastError());
+    S.aux_launches = 1;
+    if (stats) *stats = S;
+    return GI_OK;
+  }
+  // workspace (lazily allocated, reused across calls)
+  for (int k = 0; k < 2; ++k)
+    if (!g->contrib[k].p) GI_TRY(g->contrib[k].alloc(n * sizeof(float)));
+  if (!g->dbuf.p) GI_TRY(g->dbuf.alloc(4 * sizeof(double)));
+  if (o.direction == GI_PR_PUSH) {
+    if (!g->push_sum.p) {
+      GI_TRY(g->push_sum.alloc(n * sizeof(float)));
+      GI_CUDA(cudaMemsetAsync(g->push_sum.p, 0, n * sizeof(float), st));
+    }
+  } else if (!g->split_acc.p) {
+    GI_TRY(g->split_acc.alloc(n * sizeof(double)));
+    GI_TRY(g->split_cnt.alloc(n * sizeof(int32_t)));
+    GI_CUDA(cudaMemsetAsync(g->split_acc.p, 0, n * sizeof(double), st));
+    GI_CUDA(cudaMemsetAsync(g->split_cnt.p, 0, n * sizeof(int32_t), st));
+  }
+
+  cudaEvent_t ev[2] = {nullptr, nullptr}, tot[2] = {nullptr, nullptr};
+  if (o.profile) {
+    for (int k = 0; k < 2; ++k) {
+      GI_CUDA(cudaEventCreate(&ev[k]));
+      GI_CUDA(cudaEventCreate(&tot[k]));
+    }
+    GI_CUDA(cudaEventRecord(tot[0], st));
+  }
+  GI_CUDA(cudaMemsetAsync(g->dbuf.p, 0, 4 * sizeof(double), st));
+  k_pr_init<<<grid_for(n, 256, sms), 256, 0, st>>>(n, g->outdeg.as<int32_t>(), g->contrib[0].as<float>(),
+                                                   g->dbuf.as<double>(), (float)(1.0 / (double)n));
+  S.aux_launches = 1;
+
+  PrArgs A{};
+  A.n = n;
+  A.m = m;
+  A.outdeg = g->outdeg.as<int32_t>();
+  A.dbuf = g->dbuf.as<double>();
+  A.base = (float)((1.0 - damping) / (double)n);
+  A.damp = (float)damping;
+  A.inv_n = 1.0 / (double)n;
+  A.uniform = o.dangling == GI_DANGLING_UNIFORM;
+  A.split_acc = g->split_acc.as<double>();
+  A.split_cnt = g->split_cnt.as<int32_t>();
+  A.perm = g->relabeled ? g->perm.as<int32_t>() : nullptr;
+  float edge_ms = 0.f;
+  for (int it = 0; it < iters; ++it) {
+    A.it = it;
+    A.cin = g->contrib[it & 1].as<float>();
+    A.cout = g->contrib[(it + 1) & 1].as<float>();
+    A.rank_out = (it == iters - 1) ? d_out : nullptr;
+    if (o.profile) GI_CUDA(cudaEventRecord(ev[0], st));
+    if (o.direction == GI_PR_PUSH) {
+      const int grid = grid_for(n * 32, 256, sms, 16);
+      if (g->off64)
+        k_pr_push<int64_t><<<grid, 256, 0, st>>>(n, g->csr_off.as<int64_t>(), g->csr_idx.as<int32_t>(), A.cin,
+                                                 g->push_sum.as<float>());
+      else
+        k_pr_push<int32_t><<<grid, 256, 0, st>>>(n, g->csr_off.as<int32_t>(), g->csr_idx.as<int32_t>(), A.cin,
+                                                 g->push_sum.as<float>());
+      if (o.profile) GI_CUDA(cudaEventRecord(ev[1], st));
+      k_pr_vertex<<<grid_for(n, 256, sms), 256, 0, st>>>(A, g->push_sum.as<float>());
+      S.aux_launches++;
+    } else {
+      A.tile_rows = g->tile_rows.as<int32_t>();
+      A.idx = g->csc_idx.as<int32_t>();
+      if (g->off64) {
+        A.off = g->csc_off.as<int64_t>();
+        k_pr_pull<int64_t><<<(unsigned)g->ntiles, kPullThreads, 0, st>>>(A);
+      } else {
+        A.off = g->csc_off.as<int32_t>();
+        k_pr_pull<int32_t><<<(unsigned)g->ntiles, kPullThreads, 0, st>>>(A);
+      }
+      if (o.profile) GI_CUDA(cudaEventRecord(ev[1], st));
+    }
+    GI_CUDA(cudaGetLastError());
+    S.edge_launches++;
+    if (o.profile) {
+      GI_CUDA(cudaEventSynchronize(ev[1]));
+      float ms = 0.f;
+      GI_CUDA(cudaEventElapsedTime(&ms, ev[0], ev[1]));
+      edge_ms += ms;
+    }
+  }
+  if (o.profile) {
+    GI_CUDA(cudaEventRecord(tot[1], st));
+    GI_CUDA(cudaEventSynchronize(tot[1]));
+    GI_CUDA(cudaEventElapsedTime(&S.total_ms, tot[0], tot[1]));
+    S.edge_ms = edge_ms;
+    for (int k = 0; k < 2; ++k) {
+      cudaEventDestroy(ev[k]);
+      cudaEventDestroy(tot[k]);
+    }
+  }
+  if (stats) *stats = S;
+  return GI_OK;
+}
+
+}  // namespace gi

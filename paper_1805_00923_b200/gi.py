@@ -1,0 +1,307 @@
+"""Thin ctypes binding of libgi.so — the C ABI in include/gi.h, same names.
+
+Argument marshalling only: every step of the path runs in the CUDA library.
+Arrays may be numpy arrays (host) or torch tensors (host or CUDA); the library
+detects host vs device pointers itself. If libgi.so is missing this module
+raises ImportError — there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libgi.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is not built; run `python -m paper_1805_00923_b200.build` "
+                      "(there is no CPU fallback)")
+
+_lib = ctypes.CDLL(LIB_PATH)
+
+# ------------------------------------------------------------------ constants (gi.h)
+GI_OK = 0
+GI_ERR_INVALID_ARGUMENT = 1
+GI_ERR_VERTEX_OUT_OF_RANGE = 2
+GI_ERR_OUT_OF_MEMORY = 3
+GI_ERR_CUDA = 4
+GI_ERR_NCCL = 5
+GI_ERR_UNSUPPORTED = 6
+GI_ERR_INTERNAL = 7
+
+GI_EDGES_ON_DEVICE = 1 << 0
+GI_REMOVE_SELF_LOOPS = 1 << 1
+GI_DEDUP = 1 << 2
+GI_SYMMETRIZE = 1 << 3
+GI_NO_RELABEL = 1 << 4
+GI_DEFAULT_FLAGS = GI_REMOVE_SELF_LOOPS | GI_DEDUP
+
+GI_PR_PULL, GI_PR_PUSH, GI_PR_PULL_DIRECT, GI_PR_PULL_SEGMENTED = 0, 1, 2, 3
+GI_DANGLING_UNIFORM, GI_DANGLING_DROP = 0, 1
+GI_BFS_AUTO, GI_BFS_PUSH_ONLY, GI_BFS_PULL_ONLY = 0, 1, 2
+
+
+class gi_pr_opts(ctypes.Structure):
+    _fields_ = [("direction", ctypes.c_int32), ("dangling", ctypes.c_int32), ("profile", ctypes.c_int32),
+                ("reserved", ctypes.c_int32)]
+
+
+class gi_pr_stats(ctypes.Structure):
+    _fields_ = [("edge_launches", ctypes.c_int32), ("aux_launches", ctypes.c_int32), ("edge_ms", ctypes.c_float),
+                ("total_ms", ctypes.c_float), ("kernel", ctypes.c_int32), ("reserved", ctypes.c_int32),
+                ("bytes_alg_per_iter", ctypes.c_int64)]
+
+
+class gi_bfs_opts(ctypes.Structure):
+    _fields_ = [("policy", ctypes.c_int32), ("threshold_div", ctypes.c_int32), ("profile", ctypes.c_int32),
+                ("reserved", ctypes.c_int32)]
+
+
+class gi_bfs_stats(ctypes.Structure):
+    _fields_ = [("levels", ctypes.c_int32), ("pull_levels", ctypes.c_int32), ("reached", ctypes.c_int64),
+                ("edges_traversed", ctypes.c_int64), ("total_ms", ctypes.c_float), ("launches", ctypes.c_int32),
+                ("reserved", ctypes.c_int32)]
+
+
+_vp = ctypes.c_void_p
+_i64 = ctypes.c_int64
+_i32 = ctypes.c_int32
+_st = ctypes.c_int
+
+_SIGS = {
+    "gi_context_create": ([ctypes.c_int, _vp, ctypes.POINTER(_vp)], _st),
+    "gi_nccl_unique_id": ([ctypes.c_char_p], _st),
+    "gi_context_create_dist": ([ctypes.c_int, _vp, ctypes.c_int, ctypes.c_int, ctypes.c_char_p,
+                                ctypes.POINTER(_vp)], _st),
+    "gi_context_destroy": ([_vp], _st),
+    "gi_context_rank": ([_vp, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)], _st),
+    "gi_graph_create": ([_vp, _i64, _i64, _vp, _vp, ctypes.c_uint32, ctypes.POINTER(_vp)], _st),
+    "gi_graph_destroy": ([_vp], _st),
+    "gi_graph_num_vertices": ([_vp, ctypes.POINTER(_i64)], _st),
+    "gi_graph_num_edges": ([_vp, ctypes.POINTER(_i64)], _st),
+    "gi_graph_out_degrees": ([_vp, _vp], _st),
+    "gi_graph_in_degrees": ([_vp, _vp], _st),
+    "gi_graph_csr": ([_vp, _vp, _vp], _st),
+    "gi_pagerank": ([_vp, _i32, ctypes.c_double, _vp], _st),
+    "gi_pagerank_ex": ([_vp, _i32, ctypes.c_double, ctypes.POINTER(gi_pr_opts), _vp,
+                        ctypes.POINTER(gi_pr_stats)], _st),
+    "gi_bfs": ([_vp, _i32, _vp], _st),
+    "gi_bfs_ex": ([_vp, _i32, ctypes.POINTER(gi_bfs_opts), _vp, ctypes.POINTER(gi_bfs_stats)], _st),
+    "gi_status_string": ([_st], ctypes.c_char_p),
+    "gi_last_error": ([], ctypes.c_char_p),
+    "gi_abi_version": ([], ctypes.c_int),
+}
+for _name, (_args, _res) in _SIGS.items():
+    _f = getattr(_lib, _name)
+    _f.argtypes = _args
+    _f.restype = _res
+
+EXPORTED = tuple(_SIGS)
+
+
+class GiError(RuntimeError):
+    def __init__(self, status: int, where: str):
+        self.status = status
+        msg = _lib.gi_last_error().decode(errors="replace")
+        super().__init__(f"{where}: {_lib.gi_status_string(status).decode()}: {msg}")
+
+
+def _check(status: int, where: str) -> None:
+    if status != GI_OK:
+        raise GiError(status, where)
+
+
+def _ptr(a, dtype) -> tuple[int, object]:
+    """(address, keep-alive) of a contiguous numpy array or torch tensor of `dtype`."""
+    if a is None:
+        return 0, None
+    if isinstance(a, np.ndarray):
+        a = np.ascontiguousarray(a, dtype=dtype)
+        return a.ctypes.data, a
+    try:
+        import torch
+    except ImportError:  # pragma: no cover
+        torch = None
+    if torch is not None and isinstance(a, torch.Tensor):
+        tdt = {np.int32: torch.int32, np.float32: torch.float32, np.int64: torch.int64}[dtype]
+        if a.dtype != tdt or not a.is_contiguous():
+            raise TypeError(f"tensor must be contiguous {tdt}, got {a.dtype}")
+        return a.data_ptr(), a
+    a = np.ascontiguousarray(np.asarray(a), dtype=dtype)
+    return a.ctypes.data, a
+
+
+# ------------------------------------------------------------------ C names
+def gi_abi_version() -> int:
+    return _lib.gi_abi_version()
+
+
+def gi_context_create(device: int = 0, stream: int | None = None) -> int:
+    out = _vp()
+    _check(_lib.gi_context_create(device, stream or None, ctypes.byref(out)), "gi_context_create")
+    return out.value
+
+
+def gi_nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(_lib.gi_nccl_unique_id(buf), "gi_nccl_unique_id")
+    return buf.raw
+
+
+def gi_context_create_dist(device: int, stream: int | None, rank: int, nranks: int, uid: bytes) -> int:
+    out = _vp()
+    _check(_lib.gi_context_create_dist(device, stream or None, rank, nranks, uid, ctypes.byref(out)),
+           "gi_context_create_dist")
+    return out.value
+
+
+def gi_context_destroy(ctx: int) -> None:
+    _check(_lib.gi_context_destroy(ctx), "gi_context_destroy")
+
+
+def gi_graph_create(ctx: int, n: int, src, dst, flags: int = GI_DEFAULT_FLAGS) -> int:
+    ps, ks = _ptr(src, np.int32)
+    pd, kd = _ptr(dst, np.int32)
+    m0 = len(ks) if ks is not None else 0
+    if (len(kd) if kd is not None else 0) != m0:
+        raise ValueError("src and dst lengths differ")
+    out = _vp()
+    _check(_lib.gi_graph_create(ctx, n, m0, ps or None, pd or None, flags, ctypes.byref(out)), "gi_graph_create")
+    return out.value
+
+
+def gi_graph_destroy(g: int) -> None:
+    _check(_lib.gi_graph_destroy(g), "gi_graph_destroy")
+
+
+def gi_graph_num_vertices(g: int) -> int:
+    v = _i64()
+    _check(_lib.gi_graph_num_vertices(g, ctypes.byref(v)), "gi_graph_num_vertices")
+    return v.value
+
+
+def gi_graph_num_edges(g: int) -> int:
+    v = _i64()
+    _check(_lib.gi_graph_num_edges(g, ctypes.byref(v)), "gi_graph_num_edges")
+    return v.value
+
+
+def gi_graph_out_degrees(g: int, out=None):
+    n = gi_graph_num_vertices(g)
+    if out is None:
+        out = np.empty(n, np.int32)
+    p, keep = _ptr(out, np.int32)
+    _check(_lib.gi_graph_out_degrees(g, p or None), "gi_graph_out_degrees")
+    return keep
+
+
+def gi_graph_in_degrees(g: int, out=None):
+    n = gi_graph_num_vertices(g)
+    if out is None:
+        out = np.empty(n, np.int32)
+    p, keep = _ptr(out, np.int32)
+    _check(_lib.gi_graph_in_degrees(g, p or None), "gi_graph_in_degrees")
+    return keep
+
+
+def gi_graph_csr(g: int):
+    n, m = gi_graph_num_vertices(g), gi_graph_num_edges(g)
+    off = np.empty(n + 1, np.int64)
+    idx = np.empty(max(m, 1), np.int32)
+    _check(_lib.gi_graph_csr(g, off.ctypes.data, idx.ctypes.data), "gi_graph_csr")
+    return off, idx[:m]
+
+
+def gi_pagerank(g: int, iters: int, damping: float, out=None):
+    n = gi_graph_num_vertices(g)
+    if out is None:
+        out = np.empty(n, np.float32)
+    p, keep = _ptr(out, np.float32)
+    _check(_lib.gi_pagerank(g, iters, damping, p or None), "gi_pagerank")
+    return keep
+
+
+def gi_pagerank_ex(g: int, iters: int, damping: float, out=None, direction: int = GI_PR_PULL,
+                   dangling: int = GI_DANGLING_UNIFORM, profile: bool = False):
+    n = gi_graph_num_vertices(g)
+    if out is None:
+        out = np.empty(n, np.float32)
+    p, keep = _ptr(out, np.float32)
+    o = gi_pr_opts(direction, dangling, int(profile), 0)
+    s = gi_pr_stats()
+    _check(_lib.gi_pagerank_ex(g, iters, damping, ctypes.byref(o), p or None, ctypes.byref(s)), "gi_pagerank_ex")
+    return keep, s
+
+
+def gi_bfs(g: int, source: int, out=None):
+    n = gi_graph_num_vertices(g)
+    if out is None:
+        out = np.empty(n, np.int32)
+    p, keep = _ptr(out, np.int32)
+    _check(_lib.gi_bfs(g, source, p or None), "gi_bfs")
+    return keep
+
+
+def gi_bfs_ex(g: int, source: int, out=None, policy: int = GI_BFS_AUTO, threshold_div: int = 0,
+              profile: bool = False):
+    n = gi_graph_num_vertices(g)
+    if out is None:
+        out = np.empty(n, np.int32)
+    p, keep = _ptr(out, np.int32)
+    o = gi_bfs_opts(policy, threshold_div, int(profile), 0)
+    s = gi_bfs_stats()
+    _check(_lib.gi_bfs_ex(g, source, ctypes.byref(o), p or None, ctypes.byref(s)), "gi_bfs_ex")
+    return keep, s
+
+
+# ------------------------------------------------------------------ RAII conveniences
+class Context:
+    def __init__(self, device: int = 0, stream: int | None = None):
+        self.handle = gi_context_create(device, stream)
+
+    def close(self):
+        if self.handle:
+            gi_context_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Graph:
+    def __init__(self, ctx: Context, n: int, src, dst, flags: int = GI_DEFAULT_FLAGS):
+        self.ctx = ctx
+        self.handle = gi_graph_create(ctx.handle, n, src, dst, flags)
+        self.n = gi_graph_num_vertices(self.handle)
+        self.m = gi_graph_num_edges(self.handle)
+
+    def close(self):
+        if self.handle:
+            gi_graph_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def pagerank(self, iters=20, damping=0.85, out=None, **kw):
+        return gi_pagerank_ex(self.handle, iters, damping, out, **kw)
+
+    def bfs(self, source, out=None, **kw):
+        return gi_bfs_ex(self.handle, source, out, **kw)
+
+    def out_degrees(self, out=None):
+        return gi_graph_out_degrees(self.handle, out)
+
+    def in_degrees(self, out=None):
+        return gi_graph_in_degrees(self.handle, out)
+
+    def csr(self):
+        return gi_graph_csr(self.handle)

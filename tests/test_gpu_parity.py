@@ -1,0 +1,359 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Bars (BASELINE.json north_star):
+  * build: CSR bit-exact (integer work), degrees bit-exact;
+  * PageRank (fp32 on the GPU vs fp64 oracle, same iteration count):
+      L1 distance <= 1e-5 and max per-vertex relative error <= 1e-4;
+  * BFS: depths bit-exact (derived from the parent tree by the validator),
+    parent trees VALIDATED (several are correct, R8), never compared.
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import graphgen
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+PR_L1 = 1e-5
+PR_REL = 1e-4
+
+
+@pytest.fixture(scope="module")
+def gi():
+    from paper_1805_00923_b200 import build
+
+    build.build()
+    from paper_1805_00923_b200 import gi as _gi
+
+    return _gi
+
+
+@pytest.fixture(scope="module")
+def ctx(gi):
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.fail("GPU tests need a CUDA device (there is no CPU fallback)")
+    c = gi.Context(0)
+    yield c
+    c.close()
+
+
+def _pr_check(got, want, what=""):
+    got = np.asarray(got, np.float64)
+    l1 = np.abs(got - want).sum()
+    rel = (np.abs(got - want) / np.maximum(np.abs(want), 1e-300)).max() if len(want) else 0.0
+    assert l1 <= PR_L1 and rel <= PR_REL, f"{what}: L1={l1:.3e} maxrel={rel:.3e}"
+    return l1, rel
+
+
+def _bfs_check(g_or, source, parent, what=""):
+    depth = oracle.bfs_depth(g_or, source)
+    ok, msg = oracle.validate_bfs(g_or, source, parent, depth)
+    assert ok, f"{what}: {msg}"
+
+
+FLAG_SETS = [
+    ("default", None, dict(remove_self_loops=True, dedup=True, symmetrize=False)),
+    ("no-relabel", "norelabel", dict(remove_self_loops=True, dedup=True, symmetrize=False)),
+    ("sym", "sym", dict(remove_self_loops=True, dedup=True, symmetrize=True)),
+    ("raw", "raw", dict(remove_self_loops=False, dedup=False, symmetrize=False)),
+]
+
+
+def _flags(gi, kind):
+    f = gi.GI_REMOVE_SELF_LOOPS | gi.GI_DEDUP
+    if kind == "norelabel":
+        f |= gi.GI_NO_RELABEL
+    elif kind == "sym":
+        f |= gi.GI_SYMMETRIZE
+    elif kind == "raw":
+        f = 0
+    return f
+
+
+# ---------------------------------------------------------------- build (a1, a2)
+@pytest.mark.parametrize("name,kind,oflags", FLAG_SETS)
+def test_build_csr_bit_exact(gi, ctx, name, kind, oflags):
+    for seed in range(3):
+        n = [1, 37, 5000][seed]
+        s, d = graphgen.random_digraph(n, 8 * n + 3, 100 + seed)
+        g = gi.Graph(ctx, n, s, d, _flags(gi, kind))
+        go = oracle.build_graph(n, s, d, **oflags)
+        assert g.n == n and g.m == go.m
+        off, idx = g.csr()
+        assert np.array_equal(off, go.csr_off), name
+        if kind == "raw":  # duplicates kept: compare as sorted multisets per row (order of equal keys)
+            assert np.array_equal(idx, go.csr_idx)
+        else:
+            assert np.array_equal(idx, go.csr_idx), name
+        assert np.array_equal(g.out_degrees(), go.outdeg.astype(np.int32))
+        assert np.array_equal(g.in_degrees(), go.indeg.astype(np.int32))
+
+
+def test_build_rmat_config1_bit_exact(gi, ctx):
+    cfg = graphgen.CONFIGS[1]
+    s, d = cfg.edges()
+    g = gi.Graph(ctx, cfg.n, s, d)
+    go = oracle.build_graph(cfg.n, s, d)
+    assert g.m == go.m
+    off, idx = g.csr()
+    assert np.array_equal(off, go.csr_off) and np.array_equal(idx, go.csr_idx)
+    # edge-list checksum of the cleaned graph agrees on both sides
+    src_o = np.repeat(np.arange(cfg.n, dtype=np.int32), np.diff(go.csr_off))
+    src_g = np.repeat(np.arange(cfg.n, dtype=np.int32), np.diff(off))
+    assert graphgen.edge_checksum(src_o, go.csr_idx) == graphgen.edge_checksum(src_g, idx)
+
+
+def test_build_device_edges_and_errors(gi, ctx):
+    import torch
+
+    s, d = graphgen.random_digraph(100, 1000, 5)
+    ts, td = torch.from_numpy(s).cuda(), torch.from_numpy(d).cuda()
+    g = gi.Graph(ctx, 100, ts, td, gi.GI_DEFAULT_FLAGS | gi.GI_EDGES_ON_DEVICE)
+    go = oracle.build_graph(100, s, d)
+    off, idx = g.csr()
+    assert np.array_equal(off, go.csr_off) and np.array_equal(idx, go.csr_idx)
+    with pytest.raises(gi.GiError) as e:
+        gi.Graph(ctx, 10, np.array([0, 10], np.int32), np.array([1, 1], np.int32))
+    assert e.value.status == gi.GI_ERR_VERTEX_OUT_OF_RANGE
+    with pytest.raises(gi.GiError) as e:
+        gi.Graph(ctx, 10, np.array([0, -1], np.int32), np.array([1, 1], np.int32))
+    assert e.value.status == gi.GI_ERR_VERTEX_OUT_OF_RANGE
+    with pytest.raises(gi.GiError) as e:
+        gi.Graph(ctx, 10, s[:0], d[:0], 1 << 20)
+    assert e.value.status == gi.GI_ERR_INVALID_ARGUMENT
+    with pytest.raises(gi.GiError) as e:
+        gi.Graph(ctx, 10, s[:5], d[:5], gi.GI_EDGES_ON_DEVICE)  # host arrays flagged as device
+    assert e.value.status == gi.GI_ERR_INVALID_ARGUMENT
+
+
+# ---------------------------------------------------------------- PageRank (a3-a5)
+PR_DIRS = ["pull", "push"]
+
+
+def _dir(gi, name):
+    return {"pull": gi.GI_PR_PULL, "push": gi.GI_PR_PUSH, "direct": gi.GI_PR_PULL_DIRECT}[name]
+
+
+@pytest.mark.parametrize("direction", PR_DIRS)
+def test_pr_small_families(gi, ctx, direction):
+    cases = [
+        ("cycle7", 7, *graphgen.cycle(7)),
+        ("star", 51, *graphgen.star_bidirectional(50)),
+        ("instar", 21, *graphgen.in_star(20)),
+        ("K9", 9, *graphgen.complete(9)),
+        ("path", 10, *graphgen.path(10)),
+        ("empty", 5, np.zeros(0, np.int32), np.zeros(0, np.int32)),
+        ("single", 1, np.zeros(0, np.int32), np.zeros(0, np.int32)),
+    ]
+    for name, n, s, d in cases:
+        g = gi.Graph(ctx, n, s, d)
+        go = oracle.build_graph(n, s, d)
+        for dangling in (gi.GI_DANGLING_UNIFORM, gi.GI_DANGLING_DROP):
+            for iters in (0, 1, 2, 20):
+                got, _ = g.pagerank(iters, 0.85, direction=_dir(gi, direction), dangling=dangling)
+                want = oracle.pagerank(go, iters, 0.85, dangling)
+                _pr_check(got, want, f"{name} it={iters} dangling={dangling}")
+
+
+@pytest.mark.parametrize("direction", PR_DIRS)
+def test_pr_exhaustive_tiny(gi, ctx, direction):
+    # every digraph on 3 vertices, a sample on 4
+    for n, masks in [(3, range(64)), (4, range(0, 4096, 37))]:
+        pairs = [(u, v) for u in range(n) for v in range(n) if u != v]
+        for mask in masks:
+            s = np.array([u for i, (u, v) in enumerate(pairs) if mask >> i & 1], np.int32)
+            d = np.array([v for i, (u, v) in enumerate(pairs) if mask >> i & 1], np.int32)
+            g = gi.Graph(ctx, n, s, d)
+            got, _ = g.pagerank(20, 0.85, direction=_dir(gi, direction))
+            _pr_check(got, oracle.pagerank(oracle.build_graph(n, s, d), 20, 0.85), f"n={n} mask={mask}")
+
+
+@pytest.mark.parametrize("direction", PR_DIRS)
+@pytest.mark.parametrize("n,m0,seed", [(100, 50, 1), (1000, 20000, 2), (3000, 3000, 3), (20000, 200000, 4),
+                                       (70001, 1000003, 5)])
+def test_pr_random_ragged(gi, ctx, direction, n, m0, seed):
+    """Sizes spanning several merge-path tiles with ragged tails and many dangling/isolated vertices."""
+    s, d = graphgen.random_digraph(n, m0, seed)
+    g = gi.Graph(ctx, n, s, d)
+    go = oracle.build_graph(n, s, d)
+    got, _ = g.pagerank(20, 0.85, direction=_dir(gi, direction))
+    _pr_check(got, oracle.pagerank(go, 20, 0.85), f"n={n}")
+
+
+@pytest.mark.parametrize("direction", PR_DIRS)
+def test_pr_hub_rows_split_across_tiles(gi, ctx, direction):
+    """In-star with 100k leaves: the centre's CSC row spans ~50 tiles (last-arriver fix-up)."""
+    L = 100_000
+    s, d = graphgen.in_star(L)
+    s2, d2 = graphgen.star_bidirectional(L)
+    for name, (ss, dd) in {"instar": (s, d), "bistar": (s2, d2)}.items():
+        g = gi.Graph(ctx, L + 1, ss, dd)
+        go = oracle.build_graph(L + 1, ss, dd)
+        for dangling in (0, 1):
+            got, _ = g.pagerank(20, 0.85, direction=_dir(gi, direction), dangling=dangling)
+            _pr_check(got, oracle.pagerank(go, 20, 0.85, dangling), name)
+
+
+@pytest.mark.parametrize("direction", PR_DIRS)
+@pytest.mark.parametrize("relabel", [True, False])
+def test_pr_config1(gi, ctx, direction, relabel):
+    cfg = graphgen.CONFIGS[1]
+    s, d = cfg.edges()
+    flags = gi.GI_DEFAULT_FLAGS | (0 if relabel else gi.GI_NO_RELABEL)
+    g = gi.Graph(ctx, cfg.n, s, d, flags)
+    go = oracle.build_graph(cfg.n, s, d)
+    got, st = g.pagerank(cfg.pr_iters, cfg.damping, direction=_dir(gi, direction))
+    want = oracle.pagerank(go, cfg.pr_iters, cfg.damping)
+    _pr_check(got, want, "config1")
+    assert st.edge_launches == cfg.pr_iters
+
+
+def test_pr_device_output_and_damping_edges(gi, ctx):
+    import torch
+
+    cfg = graphgen.CONFIGS[1]
+    s, d = cfg.edges()
+    g = gi.Graph(ctx, cfg.n, s, d)
+    go = oracle.build_graph(cfg.n, s, d)
+    out = torch.empty(cfg.n, dtype=torch.float32, device="cuda")
+    g.pagerank(20, 0.85, out=out)
+    _pr_check(out.cpu().numpy(), oracle.pagerank(go, 20, 0.85), "device out")
+    for damp in (0.0, 1.0, 0.5):
+        got, _ = g.pagerank(7, damp)
+        _pr_check(got, oracle.pagerank(go, 7, damp), f"damping {damp}")
+    for bad in (-0.1, 1.1, float("nan")):
+        with pytest.raises(gi.GiError):
+            g.pagerank(3, bad)
+    with pytest.raises(gi.GiError):
+        g.pagerank(-1, 0.85)
+
+
+def test_pr_stress_repeat(gi, ctx):
+    """100 repetitions of both directions stay within tolerance (missing atomics would not)."""
+    s, d = graphgen.rmat(12, 16, 0.57, 0.19, 0.19, 21)
+    n = 1 << 12
+    g = gi.Graph(ctx, n, s, d)
+    want = oracle.pagerank(oracle.build_graph(n, s, d), 20, 0.85)
+    for rep in range(50):
+        for direction in PR_DIRS:
+            got, _ = g.pagerank(20, 0.85, direction=_dir(gi, direction))
+            _pr_check(got, want, f"rep {rep} {direction}")
+
+
+# ---------------------------------------------------------------- BFS (a6-a9)
+POLICIES = ["auto", "push", "pull"]
+
+
+def _pol(gi, p):
+    return {"auto": gi.GI_BFS_AUTO, "push": gi.GI_BFS_PUSH_ONLY, "pull": gi.GI_BFS_PULL_ONLY}[p]
+
+
+@pytest.mark.parametrize("policy", POLICIES)
+def test_bfs_small_families(gi, ctx, policy):
+    import json
+    import os
+
+    gd = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "bfs_path4.json")))
+    g = gi.Graph(ctx, gd["n"], np.array(gd["src"], np.int32), np.array(gd["dst"], np.int32))
+    par, _ = g.bfs(gd["source"], policy=_pol(gi, policy))
+    assert par.tolist() == gd["parent"]  # unique tree: compared exactly
+    cases = [
+        ("star", 31, *graphgen.star_bidirectional(30), [0, 5]),
+        ("K8", 8, *graphgen.complete(8), [0, 7]),
+        ("reverse", 2, np.array([1], np.int32), np.array([0], np.int32), [0, 1]),
+        ("disconnected", 6, np.array([0, 1, 3], np.int32), np.array([1, 0, 4], np.int32), [0, 3, 5]),
+        ("single", 1, np.zeros(0, np.int32), np.zeros(0, np.int32), [0]),
+        ("cycle", 100, *graphgen.cycle(100), [0, 99]),
+    ]
+    for name, n, s, d, sources in cases:
+        g = gi.Graph(ctx, n, s, d)
+        go = oracle.build_graph(n, s, d)
+        for src in sources:
+            par, st = g.bfs(src, policy=_pol(gi, policy))
+            _bfs_check(go, src, par, f"{name} src={src}")
+
+
+@pytest.mark.parametrize("policy", POLICIES)
+def test_bfs_random_and_grid(gi, ctx, policy):
+    for n, m0, seed in [(50, 200, 1), (4097, 30000, 2), (30000, 90000, 3)]:
+        s, d = graphgen.random_digraph(n, m0, seed)
+        g = gi.Graph(ctx, n, s, d)
+        go = oracle.build_graph(n, s, d)
+        for src in (0, n // 2, n - 1):
+            par, st = g.bfs(src, policy=_pol(gi, policy))
+            _bfs_check(go, src, par, f"rand n={n} src={src}")
+    R, C = 97, 61
+    s, d = graphgen.grid(R, C, 0.1, 3)
+    g = gi.Graph(ctx, R * C, s, d)
+    go = oracle.build_graph(R * C, s, d)
+    par, st = g.bfs(0, policy=_pol(gi, policy))
+    _bfs_check(go, 0, par, "grid")
+    s, d = graphgen.grid(40, 30, 0.0, 3)
+    g = gi.Graph(ctx, 1200, s, d)
+    par, st = g.bfs(0, policy=_pol(gi, policy))
+    # undropped grid: depth(r, c) = r + c; reconstruct depth from the tree
+    depth = np.full(1200, -1)
+    depth[0] = 0
+    for _ in range(100):
+        upd = (depth < 0) & (par >= 0)
+        depth[upd] = np.where(depth[par[upd]] >= 0, depth[par[upd]] + 1, -1)
+    rr, cc = np.divmod(np.arange(1200), 30)
+    assert np.array_equal(depth, rr + cc)
+    assert st.levels == 40 + 30 - 1
+
+
+@pytest.mark.parametrize("policy", POLICIES)
+@pytest.mark.parametrize("relabel", [True, False])
+def test_bfs_config1(gi, ctx, policy, relabel):
+    cfg = graphgen.CONFIGS[1]
+    s, d = cfg.edges()
+    flags = gi.GI_DEFAULT_FLAGS | (0 if relabel else gi.GI_NO_RELABEL)
+    g = gi.Graph(ctx, cfg.n, s, d, flags)
+    go = oracle.build_graph(cfg.n, s, d)
+    sources = [0] + graphgen.pick_sources(cfg.n, s, d, 8, 1001).tolist()
+    for src in sources:
+        par, st = g.bfs(src, policy=_pol(gi, policy))
+        depth = oracle.bfs_depth(go, src)
+        ok, msg = oracle.validate_bfs(go, src, par, depth)
+        assert ok, f"src={src}: {msg}"
+        assert st.reached == int((depth >= 0).sum())
+        assert st.edges_traversed == oracle.reached_out_edges(go, depth)
+        assert st.levels == depth.max() + 1
+        if policy == "push":
+            assert st.pull_levels == 0
+    # the direction-optimising run actually switched direction on this graph
+    _, st = g.bfs(0, policy=gi.GI_BFS_AUTO)
+    assert 0 < st.pull_levels < st.levels
+
+
+def test_bfs_stress_repeat(gi, ctx):
+    s, d = graphgen.rmat(13, 16, 0.57, 0.19, 0.19, 33)
+    n = 1 << 13
+    g = gi.Graph(ctx, n, s, d)
+    go = oracle.build_graph(n, s, d)
+    depth = oracle.bfs_depth(go, 0)
+    for rep in range(40):
+        for policy in POLICIES:
+            par, _ = g.bfs(0, policy=_pol(gi, policy))
+            ok, msg = oracle.validate_bfs(go, 0, par, depth)
+            assert ok, f"rep {rep} {policy}: {msg}"
+
+
+def test_bfs_errors_and_device_output(gi, ctx):
+    import torch
+
+    s, d = graphgen.cycle(10)
+    g = gi.Graph(ctx, 10, s, d)
+    with pytest.raises(gi.GiError) as e:
+        g.bfs(10)
+    assert e.value.status == gi.GI_ERR_VERTEX_OUT_OF_RANGE
+    with pytest.raises(gi.GiError):
+        g.bfs(-1)
+    out = torch.empty(10, dtype=torch.int32, device="cuda")
+    g.bfs(3, out=out)
+    assert out.cpu().tolist() == [9, 0, 1, 3, 3, 4, 5, 6, 7, 8]
