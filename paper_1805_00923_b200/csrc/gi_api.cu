@@ -155,6 +155,8 @@ gi_status gi_context_create(int device, void* cuda_stream, gi_context* out) {
 
 gi_status gi_context_destroy(gi_context ctx) {
   if (!ctx) return fail(GI_ERR_INVALID_ARGUMENT, "gi_context_destroy: NULL context");
+  if (ctx->live_graphs > 0)
+    return fail(GI_ERR_INVALID_ARGUMENT, "gi_context_destroy: destroy the context's graphs first");
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
   if (ctx->nccl_comm) {
@@ -202,6 +204,7 @@ gi_status gi_graph_create(gi_context ctx, int64_t n, int64_t m0, const int32_t* 
     delete g;
     return s;
   }
+  ctx->live_graphs++;
   *out = g;
   return GI_OK;
   GI_GUARD_END
@@ -211,6 +214,7 @@ gi_status gi_graph_destroy(gi_graph g) {
   if (!g) return fail(GI_ERR_INVALID_ARGUMENT, "gi_graph_destroy: NULL graph");
   cudaSetDevice(g->ctx->device);
   cudaStreamSynchronize(g->ctx->stream);
+  g->ctx->live_graphs--;
   delete g;
   return GI_OK;
 }

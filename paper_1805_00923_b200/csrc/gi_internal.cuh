@@ -77,6 +77,7 @@ struct gi_context_s {
   int num_sms = 148;
   // pinned host scratch for small D2H reads (counters)
   int64_t* h_scratch = nullptr;
+  int live_graphs = 0;  // graphs created on this context and not yet destroyed
 };
 
 // Pull-PageRank tiling (merge-path over CSC rows + edges).
@@ -103,7 +104,7 @@ struct gi_graph_s {
   gi::DevBuf dbuf;        // double[4]: dangling-mass ring
   gi::DevBuf split_acc;   // double[n]: partial sums of rows split across tiles
   gi::DevBuf split_cnt;   // int32[n]: arrival counters for split rows
-  gi::DevBuf push_sum;    // float[n]: push-form accumulator
+  gi::DevBuf push_sum;    // double[n]: push-form accumulator
   gi::DevBuf out_stage;   // float/int32[n]: output staging in input ids
   // BFS workspace
   gi::DevBuf parent;      // int32[n], internal ids

@@ -182,7 +182,7 @@ __global__ void __launch_bounds__(kPullThreads) k_pr_pull(PrArgs A) {
 template <typename OffT>
 __global__ void __launch_bounds__(256) k_pr_push(int64_t n, const OffT* __restrict__ off,
                                                  const int32_t* __restrict__ idx, const float* __restrict__ cin,
-                                                 float* __restrict__ acc) {
+                                                 double* __restrict__ acc) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -190,19 +190,20 @@ __global__ void __launch_bounds__(256) k_pr_push(int64_t n, const OffT* __restri
     const float c = __ldg(&cin[u]);
     if (c == 0.f) continue;
     for (int64_t j = (int64_t)off[u] + lane; j < (int64_t)off[u + 1]; j += 32)
-      atomicAdd(&acc[__ldg(&idx[j])], c);  // result unused -> RED.E.ADD.F32
+      atomicAdd(&acc[__ldg(&idx[j])], (double)c);  // result unused -> RED.E.ADD.F64 (fp64: hub rows sum
+                                                    // 1e5+ terms; fp32 atomics drift past 1e-4)
   }
 }
 
-__global__ void __launch_bounds__(256) k_pr_vertex(PrArgs A, float* __restrict__ acc) {
+__global__ void __launch_bounds__(256) k_pr_vertex(PrArgs A, double* __restrict__ acc) {
   __shared__ double sred[8];
   if (blockIdx.x == 0 && threadIdx.x == 0) A.dbuf[(A.it + 2) % 3] = 0.0;
   const double D = A.uniform ? A.dbuf[A.it % 3] : 0.0;
   const float dn = (float)(D * A.inv_n);
   double dpart = 0.0;
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < A.n; v += (int64_t)gridDim.x * blockDim.x) {
-    const float s = acc[v];
-    acc[v] = 0.f;
+    const float s = (float)acc[v];
+    acc[v] = 0.0;
     pr_epilogue(A, v, s, dn, dpart);
   }
   const double bs = block_sum(dpart, sred);
@@ -257,8 +258,8 @@ gi_status pagerank_run(gi_graph g, int32_t iters, double damping, const gi_pr_op
   if (!g->dbuf.p) GI_TRY(g->dbuf.alloc(4 * sizeof(double)));
   if (o.direction == GI_PR_PUSH) {
     if (!g->push_sum.p) {
-      GI_TRY(g->push_sum.alloc(n * sizeof(float)));
-      GI_CUDA(cudaMemsetAsync(g->push_sum.p, 0, n * sizeof(float), st));
+      GI_TRY(g->push_sum.alloc(n * sizeof(double)));
+      GI_CUDA(cudaMemsetAsync(g->push_sum.p, 0, n * sizeof(double), st));
     }
   } else if (!g->split_acc.p) {
     GI_TRY(g->split_acc.alloc(n * sizeof(double)));
@@ -303,12 +304,12 @@ gi_status pagerank_run(gi_graph g, int32_t iters, double damping, const gi_pr_op
       const int grid = grid_for(n * 32, 256, sms, 16);
       if (g->off64)
         k_pr_push<int64_t><<<grid, 256, 0, st>>>(n, g->csr_off.as<int64_t>(), g->csr_idx.as<int32_t>(), A.cin,
-                                                 g->push_sum.as<float>());
+                                                 g->push_sum.as<double>());
       else
         k_pr_push<int32_t><<<grid, 256, 0, st>>>(n, g->csr_off.as<int32_t>(), g->csr_idx.as<int32_t>(), A.cin,
-                                                 g->push_sum.as<float>());
+                                                 g->push_sum.as<double>());
       if (o.profile) GI_CUDA(cudaEventRecord(ev[1], st));
-      k_pr_vertex<<<grid_for(n, 256, sms), 256, 0, st>>>(A, g->push_sum.as<float>());
+      k_pr_vertex<<<grid_for(n, 256, sms), 256, 0, st>>>(A, g->push_sum.as<double>());
       S.aux_launches++;
     } else {
       A.tile_rows = g->tile_rows.as<int32_t>();

@@ -259,9 +259,15 @@ def gi_bfs_ex(g: int, source: int, out=None, policy: int = GI_BFS_AUTO, threshol
 # ------------------------------------------------------------------ RAII conveniences
 class Context:
     def __init__(self, device: int = 0, stream: int | None = None):
+        import weakref
+
         self.handle = gi_context_create(device, stream)
+        self._graphs = weakref.WeakSet()
 
     def close(self):
+        """Destroys the context's live graphs first (the C ABI requires it)."""
+        for g in list(getattr(self, "_graphs", ())):
+            g.close()
         if self.handle:
             gi_context_destroy(self.handle)
             self.handle = None
@@ -276,7 +282,11 @@ class Context:
 class Graph:
     def __init__(self, ctx: Context, n: int, src, dst, flags: int = GI_DEFAULT_FLAGS):
         self.ctx = ctx
+        self.handle = None
+        if not ctx.handle:
+            raise GiError(GI_ERR_INVALID_ARGUMENT, "Graph: context is closed")
         self.handle = gi_graph_create(ctx.handle, n, src, dst, flags)
+        ctx._graphs.add(self)
         self.n = gi_graph_num_vertices(self.handle)
         self.m = gi_graph_num_edges(self.handle)
 
