@@ -134,7 +134,9 @@ typedef struct {
                         (paper-literal: no D term) */
   int32_t profile;   /* 1: fill gi_pr_stats kernel timings (CUDA events on the
                         context stream around every edge-pass launch) */
-  int32_t reserved;
+  int32_t segment_size; /* GI_PR_PULL_SEGMENTED: sources per shared-memory
+                        segment; 0 = as many as fit in one CTA's shared memory
+                        (smaller values exercise many segments in tests) */
 } gi_pr_opts;
 
 typedef struct {

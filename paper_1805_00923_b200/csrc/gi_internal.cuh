@@ -105,6 +105,10 @@ struct gi_graph_s {
   gi::DevBuf split_acc;   // double[n]: partial sums of rows split across tiles
   gi::DevBuf split_cnt;   // int32[n]: arrival counters for split rows
   gi::DevBuf push_sum;    // double[n]: push-form accumulator
+  // segmented pull (pr_segmented.cu); seg_Z == 0 until built
+  int seg_Z = 0, seg_S = 0, seg_ctas = 0;
+  int64_t seg_P = 0;
+  gi::DevBuf seg_pstart, seg_idx16, seg_pc_off, seg_pc_slot, seg_tiles, seg_cta_tiles, seg_partial;
   gi::DevBuf out_stage;   // float/int32[n]: output staging in input ids
   // BFS workspace
   gi::DevBuf parent;      // int32[n], internal ids
@@ -120,6 +124,11 @@ gi_status build_graph(gi_context ctx, int64_t n, int64_t m0, const int32_t* d_sr
 // pagerank.cu
 gi_status pagerank_run(gi_graph g, int32_t iters, double damping, const gi_pr_opts& o,
                        float* d_out_input_ids, gi_pr_stats* stats);
+// pr_segmented.cu
+struct PrArgs;
+gi_status seg_build(gi_graph g, int segment_size);
+gi_status seg_edge_pass(gi_graph g, const PrArgs& A);
+gi_status seg_vertex_pass(gi_graph g, const PrArgs& A);
 // bfs.cu
 gi_status bfs_run(gi_graph g, int32_t source_input_id, const gi_bfs_opts& o,
                   int32_t* d_parent_input_ids, gi_bfs_stats* stats);

@@ -14,72 +14,25 @@
 // Push (DensePush with an all-active frontier): red.global.add.f32
 // per edge into an accumulator + a vertex kernel — the parity form.
 #include "gi_internal.cuh"
+#include "pr_common.cuh"
 
 namespace gi {
 namespace {
 
-struct PrArgs {
-  int64_t n, m;
-  const void* off;
-  const int32_t* __restrict__ idx;
-  const int32_t* __restrict__ tile_rows;
-  const float* __restrict__ cin;
-  float* __restrict__ cout;
-  const int32_t* __restrict__ outdeg;
-  double* dbuf;  // dangling-mass ring (3 slots)
-  int it;
-  float base, damp;
-  double inv_n;
-  int uniform;
-  double* split_acc;
-  int32_t* split_cnt;
-  float* rank_out;  // non-null on the final iteration (input ids)
-  const int32_t* __restrict__ perm;
-};
-
-// vertex update (a3): r' = base + d (s + D/n); contrib' = r'/outdeg; dangling partial
-__device__ __forceinline__ void pr_epilogue(const PrArgs& A, int64_t r, float s, float dn, double& dpart) {
-  float rn = A.base + A.damp * (s + dn);
-  int od = __ldg(&A.outdeg[r]);
-  A.cout[r] = od > 0 ? rn / (float)od : 0.f;
-  if (od == 0) dpart += (double)rn;
-  if (A.rank_out) A.rank_out[A.perm ? __ldg(&A.perm[r]) : r] = rn;
-}
-
-__device__ __forceinline__ double block_sum(double v, double* sred) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-  if (l == 0) sred[w] = v;
-  __syncthreads();
-  double t = 0.0;
-  if (threadIdx.x < 32) {
-    t = threadIdx.x < (blockDim.x >> 5) ? sred[threadIdx.x] : 0.0;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-  }
-  return t;  // valid in thread 0
-}
-
-// ---------------------------------------------------------------- pull (K4)
-// Tile b covers merge positions [bT, (b+1)T) of the sequence that lists, for
-// each CSC row r in order, its in-edges then an end marker; row r occupies
-// positions [r + off[r], r + off[r+1]]. Phases:
-//  A  stage this tile's row offsets in smem; gather contrib[idx[e]] for the
-//     tile's edges with coalesced index loads (the random reads of P:598-599);
-//  B  each thread walks IPT consecutive merge items, summing staged values;
-//     rows wholly inside its window are finished in registers (fused vertex
-//     update), rows crossing a thread boundary go through smem atomics;
-//  C  rows that crossed threads are finished; rows that cross tiles add a
-//     double partial + arrival count, and the last arriving tile finishes them.
+// ---------------------------------------------------------------- pull, direct gather (K4)
+// Tile b covers merge positions [bT, (b+1)T) of the CSC item sequence
+// (pr_common.cuh). Phase A stages the tile's row offsets and gathers
+// contrib[idx[e]] for its edges with coalesced index loads (the random reads
+// of P:598-599, through L1/L2); phase B is the merge-path walk with the fused
+// vertex update; rows that cross tiles add a double partial and an arrival
+// count, and the last arriving tile finishes them (pieces = tiles touched).
 template <typename OffT>
 __global__ void __launch_bounds__(kPullThreads) k_pr_pull(PrArgs A) {
   constexpr int NT = kPullThreads, IPT = kPullItemsPerThread, T = kPullTile;
   __shared__ OffT soff[T + 2];
   __shared__ float sval[T];
-  __shared__ float srow[T];
-  __shared__ uint8_t sflag[T];
-  __shared__ double sred[NT / 32];
+  __shared__ KeyVal scratch[NT / 32];
+  __shared__ double sred[32];
 
   const OffT* __restrict__ off = static_cast<const OffT*>(A.off);
   const int tid = threadIdx.x;
@@ -94,86 +47,37 @@ __global__ void __launch_bounds__(kPullThreads) k_pr_pull(PrArgs A) {
   const float dn = (float)(D * A.inv_n);
 
   for (int i = tid; i <= R; i += NT) soff[i] = off[r0 + i];
-  for (int i = tid; i < R; i += NT) {
-    srow[i] = 0.f;
-    sflag[i] = 0;
-  }
   const int64_t eb = p0 - r0;
   const int64_t ee = min((int64_t)off[r1 + 1], p1 - r1);
-  // phase A: coalesced index stream + random gather (IPT loads in flight per thread)
   {
     const int64_t ne = ee - eb;
 #pragma unroll
     for (int k = 0; k < IPT; ++k) {
-      int64_t j = tid + (int64_t)k * NT;
+      const int64_t j = tid + (int64_t)k * NT;
       if (j < ne) sval[j] = __ldg(&A.cin[__ldg(&A.idx[eb + j])]);
     }
   }
   __syncthreads();
 
   double dpart = 0.0;
-  // phase B: per-thread merge-path walk
-  const int64_t d0 = p0 + (int64_t)tid * IPT;
-  if (d0 < p1) {
-    const int64_t d1 = min(d0 + (int64_t)IPT, p1);
-    // row containing d0: min i in [0, R) with r0 + i + soff[i+1] >= d0
-    int lo = 0, hi = R - 1;
-    while (lo < hi) {
-      int mid = (lo + hi) >> 1;
-      if (r0 + mid + (int64_t)soff[mid + 1] >= d0) hi = mid;
-      else lo = mid + 1;
-    }
-    int i = lo;
-    int64_t e = d0 - (r0 + i);
-    bool own = (r0 + i + (int64_t)soff[i]) >= d0;  // row starts inside this window
-    float acc = 0.f;
-    int64_t rowend = r0 + i + (int64_t)soff[i + 1];
-    for (int64_t p = d0; p < d1; ++p) {
-      if (p < rowend) {
-        acc += sval[e - eb];
-        ++e;
-      } else {
-        if (own) {
-          pr_epilogue(A, r0 + i, acc, dn, dpart);
-        } else {
-          atomicAdd(&srow[i], acc);
-          sflag[i] = 1;
-        }
-        acc = 0.f;
-        ++i;
-        own = true;
-        if (i < R) rowend = r0 + i + (int64_t)soff[i + 1];
-      }
-    }
-    // window ended inside row i: hand the partial to phase C
-    if (i < R && (r0 + i + (int64_t)soff[i]) < d1) {
-      atomicAdd(&srow[i], acc);
-      sflag[i] = 1;
-    }
-  }
-  __syncthreads();
-
-  // phase C: rows that crossed threads or tiles
-  for (int i = tid; i < R; i += NT) {
-    if (!sflag[i]) continue;
-    const int64_t r = r0 + i;
-    const int64_t sp = r + (int64_t)soff[i], ep = r + (int64_t)soff[i + 1];
-    if (sp >= p0 && ep < p1) {
-      pr_epilogue(A, r, srow[i], dn, dpart);
-    } else {
-      const int pieces = (int)(ep / T - sp / T + 1);
-      atomicAdd(&A.split_acc[r], (double)srow[i]);
-      __threadfence();
-      const int prev = atomicAdd(&A.split_cnt[r], 1);
-      if (prev == pieces - 1) {
+  merge_tile_reduce<NT, IPT>(
+      soff, r0, R, p0, p1, eb, sval, scratch,
+      [&](int i, float v) { pr_epilogue(A, r0 + i, v, dn, dpart); },
+      [&](int i, float v) {
+        const int64_t r = r0 + i;
+        const int64_t sp = r + (int64_t)soff[i], ep = r + (int64_t)soff[i + 1];
+        const int pieces = (int)(ep / T - sp / T + 1);
+        atomicAdd(&A.split_acc[r], (double)v);
         __threadfence();
-        const double tot = atomicAdd(&A.split_acc[r], 0.0);
-        pr_epilogue(A, r, (float)tot, dn, dpart);
-        A.split_acc[r] = 0.0;
-        A.split_cnt[r] = 0;
-      }
-    }
-  }
+        const int prev = atomicAdd(&A.split_cnt[r], 1);
+        if (prev == pieces - 1) {
+          __threadfence();
+          const double tot = atomicAdd(&A.split_acc[r], 0.0);
+          pr_epilogue(A, r, (float)tot, dn, dpart);
+          A.split_acc[r] = 0.0;
+          A.split_cnt[r] = 0;
+        }
+      });
   const double bs = block_sum(dpart, sred);
   if (tid == 0 && bs != 0.0) atomicAdd(&A.dbuf[(A.it + 1) % 3], bs);
 }
@@ -238,7 +142,13 @@ gi_status pagerank_run(gi_graph g, int32_t iters, double damping, const gi_pr_op
   const int sms = ctx->num_sms;
   const int64_t n = g->n, m = g->m;
   gi_pr_stats S{};
-  S.kernel = o.direction == GI_PR_PUSH ? GI_PR_PUSH : GI_PR_PULL_DIRECT;
+  int kernel = o.direction;
+  if (kernel == GI_PR_PULL) kernel = (n > 0 && m > 0 && seg_build(g, o.segment_size) == GI_OK) ? GI_PR_PULL_SEGMENTED : GI_PR_PULL_DIRECT;
+  else if (kernel == GI_PR_PULL_SEGMENTED) {
+    if (n > 0 && m > 0) GI_TRY(seg_build(g, o.segment_size));
+    else kernel = GI_PR_PULL_DIRECT;
+  }
+  S.kernel = kernel;
   const int osz = g->off64 ? 8 : 4;
   S.bytes_alg_per_iter = 4 * m + (int64_t)(osz + 12) * n;
   if (n == 0) {
@@ -256,7 +166,7 @@ gi_status pagerank_run(gi_graph g, int32_t iters, double damping, const gi_pr_op
   for (int k = 0; k < 2; ++k)
     if (!g->contrib[k].p) GI_TRY(g->contrib[k].alloc(n * sizeof(float)));
   if (!g->dbuf.p) GI_TRY(g->dbuf.alloc(4 * sizeof(double)));
-  if (o.direction == GI_PR_PUSH) {
+  if (kernel == GI_PR_PUSH) {
     if (!g->push_sum.p) {
       GI_TRY(g->push_sum.alloc(n * sizeof(double)));
       GI_CUDA(cudaMemsetAsync(g->push_sum.p, 0, n * sizeof(double), st));
@@ -300,7 +210,7 @@ gi_status pagerank_run(gi_graph g, int32_t iters, double damping, const gi_pr_op
     A.cout = g->contrib[(it + 1) & 1].as<float>();
     A.rank_out = (it == iters - 1) ? d_out : nullptr;
     if (o.profile) GI_CUDA(cudaEventRecord(ev[0], st));
-    if (o.direction == GI_PR_PUSH) {
+    if (kernel == GI_PR_PUSH) {
       const int grid = grid_for(n * 32, 256, sms, 16);
       if (g->off64)
         k_pr_push<int64_t><<<grid, 256, 0, st>>>(n, g->csr_off.as<int64_t>(), g->csr_idx.as<int32_t>(), A.cin,
@@ -311,6 +221,11 @@ gi_status pagerank_run(gi_graph g, int32_t iters, double damping, const gi_pr_op
       if (o.profile) GI_CUDA(cudaEventRecord(ev[1], st));
       k_pr_vertex<<<grid_for(n, 256, sms), 256, 0, st>>>(A, g->push_sum.as<double>());
       S.aux_launches++;
+    } else if (kernel == GI_PR_PULL_SEGMENTED) {
+      GI_TRY(seg_edge_pass(g, A));
+      GI_TRY(seg_vertex_pass(g, A));
+      S.aux_launches++;
+      if (o.profile) GI_CUDA(cudaEventRecord(ev[1], st));
     } else {
       A.tile_rows = g->tile_rows.as<int32_t>();
       A.idx = g->csc_idx.as<int32_t>();

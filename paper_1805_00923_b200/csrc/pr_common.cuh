@@ -1,0 +1,169 @@
+// pr_common.cuh — device pieces shared by the pull-PageRank kernels.
+//
+// Merge-path tile reduction (the paper's edge-aware
+// vertex chunking, at thread granularity): a CSR-like
+// sequence of rows r (CSC rows, or (segment, row) pieces) is laid out as
+// items — each row's edges followed by one end marker — so row r occupies
+// merge positions [r + off[r], r + off[r+1]]. A tile is a fixed range of
+// positions [p0, p1); each thread walks IPT consecutive positions. Rows that
+// cross thread boundaries are joined with a block-wide segmented scan of the
+// threads' carry-outs (no atomics); rows that cross the tile boundary are
+// reported to the caller once per tile (`split`).
+#pragma once
+#include "gi_internal.cuh"
+
+namespace gi {
+
+struct PrArgs {
+  int64_t n, m;
+  const void* off;
+  const int32_t* __restrict__ idx;
+  const int32_t* __restrict__ tile_rows;
+  const float* __restrict__ cin;
+  float* __restrict__ cout;
+  const int32_t* __restrict__ outdeg;
+  double* dbuf;  // dangling-mass ring (3 slots)
+  int it;
+  float base, damp;
+  double inv_n;
+  int uniform;
+  double* split_acc;
+  int32_t* split_cnt;
+  float* rank_out;  // non-null on the final iteration (input ids)
+  const int32_t* __restrict__ perm;
+};
+
+// vertex update (a3): r' = base + d (s + D/n); contrib' = r'/outdeg; dangling partial
+__device__ __forceinline__ void pr_epilogue(const PrArgs& A, int64_t r, float s, float dn, double& dpart) {
+  const float rn = A.base + A.damp * (s + dn);
+  const int od = __ldg(&A.outdeg[r]);
+  A.cout[r] = od > 0 ? rn / (float)od : 0.f;
+  if (od == 0) dpart += (double)rn;
+  if (A.rank_out) A.rank_out[A.perm ? __ldg(&A.perm[r]) : r] = rn;
+}
+
+// Block sum of a double; result valid in thread 0. sred: >= 32 doubles.
+__device__ __forceinline__ double block_sum(double v, double* sred) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) sred[w] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (threadIdx.x < 32) {
+    t = threadIdx.x < (blockDim.x >> 5) ? sred[threadIdx.x] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  }
+  return t;
+}
+
+struct KeyVal {
+  int key;
+  float val;
+};
+
+// combine(a, b) for b following a in thread order: same key -> sum, else b.
+__device__ __forceinline__ KeyVal kv_combine(KeyVal a, KeyVal b) {
+  return KeyVal{b.key, b.key == a.key ? a.val + b.val : b.val};
+}
+
+// Block-wide segmented scan over (key, val) in thread order; keys are
+// non-decreasing across threads. Returns the exclusive prefix (the running
+// sum of the run of equal keys ending at thread t-1; key -1 for thread 0) and
+// writes the inclusive value. scratch: NT/32 KeyVal in smem.
+template <int NT>
+__device__ __forceinline__ KeyVal seg_scan(KeyVal x, KeyVal& incl, KeyVal* scratch) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  KeyVal run = x;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    KeyVal up;
+    up.key = __shfl_up_sync(0xffffffffu, run.key, o);
+    up.val = __shfl_up_sync(0xffffffffu, run.val, o);
+    if (lane >= o) run = kv_combine(up, run);
+  }
+  if (lane == 31) scratch[w] = run;
+  __syncthreads();
+  if (w == 0) {
+    KeyVal t = lane < NT / 32 ? scratch[lane] : KeyVal{0x7fffffff, 0.f};
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      KeyVal up;
+      up.key = __shfl_up_sync(0xffffffffu, t.key, o);
+      up.val = __shfl_up_sync(0xffffffffu, t.val, o);
+      if (lane >= o) t = kv_combine(up, t);
+    }
+    if (lane < NT / 32) scratch[lane] = t;  // inclusive prefix over warps
+  }
+  __syncthreads();
+  KeyVal wpre = w > 0 ? scratch[w - 1] : KeyVal{-1, 0.f};
+  incl = kv_combine(wpre, run);
+  KeyVal ex;
+  ex.key = __shfl_up_sync(0xffffffffu, run.key, 1);
+  ex.val = __shfl_up_sync(0xffffffffu, run.val, 1);
+  if (lane == 0) ex = wpre;
+  else ex = kv_combine(wpre, ex);
+  return ex;
+}
+
+// One tile of the merge-path reduction.
+//   soff[i] = off[r0 + i] for i in [0, R]  (smem; OffT)
+//   sval[e - eb] = value of edge e for edges of the tile (smem)
+//   complete(i, v): row r0+i starts and ends inside the tile; v its sum
+//   split(i, v):    row r0+i crosses the tile boundary; v is this tile's part
+//                   (called exactly once per such row per tile)
+// Must be called by all NT threads (contains __syncthreads).
+template <int NT, int IPT, typename OffT, typename Complete, typename Split>
+__device__ __forceinline__ void merge_tile_reduce(const OffT* soff, int64_t r0, int R, int64_t p0, int64_t p1,
+                                                  int64_t eb, const float* sval, KeyVal* scratch,
+                                                  Complete&& complete, Split&& split) {
+  const int tid = threadIdx.x;
+  const int64_t d0 = p0 + (int64_t)tid * IPT;
+  const int64_t d1 = min(d0 + (int64_t)IPT, p1);
+  const bool active = d0 < p1;
+  int i = R;  // current row (index relative to r0)
+  float acc = 0.f, head_val = 0.f;
+  int head = -1;  // head row completed in this window but started before d0
+  if (active) {
+    int lo = 0, hi = R - 1;  // row containing d0: min i with r0 + i + soff[i+1] >= d0
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (r0 + mid + (int64_t)soff[mid + 1] >= d0) hi = mid;
+      else lo = mid + 1;
+    }
+    i = lo;
+    int64_t e = d0 - (r0 + i);
+    bool own = (r0 + i + (int64_t)soff[i]) >= d0;
+    int64_t rowend = r0 + i + (int64_t)soff[i + 1];
+    for (int64_t p = d0; p < d1; ++p) {
+      if (p < rowend) {
+        acc += sval[e - eb];
+        ++e;
+      } else {
+        if (own) complete(i, acc);
+        else {
+          head = i;
+          head_val = acc;
+        }
+        acc = 0.f;
+        ++i;
+        own = true;
+        if (i < R) rowend = r0 + i + (int64_t)soff[i + 1];
+      }
+    }
+  }
+  // carry-out: (row open at d1, its partial inside [d0, d1))
+  KeyVal incl;
+  const KeyVal ex = seg_scan<NT>(KeyVal{active ? i : 0x7fffffff, active ? acc : 0.f}, incl, scratch);
+  if (head >= 0) {
+    const float tot = head_val + (ex.key == head ? ex.val : 0.f);
+    if (r0 + head + (int64_t)soff[head] >= p0) complete(head, tot);
+    else split(head, tot);
+  }
+  // the last active thread reports the row still open at p1, if the tile holds part of it
+  if (active && d1 == p1 && i < R && (r0 + i + (int64_t)soff[i]) < p1) split(i, incl.val);
+}
+
+}  // namespace gi

@@ -45,7 +45,7 @@ GI_BFS_AUTO, GI_BFS_PUSH_ONLY, GI_BFS_PULL_ONLY = 0, 1, 2
 
 class gi_pr_opts(ctypes.Structure):
     _fields_ = [("direction", ctypes.c_int32), ("dangling", ctypes.c_int32), ("profile", ctypes.c_int32),
-                ("reserved", ctypes.c_int32)]
+                ("segment_size", ctypes.c_int32)]
 
 
 class gi_pr_stats(ctypes.Structure):
@@ -224,12 +224,12 @@ def gi_pagerank(g: int, iters: int, damping: float, out=None):
 
 
 def gi_pagerank_ex(g: int, iters: int, damping: float, out=None, direction: int = GI_PR_PULL,
-                   dangling: int = GI_DANGLING_UNIFORM, profile: bool = False):
+                   dangling: int = GI_DANGLING_UNIFORM, profile: bool = False, segment_size: int = 0):
     n = gi_graph_num_vertices(g)
     if out is None:
         out = np.empty(n, np.float32)
     p, keep = _ptr(out, np.float32)
-    o = gi_pr_opts(direction, dangling, int(profile), 0)
+    o = gi_pr_opts(direction, dangling, int(profile), segment_size)
     s = gi_pr_stats()
     _check(_lib.gi_pagerank_ex(g, iters, damping, ctypes.byref(o), p or None, ctypes.byref(s)), "gi_pagerank_ex")
     return keep, s

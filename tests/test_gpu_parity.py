@@ -132,11 +132,12 @@ def test_build_device_edges_and_errors(gi, ctx):
 
 
 # ---------------------------------------------------------------- PageRank (a3-a5)
-PR_DIRS = ["pull", "push"]
+PR_DIRS = ["pull", "push", "direct", "segmented"]
 
 
 def _dir(gi, name):
-    return {"pull": gi.GI_PR_PULL, "push": gi.GI_PR_PUSH, "direct": gi.GI_PR_PULL_DIRECT}[name]
+    return {"pull": gi.GI_PR_PULL, "push": gi.GI_PR_PUSH, "direct": gi.GI_PR_PULL_DIRECT,
+            "segmented": gi.GI_PR_PULL_SEGMENTED}[name]
 
 
 @pytest.mark.parametrize("direction", PR_DIRS)
@@ -211,6 +212,22 @@ def test_pr_config1(gi, ctx, direction, relabel):
     want = oracle.pagerank(go, cfg.pr_iters, cfg.damping)
     _pr_check(got, want, "config1")
     assert st.edge_launches == cfg.pr_iters
+
+
+@pytest.mark.parametrize("seg", [32, 1000, 4096, 20000])
+def test_pr_segmented_many_segments(gi, ctx, seg):
+    """Small segment sizes: many segments, pieces split across tiles and CTAs, carries."""
+    cases = [(graphgen.CONFIGS[1].n, *graphgen.CONFIGS[1].edges()),
+             (70001, *graphgen.random_digraph(70001, 1000003, 5)),
+             (100001, *graphgen.in_star(100000)),
+             (100001, *graphgen.star_bidirectional(100000))]
+    for n, s, d in cases:
+        g = gi.Graph(ctx, n, s, d)
+        go = oracle.build_graph(n, s, d)
+        for dangling in (0, 1):
+            got, st = g.pagerank(20, 0.85, direction=gi.GI_PR_PULL_SEGMENTED, dangling=dangling, segment_size=seg)
+            assert st.kernel == gi.GI_PR_PULL_SEGMENTED
+            _pr_check(got, oracle.pagerank(go, 20, 0.85, dangling), f"seg={seg} n={n}")
 
 
 def test_pr_device_output_and_damping_edges(gi, ctx):
