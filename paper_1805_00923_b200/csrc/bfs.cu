@@ -20,7 +20,7 @@
 //  conversion: queue -> bitmap (atomicOr per id);
 //    bitmap -> queue (popc + warp scan + one atomicAdd per warp).
 #include <algorithm>
-#include <cub/block/block_scan.cuh>
+#include <cub/cub.cuh>
 
 #include "gi_internal.cuh"
 
@@ -28,6 +28,7 @@ namespace gi {
 namespace {
 
 constexpr int kRing = 4;  // counter slots ring: slot(l) = cnt + 2*(l % kRing): {|F_l|, sum outdeg F_l}
+constexpr int64_t kBalancedMin = 1 << 15;  // push levels with more frontier edges use k_bfs_push_bal
 
 __global__ void k_bfs_init(int32_t s_in, const int32_t* __restrict__ inv, const int32_t* __restrict__ outdeg,
                            int32_t* __restrict__ parent, int32_t* __restrict__ q, int64_t* __restrict__ cnt) {
@@ -141,6 +142,64 @@ __global__ void __launch_bounds__(256) k_bfs_pull(const uint32_t* __restrict__ f
   }
 }
 
+// Edge-balanced push level (the paper's edge-parallel strategy):
+// pre = exclusive scan of the frontier's out-degrees, E = their sum. Thread
+// g owns flattened edges [g*EPT, (g+1)*EPT): one binary search for its first
+// owner, then a forward walk, so a hub's edges spread over the whole grid.
+struct FrontierDegree {
+  const int32_t* __restrict__ outdeg;
+  const int32_t* __restrict__ q;
+  __host__ __device__ long long operator()(const int64_t& i) const { return (long long)outdeg[q[i]]; }
+};
+
+template <typename OffT, int EPT>
+__global__ void __launch_bounds__(256) k_bfs_push_bal(const int32_t* __restrict__ q, int64_t nf,
+                                                      const long long* __restrict__ pre, long long E,
+                                                      const OffT* __restrict__ off, const int32_t* __restrict__ idx,
+                                                      const int32_t* __restrict__ outdeg, int32_t* parent,
+                                                      int32_t* __restrict__ qnext, int64_t* __restrict__ cnext) {
+  const int lane = threadIdx.x & 31;
+  const long long stride = (long long)gridDim.x * blockDim.x * EPT;
+  for (long long f0 = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * EPT; f0 - (long long)lane * EPT < E;
+       f0 += stride) {
+    int64_t o = 0;
+    if (f0 < E) {  // owner of f0: last i with pre[i] <= f0
+      int64_t lo = 0, hi = nf - 1;
+      while (lo < hi) {
+        const int64_t mid = (lo + hi + 1) >> 1;
+        if (__ldg(&pre[mid]) <= f0) lo = mid;
+        else hi = mid - 1;
+      }
+      o = lo;
+    }
+#pragma unroll
+    for (int k = 0; k < EPT; ++k) {
+      const long long f = f0 + k;
+      bool won = false;
+      int32_t v = 0;
+      if (f < E) {
+        while (o + 1 < nf && __ldg(&pre[o + 1]) <= f) ++o;
+        const int32_t u = __ldg(&q[o]);
+        v = __ldg(&idx[(long long)off[u] + (f - __ldg(&pre[o]))]);
+        if (*(volatile int32_t*)&parent[v] == -1) won = atomicCAS(&parent[v], -1, u) == -1;
+      }
+      const unsigned mask = __ballot_sync(0xffffffffu, won);
+      if (mask) {
+        long long od = won ? (long long)__ldg(&outdeg[v]) : 0;
+#pragma unroll
+        for (int s = 16; s > 0; s >>= 1) od += __shfl_xor_sync(0xffffffffu, od, s);
+        long long pos = 0;
+        if (lane == 0) {
+          pos = atomicAdd((unsigned long long*)&cnext[0], (unsigned long long)__popc(mask));
+          atomicAdd((unsigned long long*)&cnext[1], (unsigned long long)od);
+        }
+        pos = __shfl_sync(0xffffffffu, pos, 0);
+        if (won) qnext[pos + __popc(mask & ((1u << lane) - 1))] = v;
+      }
+    }
+  }
+}
+
 __global__ void k_q2b(const int32_t* __restrict__ q, int64_t qlen, uint32_t* __restrict__ bm) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < qlen; i += (int64_t)gridDim.x * blockDim.x) {
     const int32_t u = q[i];
@@ -215,6 +274,12 @@ static gi_status bfs_impl(gi_graph g, int32_t source, const gi_bfs_opts& o, int3
       GI_TRY(g->bitmap[k].alloc(words * sizeof(uint32_t)));
     }
     GI_TRY(g->counters.alloc((2 * kRing + 4) * sizeof(int64_t)));
+    GI_TRY(g->bfs_pre.alloc((n + 1) * sizeof(long long)));
+    size_t tb = 0;
+    cub::TransformInputIterator<long long, FrontierDegree, cub::CountingInputIterator<int64_t>> it(
+        cub::CountingInputIterator<int64_t>(0), FrontierDegree{g->outdeg.as<int32_t>(), g->queue[0].as<int32_t>()});
+    GI_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, it, g->bfs_pre.as<long long>(), n, st));
+    GI_TRY(g->bfs_scan_tmp.alloc(tb));
   }
   int64_t* cnt = g->counters.as<int64_t>();
   unsigned long long* aux = reinterpret_cast<unsigned long long*>(cnt + 2 * kRing);  // [0]=tail [1..2]=finish
@@ -269,9 +334,22 @@ static gi_status bfs_impl(gi_graph g, int32_t source, const gi_bfs_opts& o, int3
                                                          g->queue[qc].as<int32_t>(), aux);
         S.launches++;
       }
-      const int grid = (int)std::min<int64_t>(ceil_div(nf, 256), (int64_t)sms * 8);
-      k_bfs_push<OffT><<<grid, 256, 0, st>>>(g->queue[qc].as<int32_t>(), nf, csr_off, g->csr_idx.as<int32_t>(), outdeg,
-                                             parent, g->queue[qc ^ 1].as<int32_t>(), nxt);
+      if (sdeg >= kBalancedMin) {  // edge-balanced: a hub's edges spread over the grid
+        cub::TransformInputIterator<long long, FrontierDegree, cub::CountingInputIterator<int64_t>> it(
+            cub::CountingInputIterator<int64_t>(0), FrontierDegree{outdeg, g->queue[qc].as<int32_t>()});
+        size_t tb = g->bfs_scan_tmp.bytes;
+        GI_CUDA(cub::DeviceScan::ExclusiveSum(g->bfs_scan_tmp.p, tb, it, g->bfs_pre.as<long long>(), nf, st));
+        constexpr int EPT = 8;
+        const int grid = (int)std::min<int64_t>(ceil_div(sdeg, 256 * EPT), (int64_t)sms * 8);
+        k_bfs_push_bal<OffT, EPT><<<grid, 256, 0, st>>>(g->queue[qc].as<int32_t>(), nf, g->bfs_pre.as<long long>(),
+                                                        sdeg, csr_off, g->csr_idx.as<int32_t>(), outdeg, parent,
+                                                        g->queue[qc ^ 1].as<int32_t>(), nxt);
+        S.launches++;
+      } else {
+        const int grid = (int)std::min<int64_t>(ceil_div(nf, 256), (int64_t)sms * 8);
+        k_bfs_push<OffT><<<grid, 256, 0, st>>>(g->queue[qc].as<int32_t>(), nf, csr_off, g->csr_idx.as<int32_t>(),
+                                               outdeg, parent, g->queue[qc ^ 1].as<int32_t>(), nxt);
+      }
       qc ^= 1;
       in_bitmap = false;
     }

@@ -115,6 +115,8 @@ struct gi_graph_s {
   gi::DevBuf queue[2];    // int32[n]
   gi::DevBuf bitmap[2];   // uint32[ceil(n/32)]
   gi::DevBuf counters;    // int64 slots, see bfs.cu
+  gi::DevBuf bfs_pre;     // int64[n+1]: scan of frontier degrees (balanced push)
+  gi::DevBuf bfs_scan_tmp;
 };
 
 namespace gi {

@@ -164,7 +164,7 @@ gi_status pagerank_run(gi_graph g, int32_t iters, double damping, const gi_pr_op
   }
   // workspace (lazily allocated, reused across calls)
   for (int k = 0; k < 2; ++k)
-    if (!g->contrib[k].p) GI_TRY(g->contrib[k].alloc(n * sizeof(float)));
+    if (!g->contrib[k].p) GI_TRY(g->contrib[k].alloc((n + 16) * sizeof(float)));
   if (!g->dbuf.p) GI_TRY(g->dbuf.alloc(4 * sizeof(double)));
   if (kernel == GI_PR_PUSH) {
     if (!g->push_sum.p) {

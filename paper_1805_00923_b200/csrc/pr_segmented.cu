@@ -48,9 +48,10 @@ template <typename OffT>
 __host__ __device__ constexpr int seg_soff_bytes() {
   return (int)(((kSegTile + 2) * sizeof(OffT) + 15) / 16 * 16);
 }
+// dynamic smem besides the contrib segment: soff | sval | spart
 template <typename OffT>
 constexpr int seg_fixed_dyn_bytes() {
-  return seg_soff_bytes<OffT>() + kSegTile * (int)sizeof(float);
+  return seg_soff_bytes<OffT>() + 2 * kSegTile * (int)sizeof(float);
 }
 
 template <typename OffT>
@@ -60,67 +61,158 @@ struct SegArgs {
   const OffT* __restrict__ pc_off;
   const int32_t* __restrict__ pc_slot;
   const uint16_t* __restrict__ idx16;
-  const float* __restrict__ cin;
+  const float* __restrict__ cin;  // padded to a multiple of 4 floats
   float* __restrict__ partial;
-  int64_t n;
+  int64_t n, m;
   int Z;
 };
 
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+// 1-D TMA bulk copy global -> shared, completion counted on `bar` (UBLKCP in SASS)
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// Persistent: CTA c processes tiles [cta_tiles[c], cta_tiles[c+1]) in order.
+// Software pipeline per tile t:
+//   regs(t) -> smem offsets | sync | issue loads of tile t+1 into regs |
+//   gather sval from the staged segment | sync | TMA next segment if it
+//   changes (overlaps the walk) | merge-path walk -> spart | sync | write
+//   the tile's completed piece partials (coalesced slot list in regs).
 template <typename OffT>
 __global__ void __launch_bounds__(kSegThreads, 1) k_pr_seg(SegArgs<OffT> A) {
   constexpr int NT = kSegThreads, IPT = kSegIPT, TT = kSegTile;
-  extern __shared__ __align__(16) unsigned char dyn_smem[];
-  OffT* soff = reinterpret_cast<OffT*>(dyn_smem);                          // TT + 2
-  float* sval = reinterpret_cast<float*>(dyn_smem + seg_soff_bytes<OffT>());  // TT
-  float* scontrib = sval + TT;                                             // Z
+  constexpr int OPT = (TT + 2 + NT - 1) / NT;
+  extern __shared__ __align__(128) unsigned char dyn_smem[];
+  OffT* soff = reinterpret_cast<OffT*>(dyn_smem);
+  float* sval = reinterpret_cast<float*>(dyn_smem + seg_soff_bytes<OffT>());
+  float* spart = sval + TT;
+  float* scontrib = spart + TT;
   __shared__ KeyVal scratch[NT / 32];
   __shared__ float s_carry;
+  __shared__ __align__(8) uint64_t s_bar;
   const int tid = threadIdx.x;
   const int t0 = A.cta_tiles[blockIdx.x], t1 = A.cta_tiles[blockIdx.x + 1];
-  int cur_seg = -1;
+  if (t0 >= t1) return;
+  if (tid == 0) mbar_init(&s_bar, 1);
+  __syncthreads();
+
+  auto load_segment = [&](int seg) {  // thread 0
+    const int64_t base = (int64_t)seg * A.Z;
+    const int64_t zlen = min((int64_t)A.Z, A.n - base);
+    tma_load_1d(scontrib, A.cin + base, (uint32_t)(((zlen * 4) + 15) & ~15ll), &s_bar);
+  };
+  uint16_t pidx[IPT];
+  OffT poff[OPT];
+  int32_t pslot[IPT];
+  auto prefetch = [&](const SegTile& T, int64_t p1) {
+    const int64_t r0 = T.r0;
+    const int R = T.r1 - T.r0 + 1;
+    const int64_t eb = T.pos - r0;
+    const int64_t items = p1 - T.pos;
+#pragma unroll
+    for (int k = 0; k < OPT; ++k) {
+      const int i = tid + k * NT;
+      poff[k] = i <= R ? __ldg(&A.pc_off[r0 + i]) : (OffT)0;
+    }
+#pragma unroll
+    for (int k = 0; k < IPT; ++k) {
+      const int64_t j = tid + (int64_t)k * NT;
+      pidx[k] = (j < items && eb + j < A.m) ? __ldg(&A.idx16[eb + j]) : (uint16_t)0;
+      pslot[k] = (j < R) ? __ldg(&A.pc_slot[r0 + j]) : 0;
+    }
+  };
+
+  SegTile Tn = A.tiles[t0];
+  int64_t pn1 = A.tiles[t0 + 1].pos;
+  int cur_seg = Tn.seg;
+  if (tid == 0) load_segment(cur_seg);
+  bool seg_pending = true;
+  uint32_t parity = 0;
+  prefetch(Tn, pn1);
+
   for (int t = t0; t < t1; ++t) {
-    const SegTile T = A.tiles[t];
-    const int64_t p0 = T.pos, p1 = A.tiles[t + 1].pos;
-    const int64_t r0 = T.r0, r1 = T.r1;
-    const int R = (int)(r1 - r0 + 1);
-    __syncthreads();  // previous tile is done with smem
-    if (T.seg != cur_seg) {
-      cur_seg = T.seg;
-      const int64_t base = (int64_t)cur_seg * A.Z;
-      const int zlen = (int)min((int64_t)A.Z, A.n - base);
-      const float* src = A.cin + base;
-      for (int j = tid; j < zlen; j += NT) scontrib[j] = __ldg(&src[j]);
+    const SegTile T = Tn;
+    const int64_t p0 = T.pos, p1 = pn1;
+    const int64_t r0 = T.r0;
+    const int R = T.r1 - T.r0 + 1;
+    if (t + 1 < t1) {
+      Tn = A.tiles[t + 1];
+      pn1 = A.tiles[t + 2].pos;
     }
-    for (int i = tid; i <= R; i += NT) soff[i] = __ldg(&A.pc_off[r0 + i]);
-    const int64_t eb = p0 - r0;
-    const int64_t ee = min((int64_t)__ldg(&A.pc_off[r1 + 1]), p1 - r1);
+    uint16_t cidx[IPT];
+    int32_t cslot[IPT];
+#pragma unroll
+    for (int k = 0; k < IPT; ++k) {
+      cidx[k] = pidx[k];
+      cslot[k] = pslot[k];
+    }
+    __syncthreads();  // previous tile's write-out finished reading soff
+#pragma unroll
+    for (int k = 0; k < OPT; ++k) {
+      const int i = tid + k * NT;
+      if (i <= R) soff[i] = poff[k];
+    }
     const float carry_in = s_carry;
-    __syncthreads();
-    {
-      const int64_t ne = ee - eb;
-      uint16_t ix[IPT];
-#pragma unroll
-      for (int k = 0; k < IPT; ++k) {
-        const int64_t j = tid + (int64_t)k * NT;
-        ix[k] = j < ne ? __ldg(&A.idx16[eb + j]) : (uint16_t)0;
-      }
-#pragma unroll
-      for (int k = 0; k < IPT; ++k) {
-        const int64_t j = tid + (int64_t)k * NT;
-        if (j < ne) sval[j] = scontrib[ix[k]];
-      }
+    __syncthreads();  // soff visible
+    const int64_t eb = p0 - r0;
+    const int64_t ee = min((int64_t)soff[R], p1 - (r0 + R - 1));
+    const int ne = (int)(ee - eb);
+    if (t + 1 < t1) prefetch(Tn, pn1);  // in flight during this tile
+    if (seg_pending) {
+      mbar_wait(&s_bar, parity);
+      parity ^= 1u;
+      seg_pending = false;
     }
-    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < IPT; ++k) {
+      const int j = tid + k * NT;
+      if (j < ne) sval[j] = scontrib[cidx[k]];
+    }
+    __syncthreads();  // sval ready; every read of scontrib for this tile is done
+    if (t + 1 < t1 && Tn.seg != cur_seg) {
+      cur_seg = Tn.seg;
+      if (tid == 0) load_segment(cur_seg);  // overlaps the walk below
+      seg_pending = true;
+    }
     merge_tile_reduce<NT, IPT>(
-        soff, r0, R, p0, p1, eb, sval, scratch,
-        [&](int i, float v) { A.partial[__ldg(&A.pc_slot[r0 + i])] = v; },
+        soff, r0, R, p0, p1, eb, sval, scratch, [&](int i, float v) { spart[i] = v; },
         [&](int i, float v) {
           const int64_t r = r0 + i;
           const int64_t sp = r + (int64_t)soff[i], ep = r + (int64_t)soff[i + 1];
           const float tot = v + (sp < p0 ? carry_in : 0.f);
-          if (ep < p1) A.partial[__ldg(&A.pc_slot[r])] = tot;
+          if (ep < p1) spart[i] = tot;
           else s_carry = tot;  // piece continues in this CTA's next tile
         });
+    __syncthreads();  // spart ready
+#pragma unroll
+    for (int k = 0; k < IPT; ++k) {
+      const int i = tid + k * NT;
+      if (i < R && r0 + i + (int64_t)soff[i + 1] < p1) A.partial[cslot[k]] = spart[i];
+    }
   }
 }
 
@@ -389,6 +481,7 @@ static gi_status seg_iter_t(gi_graph g, const PrArgs& A) {
   S.cin = A.cin;
   S.partial = g->seg_partial.as<float>();
   S.n = g->n;
+  S.m = g->m;
   S.Z = g->seg_Z;
   const size_t dyn = (size_t)g->seg_Z * sizeof(float) + seg_fixed_dyn_bytes<OffT>();
   static size_t attr_set[2] = {0, 0};  // largest dynamic smem size configured so far
