@@ -29,7 +29,7 @@ namespace {
 template <typename OffT>
 __global__ void __launch_bounds__(kPullThreads) k_pr_pull(PrArgs A) {
   constexpr int NT = kPullThreads, IPT = kPullItemsPerThread, T = kPullTile;
-  __shared__ OffT soff[T + 2];
+  __shared__ int loff[T + 2];
   __shared__ float sval[T];
   __shared__ KeyVal scratch[NT / 32];
   __shared__ double sred[32];
@@ -41,31 +41,32 @@ __global__ void __launch_bounds__(kPullThreads) k_pr_pull(PrArgs A) {
   const int64_t p1 = min(p0 + (int64_t)T, A.n + A.m);
   const int64_t r0 = A.tile_rows[2 * b], r1 = A.tile_rows[2 * b + 1];
   const int R = (int)(r1 - r0 + 1);
+  const int items = (int)(p1 - p0);
+  const int64_t eb = p0 - r0;  // the tile's first edge
 
   if (b == 0 && tid == 0) A.dbuf[(A.it + 2) % 3] = 0.0;
   const double D = A.uniform ? A.dbuf[A.it % 3] : 0.0;
   const float dn = (float)(D * A.inv_n);
 
-  for (int i = tid; i <= R; i += NT) soff[i] = off[r0 + i];
-  const int64_t eb = p0 - r0;
-  const int64_t ee = min((int64_t)off[r1 + 1], p1 - r1);
-  {
-    const int64_t ne = ee - eb;
+  for (int i = tid; i <= R; i += NT) {
+    const int64_t v = (int64_t)off[r0 + i] - eb;
+    loff[i] = (int)max((int64_t)-1, min(v, (int64_t)items + 1));
+  }
+  __syncthreads();
+  const int ne = min(loff[R], items - (R - 1));
 #pragma unroll
-    for (int k = 0; k < IPT; ++k) {
-      const int64_t j = tid + (int64_t)k * NT;
-      if (j < ne) sval[j] = __ldg(&A.cin[__ldg(&A.idx[eb + j])]);
-    }
+  for (int k = 0; k < IPT; ++k) {
+    const int j = tid + k * NT;
+    if (j < ne) sval[j] = __ldg(&A.cin[__ldg(&A.idx[eb + j])]);
   }
   __syncthreads();
 
   double dpart = 0.0;
-  merge_tile_reduce<NT, IPT>(
-      soff, r0, R, p0, p1, eb, sval, scratch,
-      [&](int i, float v) { pr_epilogue(A, r0 + i, v, dn, dpart); },
+  tile_walk<NT, IPT>(
+      loff, R, items, sval, scratch, [&](int i, float v) { pr_epilogue(A, r0 + i, v, dn, dpart); },
       [&](int i, float v) {
         const int64_t r = r0 + i;
-        const int64_t sp = r + (int64_t)soff[i], ep = r + (int64_t)soff[i + 1];
+        const int64_t sp = r + (int64_t)off[r], ep = r + (int64_t)off[r + 1];
         const int pieces = (int)(ep / T - sp / T + 1);
         atomicAdd(&A.split_acc[r], (double)v);
         __threadfence();

@@ -108,62 +108,67 @@ __device__ __forceinline__ KeyVal seg_scan(KeyVal x, KeyVal& incl, KeyVal* scrat
   return ex;
 }
 
-// One tile of the merge-path reduction.
-//   soff[i] = off[r0 + i] for i in [0, R]  (smem; OffT)
-//   sval[e - eb] = value of edge e for edges of the tile (smem)
-//   complete(i, v): row r0+i starts and ends inside the tile; v its sum
-//   split(i, v):    row r0+i crosses the tile boundary; v is this tile's part
+// One tile of the merge-path reduction, in tile-local 32-bit coordinates.
+//   loff[i], i in [0, R]: first edge of row i relative to the tile's first
+//     edge, clamped to [-1, items + 1] (only row 0 can start before the tile,
+//     only row R-1 can end after it); row i occupies local items
+//     [i + loff[i], i + loff[i+1]] (its edges, then its end marker)
+//   sval[e]: value of the tile's local edge e
+//   complete(i, v): row i starts and ends inside the tile; v is its sum
+//   split(i, v):    row i crosses the tile boundary; v is this tile's part
 //                   (called exactly once per such row per tile)
 // Must be called by all NT threads (contains __syncthreads).
-template <int NT, int IPT, typename OffT, typename Complete, typename Split>
-__device__ __forceinline__ void merge_tile_reduce(const OffT* soff, int64_t r0, int R, int64_t p0, int64_t p1,
-                                                  int64_t eb, const float* sval, KeyVal* scratch,
-                                                  Complete&& complete, Split&& split) {
-  const int tid = threadIdx.x;
-  const int64_t d0 = p0 + (int64_t)tid * IPT;
-  const int64_t d1 = min(d0 + (int64_t)IPT, p1);
-  const bool active = d0 < p1;
-  int i = R;  // current row (index relative to r0)
+template <int NT, int IPT, typename Complete, typename Split>
+__device__ __forceinline__ void tile_walk(const int* loff, int R, int items, const float* sval, KeyVal* scratch,
+                                          Complete&& complete, Split&& split) {
+  const int q0 = threadIdx.x * IPT;
+  const int q1 = min(q0 + IPT, items);
+  const bool active = q0 < items;
+  int i = R;  // current row
   float acc = 0.f, head_val = 0.f;
-  int head = -1;  // head row completed in this window but started before d0
+  int head = -1;  // row completed in this window that started before it
   if (active) {
-    int lo = 0, hi = R - 1;  // row containing d0: min i with r0 + i + soff[i+1] >= d0
+    int lo = 0, hi = R - 1;  // row containing q0: min i with i + loff[i+1] >= q0
     while (lo < hi) {
       const int mid = (lo + hi) >> 1;
-      if (r0 + mid + (int64_t)soff[mid + 1] >= d0) hi = mid;
+      if (mid + loff[mid + 1] >= q0) hi = mid;
       else lo = mid + 1;
     }
     i = lo;
-    int64_t e = d0 - (r0 + i);
-    bool own = (r0 + i + (int64_t)soff[i]) >= d0;
-    int64_t rowend = r0 + i + (int64_t)soff[i + 1];
-    for (int64_t p = d0; p < d1; ++p) {
-      if (p < rowend) {
-        acc += sval[e - eb];
-        ++e;
-      } else {
-        if (own) complete(i, acc);
-        else {
-          head = i;
-          head_val = acc;
+    int e = q0 - i;
+    bool own = i + loff[i] >= q0;
+    int pe = i + loff[i + 1];
+#pragma unroll
+    for (int k = 0; k < IPT; ++k) {
+      const int q = q0 + k;
+      if (q < q1) {
+        if (q < pe) {
+          acc += sval[e];
+          ++e;
+        } else {
+          if (own) complete(i, acc);
+          else {
+            head = i;
+            head_val = acc;
+          }
+          acc = 0.f;
+          ++i;
+          own = true;
+          pe = i < R ? i + loff[i + 1] : 0x7fffffff;
         }
-        acc = 0.f;
-        ++i;
-        own = true;
-        if (i < R) rowend = r0 + i + (int64_t)soff[i + 1];
       }
     }
   }
-  // carry-out: (row open at d1, its partial inside [d0, d1))
+  // carry-out: (row open at q1, its partial inside [q0, q1))
   KeyVal incl;
   const KeyVal ex = seg_scan<NT>(KeyVal{active ? i : 0x7fffffff, active ? acc : 0.f}, incl, scratch);
   if (head >= 0) {
     const float tot = head_val + (ex.key == head ? ex.val : 0.f);
-    if (r0 + head + (int64_t)soff[head] >= p0) complete(head, tot);
+    if (head + loff[head] >= 0) complete(head, tot);
     else split(head, tot);
   }
-  // the last active thread reports the row still open at p1, if the tile holds part of it
-  if (active && d1 == p1 && i < R && (r0 + i + (int64_t)soff[i]) < p1) split(i, incl.val);
+  // the last active thread reports the row still open at the tile end, if the tile holds part of it
+  if (active && q1 == items && i < R && i + loff[i] < items) split(i, incl.val);
 }
 
 }  // namespace gi

@@ -33,8 +33,9 @@ namespace gi {
 namespace {
 
 constexpr int kSegThreads = 512;
-constexpr int kSegIPT = 8;
-constexpr int kSegTile = kSegThreads * kSegIPT;
+constexpr int kSegIPT = 16;
+constexpr int kSegTile = kSegThreads * kSegIPT;  // merge items per tile
+constexpr int kSegRows = kSegTile / 2 + 2;       // max pieces touching a tile (>= 2 items each)
 
 struct SegTile {
   int64_t pos;  // first merge position
@@ -44,15 +45,9 @@ struct SegTile {
   int32_t pad;
 };
 
-template <typename OffT>
-__host__ __device__ constexpr int seg_soff_bytes() {
-  return (int)(((kSegTile + 2) * sizeof(OffT) + 15) / 16 * 16);
-}
-// dynamic smem besides the contrib segment: soff | sval | spart
-template <typename OffT>
-constexpr int seg_fixed_dyn_bytes() {
-  return seg_soff_bytes<OffT>() + 2 * kSegTile * (int)sizeof(float);
-}
+// dynamic smem besides the contrib segment: loff | sval | spart
+__host__ __device__ constexpr int seg_loff_bytes() { return ((kSegRows + 1) * 4 + 15) / 16 * 16; }
+constexpr int seg_fixed_dyn_bytes() { return seg_loff_bytes() + kSegTile * 4 + ((kSegRows * 4 + 15) / 16 * 16); }
 
 template <typename OffT>
 struct SegArgs {
@@ -101,16 +96,16 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 //   regs(t) -> smem offsets | sync | issue loads of tile t+1 into regs |
 //   gather sval from the staged segment | sync | TMA next segment if it
 //   changes (overlaps the walk) | merge-path walk -> spart | sync | write
-//   the tile's completed piece partials (coalesced slot list in regs).
+//   the tile's completed piece partials (slot list held in registers).
 template <typename OffT>
 __global__ void __launch_bounds__(kSegThreads, 1) k_pr_seg(SegArgs<OffT> A) {
   constexpr int NT = kSegThreads, IPT = kSegIPT, TT = kSegTile;
-  constexpr int OPT = (TT + 2 + NT - 1) / NT;
+  constexpr int RPT = (kSegRows + 1 + NT - 1) / NT;  // piece entries per thread
   extern __shared__ __align__(128) unsigned char dyn_smem[];
-  OffT* soff = reinterpret_cast<OffT*>(dyn_smem);
-  float* sval = reinterpret_cast<float*>(dyn_smem + seg_soff_bytes<OffT>());
+  int* loff = reinterpret_cast<int*>(dyn_smem);
+  float* sval = reinterpret_cast<float*>(dyn_smem + seg_loff_bytes());
   float* spart = sval + TT;
-  float* scontrib = spart + TT;
+  float* scontrib = reinterpret_cast<float*>(dyn_smem + seg_fixed_dyn_bytes());
   __shared__ KeyVal scratch[NT / 32];
   __shared__ float s_carry;
   __shared__ __align__(8) uint64_t s_bar;
@@ -126,62 +121,60 @@ __global__ void __launch_bounds__(kSegThreads, 1) k_pr_seg(SegArgs<OffT> A) {
     tma_load_1d(scontrib, A.cin + base, (uint32_t)(((zlen * 4) + 15) & ~15ll), &s_bar);
   };
   uint16_t pidx[IPT];
-  OffT poff[OPT];
-  int32_t pslot[IPT];
-  auto prefetch = [&](const SegTile& T, int64_t p1) {
+  int poff[RPT];
+  int32_t pslot[RPT];
+  auto prefetch = [&](const SegTile& T, int items) {
     const int64_t r0 = T.r0;
     const int R = T.r1 - T.r0 + 1;
     const int64_t eb = T.pos - r0;
-    const int64_t items = p1 - T.pos;
+    const int lim = (int)min((int64_t)items, A.m - eb);
 #pragma unroll
-    for (int k = 0; k < OPT; ++k) {
+    for (int k = 0; k < RPT; ++k) {
       const int i = tid + k * NT;
-      poff[k] = i <= R ? __ldg(&A.pc_off[r0 + i]) : (OffT)0;
+      const int64_t v = i <= R ? (int64_t)__ldg(&A.pc_off[r0 + i]) - eb : 0;
+      poff[k] = (int)max((int64_t)-1, min(v, (int64_t)items + 1));
+      pslot[k] = i < R ? __ldg(&A.pc_slot[r0 + i]) : 0;
     }
+    const uint16_t* src = A.idx16 + eb;
 #pragma unroll
     for (int k = 0; k < IPT; ++k) {
-      const int64_t j = tid + (int64_t)k * NT;
-      pidx[k] = (j < items && eb + j < A.m) ? __ldg(&A.idx16[eb + j]) : (uint16_t)0;
-      pslot[k] = (j < R) ? __ldg(&A.pc_slot[r0 + j]) : 0;
+      const int j = tid + k * NT;
+      pidx[k] = j < lim ? __ldg(&src[j]) : (uint16_t)0;
     }
   };
 
   SegTile Tn = A.tiles[t0];
-  int64_t pn1 = A.tiles[t0 + 1].pos;
+  int items_n = (int)(A.tiles[t0 + 1].pos - Tn.pos);
   int cur_seg = Tn.seg;
   if (tid == 0) load_segment(cur_seg);
   bool seg_pending = true;
   uint32_t parity = 0;
-  prefetch(Tn, pn1);
+  prefetch(Tn, items_n);
 
   for (int t = t0; t < t1; ++t) {
     const SegTile T = Tn;
-    const int64_t p0 = T.pos, p1 = pn1;
-    const int64_t r0 = T.r0;
+    const int items = items_n;
     const int R = T.r1 - T.r0 + 1;
     if (t + 1 < t1) {
       Tn = A.tiles[t + 1];
-      pn1 = A.tiles[t + 2].pos;
+      items_n = (int)(A.tiles[t + 2].pos - Tn.pos);
     }
     uint16_t cidx[IPT];
-    int32_t cslot[IPT];
+    int32_t cslot[RPT];
 #pragma unroll
-    for (int k = 0; k < IPT; ++k) {
-      cidx[k] = pidx[k];
-      cslot[k] = pslot[k];
-    }
-    __syncthreads();  // previous tile's write-out finished reading soff
+    for (int k = 0; k < IPT; ++k) cidx[k] = pidx[k];
 #pragma unroll
-    for (int k = 0; k < OPT; ++k) {
+    for (int k = 0; k < RPT; ++k) cslot[k] = pslot[k];
+    __syncthreads();  // the previous tile's write-out is done with loff
+#pragma unroll
+    for (int k = 0; k < RPT; ++k) {
       const int i = tid + k * NT;
-      if (i <= R) soff[i] = poff[k];
+      if (i <= R) loff[i] = poff[k];
     }
     const float carry_in = s_carry;
-    __syncthreads();  // soff visible
-    const int64_t eb = p0 - r0;
-    const int64_t ee = min((int64_t)soff[R], p1 - (r0 + R - 1));
-    const int ne = (int)(ee - eb);
-    if (t + 1 < t1) prefetch(Tn, pn1);  // in flight during this tile
+    __syncthreads();  // loff visible
+    const int ne = min(loff[R], items - (R - 1));
+    if (t + 1 < t1) prefetch(Tn, items_n);  // in flight during this tile
     if (seg_pending) {
       mbar_wait(&s_bar, parity);
       parity ^= 1u;
@@ -198,20 +191,18 @@ __global__ void __launch_bounds__(kSegThreads, 1) k_pr_seg(SegArgs<OffT> A) {
       if (tid == 0) load_segment(cur_seg);  // overlaps the walk below
       seg_pending = true;
     }
-    merge_tile_reduce<NT, IPT>(
-        soff, r0, R, p0, p1, eb, sval, scratch, [&](int i, float v) { spart[i] = v; },
+    tile_walk<NT, IPT>(
+        loff, R, items, sval, scratch, [&](int i, float v) { spart[i] = v; },
         [&](int i, float v) {
-          const int64_t r = r0 + i;
-          const int64_t sp = r + (int64_t)soff[i], ep = r + (int64_t)soff[i + 1];
-          const float tot = v + (sp < p0 ? carry_in : 0.f);
-          if (ep < p1) spart[i] = tot;
+          const float tot = v + (loff[i] < 0 ? carry_in : 0.f);
+          if (i + loff[i + 1] < items) spart[i] = tot;
           else s_carry = tot;  // piece continues in this CTA's next tile
         });
     __syncthreads();  // spart ready
 #pragma unroll
-    for (int k = 0; k < IPT; ++k) {
+    for (int k = 0; k < RPT; ++k) {
       const int i = tid + k * NT;
-      if (i < R && r0 + i + (int64_t)soff[i + 1] < p1) A.partial[cslot[k]] = spart[i];
+      if (i < R && i + loff[i + 1] < items) A.partial[cslot[k]] = spart[i];
     }
   }
 }
@@ -451,7 +442,7 @@ static int seg_static_smem() {
   cudaFuncGetAttributes(&a, k_pr_seg<int32_t>);
   cudaFuncAttributes b{};
   cudaFuncGetAttributes(&b, k_pr_seg<int64_t>);
-  return (int)std::max(a.sharedSizeBytes, b.sharedSizeBytes) + seg_fixed_dyn_bytes<int64_t>();
+  return (int)std::max(a.sharedSizeBytes, b.sharedSizeBytes) + seg_fixed_dyn_bytes();
 }
 
 gi_status seg_build(gi_graph g, int segment_size) {
@@ -483,7 +474,7 @@ static gi_status seg_iter_t(gi_graph g, const PrArgs& A) {
   S.n = g->n;
   S.m = g->m;
   S.Z = g->seg_Z;
-  const size_t dyn = (size_t)g->seg_Z * sizeof(float) + seg_fixed_dyn_bytes<OffT>();
+  const size_t dyn = (size_t)g->seg_Z * sizeof(float) + seg_fixed_dyn_bytes();
   static size_t attr_set[2] = {0, 0};  // largest dynamic smem size configured so far
   const int k = sizeof(OffT) == 8;
   if (attr_set[k] < dyn) {
