@@ -107,8 +107,12 @@ struct gi_graph_s {
   gi::DevBuf push_sum;    // double[n]: push-form accumulator
   // segmented pull (pr_segmented.cu); seg_Z == 0 until built
   int seg_Z = 0, seg_S = 0, seg_ctas = 0;
-  int64_t seg_P = 0;
-  gi::DevBuf seg_pstart, seg_idx16, seg_pc_off, seg_pc_slot, seg_tiles, seg_cta_tiles, seg_partial;
+  int64_t seg_P = 0, seg_C = 0, seg_T = 0;  // pieces, chunks, tiles
+  gi::DevBuf seg_pstart;                    // OffT[n+1]: first destination-major piece of v
+  gi::DevBuf seg_cidx, seg_cslot;           // chunks: 4 x uint16 source ids, slot | last-chunk bit
+  gi::DevBuf seg_tiles;                     // int32[T]: segment of each tile
+  gi::DevBuf seg_partial;                   // float[P+1]: per-piece partial sums (+1 dummy)
+  gi::DevBuf seg_carry_slot, seg_carry_val; // per CTA: piece cut by the CTA's range end
   gi::DevBuf out_stage;   // float/int32[n]: output staging in input ids
   // BFS workspace
   gi::DevBuf parent;      // int32[n], internal ids

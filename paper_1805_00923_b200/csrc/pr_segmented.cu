@@ -33,32 +33,29 @@ namespace gi {
 namespace {
 
 constexpr int kSegThreads = 512;
-constexpr int kSegIPT = 16;
-constexpr int kSegTile = kSegThreads * kSegIPT;  // merge items per tile
-constexpr int kSegRows = kSegTile / 2 + 2;       // max pieces touching a tile (>= 2 items each)
 
-struct SegTile {
-  int64_t pos;  // first merge position
-  int32_t r0;   // piece containing pos
-  int32_t r1;   // piece containing the tile's last position
-  int32_t seg;
-  int32_t pad;
-};
+// ---------------------------------------------------------------- chunked segment kernel
+// Chunked layout (built below from the piece layout): every piece is cut into
+// chunks of kChunkE = 4 edges, the last chunk padded with the index Z (a
+// shared-memory zero). chunk c holds 4 uint16 source ids (8 bytes) and
+// cslot[c] = the piece's destination-major slot, bit 31 set on the piece's
+// last chunk. Each segment's chunk list is padded to whole tiles (kTileCh
+// chunks), so every tile lies in one segment and all tiles cost the same;
+// CTA c processes tiles [c*T/C, (c+1)*T/C).
+constexpr int kChunkE = 4;
+constexpr int kCPT = 4;                          // chunks per thread per tile
+constexpr int kTileCh = kSegThreads * kCPT;      // chunks per tile (8192 edge slots)
 
-// dynamic smem besides the contrib segment: loff | sval | spart
-__host__ __device__ constexpr int seg_loff_bytes() { return ((kSegRows + 1) * 4 + 15) / 16 * 16; }
-constexpr int seg_fixed_dyn_bytes() { return seg_loff_bytes() + kSegTile * 4 + ((kSegRows * 4 + 15) / 16 * 16); }
-
-template <typename OffT>
 struct SegArgs {
-  const SegTile* __restrict__ tiles;
-  const int32_t* __restrict__ cta_tiles;
-  const OffT* __restrict__ pc_off;
-  const int32_t* __restrict__ pc_slot;
-  const uint16_t* __restrict__ idx16;
-  const float* __restrict__ cin;  // padded to a multiple of 4 floats
+  const uint4* __restrict__ cidx;   // 2 chunks per uint4
+  const int4* __restrict__ cslot;   // 4 chunks per int4
+  const int32_t* __restrict__ tile_seg;
+  int64_t ntiles;
+  const float* __restrict__ cin;    // padded to a multiple of 4 floats
   float* __restrict__ partial;
-  int64_t n, m;
+  int32_t* __restrict__ carry_slot; // per CTA: piece still open at the CTA's end (-1: none)
+  float* __restrict__ carry_val;
+  int64_t n;
   int Z;
 };
 
@@ -91,120 +88,120 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
-// Persistent: CTA c processes tiles [cta_tiles[c], cta_tiles[c+1]) in order.
-// Software pipeline per tile t:
-//   regs(t) -> smem offsets | sync | issue loads of tile t+1 into regs |
-//   gather sval from the staged segment | sync | TMA next segment if it
-//   changes (overlaps the walk) | merge-path walk -> spart | sync | write
-//   the tile's completed piece partials (slot list held in registers).
-template <typename OffT>
-__global__ void __launch_bounds__(kSegThreads, 1) k_pr_seg(SegArgs<OffT> A) {
-  constexpr int NT = kSegThreads, IPT = kSegIPT, TT = kSegTile;
-  constexpr int RPT = (kSegRows + 1 + NT - 1) / NT;  // piece entries per thread
-  extern __shared__ __align__(128) unsigned char dyn_smem[];
-  int* loff = reinterpret_cast<int*>(dyn_smem);
-  float* sval = reinterpret_cast<float*>(dyn_smem + seg_loff_bytes());
-  float* spart = sval + TT;
-  float* scontrib = reinterpret_cast<float*>(dyn_smem + seg_fixed_dyn_bytes());
+__device__ __forceinline__ float chunk_sum(const float* sc, uint32_t lo, uint32_t hi) {
+  return (sc[lo & 0xFFFFu] + sc[lo >> 16]) + (sc[hi & 0xFFFFu] + sc[hi >> 16]);
+}
+
+// Per tile: thread t owns chunks [t*kCPT, (t+1)*kCPT) (32 B of indices, 16 B
+// of slots, one vector load each, prefetched one tile ahead). It sums its
+// chunks from the staged segment, stores every piece that ends inside its
+// window and starts inside it, and hands (slot of its last piece, open
+// partial) to a block segmented scan; the first piece that ends in its window
+// adds the scan's exclusive prefix. The open piece at the tile end is carried
+// to the next tile; at the CTA end it is exported for k_fold_carries.
+__global__ void __launch_bounds__(kSegThreads, 1) k_pr_seg(SegArgs A) {
+  constexpr int NT = kSegThreads;
+  extern __shared__ __align__(128) float scontrib[];  // Z + 4 floats; scontrib[Z] = 0 (chunk padding)
   __shared__ KeyVal scratch[NT / 32];
-  __shared__ float s_carry;
+  __shared__ int s_carry_key;
+  __shared__ float s_carry_val;
   __shared__ __align__(8) uint64_t s_bar;
   const int tid = threadIdx.x;
-  const int t0 = A.cta_tiles[blockIdx.x], t1 = A.cta_tiles[blockIdx.x + 1];
-  if (t0 >= t1) return;
-  if (tid == 0) mbar_init(&s_bar, 1);
+  const int64_t ta = A.ntiles * blockIdx.x / gridDim.x, tb = A.ntiles * (blockIdx.x + 1) / gridDim.x;
+  if (ta >= tb) {
+    if (tid == 0) A.carry_slot[blockIdx.x] = -1;
+    return;
+  }
+  if (tid == 0) {
+    mbar_init(&s_bar, 1);
+    scontrib[A.Z] = 0.f;
+    s_carry_key = -1;
+    s_carry_val = 0.f;
+  }
   __syncthreads();
-
   auto load_segment = [&](int seg) {  // thread 0
     const int64_t base = (int64_t)seg * A.Z;
     const int64_t zlen = min((int64_t)A.Z, A.n - base);
     tma_load_1d(scontrib, A.cin + base, (uint32_t)(((zlen * 4) + 15) & ~15ll), &s_bar);
   };
-  uint16_t pidx[IPT];
-  int poff[RPT];
-  int32_t pslot[RPT];
-  auto prefetch = [&](const SegTile& T, int items) {
-    const int64_t r0 = T.r0;
-    const int R = T.r1 - T.r0 + 1;
-    const int64_t eb = T.pos - r0;
-    const int lim = (int)min((int64_t)items, A.m - eb);
-#pragma unroll
-    for (int k = 0; k < RPT; ++k) {
-      const int i = tid + k * NT;
-      const int64_t v = i <= R ? (int64_t)__ldg(&A.pc_off[r0 + i]) - eb : 0;
-      poff[k] = (int)max((int64_t)-1, min(v, (int64_t)items + 1));
-      pslot[k] = i < R ? __ldg(&A.pc_slot[r0 + i]) : 0;
-    }
-    const uint16_t* src = A.idx16 + eb;
-#pragma unroll
-    for (int k = 0; k < IPT; ++k) {
-      const int j = tid + k * NT;
-      pidx[k] = j < lim ? __ldg(&src[j]) : (uint16_t)0;
-    }
-  };
-
-  SegTile Tn = A.tiles[t0];
-  int items_n = (int)(A.tiles[t0 + 1].pos - Tn.pos);
-  int cur_seg = Tn.seg;
+  int cur_seg = __ldg(&A.tile_seg[ta]);
   if (tid == 0) load_segment(cur_seg);
-  bool seg_pending = true;
   uint32_t parity = 0;
-  prefetch(Tn, items_n);
-
-  for (int t = t0; t < t1; ++t) {
-    const SegTile T = Tn;
-    const int items = items_n;
-    const int R = T.r1 - T.r0 + 1;
-    if (t + 1 < t1) {
-      Tn = A.tiles[t + 1];
-      items_n = (int)(A.tiles[t + 2].pos - Tn.pos);
+  bool pending = true;
+  // prefetch registers: 4 chunks = 2 x uint4 of indices + 1 x int4 of slots
+  const int64_t c0 = ta * kTileCh + (int64_t)tid * kCPT;
+  uint4 pa = __ldg(&A.cidx[c0 / 2]), pb = __ldg(&A.cidx[c0 / 2 + 1]);
+  int4 ps = __ldg(&A.cslot[c0 / 4]);
+  for (int64_t t = ta; t < tb; ++t) {
+    const uint4 ia = pa, ib = pb;
+    const int4 sl = ps;
+    const int next_seg = t + 1 < tb ? __ldg(&A.tile_seg[t + 1]) : cur_seg;
+    if (t + 1 < tb) {  // in flight during this tile
+      const int64_t cn = (t + 1) * kTileCh + (int64_t)tid * kCPT;
+      pa = __ldg(&A.cidx[cn / 2]);
+      pb = __ldg(&A.cidx[cn / 2 + 1]);
+      ps = __ldg(&A.cslot[cn / 4]);
     }
-    uint16_t cidx[IPT];
-    int32_t cslot[RPT];
-#pragma unroll
-    for (int k = 0; k < IPT; ++k) cidx[k] = pidx[k];
-#pragma unroll
-    for (int k = 0; k < RPT; ++k) cslot[k] = pslot[k];
-    __syncthreads();  // the previous tile's write-out is done with loff
-#pragma unroll
-    for (int k = 0; k < RPT; ++k) {
-      const int i = tid + k * NT;
-      if (i <= R) loff[i] = poff[k];
-    }
-    const float carry_in = s_carry;
-    __syncthreads();  // loff visible
-    const int ne = min(loff[R], items - (R - 1));
-    if (t + 1 < t1) prefetch(Tn, items_n);  // in flight during this tile
-    if (seg_pending) {
+    if (pending) {
       mbar_wait(&s_bar, parity);
       parity ^= 1u;
-      seg_pending = false;
+      pending = false;
     }
+    float v[kCPT];
+    v[0] = chunk_sum(scontrib, ia.x, ia.y);
+    v[1] = chunk_sum(scontrib, ia.z, ia.w);
+    v[2] = chunk_sum(scontrib, ib.x, ib.y);
+    v[3] = chunk_sum(scontrib, ib.z, ib.w);
+    const int s[kCPT] = {sl.x, sl.y, sl.z, sl.w};
+    __syncthreads();  // every read of scontrib for this tile is done
+    if (next_seg != cur_seg) {
+      cur_seg = next_seg;
+      if (tid == 0) load_segment(cur_seg);  // overlaps the rest of this tile
+      pending = true;
+    }
+    const int carry_key = s_carry_key;
+    const float carry_val = s_carry_val;
+    float acc = 0.f, head_val = 0.f;
+    int head = -1;
 #pragma unroll
-    for (int k = 0; k < IPT; ++k) {
-      const int j = tid + k * NT;
-      if (j < ne) sval[j] = scontrib[cidx[k]];
+    for (int k = 0; k < kCPT; ++k) {
+      acc += v[k];
+      if (s[k] < 0) {  // last chunk of its piece
+        const int slot = s[k] & 0x7fffffff;
+        if (head < 0) {
+          head = slot;
+          head_val = acc;
+        } else {
+          A.partial[slot] = acc;
+        }
+        acc = 0.f;
+      }
     }
-    __syncthreads();  // sval ready; every read of scontrib for this tile is done
-    if (t + 1 < t1 && Tn.seg != cur_seg) {
-      cur_seg = Tn.seg;
-      if (tid == 0) load_segment(cur_seg);  // overlaps the walk below
-      seg_pending = true;
+    const int last_key = s[kCPT - 1] & 0x7fffffff;
+    if (tid == 0) {  // fold the carry from the previous tile into the first run
+      if (head >= 0) head_val += head == carry_key ? carry_val : 0.f;
+      else if (last_key == carry_key) acc += carry_val;
     }
-    tile_walk<NT, IPT>(
-        loff, R, items, sval, scratch, [&](int i, float v) { spart[i] = v; },
-        [&](int i, float v) {
-          const float tot = v + (loff[i] < 0 ? carry_in : 0.f);
-          if (i + loff[i + 1] < items) spart[i] = tot;
-          else s_carry = tot;  // piece continues in this CTA's next tile
-        });
-    __syncthreads();  // spart ready
-#pragma unroll
-    for (int k = 0; k < RPT; ++k) {
-      const int i = tid + k * NT;
-      if (i < R && i + loff[i + 1] < items) A.partial[cslot[k]] = spart[i];
+    KeyVal incl;
+    const KeyVal ex = seg_scan<NT>(KeyVal{last_key, acc}, incl, scratch);
+    if (head >= 0) A.partial[head] = head_val + (tid > 0 && ex.key == head ? ex.val : 0.f);
+    if (tid == NT - 1) {
+      const bool open = s[kCPT - 1] >= 0;
+      s_carry_key = open ? last_key : -1;
+      s_carry_val = open ? incl.val : 0.f;
+      if (t + 1 == tb) {
+        A.carry_slot[blockIdx.x] = open ? last_key : -1;
+        A.carry_val[blockIdx.x] = open ? incl.val : 0.f;
+      }
     }
   }
+}
+
+// partial[carry_slot[c]] += carry_val[c]: pieces cut by CTA boundaries
+__global__ void k_fold_carries(const int32_t* __restrict__ slot, const float* __restrict__ val, int C,
+                               float* __restrict__ partial) {
+  for (int c = threadIdx.x; c < C; c += blockDim.x)
+    if (slot[c] >= 0) atomicAdd(&partial[slot[c]], val[c]);
 }
 
 template <typename OffT>
@@ -297,6 +294,67 @@ __global__ void k_seg_starts(const uint32_t* __restrict__ sseg, int64_t m, int S
   }
 }
 
+template <typename OffT>
+__global__ void k_piece_nch(const OffT* __restrict__ pc_off, int64_t P, int64_t* __restrict__ nch) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p <= P; p += (int64_t)gridDim.x * blockDim.x)
+    nch[p] = p < P ? ((int64_t)pc_off[p + 1] - (int64_t)pc_off[p] + kChunkE - 1) / kChunkE : 0;
+}
+
+// seg_p[s] = first piece of segment s (lower bound of seg_e[s] in pc_off)
+template <typename OffT>
+__global__ void k_seg_piece_starts(const OffT* __restrict__ pc_off, int64_t P, const int64_t* __restrict__ seg_e,
+                                   int S, int64_t* __restrict__ seg_p) {
+  for (int s = blockIdx.x * blockDim.x + threadIdx.x; s <= S; s += gridDim.x * blockDim.x) {
+    int64_t lo = 0, hi = P;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if ((int64_t)pc_off[mid] < seg_e[s]) lo = mid + 1;
+      else hi = mid;
+    }
+    seg_p[s] = lo;
+  }
+}
+
+__global__ void k_gather_i64(const int64_t* __restrict__ src, const int64_t* __restrict__ at, int k,
+                             int64_t* __restrict__ out) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < k; i += gridDim.x * blockDim.x) out[i] = src[at[i]];
+}
+
+__global__ void k_fill_pad(uint16_t* __restrict__ cidx, int32_t* __restrict__ cslot, int64_t C, uint16_t pad_idx,
+                           int32_t pad_slot) {
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < C; c += (int64_t)gridDim.x * blockDim.x) {
+    for (int k = 0; k < kChunkE; ++k) cidx[c * kChunkE + k] = pad_idx;
+    cslot[c] = pad_slot;
+  }
+}
+
+template <typename OffT>
+__global__ void k_fill_chunks(const OffT* __restrict__ pc_off, const int32_t* __restrict__ pc_slot,
+                              const uint16_t* __restrict__ idx16, int64_t P, const int64_t* __restrict__ cp,
+                              const int64_t* __restrict__ seg_p, const int64_t* __restrict__ seg_base, int S, int Z,
+                              uint16_t* __restrict__ cidx, int32_t* __restrict__ cslot) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < P; p += (int64_t)gridDim.x * blockDim.x) {
+    int lo = 0, hi = S - 1;  // segment of p: last s with seg_p[s] <= p
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (seg_p[mid] <= p) lo = mid;
+      else hi = mid - 1;
+    }
+    const int64_t c0 = seg_base[lo] + (cp[p] - cp[seg_p[lo]]);
+    const int64_t e0 = pc_off[p], len = (int64_t)pc_off[p + 1] - e0;
+    const int64_t nch = (len + kChunkE - 1) / kChunkE;
+    const int32_t slot = pc_slot[p];
+    for (int64_t j = 0; j < nch; ++j) {
+      const int64_t c = c0 + j;
+      for (int k = 0; k < kChunkE; ++k) {
+        const int64_t e = j * kChunkE + k;
+        cidx[c * kChunkE + k] = e < len ? idx16[e0 + e] : (uint16_t)Z;
+      }
+      cslot[c] = j == nch - 1 ? (int32_t)(slot | 0x80000000u) : slot;
+    }
+  }
+}
+
 }  // namespace
 
 template <typename OffT>
@@ -308,7 +366,8 @@ static gi_status seg_build_t(gi_graph g, int Z) {
   const OffT* off = g->csc_off.as<OffT>();
   const int32_t* idx = g->csc_idx.as<int32_t>();
   const int S = (int)ceil_div(n, Z);
-  DevBuf flag, ex, pdm, seg, seg2, eid, order, spdm, tmp, nsel, seg_e;
+  // ---- piece layout: (segment, destination) runs of the CSC
+  DevBuf flag, ex, pdm, seg, seg2, eid, order, spdm, tmp, nsel, seg_e, pc_off, pc_slot, idx16;
   GI_TRY(flag.alloc((m + 1) * sizeof(int32_t)));
   GI_TRY(ex.alloc((m + 1) * sizeof(OffT)));
   k_piece_flags<<<grid_for(m + 1, 256, sms), 256, 0, st>>>(idx, m, Z, flag.as<int32_t>());
@@ -317,9 +376,11 @@ static gi_status seg_build_t(gi_graph g, int Z) {
   GI_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, flag.as<int32_t>(), ex.as<OffT>(), m + 1, st));
   GI_TRY(tmp.alloc(tb));
   GI_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb, flag.as<int32_t>(), ex.as<OffT>(), m + 1, st));
-  OffT P = 0;
-  GI_CUDA(cudaMemcpyAsync(&P, ex.as<OffT>() + m, sizeof(OffT), cudaMemcpyDeviceToHost, st));
+  OffT Pt = 0;
+  GI_CUDA(cudaMemcpyAsync(&Pt, ex.as<OffT>() + m, sizeof(OffT), cudaMemcpyDeviceToHost, st));
   GI_CUDA(cudaStreamSynchronize(st));
+  const int64_t P = (int64_t)Pt;
+  if (P >= INT32_MAX) return fail(GI_ERR_UNSUPPORTED, "segmented pull: more than 2^31 pieces");
   GI_TRY(g->seg_pstart.alloc((n + 1) * sizeof(OffT)));
   k_pstart<OffT><<<grid_for(n + 1, 256, sms), 256, 0, st>>>(off, ex.as<OffT>(), n, g->seg_pstart.as<OffT>());
   GI_TRY(pdm.alloc(m * sizeof(OffT)));
@@ -329,6 +390,7 @@ static gi_status seg_build_t(gi_graph g, int Z) {
   GI_TRY(order.alloc(m * sizeof(OffT)));
   k_piece_dm<OffT><<<grid_for(m, 256, sms), 256, 0, st>>>(flag.as<int32_t>(), ex.as<OffT>(), m, idx, Z, pdm.as<OffT>(),
                                                           seg.as<uint32_t>(), eid.as<OffT>());
+  ex.reset();
   int sbits = 1;
   while ((1ll << sbits) < S) ++sbits;
   tb = 0;
@@ -337,122 +399,98 @@ static gi_status seg_build_t(gi_graph g, int Z) {
   GI_TRY(tmp.alloc(tb));
   GI_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, seg.as<uint32_t>(), seg2.as<uint32_t>(), eid.as<OffT>(),
                                           order.as<OffT>(), m, 0, sbits, st));
-  GI_TRY(g->seg_idx16.alloc((m + 64) * sizeof(uint16_t)));
+  eid.reset();
+  seg.reset();
+  GI_TRY(idx16.alloc((m + 64) * sizeof(uint16_t)));
   GI_TRY(spdm.alloc(m * sizeof(OffT)));
   k_seg_gather<OffT><<<grid_for(m, 256, sms), 256, 0, st>>>(order.as<OffT>(), seg2.as<uint32_t>(), m, idx,
-                                                            pdm.as<OffT>(), Z, g->seg_idx16.as<uint16_t>(),
-                                                            spdm.as<OffT>());
-  // piece starts in segment-major order
+                                                            pdm.as<OffT>(), Z, idx16.as<uint16_t>(), spdm.as<OffT>());
+  order.reset();
+  pdm.reset();
   k_piece_start_flags<OffT><<<grid_for(m, 256, sms), 256, 0, st>>>(spdm.as<OffT>(), m, flag.as<int32_t>());
-  GI_TRY(g->seg_pc_off.alloc(((int64_t)P + 2) * sizeof(OffT)));
+  GI_TRY(pc_off.alloc((P + 2) * sizeof(OffT)));
   GI_TRY(nsel.alloc(sizeof(int64_t)));
   cub::CountingInputIterator<OffT> cnt(0);
   tb = 0;
-  GI_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, cnt, flag.as<int32_t>(), g->seg_pc_off.as<OffT>(), nsel.as<int64_t>(),
-                                     m, st));
+  GI_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, cnt, flag.as<int32_t>(), pc_off.as<OffT>(), nsel.as<int64_t>(), m, st));
   GI_TRY(tmp.alloc(tb));
-  GI_CUDA(cub::DeviceSelect::Flagged(tmp.p, tb, cnt, flag.as<int32_t>(), g->seg_pc_off.as<OffT>(), nsel.as<int64_t>(),
-                                     m, st));
+  GI_CUDA(cub::DeviceSelect::Flagged(tmp.p, tb, cnt, flag.as<int32_t>(), pc_off.as<OffT>(), nsel.as<int64_t>(), m, st));
   const OffT mm = (OffT)m;
-  GI_CUDA(cudaMemcpyAsync(g->seg_pc_off.as<OffT>() + P, &mm, sizeof(OffT), cudaMemcpyHostToDevice, st));
-  GI_TRY(g->seg_pc_slot.alloc(((int64_t)P + 1) * sizeof(int32_t)));
-  k_piece_slot<OffT><<<grid_for(P, 256, sms), 256, 0, st>>>(g->seg_pc_off.as<OffT>(), P, spdm.as<OffT>(),
-                                                            g->seg_pc_slot.as<int32_t>());
+  GI_CUDA(cudaMemcpyAsync(pc_off.as<OffT>() + P, &mm, sizeof(OffT), cudaMemcpyHostToDevice, st));
+  GI_TRY(pc_slot.alloc((P + 1) * sizeof(int32_t)));
+  k_piece_slot<OffT><<<grid_for(P, 256, sms), 256, 0, st>>>(pc_off.as<OffT>(), P, spdm.as<OffT>(), pc_slot.as<int32_t>());
   GI_TRY(seg_e.alloc((S + 1) * sizeof(int64_t)));
   k_seg_starts<<<grid_for(S + 1, 256, sms), 256, 0, st>>>(seg2.as<uint32_t>(), m, S, seg_e.as<int64_t>());
-  GI_CUDA(cudaGetLastError());
+  spdm.reset();
+  seg2.reset();
+  flag.reset();
 
-  // ---- host tile planning (native runtime: merge-path cuts, one CTA per SM)
-  std::vector<OffT> h_off((size_t)P + 1);
-  std::vector<int64_t> h_seg_e(S + 1);
-  GI_CUDA(cudaMemcpyAsync(h_off.data(), g->seg_pc_off.p, ((size_t)P + 1) * sizeof(OffT), cudaMemcpyDeviceToHost, st));
-  GI_CUDA(cudaMemcpyAsync(h_seg_e.data(), seg_e.p, (S + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  // ---- chunked layout
+  DevBuf nch, cp, seg_p, cp_at, seg_base;
+  GI_TRY(nch.alloc((P + 1) * sizeof(int64_t)));
+  GI_TRY(cp.alloc((P + 1) * sizeof(int64_t)));
+  k_piece_nch<OffT><<<grid_for(P + 1, 256, sms), 256, 0, st>>>(pc_off.as<OffT>(), P, nch.as<int64_t>());
+  tb = 0;
+  GI_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, nch.as<int64_t>(), cp.as<int64_t>(), P + 1, st));
+  GI_TRY(tmp.alloc(tb));
+  GI_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb, nch.as<int64_t>(), cp.as<int64_t>(), P + 1, st));
+  GI_TRY(seg_p.alloc((S + 1) * sizeof(int64_t)));
+  GI_TRY(cp_at.alloc((S + 1) * sizeof(int64_t)));
+  k_seg_piece_starts<OffT><<<grid_for(S + 1, 256, sms), 256, 0, st>>>(pc_off.as<OffT>(), P, seg_e.as<int64_t>(), S,
+                                                                      seg_p.as<int64_t>());
+  k_gather_i64<<<grid_for(S + 1, 256, sms), 256, 0, st>>>(cp.as<int64_t>(), seg_p.as<int64_t>(), S + 1,
+                                                          cp_at.as<int64_t>());
+  std::vector<int64_t> h_cp_at(S + 1);
+  GI_CUDA(cudaMemcpyAsync(h_cp_at.data(), cp_at.p, (S + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   GI_CUDA(cudaStreamSynchronize(st));
-  const int64_t PP = (int64_t)P;
-  const int64_t I = PP + m;
-  auto pe = [&](int64_t p) { return p + (int64_t)h_off[p + 1]; };
-  auto ps = [&](int64_t p) { return p + (int64_t)h_off[p]; };
-  auto piece_at = [&](int64_t x) {  // min p with pe(p) >= x
-    int64_t lo = 0, hi = PP - 1;
-    while (lo < hi) {
-      const int64_t mid = (lo + hi) >> 1;
-      if (pe(mid) >= x) hi = mid;
-      else lo = mid + 1;
-    }
-    return lo;
-  };
-  std::vector<int64_t> seg_p(S + 1);  // first piece of each segment
-  for (int s = 0; s <= S; ++s) {
-    int64_t lo = 0, hi = PP;  // lower_bound(h_off[0..P), seg_e[s])
-    while (lo < hi) {
-      const int64_t mid = (lo + hi) >> 1;
-      if ((int64_t)h_off[mid] < h_seg_e[s]) lo = mid + 1;
-      else hi = mid;
-    }
-    seg_p[s] = lo;
+  std::vector<int64_t> h_base(S + 1);
+  std::vector<int32_t> h_tile_seg;
+  int64_t C = 0;
+  for (int s = 0; s < S; ++s) {
+    h_base[s] = C;
+    const int64_t raw = h_cp_at[s + 1] - h_cp_at[s];
+    const int64_t tiles = ceil_div(raw, kTileCh);
+    for (int64_t t = 0; t < tiles; ++t) h_tile_seg.push_back(s);
+    C += tiles * kTileCh;
   }
-  const int C = sms;
-  std::vector<int64_t> cuts(C + 1, 0);
-  cuts[C] = I;
-  for (int c = 1; c < C; ++c) {
-    const int64_t target = (int64_t)((__int128)I * c / C);
-    int64_t cut = PP > 0 ? pe(piece_at(target)) + 1 : 0;
-    cut = std::min(std::max(cut, cuts[c - 1]), I);
-    cuts[c] = cut;
-  }
-  std::vector<SegTile> tiles;
-  std::vector<int32_t> cta_tiles(C + 1);
-  tiles.reserve((size_t)(I / kSegTile + 2 * (S + C) + 2));
-  int seg_cur = 0;
-  for (int c = 0; c < C; ++c) {
-    cta_tiles[c] = (int32_t)tiles.size();
-    int64_t pos = cuts[c];
-    while (pos < cuts[c + 1]) {
-      const int64_t p = piece_at(pos);
-      while (seg_cur + 1 <= S && seg_p[seg_cur + 1] <= p) ++seg_cur;
-      const int64_t seg_end = seg_p[seg_cur + 1] >= PP ? I : ps(seg_p[seg_cur + 1]);
-      const int64_t end = std::min(std::min(pos + (int64_t)kSegTile, cuts[c + 1]), seg_end);
-      SegTile T;
-      T.pos = pos;
-      T.r0 = (int32_t)p;
-      T.r1 = (int32_t)piece_at(end - 1);
-      T.seg = seg_cur;
-      T.pad = 0;
-      tiles.push_back(T);
-      pos = end;
-    }
-  }
-  cta_tiles[C] = (int32_t)tiles.size();
-  tiles.push_back(SegTile{I, 0, 0, 0, 0});
-  GI_TRY(g->seg_tiles.alloc(tiles.size() * sizeof(SegTile)));
-  GI_TRY(g->seg_cta_tiles.alloc((C + 1) * sizeof(int32_t)));
-  GI_CUDA(cudaMemcpyAsync(g->seg_tiles.p, tiles.data(), tiles.size() * sizeof(SegTile), cudaMemcpyHostToDevice, st));
-  GI_CUDA(cudaMemcpyAsync(g->seg_cta_tiles.p, cta_tiles.data(), (C + 1) * sizeof(int32_t), cudaMemcpyHostToDevice, st));
-  GI_TRY(g->seg_partial.alloc(((int64_t)P + 1) * sizeof(float)));
+  h_base[S] = C;
+  const int64_t T = (int64_t)h_tile_seg.size();
+  GI_TRY(seg_base.alloc((S + 1) * sizeof(int64_t)));
+  GI_CUDA(cudaMemcpyAsync(seg_base.p, h_base.data(), (S + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  GI_TRY(g->seg_cidx.alloc((C > 0 ? C : 1) * kChunkE * sizeof(uint16_t)));
+  GI_TRY(g->seg_cslot.alloc((C > 0 ? C : 1) * sizeof(int32_t)));
+  GI_TRY(g->seg_tiles.alloc((T > 0 ? T : 1) * sizeof(int32_t)));
+  if (T > 0)
+    GI_CUDA(cudaMemcpyAsync(g->seg_tiles.p, h_tile_seg.data(), T * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+  k_fill_pad<<<grid_for(C, 256, sms), 256, 0, st>>>(g->seg_cidx.as<uint16_t>(), g->seg_cslot.as<int32_t>(), C,
+                                                    (uint16_t)Z, (int32_t)((uint32_t)P | 0x80000000u));
+  k_fill_chunks<OffT><<<grid_for(P, 256, sms), 256, 0, st>>>(
+      pc_off.as<OffT>(), pc_slot.as<int32_t>(), idx16.as<uint16_t>(), P, cp.as<int64_t>(), seg_p.as<int64_t>(),
+      seg_base.as<int64_t>(), S, Z, g->seg_cidx.as<uint16_t>(), g->seg_cslot.as<int32_t>());
+  GI_TRY(g->seg_partial.alloc((P + 1) * sizeof(float)));
+  GI_TRY(g->seg_carry_slot.alloc(sms * sizeof(int32_t)));
+  GI_TRY(g->seg_carry_val.alloc(sms * sizeof(float)));
+  GI_CUDA(cudaGetLastError());
   GI_CUDA(cudaStreamSynchronize(st));
   g->seg_Z = Z;
   g->seg_S = S;
-  g->seg_P = PP;
-  g->seg_ctas = C;
+  g->seg_P = P;
+  g->seg_C = C;
+  g->seg_T = T;
+  g->seg_ctas = sms;
   return GI_OK;
-}
-
-static int seg_static_smem() {
-  cudaFuncAttributes a{};
-  cudaFuncGetAttributes(&a, k_pr_seg<int32_t>);
-  cudaFuncAttributes b{};
-  cudaFuncGetAttributes(&b, k_pr_seg<int64_t>);
-  return (int)std::max(a.sharedSizeBytes, b.sharedSizeBytes) + seg_fixed_dyn_bytes();
 }
 
 gi_status seg_build(gi_graph g, int segment_size) {
   if (segment_size < 0) return fail(GI_ERR_INVALID_ARGUMENT, "segment_size < 0");
   int optin = 0;
   GI_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, g->ctx->device));
-  int Z = (optin - seg_static_smem() - 1024) / 4;
-  Z = std::min(Z, 65536) & ~31;
+  cudaFuncAttributes a{};
+  GI_CUDA(cudaFuncGetAttributes(&a, k_pr_seg));
+  int Z = (optin - (int)a.sharedSizeBytes - 64) / 4 - 4;
+  Z = std::min(Z, 65535) & ~31;
   if (Z < 1024) return fail(GI_ERR_UNSUPPORTED, "segmented pull: not enough shared memory");
-  if (segment_size > 0) Z = std::min(Z, segment_size);
+  if (segment_size > 0) Z = std::max(32, std::min(Z, segment_size) & ~3);
   if (g->seg_Z == Z) return GI_OK;
   g->seg_Z = 0;
   if (g->m == 0 || g->n == 0) return fail(GI_ERR_UNSUPPORTED, "segmented pull: empty graph");
@@ -460,49 +498,41 @@ gi_status seg_build(gi_graph g, int segment_size) {
   return seg_build_t<int32_t>(g, Z);
 }
 
-template <typename OffT>
-static gi_status seg_iter_t(gi_graph g, const PrArgs& A) {
+gi_status seg_edge_pass(gi_graph g, const PrArgs& A) {
   cudaStream_t st = g->ctx->stream;
-  SegArgs<OffT> S;
-  S.tiles = g->seg_tiles.as<SegTile>();
-  S.cta_tiles = g->seg_cta_tiles.as<int32_t>();
-  S.pc_off = g->seg_pc_off.as<OffT>();
-  S.pc_slot = g->seg_pc_slot.as<int32_t>();
-  S.idx16 = g->seg_idx16.as<uint16_t>();
+  SegArgs S;
+  S.cidx = g->seg_cidx.as<uint4>();
+  S.cslot = g->seg_cslot.as<int4>();
+  S.tile_seg = g->seg_tiles.as<int32_t>();
+  S.ntiles = g->seg_T;
   S.cin = A.cin;
   S.partial = g->seg_partial.as<float>();
+  S.carry_slot = g->seg_carry_slot.as<int32_t>();
+  S.carry_val = g->seg_carry_val.as<float>();
   S.n = g->n;
-  S.m = g->m;
   S.Z = g->seg_Z;
-  const size_t dyn = (size_t)g->seg_Z * sizeof(float) + seg_fixed_dyn_bytes();
-  static size_t attr_set[2] = {0, 0};  // largest dynamic smem size configured so far
-  const int k = sizeof(OffT) == 8;
-  if (attr_set[k] < dyn) {
-    GI_CUDA(cudaFuncSetAttribute(k_pr_seg<OffT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
-    attr_set[k] = dyn;
+  const size_t dyn = ((size_t)g->seg_Z + 4) * sizeof(float);
+  static size_t attr_set = 0;  // largest dynamic smem size configured so far
+  if (attr_set < dyn) {
+    GI_CUDA(cudaFuncSetAttribute(k_pr_seg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+    attr_set = dyn;
   }
-  k_pr_seg<OffT><<<g->seg_ctas, kSegThreads, dyn, st>>>(S);
+  k_pr_seg<<<g->seg_ctas, kSegThreads, dyn, st>>>(S);
+  k_fold_carries<<<1, 256, 0, st>>>(S.carry_slot, S.carry_val, g->seg_ctas, S.partial);
   GI_CUDA(cudaGetLastError());
   return GI_OK;
-}
-
-template <typename OffT>
-static gi_status seg_merge_t(gi_graph g, const PrArgs& A) {
-  cudaStream_t st = g->ctx->stream;
-  k_pr_merge<OffT><<<grid_for(g->n, 256, g->ctx->num_sms, 16), 256, 0, st>>>(A, g->seg_pstart.as<OffT>(),
-                                                                              g->seg_partial.as<float>());
-  GI_CUDA(cudaGetLastError());
-  return GI_OK;
-}
-
-gi_status seg_edge_pass(gi_graph g, const PrArgs& A) {
-  if (g->off64) return seg_iter_t<int64_t>(g, A);
-  return seg_iter_t<int32_t>(g, A);
 }
 
 gi_status seg_vertex_pass(gi_graph g, const PrArgs& A) {
-  if (g->off64) return seg_merge_t<int64_t>(g, A);
-  return seg_merge_t<int32_t>(g, A);
+  cudaStream_t st = g->ctx->stream;
+  if (g->off64)
+    k_pr_merge<int64_t><<<grid_for(g->n, 256, g->ctx->num_sms, 16), 256, 0, st>>>(A, g->seg_pstart.as<int64_t>(),
+                                                                                   g->seg_partial.as<float>());
+  else
+    k_pr_merge<int32_t><<<grid_for(g->n, 256, g->ctx->num_sms, 16), 256, 0, st>>>(A, g->seg_pstart.as<int32_t>(),
+                                                                                   g->seg_partial.as<float>());
+  GI_CUDA(cudaGetLastError());
+  return GI_OK;
 }
 
 }  // namespace gi
