@@ -20,7 +20,10 @@
 //  conversion: queue -> bitmap (atomicOr per id);
 //    bitmap -> queue (popc + warp scan + one atomicAdd per warp).
 #include <algorithm>
+#include <cooperative_groups.h>
 #include <cub/cub.cuh>
+
+namespace cg = cooperative_groups;
 
 #include "gi_internal.cuh"
 
@@ -29,6 +32,7 @@ namespace {
 
 constexpr int kRing = 4;  // counter slots ring: slot(l) = cnt + 2*(l % kRing): {|F_l|, sum outdeg F_l}
 constexpr int64_t kBalancedMin = 1 << 15;  // push levels with more frontier edges use k_bfs_push_bal
+constexpr int64_t kPersistMax = 1 << 15;   // push levels with fewer frontier edges run in k_bfs_persist
 
 __global__ void k_bfs_init(int32_t s_in, const int32_t* __restrict__ inv, const int32_t* __restrict__ outdeg,
                            int32_t* __restrict__ parent, int32_t* __restrict__ q, int64_t* __restrict__ cnt) {
@@ -39,17 +43,22 @@ __global__ void k_bfs_init(int32_t s_in, const int32_t* __restrict__ inv, const 
   cnt[1] = outdeg[s];
 }
 
+struct PushSmem {
+  cub::BlockScan<long long, 256>::TempStorage scan;
+  long long pre[257];
+  long long beg[256];
+  int32_t u[256];
+};
+
+// One push level over queue q[0, qlen) by this CTA's share of 256-vertex
+// chunks (CTA-wide scan of degrees, then a balanced walk of the chunk's edges).
 template <typename OffT>
-__global__ void __launch_bounds__(256) k_bfs_push(const int32_t* __restrict__ q, int64_t qlen,
-                                                  const OffT* __restrict__ off, const int32_t* __restrict__ idx,
-                                                  const int32_t* __restrict__ outdeg, int32_t* parent,
-                                                  int32_t* __restrict__ qnext, int64_t* __restrict__ cnext) {
+__device__ __forceinline__ void push_chunks(const int32_t* __restrict__ q, int64_t qlen, const OffT* __restrict__ off,
+                                            const int32_t* __restrict__ idx, const int32_t* __restrict__ outdeg,
+                                            int32_t* parent, int32_t* __restrict__ qnext, int64_t* cnext,
+                                            PushSmem& sm) {
   constexpr int NT = 256;
   using Scan = cub::BlockScan<long long, NT>;
-  __shared__ typename Scan::TempStorage scan_tmp;
-  __shared__ long long s_pre[NT + 1];
-  __shared__ long long s_beg[NT];
-  __shared__ int32_t s_u[NT];
   const int tid = threadIdx.x, lane = tid & 31;
   for (int64_t c0 = (int64_t)blockIdx.x * NT; c0 < qlen; c0 += (int64_t)gridDim.x * NT) {
     const int64_t i = c0 + tid;
@@ -61,32 +70,31 @@ __global__ void __launch_bounds__(256) k_bfs_push(const int32_t* __restrict__ q,
       deg = (long long)off[u + 1] - beg;
     }
     long long pre, total;
-    Scan(scan_tmp).ExclusiveSum(deg, pre, total);
-    s_pre[tid] = pre;
-    s_beg[tid] = beg;
-    s_u[tid] = u;
-    if (tid == 0) s_pre[NT] = total;
+    Scan(sm.scan).ExclusiveSum(deg, pre, total);
+    sm.pre[tid] = pre;
+    sm.beg[tid] = beg;
+    sm.u[tid] = u;
     __syncthreads();
     for (long long base = 0; base < total; base += NT) {
       const long long f = base + tid;
       bool won = false;
       int32_t v = 0;
       if (f < total) {
-        int lo = 0, hi = NT - 1;  // owner = last k with s_pre[k] <= f
+        int lo = 0, hi = NT - 1;  // owner = last k with pre[k] <= f
         while (lo < hi) {
-          int mid = (lo + hi + 1) >> 1;
-          if (s_pre[mid] <= f) lo = mid;
+          const int mid = (lo + hi + 1) >> 1;
+          if (sm.pre[mid] <= f) lo = mid;
           else hi = mid - 1;
         }
-        const int32_t uu = s_u[lo];
-        v = __ldg(&idx[s_beg[lo] + (f - s_pre[lo])]);
+        const int32_t uu = sm.u[lo];
+        v = __ldg(&idx[sm.beg[lo] + (f - sm.pre[lo])]);
         if (*(volatile int32_t*)&parent[v] == -1) won = atomicCAS(&parent[v], -1, uu) == -1;
       }
       const unsigned mask = __ballot_sync(0xffffffffu, won);
-      long long od = won ? (long long)__ldg(&outdeg[v]) : 0;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) od += __shfl_xor_sync(0xffffffffu, od, o);
       if (mask) {
+        long long od = won ? (long long)__ldg(&outdeg[v]) : 0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) od += __shfl_xor_sync(0xffffffffu, od, o);
         long long pos = 0;
         if (lane == 0) {
           pos = atomicAdd((unsigned long long*)&cnext[0], (unsigned long long)__popc(mask));
@@ -97,6 +105,53 @@ __global__ void __launch_bounds__(256) k_bfs_push(const int32_t* __restrict__ q,
       }
     }
     __syncthreads();
+  }
+}
+
+template <typename OffT>
+__global__ void __launch_bounds__(256) k_bfs_push(const int32_t* __restrict__ q, int64_t qlen,
+                                                  const OffT* __restrict__ off, const int32_t* __restrict__ idx,
+                                                  const int32_t* __restrict__ outdeg, int32_t* parent,
+                                                  int32_t* __restrict__ qnext, int64_t* __restrict__ cnext) {
+  __shared__ PushSmem sm;
+  push_chunks<OffT>(q, qlen, off, idx, outdeg, parent, qnext, cnext, sm);
+}
+
+// Persistent small-frontier BFS (cooperative launch): runs consecutive push
+// levels with a grid-wide barrier instead of a host round trip per level,
+// until the frontier empties, the direction rule picks pull, or the frontier's
+// edge count exceeds `small_max` (then the host continues with the level
+// kernels). High-diameter graphs (config 3: thousands of tiny levels)
+// spend their whole traversal here. state[0] = level, state[1] = current queue.
+template <typename OffT>
+__global__ void __launch_bounds__(256) k_bfs_persist(const OffT* __restrict__ off, const int32_t* __restrict__ idx,
+                                                     const int32_t* __restrict__ outdeg, int32_t* parent,
+                                                     int32_t* q0, int32_t* q1, int64_t* cnt, int64_t* state,
+                                                     int64_t m_div, int64_t small_max, int policy) {
+  __shared__ PushSmem sm;
+  cg::grid_group grid = cg::this_grid();
+  int64_t level = state[0];
+  int qc = (int)state[1];
+  for (;;) {
+    const int64_t* cur = cnt + 2 * (level % kRing);
+    const int64_t nf = *(volatile const int64_t*)&cur[0];
+    const int64_t sdeg = *(volatile const int64_t*)&cur[1];
+    if (nf == 0) break;
+    const bool pull = policy == GI_BFS_PULL_ONLY ? level > 0 : (policy == GI_BFS_AUTO && nf + sdeg > m_div);
+    if (pull || sdeg > small_max) break;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {  // slot for level + 2 (its old contents are two levels stale)
+      int64_t* z = cnt + 2 * ((level + 2) % kRing);
+      z[0] = 0;
+      z[1] = 0;
+    }
+    push_chunks<OffT>(qc ? q1 : q0, nf, off, idx, outdeg, parent, qc ? q0 : q1, cnt + 2 * ((level + 1) % kRing), sm);
+    grid.sync();
+    ++level;
+    qc ^= 1;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    state[0] = level;
+    state[1] = qc;
   }
 }
 
@@ -273,7 +328,7 @@ static gi_status bfs_impl(gi_graph g, int32_t source, const gi_bfs_opts& o, int3
       GI_TRY(g->queue[k].alloc(n * sizeof(int32_t)));
       GI_TRY(g->bitmap[k].alloc(words * sizeof(uint32_t)));
     }
-    GI_TRY(g->counters.alloc((2 * kRing + 4) * sizeof(int64_t)));
+    GI_TRY(g->counters.alloc((2 * kRing + 8) * sizeof(int64_t)));
     GI_TRY(g->bfs_pre.alloc((n + 1) * sizeof(long long)));
     size_t tb = 0;
     cub::TransformInputIterator<long long, FrontierDegree, cub::CountingInputIterator<int64_t>> it(
@@ -297,13 +352,21 @@ static gi_status bfs_impl(gi_graph g, int32_t source, const gi_bfs_opts& o, int3
     GI_CUDA(cudaEventRecord(e0, st));
   }
   GI_CUDA(cudaMemsetAsync(parent, 0xFF, n * sizeof(int32_t), st));
-  GI_CUDA(cudaMemsetAsync(cnt, 0, (2 * kRing + 4) * sizeof(int64_t), st));
+  GI_CUDA(cudaMemsetAsync(cnt, 0, (2 * kRing + 8) * sizeof(int64_t), st));
   k_bfs_init<<<1, 1, 0, st>>>(source, g->relabeled ? g->inv.as<int32_t>() : nullptr, outdeg, parent,
                               g->queue[0].as<int32_t>(), cnt);
   S.launches = 1;
   int qc = 0, bc = 0;     // current queue / bitmap buffers
   bool in_bitmap = false;  // representation of the current frontier
-  for (int64_t level = 0;; ++level) {
+  int64_t* state = cnt + 2 * kRing + 4;  // [level, current queue] for k_bfs_persist
+  static int persist_grid[2] = {0, 0};
+  const int pk = sizeof(OffT) == 8;
+  if (!persist_grid[pk]) {
+    int bpm = 0;
+    GI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bpm, k_bfs_persist<OffT>, 256, 0));
+    persist_grid[pk] = bpm > 0 ? sms : -1;
+  }
+  for (int64_t level = 0;;) {
     int64_t* cur = cnt + 2 * (level % kRing);
     int64_t* nxt = cnt + 2 * ((level + 1) % kRing);
     GI_CUDA(cudaMemcpyAsync(h, cur, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
@@ -315,6 +378,27 @@ static gi_status bfs_impl(gi_graph g, int32_t source, const gi_bfs_opts& o, int3
     else if (o.policy == GI_BFS_PULL_ONLY) pull = level > 0;
     else pull = (nf + sdeg) > m / div;
     GI_CUDA(cudaMemsetAsync(nxt, 0, 2 * sizeof(int64_t), st));
+    if (!pull && !in_bitmap && sdeg <= kPersistMax && persist_grid[pk] > 0) {
+      // run as many small push levels as possible on the device
+      h[2] = level;
+      h[3] = qc;
+      GI_CUDA(cudaMemcpyAsync(state, h + 2, 2 * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+      const int32_t* cidx = g->csr_idx.as<int32_t>();
+      int32_t* q0p = g->queue[0].as<int32_t>();
+      int32_t* q1p = g->queue[1].as<int32_t>();
+      int64_t mdiv = m / div, smax = kPersistMax;
+      int pol = o.policy;
+      void* args[] = {(void*)&csr_off, (void*)&cidx, (void*)&outdeg, (void*)&parent, (void*)&q0p, (void*)&q1p,
+                      (void*)&cnt, (void*)&state, (void*)&mdiv, (void*)&smax, (void*)&pol};
+      GI_CUDA(cudaLaunchCooperativeKernel((void*)k_bfs_persist<OffT>, dim3(persist_grid[pk]), dim3(256), args, 0, st));
+      GI_CUDA(cudaMemcpyAsync(h + 2, state, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+      GI_CUDA(cudaStreamSynchronize(st));
+      S.levels += (int32_t)(h[2] - level);
+      S.launches++;
+      level = h[2];
+      qc = (int)h[3];
+      continue;
+    }
     if (pull) {
       if (!in_bitmap) {
         GI_CUDA(cudaMemsetAsync(g->bitmap[bc].p, 0, words * sizeof(uint32_t), st));
@@ -356,6 +440,7 @@ static gi_status bfs_impl(gi_graph g, int32_t source, const gi_bfs_opts& o, int3
     GI_CUDA(cudaGetLastError());
     S.launches++;
     S.levels++;
+    ++level;
   }
   GI_CUDA(cudaMemsetAsync(aux + 1, 0, 2 * sizeof(unsigned long long), st));
   k_bfs_finish<<<grid_for(n, 256, sms), 256, 0, st>>>(parent, n, g->relabeled ? g->perm.as<int32_t>() : nullptr,

@@ -32,7 +32,7 @@
 namespace gi {
 namespace {
 
-constexpr int kSegThreads = 512;
+constexpr int kSegThreads = 1024;
 
 // ---------------------------------------------------------------- chunked segment kernel
 // Chunked layout (built below from the piece layout): every piece is cut into
