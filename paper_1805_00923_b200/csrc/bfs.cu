@@ -364,7 +364,7 @@ static gi_status bfs_impl(gi_graph g, int32_t source, const gi_bfs_opts& o, int3
   if (!persist_grid[pk]) {
     int bpm = 0;
     GI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bpm, k_bfs_persist<OffT>, 256, 0));
-    persist_grid[pk] = bpm > 0 ? sms : -1;
+    persist_grid[pk] = bpm > 0 ? std::min(sms, 64) : -1;  // few CTAs: cheap grid barrier
   }
   for (int64_t level = 0;;) {
     int64_t* cur = cnt + 2 * (level % kRing);

@@ -111,6 +111,7 @@ struct gi_graph_s {
   gi::DevBuf seg_pstart;                    // OffT[n+1]: first destination-major piece of v
   gi::DevBuf seg_cidx, seg_cslot;           // chunks: 4 x uint16 source ids, slot | last-chunk bit
   gi::DevBuf seg_tiles;                     // int32[T]: segment of each tile
+  gi::DevBuf seg_cta_tiles;                 // int32[C+1]: cost-balanced tile range of each CTA
   gi::DevBuf seg_partial;                   // float[P+1]: per-piece partial sums (+1 dummy)
   gi::DevBuf seg_carry_slot, seg_carry_val; // per CTA: piece cut by the CTA's range end
   gi::DevBuf out_stage;   // float/int32[n]: output staging in input ids

@@ -40,17 +40,19 @@ constexpr int kSegThreads = 1024;
 // shared-memory zero). chunk c holds 4 uint16 source ids (8 bytes) and
 // cslot[c] = the piece's destination-major slot, bit 31 set on the piece's
 // last chunk. Each segment's chunk list is padded to whole tiles (kTileCh
-// chunks), so every tile lies in one segment and all tiles cost the same;
-// CTA c processes tiles [c*T/C, (c+1)*T/C).
+// chunks), so every tile lies in one segment. CTA c processes the contiguous
+// tile range [cta_tiles[c], cta_tiles[c+1]), cut so that every CTA carries the
+// same modelled cost (chunks + kTailCost x pieces ending in its tiles).
 constexpr int kChunkE = 4;
 constexpr int kCPT = 4;                          // chunks per thread per tile
-constexpr int kTileCh = kSegThreads * kCPT;      // chunks per tile (8192 edge slots)
+constexpr int kTileCh = kSegThreads * kCPT;      // chunks per tile
+constexpr int kTailCost = 2;                     // cost of a piece completion, in chunks
 
 struct SegArgs {
   const uint4* __restrict__ cidx;   // 2 chunks per uint4
   const int4* __restrict__ cslot;   // 4 chunks per int4
   const int32_t* __restrict__ tile_seg;
-  int64_t ntiles;
+  const int32_t* __restrict__ cta_tiles;  // CTA c: tiles [cta_tiles[c], cta_tiles[c+1])
   const float* __restrict__ cin;    // padded to a multiple of 4 floats
   float* __restrict__ partial;
   int32_t* __restrict__ carry_slot; // per CTA: piece still open at the CTA's end (-1: none)
@@ -107,7 +109,7 @@ __global__ void __launch_bounds__(kSegThreads, 1) k_pr_seg(SegArgs A) {
   __shared__ float s_carry_val;
   __shared__ __align__(8) uint64_t s_bar;
   const int tid = threadIdx.x;
-  const int64_t ta = A.ntiles * blockIdx.x / gridDim.x, tb = A.ntiles * (blockIdx.x + 1) / gridDim.x;
+  const int64_t ta = A.cta_tiles[blockIdx.x], tb = A.cta_tiles[blockIdx.x + 1];
   if (ta >= tb) {
     if (tid == 0) A.carry_slot[blockIdx.x] = -1;
     return;
@@ -207,22 +209,50 @@ __global__ void k_fold_carries(const int32_t* __restrict__ slot, const float* __
 template <typename OffT>
 __global__ void __launch_bounds__(256) k_pr_merge(PrArgs A, const OffT* __restrict__ pstart,
                                                   const float* __restrict__ partial) {
+  // Each thread finishes kV vertices spaced blockDim apart, issuing all their
+  // loads before consuming any (independent chains: pstart -> partial, outdeg).
+  constexpr int kV = 4;
   __shared__ double sred[32];
   if (blockIdx.x == 0 && threadIdx.x == 0) A.dbuf[(A.it + 2) % 3] = 0.0;
   const double D = A.uniform ? A.dbuf[A.it % 3] : 0.0;
   const float dn = (float)(D * A.inv_n);
   double dpart = 0.0;
-  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < A.n; v += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t a = pstart[v], b = pstart[v + 1];
-    float s = 0.f;
-    if (b - a == 1) {
-      s = __ldg(&partial[a]);
-    } else {
-      double ds = 0.0;
-      for (int64_t j = a; j < b; ++j) ds += (double)__ldg(&partial[j]);
-      s = (float)ds;
+  const int64_t span = (int64_t)blockDim.x * kV;
+  for (int64_t base = (int64_t)blockIdx.x * span; base < A.n; base += (int64_t)gridDim.x * span) {
+    int64_t a[kV], b[kV];
+    int od[kV];
+#pragma unroll
+    for (int k = 0; k < kV; ++k) {
+      const int64_t v = base + threadIdx.x + (int64_t)k * blockDim.x;
+      a[k] = b[k] = 0;
+      od[k] = 0;
+      if (v < A.n) {
+        a[k] = (int64_t)__ldg(&pstart[v]);
+        b[k] = (int64_t)__ldg(&pstart[v + 1]);
+        od[k] = __ldg(&A.outdeg[v]);
+      }
     }
-    pr_epilogue(A, v, s, dn, dpart);
+    float s[kV];
+#pragma unroll
+    for (int k = 0; k < kV; ++k) s[k] = b[k] > a[k] ? __ldg(&partial[a[k]]) : 0.f;
+#pragma unroll
+    for (int k = 0; k < kV; ++k) {
+      if (b[k] - a[k] > 1) {
+        double ds = (double)s[k];
+        for (int64_t j = a[k] + 1; j < b[k]; ++j) ds += (double)__ldg(&partial[j]);
+        s[k] = (float)ds;
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kV; ++k) {
+      const int64_t v = base + threadIdx.x + (int64_t)k * blockDim.x;
+      if (v < A.n) {
+        const float rn = A.base + A.damp * (s[k] + dn);
+        A.cout[v] = od[k] > 0 ? rn / (float)od[k] : 0.f;
+        if (od[k] == 0) dpart += (double)rn;
+        if (A.rank_out) A.rank_out[A.perm ? __ldg(&A.perm[v]) : v] = rn;
+      }
+    }
   }
   const double bs = block_sum(dpart, sred);
   if (threadIdx.x == 0 && bs != 0.0) atomicAdd(&A.dbuf[(A.it + 1) % 3], bs);
@@ -318,6 +348,18 @@ __global__ void k_seg_piece_starts(const OffT* __restrict__ pc_off, int64_t P, c
 __global__ void k_gather_i64(const int64_t* __restrict__ src, const int64_t* __restrict__ at, int k,
                              int64_t* __restrict__ out) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < k; i += gridDim.x * blockDim.x) out[i] = src[at[i]];
+}
+
+// tails[t] = number of pieces ending in tile t (chunks with bit 31 set)
+__global__ void __launch_bounds__(256) k_tile_tails(const int32_t* __restrict__ cslot, int32_t* __restrict__ tails) {
+  __shared__ int cnt;
+  if (threadIdx.x == 0) cnt = 0;
+  __syncthreads();
+  int c = 0;
+  for (int i = threadIdx.x; i < kTileCh; i += blockDim.x) c += cslot[(int64_t)blockIdx.x * kTileCh + i] < 0;
+  atomicAdd(&cnt, c);
+  __syncthreads();
+  if (threadIdx.x == 0) tails[blockIdx.x] = cnt;
 }
 
 __global__ void k_fill_pad(uint16_t* __restrict__ cidx, int32_t* __restrict__ cslot, int64_t C, uint16_t pad_idx,
@@ -467,6 +509,29 @@ static gi_status seg_build_t(gi_graph g, int Z) {
   k_fill_chunks<OffT><<<grid_for(P, 256, sms), 256, 0, st>>>(
       pc_off.as<OffT>(), pc_slot.as<int32_t>(), idx16.as<uint16_t>(), P, cp.as<int64_t>(), seg_p.as<int64_t>(),
       seg_base.as<int64_t>(), S, Z, g->seg_cidx.as<uint16_t>(), g->seg_cslot.as<int32_t>());
+  // cost-balanced CTA ranges over tiles
+  std::vector<int32_t> h_tails(T > 0 ? T : 1, 0);
+  if (T > 0) {
+    DevBuf tails;
+    GI_TRY(tails.alloc(T * sizeof(int32_t)));
+    k_tile_tails<<<(unsigned)T, 256, 0, st>>>(g->seg_cslot.as<int32_t>(), tails.as<int32_t>());
+    GI_CUDA(cudaMemcpyAsync(h_tails.data(), tails.p, T * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    GI_CUDA(cudaStreamSynchronize(st));
+  }
+  std::vector<int32_t> h_cta(sms + 1, 0);
+  {
+    double total = 0;
+    for (int64_t t = 0; t < T; ++t) total += kTileCh + (double)kTailCost * h_tails[t];
+    double acc = 0;
+    int c = 1;
+    for (int64_t t = 0; t < T && c < sms; ++t) {
+      acc += kTileCh + (double)kTailCost * h_tails[t];
+      while (c < sms && acc >= total * c / sms) h_cta[c++] = (int32_t)(t + 1);
+    }
+    for (; c <= sms; ++c) h_cta[c] = (int32_t)T;
+  }
+  GI_TRY(g->seg_cta_tiles.alloc((sms + 1) * sizeof(int32_t)));
+  GI_CUDA(cudaMemcpyAsync(g->seg_cta_tiles.p, h_cta.data(), (sms + 1) * sizeof(int32_t), cudaMemcpyHostToDevice, st));
   GI_TRY(g->seg_partial.alloc((P + 1) * sizeof(float)));
   GI_TRY(g->seg_carry_slot.alloc(sms * sizeof(int32_t)));
   GI_TRY(g->seg_carry_val.alloc(sms * sizeof(float)));
@@ -504,7 +569,7 @@ gi_status seg_edge_pass(gi_graph g, const PrArgs& A) {
   S.cidx = g->seg_cidx.as<uint4>();
   S.cslot = g->seg_cslot.as<int4>();
   S.tile_seg = g->seg_tiles.as<int32_t>();
-  S.ntiles = g->seg_T;
+  S.cta_tiles = g->seg_cta_tiles.as<int32_t>();
   S.cin = A.cin;
   S.partial = g->seg_partial.as<float>();
   S.carry_slot = g->seg_carry_slot.as<int32_t>();
@@ -526,10 +591,10 @@ gi_status seg_edge_pass(gi_graph g, const PrArgs& A) {
 gi_status seg_vertex_pass(gi_graph g, const PrArgs& A) {
   cudaStream_t st = g->ctx->stream;
   if (g->off64)
-    k_pr_merge<int64_t><<<grid_for(g->n, 256, g->ctx->num_sms, 16), 256, 0, st>>>(A, g->seg_pstart.as<int64_t>(),
+    k_pr_merge<int64_t><<<grid_for(ceil_div(g->n, 4), 256, g->ctx->num_sms, 8), 256, 0, st>>>(A, g->seg_pstart.as<int64_t>(),
                                                                                    g->seg_partial.as<float>());
   else
-    k_pr_merge<int32_t><<<grid_for(g->n, 256, g->ctx->num_sms, 16), 256, 0, st>>>(A, g->seg_pstart.as<int32_t>(),
+    k_pr_merge<int32_t><<<grid_for(ceil_div(g->n, 4), 256, g->ctx->num_sms, 8), 256, 0, st>>>(A, g->seg_pstart.as<int32_t>(),
                                                                                    g->seg_partial.as<float>());
   GI_CUDA(cudaGetLastError());
   return GI_OK;
