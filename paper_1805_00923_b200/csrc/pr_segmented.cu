@@ -23,6 +23,8 @@
 //   k_pr_merge r'[v] = (1-d)/n + d (sum of v's partials + D/n), contrib',
 //              dangling mass (fused vertex update, a3).
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cub/cub.cuh>
 #include <vector>
 
@@ -59,7 +61,14 @@ struct SegArgs {
   float* __restrict__ carry_val;
   int64_t n;
   int Z;
+  unsigned long long* timing;  // optional (GI_DEBUG_SEG_TIMING): per CTA [start, end] globaltimer
 };
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -114,6 +123,7 @@ __global__ void __launch_bounds__(kSegThreads, 1) k_pr_seg(SegArgs A) {
     if (tid == 0) A.carry_slot[blockIdx.x] = -1;
     return;
   }
+  if (tid == 0 && A.timing) A.timing[2 * blockIdx.x] = globaltimer();
   if (tid == 0) {
     mbar_init(&s_bar, 1);
     scontrib[A.Z] = 0.f;
@@ -197,6 +207,7 @@ __global__ void __launch_bounds__(kSegThreads, 1) k_pr_seg(SegArgs A) {
       }
     }
   }
+  if (tid == 0 && A.timing) A.timing[2 * blockIdx.x + 1] = globaltimer();
 }
 
 // partial[carry_slot[c]] += carry_val[c]: pieces cut by CTA boundaries
@@ -518,6 +529,12 @@ static gi_status seg_build_t(gi_graph g, int Z) {
     GI_CUDA(cudaMemcpyAsync(h_tails.data(), tails.p, T * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
     GI_CUDA(cudaStreamSynchronize(st));
   }
+  if (const char* dbg = getenv("GI_DEBUG_SEG_TILES")) {  // diagnostics: per-tile segment and piece ends
+    if (FILE* f = fopen(dbg, "w")) {
+      for (int64_t t = 0; t < T; ++t) fprintf(f, "%lld,%d,%d\n", (long long)t, h_tile_seg[t], h_tails[t]);
+      fclose(f);
+    }
+  }
   std::vector<int32_t> h_cta(sms + 1, 0);
   {
     double total = 0;
@@ -582,7 +599,26 @@ gi_status seg_edge_pass(gi_graph g, const PrArgs& A) {
     GI_CUDA(cudaFuncSetAttribute(k_pr_seg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
     attr_set = dyn;
   }
+  static const char* dbg = getenv("GI_DEBUG_SEG_TIMING");  // diagnostics: file to append per-CTA timings to
+  DevBuf tbuf;
+  S.timing = nullptr;
+  if (dbg) {
+    GI_TRY(tbuf.alloc(2 * g->seg_ctas * sizeof(unsigned long long)));
+    S.timing = tbuf.as<unsigned long long>();
+  }
   k_pr_seg<<<g->seg_ctas, kSegThreads, dyn, st>>>(S);
+  if (dbg) {
+    std::vector<unsigned long long> ht(2 * g->seg_ctas);
+    std::vector<int32_t> hc(g->seg_ctas + 1);
+    GI_CUDA(cudaMemcpyAsync(ht.data(), tbuf.p, ht.size() * 8, cudaMemcpyDeviceToHost, st));
+    GI_CUDA(cudaMemcpyAsync(hc.data(), g->seg_cta_tiles.p, hc.size() * 4, cudaMemcpyDeviceToHost, st));
+    GI_CUDA(cudaStreamSynchronize(st));
+    if (FILE* f = fopen(dbg, "a")) {
+      for (int c = 0; c < g->seg_ctas; ++c)
+        fprintf(f, "%d,%d,%d,%llu,%llu\n", c, hc[c], hc[c + 1], ht[2 * c], ht[2 * c + 1]);
+      fclose(f);
+    }
+  }
   k_fold_carries<<<1, 256, 0, st>>>(S.carry_slot, S.carry_val, g->seg_ctas, S.partial);
   GI_CUDA(cudaGetLastError());
   return GI_OK;
