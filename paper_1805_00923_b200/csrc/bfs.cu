@@ -32,7 +32,8 @@ namespace {
 
 constexpr int kRing = 4;  // counter slots ring: slot(l) = cnt + 2*(l % kRing): {|F_l|, sum outdeg F_l}
 constexpr int64_t kBalancedMin = 1 << 15;  // push levels with more frontier edges use k_bfs_push_bal
-constexpr int64_t kPersistMax = 1 << 15;   // push levels with fewer frontier edges run in k_bfs_persist
+constexpr int64_t kPersistMax = 1 << 15;
+constexpr int64_t kStampMin = 1 << 18;      // push levels with more frontier edges use stamp + collect   // push levels with fewer frontier edges run in k_bfs_persist
 
 __global__ void k_bfs_init(int32_t s_in, const int32_t* __restrict__ inv, const int32_t* __restrict__ outdeg,
                            int32_t* __restrict__ parent, int32_t* __restrict__ q, int64_t* __restrict__ cnt) {
@@ -255,6 +256,82 @@ __global__ void __launch_bounds__(256) k_bfs_push_bal(const int32_t* __restrict_
   }
 }
 
+// Large push levels, two phases, no atomics on the vertex data (the dedup of
+// applyModified, done by a stamp instead of a CAS: thousands of
+// frontier edges that reach the same hub would otherwise serialise on one
+// L2 atomic unit).
+//  phase 1 (edge-balanced like k_bfs_push_bal): for frontier edge (u, v)
+//    with parent[v] == -1, stamp cand[v] = (epoch << 32 | u) with a plain
+//    store unless already stamped this epoch — racing writers all write a
+//    valid parent (same level), the last one wins;
+//  phase 2 (k_bfs_collect, vertex order): every v stamped this epoch and still
+//    unvisited takes parent[v] = u and is appended to the next queue.
+template <typename OffT, int EPT>
+__global__ void __launch_bounds__(256) k_bfs_push_stamp(const int32_t* __restrict__ q, int64_t nf,
+                                                        const long long* __restrict__ pre, long long E,
+                                                        const OffT* __restrict__ off, const int32_t* __restrict__ idx,
+                                                        const int32_t* __restrict__ parent,
+                                                        unsigned long long* cand, unsigned epoch) {
+  const long long stride = (long long)gridDim.x * blockDim.x * EPT;
+  for (long long f0 = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * EPT; f0 < E; f0 += stride) {
+    int64_t lo = 0, hi = nf - 1;  // owner of f0: last i with pre[i] <= f0
+    while (lo < hi) {
+      const int64_t mid = (lo + hi + 1) >> 1;
+      if (__ldg(&pre[mid]) <= f0) lo = mid;
+      else hi = mid - 1;
+    }
+    int64_t o = lo;
+#pragma unroll
+    for (int k = 0; k < EPT; ++k) {
+      const long long f = f0 + k;
+      if (f < E) {
+        while (o + 1 < nf && __ldg(&pre[o + 1]) <= f) ++o;
+        const int32_t u = __ldg(&q[o]);
+        const int32_t v = __ldg(&idx[(long long)off[u] + (f - __ldg(&pre[o]))]);
+        if (parent[v] == -1 && (unsigned)(cand[v] >> 32) != epoch)
+          cand[v] = ((unsigned long long)epoch << 32) | (uint32_t)u;
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) k_bfs_collect(const unsigned long long* __restrict__ cand, unsigned epoch,
+                                                     int32_t* __restrict__ parent, const int32_t* __restrict__ outdeg,
+                                                     int64_t n, int32_t* __restrict__ qnext,
+                                                     int64_t* __restrict__ cnext) {
+  const int lane = threadIdx.x & 31;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t vb = blockIdx.x * (int64_t)blockDim.x + threadIdx.x - lane; vb < n; vb += stride) {
+    const int64_t v = vb + lane;
+    bool won = false;
+    int32_t u = -1;
+    if (v < n) {
+      const unsigned long long c = cand[v];
+      if ((unsigned)(c >> 32) == epoch && parent[v] == -1) {
+        won = true;
+        u = (int32_t)(uint32_t)c;
+      }
+    }
+    const unsigned mask = __ballot_sync(0xffffffffu, won);
+    if (mask) {
+      long long od = 0;
+      if (won) {
+        parent[v] = u;
+        od = __ldg(&outdeg[v]);
+      }
+#pragma unroll
+      for (int s = 16; s > 0; s >>= 1) od += __shfl_xor_sync(0xffffffffu, od, s);
+      long long pos = 0;
+      if (lane == 0) {
+        pos = atomicAdd((unsigned long long*)&cnext[0], (unsigned long long)__popc(mask));
+        atomicAdd((unsigned long long*)&cnext[1], (unsigned long long)od);
+      }
+      pos = __shfl_sync(0xffffffffu, pos, 0);
+      if (won) qnext[pos + __popc(mask & ((1u << lane) - 1))] = (int32_t)v;
+    }
+  }
+}
+
 __global__ void k_q2b(const int32_t* __restrict__ q, int64_t qlen, uint32_t* __restrict__ bm) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < qlen; i += (int64_t)gridDim.x * blockDim.x) {
     const int32_t u = q[i];
@@ -425,10 +502,26 @@ static gi_status bfs_impl(gi_graph g, int32_t source, const gi_bfs_opts& o, int3
         GI_CUDA(cub::DeviceScan::ExclusiveSum(g->bfs_scan_tmp.p, tb, it, g->bfs_pre.as<long long>(), nf, st));
         constexpr int EPT = 8;
         const int grid = (int)std::min<int64_t>(ceil_div(sdeg, 256 * EPT), (int64_t)sms * 8);
-        k_bfs_push_bal<OffT, EPT><<<grid, 256, 0, st>>>(g->queue[qc].as<int32_t>(), nf, g->bfs_pre.as<long long>(),
-                                                        sdeg, csr_off, g->csr_idx.as<int32_t>(), outdeg, parent,
-                                                        g->queue[qc ^ 1].as<int32_t>(), nxt);
-        S.launches++;
+        if (sdeg >= kStampMin) {  // two-phase stamp + collect (no atomics on hub destinations)
+          if (!g->bfs_cand.p || ++g->bfs_epoch == 0) {
+            if (!g->bfs_cand.p) GI_TRY(g->bfs_cand.alloc(n * sizeof(unsigned long long)));
+            GI_CUDA(cudaMemsetAsync(g->bfs_cand.p, 0, n * sizeof(unsigned long long), st));
+            g->bfs_epoch = 1;
+          }
+          k_bfs_push_stamp<OffT, EPT><<<grid, 256, 0, st>>>(g->queue[qc].as<int32_t>(), nf,
+                                                            g->bfs_pre.as<long long>(), sdeg, csr_off,
+                                                            g->csr_idx.as<int32_t>(), parent,
+                                                            g->bfs_cand.as<unsigned long long>(), g->bfs_epoch);
+          k_bfs_collect<<<grid_for(n, 256, sms, 8), 256, 0, st>>>(g->bfs_cand.as<unsigned long long>(), g->bfs_epoch,
+                                                                 parent, outdeg, n, g->queue[qc ^ 1].as<int32_t>(),
+                                                                 nxt);
+          S.launches += 2;
+        } else {
+          k_bfs_push_bal<OffT, EPT><<<grid, 256, 0, st>>>(g->queue[qc].as<int32_t>(), nf, g->bfs_pre.as<long long>(),
+                                                          sdeg, csr_off, g->csr_idx.as<int32_t>(), outdeg, parent,
+                                                          g->queue[qc ^ 1].as<int32_t>(), nxt);
+          S.launches++;
+        }
       } else {
         const int grid = (int)std::min<int64_t>(ceil_div(nf, 256), (int64_t)sms * 8);
         k_bfs_push<OffT><<<grid, 256, 0, st>>>(g->queue[qc].as<int32_t>(), nf, csr_off, g->csr_idx.as<int32_t>(),

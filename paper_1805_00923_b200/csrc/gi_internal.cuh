@@ -122,6 +122,8 @@ struct gi_graph_s {
   gi::DevBuf counters;    // int64 slots, see bfs.cu
   gi::DevBuf bfs_pre;     // int64[n+1]: scan of frontier degrees (balanced push)
   gi::DevBuf bfs_scan_tmp;
+  gi::DevBuf bfs_cand;    // uint64[n]: (epoch << 32 | parent candidate), stamp + collect push
+  unsigned bfs_epoch = 0;
 };
 
 namespace gi {

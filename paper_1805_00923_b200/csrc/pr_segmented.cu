@@ -34,7 +34,7 @@
 namespace gi {
 namespace {
 
-constexpr int kSegThreads = 1024;
+constexpr int kSegThreads = 512;
 
 // ---------------------------------------------------------------- chunked segment kernel
 // Chunked layout (built below from the piece layout): every piece is cut into
@@ -48,7 +48,7 @@ constexpr int kSegThreads = 1024;
 constexpr int kChunkE = 4;
 constexpr int kCPT = 4;                          // chunks per thread per tile
 constexpr int kTileCh = kSegThreads * kCPT;      // chunks per tile
-constexpr int kTailCost = 2;                     // cost of a piece completion, in chunks
+constexpr int kTailCost = 0;                     // cost of a piece completion, in chunks (measured ~0)
 
 struct SegArgs {
   const uint4* __restrict__ cidx;   // 2 chunks per uint4
@@ -140,20 +140,21 @@ __global__ void __launch_bounds__(kSegThreads, 1) k_pr_seg(SegArgs A) {
   if (tid == 0) load_segment(cur_seg);
   uint32_t parity = 0;
   bool pending = true;
-  // prefetch registers: 4 chunks = 2 x uint4 of indices + 1 x int4 of slots
-  const int64_t c0 = ta * kTileCh + (int64_t)tid * kCPT;
-  uint4 pa = __ldg(&A.cidx[c0 / 2]), pb = __ldg(&A.cidx[c0 / 2 + 1]);
-  int4 ps = __ldg(&A.cslot[c0 / 4]);
-  for (int64_t t = ta; t < tb; ++t) {
+  // Register prefetch two tiles ahead (two register sets, the loop unrolled by
+  // two so each set stays in place): 4 chunks = 2 x uint4 indices + 1 x int4 slots.
+  auto fetch = [&](int64_t t, uint4& a, uint4& b, int4& sl) {
+    if (t < tb) {
+      const int64_t c = t * kTileCh + (int64_t)tid * kCPT;
+      a = __ldg(&A.cidx[c / 2]);
+      b = __ldg(&A.cidx[c / 2 + 1]);
+      sl = __ldg(&A.cslot[c / 4]);
+    }
+  };
+  auto tile = [&](int64_t t, uint4& pa, uint4& pb, int4& ps) {
     const uint4 ia = pa, ib = pb;
     const int4 sl = ps;
+    fetch(t + 2, pa, pb, ps);  // in flight during the next two tiles
     const int next_seg = t + 1 < tb ? __ldg(&A.tile_seg[t + 1]) : cur_seg;
-    if (t + 1 < tb) {  // in flight during this tile
-      const int64_t cn = (t + 1) * kTileCh + (int64_t)tid * kCPT;
-      pa = __ldg(&A.cidx[cn / 2]);
-      pb = __ldg(&A.cidx[cn / 2 + 1]);
-      ps = __ldg(&A.cslot[cn / 4]);
-    }
     if (pending) {
       mbar_wait(&s_bar, parity);
       parity ^= 1u;
@@ -206,6 +207,14 @@ __global__ void __launch_bounds__(kSegThreads, 1) k_pr_seg(SegArgs A) {
         A.carry_val[blockIdx.x] = open ? incl.val : 0.f;
       }
     }
+  };
+  uint4 a0 = make_uint4(0, 0, 0, 0), b0 = a0, a1 = a0, b1 = a0;
+  int4 s0 = make_int4(0, 0, 0, 0), s1 = s0;
+  fetch(ta, a0, b0, s0);
+  fetch(ta + 1, a1, b1, s1);
+  for (int64_t t = ta; t < tb; t += 2) {
+    tile(t, a0, b0, s0);
+    if (t + 1 < tb) tile(t + 1, a1, b1, s1);
   }
   if (tid == 0 && A.timing) A.timing[2 * blockIdx.x + 1] = globaltimer();
 }
