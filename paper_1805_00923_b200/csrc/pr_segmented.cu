@@ -48,7 +48,7 @@ constexpr int kSegThreads = 512;
 constexpr int kChunkE = 4;
 constexpr int kCPT = 4;                          // chunks per thread per tile
 constexpr int kTileCh = kSegThreads * kCPT;      // chunks per tile
-constexpr int kTailCost = 0;                     // cost of a piece completion, in chunks (measured ~0)
+constexpr float kTailCost = 0.45f;               // cost of a piece completion, in chunks (fitted from per-CTA timings)
 
 struct SegArgs {
   const uint4* __restrict__ cidx;   // 2 chunks per uint4
@@ -99,8 +99,15 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
-__device__ __forceinline__ float chunk_sum(const float* sc, uint32_t lo, uint32_t hi) {
-  return (sc[lo & 0xFFFFu] + sc[lo >> 16]) + (sc[hi & 0xFFFFu] + sc[hi >> 16]);
+// Sum of one chunk's 4 staged contributions; padding entries (index Z) are
+// skipped (predicated loads: fewer active lanes per shared-memory wavefront).
+__device__ __forceinline__ float chunk_sum(const float* sc, uint32_t lo, uint32_t hi, uint32_t Z) {
+  const uint32_t i0 = lo & 0xFFFFu, i1 = lo >> 16, i2 = hi & 0xFFFFu, i3 = hi >> 16;
+  const float a = sc[i0];
+  const float b = i1 != Z ? sc[i1] : 0.f;
+  const float c = i2 != Z ? sc[i2] : 0.f;
+  const float d = i3 != Z ? sc[i3] : 0.f;
+  return (a + b) + (c + d);
 }
 
 // Per tile: thread t owns chunks [t*kCPT, (t+1)*kCPT) (32 B of indices, 16 B
@@ -118,6 +125,7 @@ __global__ void __launch_bounds__(kSegThreads, 1) k_pr_seg(SegArgs A) {
   __shared__ float s_carry_val;
   __shared__ __align__(8) uint64_t s_bar;
   const int tid = threadIdx.x;
+  const uint32_t zpad = (uint32_t)A.Z;
   const int64_t ta = A.cta_tiles[blockIdx.x], tb = A.cta_tiles[blockIdx.x + 1];
   if (ta >= tb) {
     if (tid == 0) A.carry_slot[blockIdx.x] = -1;
@@ -161,10 +169,10 @@ __global__ void __launch_bounds__(kSegThreads, 1) k_pr_seg(SegArgs A) {
       pending = false;
     }
     float v[kCPT];
-    v[0] = chunk_sum(scontrib, ia.x, ia.y);
-    v[1] = chunk_sum(scontrib, ia.z, ia.w);
-    v[2] = chunk_sum(scontrib, ib.x, ib.y);
-    v[3] = chunk_sum(scontrib, ib.z, ib.w);
+    v[0] = chunk_sum(scontrib, ia.x, ia.y, zpad);
+    v[1] = chunk_sum(scontrib, ia.z, ia.w, zpad);
+    v[2] = chunk_sum(scontrib, ib.x, ib.y, zpad);
+    v[3] = chunk_sum(scontrib, ib.z, ib.w, zpad);
     const int s[kCPT] = {sl.x, sl.y, sl.z, sl.w};
     __syncthreads();  // every read of scontrib for this tile is done
     if (next_seg != cur_seg) {
