@@ -31,7 +31,7 @@ namespace gi {
 namespace {
 
 constexpr int kRing = 4;  // counter slots ring: slot(l) = cnt + 2*(l % kRing): {|F_l|, sum outdeg F_l}
-constexpr int64_t kBalancedMin = 1 << 15;  // push levels with more frontier edges use k_bfs_push_bal
+constexpr int64_t kBalancedMin = 1 << 17;  // push levels with more frontier edges use k_bfs_push_bal
 constexpr int64_t kPersistMax = 1 << 15;
 constexpr int64_t kStampMin = 1 << 18;      // push levels with more frontier edges use stamp + collect   // push levels with fewer frontier edges run in k_bfs_persist
 
@@ -202,10 +202,10 @@ __global__ void __launch_bounds__(256) k_bfs_pull(const uint32_t* __restrict__ f
 // memory (the north_star's "bitmap staged in shared memory"): vertices are
 // relabelled hottest-first, so the first `sw` words (up to ~1.8 M vertices)
 // answer almost every in-neighbour membership test from smem (~7 random
-// reads / SM-clock measured) instead of L2 (~1). One CTA per SM, grid-stride
+// reads / SM-clock measured) instead of L2 (~1). Two CTAs per SM, grid-stride
 // over output words; each warp owns one word (32 vertices, ballot write).
 template <typename OffT>
-__global__ void __launch_bounds__(1024, 1) k_bfs_pull_smem(const uint32_t* __restrict__ fcur,
+__global__ void __launch_bounds__(1024, 2) k_bfs_pull_smem(const uint32_t* __restrict__ fcur,
                                                            uint32_t* __restrict__ fnext, int32_t* __restrict__ parent,
                                                            const OffT* __restrict__ off,
                                                            const int32_t* __restrict__ idx,
@@ -224,14 +224,22 @@ __global__ void __launch_bounds__(1024, 1) k_bfs_pull_smem(const uint32_t* __res
     const int64_t v = (w << 5) + lane;
     bool found = false;
     if (v < n && parent[v] == -1) {
+      // probe 4 in-edges per step (independent loads; rows are sorted by
+      // source id = hottest first, so most vertices stop in the first step)
       const int64_t e1 = (int64_t)off[v + 1];
-      for (int64_t e = (int64_t)off[v]; e < e1; ++e) {
-        const uint32_t u = (uint32_t)__ldg(&idx[e]);
-        const uint32_t word = u < lim ? sbits[u >> 5] : __ldg(&fcur[u >> 5]);
-        if ((word >> (u & 31)) & 1u) {
-          parent[v] = (int32_t)u;
-          found = true;
-          break;
+      for (int64_t e = (int64_t)off[v]; e < e1 && !found; e += 4) {
+        uint32_t u[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) u[k] = e + k < e1 ? (uint32_t)__ldg(&idx[e + k]) : 0xffffffffu;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          if (!found && u[k] != 0xffffffffu) {
+            const uint32_t word = u[k] < lim ? sbits[u[k] >> 5] : __ldg(&fcur[u[k] >> 5]);
+            if ((word >> (u[k] & 31)) & 1u) {
+              parent[v] = (int32_t)u[k];
+              found = true;
+            }
+          }
         }
       }
     }
@@ -350,40 +358,59 @@ __global__ void __launch_bounds__(256) k_bfs_push_stamp(const int32_t* __restric
   }
 }
 
+// Phase 2 of the stamped push: vertex order, CTA chunks of 2048 vertices.
+// Winners are appended with ONE atomic per chunk (block scan of per-thread
+// counts; per-warp atomics on a single counter serialised at L2), and the next
+// frontier's bitmap words are written directly from the warp ballots, so a
+// following pull level needs no queue -> bitmap conversion.
 __global__ void __launch_bounds__(256) k_bfs_collect(const unsigned long long* __restrict__ cand, unsigned epoch,
                                                      int32_t* __restrict__ parent, const int32_t* __restrict__ outdeg,
                                                      int64_t n, int32_t* __restrict__ qnext,
-                                                     int64_t* __restrict__ cnext) {
-  const int lane = threadIdx.x & 31;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t vb = blockIdx.x * (int64_t)blockDim.x + threadIdx.x - lane; vb < n; vb += stride) {
-    const int64_t v = vb + lane;
-    bool won = false;
-    int32_t u = -1;
-    if (v < n) {
-      const unsigned long long c = cand[v];
-      if ((unsigned)(c >> 32) == epoch && parent[v] == -1) {
-        won = true;
-        u = (int32_t)(uint32_t)c;
-      }
-    }
-    const unsigned mask = __ballot_sync(0xffffffffu, won);
-    if (mask) {
-      long long od = 0;
-      if (won) {
-        parent[v] = u;
-        od = __ldg(&outdeg[v]);
-      }
+                                                     uint32_t* __restrict__ bnext, int64_t* __restrict__ cnext) {
+  constexpr int NT = 256, K = 8, CH = NT * K;
+  using Scan = cub::BlockScan<int, NT>;
+  using Red = cub::BlockReduce<long long, NT>;
+  __shared__ typename Scan::TempStorage scan_tmp;
+  __shared__ typename Red::TempStorage red_tmp;
+  __shared__ long long s_base;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int64_t nchunks = (n + CH - 1) / CH;
+  for (int64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+    unsigned won = 0;  // bit k: vertex ch*CH + k*NT + tid claimed
+    int32_t par[K];
+    long long od = 0;
 #pragma unroll
-      for (int s = 16; s > 0; s >>= 1) od += __shfl_xor_sync(0xffffffffu, od, s);
-      long long pos = 0;
-      if (lane == 0) {
-        pos = atomicAdd((unsigned long long*)&cnext[0], (unsigned long long)__popc(mask));
-        atomicAdd((unsigned long long*)&cnext[1], (unsigned long long)od);
+    for (int k = 0; k < K; ++k) {
+      const int64_t v = ch * CH + (int64_t)k * NT + tid;
+      bool w = false;
+      par[k] = -1;
+      if (v < n) {
+        const unsigned long long c = cand[v];
+        if ((unsigned)(c >> 32) == epoch && parent[v] == -1) {
+          w = true;
+          par[k] = (int32_t)(uint32_t)c;
+          parent[v] = par[k];
+          od += __ldg(&outdeg[v]);
+        }
       }
-      pos = __shfl_sync(0xffffffffu, pos, 0);
-      if (won) qnext[pos + __popc(mask & ((1u << lane) - 1))] = (int32_t)v;
+      const unsigned mask = __ballot_sync(0xffffffffu, w);
+      if (lane == 0 && ((ch * CH + (int64_t)k * NT + tid) >> 5) < ((n + 31) >> 5))
+        bnext[(ch * CH + (int64_t)k * NT + tid) >> 5] = mask;
+      won |= (unsigned)w << k;
     }
+    int cnt = __popc(won), pre = 0, total = 0;
+    Scan(scan_tmp).ExclusiveSum(cnt, pre, total);
+    const long long dsum = Red(red_tmp).Sum(od);
+    if (tid == 0) {
+      s_base = total ? (long long)atomicAdd((unsigned long long*)&cnext[0], (unsigned long long)total) : 0;
+      if (dsum) atomicAdd((unsigned long long*)&cnext[1], (unsigned long long)dsum);
+    }
+    __syncthreads();
+    long long pos = s_base + pre;
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+      if ((won >> k) & 1u) qnext[pos++] = (int32_t)(ch * CH + (int64_t)k * NT + tid);
+    __syncthreads();
   }
 }
 
@@ -490,6 +517,7 @@ static gi_status bfs_impl(gi_graph g, int32_t source, const gi_bfs_opts& o, int3
   S.launches = 1;
   int qc = 0, bc = 0;     // current queue / bitmap buffers
   bool in_bitmap = false;  // representation of the current frontier
+  bool bitmap_ready = false;  // bitmap[bc] also holds the current frontier (written by k_bfs_collect)
   int64_t* state = cnt + 2 * kRing + 4;  // [level, current queue] for k_bfs_persist
   static int persist_grid[2] = {0, 0};
   const int pk = sizeof(OffT) == 8;
@@ -529,10 +557,12 @@ static gi_status bfs_impl(gi_graph g, int32_t source, const gi_bfs_opts& o, int3
       S.launches++;
       level = h[2];
       qc = (int)h[3];
+      bitmap_ready = false;
       continue;
     }
+    bool next_bitmap_ready = false;
     if (pull) {
-      if (!in_bitmap) {
+      if (!in_bitmap && !bitmap_ready) {
         GI_CUDA(cudaMemsetAsync(g->bitmap[bc].p, 0, words * sizeof(uint32_t), st));
         k_q2b<<<grid_for(nf, 256, sms), 256, 0, st>>>(g->queue[qc].as<int32_t>(), nf, g->bitmap[bc].as<uint32_t>());
         S.launches++;
@@ -542,14 +572,16 @@ static gi_status bfs_impl(gi_graph g, int32_t source, const gi_bfs_opts& o, int3
         if (smem_words < 0) {
           int optin = 0;
           GI_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
-          smem_words = (optin - 2048) / 4;
+          int per_sm = 0;
+          GI_CUDA(cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, ctx->device));
+          smem_words = std::min(optin - 2048, per_sm / 2 - 2048) / 4;  // two CTAs per SM
           GI_CUDA(cudaFuncSetAttribute(k_bfs_pull_smem<int32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        smem_words * 4));
           GI_CUDA(cudaFuncSetAttribute(k_bfs_pull_smem<int64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        smem_words * 4));
         }
         const int sw = (int)std::min<int64_t>(words, smem_words);
-        k_bfs_pull_smem<OffT><<<sms, 1024, (size_t)sw * 4, st>>>(g->bitmap[bc].as<uint32_t>(),
+        k_bfs_pull_smem<OffT><<<2 * sms, 1024, (size_t)sw * 4, st>>>(g->bitmap[bc].as<uint32_t>(),
                                                                  g->bitmap[bc ^ 1].as<uint32_t>(), parent, csc_off,
                                                                  g->csc_idx.as<int32_t>(), outdeg, n, sw, nxt);
       }
@@ -580,9 +612,10 @@ static gi_status bfs_impl(gi_graph g, int32_t source, const gi_bfs_opts& o, int3
                                                             g->bfs_pre.as<long long>(), sdeg, csr_off,
                                                             g->csr_idx.as<int32_t>(), parent,
                                                             g->bfs_cand.as<unsigned long long>(), g->bfs_epoch);
-          k_bfs_collect<<<grid_for(n, 256, sms, 8), 256, 0, st>>>(g->bfs_cand.as<unsigned long long>(), g->bfs_epoch,
-                                                                 parent, outdeg, n, g->queue[qc ^ 1].as<int32_t>(),
-                                                                 nxt);
+          k_bfs_collect<<<grid_for(ceil_div(n, 2048), 1, sms, 8), 256, 0, st>>>(
+              g->bfs_cand.as<unsigned long long>(), g->bfs_epoch, parent, outdeg, n, g->queue[qc ^ 1].as<int32_t>(),
+              g->bitmap[bc].as<uint32_t>(), nxt);
+          next_bitmap_ready = true;  // bitmap[bc] now holds the next frontier too
           S.launches += 2;
         } else {
           k_bfs_push_bal<OffT, EPT><<<grid, 256, 0, st>>>(g->queue[qc].as<int32_t>(), nf, g->bfs_pre.as<long long>(),
@@ -602,6 +635,7 @@ static gi_status bfs_impl(gi_graph g, int32_t source, const gi_bfs_opts& o, int3
     S.launches++;
     S.levels++;
     ++level;
+    bitmap_ready = next_bitmap_ready;
   }
   GI_CUDA(cudaMemsetAsync(aux + 1, 0, 2 * sizeof(unsigned long long), st));
   k_bfs_finish<<<grid_for(n, 256, sms), 256, 0, st>>>(parent, n, g->relabeled ? g->perm.as<int32_t>() : nullptr,
