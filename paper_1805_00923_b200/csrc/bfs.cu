@@ -530,7 +530,7 @@ static gi_status bfs_impl(gi_graph g, int32_t source, const gi_bfs_opts& o, int3
     int64_t* cur = cnt + 2 * (level % kRing);
     int64_t* nxt = cnt + 2 * ((level + 1) % kRing);
     GI_CUDA(cudaMemcpyAsync(h, cur, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-    GI_CUDA(cudaStreamSynchronize(st));
+    GI_CUDA(stream_wait(st));
     const int64_t nf = h[0], sdeg = h[1];
     if (nf == 0) break;
     bool pull;
@@ -552,7 +552,7 @@ static gi_status bfs_impl(gi_graph g, int32_t source, const gi_bfs_opts& o, int3
                       (void*)&cnt, (void*)&state, (void*)&mdiv, (void*)&smax, (void*)&pol};
       GI_CUDA(cudaLaunchCooperativeKernel((void*)k_bfs_persist<OffT>, dim3(persist_grid[pk]), dim3(256), args, 0, st));
       GI_CUDA(cudaMemcpyAsync(h + 2, state, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-      GI_CUDA(cudaStreamSynchronize(st));
+      GI_CUDA(stream_wait(st));
       S.levels += (int32_t)(h[2] - level);
       S.launches++;
       level = h[2];

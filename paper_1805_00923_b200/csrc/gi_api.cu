@@ -78,7 +78,7 @@ struct OutBuf {
 };
 
 static gi_status sync(gi_context ctx) {
-  GI_CUDA(cudaStreamSynchronize(ctx->stream));
+  GI_CUDA(stream_wait(ctx->stream));
   GI_CUDA(cudaGetLastError());
   return GI_OK;
 }

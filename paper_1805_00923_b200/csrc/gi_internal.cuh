@@ -141,6 +141,15 @@ gi_status seg_vertex_pass(gi_graph g, const PrArgs& A);
 // bfs.cu
 gi_status bfs_run(gi_graph g, int32_t source_input_id, const gi_bfs_opts& o,
                   int32_t* d_parent_input_ids, gi_bfs_stats* stats);
+// Low-latency wait for the stream: spin on cudaStreamQuery instead of a
+// blocking synchronise (which may yield the thread and add tens of µs of
+// wake-up latency to every BFS level's host round trip).
+inline cudaError_t stream_wait(cudaStream_t st) {
+  cudaError_t e;
+  while ((e = cudaStreamQuery(st)) == cudaErrorNotReady) {
+  }
+  return e;
+}
 // util
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 inline int grid_for(int64_t work, int threads, int num_sms, int per_sm = 8) {

@@ -374,3 +374,39 @@ def test_bfs_errors_and_device_output(gi, ctx):
     out = torch.empty(10, dtype=torch.int32, device="cuda")
     g.bfs(3, out=out)
     assert out.cpu().tolist() == [9, 0, 1, 3, 3, 4, 5, 6, 7, 8]
+
+
+# ---------------------------------------------------------------- full-size configs (BASELINE configs[1], [2])
+@pytest.fixture(scope="module")
+def full_graphs():
+    """Oracle graphs of configs 2 and 3 (built once; ~1 min of host time each)."""
+    return {}
+
+
+@pytest.mark.parametrize("cfg_idx", [2, 3])
+def test_full_config_parity(gi, ctx, full_graphs, cfg_idx):
+    """The bench workload at full size, in the launch configuration bench.py times:
+    PageRank (auto pull kernel) against the full fp64 oracle, and BFS from
+    several sources validated against oracle depths."""
+    cfg = graphgen.CONFIGS[cfg_idx]
+    s, d = cfg.edges()
+    go = oracle.build_graph(cfg.n, s, d)
+    import torch
+
+    g = gi.Graph(ctx, cfg.n, torch.from_numpy(s).cuda(), torch.from_numpy(d).cuda(),
+                 gi.GI_DEFAULT_FLAGS | gi.GI_EDGES_ON_DEVICE)
+    assert g.m == go.m
+    out = torch.empty(cfg.n, dtype=torch.float32, device="cuda")
+    _, st = g.pagerank(cfg.pr_iters, cfg.damping, out=out)
+    want = oracle.pagerank(go, cfg.pr_iters, cfg.damping)
+    got = out.cpu().numpy()
+    _pr_check(got, want, cfg.name)
+    assert abs(got.astype(np.float64).sum() - 1.0) < 1e-5  # mass conserved (uniform rule)
+    sources = cfg.sources(s, d)[:4].tolist() if cfg.source_seed else [0]
+    par = torch.empty(cfg.n, dtype=torch.int32, device="cuda")
+    for src in sources:
+        _, bs = g.bfs(int(src), out=par)
+        depth = oracle.bfs_depth(go, int(src))
+        ok, msg = oracle.validate_bfs(go, int(src), par.cpu().numpy(), depth)
+        assert ok, f"{cfg.name} src={src}: {msg}"
+        assert bs.edges_traversed == oracle.reached_out_edges(go, depth)
