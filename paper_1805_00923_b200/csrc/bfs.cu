@@ -20,6 +20,9 @@
 //  conversion: queue -> bitmap (atomicOr per id);
 //    bitmap -> queue (popc + warp scan + one atomicAdd per warp).
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cooperative_groups.h>
 #include <cub/cub.cuh>
 
@@ -526,12 +529,20 @@ static gi_status bfs_impl(gi_graph g, int32_t source, const gi_bfs_opts& o, int3
     GI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bpm, k_bfs_persist<OffT>, 256, 0));
     persist_grid[pk] = bpm > 0 ? std::min(sms, 64) : -1;  // few CTAs: cheap grid barrier
   }
+  static const char* dbg = getenv("GI_DEBUG_BFS");  // diagnostics: per-level host timeline
+  FILE* dbgf = dbg ? fopen(dbg, "a") : nullptr;
+  auto now_us = [] {
+    return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
+  };
+  const double t_begin = now_us();
   for (int64_t level = 0;;) {
     int64_t* cur = cnt + 2 * (level % kRing);
     int64_t* nxt = cnt + 2 * ((level + 1) % kRing);
     GI_CUDA(cudaMemcpyAsync(h, cur, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
     GI_CUDA(stream_wait(st));
     const int64_t nf = h[0], sdeg = h[1];
+    if (dbgf) fprintf(dbgf, "src=%d level=%lld nf=%lld sdeg=%lld t=%.1f\n", source, (long long)level, (long long)nf,
+                      (long long)sdeg, now_us() - t_begin);
     if (nf == 0) break;
     bool pull;
     if (o.policy == GI_BFS_PUSH_ONLY) pull = false;
@@ -637,6 +648,7 @@ static gi_status bfs_impl(gi_graph g, int32_t source, const gi_bfs_opts& o, int3
     ++level;
     bitmap_ready = next_bitmap_ready;
   }
+  if (dbgf) fclose(dbgf);
   GI_CUDA(cudaMemsetAsync(aux + 1, 0, 2 * sizeof(unsigned long long), st));
   k_bfs_finish<<<grid_for(n, 256, sms), 256, 0, st>>>(parent, n, g->relabeled ? g->perm.as<int32_t>() : nullptr,
                                                       outdeg, d_out, aux + 1);
