@@ -112,13 +112,92 @@ __device__ __forceinline__ void push_chunks(const int32_t* __restrict__ q, int64
   }
 }
 
+// Small frontiers (nf <= kSmallF): every CTA of the grid scans the whole
+// frontier's degrees in shared memory (cheap, redundant) and then walks an
+// equal slice of the flattened edge list, so a frontier of a few hubs is
+// spread over the whole grid instead of landing on one CTA.
+constexpr int kSmallF = 4096;
+struct SmallSmem {
+  cub::BlockScan<int, 256>::TempStorage scan;
+  int pre[kSmallF + 1];  // inclusive scan of degrees, pre[0] = 0
+  int32_t u[kSmallF];
+};
+
+template <typename OffT>
+__device__ __forceinline__ void push_small(const int32_t* __restrict__ q, int nf, const OffT* __restrict__ off,
+                                           const int32_t* __restrict__ idx, const int32_t* __restrict__ outdeg,
+                                           int32_t* parent, int32_t* __restrict__ qnext, int64_t* cnext,
+                                           SmallSmem& sm) {
+  constexpr int NT = 256, PT = kSmallF / NT;  // 16 frontier entries per thread
+  const int tid = threadIdx.x, lane = tid & 31;
+  int d[PT];
+  int run = 0;
+#pragma unroll
+  for (int k = 0; k < PT; ++k) {  // thread t owns entries [t*PT, (t+1)*PT)
+    const int i = tid * PT + k;
+    d[k] = 0;
+    if (i < nf) {
+      const int32_t u = q[i];
+      sm.u[i] = u;
+      d[k] = (int)(off[u + 1] - off[u]);
+    }
+    run += d[k];
+  }
+  int excl, total;
+  cub::BlockScan<int, NT>(sm.scan).ExclusiveSum(run, excl, total);
+#pragma unroll
+  for (int k = 0; k < PT; ++k) {
+    const int i = tid * PT + k;
+    if (i < nf) sm.pre[i] = excl;
+    excl += d[k];
+  }
+  if (tid == 0) sm.pre[nf] = total;
+  __syncthreads();
+  const long long E = total;
+  const long long lo = E * blockIdx.x / gridDim.x, hi = E * (blockIdx.x + 1) / gridDim.x;
+  for (long long base = lo; base < hi; base += NT) {
+    const long long f = base + tid;
+    bool won = false;
+    int32_t v = 0;
+    if (f < hi) {
+      int a = 0, b = nf - 1;  // owner = last i with pre[i] <= f
+      while (a < b) {
+        const int mid = (a + b + 1) >> 1;
+        if (sm.pre[mid] <= f) a = mid;
+        else b = mid - 1;
+      }
+      const int32_t uu = sm.u[a];
+      v = __ldg(&idx[(long long)off[uu] + (f - sm.pre[a])]);
+      if (*(volatile int32_t*)&parent[v] == -1) won = atomicCAS(&parent[v], -1, uu) == -1;
+    }
+    const unsigned mask = __ballot_sync(0xffffffffu, won);
+    if (mask) {
+      long long od = won ? (long long)__ldg(&outdeg[v]) : 0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) od += __shfl_xor_sync(0xffffffffu, od, o);
+      long long pos = 0;
+      if (lane == 0) {
+        pos = atomicAdd((unsigned long long*)&cnext[0], (unsigned long long)__popc(mask));
+        atomicAdd((unsigned long long*)&cnext[1], (unsigned long long)od);
+      }
+      pos = __shfl_sync(0xffffffffu, pos, 0);
+      if (won) qnext[pos + __popc(mask & ((1u << lane) - 1))] = v;
+    }
+  }
+  __syncthreads();
+}
+
 template <typename OffT>
 __global__ void __launch_bounds__(256) k_bfs_push(const int32_t* __restrict__ q, int64_t qlen,
                                                   const OffT* __restrict__ off, const int32_t* __restrict__ idx,
                                                   const int32_t* __restrict__ outdeg, int32_t* parent,
-                                                  int32_t* __restrict__ qnext, int64_t* __restrict__ cnext) {
-  __shared__ PushSmem sm;
-  push_chunks<OffT>(q, qlen, off, idx, outdeg, parent, qnext, cnext, sm);
+                                                  int32_t* __restrict__ qnext, int64_t* __restrict__ cnext, int small) {
+  __shared__ union {
+    PushSmem chunks;
+    SmallSmem small;
+  } sm;
+  if (small) push_small<OffT>(q, (int)qlen, off, idx, outdeg, parent, qnext, cnext, sm.small);
+  else push_chunks<OffT>(q, qlen, off, idx, outdeg, parent, qnext, cnext, sm.chunks);
 }
 
 // Persistent small-frontier BFS (cooperative launch): runs consecutive push
@@ -132,7 +211,10 @@ __global__ void __launch_bounds__(256) k_bfs_persist(const OffT* __restrict__ of
                                                      const int32_t* __restrict__ outdeg, int32_t* parent,
                                                      int32_t* q0, int32_t* q1, int64_t* cnt, int64_t* state,
                                                      int64_t m_div, int64_t small_max, int policy) {
-  __shared__ PushSmem sm;
+  __shared__ union {
+    PushSmem chunks;
+    SmallSmem small;
+  } sm;
   cg::grid_group grid = cg::this_grid();
   int64_t level = state[0];
   int qc = (int)state[1];
@@ -148,7 +230,12 @@ __global__ void __launch_bounds__(256) k_bfs_persist(const OffT* __restrict__ of
       z[0] = 0;
       z[1] = 0;
     }
-    push_chunks<OffT>(qc ? q1 : q0, nf, off, idx, outdeg, parent, qc ? q0 : q1, cnt + 2 * ((level + 1) % kRing), sm);
+    if (nf <= kSmallF && sdeg < INT32_MAX)
+      push_small<OffT>(qc ? q1 : q0, (int)nf, off, idx, outdeg, parent, qc ? q0 : q1, cnt + 2 * ((level + 1) % kRing),
+                       sm.small);
+    else
+      push_chunks<OffT>(qc ? q1 : q0, nf, off, idx, outdeg, parent, qc ? q0 : q1, cnt + 2 * ((level + 1) % kRing),
+                        sm.chunks);
     grid.sync();
     ++level;
     qc ^= 1;
@@ -635,9 +722,11 @@ static gi_status bfs_impl(gi_graph g, int32_t source, const gi_bfs_opts& o, int3
           S.launches++;
         }
       } else {
-        const int grid = (int)std::min<int64_t>(ceil_div(nf, 256), (int64_t)sms * 8);
+        const int small = nf <= kSmallF && sdeg < INT32_MAX;
+        const int grid = small ? (int)std::min<int64_t>(std::max<int64_t>(ceil_div(sdeg, 1024), 1), (int64_t)sms * 4)
+                                       : (int)std::min<int64_t>(ceil_div(nf, 256), (int64_t)sms * 8);
         k_bfs_push<OffT><<<grid, 256, 0, st>>>(g->queue[qc].as<int32_t>(), nf, csr_off, g->csr_idx.as<int32_t>(),
-                                               outdeg, parent, g->queue[qc ^ 1].as<int32_t>(), nxt);
+                                               outdeg, parent, g->queue[qc ^ 1].as<int32_t>(), nxt, small);
       }
       qc ^= 1;
       in_bitmap = false;

@@ -1,0 +1,88 @@
+#!/usr/bin/env python3
+"""Summarise an ncu --set full report: per-launch duration, DRAM bytes, throughput.
+
+    python tools/ncu_summary.py gpurun_out/prof_r01.ncu-rep profiles/r01_ncu_summary.md [--json profiles/ncu_summary.json]
+"""
+import csv
+import io
+import json
+import subprocess
+import sys
+
+METRICS = {
+    "gpu__time_duration.sum": "duration_ns",
+    "dram__bytes_read.sum": "dram_read",
+    "dram__bytes_write.sum": "dram_write",
+    "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed": "dram_pct",
+    "sm__throughput.avg.pct_of_peak_sustained_elapsed": "sm_pct",
+    "lts__t_sector_hit_rate.pct": "l2_hit_pct",
+    "sm__warps_active.avg.pct_of_peak_sustained_active": "occupancy_pct",
+    "smsp__issue_active.avg.pct_of_peak_sustained_active": "issue_pct",
+    "launch__registers_per_thread": "regs",
+    "launch__grid_size": "grid",
+    "launch__block_size": "block",
+    "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_ld.sum": "smem_ld_wavefronts",
+}
+UNITS = {"dram_read": {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9},
+         "duration_ns": {"nsecond": 1, "usecond": 1e3, "msecond": 1e6}}
+
+
+def main():
+    rep, out = sys.argv[1], sys.argv[2]
+    js = sys.argv[sys.argv.index("--json") + 1] if "--json" in sys.argv else None
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    hdr, units = rows[0], rows[1]
+    launches = []
+    for r in rows[2:]:
+        d = {"kernel": r[hdr.index("Kernel Name")][:80]}
+        for k, name in METRICS.items():
+            if k in hdr:
+                i = hdr.index(k)
+                try:
+                    v = float(r[i].replace(",", ""))
+                except ValueError:
+                    continue
+                u = units[i]
+                if name in ("dram_read", "dram_write"):
+                    v *= {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
+                if name == "duration_ns":
+                    v *= {"nsecond": 1, "ns": 1, "usecond": 1e3, "us": 1e3, "msecond": 1e6, "ms": 1e6}.get(u, 1)
+                d[name] = v
+        launches.append(d)
+    lines = ["| kernel | grid x block | regs | duration µs | DRAM read MB | DRAM write MB | DRAM % | SM % | L2 hit % | occupancy % | issue % |",
+             "|---|---|---|---|---|---|---|---|---|---|---|"]
+    for d in launches:
+        lines.append("| {} | {}x{} | {:.0f} | {:.1f} | {:.1f} | {:.1f} | {:.1f} | {:.1f} | {:.1f} | {:.1f} | {:.1f} |".format(
+            d["kernel"].split("(")[0], int(d.get("grid", 0)), int(d.get("block", 0)), d.get("regs", 0),
+            d.get("duration_ns", 0) / 1e3, d.get("dram_read", 0) / 1e6, d.get("dram_write", 0) / 1e6,
+            d.get("dram_pct", 0), d.get("sm_pct", 0), d.get("l2_hit_pct", 0), d.get("occupancy_pct", 0),
+            d.get("issue_pct", 0)))
+    with open(out, "w") as f:
+        f.write(f"ncu --set full --clock-control none summary of `{rep}` (cold-cache, serialised replays)\n\n")
+        f.write("\n".join(lines) + "\n")
+    print("\n".join(lines))
+    if js:
+        agg = {}
+        for d in launches:
+            k = d["kernel"]
+            for key, name in (("k_pr_seg", "pr_seg"), ("k_pr_merge", "pr_merge"), ("k_pr_pull", "pr_direct"),
+                              ("k_bfs_pull_smem", "bfs_pull"), ("k_bfs_push_stamp", "bfs_push_stamp")):
+                if key in k:
+                    a = agg.setdefault(name, {"launches": 0, "dram_bytes": 0.0, "duration_ns": 0.0})
+                    a["launches"] += 1
+                    a["dram_bytes"] += d.get("dram_read", 0) + d.get("dram_write", 0)
+                    a["duration_ns"] += d.get("duration_ns", 0)
+        for a in agg.values():
+            a["dram_bytes_per_launch"] = a["dram_bytes"] / a["launches"]
+            a["duration_us_per_launch"] = a["duration_ns"] / a["launches"] / 1e3
+        if "pr_seg" in agg and "pr_merge" in agg:  # one pull iteration = segment pass + merge pass
+            agg["pr_pull"] = {"dram_bytes_per_launch": agg["pr_seg"]["dram_bytes_per_launch"] +
+                              agg["pr_merge"]["dram_bytes_per_launch"],
+                              "note": "per PageRank iteration: k_pr_seg + k_pr_merge (k_fold_carries negligible)"}
+        agg["source"] = rep
+        json.dump(agg, open(js, "w"), indent=1)
+
+
+if __name__ == "__main__":
+    main()
