@@ -20,6 +20,7 @@
 //  conversion: queue -> bitmap (atomicOr per id);
 //    bitmap -> queue (popc + warp scan + one atomicAdd per warp).
 #include <algorithm>
+#include <climits>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -361,91 +362,122 @@ struct FrontierDegree {
   __host__ __device__ long long operator()(const int64_t& i) const { return (long long)outdeg[q[i]]; }
 };
 
-template <typename OffT, int EPT>
+// Flattened-edge walk shared by the edge-balanced push kernels. Each CTA step
+// takes kFlatCH consecutive edges of the frontier's flattened edge list; thread
+// 0 finds the step's first owner once (binary search in `pre`), the CTA stages
+// the next kFlatW owners' prefix values and ids in shared memory, and every
+// edge finds its owner there (an owner beyond the window — only possible with
+// many zero-degree frontier vertices — falls back to a global search).
+constexpr int kFlatCH = 2048;
+constexpr int kFlatW = kFlatCH + 1;
+struct FlatSmem {
+  long long pre[kFlatW + 1];
+  int32_t u[kFlatW];
+  long long o0;
+};
+
+template <typename OffT, typename Visit>
+__device__ __forceinline__ void flat_edges(const int32_t* __restrict__ q, int64_t nf, const long long* __restrict__ pre,
+                                           long long E, const OffT* __restrict__ off,
+                                           const int32_t* __restrict__ idx, FlatSmem& sm, Visit&& visit) {
+  const int tid = threadIdx.x;
+  auto global_owner = [&](long long f) {  // last i with pre[i] <= f
+    int64_t lo = 0, hi = nf - 1;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi + 1) >> 1;
+      if (__ldg(&pre[mid]) <= f) lo = mid;
+      else hi = mid - 1;
+    }
+    return lo;
+  };
+  for (long long lo = (long long)blockIdx.x * kFlatCH; lo < E; lo += (long long)gridDim.x * kFlatCH) {
+    const long long hi = min(lo + (long long)kFlatCH, E);
+    if (tid == 0) sm.o0 = global_owner(lo);
+    __syncthreads();
+    const int64_t o0 = sm.o0;
+    for (int i = tid; i <= kFlatW; i += blockDim.x) {
+      const int64_t o = o0 + i;
+      sm.pre[i] = o < nf ? __ldg(&pre[o]) : LLONG_MAX;
+      if (i < kFlatW) sm.u[i] = o < nf ? __ldg(&q[o]) : -1;
+    }
+    __syncthreads();
+    for (long long base = lo; base < hi; base += blockDim.x) {
+      const long long f = base + tid;
+      const bool valid = f < hi;
+      int32_t u = -1, v = -1;
+      if (valid) {
+        long long pf;
+        if (sm.pre[kFlatW] <= f) {  // owner outside the staged window
+          const int64_t o = global_owner(f);
+          u = __ldg(&q[o]);
+          pf = __ldg(&pre[o]);
+        } else {
+          int a = 0, b = kFlatW - 1;
+          while (a < b) {
+            const int mid = (a + b + 1) >> 1;
+            if (sm.pre[mid] <= f) a = mid;
+            else b = mid - 1;
+          }
+          u = sm.u[a];
+          pf = sm.pre[a];
+        }
+        v = __ldg(&idx[(long long)off[u] + (f - pf)]);
+      }
+      visit(valid, u, v);
+    }
+    __syncthreads();
+  }
+}
+
+// Edge-balanced push level with CAS claims (mid-size levels).
+template <typename OffT>
 __global__ void __launch_bounds__(256) k_bfs_push_bal(const int32_t* __restrict__ q, int64_t nf,
                                                       const long long* __restrict__ pre, long long E,
                                                       const OffT* __restrict__ off, const int32_t* __restrict__ idx,
                                                       const int32_t* __restrict__ outdeg, int32_t* parent,
                                                       int32_t* __restrict__ qnext, int64_t* __restrict__ cnext) {
+  __shared__ FlatSmem sm;
   const int lane = threadIdx.x & 31;
-  const long long stride = (long long)gridDim.x * blockDim.x * EPT;
-  for (long long f0 = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * EPT; f0 - (long long)lane * EPT < E;
-       f0 += stride) {
-    int64_t o = 0;
-    if (f0 < E) {  // owner of f0: last i with pre[i] <= f0
-      int64_t lo = 0, hi = nf - 1;
-      while (lo < hi) {
-        const int64_t mid = (lo + hi + 1) >> 1;
-        if (__ldg(&pre[mid]) <= f0) lo = mid;
-        else hi = mid - 1;
-      }
-      o = lo;
-    }
+  flat_edges<OffT>(q, nf, pre, E, off, idx, sm, [&](bool valid, int32_t u, int32_t v) {
+    bool won = false;
+    if (valid && *(volatile int32_t*)&parent[v] == -1) won = atomicCAS(&parent[v], -1, u) == -1;
+    const unsigned mask = __ballot_sync(0xffffffffu, won);
+    if (mask) {
+      long long od = won ? (long long)__ldg(&outdeg[v]) : 0;
 #pragma unroll
-    for (int k = 0; k < EPT; ++k) {
-      const long long f = f0 + k;
-      bool won = false;
-      int32_t v = 0;
-      if (f < E) {
-        while (o + 1 < nf && __ldg(&pre[o + 1]) <= f) ++o;
-        const int32_t u = __ldg(&q[o]);
-        v = __ldg(&idx[(long long)off[u] + (f - __ldg(&pre[o]))]);
-        if (*(volatile int32_t*)&parent[v] == -1) won = atomicCAS(&parent[v], -1, u) == -1;
+      for (int s = 16; s > 0; s >>= 1) od += __shfl_xor_sync(0xffffffffu, od, s);
+      long long pos = 0;
+      if (lane == 0) {
+        pos = atomicAdd((unsigned long long*)&cnext[0], (unsigned long long)__popc(mask));
+        atomicAdd((unsigned long long*)&cnext[1], (unsigned long long)od);
       }
-      const unsigned mask = __ballot_sync(0xffffffffu, won);
-      if (mask) {
-        long long od = won ? (long long)__ldg(&outdeg[v]) : 0;
-#pragma unroll
-        for (int s = 16; s > 0; s >>= 1) od += __shfl_xor_sync(0xffffffffu, od, s);
-        long long pos = 0;
-        if (lane == 0) {
-          pos = atomicAdd((unsigned long long*)&cnext[0], (unsigned long long)__popc(mask));
-          atomicAdd((unsigned long long*)&cnext[1], (unsigned long long)od);
-        }
-        pos = __shfl_sync(0xffffffffu, pos, 0);
-        if (won) qnext[pos + __popc(mask & ((1u << lane) - 1))] = v;
-      }
+      pos = __shfl_sync(0xffffffffu, pos, 0);
+      if (won) qnext[pos + __popc(mask & ((1u << lane) - 1))] = v;
     }
-  }
+  });
 }
 
 // Large push levels, two phases, no atomics on the vertex data (the dedup of
 // applyModified, done by a stamp instead of a CAS: thousands of
 // frontier edges that reach the same hub would otherwise serialise on one
 // L2 atomic unit).
-//  phase 1 (edge-balanced like k_bfs_push_bal): for frontier edge (u, v)
-//    with parent[v] == -1, stamp cand[v] = (epoch << 32 | u) with a plain
-//    store unless already stamped this epoch — racing writers all write a
-//    valid parent (same level), the last one wins;
+//  phase 1 (k_bfs_push_stamp, edge-balanced): for frontier edge (u, v) with
+//    parent[v] == -1, stamp cand[v] = (epoch << 32 | u) with a plain store
+//    unless already stamped this epoch — racing writers all write a valid
+//    parent (same level), the last one wins;
 //  phase 2 (k_bfs_collect, vertex order): every v stamped this epoch and still
 //    unvisited takes parent[v] = u and is appended to the next queue.
-template <typename OffT, int EPT>
+template <typename OffT>
 __global__ void __launch_bounds__(256) k_bfs_push_stamp(const int32_t* __restrict__ q, int64_t nf,
                                                         const long long* __restrict__ pre, long long E,
                                                         const OffT* __restrict__ off, const int32_t* __restrict__ idx,
                                                         const int32_t* __restrict__ parent,
                                                         unsigned long long* cand, unsigned epoch) {
-  const long long stride = (long long)gridDim.x * blockDim.x * EPT;
-  for (long long f0 = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * EPT; f0 < E; f0 += stride) {
-    int64_t lo = 0, hi = nf - 1;  // owner of f0: last i with pre[i] <= f0
-    while (lo < hi) {
-      const int64_t mid = (lo + hi + 1) >> 1;
-      if (__ldg(&pre[mid]) <= f0) lo = mid;
-      else hi = mid - 1;
-    }
-    int64_t o = lo;
-#pragma unroll
-    for (int k = 0; k < EPT; ++k) {
-      const long long f = f0 + k;
-      if (f < E) {
-        while (o + 1 < nf && __ldg(&pre[o + 1]) <= f) ++o;
-        const int32_t u = __ldg(&q[o]);
-        const int32_t v = __ldg(&idx[(long long)off[u] + (f - __ldg(&pre[o]))]);
-        if (parent[v] == -1 && (unsigned)(cand[v] >> 32) != epoch)
-          cand[v] = ((unsigned long long)epoch << 32) | (uint32_t)u;
-      }
-    }
-  }
+  __shared__ FlatSmem sm;
+  flat_edges<OffT>(q, nf, pre, E, off, idx, sm, [&](bool valid, int32_t u, int32_t v) {
+    if (valid && parent[v] == -1 && (unsigned)(cand[v] >> 32) != epoch)
+      cand[v] = ((unsigned long long)epoch << 32) | (uint32_t)u;
+  });
 }
 
 // Phase 2 of the stamped push: vertex order, CTA chunks of 2048 vertices.
@@ -698,15 +730,14 @@ static gi_status bfs_impl(gi_graph g, int32_t source, const gi_bfs_opts& o, int3
             cub::CountingInputIterator<int64_t>(0), FrontierDegree{outdeg, g->queue[qc].as<int32_t>()});
         size_t tb = g->bfs_scan_tmp.bytes;
         GI_CUDA(cub::DeviceScan::ExclusiveSum(g->bfs_scan_tmp.p, tb, it, g->bfs_pre.as<long long>(), nf, st));
-        constexpr int EPT = 8;
-        const int grid = (int)std::min<int64_t>(ceil_div(sdeg, 256 * EPT), (int64_t)sms * 8);
+        const int grid = (int)std::min<int64_t>(ceil_div(sdeg, kFlatCH), (int64_t)sms * 8);
         if (sdeg >= kStampMin) {  // two-phase stamp + collect (no atomics on hub destinations)
           if (!g->bfs_cand.p || ++g->bfs_epoch == 0) {
             if (!g->bfs_cand.p) GI_TRY(g->bfs_cand.alloc(n * sizeof(unsigned long long)));
             GI_CUDA(cudaMemsetAsync(g->bfs_cand.p, 0, n * sizeof(unsigned long long), st));
             g->bfs_epoch = 1;
           }
-          k_bfs_push_stamp<OffT, EPT><<<grid, 256, 0, st>>>(g->queue[qc].as<int32_t>(), nf,
+          k_bfs_push_stamp<OffT><<<grid, 256, 0, st>>>(g->queue[qc].as<int32_t>(), nf,
                                                             g->bfs_pre.as<long long>(), sdeg, csr_off,
                                                             g->csr_idx.as<int32_t>(), parent,
                                                             g->bfs_cand.as<unsigned long long>(), g->bfs_epoch);
@@ -716,7 +747,7 @@ static gi_status bfs_impl(gi_graph g, int32_t source, const gi_bfs_opts& o, int3
           next_bitmap_ready = true;  // bitmap[bc] now holds the next frontier too
           S.launches += 2;
         } else {
-          k_bfs_push_bal<OffT, EPT><<<grid, 256, 0, st>>>(g->queue[qc].as<int32_t>(), nf, g->bfs_pre.as<long long>(),
+          k_bfs_push_bal<OffT><<<grid, 256, 0, st>>>(g->queue[qc].as<int32_t>(), nf, g->bfs_pre.as<long long>(),
                                                           sdeg, csr_off, g->csr_idx.as<int32_t>(), outdeg, parent,
                                                           g->queue[qc ^ 1].as<int32_t>(), nxt);
           S.launches++;
