@@ -53,6 +53,7 @@ typedef enum {
 } gi_status;
 
 typedef struct gi_context_s* gi_context; /* device, CUDA stream, optional NCCL comm */
+typedef struct gi_local_group_s* gi_local_group; /* in-process simulated ranks (tests) */
 typedef struct gi_graph_s* gi_graph;     /* device CSR + CSC + degrees (+ partition) */
 
 /* ---------------------------------------------------------------- context */
@@ -70,6 +71,25 @@ GI_API gi_status gi_context_create_dist(int device, void* cuda_stream, int rank,
                                  const unsigned char id[128], gi_context* out);
 GI_API gi_status gi_context_destroy(gi_context ctx);
 GI_API gi_status gi_context_rank(gi_context ctx, int* rank, int* nranks);
+
+/* Test hook for the partitioned path on ONE GPU: nranks simulated ranks,
+ * each driven by its own host thread with its own context created by
+ * gi_context_create_local(device, stream, group, rank). Every collective of the
+ * multi-GPU path (allreduce, allgatherv, alltoallv) is performed by device
+ * copies between the ranks' buffers plus a host barrier; no kernel waits on
+ * another rank. All ranks must make the same calls in the same order, as with
+ * NCCL. Destroy the group after every context of it. */
+GI_API gi_status gi_local_group_create(int nranks, gi_local_group* out);
+GI_API gi_status gi_local_group_destroy(gi_local_group grp);
+GI_API gi_status gi_context_create_local(int device, void* cuda_stream, gi_local_group grp, int rank,
+                                  gi_context* out);
+
+/* Host-only helper (no device): the 1-D destination partition the multi-GPU
+ * build uses: bounds[0] = 0 <= bounds[1] <= ... <= bounds[nranks] = n,
+ * inner bounds multiples of 32 (whole frontier-bitmap words), each range
+ * holding ~1/nranks of the total weight; weight_prefix[i] = sum of the weights
+ * of vertices < i (length n+1, host memory; the build uses in-degree + 1). */
+GI_API gi_status gi_partition_ranges(int64_t n, int nranks, const int64_t* weight_prefix, int64_t* bounds);
 
 /* ---------------------------------------------------------------- graph */
 
@@ -103,6 +123,10 @@ GI_API gi_status gi_graph_create(gi_context ctx, int64_t num_vertices, int64_t n
 GI_API gi_status gi_graph_destroy(gi_graph g);
 GI_API gi_status gi_graph_num_vertices(gi_graph g, int64_t* n);
 GI_API gi_status gi_graph_num_edges(gi_graph g, int64_t* m); /* global m after cleanup */
+
+/* Owned destination range [*lo, *hi) of this rank (input ids are not ranges:
+ * this is in the library's internal vertex order; single GPU: [0, n)). */
+GI_API gi_status gi_graph_partition(gi_graph g, int64_t* lo, int64_t* hi, int64_t* local_edges);
 
 /* Test hooks (length n, input ids; host or device pointers). */
 GI_API gi_status gi_graph_out_degrees(gi_graph g, int32_t* outdeg);

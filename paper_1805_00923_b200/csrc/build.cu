@@ -13,6 +13,7 @@
 #include <cub/cub.cuh>
 
 #include "gi_internal.cuh"
+#include "comm.cuh"
 
 namespace gi {
 namespace {
@@ -137,13 +138,15 @@ struct Temp {
 
 }  // namespace
 
+// rows + 1 offsets (lower bounds of r << bits) and the low-bit column ids
 template <typename OffT>
-static gi_status csr_from_sorted(gi_graph g, const uint64_t* keys, int64_t m, int bits, DevBuf& off, DevBuf& idx) {
+static gi_status csr_from_sorted(gi_graph g, const uint64_t* keys, int64_t m, int bits, int64_t rows, DevBuf& off,
+                                 DevBuf& idx) {
   cudaStream_t st = g->ctx->stream;
   const int sms = g->ctx->num_sms;
-  GI_TRY(off.alloc((g->n + 1) * sizeof(OffT)));
+  GI_TRY(off.alloc((rows + 1) * sizeof(OffT)));
   GI_TRY(idx.alloc(m * sizeof(int32_t)));
-  k_offsets<OffT><<<grid_for(g->n + 1, 256, sms), 256, 0, st>>>(keys, m, g->n, bits, off.as<OffT>());
+  k_offsets<OffT><<<grid_for(rows + 1, 256, sms), 256, 0, st>>>(keys, m, rows, bits, off.as<OffT>());
   k_low_bits<<<grid_for(m, 256, sms), 256, 0, st>>>(keys, m, bits, idx.as<int32_t>());
   GI_CUDA(cudaGetLastError());
   return GI_OK;
@@ -215,6 +218,9 @@ gi_status build_graph(gi_context ctx, int64_t n, int64_t m0, const int32_t* d_sr
     std::swap(cur, alt);
   }
   g->m = m;
+  g->ml = m;
+  g->r0 = 0;
+  g->nr = n;
   g->off64 = m >= (int64_t)INT32_MAX;
 
   // 6. out-degrees in input ids (from the input-id CSR)
@@ -257,8 +263,8 @@ gi_status build_graph(gi_context ctx, int64_t n, int64_t m0, const int32_t* d_sr
       GI_TRY(sort_keys(m));
     }
   }
-  if (g->off64) GI_TRY(csr_from_sorted<int64_t>(g, cur->as<uint64_t>(), m, bits, g->csr_off, g->csr_idx));
-  else GI_TRY(csr_from_sorted<int32_t>(g, cur->as<uint64_t>(), m, bits, g->csr_off, g->csr_idx));
+  if (g->off64) GI_TRY(csr_from_sorted<int64_t>(g, cur->as<uint64_t>(), m, bits, n, g->csr_off, g->csr_idx));
+  else GI_TRY(csr_from_sorted<int32_t>(g, cur->as<uint64_t>(), m, bits, n, g->csr_off, g->csr_idx));
   if (inv) {  // out-degrees in internal ids
     if (g->off64) k_degrees<int64_t><<<grid_for(n, 256, sms), 256, 0, st>>>(g->csr_off.as<int64_t>(), n, g->outdeg.as<int32_t>());
     else k_degrees<int32_t><<<grid_for(n, 256, sms), 256, 0, st>>>(g->csr_off.as<int32_t>(), n, g->outdeg.as<int32_t>());
@@ -269,8 +275,8 @@ gi_status build_graph(gi_context ctx, int64_t n, int64_t m0, const int32_t* d_sr
     k_rekey<<<grid_for(m, 256, sms), 256, 0, st>>>(edges_in.as<uint64_t>(), m, bits, inv, 1, cur->as<uint64_t>());
     GI_TRY(sort_keys(m));
   }
-  if (g->off64) GI_TRY(csr_from_sorted<int64_t>(g, cur->as<uint64_t>(), m, bits, g->csc_off, g->csc_idx));
-  else GI_TRY(csr_from_sorted<int32_t>(g, cur->as<uint64_t>(), m, bits, g->csc_off, g->csc_idx));
+  if (g->off64) GI_TRY(csr_from_sorted<int64_t>(g, cur->as<uint64_t>(), m, bits, n, g->csc_off, g->csc_idx));
+  else GI_TRY(csr_from_sorted<int32_t>(g, cur->as<uint64_t>(), m, bits, n, g->csc_off, g->csc_idx));
 
   // 10. pull tiling metadata
   g->ntiles = n > 0 ? ceil_div(n + m, kPullTile) : 0;
@@ -282,6 +288,306 @@ gi_status build_graph(gi_context ctx, int64_t n, int64_t m0, const int32_t* d_sr
     else
       k_tile_rows<int32_t><<<grid_for(2 * g->ntiles, 256, sms), 256, 0, st>>>(g->csc_off.as<int32_t>(), n, m, g->ntiles,
                                                                             kPullTile, g->tile_rows.as<int32_t>());
+  }
+  GI_CUDA(cudaGetLastError());
+  GI_CUDA(cudaStreamSynchronize(st));
+  return GI_OK;
+}
+
+
+// ---------------------------------------------------------------------------------------------
+// Multi-GPU build: 1-D destination-range partition. Every rank
+// passes any share of the edge list; the graph is the union.
+//   1. validate (allreduce of an error flag: every rank fails alike)
+//   2. local keys (u << 32 | v), self-loops dropped, optional symmetrisation
+//   3. approximate degree histograms (before dedup) -> allreduce
+//   4. relabel by approximate out-degree (identical on every rank: same input,
+//      same deterministic radix sort); only the internal order depends on it
+//   5. owner ranges: in-degree + 1 weights, equal shares cut at whole bitmap
+//      words (partition_ranges)
+//   6. owner shuffle: sort keys by owner, alltoallv (NCCL grouped send/recv)
+//   7. local sort + dedup (duplicates share an owner), CSR by source over all
+//      n sources (edges into the owned range), CSC of the owned rows, exact
+//      out-degrees by allreduce, global m by allreduce
+namespace {
+
+__global__ void k_key_hist(const uint64_t* __restrict__ keys, int64_t k, int32_t* __restrict__ od,
+                           int32_t* __restrict__ id) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < k; i += (int64_t)gridDim.x * blockDim.x) {
+    atomicAdd(&od[keys[i] >> 32], 1);
+    atomicAdd(&id[keys[i] & 0xFFFFFFFFull], 1);
+  }
+}
+
+__global__ void k_weights(const int32_t* __restrict__ perm, const int32_t* __restrict__ indeg, int64_t n,
+                          int64_t* __restrict__ w) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= n; i += (int64_t)gridDim.x * blockDim.x)
+    w[i] = i < n ? (int64_t)indeg[perm ? perm[i] : i] + 1 : 0;
+}
+
+__global__ void k_dist_owner(const uint64_t* __restrict__ keys, int64_t k, const int32_t* __restrict__ inv,
+                             const int64_t* __restrict__ bounds, int P, uint32_t* __restrict__ owner,
+                             uint64_t* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < k; i += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t u = keys[i] >> 32, v = keys[i] & 0xFFFFFFFFull;
+    if (inv) {
+      u = (uint32_t)inv[u];
+      v = (uint32_t)inv[v];
+    }
+    int lo = 0, hi = P - 1;  // last p with bounds[p] <= v
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (bounds[mid] <= (int64_t)v) lo = mid;
+      else hi = mid - 1;
+    }
+    owner[i] = (uint32_t)lo;
+    out[i] = (u << 32) | v;
+  }
+}
+
+__global__ void k_owner_starts(const uint32_t* __restrict__ owner, int64_t k, int P, int64_t* __restrict__ starts) {
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p <= P; p += gridDim.x * blockDim.x) {
+    int64_t lo = 0, hi = k;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (owner[mid] < (uint32_t)p) lo = mid + 1;
+      else hi = mid;
+    }
+    starts[p] = lo;
+  }
+}
+
+// (u << 32 | v) -> (u << b | v)  or, transposed for the local CSC, ((v - r0) << b | u)
+__global__ void k_pack_local(const uint64_t* __restrict__ in, int64_t k, int bits, int64_t r0, int transpose,
+                             uint64_t* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < k; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t u = in[i] >> 32, v = in[i] & 0xFFFFFFFFull;
+    out[i] = transpose ? (((v - (uint64_t)r0) << bits) | u) : ((u << bits) | v);
+  }
+}
+
+// (u << b | v) -> ((v - r0) << b | u)
+__global__ void k_repack_transpose(const uint64_t* __restrict__ in, int64_t k, int bits, int64_t r0,
+                                   uint64_t* __restrict__ out) {
+  const uint64_t mask = (1ull << bits) - 1;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < k; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t u = in[i] >> bits, v = in[i] & mask;
+    out[i] = ((v - (uint64_t)r0) << bits) | u;
+  }
+}
+
+struct DevPrefix {
+  const int64_t* d;
+};
+int64_t dev_prefix(void* ctx, int64_t i) {
+  int64_t v = 0;
+  cudaMemcpy(&v, static_cast<DevPrefix*>(ctx)->d + i, sizeof(int64_t), cudaMemcpyDeviceToHost);
+  return v;
+}
+
+}  // namespace
+
+gi_status build_graph_dist(gi_context ctx, int64_t n, int64_t m0, const int32_t* d_src, const int32_t* d_dst,
+                           uint32_t flags, gi_graph g) {
+  Comm* C = ctx->comm;
+  if (!C) return fail(GI_ERR_INTERNAL, "multi-GPU context without a comm layer");
+  cudaStream_t st = ctx->stream;
+  const int sms = ctx->num_sms;
+  const int P = C->nranks, R = C->rank;
+  g->ctx = ctx;
+  g->n = n;
+  const bool rm_self = flags & GI_REMOVE_SELF_LOOPS;
+  const bool dedup = flags & GI_DEDUP;
+  const bool sym = flags & GI_SYMMETRIZE;
+  g->relabeled = !(flags & GI_NO_RELABEL) && n > 1;
+
+  // 1. validate
+  DevBuf bad;
+  GI_TRY(bad.alloc(sizeof(int32_t)));
+  GI_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int32_t), st));
+  if (m0 > 0) k_validate<<<grid_for(m0, 256, sms), 256, 0, st>>>(d_src, d_dst, m0, n, bad.as<int>());
+  GI_TRY(C->allreduce_i32(bad.as<int32_t>(), 1, st));
+  int32_t h_bad = 0;
+  GI_CUDA(cudaMemcpyAsync(&h_bad, bad.p, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  GI_CUDA(cudaStreamSynchronize(st));
+  if (h_bad) return fail(GI_ERR_VERTEX_OUT_OF_RANGE, "gi_graph_create: an edge endpoint is outside [0, n) on some rank");
+
+  // 2. local keys in input ids (u << 32 | v)
+  const int64_t mk = sym ? 2 * m0 : m0;
+  DevBuf kA, kB, nsel, tmp;
+  GI_TRY(kA.alloc(mk * sizeof(uint64_t)));
+  GI_TRY(kB.alloc(mk * sizeof(uint64_t)));
+  GI_TRY(nsel.alloc(sizeof(int64_t)));
+  int64_t k = 0;
+  size_t tb = 0;
+  if (mk > 0) {
+    k_make_keys<<<grid_for(m0, 256, sms), 256, 0, st>>>(d_src, d_dst, m0, 32, rm_self, sym, kA.as<uint64_t>());
+    GI_CUDA(cub::DeviceSelect::If(nullptr, tb, kA.as<uint64_t>(), kB.as<uint64_t>(), nsel.as<int64_t>(), mk,
+                                  NotSentinel(), st));
+    GI_TRY(tmp.alloc(tb));
+    GI_CUDA(cub::DeviceSelect::If(tmp.p, tb, kA.as<uint64_t>(), kB.as<uint64_t>(), nsel.as<int64_t>(), mk,
+                                  NotSentinel(), st));
+    GI_CUDA(cudaMemcpyAsync(&k, nsel.p, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    GI_CUDA(cudaStreamSynchronize(st));
+  }
+  // 3. approximate degree histograms (duplicates counted), summed over ranks
+  DevBuf hod, hid;
+  GI_TRY(hod.alloc(n * sizeof(int32_t)));
+  GI_TRY(hid.alloc(n * sizeof(int32_t)));
+  GI_CUDA(cudaMemsetAsync(hod.p, 0, n * sizeof(int32_t), st));
+  GI_CUDA(cudaMemsetAsync(hid.p, 0, n * sizeof(int32_t), st));
+  if (k > 0) k_key_hist<<<grid_for(k, 256, sms), 256, 0, st>>>(kB.as<uint64_t>(), k, hod.as<int32_t>(), hid.as<int32_t>());
+  GI_TRY(C->allreduce_i32(hod.as<int32_t>(), n, st));
+  GI_TRY(C->allreduce_i32(hid.as<int32_t>(), n, st));
+  // 4. relabel (same permutation on every rank)
+  const int32_t* inv = nullptr;
+  if (g->relabeled) {
+    DevBuf rk, rk2, ids;
+    GI_TRY(rk.alloc(n * sizeof(uint32_t)));
+    GI_TRY(rk2.alloc(n * sizeof(uint32_t)));
+    GI_TRY(ids.alloc(n * sizeof(int32_t)));
+    GI_TRY(g->perm.alloc(n * sizeof(int32_t)));
+    GI_TRY(g->inv.alloc(n * sizeof(int32_t)));
+    k_relabel_keys<<<grid_for(n, 256, sms), 256, 0, st>>>(hod.as<int32_t>(), n, rk.as<uint32_t>(), ids.as<int32_t>());
+    tb = 0;
+    GI_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, rk.as<uint32_t>(), rk2.as<uint32_t>(), ids.as<int32_t>(),
+                                            g->perm.as<int32_t>(), n, 0, 32, st));
+    GI_TRY(tmp.alloc(tb));
+    GI_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, rk.as<uint32_t>(), rk2.as<uint32_t>(), ids.as<int32_t>(),
+                                            g->perm.as<int32_t>(), n, 0, 32, st));
+    k_invert<<<grid_for(n, 256, sms), 256, 0, st>>>(g->perm.as<int32_t>(), n, g->inv.as<int32_t>());
+    inv = g->inv.as<int32_t>();
+  }
+  // 5. owner ranges over internal ids
+  {
+    DevBuf w, pre;
+    GI_TRY(w.alloc((n + 1) * sizeof(int64_t)));
+    GI_TRY(pre.alloc((n + 1) * sizeof(int64_t)));
+    k_weights<<<grid_for(n + 1, 256, sms), 256, 0, st>>>(g->relabeled ? g->perm.as<int32_t>() : nullptr,
+                                                         hid.as<int32_t>(), n, w.as<int64_t>());
+    tb = 0;
+    GI_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, w.as<int64_t>(), pre.as<int64_t>(), n + 1, st));
+    GI_TRY(tmp.alloc(tb));
+    GI_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb, w.as<int64_t>(), pre.as<int64_t>(), n + 1, st));
+    GI_CUDA(cudaStreamSynchronize(st));
+    g->bounds.assign(P + 1, 0);
+    DevPrefix dp{pre.as<int64_t>()};
+    partition_ranges(n, P, dev_prefix, &dp, g->bounds.data());
+  }
+  g->r0 = g->bounds[R];
+  g->nr = g->bounds[R + 1] - g->bounds[R];
+  // 6. owner shuffle
+  DevBuf owner, owner2, dbounds, starts;
+  GI_TRY(owner.alloc(k * sizeof(uint32_t)));
+  GI_TRY(owner2.alloc(k * sizeof(uint32_t)));
+  GI_TRY(dbounds.alloc((P + 1) * sizeof(int64_t)));
+  GI_TRY(starts.alloc((P + 1) * sizeof(int64_t)));
+  GI_CUDA(cudaMemcpyAsync(dbounds.p, g->bounds.data(), (P + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  if (k > 0) {
+    k_dist_owner<<<grid_for(k, 256, sms), 256, 0, st>>>(kB.as<uint64_t>(), k, inv, dbounds.as<int64_t>(), P,
+                                                       owner.as<uint32_t>(), kA.as<uint64_t>());
+    int obits = 1;
+    while ((1 << obits) < P) ++obits;
+    tb = 0;
+    GI_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, owner.as<uint32_t>(), owner2.as<uint32_t>(),
+                                            kA.as<uint64_t>(), kB.as<uint64_t>(), k, 0, obits, st));
+    GI_TRY(tmp.alloc(tb));
+    GI_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, owner.as<uint32_t>(), owner2.as<uint32_t>(),
+                                            kA.as<uint64_t>(), kB.as<uint64_t>(), k, 0, obits, st));
+  }
+  k_owner_starts<<<1, 64, 0, st>>>(owner2.as<uint32_t>(), k, P, starts.as<int64_t>());
+  std::vector<int64_t> h_starts(P + 1);
+  GI_CUDA(cudaMemcpyAsync(h_starts.data(), starts.p, (P + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  GI_CUDA(cudaStreamSynchronize(st));
+  // exchange the count matrix: row R = what this rank sends to each owner
+  DevBuf mat;
+  GI_TRY(mat.alloc((size_t)P * P * sizeof(int64_t)));
+  GI_CUDA(cudaMemsetAsync(mat.p, 0, (size_t)P * P * sizeof(int64_t), st));
+  std::vector<int64_t> row(P);
+  for (int p = 0; p < P; ++p) row[p] = h_starts[p + 1] - h_starts[p];
+  GI_CUDA(cudaMemcpyAsync(mat.as<int64_t>() + (size_t)R * P, row.data(), P * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  GI_TRY(C->allreduce_i64(mat.as<int64_t>(), (int64_t)P * P, st));
+  std::vector<int64_t> h_mat((size_t)P * P);
+  GI_CUDA(cudaMemcpyAsync(h_mat.data(), mat.p, (size_t)P * P * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  GI_CUDA(cudaStreamSynchronize(st));
+  std::vector<int64_t> soff(P + 1), roff(P + 1);
+  soff[0] = roff[0] = 0;
+  for (int p = 0; p < P; ++p) {
+    soff[p + 1] = soff[p] + row[p] * 8;
+    roff[p + 1] = roff[p] + h_mat[(size_t)p * P + R] * 8;
+  }
+  const int64_t kr = roff[P] / 8;  // edges received (owned destinations)
+  DevBuf recv;
+  GI_TRY(recv.alloc(kr * sizeof(uint64_t)));
+  GI_TRY(C->alltoallv(kB.p, soff, recv.p, roff, st));
+  kA.reset();
+  kB.reset();
+  owner.reset();
+  owner2.reset();
+
+  // 7. local graph: CSR by source (edges into the owned range) and CSC of owned rows
+  const int bits = bits_for(n > 1 ? n : 2);
+  DevBuf cur, alt;
+  GI_TRY(cur.alloc(kr * sizeof(uint64_t)));
+  GI_TRY(alt.alloc(kr * sizeof(uint64_t)));
+  if (kr > 0) k_pack_local<<<grid_for(kr, 256, sms), 256, 0, st>>>(recv.as<uint64_t>(), kr, bits, 0, 0, cur.as<uint64_t>());
+  DevBuf* pc = &cur;
+  DevBuf* pa = &alt;
+  auto sort_keys = [&](int64_t count) -> gi_status {
+    if (count <= 1) return GI_OK;
+    cub::DoubleBuffer<uint64_t> db(pc->as<uint64_t>(), pa->as<uint64_t>());
+    size_t b = 0;
+    GI_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, b, db, count, 0, 2 * bits, st));
+    GI_TRY(tmp.alloc(b));
+    GI_CUDA(cub::DeviceRadixSort::SortKeys(tmp.p, b, db, count, 0, 2 * bits, st));
+    if (db.Current() != pc->as<uint64_t>()) std::swap(pc, pa);
+    return GI_OK;
+  };
+  GI_TRY(sort_keys(kr));
+  int64_t ml = kr;
+  if (dedup && kr > 1) {
+    size_t b = 0;
+    GI_CUDA(cub::DeviceSelect::Unique(nullptr, b, pc->as<uint64_t>(), pa->as<uint64_t>(), nsel.as<int64_t>(), kr, st));
+    GI_TRY(tmp.alloc(b));
+    GI_CUDA(cub::DeviceSelect::Unique(tmp.p, b, pc->as<uint64_t>(), pa->as<uint64_t>(), nsel.as<int64_t>(), kr, st));
+    GI_CUDA(cudaMemcpyAsync(&ml, nsel.p, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    GI_CUDA(cudaStreamSynchronize(st));
+    std::swap(pc, pa);
+  }
+  g->ml = ml;
+  g->off64 = ml >= (int64_t)INT32_MAX;
+  if (g->off64) GI_TRY(csr_from_sorted<int64_t>(g, pc->as<uint64_t>(), ml, bits, n, g->csr_off, g->csr_idx));
+  else GI_TRY(csr_from_sorted<int32_t>(g, pc->as<uint64_t>(), ml, bits, n, g->csr_off, g->csr_idx));
+  // exact out-degrees: local row lengths summed over ranks
+  GI_TRY(g->outdeg.alloc(n * sizeof(int32_t)));
+  if (g->off64) k_degrees<int64_t><<<grid_for(n, 256, sms), 256, 0, st>>>(g->csr_off.as<int64_t>(), n, g->outdeg.as<int32_t>());
+  else k_degrees<int32_t><<<grid_for(n, 256, sms), 256, 0, st>>>(g->csr_off.as<int32_t>(), n, g->outdeg.as<int32_t>());
+  GI_TRY(C->allreduce_i32(g->outdeg.as<int32_t>(), n, st));
+  DevBuf msum;
+  GI_TRY(msum.alloc(sizeof(int64_t)));
+  GI_CUDA(cudaMemcpyAsync(msum.p, &ml, sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  GI_TRY(C->allreduce_i64(msum.as<int64_t>(), 1, st));
+  int64_t mg = 0;
+  GI_CUDA(cudaMemcpyAsync(&mg, msum.p, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  GI_CUDA(cudaStreamSynchronize(st));
+  g->m = mg;
+  // CSC of the owned rows: ((v - r0) << b | u), sorted
+  if (ml > 0)
+    k_repack_transpose<<<grid_for(ml, 256, sms), 256, 0, st>>>(pc->as<uint64_t>(), ml, bits, g->r0, pa->as<uint64_t>());
+  std::swap(pc, pa);
+  GI_TRY(sort_keys(ml));
+  if (g->off64) GI_TRY(csr_from_sorted<int64_t>(g, pc->as<uint64_t>(), ml, bits, g->nr, g->csc_off, g->csc_idx));
+  else GI_TRY(csr_from_sorted<int32_t>(g, pc->as<uint64_t>(), ml, bits, g->nr, g->csc_off, g->csc_idx));
+  // pull tiling over the owned rows
+  g->ntiles = g->nr > 0 ? ceil_div(g->nr + ml, kPullTile) : 0;
+  GI_TRY(g->tile_rows.alloc(2 * (g->ntiles > 0 ? g->ntiles : 1) * sizeof(int32_t)));
+  if (g->ntiles > 0) {
+    if (g->off64)
+      k_tile_rows<int64_t><<<grid_for(2 * g->ntiles, 256, sms), 256, 0, st>>>(g->csc_off.as<int64_t>(), g->nr, ml,
+                                                                            g->ntiles, kPullTile, g->tile_rows.as<int32_t>());
+    else
+      k_tile_rows<int32_t><<<grid_for(2 * g->ntiles, 256, sms), 256, 0, st>>>(g->csc_off.as<int32_t>(), g->nr, ml,
+                                                                            g->ntiles, kPullTile, g->tile_rows.as<int32_t>());
   }
   GI_CUDA(cudaGetLastError());
   GI_CUDA(cudaStreamSynchronize(st));

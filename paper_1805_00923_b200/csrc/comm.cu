@@ -1,0 +1,146 @@
+// comm.cu — NcclComm and LocalComm (see comm.cuh).
+#include <nccl.h>
+
+#include <cstring>
+
+#include "comm.cuh"
+#include "nccl_dyn.cuh"
+
+namespace gi {
+
+void LocalGroup::barrier() {
+  std::unique_lock<std::mutex> lk(mu);
+  const int64_t g = gen;
+  if (++arrived == n) {
+    arrived = 0;
+    ++gen;
+    cv.notify_all();
+  } else {
+    cv.wait(lk, [&] { return gen != g; });
+  }
+}
+
+namespace {
+
+class NcclComm : public Comm {
+ public:
+  NcclComm(ncclComm_t c, int r, int p) : comm_(c) {
+    rank = r;
+    nranks = p;
+  }
+  gi_status allreduce_i32(int32_t* d, int64_t count, cudaStream_t st) override {
+    return red(d, count, ncclInt32, st);
+  }
+  gi_status allreduce_i64(int64_t* d, int64_t count, cudaStream_t st) override {
+    return red(d, count, ncclInt64, st);
+  }
+  gi_status allreduce_f64(double* d, int64_t count, cudaStream_t st) override {
+    return red(d, count, ncclFloat64, st);
+  }
+  gi_status allgatherv(void* buf, const std::vector<int64_t>& off, cudaStream_t st) override {
+    const NcclApi* a = nccl_api();
+    if (!a) return GI_ERR_NCCL;
+    char* b = static_cast<char*>(buf);
+    GI_TRY(nccl_check(a->groupStart(), "ncclGroupStart"));
+    for (int p = 0; p < nranks; ++p) {
+      const size_t len = (size_t)(off[p + 1] - off[p]);
+      if (len == 0) continue;
+      GI_TRY(nccl_check(a->broadcast(b + off[p], b + off[p], len, ncclUint8, p, comm_, st), "ncclBroadcast"));
+    }
+    return nccl_check(a->groupEnd(), "ncclGroupEnd");
+  }
+  gi_status alltoallv(const void* send, const std::vector<int64_t>& soff, void* recv,
+                      const std::vector<int64_t>& roff, cudaStream_t st) override {
+    const NcclApi* a = nccl_api();
+    if (!a) return GI_ERR_NCCL;
+    const char* s = static_cast<const char*>(send);
+    char* r = static_cast<char*>(recv);
+    GI_TRY(nccl_check(a->groupStart(), "ncclGroupStart"));
+    for (int p = 0; p < nranks; ++p) {
+      const size_t sl = (size_t)(soff[p + 1] - soff[p]), rl = (size_t)(roff[p + 1] - roff[p]);
+      if (sl) GI_TRY(nccl_check(a->send(s + soff[p], sl, ncclUint8, p, comm_, st), "ncclSend"));
+      if (rl) GI_TRY(nccl_check(a->recv(r + roff[p], rl, ncclUint8, p, comm_, st), "ncclRecv"));
+    }
+    return nccl_check(a->groupEnd(), "ncclGroupEnd");
+  }
+
+ private:
+  gi_status red(void* d, int64_t count, ncclDataType_t t, cudaStream_t st) {
+    const NcclApi* a = nccl_api();
+    if (!a) return GI_ERR_NCCL;
+    if (count == 0) return GI_OK;
+    return nccl_check(a->allReduce(d, d, (size_t)count, t, ncclSum, comm_, st), "ncclAllReduce");
+  }
+  ncclComm_t comm_;
+};
+
+class LocalComm : public Comm {
+ public:
+  LocalComm(LocalGroup* g, int r) : g_(g) {
+    rank = r;
+    nranks = g->n;
+  }
+  gi_status allreduce_i32(int32_t* d, int64_t count, cudaStream_t st) override { return red<int32_t>(d, count, st); }
+  gi_status allreduce_i64(int64_t* d, int64_t count, cudaStream_t st) override { return red<int64_t>(d, count, st); }
+  gi_status allreduce_f64(double* d, int64_t count, cudaStream_t st) override { return red<double>(d, count, st); }
+  gi_status allgatherv(void* buf, const std::vector<int64_t>& off, cudaStream_t st) override {
+    GI_CUDA(cudaStreamSynchronize(st));
+    g_->ptr[rank] = buf;
+    g_->barrier();
+    char* b = static_cast<char*>(buf);
+    for (int p = 0; p < nranks; ++p) {
+      const int64_t len = off[p + 1] - off[p];
+      if (p == rank || len == 0) continue;
+      GI_CUDA(cudaMemcpyAsync(b + off[p], static_cast<const char*>(g_->ptr[p]) + off[p], len,
+                              cudaMemcpyDeviceToDevice, st));
+    }
+    GI_CUDA(cudaStreamSynchronize(st));
+    g_->barrier();
+    return GI_OK;
+  }
+  gi_status alltoallv(const void* send, const std::vector<int64_t>& soff, void* recv,
+                      const std::vector<int64_t>& roff, cudaStream_t st) override {
+    GI_CUDA(cudaStreamSynchronize(st));
+    g_->ptr[rank] = send;
+    g_->offs[rank] = soff;
+    g_->barrier();
+    for (int p = 0; p < nranks; ++p) {
+      const int64_t a = g_->offs[p][rank], b = g_->offs[p][rank + 1];
+      if (b - a != roff[p + 1] - roff[p]) return fail(GI_ERR_INTERNAL, "alltoallv: count mismatch");
+      if (b > a)
+        GI_CUDA(cudaMemcpyAsync(static_cast<char*>(recv) + roff[p], static_cast<const char*>(g_->ptr[p]) + a, b - a,
+                                cudaMemcpyDeviceToDevice, st));
+    }
+    GI_CUDA(cudaStreamSynchronize(st));
+    g_->barrier();
+    return GI_OK;
+  }
+
+ private:
+  template <typename T>
+  gi_status red(T* d, int64_t count, cudaStream_t st) {
+    GI_CUDA(cudaStreamSynchronize(st));
+    g_->ptr[rank] = d;
+    g_->barrier();
+    std::vector<T> acc((size_t)count, T(0)), tmp((size_t)count);
+    for (int p = 0; p < nranks; ++p) {  // same order on every rank: identical sums
+      GI_CUDA(cudaMemcpy(tmp.data(), g_->ptr[p], count * sizeof(T), cudaMemcpyDeviceToHost));
+      for (int64_t i = 0; i < count; ++i) acc[i] += tmp[i];
+    }
+    g_->barrier();  // everyone has read every buffer before anyone overwrites its own
+    GI_CUDA(cudaMemcpy(d, acc.data(), count * sizeof(T), cudaMemcpyHostToDevice));
+    g_->barrier();
+    return GI_OK;
+  }
+  LocalGroup* g_;
+};
+
+}  // namespace
+
+Comm* make_nccl_comm(void* nccl_comm, int rank, int nranks) {
+  return new NcclComm(static_cast<ncclComm_t>(nccl_comm), rank, nranks);
+}
+
+Comm* make_local_comm(LocalGroup* g, int rank) { return new LocalComm(g, rank); }
+
+}  // namespace gi

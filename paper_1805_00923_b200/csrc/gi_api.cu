@@ -10,6 +10,7 @@
 
 #include "gi_internal.cuh"
 #include "nccl_dyn.cuh"
+#include "comm.cuh"
 
 namespace gi {
 
@@ -159,6 +160,8 @@ gi_status gi_context_destroy(gi_context ctx) {
     return fail(GI_ERR_INVALID_ARGUMENT, "gi_context_destroy: destroy the context's graphs first");
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
+  delete ctx->comm;
+  ctx->comm = nullptr;
   if (ctx->nccl_comm) {
     const NcclApi* a = nccl_api();
     if (a) a->commDestroy(static_cast<ncclComm_t>(ctx->nccl_comm));
@@ -189,7 +192,6 @@ gi_status gi_graph_create(gi_context ctx, int64_t n, int64_t m0, const int32_t* 
   const uint32_t known = GI_EDGES_ON_DEVICE | GI_REMOVE_SELF_LOOPS | GI_DEDUP | GI_SYMMETRIZE | GI_NO_RELABEL;
   if (flags & ~known) return fail(GI_ERR_INVALID_ARGUMENT, "gi_graph_create: unknown flag bits");
   if (n == 0 && m0 > 0) return fail(GI_ERR_VERTEX_OUT_OF_RANGE, "gi_graph_create: edges given but n = 0");
-  if (ctx->nranks > 1) return fail(GI_ERR_UNSUPPORTED, "gi_graph_create: multi-GPU graphs not built yet");
   GI_CUDA(cudaSetDevice(ctx->device));
   if ((flags & GI_EDGES_ON_DEVICE) && m0 > 0 && !(is_device_ptr(src) && is_device_ptr(dst)))
     return fail(GI_ERR_INVALID_ARGUMENT, "gi_graph_create: GI_EDGES_ON_DEVICE but edges are host memory");
@@ -198,7 +200,8 @@ gi_status gi_graph_create(gi_context ctx, int64_t n, int64_t m0, const int32_t* 
   GI_TRY(to_device(ctx, src, m0, hs, &ds));
   GI_TRY(to_device(ctx, dst, m0, hd, &dd));
   gi_graph g = new gi_graph_s();
-  gi_status s = build_graph(ctx, n, m0, ds, dd, flags, g);
+  gi_status s = ctx->nranks > 1 ? build_graph_dist(ctx, n, m0, ds, dd, flags, g)
+                                : build_graph(ctx, n, m0, ds, dd, flags, g);
   if (s == GI_OK) s = sync(ctx);
   if (s != GI_OK) {
     delete g;
@@ -409,6 +412,82 @@ gi_status gi_bfs_ex(gi_graph g, int32_t source, const gi_bfs_opts* opts, int32_t
 
 gi_status gi_bfs(gi_graph g, int32_t source, int32_t* parent_out) {
   return gi_bfs_ex(g, source, nullptr, parent_out, nullptr);
+}
+
+}  // extern "C"
+
+namespace gi {
+
+void partition_ranges(int64_t n, int nranks, int64_t (*prefix)(void*, int64_t), void* ctx, int64_t* bounds) {
+  bounds[0] = 0;
+  bounds[nranks] = n;
+  const int64_t total = prefix(ctx, n);
+  for (int r = 1; r < nranks; ++r) {
+    const long double target = (long double)total * r / nranks;
+    int64_t lo = 0, hi = n;  // first i with prefix(i) >= target
+    while (lo < hi) {
+      const int64_t mid = lo + (hi - lo) / 2;
+      if ((long double)prefix(ctx, mid) >= target) hi = mid;
+      else lo = mid + 1;
+    }
+    int64_t b = (lo + 31) / 32 * 32;  // whole bitmap words per rank
+    b = std::min(std::max(b, bounds[r - 1]), n);
+    bounds[r] = b;
+  }
+}
+
+}  // namespace gi
+
+static int64_t host_prefix(void* ctx, int64_t i) { return static_cast<const int64_t*>(ctx)[i]; }
+
+extern "C" {
+
+gi_status gi_partition_ranges(int64_t n, int nranks, const int64_t* weight_prefix, int64_t* bounds) {
+  if (n < 0 || nranks < 1 || !weight_prefix || !bounds)
+    return fail(GI_ERR_INVALID_ARGUMENT, "gi_partition_ranges: bad argument");
+  partition_ranges(n, nranks, host_prefix, const_cast<int64_t*>(weight_prefix), bounds);
+  return GI_OK;
+}
+
+gi_status gi_local_group_create(int nranks, gi_local_group* out) {
+  GI_GUARD_BEGIN
+  if (!out || nranks < 1) return fail(GI_ERR_INVALID_ARGUMENT, "gi_local_group_create: bad argument");
+  gi_local_group grp = new gi_local_group_s();
+  grp->g.n = nranks;
+  grp->g.ptr.assign(nranks, nullptr);
+  grp->g.offs.assign(nranks, {});
+  *out = grp;
+  return GI_OK;
+  GI_GUARD_END
+}
+
+gi_status gi_local_group_destroy(gi_local_group grp) {
+  if (!grp) return fail(GI_ERR_INVALID_ARGUMENT, "gi_local_group_destroy: NULL group");
+  delete grp;
+  return GI_OK;
+}
+
+gi_status gi_context_create_local(int device, void* cuda_stream, gi_local_group grp, int rank, gi_context* out) {
+  GI_GUARD_BEGIN
+  if (!out || !grp || rank < 0 || rank >= grp->g.n)
+    return fail(GI_ERR_INVALID_ARGUMENT, "gi_context_create_local: bad argument");
+  *out = nullptr;
+  gi_context c = nullptr;
+  GI_TRY(gi_context_create(device, cuda_stream, &c));
+  c->rank = rank;
+  c->nranks = grp->g.n;
+  if (c->nranks > 1) c->comm = make_local_comm(&grp->g, rank);
+  *out = c;
+  return GI_OK;
+  GI_GUARD_END
+}
+
+gi_status gi_graph_partition(gi_graph g, int64_t* lo, int64_t* hi, int64_t* local_edges) {
+  if (!g || !lo || !hi || !local_edges) return fail(GI_ERR_INVALID_ARGUMENT, "gi_graph_partition: NULL argument");
+  *lo = g->r0;
+  *hi = g->r0 + g->nr;
+  *local_edges = g->ml;
+  return GI_OK;
 }
 
 }  // extern "C"

@@ -10,6 +10,7 @@
 #include <stdint.h>
 
 #include <string>
+#include <vector>
 
 #include "gi.h"
 
@@ -66,14 +67,18 @@ struct DevBuf {
 }  // namespace gi
 
 // ------------------------------------------------------------------ context / graph
-struct NcclApi;  // dynamically loaded NCCL entry points (nccl_dyn.cpp)
+struct NcclApi;  // dynamically loaded NCCL entry points (nccl_dyn.cu)
+namespace gi {
+struct Comm;  // comm.cuh
+}
 
 struct gi_context_s {
   int device = 0;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   int rank = 0, nranks = 1;
-  void* nccl_comm = nullptr;  // ncclComm_t when nranks > 1
+  void* nccl_comm = nullptr;  // ncclComm_t when nranks > 1 (NCCL contexts)
+  gi::Comm* comm = nullptr;   // exchange layer when nranks > 1 (NCCL or in-process local group)
   int num_sms = 148;
   // pinned host scratch for small D2H reads (counters)
   int64_t* h_scratch = nullptr;
@@ -87,8 +92,13 @@ constexpr int kPullTile = kPullThreads * kPullItemsPerThread;  // merge items pe
 
 struct gi_graph_s {
   gi_context ctx = nullptr;
-  int64_t n = 0;       // vertices
+  int64_t n = 0;       // vertices (global)
   int64_t m = 0;       // directed edges after cleanup (global)
+  // 1-D destination partition; single GPU: r0 = 0, nr = n, ml = m.
+  // CSC rows = owned destinations [r0, r0 + nr) (local row = id - r0); the CSR
+  // rows are all n sources but hold only the edges into the owned range.
+  int64_t r0 = 0, nr = 0, ml = 0;
+  std::vector<int64_t> bounds;  // nranks + 1 owner boundaries (multiples of 32)
   bool off64 = false;  // offsets stored as int64 (m >= 2^31) else int32
   bool relabeled = false;
   // vertex relabelling (n each; empty when !relabeled)
@@ -127,7 +137,12 @@ struct gi_graph_s {
 };
 
 namespace gi {
+// host-side partition of [0, n) into nranks ranges of ~equal weight, cut at
+// multiples of 32 (bitmap words); prefix(i) = sum of weights of vertices < i.
+void partition_ranges(int64_t n, int nranks, int64_t (*prefix)(void*, int64_t), void* ctx, int64_t* bounds);
 // build.cu
+gi_status build_graph_dist(gi_context ctx, int64_t n, int64_t m0, const int32_t* d_src,
+                           const int32_t* d_dst, uint32_t flags, gi_graph g);
 gi_status build_graph(gi_context ctx, int64_t n, int64_t m0, const int32_t* d_src,
                       const int32_t* d_dst, uint32_t flags, gi_graph g);
 // pagerank.cu

@@ -13,6 +13,7 @@
 
 #include "gi_internal.cuh"
 #include "nccl_dyn.cuh"
+#include "comm.cuh"
 
 namespace gi {
 
@@ -110,6 +111,7 @@ gi_status gi_context_create_dist(int device, void* cuda_stream, int rank, int nr
       return s;
     }
     c->nccl_comm = comm;
+    c->comm = make_nccl_comm(comm, rank, nranks);
   }
   *out = c;
   return GI_OK;
