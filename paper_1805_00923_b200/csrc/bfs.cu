@@ -30,6 +30,7 @@
 namespace cg = cooperative_groups;
 
 #include "gi_internal.cuh"
+#include "comm.cuh"
 
 namespace gi {
 namespace {
@@ -301,7 +302,9 @@ __global__ void __launch_bounds__(1024, 2) k_bfs_pull_smem(const uint32_t* __res
                                                            const OffT* __restrict__ off,
                                                            const int32_t* __restrict__ idx,
                                                            const int32_t* __restrict__ outdeg, int64_t n, int sw,
-                                                           int64_t* __restrict__ cnext) {
+                                                           int64_t* __restrict__ cnext, int64_t r0) {
+  // n = CSC rows held here, r0 = global id of row 0 (a multiple of 32);
+  // parent is indexed by local row, fnext / outdeg by global id
   extern __shared__ uint32_t sbits[];
   for (int i = threadIdx.x; i < sw; i += blockDim.x) sbits[i] = __ldg(&fcur[i]);
   __syncthreads();
@@ -335,10 +338,10 @@ __global__ void __launch_bounds__(1024, 2) k_bfs_pull_smem(const uint32_t* __res
       }
     }
     const unsigned mask = __ballot_sync(0xffffffffu, found);
-    if (lane == 0) fnext[w] = mask;
+    if (lane == 0) fnext[(r0 >> 5) + w] = mask;
     if (found) {
       cnt += 1;
-      sdeg += __ldg(&outdeg[v]);
+      sdeg += __ldg(&outdeg[r0 + v]);
     }
   }
 #pragma unroll
@@ -713,7 +716,7 @@ static gi_status bfs_impl(gi_graph g, int32_t source, const gi_bfs_opts& o, int3
         const int sw = (int)std::min<int64_t>(words, smem_words);
         k_bfs_pull_smem<OffT><<<2 * sms, 1024, (size_t)sw * 4, st>>>(g->bitmap[bc].as<uint32_t>(),
                                                                  g->bitmap[bc ^ 1].as<uint32_t>(), parent, csc_off,
-                                                                 g->csc_idx.as<int32_t>(), outdeg, n, sw, nxt);
+                                                                 g->csc_idx.as<int32_t>(), outdeg, n, sw, nxt, 0);
       }
       bc ^= 1;
       in_bitmap = true;
@@ -788,7 +791,187 @@ static gi_status bfs_impl(gi_graph g, int32_t source, const gi_bfs_opts& o, int3
   return GI_OK;
 }
 
+// ---------------------------------------------------------------------------------------------
+// Multi-GPU BFS: each rank owns the destinations [r0, r0 + nr)
+// and their parents; the frontier is a replicated bitmap. Per level:
+//   pull: owned unvisited rows scan their in-edges against the replicated
+//         bitmap (k_bfs_pull_smem with a row offset);
+//   push: every rank turns the replicated bitmap into the same queue and
+//         expands only the edges into its range (local CSR by source),
+//         claiming with CAS and setting bits of its own bitmap words;
+//   exchange: allgatherv of the owned bitmap words + allreduce of
+//         (|F|, sum outdeg F); the direction decision is identical everywhere.
+// The owned parent slices are allgathered once at the end.
+namespace {
+
+template <typename OffT>
+struct LocalFrontierDegree {
+  const OffT* __restrict__ off;
+  const int32_t* __restrict__ q;
+  int64_t nf;
+  __host__ __device__ long long operator()(const int64_t& i) const {
+    return i < nf ? (long long)(off[q[i] + 1] - off[q[i]]) : 0;
+  }
+};
+
+template <typename OffT>
+__global__ void __launch_bounds__(256) k_dist_push(const int32_t* __restrict__ q, int64_t nf,
+                                                   const long long* __restrict__ pre, long long E,
+                                                   const OffT* __restrict__ off, const int32_t* __restrict__ idx,
+                                                   const int32_t* __restrict__ outdeg, int32_t* parent, int64_t r0,
+                                                   uint32_t* __restrict__ fnext, int64_t* __restrict__ cnext) {
+  __shared__ FlatSmem sm;
+  long long cnt = 0, sdeg = 0;
+  flat_edges<OffT>(q, nf, pre, E, off, idx, sm, [&](bool valid, int32_t u, int32_t v) {
+    if (valid) {
+      int32_t* p = &parent[v - r0];
+      if (*(volatile int32_t*)p == -1 && atomicCAS(p, -1, u) == -1) {
+        atomicOr(&fnext[v >> 5], 1u << (v & 31));
+        cnt += 1;
+        sdeg += __ldg(&outdeg[v]);
+      }
+    }
+  });
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    sdeg += __shfl_xor_sync(0xffffffffu, sdeg, o);
+  }
+  if ((threadIdx.x & 31) == 0 && cnt) {
+    atomicAdd((unsigned long long*)&cnext[0], (unsigned long long)cnt);
+    atomicAdd((unsigned long long*)&cnext[1], (unsigned long long)sdeg);
+  }
+}
+
+__global__ void k_dist_init(int32_t s_in, const int32_t* __restrict__ inv, const int32_t* __restrict__ outdeg,
+                            int64_t r0, int64_t nr, int32_t* __restrict__ parent, uint32_t* __restrict__ bm,
+                            int64_t* __restrict__ h2) {
+  const int32_t s = inv ? inv[s_in] : s_in;
+  bm[s >> 5] = 1u << (s & 31);
+  if (s >= r0 && s < r0 + nr) parent[s - r0] = s;
+  h2[0] = 1;
+  h2[1] = outdeg[s];
+}
+
+}  // namespace
+
+template <typename OffT>
+static gi_status bfs_dist_impl(gi_graph g, int32_t source, const gi_bfs_opts& o, int32_t* d_out, gi_bfs_stats* stats) {
+  gi_context ctx = g->ctx;
+  Comm* C = ctx->comm;
+  cudaStream_t st = ctx->stream;
+  const int sms = ctx->num_sms;
+  const int64_t n = g->n, nr = g->nr, r0 = g->r0, m = g->m;
+  const int64_t words = (n + 31) >> 5;
+  const int div = o.threshold_div > 0 ? o.threshold_div : 20;
+  if (!g->parent.p) {
+    GI_TRY(g->parent.alloc((n + 1) * sizeof(int32_t)));  // owned slice first, then the gathered full vector
+    GI_TRY(g->queue[0].alloc((n + 1) * sizeof(int32_t)));
+    for (int k = 0; k < 2; ++k) GI_TRY(g->bitmap[k].alloc((words + 1) * sizeof(uint32_t)));
+    GI_TRY(g->counters.alloc(8 * sizeof(int64_t)));
+    GI_TRY(g->bfs_pre.alloc((n + 2) * sizeof(long long)));
+    size_t tb = 0;
+    cub::TransformInputIterator<long long, LocalFrontierDegree<OffT>, cub::CountingInputIterator<int64_t>> it(
+        cub::CountingInputIterator<int64_t>(0), LocalFrontierDegree<OffT>{g->csr_off.as<OffT>(), g->queue[0].as<int32_t>(), 0});
+    GI_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, it, g->bfs_pre.as<long long>(), n + 1, st));
+    GI_TRY(g->bfs_scan_tmp.alloc(tb));
+  }
+  DevBuf parent_full;
+  GI_TRY(parent_full.alloc((n + 1) * sizeof(int32_t)));
+  int32_t* parent = g->parent.as<int32_t>();
+  int64_t* cnt = g->counters.as<int64_t>();
+  unsigned long long* aux = reinterpret_cast<unsigned long long*>(cnt + 4);
+  int64_t* h = ctx->h_scratch;
+  const OffT* csr_off = g->csr_off.as<OffT>();
+  const OffT* csc_off = g->csc_off.as<OffT>();
+  const int32_t* outdeg = g->outdeg.as<int32_t>();
+  const int P = C->nranks;
+  std::vector<int64_t> wslice(P + 1), pslice(P + 1);
+  for (int p = 0; p <= P; ++p) {
+    wslice[p] = std::min<int64_t>((g->bounds[p] + 31) >> 5, words) * 4;
+    pslice[p] = g->bounds[p] * 4;
+  }
+  gi_bfs_stats S{};
+  int bc = 0;
+  GI_CUDA(cudaMemsetAsync(parent, 0xFF, (nr + 1) * sizeof(int32_t), st));
+  GI_CUDA(cudaMemsetAsync(g->bitmap[bc].p, 0, words * sizeof(uint32_t), st));
+  k_dist_init<<<1, 1, 0, st>>>(source, g->relabeled ? g->inv.as<int32_t>() : nullptr, outdeg, r0, nr, parent,
+                               g->bitmap[bc].as<uint32_t>(), cnt);
+  S.launches++;
+  static int smem_words = -1;
+  if (smem_words < 0) {
+    int optin = 0, per_sm = 0;
+    GI_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
+    GI_CUDA(cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, ctx->device));
+    smem_words = std::min(optin - 2048, per_sm / 2 - 2048) / 4;
+    GI_CUDA(cudaFuncSetAttribute(k_bfs_pull_smem<OffT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_words * 4));
+  }
+  for (int64_t level = 0;; ++level) {
+    GI_CUDA(cudaMemcpyAsync(h, cnt, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    GI_CUDA(stream_wait(st));
+    const int64_t nf = h[0], sdeg = h[1];
+    if (nf == 0) break;
+    bool pull;
+    if (o.policy == GI_BFS_PUSH_ONLY) pull = false;
+    else if (o.policy == GI_BFS_PULL_ONLY) pull = level > 0;
+    else pull = (nf + sdeg) > m / div;
+    GI_CUDA(cudaMemsetAsync(cnt, 0, 2 * sizeof(int64_t), st));
+    GI_CUDA(cudaMemsetAsync(g->bitmap[bc ^ 1].p, 0, words * sizeof(uint32_t), st));
+    if (pull) {
+      const int sw = (int)std::min<int64_t>(words, smem_words);
+      if (nr > 0)
+        k_bfs_pull_smem<OffT><<<2 * sms, 1024, (size_t)sw * 4, st>>>(g->bitmap[bc].as<uint32_t>(),
+                                                                     g->bitmap[bc ^ 1].as<uint32_t>(), parent, csc_off,
+                                                                     g->csc_idx.as<int32_t>(), outdeg, nr, sw, cnt, r0);
+      S.pull_levels++;
+    } else {
+      GI_CUDA(cudaMemsetAsync(aux, 0, sizeof(unsigned long long), st));
+      k_b2q<<<grid_for(words, 256, sms), 256, 0, st>>>(g->bitmap[bc].as<uint32_t>(), words, g->queue[0].as<int32_t>(),
+                                                       aux);
+      cub::TransformInputIterator<long long, LocalFrontierDegree<OffT>, cub::CountingInputIterator<int64_t>> it(
+          cub::CountingInputIterator<int64_t>(0), LocalFrontierDegree<OffT>{csr_off, g->queue[0].as<int32_t>(), nf});
+      size_t tb = g->bfs_scan_tmp.bytes;
+      GI_CUDA(cub::DeviceScan::ExclusiveSum(g->bfs_scan_tmp.p, tb, it, g->bfs_pre.as<long long>(), nf + 1, st));
+      GI_CUDA(cudaMemcpyAsync(h + 2, g->bfs_pre.as<long long>() + nf, sizeof(long long), cudaMemcpyDeviceToHost, st));
+      GI_CUDA(stream_wait(st));
+      const long long E = h[2];
+      if (E > 0) {
+        const int grid = (int)std::min<int64_t>(ceil_div(E, kFlatCH), (int64_t)sms * 8);
+        k_dist_push<OffT><<<grid, 256, 0, st>>>(g->queue[0].as<int32_t>(), nf, g->bfs_pre.as<long long>(), E, csr_off,
+                                                g->csr_idx.as<int32_t>(), outdeg, parent, r0,
+                                                g->bitmap[bc ^ 1].as<uint32_t>(), cnt);
+      }
+      S.launches += 2;
+    }
+    GI_CUDA(cudaGetLastError());
+    GI_TRY(C->allgatherv(g->bitmap[bc ^ 1].p, wslice, st));
+    GI_TRY(C->allreduce_i64(cnt, 2, st));
+    bc ^= 1;
+    S.launches++;
+    S.levels++;
+  }
+  // gather the owned parent slices, then translate to input ids
+  GI_CUDA(cudaMemcpyAsync(parent_full.as<int32_t>() + r0, parent, nr * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
+  GI_TRY(C->allgatherv(parent_full.p, pslice, st));
+  GI_CUDA(cudaMemsetAsync(aux + 1, 0, 2 * sizeof(unsigned long long), st));
+  k_bfs_finish<<<grid_for(n, 256, sms), 256, 0, st>>>(parent_full.as<int32_t>(), n,
+                                                      g->relabeled ? g->perm.as<int32_t>() : nullptr, outdeg, d_out,
+                                                      aux + 1);
+  S.launches++;
+  GI_CUDA(cudaGetLastError());
+  GI_CUDA(cudaMemcpyAsync(h, aux + 1, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  GI_CUDA(stream_wait(st));
+  S.reached = h[0];
+  S.edges_traversed = h[1];
+  if (stats) *stats = S;
+  return GI_OK;
+}
+
 gi_status bfs_run(gi_graph g, int32_t source, const gi_bfs_opts& o, int32_t* d_out, gi_bfs_stats* stats) {
+  if (g->ctx->nranks > 1) {
+    if (g->off64) return bfs_dist_impl<int64_t>(g, source, o, d_out, stats);
+    return bfs_dist_impl<int32_t>(g, source, o, d_out, stats);
+  }
   if (g->off64) return bfs_impl<int64_t>(g, source, o, d_out, stats);
   return bfs_impl<int32_t>(g, source, o, d_out, stats);
 }

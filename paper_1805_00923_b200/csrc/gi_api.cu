@@ -295,6 +295,7 @@ gi_status gi_graph_out_degrees(gi_graph g, int32_t* outdeg) {
 gi_status gi_graph_in_degrees(gi_graph g, int32_t* indeg) {
   GI_GUARD_BEGIN
   if (!g || (!indeg && g->n > 0)) return fail(GI_ERR_INVALID_ARGUMENT, "gi_graph_in_degrees: NULL argument");
+  if (g->ctx->nranks > 1) return fail(GI_ERR_UNSUPPORTED, "gi_graph_in_degrees: single-GPU graphs only");
   gi_context ctx = g->ctx;
   GI_CUDA(cudaSetDevice(ctx->device));
   if (g->n == 0) return GI_OK;
@@ -315,6 +316,7 @@ gi_status gi_graph_in_degrees(gi_graph g, int32_t* indeg) {
 gi_status gi_graph_csr(gi_graph g, int64_t* off, int32_t* idx) {
   GI_GUARD_BEGIN
   if (!g || !off || (!idx && g->m > 0)) return fail(GI_ERR_INVALID_ARGUMENT, "gi_graph_csr: NULL argument");
+  if (g->ctx->nranks > 1) return fail(GI_ERR_UNSUPPORTED, "gi_graph_csr: single-GPU graphs only");
   gi_context ctx = g->ctx;
   cudaStream_t st = ctx->stream;
   GI_CUDA(cudaSetDevice(ctx->device));

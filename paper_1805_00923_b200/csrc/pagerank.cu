@@ -15,6 +15,7 @@
 // per edge into an accumulator + a vertex kernel — the parity form.
 #include "gi_internal.cuh"
 #include "pr_common.cuh"
+#include "comm.cuh"
 
 namespace gi {
 namespace {
@@ -85,7 +86,7 @@ __global__ void __launch_bounds__(kPullThreads) k_pr_pull(PrArgs A) {
 
 // ---------------------------------------------------------------- push (K5)
 template <typename OffT>
-__global__ void __launch_bounds__(256) k_pr_push(int64_t n, const OffT* __restrict__ off,
+__global__ void __launch_bounds__(256) k_pr_push(int64_t n, int64_t row0, const OffT* __restrict__ off,
                                                  const int32_t* __restrict__ idx, const float* __restrict__ cin,
                                                  double* __restrict__ acc) {
   const int lane = threadIdx.x & 31;
@@ -95,7 +96,7 @@ __global__ void __launch_bounds__(256) k_pr_push(int64_t n, const OffT* __restri
     const float c = __ldg(&cin[u]);
     if (c == 0.f) continue;
     for (int64_t j = (int64_t)off[u] + lane; j < (int64_t)off[u + 1]; j += 32)
-      atomicAdd(&acc[__ldg(&idx[j])], (double)c);  // result unused -> RED.E.ADD.F64 (fp64: hub rows sum
+      atomicAdd(&acc[__ldg(&idx[j]) - row0], (double)c);  // result unused -> RED.E.ADD.F64 (fp64: hub rows sum
                                                     // 1e5+ terms; fp32 atomics drift past 1e-4)
   }
 }
@@ -129,6 +130,13 @@ __global__ void __launch_bounds__(256) k_pr_init(int64_t n, const int32_t* __res
   if (threadIdx.x == 0 && bs != 0.0) atomicAdd(&dbuf[0], bs);
 }
 
+// out[perm[v]] = in[v] (internal ids -> input ids)
+__global__ void k_permute_out(const float* __restrict__ in, const int32_t* __restrict__ perm, int64_t n,
+                              float* __restrict__ out) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x)
+    out[perm ? perm[v] : v] = in[v];
+}
+
 __global__ void k_fill(float* __restrict__ out, int64_t n, float v) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     out[i] = v;
@@ -141,17 +149,30 @@ gi_status pagerank_run(gi_graph g, int32_t iters, double damping, const gi_pr_op
   gi_context ctx = g->ctx;
   cudaStream_t st = ctx->stream;
   const int sms = ctx->num_sms;
-  const int64_t n = g->n, m = g->m;
+  const int64_t n = g->n;                 // global vertices
+  const int64_t nr = g->nr, ml = g->ml;   // rows and edges held by this rank
+  const bool dist = ctx->nranks > 1;
   gi_pr_stats S{};
   int kernel = o.direction;
-  if (kernel == GI_PR_PULL) kernel = (n > 0 && m > 0 && seg_build(g, o.segment_size) == GI_OK) ? GI_PR_PULL_SEGMENTED : GI_PR_PULL_DIRECT;
+  if (kernel == GI_PR_PULL) kernel = (nr > 0 && ml > 0 && seg_build(g, o.segment_size) == GI_OK) ? GI_PR_PULL_SEGMENTED : GI_PR_PULL_DIRECT;
   else if (kernel == GI_PR_PULL_SEGMENTED) {
-    if (n > 0 && m > 0) GI_TRY(seg_build(g, o.segment_size));
+    if (nr > 0 && ml > 0) GI_TRY(seg_build(g, o.segment_size));
     else kernel = GI_PR_PULL_DIRECT;
+  }
+  if (dist) {  // every rank must run the same kernel family (collective call sequence)
+    DevBuf kk;
+    GI_TRY(kk.alloc(sizeof(int32_t)));
+    int32_t mine = kernel == GI_PR_PULL_SEGMENTED ? 1 : 0;
+    GI_CUDA(cudaMemcpyAsync(kk.p, &mine, sizeof(int32_t), cudaMemcpyHostToDevice, st));
+    GI_TRY(ctx->comm->allreduce_i32(kk.as<int32_t>(), 1, st));
+    int32_t all = 0;
+    GI_CUDA(cudaMemcpyAsync(&all, kk.p, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    GI_CUDA(cudaStreamSynchronize(st));
+    if (o.direction == GI_PR_PULL && all != 0 && all != ctx->nranks) kernel = GI_PR_PULL_DIRECT;
   }
   S.kernel = kernel;
   const int osz = g->off64 ? 8 : 4;
-  S.bytes_alg_per_iter = 4 * m + (int64_t)(osz + 12) * n;
+  S.bytes_alg_per_iter = 4 * ml + (int64_t)(osz + 12) * nr;
   if (n == 0) {
     if (stats) *stats = S;
     return GI_OK;
@@ -169,14 +190,23 @@ gi_status pagerank_run(gi_graph g, int32_t iters, double damping, const gi_pr_op
   if (!g->dbuf.p) GI_TRY(g->dbuf.alloc(4 * sizeof(double)));
   if (kernel == GI_PR_PUSH) {
     if (!g->push_sum.p) {
-      GI_TRY(g->push_sum.alloc(n * sizeof(double)));
-      GI_CUDA(cudaMemsetAsync(g->push_sum.p, 0, n * sizeof(double), st));
+      GI_TRY(g->push_sum.alloc((nr + 1) * sizeof(double)));
+      GI_CUDA(cudaMemsetAsync(g->push_sum.p, 0, (nr + 1) * sizeof(double), st));
     }
   } else if (!g->split_acc.p) {
-    GI_TRY(g->split_acc.alloc(n * sizeof(double)));
-    GI_TRY(g->split_cnt.alloc(n * sizeof(int32_t)));
-    GI_CUDA(cudaMemsetAsync(g->split_acc.p, 0, n * sizeof(double), st));
-    GI_CUDA(cudaMemsetAsync(g->split_cnt.p, 0, n * sizeof(int32_t), st));
+    GI_TRY(g->split_acc.alloc((nr + 1) * sizeof(double)));
+    GI_TRY(g->split_cnt.alloc((nr + 1) * sizeof(int32_t)));
+    GI_CUDA(cudaMemsetAsync(g->split_acc.p, 0, (nr + 1) * sizeof(double), st));
+    GI_CUDA(cudaMemsetAsync(g->split_cnt.p, 0, (nr + 1) * sizeof(int32_t), st));
+  }
+  // multi-GPU: contrib slices exchanged every iteration; the final ranks
+  // gathered in internal order, then permuted to input ids
+  std::vector<int64_t> cb;
+  DevBuf rank_int;
+  if (dist) {
+    cb.resize(g->bounds.size());
+    for (size_t i = 0; i < cb.size(); ++i) cb[i] = g->bounds[i] * (int64_t)sizeof(float);
+    GI_TRY(rank_int.alloc(n * sizeof(float)));
   }
 
   cudaEvent_t ev[2] = {nullptr, nullptr}, tot[2] = {nullptr, nullptr};
@@ -193,8 +223,9 @@ gi_status pagerank_run(gi_graph g, int32_t iters, double damping, const gi_pr_op
   S.aux_launches = 1;
 
   PrArgs A{};
-  A.n = n;
-  A.m = m;
+  A.n = nr;
+  A.m = ml;
+  A.row0 = g->r0;
   A.outdeg = g->outdeg.as<int32_t>();
   A.dbuf = g->dbuf.as<double>();
   A.base = (float)((1.0 - damping) / (double)n);
@@ -203,24 +234,25 @@ gi_status pagerank_run(gi_graph g, int32_t iters, double damping, const gi_pr_op
   A.uniform = o.dangling == GI_DANGLING_UNIFORM;
   A.split_acc = g->split_acc.as<double>();
   A.split_cnt = g->split_cnt.as<int32_t>();
-  A.perm = g->relabeled ? g->perm.as<int32_t>() : nullptr;
+  A.perm = (g->relabeled && !dist) ? g->perm.as<int32_t>() : nullptr;
   float edge_ms = 0.f;
   for (int it = 0; it < iters; ++it) {
     A.it = it;
     A.cin = g->contrib[it & 1].as<float>();
     A.cout = g->contrib[(it + 1) & 1].as<float>();
-    A.rank_out = (it == iters - 1) ? d_out : nullptr;
+    A.rank_out = (it == iters - 1) ? (dist ? rank_int.as<float>() : d_out) : nullptr;
     if (o.profile) GI_CUDA(cudaEventRecord(ev[0], st));
+    if (dist) GI_CUDA(cudaMemsetAsync(A.dbuf + (it + 1) % 3, 0, sizeof(double), st));  // ranks without rows
     if (kernel == GI_PR_PUSH) {
       const int grid = grid_for(n * 32, 256, sms, 16);
       if (g->off64)
-        k_pr_push<int64_t><<<grid, 256, 0, st>>>(n, g->csr_off.as<int64_t>(), g->csr_idx.as<int32_t>(), A.cin,
+        k_pr_push<int64_t><<<grid, 256, 0, st>>>(n, g->r0, g->csr_off.as<int64_t>(), g->csr_idx.as<int32_t>(), A.cin,
                                                  g->push_sum.as<double>());
       else
-        k_pr_push<int32_t><<<grid, 256, 0, st>>>(n, g->csr_off.as<int32_t>(), g->csr_idx.as<int32_t>(), A.cin,
+        k_pr_push<int32_t><<<grid, 256, 0, st>>>(n, g->r0, g->csr_off.as<int32_t>(), g->csr_idx.as<int32_t>(), A.cin,
                                                  g->push_sum.as<double>());
       if (o.profile) GI_CUDA(cudaEventRecord(ev[1], st));
-      k_pr_vertex<<<grid_for(n, 256, sms), 256, 0, st>>>(A, g->push_sum.as<double>());
+      k_pr_vertex<<<grid_for(nr, 256, sms), 256, 0, st>>>(A, g->push_sum.as<double>());
       S.aux_launches++;
     } else if (kernel == GI_PR_PULL_SEGMENTED) {
       GI_TRY(seg_edge_pass(g, A));
@@ -232,15 +264,26 @@ gi_status pagerank_run(gi_graph g, int32_t iters, double damping, const gi_pr_op
       A.idx = g->csc_idx.as<int32_t>();
       if (g->off64) {
         A.off = g->csc_off.as<int64_t>();
-        k_pr_pull<int64_t><<<(unsigned)g->ntiles, kPullThreads, 0, st>>>(A);
+        if (g->ntiles > 0) k_pr_pull<int64_t><<<(unsigned)g->ntiles, kPullThreads, 0, st>>>(A);
       } else {
         A.off = g->csc_off.as<int32_t>();
-        k_pr_pull<int32_t><<<(unsigned)g->ntiles, kPullThreads, 0, st>>>(A);
+        if (g->ntiles > 0) k_pr_pull<int32_t><<<(unsigned)g->ntiles, kPullThreads, 0, st>>>(A);
       }
       if (o.profile) GI_CUDA(cudaEventRecord(ev[1], st));
     }
     GI_CUDA(cudaGetLastError());
     S.edge_launches++;
+    if (dist) {  // dangling partials (allreduce) + contrib slices (allgatherv)
+      GI_TRY(ctx->comm->allreduce_f64(A.dbuf + (it + 1) % 3, 1, st));
+      GI_TRY(ctx->comm->allgatherv(A.cout, cb, st));
+      if (it == iters - 1) {
+        std::vector<int64_t> rb = cb;
+        GI_TRY(ctx->comm->allgatherv(rank_int.p, rb, st));
+        k_permute_out<<<grid_for(n, 256, sms), 256, 0, st>>>(rank_int.as<float>(),
+                                                             g->relabeled ? g->perm.as<int32_t>() : nullptr, n, d_out);
+        S.aux_launches++;
+      }
+    }
     if (o.profile) {
       GI_CUDA(cudaEventSynchronize(ev[1]));
       float ms = 0.f;

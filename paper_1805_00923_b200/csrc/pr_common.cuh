@@ -15,7 +15,8 @@
 namespace gi {
 
 struct PrArgs {
-  int64_t n, m;
+  int64_t n, m;     // CSC rows and edges held here (single GPU: all)
+  int64_t row0;     // global id of local row 0 (destination partition)
   const void* off;
   const int32_t* __restrict__ idx;
   const int32_t* __restrict__ tile_rows;
@@ -34,12 +35,14 @@ struct PrArgs {
 };
 
 // vertex update (a3): r' = base + d (s + D/n); contrib' = r'/outdeg; dangling partial
+// (r is a local row; outdeg, contrib and perm are indexed by global id row0 + r)
 __device__ __forceinline__ void pr_epilogue(const PrArgs& A, int64_t r, float s, float dn, double& dpart) {
+  const int64_t v = A.row0 + r;
   const float rn = A.base + A.damp * (s + dn);
-  const int od = __ldg(&A.outdeg[r]);
-  A.cout[r] = od > 0 ? rn / (float)od : 0.f;
+  const int od = __ldg(&A.outdeg[v]);
+  A.cout[v] = od > 0 ? rn / (float)od : 0.f;
   if (od == 0) dpart += (double)rn;
-  if (A.rank_out) A.rank_out[A.perm ? __ldg(&A.perm[r]) : r] = rn;
+  if (A.rank_out) A.rank_out[A.perm ? __ldg(&A.perm[v]) : v] = rn;
 }
 
 // Block sum of a double; result valid in thread 0. sred: >= 32 doubles.

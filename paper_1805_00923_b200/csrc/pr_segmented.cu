@@ -257,7 +257,7 @@ __global__ void __launch_bounds__(256) k_pr_merge(PrArgs A, const OffT* __restri
       if (v < A.n) {
         a[k] = (int64_t)__ldg(&pstart[v]);
         b[k] = (int64_t)__ldg(&pstart[v + 1]);
-        od[k] = __ldg(&A.outdeg[v]);
+        od[k] = __ldg(&A.outdeg[A.row0 + v]);
       }
     }
     float s[kV];
@@ -275,10 +275,11 @@ __global__ void __launch_bounds__(256) k_pr_merge(PrArgs A, const OffT* __restri
     for (int k = 0; k < kV; ++k) {
       const int64_t v = base + threadIdx.x + (int64_t)k * blockDim.x;
       if (v < A.n) {
+        const int64_t gv = A.row0 + v;
         const float rn = A.base + A.damp * (s[k] + dn);
-        A.cout[v] = od[k] > 0 ? rn / (float)od[k] : 0.f;
+        A.cout[gv] = od[k] > 0 ? rn / (float)od[k] : 0.f;
         if (od[k] == 0) dpart += (double)rn;
-        if (A.rank_out) A.rank_out[A.perm ? __ldg(&A.perm[v]) : v] = rn;
+        if (A.rank_out) A.rank_out[A.perm ? __ldg(&A.perm[gv]) : gv] = rn;
       }
     }
   }
@@ -432,10 +433,10 @@ static gi_status seg_build_t(gi_graph g, int Z) {
   gi_context ctx = g->ctx;
   cudaStream_t st = ctx->stream;
   const int sms = ctx->num_sms;
-  const int64_t n = g->n, m = g->m;
+  const int64_t n = g->nr, m = g->ml;  // CSC rows (owned destinations) and local edges
   const OffT* off = g->csc_off.as<OffT>();
   const int32_t* idx = g->csc_idx.as<int32_t>();
-  const int S = (int)ceil_div(n, Z);
+  const int S = (int)ceil_div(g->n, Z);  // segments over all sources
   // ---- piece layout: (segment, destination) runs of the CSC
   DevBuf flag, ex, pdm, seg, seg2, eid, order, spdm, tmp, nsel, seg_e, pc_off, pc_slot, idx16;
   GI_TRY(flag.alloc((m + 1) * sizeof(int32_t)));
@@ -592,7 +593,7 @@ gi_status seg_build(gi_graph g, int segment_size) {
   if (segment_size > 0) Z = std::max(32, std::min(Z, segment_size) & ~3);
   if (g->seg_Z == Z) return GI_OK;
   g->seg_Z = 0;
-  if (g->m == 0 || g->n == 0) return fail(GI_ERR_UNSUPPORTED, "segmented pull: empty graph");
+  if (g->ml == 0 || g->nr == 0) return fail(GI_ERR_UNSUPPORTED, "segmented pull: empty graph");
   if (g->off64) return seg_build_t<int64_t>(g, Z);
   return seg_build_t<int32_t>(g, Z);
 }
@@ -644,10 +645,10 @@ gi_status seg_edge_pass(gi_graph g, const PrArgs& A) {
 gi_status seg_vertex_pass(gi_graph g, const PrArgs& A) {
   cudaStream_t st = g->ctx->stream;
   if (g->off64)
-    k_pr_merge<int64_t><<<grid_for(ceil_div(g->n, 4), 256, g->ctx->num_sms, 8), 256, 0, st>>>(A, g->seg_pstart.as<int64_t>(),
+    k_pr_merge<int64_t><<<grid_for(ceil_div(g->nr, 4), 256, g->ctx->num_sms, 8), 256, 0, st>>>(A, g->seg_pstart.as<int64_t>(),
                                                                                    g->seg_partial.as<float>());
   else
-    k_pr_merge<int32_t><<<grid_for(ceil_div(g->n, 4), 256, g->ctx->num_sms, 8), 256, 0, st>>>(A, g->seg_pstart.as<int32_t>(),
+    k_pr_merge<int32_t><<<grid_for(ceil_div(g->nr, 4), 256, g->ctx->num_sms, 8), 256, 0, st>>>(A, g->seg_pstart.as<int32_t>(),
                                                                                    g->seg_partial.as<float>());
   GI_CUDA(cudaGetLastError());
   return GI_OK;

@@ -77,6 +77,11 @@ _SIGS = {
                                 ctypes.POINTER(_vp)], _st),
     "gi_context_destroy": ([_vp], _st),
     "gi_context_rank": ([_vp, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)], _st),
+    "gi_local_group_create": ([ctypes.c_int, ctypes.POINTER(_vp)], _st),
+    "gi_local_group_destroy": ([_vp], _st),
+    "gi_context_create_local": ([ctypes.c_int, _vp, _vp, ctypes.c_int, ctypes.POINTER(_vp)], _st),
+    "gi_partition_ranges": ([_i64, ctypes.c_int, _vp, _vp], _st),
+    "gi_graph_partition": ([_vp, ctypes.POINTER(_i64), ctypes.POINTER(_i64), ctypes.POINTER(_i64)], _st),
     "gi_graph_create": ([_vp, _i64, _i64, _vp, _vp, ctypes.c_uint32, ctypes.POINTER(_vp)], _st),
     "gi_graph_destroy": ([_vp], _st),
     "gi_graph_num_vertices": ([_vp, ctypes.POINTER(_i64)], _st),
@@ -155,6 +160,38 @@ def gi_context_create_dist(device: int, stream: int | None, rank: int, nranks: i
     _check(_lib.gi_context_create_dist(device, stream or None, rank, nranks, uid, ctypes.byref(out)),
            "gi_context_create_dist")
     return out.value
+
+
+def gi_local_group_create(nranks: int) -> int:
+    out = _vp()
+    _check(_lib.gi_local_group_create(nranks, ctypes.byref(out)), "gi_local_group_create")
+    return out.value
+
+
+def gi_local_group_destroy(grp: int) -> None:
+    _check(_lib.gi_local_group_destroy(grp), "gi_local_group_destroy")
+
+
+def gi_context_create_local(device: int, stream: int | None, grp: int, rank: int) -> int:
+    out = _vp()
+    _check(_lib.gi_context_create_local(device, stream or None, grp, rank, ctypes.byref(out)),
+           "gi_context_create_local")
+    return out.value
+
+
+def gi_partition_ranges(n: int, nranks: int, weight_prefix) -> np.ndarray:
+    pre = np.ascontiguousarray(weight_prefix, np.int64)
+    if pre.shape != (n + 1,):
+        raise ValueError("weight_prefix must have n + 1 entries")
+    out = np.empty(nranks + 1, np.int64)
+    _check(_lib.gi_partition_ranges(n, nranks, pre.ctypes.data, out.ctypes.data), "gi_partition_ranges")
+    return out
+
+
+def gi_graph_partition(g: int) -> tuple[int, int, int]:
+    lo, hi, ml = _i64(), _i64(), _i64()
+    _check(_lib.gi_graph_partition(g, ctypes.byref(lo), ctypes.byref(hi), ctypes.byref(ml)), "gi_graph_partition")
+    return lo.value, hi.value, ml.value
 
 
 def gi_context_destroy(ctx: int) -> None:
@@ -258,10 +295,17 @@ def gi_bfs_ex(g: int, source: int, out=None, policy: int = GI_BFS_AUTO, threshol
 
 # ------------------------------------------------------------------ RAII conveniences
 class Context:
-    def __init__(self, device: int = 0, stream: int | None = None):
+    def __init__(self, device: int = 0, stream: int | None = None, *, local_group: int | None = None,
+                 rank: int = 0, nccl: tuple | None = None):
+        """local_group: simulated ranks in this process (tests); nccl: (rank, nranks, unique_id)."""
         import weakref
 
-        self.handle = gi_context_create(device, stream)
+        if local_group is not None:
+            self.handle = gi_context_create_local(device, stream, local_group, rank)
+        elif nccl is not None:
+            self.handle = gi_context_create_dist(device, stream, nccl[0], nccl[1], nccl[2])
+        else:
+            self.handle = gi_context_create(device, stream)
         self._graphs = weakref.WeakSet()
 
     def close(self):
@@ -315,3 +359,7 @@ class Graph:
 
     def csr(self):
         return gi_graph_csr(self.handle)
+
+    def partition(self):
+        """(lo, hi, local_edges): owned destination range in internal ids."""
+        return gi_graph_partition(self.handle)
