@@ -20,9 +20,11 @@ roofline: the pull-PageRank edge kernel (dominant), algorithmic bytes
 cpu_baseline: the oracle (oracle/, plain C, OpenMP) on a bounded sample of
          the same graph (2 PR iterations + 2 BFS sources).
 
-Multi-GPU (torchrun, one process per GPU): the units of this workload are
-independent problems, so N > 1 runs N replicas (weak scaling, no data-path
-collective); see DESIGN.md "Multi-GPU".
+Multi-GPU (torchrun, one process per GPU): by default the graph is
+destination-partitioned over the N GPUs (each rank passes a share of the
+edge list; NCCL allgather of contrib slices / frontier bitmaps each iteration
+or level, SURVEY §8(e)) and the same single job is timed (strong scaling);
+--mode replicas runs N independent copies instead (weak scaling).
 """
 from __future__ import annotations
 
@@ -53,6 +55,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--pr-direction", default="pull", choices=["pull", "push", "direct", "segmented"])
+    ap.add_argument("--mode", default="partition", choices=["partition", "replicas"],
+                    help="N > 1: destination-partitioned graph over NCCL (strong scaling, SURVEY §8(e)) or "
+                         "independent replicas (weak scaling)")
     return ap.parse_args()
 
 
@@ -221,8 +226,18 @@ def run_ours(args):
     from paper_1805_00923_b200 import gi
 
     stream = torch.cuda.Stream()
-    ctx = gi.Context(dev, stream.cuda_stream)
+    partition = world > 1 and args.mode == "partition"
+    if partition:  # NCCL communicator of the library; torch.distributed only ships the unique id
+        uid = torch.zeros(128, dtype=torch.uint8, device=dev)
+        if rank == 0:
+            uid.copy_(torch.frombuffer(bytearray(gi.gi_nccl_unique_id()), dtype=torch.uint8))
+        torch.distributed.broadcast(uid, 0)
+        ctx = gi.Context(dev, stream.cuda_stream, nccl=(rank, world, bytes(uid.cpu().numpy().tobytes())))
+    else:
+        ctx = gi.Context(dev, stream.cuda_stream)
     cfg, s, d, sources, gen_s = workload(args.config)
+    if partition:  # every rank passes its own share of the edge list; the graph is the union
+        s, d = s[rank::world].copy(), d[rank::world].copy()
     flags = gi.GI_DEFAULT_FLAGS | (gi.GI_SYMMETRIZE if cfg.symmetrize else 0)
     direction = {"pull": gi.GI_PR_PULL, "push": gi.GI_PR_PUSH, "direct": gi.GI_PR_PULL_DIRECT,
                  "segmented": gi.GI_PR_PULL_SEGMENTED}[args.pr_direction]
@@ -287,7 +302,8 @@ def run_ours(args):
         mx = tt.clone()
         torch.distributed.all_reduce(mx[:1], op=torch.distributed.ReduceOp.MAX)
         torch.distributed.all_reduce(tt[1:], op=torch.distributed.ReduceOp.SUM)
-        ms_max, edges_all = float(mx[0]), float(tt[1])
+        # partition: every rank reports the same global edge count (one job); replicas: N jobs
+        ms_max, edges_all = float(mx[0]), float(tt[1]) / (world if partition else 1)
     else:
         ms_max, edges_all = ms, float(tot_pr + tot_bfs)
     value = edges_all / (ms_max * 1e-3) / 1e9
@@ -323,7 +339,12 @@ def run_ours(args):
             g2.close()
         torch.cuda.synchronize()
         e2e_s = time.perf_counter() - t
-        e2e = {"value": e_edges / e2e_s / 1e9 * world, "unit": "GTEPS", "h2d_bytes_per_step": int(8 * len(s)),
+        if world > 1:
+            te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+            torch.distributed.all_reduce(te, op=torch.distributed.ReduceOp.MAX)
+            e2e_s = float(te[0])
+        e2e = {"value": e_edges / e2e_s / 1e9 * (1 if partition else world), "unit": "GTEPS",
+               "h2d_bytes_per_step": int(8 * len(s)),
                "d2h_bytes_per_step": int(4 * n * (1 + len(srcs))), "steps": e2e_steps,
                "includes": "gi_graph_create from pinned host edges + gi_pagerank + gi_bfs x sources, host outputs"}
 
@@ -335,13 +356,14 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": value, "unit": "GTEPS", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "scaling": "strong" if partition else "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded counter-based RMAT; stands in for LiveJournal, paper datasets unavailable)",
             "config": {"workload": f"{cfg.name} (BASELINE configs[{cfg.idx - 1}])", "n": n, "m": m,
                        "pr_iters": cfg.pr_iters, "damping": cfg.damping, "bfs_sources": len(srcs),
                        "pr_direction": args.pr_direction, "bfs_policy": "auto (m/20)",
                        "l2": "inputs larger than L2 (CSR+CSC ~ 8m bytes > 126 MB), no flush",
-                       "parallelism": f"replicas x{world}" if world > 1 else "single"},
+                       "parallelism": (f"dst-partition x{world} (NCCL allgather of contrib / frontier bitmap)"
+                                       if partition else f"replicas x{world}") if world > 1 else "single"},
             "e2e": e2e, "gpu_launches": launches, "roofline": roofline, "cpu_baseline": cpu, "clocks": clocks,
             "pr_gteps": cfg.pr_iters * m / (pr_ms * 1e-3) / 1e9, "pr_ms": pr_ms,
             "bfs_gteps": (tot_bfs / args.steps) / (bfs_ms * 1e-3) / 1e9 if bfs_ms > 0 else None,

@@ -734,7 +734,8 @@ static gi_status bfs_impl(gi_graph g, int32_t source, const gi_bfs_opts& o, int3
         size_t tb = g->bfs_scan_tmp.bytes;
         GI_CUDA(cub::DeviceScan::ExclusiveSum(g->bfs_scan_tmp.p, tb, it, g->bfs_pre.as<long long>(), nf, st));
         const int grid = (int)std::min<int64_t>(ceil_div(sdeg, kFlatCH), (int64_t)sms * 8);
-        if (sdeg >= kStampMin) {  // two-phase stamp + collect (no atomics on hub destinations)
+        static const int64_t stamp_min = getenv("GI_BFS_STAMP_MIN") ? atoll(getenv("GI_BFS_STAMP_MIN")) : kStampMin;
+        if (sdeg >= stamp_min) {  // two-phase stamp + collect (no atomics on hub destinations)
           if (!g->bfs_cand.p || ++g->bfs_epoch == 0) {
             if (!g->bfs_cand.p) GI_TRY(g->bfs_cand.alloc(n * sizeof(unsigned long long)));
             GI_CUDA(cudaMemsetAsync(g->bfs_cand.p, 0, n * sizeof(unsigned long long), st));
