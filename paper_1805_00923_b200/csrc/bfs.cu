@@ -24,6 +24,7 @@
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <cooperative_groups.h>
 #include <cub/cub.cuh>
 
@@ -575,6 +576,8 @@ __global__ void k_b2q(const uint32_t* __restrict__ bm, int64_t words, int32_t* _
 __global__ void __launch_bounds__(256) k_bfs_finish(const int32_t* __restrict__ parent, int64_t n,
                                                     const int32_t* __restrict__ perm, const int32_t* __restrict__ outdeg,
                                                     int32_t* __restrict__ out, unsigned long long* __restrict__ red) {
+  using Red = cub::BlockReduce<long long, 256>;
+  __shared__ typename Red::TempStorage t0, t1;
   long long reached = 0, edges = 0;
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
     const int32_t p = parent[v];
@@ -585,12 +588,10 @@ __global__ void __launch_bounds__(256) k_bfs_finish(const int32_t* __restrict__ 
       edges += outdeg[v];
     }
   }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    reached += __shfl_xor_sync(0xffffffffu, reached, o);
-    edges += __shfl_xor_sync(0xffffffffu, edges, o);
-  }
-  if ((threadIdx.x & 31) == 0 && reached) {
+  // one atomic pair per CTA (per-warp atomics on two addresses serialise at L2)
+  reached = Red(t0).Sum(reached);
+  edges = Red(t1).Sum(edges);
+  if (threadIdx.x == 0 && reached) {
     atomicAdd(&red[0], (unsigned long long)reached);
     atomicAdd(&red[1], (unsigned long long)edges);
   }
@@ -968,7 +969,28 @@ static gi_status bfs_dist_impl(gi_graph g, int32_t source, const gi_bfs_opts& o,
   return GI_OK;
 }
 
+// parent (internal ids, full n) -> input ids; reached vertices and their out-edges
+gi_status bfs_finish_output(gi_graph g, const int32_t* parent, int32_t* d_out, int64_t* reached, int64_t* edges) {
+  gi_context ctx = g->ctx;
+  cudaStream_t st = ctx->stream;
+  if (!g->counters.p) GI_TRY(g->counters.alloc((2 * kRing + 8) * sizeof(int64_t)));
+  unsigned long long* red = reinterpret_cast<unsigned long long*>(g->counters.as<int64_t>() + 2 * kRing + 6);
+  GI_CUDA(cudaMemsetAsync(red, 0, 2 * sizeof(unsigned long long), st));
+  k_bfs_finish<<<grid_for(g->n, 256, ctx->num_sms), 256, 0, st>>>(parent, g->n,
+                                                                 g->relabeled ? g->perm.as<int32_t>() : nullptr,
+                                                                 g->outdeg.as<int32_t>(), d_out, red);
+  GI_CUDA(cudaGetLastError());
+  int64_t* h = ctx->h_scratch;
+  GI_CUDA(cudaMemcpyAsync(h + 8, red, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  GI_CUDA(stream_wait(st));
+  *reached = h[8];
+  *edges = h[9];
+  return GI_OK;
+}
+
 gi_status bfs_run(gi_graph g, int32_t source, const gi_bfs_opts& o, int32_t* d_out, gi_bfs_stats* stats) {
+  static const char* impl = getenv("GI_BFS_IMPL");  // "host": the host-driven level loop (A/B comparisons)
+  if (g->ctx->nranks == 1 && !(impl && strcmp(impl, "host") == 0) && !o.profile) return bfs_fused(g, source, o, d_out, stats);
   if (g->ctx->nranks > 1) {
     if (g->off64) return bfs_dist_impl<int64_t>(g, source, o, d_out, stats);
     return bfs_dist_impl<int32_t>(g, source, o, d_out, stats);

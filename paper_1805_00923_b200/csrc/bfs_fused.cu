@@ -1,0 +1,448 @@
+// bfs_fused.cu — the whole direction-optimising BFS as ONE cooperative,
+// persistent kernel (single GPU).
+//
+// Every level of the host-driven loop in bfs.cu costs a device->host read of
+// two counters (|F|, sum outdeg F) before the direction (PAPER.md P:661-675,
+// R7) can be chosen: ~15-20 µs of round trip per level, a third of a config-2
+// BFS. Here every CTA reads the same counters after a grid barrier and takes
+// the same decision, so the host launches once per source.
+//
+// Data written by other CTAs in earlier levels (parent, bitmaps, queues) is
+// read with ld.global.cg (L2) so no stale L1 line survives a grid barrier.
+//
+// Per level l (frontier F_l held as bitmap bm[l%3] and, after push levels, as
+// queue q[l&1]; counters ring cnt[l%4]):
+//   pull (DensePull + bitvector + early exit): each
+//     warp owns one 32-vertex word; unvisited vertices probe in-edges (4 per
+//     step) against the frontier bitmap, whose hot prefix is staged in shared
+//     memory; the next bitmap word is the ballot (no atomics);
+//   push (SparsePush + CAS claim): if the frontier
+//     is only a bitmap it is compacted to a queue first (CTA-aggregated); then
+//     small frontiers (<= kFSmall vertices) are expanded by every CTA over an
+//     equal slice of their flattened edge list (each CTA scans the frontier's
+//     degrees itself), large ones by a grid-wide scan of degrees (two extra
+//     barriers) and the same flattened walk; claims append to the next queue
+//     with one atomic per CTA step and set the next bitmap bit;
+//   bm[(l+2)%3] and cnt[(l+2)%4] are cleared during level l (unused then).
+#include <cooperative_groups.h>
+
+#include <algorithm>
+#include <climits>
+#include <cub/cub.cuh>
+
+#include "gi_internal.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace gi {
+namespace {
+
+constexpr int kFT = 1024;        // threads per CTA
+constexpr int kFW = kFT / 32;    // warps per CTA
+constexpr int kFSmall = 4096;    // frontier size expanded by the per-CTA scan
+constexpr int kFChunk = kFT;     // frontier entries per scan chunk (large frontiers)
+
+template <typename OffT>
+struct FusedArgs {
+  const OffT* __restrict__ csr_off;
+  const int32_t* __restrict__ csr_idx;
+  const OffT* __restrict__ csc_off;
+  const int32_t* __restrict__ csc_idx;
+  const int32_t* __restrict__ outdeg;
+  int32_t* parent;
+  int32_t* q[2];
+  uint32_t* bm[3];
+  int64_t* cnt;        // 4-level ring of {|F|, sum outdeg F}
+  long long* tail;     // 4-level ring of queue tails (bitmap -> queue compaction)
+  long long* pre;      // per-entry exclusive prefix of degrees within its chunk
+  long long* ctot;     // chunk totals -> exclusive chunk offsets; ctot[nchunks] = E
+  int64_t* stats;      // [levels, pull levels]
+  int64_t n, mdiv;
+  int policy, sw;
+};
+
+struct FSmem {  // carved from dynamic shared memory, phase by phase
+  union {
+    struct {
+      int pre[kFSmall + 1];
+      int32_t u[kFSmall];
+    } small;
+    struct {
+      long long pre[kFChunk + 2];
+      int32_t u[kFChunk + 1];
+    } win;
+  };
+};
+
+__device__ __forceinline__ long long vload(const long long* p) { return *(volatile const long long*)p; }
+__device__ __forceinline__ int64_t vload(const int64_t* p) { return *(volatile const int64_t*)p; }
+
+// CTA-aggregated append of the lanes with `want` set: one atomic per CTA step.
+// Must be called by all threads of the CTA.
+__device__ __forceinline__ void cta_append(bool want, int32_t v, int32_t* __restrict__ q,
+                                           unsigned long long* __restrict__ tail, int* s_warp, long long* s_base) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const unsigned mask = __ballot_sync(0xffffffffu, want);
+  if (lane == 0) s_warp[w] = __popc(mask);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int tot = 0;
+    for (int i = 0; i < kFW; ++i) {
+      const int c = s_warp[i];
+      s_warp[i] = tot;
+      tot += c;
+    }
+    *s_base = tot ? (long long)atomicAdd(tail, (unsigned long long)tot) : 0;
+  }
+  __syncthreads();
+  if (want) q[*s_base + s_warp[w] + __popc(mask & ((1u << lane) - 1))] = v;
+  __syncthreads();
+}
+
+template <typename OffT>
+__global__ void __launch_bounds__(kFT, 2) k_bfs_fused(FusedArgs<OffT> A) {
+  extern __shared__ __align__(16) unsigned char fsmem[];
+  FSmem& sm = *reinterpret_cast<FSmem*>(fsmem);
+  uint32_t* sbits = reinterpret_cast<uint32_t*>(fsmem);  // pull phase: staged bitmap prefix
+  __shared__ int s_warp[kFW];
+  __shared__ long long s_base;
+  __shared__ long long s_red[2][kFW];
+  __shared__ union {
+    typename cub::BlockScan<int, kFT>::TempStorage i;
+    typename cub::BlockScan<long long, kFT>::TempStorage l;
+  } scan_tmp;
+  cg::grid_group grid = cg::this_grid();
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int64_t G = gridDim.x;
+  const int64_t words = (A.n + 31) >> 5;
+  bool qvalid = true;  // level 0's frontier {s} is a queue (and a bitmap)
+  int64_t level = 0, pulls = 0;
+  for (;;) {
+    const int64_t* c = A.cnt + 2 * (level % 4);
+    const int64_t nf = vload(c), sdeg = vload(c + 1);
+    if (nf == 0) break;
+    const bool pull = A.policy == GI_BFS_PULL_ONLY ? level > 0
+                                                   : (A.policy == GI_BFS_AUTO && nf + sdeg > A.mdiv);
+    uint32_t* bcur = A.bm[level % 3];
+    uint32_t* bnext = A.bm[(level + 1) % 3];
+    uint32_t* bzero = A.bm[(level + 2) % 3];
+    int32_t* qcur = A.q[level & 1];
+    int32_t* qnext = A.q[(level + 1) & 1];
+    int64_t* cn = A.cnt + 2 * ((level + 1) % 4);
+    if (blockIdx.x == 0 && tid == 0) {
+      A.cnt[2 * ((level + 2) % 4)] = 0;
+      A.cnt[2 * ((level + 2) % 4) + 1] = 0;
+      A.tail[(level + 2) % 4] = 0;
+    }
+    for (int64_t i = blockIdx.x * (int64_t)kFT + tid; i < words; i += G * kFT) bzero[i] = 0u;
+    long long fcnt = 0, fdeg = 0;  // this thread's share of |F_{l+1}| and its out-degrees
+
+    if (pull) {
+      ++pulls;
+      for (int i = tid; i < A.sw; i += kFT) sbits[i] = __ldcg(&bcur[i]);
+      __syncthreads();
+      const uint32_t lim = (uint32_t)A.sw * 32u;
+      for (int64_t wd = blockIdx.x * (int64_t)kFW + w; wd < words; wd += G * kFW) {
+        const int64_t v = (wd << 5) + lane;
+        bool found = false;
+        if (v < A.n && __ldcg(&A.parent[v]) == -1) {
+          const int64_t e1 = (int64_t)A.csc_off[v + 1];
+          for (int64_t e = (int64_t)A.csc_off[v]; e < e1 && !found; e += 4) {
+            uint32_t u[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) u[k] = e + k < e1 ? (uint32_t)__ldg(&A.csc_idx[e + k]) : 0xffffffffu;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              if (!found && u[k] != 0xffffffffu) {
+                const uint32_t word = u[k] < lim ? sbits[u[k] >> 5] : __ldcg(&bcur[u[k] >> 5]);
+                if ((word >> (u[k] & 31)) & 1u) {
+                  A.parent[v] = (int32_t)u[k];
+                  found = true;
+                }
+              }
+            }
+          }
+        }
+        const unsigned mask = __ballot_sync(0xffffffffu, found);
+        if (lane == 0) bnext[wd] = mask;
+        if (found) {
+          fcnt += 1;
+          fdeg += __ldg(&A.outdeg[v]);
+        }
+      }
+      qvalid = false;
+    } else {
+      if (!qvalid) {  // bitmap -> queue, one atomic per CTA word block
+        unsigned long long* t = reinterpret_cast<unsigned long long*>(A.tail + level % 4);
+        const int64_t per = (words + G - 1) / G;
+        const int64_t w0 = blockIdx.x * per, w1 = min(words, w0 + per);
+        for (int64_t b = w0; b < w1; b += kFT) {
+          const int64_t wd = b + tid;
+          uint32_t bits = wd < w1 ? __ldcg(&bcur[wd]) : 0u;
+          int pos, tot;
+          cub::BlockScan<int, kFT>(scan_tmp.i).ExclusiveSum(__popc(bits), pos, tot);
+          if (tid == 0) s_base = tot ? (long long)atomicAdd(t, (unsigned long long)tot) : 0;
+          __syncthreads();
+          long long p = s_base + pos;
+          while (bits) {
+            const int k = __ffs(bits) - 1;
+            bits &= bits - 1;
+            qcur[p++] = (int32_t)((wd << 5) + k);
+          }
+          __syncthreads();
+        }
+        grid.sync();
+      }
+      unsigned long long* tn = reinterpret_cast<unsigned long long*>(cn);
+      // visit one flattened edge (u -> v): claim v, append, set its next-bitmap bit
+      auto claim_step = [&](bool valid, int32_t u, int32_t v) {
+        bool won = false;
+        if (valid && *(volatile int32_t*)&A.parent[v] == -1) won = atomicCAS(&A.parent[v], -1, u) == -1;
+        if (won) {
+          atomicOr(&bnext[v >> 5], 1u << (v & 31));
+          fdeg += __ldg(&A.outdeg[v]);
+        }
+        cta_append(won, v, qnext, tn, s_warp, &s_base);
+      };
+      if (nf <= kFSmall && sdeg < INT_MAX) {
+        // every CTA scans the whole (small) frontier's degrees, then walks 1/G of the edges
+        constexpr int PT = kFSmall / kFT;
+        int d[PT], run = 0;
+#pragma unroll
+        for (int k = 0; k < PT; ++k) {
+          const int i = tid * PT + k;
+          d[k] = 0;
+          if (i < nf) {
+            const int32_t u = __ldcg(&qcur[i]);
+            sm.small.u[i] = u;
+            d[k] = (int)(A.csr_off[u + 1] - A.csr_off[u]);
+          }
+          run += d[k];
+        }
+        int excl, total;
+        cub::BlockScan<int, kFT>(scan_tmp.i).ExclusiveSum(run, excl, total);
+#pragma unroll
+        for (int k = 0; k < PT; ++k) {
+          const int i = tid * PT + k;
+          if (i < nf) sm.small.pre[i] = excl;
+          excl += d[k];
+        }
+        __syncthreads();
+        const long long E = total;
+        const long long lo = E * blockIdx.x / G, hi = E * (blockIdx.x + 1) / G;
+        for (long long base = lo; base < hi; base += kFT) {
+          const long long f = base + tid;
+          int32_t u = -1, v = -1;
+          if (f < hi) {
+            int a = 0, b = (int)nf - 1;
+            while (a < b) {
+              const int mid = (a + b + 1) >> 1;
+              if (sm.small.pre[mid] <= f) a = mid;
+              else b = mid - 1;
+            }
+            u = sm.small.u[a];
+            v = __ldg(&A.csr_idx[(long long)A.csr_off[u] + (f - sm.small.pre[a])]);
+          }
+          claim_step(f < hi, u, v);
+        }
+        fcnt = 0;  // counted through the tail below
+      } else {
+        // grid-wide scan of the frontier's degrees: chunk prefixes, then chunk offsets
+        const int64_t nch = (nf + kFChunk - 1) / kFChunk;
+        for (int64_t ch = blockIdx.x; ch < nch; ch += G) {
+          const int64_t i = ch * kFChunk + tid;
+          long long dg = 0;
+          if (i < nf) {
+            const int32_t u = __ldcg(&qcur[i]);
+            dg = (long long)(A.csr_off[u + 1] - A.csr_off[u]);
+          }
+          long long ex, tot;
+          cub::BlockScan<long long, kFT>(scan_tmp.l).ExclusiveSum(dg, ex, tot);
+          if (i < nf) A.pre[i] = ex;
+          if (tid == 0) A.ctot[ch] = tot;
+          __syncthreads();
+        }
+        grid.sync();
+        if (blockIdx.x == 0) {
+          long long carry = 0;
+          for (int64_t b = 0; b < nch; b += kFT) {
+            const int64_t i = b + tid;
+            const long long x = i < nch ? A.ctot[i] : 0;
+            long long ex, tot;
+            cub::BlockScan<long long, kFT>(scan_tmp.l).ExclusiveSum(x, ex, tot);
+            if (i < nch) A.ctot[i] = carry + ex;
+            carry += tot;
+            __syncthreads();
+          }
+          if (tid == 0) A.ctot[nch] = carry;
+        }
+        grid.sync();
+        const long long E = vload(A.ctot + nch);
+        auto gpre = [&](int64_t i) { return vload(A.ctot + i / kFChunk) + vload(A.pre + i); };
+        auto owner = [&](long long f) {  // last i with gpre(i) <= f
+          int64_t a = 0, b = nf - 1;
+          while (a < b) {
+            const int64_t mid = (a + b + 1) >> 1;
+            if (gpre(mid) <= f) a = mid;
+            else b = mid - 1;
+          }
+          return a;
+        };
+        for (long long lo = (long long)blockIdx.x * kFChunk; lo < E; lo += G * kFChunk) {
+          const long long hi = min(lo + (long long)kFChunk, E);
+          if (tid == 0) s_base = owner(lo);
+          __syncthreads();
+          const int64_t o0 = s_base;
+          for (int i = tid; i <= kFChunk + 1; i += kFT) {
+            const int64_t o = o0 + i;
+            sm.win.pre[i] = o < nf ? gpre(o) : LLONG_MAX;
+            if (i <= kFChunk) sm.win.u[i] = o < nf ? __ldcg(&qcur[o]) : -1;
+          }
+          __syncthreads();
+          const long long f = lo + tid;
+          int32_t u = -1, v = -1;
+          if (f < hi) {
+            long long pf;
+            if (sm.win.pre[kFChunk + 1] <= f) {
+              const int64_t o = owner(f);
+              u = __ldcg(&qcur[o]);
+              pf = gpre(o);
+            } else {
+              int a = 0, b = kFChunk;
+              while (a < b) {
+                const int mid = (a + b + 1) >> 1;
+                if (sm.win.pre[mid] <= f) a = mid;
+                else b = mid - 1;
+              }
+              u = sm.win.u[a];
+              pf = sm.win.pre[a];
+            }
+            v = __ldg(&A.csr_idx[(long long)A.csr_off[u] + (f - pf)]);
+          }
+          claim_step(f < hi, u, v);
+        }
+        fcnt = 0;
+      }
+      qvalid = true;
+    }
+    // |F_{l+1}| and sum of its out-degrees: one atomic pair per CTA
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      fcnt += __shfl_xor_sync(0xffffffffu, fcnt, o);
+      fdeg += __shfl_xor_sync(0xffffffffu, fdeg, o);
+    }
+    if (lane == 0) {
+      s_red[0][w] = fcnt;
+      s_red[1][w] = fdeg;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      long long a = 0, b = 0;
+      for (int i = 0; i < kFW; ++i) {
+        a += s_red[0][i];
+        b += s_red[1][i];
+      }
+      if (a) atomicAdd((unsigned long long*)&cn[0], (unsigned long long)a);
+      if (b) atomicAdd((unsigned long long*)&cn[1], (unsigned long long)b);
+    }
+    grid.sync();
+    ++level;
+  }
+  if (blockIdx.x == 0 && tid == 0) {
+    A.stats[0] = level;
+    A.stats[1] = pulls;
+  }
+}
+
+__global__ void k_fused_init(int32_t s_in, const int32_t* __restrict__ inv, const int32_t* __restrict__ outdeg,
+                             int32_t* __restrict__ parent, int32_t* __restrict__ q, uint32_t* __restrict__ bm,
+                             int64_t* __restrict__ cnt, long long* __restrict__ tail) {
+  const int32_t s = inv ? inv[s_in] : s_in;
+  parent[s] = s;
+  q[0] = s;
+  bm[s >> 5] = 1u << (s & 31);
+  for (int i = 0; i < 8; ++i) cnt[i] = 0;
+  for (int i = 0; i < 4; ++i) tail[i] = 0;
+  cnt[0] = 1;
+  cnt[1] = outdeg[s];
+}
+
+}  // namespace
+
+template <typename OffT>
+static gi_status bfs_fused_t(gi_graph g, int32_t source, const gi_bfs_opts& o, int32_t* d_out, gi_bfs_stats* stats) {
+  gi_context ctx = g->ctx;
+  cudaStream_t st = ctx->stream;
+  const int64_t n = g->n, words = (n + 31) >> 5;
+  auto& F = g->fused;
+  if (!F.ready) {
+    GI_TRY(F.parent.alloc((n + 1) * sizeof(int32_t)));
+    for (int k = 0; k < 2; ++k) GI_TRY(F.q[k].alloc((n + 1) * sizeof(int32_t)));
+    for (int k = 0; k < 3; ++k) GI_TRY(F.bm[k].alloc((words + 1) * sizeof(uint32_t)));
+    GI_TRY(F.cnt.alloc(16 * sizeof(int64_t)));
+    GI_TRY(F.pre.alloc((n + 1) * sizeof(long long)));
+    GI_TRY(F.ctot.alloc((n / kFChunk + 2) * sizeof(long long)));
+    int optin = 0, per_sm = 0;
+    GI_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
+    GI_CUDA(cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, ctx->device));
+    cudaFuncAttributes fa{};
+    GI_CUDA(cudaFuncGetAttributes(&fa, k_bfs_fused<OffT>));
+    int dyn = std::min(optin, per_sm / 2) - (int)fa.sharedSizeBytes - 2048;
+    dyn = std::max(dyn, (int)sizeof(FSmem)) & ~15;
+    GI_CUDA(cudaFuncSetAttribute(k_bfs_fused<OffT>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
+    int bpm = 0;
+    GI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bpm, k_bfs_fused<OffT>, kFT, dyn));
+    if (bpm < 1) return fail(GI_ERR_UNSUPPORTED, "fused BFS kernel cannot be co-resident");
+    F.dyn = dyn;
+    F.grid = bpm * ctx->num_sms;
+    F.ready = true;
+  }
+  GI_CUDA(cudaMemsetAsync(F.parent.p, 0xFF, n * sizeof(int32_t), st));
+  for (int k = 0; k < 3; ++k) GI_CUDA(cudaMemsetAsync(F.bm[k].p, 0, words * sizeof(uint32_t), st));
+  int64_t* cnt = F.cnt.as<int64_t>();
+  long long* tail = reinterpret_cast<long long*>(cnt + 8);
+  int64_t* stt = cnt + 12;
+  k_fused_init<<<1, 1, 0, st>>>(source, g->relabeled ? g->inv.as<int32_t>() : nullptr, g->outdeg.as<int32_t>(),
+                                F.parent.as<int32_t>(), F.q[0].as<int32_t>(), F.bm[0].as<uint32_t>(), cnt, tail);
+  FusedArgs<OffT> A;
+  A.csr_off = g->csr_off.as<OffT>();
+  A.csr_idx = g->csr_idx.as<int32_t>();
+  A.csc_off = g->csc_off.as<OffT>();
+  A.csc_idx = g->csc_idx.as<int32_t>();
+  A.outdeg = g->outdeg.as<int32_t>();
+  A.parent = F.parent.as<int32_t>();
+  A.q[0] = F.q[0].as<int32_t>();
+  A.q[1] = F.q[1].as<int32_t>();
+  for (int k = 0; k < 3; ++k) A.bm[k] = F.bm[k].as<uint32_t>();
+  A.cnt = cnt;
+  A.tail = tail;
+  A.pre = F.pre.as<long long>();
+  A.ctot = F.ctot.as<long long>();
+  A.stats = stt;
+  A.n = n;
+  A.mdiv = g->m / (o.threshold_div > 0 ? o.threshold_div : 20);
+  A.policy = o.policy;
+  A.sw = (int)std::min<int64_t>(words, (int64_t)((F.dyn) / 4));
+  void* args[] = {&A};
+  GI_CUDA(cudaLaunchCooperativeKernel((void*)k_bfs_fused<OffT>, dim3(F.grid), dim3(kFT), args, (size_t)F.dyn, st));
+  GI_CUDA(cudaGetLastError());
+  int64_t lv[2] = {0, 0};
+  GI_CUDA(cudaMemcpyAsync(lv, stt, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  int64_t reached = 0, edges = 0;
+  GI_TRY(bfs_finish_output(g, F.parent.as<int32_t>(), d_out, &reached, &edges));
+  if (stats) {
+    stats->levels = (int32_t)lv[0];
+    stats->pull_levels = (int32_t)lv[1];
+    stats->reached = reached;
+    stats->edges_traversed = edges;
+    stats->launches = 3;
+  }
+  return GI_OK;
+}
+
+gi_status bfs_fused(gi_graph g, int32_t source, const gi_bfs_opts& o, int32_t* d_out, gi_bfs_stats* stats) {
+  if (g->off64) return bfs_fused_t<int64_t>(g, source, o, d_out, stats);
+  return bfs_fused_t<int32_t>(g, source, o, d_out, stats);
+}
+
+}  // namespace gi

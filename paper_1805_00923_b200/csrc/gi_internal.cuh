@@ -133,6 +133,11 @@ struct gi_graph_s {
   gi::DevBuf bfs_pre;     // int64[n+1]: scan of frontier degrees (balanced push)
   gi::DevBuf bfs_scan_tmp;
   gi::DevBuf bfs_cand;    // uint64[n]: (epoch << 32 | parent candidate), stamp + collect push
+  struct {                // fused cooperative BFS (bfs_fused.cu)
+    bool ready = false;
+    int dyn = 0, grid = 0;
+    gi::DevBuf parent, q[2], bm[3], cnt, pre, ctot;
+  } fused;
   unsigned bfs_epoch = 0;
 };
 
@@ -153,7 +158,11 @@ struct PrArgs;
 gi_status seg_build(gi_graph g, int segment_size);
 gi_status seg_edge_pass(gi_graph g, const PrArgs& A);
 gi_status seg_vertex_pass(gi_graph g, const PrArgs& A);
-// bfs.cu
+// bfs.cu / bfs_fused.cu
+gi_status bfs_fused(gi_graph g, int32_t source_input_id, const gi_bfs_opts& o, int32_t* d_parent_input_ids,
+                    gi_bfs_stats* stats);
+gi_status bfs_finish_output(gi_graph g, const int32_t* parent_internal, int32_t* d_out, int64_t* reached,
+                            int64_t* edges);
 gi_status bfs_run(gi_graph g, int32_t source_input_id, const gi_bfs_opts& o,
                   int32_t* d_parent_input_ids, gi_bfs_stats* stats);
 // Low-latency wait for the stream: spin on cudaStreamQuery instead of a
