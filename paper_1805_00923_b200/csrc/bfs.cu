@@ -990,7 +990,7 @@ gi_status bfs_finish_output(gi_graph g, const int32_t* parent, int32_t* d_out, i
 
 gi_status bfs_run(gi_graph g, int32_t source, const gi_bfs_opts& o, int32_t* d_out, gi_bfs_stats* stats) {
   static const char* impl = getenv("GI_BFS_IMPL");  // "host": the host-driven level loop (A/B comparisons)
-  if (g->ctx->nranks == 1 && !(impl && strcmp(impl, "host") == 0) && !o.profile) return bfs_fused(g, source, o, d_out, stats);
+  if (g->ctx->nranks == 1 && !(impl && strcmp(impl, "host") == 0)) return bfs_fused(g, source, o, d_out, stats);
   if (g->ctx->nranks > 1) {
     if (g->off64) return bfs_dist_impl<int64_t>(g, source, o, d_out, stats);
     return bfs_dist_impl<int32_t>(g, source, o, d_out, stats);

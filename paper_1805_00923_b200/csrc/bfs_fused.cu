@@ -397,6 +397,12 @@ static gi_status bfs_fused_t(gi_graph g, int32_t source, const gi_bfs_opts& o, i
     F.grid = bpm * ctx->num_sms;
     F.ready = true;
   }
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (o.profile) {
+    GI_CUDA(cudaEventCreate(&e0));
+    GI_CUDA(cudaEventCreate(&e1));
+    GI_CUDA(cudaEventRecord(e0, st));
+  }
   GI_CUDA(cudaMemsetAsync(F.parent.p, 0xFF, n * sizeof(int32_t), st));
   for (int k = 0; k < 3; ++k) GI_CUDA(cudaMemsetAsync(F.bm[k].p, 0, words * sizeof(uint32_t), st));
   int64_t* cnt = F.cnt.as<int64_t>();
@@ -430,7 +436,16 @@ static gi_status bfs_fused_t(gi_graph g, int32_t source, const gi_bfs_opts& o, i
   GI_CUDA(cudaMemcpyAsync(lv, stt, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   int64_t reached = 0, edges = 0;
   GI_TRY(bfs_finish_output(g, F.parent.as<int32_t>(), d_out, &reached, &edges));
+  float ms = 0.f;
+  if (o.profile) {
+    GI_CUDA(cudaEventRecord(e1, st));
+    GI_CUDA(cudaEventSynchronize(e1));
+    GI_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+  }
   if (stats) {
+    stats->total_ms = ms;
     stats->levels = (int32_t)lv[0];
     stats->pull_levels = (int32_t)lv[1];
     stats->reached = reached;
