@@ -4,8 +4,8 @@ Only `tests/`, `__graft_entry__.smoke()` and `bench.py`'s cpu_baseline /
 `--impl reference` legs may import this package. The product path
 (`paper_1805_00923_b200`) never imports it and shares no code with it.
 
-All arithmetic lives in `gi_oracle.c` (plain C, fp64 PageRank, FIFO BFS,
-Graph500-style validator); see its header for the PAPER.md passages each
+All arithmetic lives in `gi_oracle.c` (plain C, fp64 PageRank and
+PageRankDelta, FIFO BFS, Graph500-style validator); see its header for the PAPER.md passages each
 function follows. This module only marshals numpy arrays.
 
 Pins: tests/test_oracle_pins.py (closed forms, invariants, brute force).
@@ -33,7 +33,7 @@ def build(force: bool = False) -> str:
     """Compile the oracle in-tree with gcc (building the checker is not using it)."""
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
         tmp = _LIB + f".tmp{os.getpid()}"
-        subprocess.check_call(["gcc", "-O2", "-fopenmp", "-shared", "-fPIC", "-o", tmp, _SRC])
+        subprocess.check_call(["gcc", "-O2", "-fopenmp", "-shared", "-fPIC", "-o", tmp, _SRC, "-lm"])
         os.replace(tmp, _LIB)
     return _LIB
 
@@ -63,6 +63,8 @@ def _get():
             lib.or_validate_bfs.restype = ctypes.c_int
             lib.or_reached_out_edges.argtypes = [vp, i32p]
             lib.or_reached_out_edges.restype = ctypes.c_int64
+            lib.or_pagerank_delta.argtypes = [vp, ctypes.c_int, ctypes.c_double, ctypes.c_double, f64p, vp]
+            lib.or_pagerank_delta.restype = ctypes.c_int
             _lib = lib
     return _lib
 
@@ -162,3 +164,15 @@ def validate_bfs(g: Graph, source: int, parent, depth=None) -> tuple[bool, str]:
 
 def reached_out_edges(g: Graph, depth) -> int:
     return int(_get().or_reached_out_edges(g._h, np.ascontiguousarray(depth, np.int32)))
+
+
+def pagerank_delta(g: Graph, iters: int = 10, damping: float = 0.85, epsilon: float = 0.1,
+                   return_frontiers: bool = False):
+    """PageRankDelta (readings R17, R18). Returns Rank (and the
+    frontier size entering each round if return_frontiers)."""
+    r = np.empty(max(g.n, 1), np.float64)
+    fs = np.zeros(max(iters, 1), np.int64)
+    rc = _get().or_pagerank_delta(g._h, iters, damping, epsilon, r, fs.ctypes.data)
+    if rc != 0:
+        raise OracleError(f"or_pagerank_delta failed ({rc})")
+    return (r[: g.n], fs[:iters]) if return_frontiers else r[: g.n]

@@ -44,6 +44,7 @@
  */
 #include <stdint.h>
 #include <stdlib.h>
+#include <math.h>
 #include <string.h>
 
 typedef struct {
@@ -220,4 +221,63 @@ int64_t or_reached_out_edges(const or_graph* g, const int32_t* depth) {
   for (int64_t v = 0; v < g->n; ++v)
     if (depth[v] >= 0) s += g->csr_off[v + 1] - g->csr_off[v];
   return s;
+}
+
+/* PageRankDelta (NEXT #1 of SURVEY §8(f)), fp64, following the GraphIt program
+ * P:849-893 (with Alg. PageRankDelta):
+ *   Rank = 0, DeltaSum = 0, Delta = 1/V, Frontier = V
+ *   for round 1..MaxIter:
+ *     DeltaSum[dst] += Delta[src] / OutDegree[src] for every edge (src, dst)
+ *       with src in Frontier                        edges.from(frontier) P:862-864
+ *     round 1: Delta = d*DeltaSum + (1-d)/V; Rank += Delta; Delta -= 1/V
+ *       (the program's order, P:865-868 and Ligra's P:3018-3021 [punt]; the
+ *       pseudocode P:440-446 subtracts before adding — reading R17)
+ *     later:   Delta = DeltaSum * d; Rank += Delta
+ *     DeltaSum = 0; v joins the next frontier iff |Delta[v]| > eps * Rank[v]
+ *       (P:869's garbled fabs(Delta[v] > eps*Rank[v]) read as P:874 — R18)
+ *   updateVertex runs on every vertex every round (vertices.filter), so a
+ *   vertex outside the frontier still takes the deltas it receives.
+ * frontier_sizes[k] (optional) = |Frontier| entering round k+1. */
+int or_pagerank_delta(const or_graph* g, int iters, double damp, double eps, double* rank,
+                      int64_t* frontier_sizes) {
+  const int64_t n = g->n;
+  if (iters < 0 || damp < 0.0 || damp > 1.0 || eps < 0.0) return -1;
+  if (n == 0) return 0;
+  double* delta = (double*)malloc((size_t)n * sizeof(double));
+  double* dsum = (double*)calloc((size_t)n, sizeof(double));
+  unsigned char* inF = (unsigned char*)malloc((size_t)n);
+  if (!delta || !dsum || !inF) { free(delta); free(dsum); free(inF); return -3; }
+  const double invV = 1.0 / (double)n, base = (1.0 - damp) / (double)n;
+  for (int64_t v = 0; v < n; ++v) { rank[v] = 0.0; delta[v] = invV; inF[v] = 1; }
+  for (int round = 1; round <= iters; ++round) {
+    int64_t fs = 0;
+    for (int64_t v = 0; v < n; ++v) fs += inF[v];
+    if (frontier_sizes) frontier_sizes[round - 1] = fs;
+    /* edge pass, pull form over CSC rows (ascending sources): same sums as the push loop */
+#pragma omp parallel for schedule(dynamic, 4096)
+    for (int64_t v = 0; v < n; ++v) {
+      double s = 0.0;
+      for (int64_t j = g->csc_off[v]; j < g->csc_off[v + 1]; ++j) {
+        const int32_t u = g->csc_idx[j];
+        if (inF[u]) s += delta[u] / (double)(g->csr_off[u + 1] - g->csr_off[u]);
+      }
+      dsum[v] = s;
+    }
+    for (int64_t v = 0; v < n; ++v) {
+      if (round == 1) {
+        delta[v] = damp * dsum[v] + base;
+        rank[v] += delta[v];
+        delta[v] = delta[v] - invV;
+      } else {
+        delta[v] = dsum[v] * damp;
+        rank[v] += delta[v];
+      }
+      dsum[v] = 0.0;
+      inF[v] = fabs(delta[v]) > eps * rank[v];
+    }
+  }
+  free(delta);
+  free(dsum);
+  free(inF);
+  return 0;
 }

@@ -369,3 +369,38 @@ def test_build_out_of_range():
         oracle.build_graph(3, np.array([0, 3], np.int32), np.array([1, 1], np.int32))
     with pytest.raises(oracle.OracleError):
         oracle.build_graph(3, np.array([0, -1], np.int32), np.array([1, 1], np.int32))
+
+
+# ---------------------------------------------------------------- PageRankDelta pins
+def test_prdelta_eps0_is_pagerank_drop_rule():
+    """With eps = 0 every vertex with a nonzero delta propagates, and by linearity
+    Rank_k = r_k of Jacobi PageRank under the drop rule (no dangling term):
+    round 1 gives r_1 and Delta_1 = r_1 - r_0; round k adds d * P Delta_{k-1} = r_k - r_{k-1}."""
+    for seed, (n, m0) in enumerate([(50, 300), (300, 900), (1000, 8000)]):
+        s, d = graphgen.random_digraph(n, m0, 70 + seed)
+        g = oracle.build_graph(n, s, d)
+        for k in (1, 2, 7, 15):
+            np.testing.assert_allclose(oracle.pagerank_delta(g, k, 0.85, 0.0),
+                                       oracle.pagerank(g, k, 0.85, oracle.DROP), rtol=1e-11, atol=1e-15)
+
+
+def test_prdelta_huge_eps_stops_after_round_one():
+    s, d = graphgen.random_digraph(200, 1500, 4)
+    g = oracle.build_graph(200, s, d)
+    r1 = oracle.pagerank(g, 1, 0.85, oracle.DROP)
+    rk, fs = oracle.pagerank_delta(g, 6, 0.85, 1e30, return_frontiers=True)
+    np.testing.assert_allclose(rk, r1, rtol=1e-14)
+    assert fs[0] == 200 and fs[1:].sum() == 0  # round 1 from all vertices, then nothing is active
+
+
+def test_prdelta_cycle_symmetry_and_frontier_shrinks():
+    s, d = graphgen.cycle(3)  # SPEC S:508: all ranks equal by symmetry
+    g = oracle.build_graph(3, s, d)
+    r = oracle.pagerank_delta(g, 10, 0.85, 0.1)
+    assert np.ptp(r) == 0.0
+    s, d = graphgen.rmat(12, 8, 0.57, 0.19, 0.19, 3)
+    g = oracle.build_graph(1 << 12, s, d)
+    r, fs = oracle.pagerank_delta(g, 12, 0.85, 0.1, return_frontiers=True)
+    assert fs[0] == 1 << 12 and fs[-1] < fs[1]  # the active set shrinks as ranks converge (P:664-667)
+    rpr = oracle.pagerank(g, 12, 0.85, oracle.DROP)
+    assert np.abs(r - rpr).sum() < 0.05 * rpr.sum()  # an approximation of PageRank
