@@ -28,6 +28,9 @@
 
 #include <algorithm>
 #include <climits>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
 #include <cub/cub.cuh>
 
 #include "gi_internal.cuh"
@@ -59,7 +62,15 @@ struct FusedArgs {
   int64_t* stats;      // [levels, pull levels]
   int64_t n, mdiv;
   int policy, sw;
+  unsigned long long* times;  // optional (GI_DEBUG_BFS_FUSED): per level [start, work done, barrier done]
+  int max_times;
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 
 struct FSmem {  // carved from dynamic shared memory, phase by phase
   union {
@@ -120,6 +131,8 @@ __global__ void __launch_bounds__(kFT, 2) k_bfs_fused(FusedArgs<OffT> A) {
   for (;;) {
     const int64_t* c = A.cnt + 2 * (level % 4);
     const int64_t nf = vload(c), sdeg = vload(c + 1);
+    const bool timed = A.times && blockIdx.x == 0 && tid == 0 && level < A.max_times;
+    if (timed) A.times[3 * level] = gtimer();
     if (nf == 0) break;
     const bool pull = A.policy == GI_BFS_PULL_ONLY ? level > 0
                                                    : (A.policy == GI_BFS_AUTO && nf + sdeg > A.mdiv);
@@ -345,7 +358,9 @@ __global__ void __launch_bounds__(kFT, 2) k_bfs_fused(FusedArgs<OffT> A) {
       if (a) atomicAdd((unsigned long long*)&cn[0], (unsigned long long)a);
       if (b) atomicAdd((unsigned long long*)&cn[1], (unsigned long long)b);
     }
+    if (timed) A.times[3 * level + 1] = gtimer();
     grid.sync();
+    if (timed) A.times[3 * level + 2] = gtimer();
     ++level;
   }
   if (blockIdx.x == 0 && tid == 0) {
@@ -429,6 +444,16 @@ static gi_status bfs_fused_t(gi_graph g, int32_t source, const gi_bfs_opts& o, i
   A.mdiv = g->m / (o.threshold_div > 0 ? o.threshold_div : 20);
   A.policy = o.policy;
   A.sw = (int)std::min<int64_t>(words, (int64_t)((F.dyn) / 4));
+  static const char* dbg = getenv("GI_DEBUG_BFS_FUSED");  // diagnostics: per-level timeline file
+  DevBuf tbuf;
+  A.times = nullptr;
+  A.max_times = 0;
+  if (dbg) {
+    A.max_times = 1 << 16;
+    GI_TRY(tbuf.alloc((size_t)3 * A.max_times * sizeof(unsigned long long)));
+    GI_CUDA(cudaMemsetAsync(tbuf.p, 0, (size_t)3 * A.max_times * sizeof(unsigned long long), st));
+    A.times = tbuf.as<unsigned long long>();
+  }
   void* args[] = {&A};
   GI_CUDA(cudaLaunchCooperativeKernel((void*)k_bfs_fused<OffT>, dim3(F.grid), dim3(kFT), args, (size_t)F.dyn, st));
   GI_CUDA(cudaGetLastError());
@@ -436,6 +461,17 @@ static gi_status bfs_fused_t(gi_graph g, int32_t source, const gi_bfs_opts& o, i
   GI_CUDA(cudaMemcpyAsync(lv, stt, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   int64_t reached = 0, edges = 0;
   GI_TRY(bfs_finish_output(g, F.parent.as<int32_t>(), d_out, &reached, &edges));
+  if (dbg) {
+    std::vector<unsigned long long> ht((size_t)3 * A.max_times);
+    GI_CUDA(cudaMemcpy(ht.data(), tbuf.p, ht.size() * 8, cudaMemcpyDeviceToHost));
+    if (FILE* f = fopen(dbg, "a")) {
+      for (int l = 0; l < A.max_times && ht[3 * l]; ++l)
+        fprintf(f, "src=%d level=%d work_us=%.2f barrier_us=%.2f\n", source, l,
+                ht[3 * l + 1] ? (ht[3 * l + 1] - ht[3 * l]) / 1e3 : 0.0,
+                ht[3 * l + 2] ? (ht[3 * l + 2] - ht[3 * l + 1]) / 1e3 : 0.0);
+      fclose(f);
+    }
+  }
   float ms = 0.f;
   if (o.profile) {
     GI_CUDA(cudaEventRecord(e1, st));
