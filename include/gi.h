@@ -176,6 +176,37 @@ typedef struct {
 GI_API gi_status gi_pagerank_ex(gi_graph g, int32_t iters, double damping, const gi_pr_opts* opts,
                          float* out, gi_pr_stats* stats /* may be NULL */);
 
+/* ---------------------------------------------------------------- PageRankDelta */
+
+/* PageRankDelta (the paper's running example: Alg.
+ * PageRankDelta P:426-456, GraphIt program P:849-893): Rank = 0, Delta = 1/V,
+ * Frontier = V; each round DeltaSum[dst] += Delta[src]/outdeg(src) over edges
+ * from the frontier, round 1: Delta = d*DeltaSum + (1-d)/V, Rank += Delta,
+ * Delta -= 1/V; later: Delta = d*DeltaSum, Rank += Delta; the next frontier
+ * is {v : |Delta[v]| > epsilon * Rank[v]} (readings R17, R18). The edge pass
+ * is DensePull-SparsePush: pull iff |F| + sum outdeg(F) > m / threshold_div.
+ *   iters >= 0 rounds (stops early if the frontier empties), damping in [0,1],
+ *   epsilon >= 0; out: float[n] Rank in input ids. Single-GPU graphs only. */
+enum { GI_PRD_AUTO = 0, GI_PRD_PUSH_ONLY = 1, GI_PRD_PULL_ONLY = 2 };
+typedef struct {
+  int32_t policy;        /* GI_PRD_AUTO / PUSH_ONLY / PULL_ONLY */
+  int32_t threshold_div; /* 0 -> 20 */
+  int32_t profile;       /* 1: total_ms */
+  int32_t reserved;
+} gi_prdelta_opts;
+
+typedef struct {
+  int32_t rounds;       /* rounds executed */
+  int32_t pull_rounds;  /* rounds whose edge pass ran in the pull direction */
+  int64_t active_total; /* sum over rounds of the frontier size */
+  float total_ms;       /* profile=1 */
+  int32_t launches;
+  int32_t reserved;
+} gi_prdelta_stats;
+
+GI_API gi_status gi_pagerank_delta(gi_graph g, int32_t iters, double damping, double epsilon,
+                                   const gi_prdelta_opts* opts, float* out, gi_prdelta_stats* stats);
+
 /* ---------------------------------------------------------------- BFS */
 
 /* Breadth-first search from `source` along out-edges (R9), direction-

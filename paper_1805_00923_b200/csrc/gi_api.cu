@@ -388,6 +388,33 @@ gi_status gi_pagerank_ex(gi_graph g, int32_t iters, double damping, const gi_pr_
   GI_GUARD_END
 }
 
+gi_status gi_pagerank_delta(gi_graph g, int32_t iters, double damping, double epsilon, const gi_prdelta_opts* opts,
+                            float* out, gi_prdelta_stats* stats) {
+  GI_GUARD_BEGIN
+  if (!g) return fail(GI_ERR_INVALID_ARGUMENT, "gi_pagerank_delta: NULL graph");
+  if (!out && g->n > 0) return fail(GI_ERR_INVALID_ARGUMENT, "gi_pagerank_delta: NULL output");
+  if (iters < 0) return fail(GI_ERR_INVALID_ARGUMENT, "gi_pagerank_delta: iters < 0");
+  if (!(damping >= 0.0 && damping <= 1.0)) return fail(GI_ERR_INVALID_ARGUMENT, "gi_pagerank_delta: damping not in [0,1]");
+  if (!(epsilon >= 0.0)) return fail(GI_ERR_INVALID_ARGUMENT, "gi_pagerank_delta: epsilon < 0");
+  gi_prdelta_opts o{};
+  if (opts) o = *opts;
+  if (o.policy < GI_PRD_AUTO || o.policy > GI_PRD_PULL_ONLY || o.threshold_div < 0)
+    return fail(GI_ERR_INVALID_ARGUMENT, "gi_pagerank_delta: bad options");
+  gi_context ctx = g->ctx;
+  GI_CUDA(cudaSetDevice(ctx->device));
+  if (g->n == 0) {
+    if (stats) *stats = gi_prdelta_stats{};
+    return GI_OK;
+  }
+  OutBuf<float> ob{out, g->n, false, &g->out_stage};
+  float* d = nullptr;
+  GI_TRY(ob.prepare(g, &d));
+  GI_TRY(prdelta_run(g, iters, damping, epsilon, o, d, stats));
+  GI_TRY(ob.finish(ctx));
+  return sync(ctx);
+  GI_GUARD_END
+}
+
 gi_status gi_pagerank(gi_graph g, int32_t iters, double damping, float* out) {
   return gi_pagerank_ex(g, iters, damping, nullptr, out, nullptr);
 }

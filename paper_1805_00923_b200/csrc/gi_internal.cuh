@@ -158,6 +158,9 @@ struct PrArgs;
 gi_status seg_build(gi_graph g, int segment_size);
 gi_status seg_edge_pass(gi_graph g, const PrArgs& A);
 gi_status seg_vertex_pass(gi_graph g, const PrArgs& A);
+// prdelta.cu
+gi_status prdelta_run(gi_graph g, int32_t iters, double damping, double eps, const gi_prdelta_opts& o, float* d_out,
+                      gi_prdelta_stats* stats);
 // bfs.cu / bfs_fused.cu
 gi_status bfs_fused(gi_graph g, int32_t source_input_id, const gi_bfs_opts& o, int32_t* d_parent_input_ids,
                     gi_bfs_stats* stats);

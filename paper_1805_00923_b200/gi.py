@@ -41,6 +41,7 @@ GI_DEFAULT_FLAGS = GI_REMOVE_SELF_LOOPS | GI_DEDUP
 GI_PR_PULL, GI_PR_PUSH, GI_PR_PULL_DIRECT, GI_PR_PULL_SEGMENTED = 0, 1, 2, 3
 GI_DANGLING_UNIFORM, GI_DANGLING_DROP = 0, 1
 GI_BFS_AUTO, GI_BFS_PUSH_ONLY, GI_BFS_PULL_ONLY = 0, 1, 2
+GI_PRD_AUTO, GI_PRD_PUSH_ONLY, GI_PRD_PULL_ONLY = 0, 1, 2
 
 
 class gi_pr_opts(ctypes.Structure):
@@ -52,6 +53,16 @@ class gi_pr_stats(ctypes.Structure):
     _fields_ = [("edge_launches", ctypes.c_int32), ("aux_launches", ctypes.c_int32), ("edge_ms", ctypes.c_float),
                 ("total_ms", ctypes.c_float), ("kernel", ctypes.c_int32), ("reserved", ctypes.c_int32),
                 ("bytes_alg_per_iter", ctypes.c_int64)]
+
+
+class gi_prdelta_opts(ctypes.Structure):
+    _fields_ = [("policy", ctypes.c_int32), ("threshold_div", ctypes.c_int32), ("profile", ctypes.c_int32),
+                ("reserved", ctypes.c_int32)]
+
+
+class gi_prdelta_stats(ctypes.Structure):
+    _fields_ = [("rounds", ctypes.c_int32), ("pull_rounds", ctypes.c_int32), ("active_total", ctypes.c_int64),
+                ("total_ms", ctypes.c_float), ("launches", ctypes.c_int32), ("reserved", ctypes.c_int32)]
 
 
 class gi_bfs_opts(ctypes.Structure):
@@ -92,6 +103,8 @@ _SIGS = {
     "gi_pagerank": ([_vp, _i32, ctypes.c_double, _vp], _st),
     "gi_pagerank_ex": ([_vp, _i32, ctypes.c_double, ctypes.POINTER(gi_pr_opts), _vp,
                         ctypes.POINTER(gi_pr_stats)], _st),
+    "gi_pagerank_delta": ([_vp, _i32, ctypes.c_double, ctypes.c_double, ctypes.POINTER(gi_prdelta_opts), _vp,
+                           ctypes.POINTER(gi_prdelta_stats)], _st),
     "gi_bfs": ([_vp, _i32, _vp], _st),
     "gi_bfs_ex": ([_vp, _i32, ctypes.POINTER(gi_bfs_opts), _vp, ctypes.POINTER(gi_bfs_stats)], _st),
     "gi_status_string": ([_st], ctypes.c_char_p),
@@ -272,6 +285,19 @@ def gi_pagerank_ex(g: int, iters: int, damping: float, out=None, direction: int 
     return keep, s
 
 
+def gi_pagerank_delta(g: int, iters: int, damping: float, epsilon: float, out=None, policy: int = GI_PRD_AUTO,
+                      threshold_div: int = 0, profile: bool = False):
+    n = gi_graph_num_vertices(g)
+    if out is None:
+        out = np.empty(n, np.float32)
+    p, keep = _ptr(out, np.float32)
+    o = gi_prdelta_opts(policy, threshold_div, int(profile), 0)
+    s = gi_prdelta_stats()
+    _check(_lib.gi_pagerank_delta(g, iters, damping, epsilon, ctypes.byref(o), p or None, ctypes.byref(s)),
+           "gi_pagerank_delta")
+    return keep, s
+
+
 def gi_bfs(g: int, source: int, out=None):
     n = gi_graph_num_vertices(g)
     if out is None:
@@ -347,6 +373,9 @@ class Graph:
 
     def pagerank(self, iters=20, damping=0.85, out=None, **kw):
         return gi_pagerank_ex(self.handle, iters, damping, out, **kw)
+
+    def pagerank_delta(self, iters=10, damping=0.85, epsilon=0.1, out=None, **kw):
+        return gi_pagerank_delta(self.handle, iters, damping, epsilon, out, **kw)
 
     def bfs(self, source, out=None, **kw):
         return gi_bfs_ex(self.handle, source, out, **kw)

@@ -410,3 +410,45 @@ def test_full_config_parity(gi, ctx, full_graphs, cfg_idx):
         ok, msg = oracle.validate_bfs(go, int(src), par.cpu().numpy(), depth)
         assert ok, f"{cfg.name} src={src}: {msg}"
         assert bs.edges_traversed == oracle.reached_out_edges(go, depth)
+
+
+# ---------------------------------------------------------------- PageRankDelta
+PRD_POLICIES = ["auto", "push", "pull"]
+
+
+def _prd_pol(gi, p):
+    return {"auto": gi.GI_PRD_AUTO, "push": gi.GI_PRD_PUSH_ONLY, "pull": gi.GI_PRD_PULL_ONLY}[p]
+
+
+@pytest.mark.parametrize("policy", PRD_POLICIES)
+def test_prdelta_parity(gi, ctx, policy):
+    """GPU PageRankDelta vs the fp64 oracle on the same rounds. The frontier test
+    |Delta| > eps*Rank is taken in fp64 on both sides (the paper's precision);
+    the per-round frontier sizes must agree exactly, ranks within the PR bars."""
+    cases = [("config1", graphgen.CONFIGS[1].n, *graphgen.CONFIGS[1].edges()),
+             ("random", 20000, *graphgen.random_digraph(20000, 200000, 4)),
+             ("bistar", 5001, *graphgen.star_bidirectional(5000))]
+    for name, n, s, d in cases:
+        g = gi.Graph(ctx, n, s, d)
+        go = oracle.build_graph(n, s, d)
+        for eps, iters in [(0.0, 10), (0.1, 10), (0.01, 15)]:
+            want, fs = oracle.pagerank_delta(go, iters, 0.85, eps, return_frontiers=True)
+            got, st = g.pagerank_delta(iters, 0.85, eps, policy=_prd_pol(gi, policy))
+            assert st.active_total == int(fs.sum()), (name, eps, st.active_total, fs.tolist())
+            got = np.asarray(got, np.float64)
+            l1 = np.abs(got - want).sum()
+            rel = (np.abs(got - want) / np.maximum(want, 1e-300)).max()
+            assert l1 <= 1e-5 and rel <= 1e-4, (name, eps, policy, l1, rel)
+        if policy == "auto":
+            # the paper's point: the frontier shrinks, so later rounds switch to push
+            _, st = g.pagerank_delta(15, 0.85, 0.01)
+            assert st.rounds == 15 and 0 < st.pull_rounds < st.rounds
+
+
+def test_prdelta_equals_pagerank_drop_at_eps0(gi, ctx):
+    cfg = graphgen.CONFIGS[1]
+    s, d = cfg.edges()
+    g = gi.Graph(ctx, cfg.n, s, d)
+    want = oracle.pagerank(oracle.build_graph(cfg.n, s, d), 12, 0.85, oracle.DROP)
+    got, _ = g.pagerank_delta(12, 0.85, 0.0)
+    _pr_check(got, want, "prdelta eps=0 vs PR drop")
