@@ -42,7 +42,7 @@ namespace {
 
 constexpr int kFT = 1024;        // threads per CTA
 constexpr int kFW = kFT / 32;    // warps per CTA
-constexpr int kFSmall = 4096;    // frontier size expanded by the per-CTA scan
+constexpr int kFSmall = 8192;    // frontier size expanded by the per-CTA scan
 constexpr int kFChunk = kFT;     // frontier entries per scan chunk (large frontiers)
 
 template <typename OffT>
@@ -217,7 +217,34 @@ __global__ void __launch_bounds__(kFT, 2) k_bfs_fused(FusedArgs<OffT> A) {
         }
         cta_append(won, v, qnext, tn, s_warp, &s_base);
       };
-      if (nf <= kFSmall && sdeg < INT_MAX) {
+      if (sdeg <= 4 * nf) {
+        // low-degree frontier (road/grid-like levels): thread per frontier vertex,
+        // no scan; every thread steps through the same number of rounds so the
+        // CTA-aggregated append stays collective
+        const int64_t per = (nf + G - 1) / G;
+        const int64_t i0 = blockIdx.x * per, i1 = min(nf, i0 + per);
+        for (int64_t b = i0; b < i1; b += kFT) {
+          const int64_t i = b + tid;
+          int32_t u = -1;
+          int64_t e = 0, e1 = 0;
+          if (i < i1) {
+            u = __ldcg(&qcur[i]);
+            e = (int64_t)A.csr_off[u];
+            e1 = (int64_t)A.csr_off[u + 1];
+          }
+          int rounds = (int)min(e1 - e, (int64_t)INT_MAX);
+          for (int o = 16; o > 0; o >>= 1) rounds = max(rounds, __shfl_xor_sync(0xffffffffu, rounds, o));
+          if (lane == 0) s_warp[w] = rounds;
+          __syncthreads();
+          int cta_rounds = 0;
+          for (int k = 0; k < kFW; ++k) cta_rounds = max(cta_rounds, s_warp[k]);
+          __syncthreads();
+          for (int k = 0; k < cta_rounds; ++k) {
+            const bool valid = e + k < e1;
+            claim_step(valid, u, valid ? __ldg(&A.csr_idx[e + k]) : -1);
+          }
+        }
+      } else if (nf <= kFSmall && sdeg < INT_MAX) {
         // every CTA scans the whole (small) frontier's degrees, then walks 1/G of the edges
         constexpr int PT = kFSmall / kFT;
         int d[PT], run = 0;
