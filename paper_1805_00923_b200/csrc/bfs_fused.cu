@@ -22,8 +22,9 @@
 //     equal slice of their flattened edge list (each CTA scans the frontier's
 //     degrees itself), large ones by a grid-wide scan of degrees (two extra
 //     barriers) and the same flattened walk; claims append to the next queue
-//     with one atomic per CTA step and set the next bitmap bit;
-//   bm[(l+2)%3] and cnt[(l+2)%4] are cleared during level l (unused then).
+//     with one atomic per CTA step (per warp for low-degree frontiers);
+//   push levels leave only a queue: a pull level after them first rebuilds the
+//   frontier bitmap; cnt[(l+2)%4] is cleared during level l (unused then).
 #include <cooperative_groups.h>
 
 #include <algorithm>
@@ -126,7 +127,8 @@ __global__ void __launch_bounds__(kFT, 2) k_bfs_fused(FusedArgs<OffT> A) {
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int64_t G = gridDim.x;
   const int64_t words = (A.n + 31) >> 5;
-  bool qvalid = true;  // level 0's frontier {s} is a queue (and a bitmap)
+  bool qvalid = true;  // the current frontier is available as a queue ...
+  bool bvalid = true;  // ... and as a bitmap (level 0: both, set up by the host)
   int64_t level = 0, pulls = 0;
   for (;;) {
     const int64_t* c = A.cnt + 2 * (level % 4);
@@ -138,7 +140,6 @@ __global__ void __launch_bounds__(kFT, 2) k_bfs_fused(FusedArgs<OffT> A) {
                                                    : (A.policy == GI_BFS_AUTO && nf + sdeg > A.mdiv);
     uint32_t* bcur = A.bm[level % 3];
     uint32_t* bnext = A.bm[(level + 1) % 3];
-    uint32_t* bzero = A.bm[(level + 2) % 3];
     int32_t* qcur = A.q[level & 1];
     int32_t* qnext = A.q[(level + 1) & 1];
     int64_t* cn = A.cnt + 2 * ((level + 1) % 4);
@@ -147,11 +148,19 @@ __global__ void __launch_bounds__(kFT, 2) k_bfs_fused(FusedArgs<OffT> A) {
       A.cnt[2 * ((level + 2) % 4) + 1] = 0;
       A.tail[(level + 2) % 4] = 0;
     }
-    for (int64_t i = blockIdx.x * (int64_t)kFT + tid; i < words; i += G * kFT) bzero[i] = 0u;
     long long fcnt = 0, fdeg = 0;  // this thread's share of |F_{l+1}| and its out-degrees
 
     if (pull) {
       ++pulls;
+      if (!bvalid) {  // frontier only as a queue (after push levels): build its bitmap
+        for (int64_t i = blockIdx.x * (int64_t)kFT + tid; i < words; i += G * kFT) bcur[i] = 0u;
+        grid.sync();
+        for (int64_t i = blockIdx.x * (int64_t)kFT + tid; i < nf; i += G * kFT) {
+          const int32_t u = __ldcg(&qcur[i]);
+          atomicOr(&bcur[u >> 5], 1u << (u & 31));
+        }
+        grid.sync();
+      }
       for (int i = tid; i < A.sw; i += kFT) sbits[i] = __ldcg(&bcur[i]);
       __syncthreads();
       const uint32_t lim = (uint32_t)A.sw * 32u;
@@ -184,6 +193,7 @@ __global__ void __launch_bounds__(kFT, 2) k_bfs_fused(FusedArgs<OffT> A) {
         }
       }
       qvalid = false;
+      bvalid = true;
     } else {
       if (!qvalid) {  // bitmap -> queue, one atomic per CTA word block
         unsigned long long* t = reinterpret_cast<unsigned long long*>(A.tail + level % 4);
@@ -211,10 +221,7 @@ __global__ void __launch_bounds__(kFT, 2) k_bfs_fused(FusedArgs<OffT> A) {
       auto claim_step = [&](bool valid, int32_t u, int32_t v) {
         bool won = false;
         if (valid && *(volatile int32_t*)&A.parent[v] == -1) won = atomicCAS(&A.parent[v], -1, u) == -1;
-        if (won) {
-          atomicOr(&bnext[v >> 5], 1u << (v & 31));
-          fdeg += __ldg(&A.outdeg[v]);
-        }
+        if (won) fdeg += __ldg(&A.outdeg[v]);
         cta_append(won, v, qnext, tn, s_warp, &s_base);
       };
       if (sdeg <= 4 * nf) {
@@ -234,14 +241,21 @@ __global__ void __launch_bounds__(kFT, 2) k_bfs_fused(FusedArgs<OffT> A) {
           }
           int rounds = (int)min(e1 - e, (int64_t)INT_MAX);
           for (int o = 16; o > 0; o >>= 1) rounds = max(rounds, __shfl_xor_sync(0xffffffffu, rounds, o));
-          if (lane == 0) s_warp[w] = rounds;
-          __syncthreads();
-          int cta_rounds = 0;
-          for (int k = 0; k < kFW; ++k) cta_rounds = max(cta_rounds, s_warp[k]);
-          __syncthreads();
-          for (int k = 0; k < cta_rounds; ++k) {
-            const bool valid = e + k < e1;
-            claim_step(valid, u, valid ? __ldg(&A.csr_idx[e + k]) : -1);
+          for (int k = 0; k < rounds; ++k) {  // warp-uniform; appends aggregated per warp
+            bool won = false;
+            int32_t v = -1;
+            if (e + k < e1) {
+              v = __ldg(&A.csr_idx[e + k]);
+              if (*(volatile int32_t*)&A.parent[v] == -1) won = atomicCAS(&A.parent[v], -1, u) == -1;
+            }
+            const unsigned mask = __ballot_sync(0xffffffffu, won);
+            if (mask) {
+              if (won) fdeg += __ldg(&A.outdeg[v]);
+              long long pos = 0;
+              if (lane == 0) pos = (long long)atomicAdd(tn, (unsigned long long)__popc(mask));
+              pos = __shfl_sync(0xffffffffu, pos, 0);
+              if (won) qnext[pos + __popc(mask & ((1u << lane) - 1))] = v;
+            }
           }
         }
       } else if (nf <= kFSmall && sdeg < INT_MAX) {
@@ -364,6 +378,7 @@ __global__ void __launch_bounds__(kFT, 2) k_bfs_fused(FusedArgs<OffT> A) {
         fcnt = 0;
       }
       qvalid = true;
+      bvalid = false;  // push levels produce only the queue
     }
     // |F_{l+1}| and sum of its out-degrees: one atomic pair per CTA
 #pragma unroll

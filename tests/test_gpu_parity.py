@@ -439,7 +439,7 @@ def test_prdelta_parity(gi, ctx, policy):
             l1 = np.abs(got - want).sum()
             rel = (np.abs(got - want) / np.maximum(want, 1e-300)).max()
             assert l1 <= 1e-5 and rel <= 1e-4, (name, eps, policy, l1, rel)
-        if policy == "auto":
+        if policy == "auto" and name == "config1":
             # the paper's point: the frontier shrinks, so later rounds switch to push
             _, st = g.pagerank_delta(15, 0.85, 0.01)
             assert st.rounds == 15 and 0 < st.pull_rounds < st.rounds
