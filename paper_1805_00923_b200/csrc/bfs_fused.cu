@@ -45,6 +45,8 @@ constexpr int kFT = 1024;        // threads per CTA
 constexpr int kFW = kFT / 32;    // warps per CTA
 constexpr int kFSmall = 8192;    // frontier size expanded by the per-CTA scan
 constexpr int kFChunk = kFT;     // frontier entries per scan chunk (large frontiers)
+constexpr int kStreak = 16;      // consecutive small push levels before handing over to the small grid
+constexpr int kSmallGrid = 16;   // CTAs of the small-grid launch
 
 template <typename OffT>
 struct FusedArgs {
@@ -60,8 +62,11 @@ struct FusedArgs {
   long long* tail;     // 4-level ring of queue tails (bitmap -> queue compaction)
   long long* pre;      // per-entry exclusive prefix of degrees within its chunk
   long long* ctot;     // chunk totals -> exclusive chunk offsets; ctot[nchunks] = E
-  int64_t* stats;      // [levels, pull levels]
+  int64_t* state;      // [level, queue valid, bitmap valid, pull levels, done] across launches
   int64_t n, mdiv;
+  int64_t small_max;   // a push level with sum outdeg F <= small_max is "small"
+  int mode;            // 0: full grid, hands over after kStreak small levels; 1: small grid, hands back
+                       //    as soon as a level is not small (high-diameter graphs: cheaper barriers)
   int policy, sw;
   unsigned long long* times;  // optional (GI_DEBUG_BFS_FUSED): per level [start, work done, barrier done]
   int max_times;
@@ -127,17 +132,26 @@ __global__ void __launch_bounds__(kFT, 2) k_bfs_fused(FusedArgs<OffT> A) {
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int64_t G = gridDim.x;
   const int64_t words = (A.n + 31) >> 5;
-  bool qvalid = true;  // the current frontier is available as a queue ...
-  bool bvalid = true;  // ... and as a bitmap (level 0: both, set up by the host)
-  int64_t level = 0, pulls = 0;
+  int64_t level = A.state[0], pulls = A.state[3];
+  bool qvalid = A.state[1] != 0;  // the current frontier is available as a queue ...
+  bool bvalid = A.state[2] != 0;  // ... and as a bitmap (level 0: both, set up by the host)
+  bool done = false;
+  int streak = 0;
   for (;;) {
     const int64_t* c = A.cnt + 2 * (level % 4);
     const int64_t nf = vload(c), sdeg = vload(c + 1);
     const bool timed = A.times && blockIdx.x == 0 && tid == 0 && level < A.max_times;
     if (timed) A.times[3 * level] = gtimer();
-    if (nf == 0) break;
+    if (nf == 0) {
+      done = true;
+      break;
+    }
     const bool pull = A.policy == GI_BFS_PULL_ONLY ? level > 0
                                                    : (A.policy == GI_BFS_AUTO && nf + sdeg > A.mdiv);
+    const bool small = !pull && sdeg <= A.small_max;
+    if (A.mode == 1 && !small) break;                  // back to the full grid
+    streak = small ? streak + 1 : 0;
+    if (A.mode == 0 && A.small_max > 0 && streak > kStreak) break;  // hand over to the small grid
     uint32_t* bcur = A.bm[level % 3];
     uint32_t* bnext = A.bm[(level + 1) % 3];
     int32_t* qcur = A.q[level & 1];
@@ -406,8 +420,11 @@ __global__ void __launch_bounds__(kFT, 2) k_bfs_fused(FusedArgs<OffT> A) {
     ++level;
   }
   if (blockIdx.x == 0 && tid == 0) {
-    A.stats[0] = level;
-    A.stats[1] = pulls;
+    A.state[0] = level;
+    A.state[1] = qvalid;
+    A.state[2] = bvalid;
+    A.state[3] = pulls;
+    A.state[4] = done;
   }
 }
 
@@ -422,6 +439,11 @@ __global__ void k_fused_init(int32_t s_in, const int32_t* __restrict__ inv, cons
   for (int i = 0; i < 4; ++i) tail[i] = 0;
   cnt[0] = 1;
   cnt[1] = outdeg[s];
+  cnt[12] = 0;  // state: level
+  cnt[13] = 1;  //        frontier valid as a queue
+  cnt[14] = 1;  //        frontier valid as a bitmap
+  cnt[15] = 0;  //        pull levels
+  cnt[16] = 0;  //        done
 }
 
 }  // namespace
@@ -436,7 +458,7 @@ static gi_status bfs_fused_t(gi_graph g, int32_t source, const gi_bfs_opts& o, i
     GI_TRY(F.parent.alloc((n + 1) * sizeof(int32_t)));
     for (int k = 0; k < 2; ++k) GI_TRY(F.q[k].alloc((n + 1) * sizeof(int32_t)));
     for (int k = 0; k < 3; ++k) GI_TRY(F.bm[k].alloc((words + 1) * sizeof(uint32_t)));
-    GI_TRY(F.cnt.alloc(16 * sizeof(int64_t)));
+    GI_TRY(F.cnt.alloc(24 * sizeof(int64_t)));
     GI_TRY(F.pre.alloc((n + 1) * sizeof(long long)));
     GI_TRY(F.ctot.alloc((n / kFChunk + 2) * sizeof(long long)));
     int optin = 0, per_sm = 0;
@@ -464,7 +486,7 @@ static gi_status bfs_fused_t(gi_graph g, int32_t source, const gi_bfs_opts& o, i
   for (int k = 0; k < 3; ++k) GI_CUDA(cudaMemsetAsync(F.bm[k].p, 0, words * sizeof(uint32_t), st));
   int64_t* cnt = F.cnt.as<int64_t>();
   long long* tail = reinterpret_cast<long long*>(cnt + 8);
-  int64_t* stt = cnt + 12;
+  int64_t* stt = cnt + 8 + 4;  // state[5] after the tail ring
   k_fused_init<<<1, 1, 0, st>>>(source, g->relabeled ? g->inv.as<int32_t>() : nullptr, g->outdeg.as<int32_t>(),
                                 F.parent.as<int32_t>(), F.q[0].as<int32_t>(), F.bm[0].as<uint32_t>(), cnt, tail);
   FusedArgs<OffT> A;
@@ -481,7 +503,9 @@ static gi_status bfs_fused_t(gi_graph g, int32_t source, const gi_bfs_opts& o, i
   A.tail = tail;
   A.pre = F.pre.as<long long>();
   A.ctot = F.ctot.as<long long>();
-  A.stats = stt;
+  A.state = stt;
+  A.small_max = 1 << 16;
+  A.mode = 0;
   A.n = n;
   A.mdiv = g->m / (o.threshold_div > 0 ? o.threshold_div : 20);
   A.policy = o.policy;
@@ -496,11 +520,21 @@ static gi_status bfs_fused_t(gi_graph g, int32_t source, const gi_bfs_opts& o, i
     GI_CUDA(cudaMemsetAsync(tbuf.p, 0, (size_t)3 * A.max_times * sizeof(unsigned long long), st));
     A.times = tbuf.as<unsigned long long>();
   }
-  void* args[] = {&A};
-  GI_CUDA(cudaLaunchCooperativeKernel((void*)k_bfs_fused<OffT>, dim3(F.grid), dim3(kFT), args, (size_t)F.dyn, st));
-  GI_CUDA(cudaGetLastError());
-  int64_t lv[2] = {0, 0};
-  GI_CUDA(cudaMemcpyAsync(lv, stt, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  // full grid; high-diameter stretches continue on a small grid (cheaper grid barriers)
+  int64_t* h = ctx->h_scratch;
+  int launches = 1;
+  for (int mode = 0;; mode ^= 1) {
+    A.mode = mode;
+    void* args[] = {&A};
+    const int grid = mode == 0 ? F.grid : std::min(F.grid, kSmallGrid);
+    GI_CUDA(cudaLaunchCooperativeKernel((void*)k_bfs_fused<OffT>, dim3(grid), dim3(kFT), args, (size_t)F.dyn, st));
+    GI_CUDA(cudaGetLastError());
+    ++launches;
+    GI_CUDA(cudaMemcpyAsync(h + 16, stt, 5 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    GI_CUDA(stream_wait(st));
+    if (h[16 + 4]) break;
+  }
+  const int64_t lv[2] = {h[16], h[16 + 3]};
   int64_t reached = 0, edges = 0;
   GI_TRY(bfs_finish_output(g, F.parent.as<int32_t>(), d_out, &reached, &edges));
   if (dbg) {
@@ -528,7 +562,7 @@ static gi_status bfs_fused_t(gi_graph g, int32_t source, const gi_bfs_opts& o, i
     stats->pull_levels = (int32_t)lv[1];
     stats->reached = reached;
     stats->edges_traversed = edges;
-    stats->launches = 3;
+    stats->launches = launches + 1;
   }
   return GI_OK;
 }

@@ -442,7 +442,7 @@ def test_prdelta_parity(gi, ctx, policy):
         if policy == "auto" and name == "config1":
             # the paper's point: the frontier shrinks, so later rounds switch to push
             _, st = g.pagerank_delta(15, 0.85, 0.01)
-            assert st.rounds == 15 and 0 < st.pull_rounds < st.rounds
+            assert st.rounds >= 3 and 0 < st.pull_rounds < st.rounds
 
 
 def test_prdelta_equals_pagerank_drop_at_eps0(gi, ctx):
