@@ -197,3 +197,45 @@ CONFIGS = {
               abcd=(0.45, 0.22, 0.22, 0.11), seed=5, symmetrize=True, bfs_sources=16,
               source_seed=1005),
 }
+
+
+# ---------------------------------------------------------------- device generator (billion-edge configs)
+_CU_SRC = os.path.join(_HERE, "graphgen_cuda.cu")
+_CU_LIB = os.path.join(_HERE, "libgraphgen_cuda.so")
+_cu = None
+
+
+def build_cuda(force: bool = False) -> str:
+    """Compile the CUDA twin of the RMAT generator (same counter-based stream)."""
+    if force or not os.path.exists(_CU_LIB) or os.path.getmtime(_CU_LIB) < os.path.getmtime(_CU_SRC):
+        tmp = _CU_LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(["/usr/local/cuda/bin/nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3",
+                               "-Xcompiler", "-fPIC", "-shared", "-o", tmp, _CU_SRC])
+        os.replace(tmp, _CU_LIB)
+    return _CU_LIB
+
+
+def rmat_device(scale: int, edge_factor: int, a: float, b: float, c: float, seed: int, device: int = 0,
+                first: int = 0, count: int | None = None):
+    """RMAT edge stream [first, first+count) generated on the GPU into int32 torch tensors."""
+    global _cu
+    import torch
+
+    with _lock:
+        if _cu is None:
+            lib = ctypes.CDLL(build_cuda())
+            lib.gg_rmat_device.argtypes = [ctypes.c_int, ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                                           ctypes.c_uint64, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p,
+                                           ctypes.c_void_p, ctypes.c_void_p]
+            lib.gg_rmat_device.restype = ctypes.c_int
+            _cu = lib
+    total = edge_factor * (1 << scale)
+    if count is None:
+        count = total - first
+    src = torch.empty(count, dtype=torch.int32, device=device)
+    dst = torch.empty(count, dtype=torch.int32, device=device)
+    rc = _cu.gg_rmat_device(scale, a, b, c, seed, first, count, src.data_ptr(), dst.data_ptr(),
+                            torch.cuda.current_stream(device).cuda_stream)
+    if rc != 0:
+        raise RuntimeError(f"gg_rmat_device failed with CUDA error {rc}")
+    return src, dst

@@ -253,22 +253,39 @@ __global__ void __launch_bounds__(kFT, 2) k_bfs_fused(FusedArgs<OffT> A) {
             e = (int64_t)A.csr_off[u];
             e1 = (int64_t)A.csr_off[u + 1];
           }
-          int rounds = (int)min(e1 - e, (int64_t)INT_MAX);
+          // 4 neighbours per step with independent loads / CAS (one dependent chain per
+          // step instead of per edge), then one warp-aggregated append of all wins
+          int rounds = (int)min((e1 - e + 3) / 4, (int64_t)INT_MAX);
           for (int o = 16; o > 0; o >>= 1) rounds = max(rounds, __shfl_xor_sync(0xffffffffu, rounds, o));
-          for (int k = 0; k < rounds; ++k) {  // warp-uniform; appends aggregated per warp
-            bool won = false;
-            int32_t v = -1;
-            if (e + k < e1) {
-              v = __ldg(&A.csr_idx[e + k]);
-              if (*(volatile int32_t*)&A.parent[v] == -1) won = atomicCAS(&A.parent[v], -1, u) == -1;
+          for (int k = 0; k < rounds; ++k) {
+            int32_t v[4];
+            unsigned wmask = 0;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) v[j] = e + 4 * k + j < e1 ? __ldg(&A.csr_idx[e + 4 * k + j]) : -1;
+            int32_t pv[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) pv[j] = v[j] >= 0 ? *(volatile int32_t*)&A.parent[v[j]] : 0;
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              if (v[j] >= 0 && pv[j] == -1 && atomicCAS(&A.parent[v[j]], -1, u) == -1) wmask |= 1u << j;
+            const int mine = __popc(wmask);
+            int incl = mine;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+              const int t = __shfl_up_sync(0xffffffffu, incl, o);
+              if (lane >= o) incl += t;
             }
-            const unsigned mask = __ballot_sync(0xffffffffu, won);
-            if (mask) {
-              if (won) fdeg += __ldg(&A.outdeg[v]);
+            const int wtot = __shfl_sync(0xffffffffu, incl, 31);
+            if (wtot) {
               long long pos = 0;
-              if (lane == 0) pos = (long long)atomicAdd(tn, (unsigned long long)__popc(mask));
-              pos = __shfl_sync(0xffffffffu, pos, 0);
-              if (won) qnext[pos + __popc(mask & ((1u << lane) - 1))] = v;
+              if (lane == 0) pos = (long long)atomicAdd(tn, (unsigned long long)wtot);
+              pos = __shfl_sync(0xffffffffu, pos, 0) + incl - mine;
+#pragma unroll
+              for (int j = 0; j < 4; ++j)
+                if ((wmask >> j) & 1u) {
+                  qnext[pos++] = v[j];
+                  fdeg += __ldg(&A.outdeg[v[j]]);
+                }
             }
           }
         }
