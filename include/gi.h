@@ -161,6 +161,9 @@ typedef struct {
   int32_t segment_size; /* GI_PR_PULL_SEGMENTED: sources per shared-memory
                         segment; 0 = as many as fit in one CTA's shared memory
                         (smaller values exercise many segments in tests) */
+  int32_t dst_block;    /* GI_PR_PULL_SEGMENTED: destination rows per block
+                        (the per-row accumulator of one block stays in L2);
+                        0 = automatic */
 } gi_pr_opts;
 
 typedef struct {
@@ -169,7 +172,8 @@ typedef struct {
   float edge_ms;           /* sum of edge-pass kernel durations (profile=1) */
   float total_ms;          /* whole call on the stream (profile=1) */
   int32_t kernel;          /* GI_PR_* kernel actually used */
-  int32_t reserved;
+  float vertex_ms;         /* segmented pull: part of edge_ms spent in the
+                              vertex-update kernel (profile=1) */
   int64_t bytes_alg_per_iter; /* 4m + (o+12)n for pull */
 } gi_pr_stats;
 

@@ -377,6 +377,8 @@ gi_status gi_pagerank_ex(gi_graph g, int32_t iters, double damping, const gi_pr_
     return fail(GI_ERR_INVALID_ARGUMENT, "gi_pagerank: bad direction");
   if (o.dangling != GI_DANGLING_UNIFORM && o.dangling != GI_DANGLING_DROP)
     return fail(GI_ERR_INVALID_ARGUMENT, "gi_pagerank: bad dangling rule");
+  if (o.segment_size < 0 || o.dst_block < 0)
+    return fail(GI_ERR_INVALID_ARGUMENT, "gi_pagerank: segment_size / dst_block < 0");
   gi_context ctx = g->ctx;
   GI_CUDA(cudaSetDevice(ctx->device));
   OutBuf<float> ob{out, g->n, false, &g->out_stage};

@@ -116,14 +116,18 @@ struct gi_graph_s {
   gi::DevBuf split_cnt;   // int32[n]: arrival counters for split rows
   gi::DevBuf push_sum;    // double[n]: push-form accumulator
   // segmented pull (pr_segmented.cu); seg_Z == 0 until built
-  int seg_Z = 0, seg_S = 0, seg_ctas = 0;
-  int64_t seg_P = 0, seg_C = 0, seg_T = 0;  // pieces, chunks, tiles
-  gi::DevBuf seg_pstart;                    // OffT[n+1]: first destination-major piece of v
-  gi::DevBuf seg_cidx, seg_cslot;           // chunks: 4 x uint16 source ids, slot | last-chunk bit
-  gi::DevBuf seg_tiles;                     // int32[T]: segment of each tile
-  gi::DevBuf seg_cta_tiles;                 // int32[C+1]: cost-balanced tile range of each CTA
-  gi::DevBuf seg_partial;                   // float[P+1]: per-piece partial sums (+1 dummy)
-  gi::DevBuf seg_carry_slot, seg_carry_val; // per CTA: piece cut by the CTA's range end
+  int seg_Z = 0, seg_S = 0, seg_U = 0, seg_ctas = 0;  // segment size, segments, units, CTAs
+  int64_t seg_DB = 0, seg_P = 0, seg_C = 0;          // rows per destination block, pieces, chunks
+  gi::DevBuf seg_idx;      // build only: uint16 per edge slot: source - segment base (padding: Z)
+  gi::DevBuf seg_head;     // build only: uint32 bits: slot starts a piece
+  gi::DevBuf seg_cbase;    // build only: int32[C+1]: piece index of each chunk's first slot
+  gi::DevBuf seg_rec;      // chunk records: idx | head | cbase (pr_segmented.cu)
+  gi::DevBuf seg_pdst;     // int32[P]: local destination row of each piece
+  gi::DevBuf seg_unit_c0;  // int32[U+1]: first chunk of each (block, segment) unit
+  gi::DevBuf seg_cta;      // int32[CTAs+1]: cost-balanced chunk range of each CTA
+  gi::DevBuf seg_acc;      // float[2][seg_acc_stride]: per-row sums (ping-pong), L2-resident
+  int64_t seg_acc_stride = 0;
+  int seg_acc_cur = 0;     // buffer the next edge pass reduces into (all zero)
   gi::DevBuf out_stage;   // float/int32[n]: output staging in input ids
   // BFS workspace
   gi::DevBuf parent;      // int32[n], internal ids
@@ -155,8 +159,14 @@ gi_status pagerank_run(gi_graph g, int32_t iters, double damping, const gi_pr_op
                        float* d_out_input_ids, gi_pr_stats* stats);
 // pr_segmented.cu
 struct PrArgs;
-gi_status seg_build(gi_graph g, int segment_size);
-gi_status seg_edge_pass(gi_graph g, const PrArgs& A);
+// segment_size / block_rows: 0 = automatic (tests pass small values)
+gi_status seg_build(gi_graph g, int segment_size, int64_t block_rows);
+// seg_acc_buf(g, cur)[v] = sum of cin over v's in-edges (the buffer is zero before the pass)
+gi_status seg_edge_pass(gi_graph g, const float* cin);
+// the two accumulators: cur holds the sums of the last edge pass; the other is zero
+inline float* seg_acc_buf(gi_graph g, int which) { return g->seg_acc.as<float>() + which * g->seg_acc_stride; }
+// vertex update from the current accumulator; zeroes the other one (never a
+// load and a store to the same line: that stalls on L2 misses) and flips them
 gi_status seg_vertex_pass(gi_graph g, const PrArgs& A);
 // prdelta.cu
 gi_status prdelta_run(gi_graph g, int32_t iters, double damping, double eps, const gi_prdelta_opts& o, float* d_out,

@@ -154,9 +154,9 @@ gi_status pagerank_run(gi_graph g, int32_t iters, double damping, const gi_pr_op
   const bool dist = ctx->nranks > 1;
   gi_pr_stats S{};
   int kernel = o.direction;
-  if (kernel == GI_PR_PULL) kernel = (nr > 0 && ml > 0 && seg_build(g, o.segment_size) == GI_OK) ? GI_PR_PULL_SEGMENTED : GI_PR_PULL_DIRECT;
+  if (kernel == GI_PR_PULL) kernel = (nr > 0 && ml > 0 && seg_build(g, o.segment_size, o.dst_block) == GI_OK) ? GI_PR_PULL_SEGMENTED : GI_PR_PULL_DIRECT;
   else if (kernel == GI_PR_PULL_SEGMENTED) {
-    if (nr > 0 && ml > 0) GI_TRY(seg_build(g, o.segment_size));
+    if (nr > 0 && ml > 0) GI_TRY(seg_build(g, o.segment_size, o.dst_block));
     else kernel = GI_PR_PULL_DIRECT;
   }
   if (dist) {  // every rank must run the same kernel family (collective call sequence)
@@ -209,12 +209,10 @@ gi_status pagerank_run(gi_graph g, int32_t iters, double damping, const gi_pr_op
     GI_TRY(rank_int.alloc(n * sizeof(float)));
   }
 
-  cudaEvent_t ev[2] = {nullptr, nullptr}, tot[2] = {nullptr, nullptr};
+  cudaEvent_t ev[3] = {nullptr, nullptr, nullptr}, tot[2] = {nullptr, nullptr};
   if (o.profile) {
-    for (int k = 0; k < 2; ++k) {
-      GI_CUDA(cudaEventCreate(&ev[k]));
-      GI_CUDA(cudaEventCreate(&tot[k]));
-    }
+    for (int k = 0; k < 3; ++k) GI_CUDA(cudaEventCreate(&ev[k]));
+    for (int k = 0; k < 2; ++k) GI_CUDA(cudaEventCreate(&tot[k]));
     GI_CUDA(cudaEventRecord(tot[0], st));
   }
   GI_CUDA(cudaMemsetAsync(g->dbuf.p, 0, 4 * sizeof(double), st));
@@ -235,7 +233,7 @@ gi_status pagerank_run(gi_graph g, int32_t iters, double damping, const gi_pr_op
   A.split_acc = g->split_acc.as<double>();
   A.split_cnt = g->split_cnt.as<int32_t>();
   A.perm = (g->relabeled && !dist) ? g->perm.as<int32_t>() : nullptr;
-  float edge_ms = 0.f;
+  float edge_ms = 0.f, vertex_ms = 0.f;
   for (int it = 0; it < iters; ++it) {
     A.it = it;
     A.cin = g->contrib[it & 1].as<float>();
@@ -255,7 +253,8 @@ gi_status pagerank_run(gi_graph g, int32_t iters, double damping, const gi_pr_op
       k_pr_vertex<<<grid_for(nr, 256, sms), 256, 0, st>>>(A, g->push_sum.as<double>());
       S.aux_launches++;
     } else if (kernel == GI_PR_PULL_SEGMENTED) {
-      GI_TRY(seg_edge_pass(g, A));
+      GI_TRY(seg_edge_pass(g, A.cin));
+      if (o.profile) GI_CUDA(cudaEventRecord(ev[2], st));
       GI_TRY(seg_vertex_pass(g, A));
       S.aux_launches++;
       if (o.profile) GI_CUDA(cudaEventRecord(ev[1], st));
@@ -289,6 +288,10 @@ gi_status pagerank_run(gi_graph g, int32_t iters, double damping, const gi_pr_op
       float ms = 0.f;
       GI_CUDA(cudaEventElapsedTime(&ms, ev[0], ev[1]));
       edge_ms += ms;
+      if (kernel == GI_PR_PULL_SEGMENTED) {
+        GI_CUDA(cudaEventElapsedTime(&ms, ev[2], ev[1]));
+        vertex_ms += ms;
+      }
     }
   }
   if (o.profile) {
@@ -296,10 +299,9 @@ gi_status pagerank_run(gi_graph g, int32_t iters, double damping, const gi_pr_op
     GI_CUDA(cudaEventSynchronize(tot[1]));
     GI_CUDA(cudaEventElapsedTime(&S.total_ms, tot[0], tot[1]));
     S.edge_ms = edge_ms;
-    for (int k = 0; k < 2; ++k) {
-      cudaEventDestroy(ev[k]);
-      cudaEventDestroy(tot[k]);
-    }
+    S.vertex_ms = vertex_ms;
+    for (int k = 0; k < 3; ++k) cudaEventDestroy(ev[k]);
+    for (int k = 0; k < 2; ++k) cudaEventDestroy(tot[k]);
   }
   if (stats) *stats = S;
   return GI_OK;

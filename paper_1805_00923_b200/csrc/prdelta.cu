@@ -32,8 +32,8 @@ constexpr int kVT = 256;
 template <typename OffT>
 struct PrdVertexArgs {
   int64_t n;
-  const OffT* __restrict__ pstart;     // pull: destination-major piece starts
-  const float* __restrict__ partial;   // pull: per-piece partial sums
+  const float* __restrict__ pacc;      // pull: per-vertex sums of the segmented pass
+  float* __restrict__ pzero;           // pull: the other accumulator, zeroed here
   double* __restrict__ acc;            // push: per-vertex accumulator (zeroed here)
   const int32_t* __restrict__ outdeg;
   double* __restrict__ rank;           // fp64 like the paper's vectors: the frontier
@@ -62,9 +62,8 @@ __global__ void __launch_bounds__(kVT) k_prd_vertex(PrdVertexArgs<OffT> A) {
         ds = A.acc[v];
         A.acc[v] = 0.0;
       } else {
-        const int64_t a = A.pstart[v], e = A.pstart[v + 1];
-        ds = 0.0;
-        for (int64_t j = a; j < e; ++j) ds += (double)__ldg(&A.partial[j]);
+        ds = (double)A.pacc[v];
+        A.pzero[v] = 0.f;
       }
       double delta;
       if (A.first) {
@@ -136,7 +135,7 @@ static gi_status prdelta_t(gi_graph g, int32_t iters, double damping, double eps
   const int sms = ctx->num_sms;
   const int64_t n = g->n, m = g->m;
   gi_prdelta_stats S{};
-  const bool can_pull = o.policy != GI_PRD_PUSH_ONLY && seg_build(g, 0) == GI_OK;
+  const bool can_pull = o.policy != GI_PRD_PUSH_ONLY && seg_build(g, 0, 0) == GI_OK;
   if (o.policy == GI_PRD_PULL_ONLY && !can_pull)
     return fail(GI_ERR_UNSUPPORTED, "gi_pagerank_delta: pull needs the segmented layout (non-empty graph)");
   DevBuf rank, cbuf[2], q[2], acc, cnt;
@@ -179,11 +178,10 @@ static gi_status prdelta_t(gi_graph g, int32_t iters, double damping, double eps
     V.first = r == 1;
     GI_CUDA(cudaMemsetAsync(cn, 0, 2 * sizeof(unsigned long long), st));
     if (pull) {
-      PrArgs A{};
-      A.cin = cbuf[cur].as<float>();
-      GI_TRY(seg_edge_pass(g, A));  // partial[piece] = sum of contrib over the piece
-      V.pstart = g->seg_pstart.as<OffT>();
-      V.partial = g->seg_partial.as<float>();
+      GI_TRY(seg_edge_pass(g, cbuf[cur].as<float>()));  // seg_acc[v] = sum of contrib over in(v)
+      V.pacc = seg_acc_buf(g, g->seg_acc_cur);
+      V.pzero = seg_acc_buf(g, g->seg_acc_cur ^ 1);
+      g->seg_acc_cur ^= 1;
       S.pull_rounds++;
       S.launches += 2;
     } else {

@@ -46,12 +46,12 @@ GI_PRD_AUTO, GI_PRD_PUSH_ONLY, GI_PRD_PULL_ONLY = 0, 1, 2
 
 class gi_pr_opts(ctypes.Structure):
     _fields_ = [("direction", ctypes.c_int32), ("dangling", ctypes.c_int32), ("profile", ctypes.c_int32),
-                ("segment_size", ctypes.c_int32)]
+                ("segment_size", ctypes.c_int32), ("dst_block", ctypes.c_int32)]
 
 
 class gi_pr_stats(ctypes.Structure):
     _fields_ = [("edge_launches", ctypes.c_int32), ("aux_launches", ctypes.c_int32), ("edge_ms", ctypes.c_float),
-                ("total_ms", ctypes.c_float), ("kernel", ctypes.c_int32), ("reserved", ctypes.c_int32),
+                ("total_ms", ctypes.c_float), ("kernel", ctypes.c_int32), ("vertex_ms", ctypes.c_float),
                 ("bytes_alg_per_iter", ctypes.c_int64)]
 
 
@@ -274,12 +274,13 @@ def gi_pagerank(g: int, iters: int, damping: float, out=None):
 
 
 def gi_pagerank_ex(g: int, iters: int, damping: float, out=None, direction: int = GI_PR_PULL,
-                   dangling: int = GI_DANGLING_UNIFORM, profile: bool = False, segment_size: int = 0):
+                   dangling: int = GI_DANGLING_UNIFORM, profile: bool = False, segment_size: int = 0,
+                   dst_block: int = 0):
     n = gi_graph_num_vertices(g)
     if out is None:
         out = np.empty(n, np.float32)
     p, keep = _ptr(out, np.float32)
-    o = gi_pr_opts(direction, dangling, int(profile), segment_size)
+    o = gi_pr_opts(direction, dangling, int(profile), segment_size, dst_block)
     s = gi_pr_stats()
     _check(_lib.gi_pagerank_ex(g, iters, damping, ctypes.byref(o), p or None, ctypes.byref(s)), "gi_pagerank_ex")
     return keep, s

@@ -214,9 +214,10 @@ def test_pr_config1(gi, ctx, direction, relabel):
     assert st.edge_launches == cfg.pr_iters
 
 
-@pytest.mark.parametrize("seg", [32, 1000, 4096, 20000])
-def test_pr_segmented_many_segments(gi, ctx, seg):
-    """Small segment sizes: many segments, pieces split across tiles and CTAs, carries."""
+@pytest.mark.parametrize("seg,dblk", [(32, 0), (1000, 777), (4096, 50000), (20000, 0), (0, 3000)])
+def test_pr_segmented_many_segments(gi, ctx, seg, dblk):
+    """Small segment sizes and destination blocks: many (block, segment) units,
+    pieces split across chunks and CTAs, tiny units gathered without staging."""
     cases = [(graphgen.CONFIGS[1].n, *graphgen.CONFIGS[1].edges()),
              (70001, *graphgen.random_digraph(70001, 1000003, 5)),
              (100001, *graphgen.in_star(100000)),
@@ -225,9 +226,10 @@ def test_pr_segmented_many_segments(gi, ctx, seg):
         g = gi.Graph(ctx, n, s, d)
         go = oracle.build_graph(n, s, d)
         for dangling in (0, 1):
-            got, st = g.pagerank(20, 0.85, direction=gi.GI_PR_PULL_SEGMENTED, dangling=dangling, segment_size=seg)
+            got, st = g.pagerank(20, 0.85, direction=gi.GI_PR_PULL_SEGMENTED, dangling=dangling, segment_size=seg,
+                                 dst_block=dblk)
             assert st.kernel == gi.GI_PR_PULL_SEGMENTED
-            _pr_check(got, oracle.pagerank(go, 20, 0.85, dangling), f"seg={seg} n={n}")
+            _pr_check(got, oracle.pagerank(go, 20, 0.85, dangling), f"seg={seg} dblk={dblk} n={n}")
 
 
 def test_pr_device_output_and_damping_edges(gi, ctx):

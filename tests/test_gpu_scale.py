@@ -91,11 +91,9 @@ def test_config4_full_scale(gi):
         assert p[int(s0)].item() == int(s0)
         reached = p >= 0
         # depth by pointer jumping over the parent tree
-        depth = torch.where(reached, torch.zeros_like(p), torch.full_like(p, -1))
-        anc = p.clone()
-        anc[int(s0)] = int(s0)
+        # walk from every reached vertex itself, so depth(s) = 0 and depth(child of s) = 1
         steps = torch.zeros_like(p)
-        cur = torch.where(reached, anc, torch.full_like(p, int(s0)))
+        cur = torch.where(reached, torch.arange(n, device=p.device), torch.full_like(p, int(s0)))
         for _ in range(64):
             moving = cur != int(s0)
             if not bool(moving.any()):

@@ -37,7 +37,7 @@ direction = {"pull": gi.GI_PR_PULL, "push": gi.GI_PR_PUSH, "direct": gi.GI_PR_PU
 for _ in range(args.pr_reps):
     t = time.perf_counter()
     _, st = g.pagerank(args.pr_iters, cfg.damping, out=out, direction=direction, profile=True)
-    print(f"pr: {st.edge_ms / max(st.edge_launches, 1):.4f} ms/iter, total {st.total_ms:.3f} ms, "
+    print(f"pr: {st.edge_ms / max(st.edge_launches, 1):.4f} ms/iter (vertex {st.vertex_ms / max(st.edge_launches, 1):.4f}), total {st.total_ms:.3f} ms, "
           f"{st.bytes_alg_per_iter / (st.edge_ms / st.edge_launches * 1e-3) / 1e9:.1f} GB/s alg")
 for src in srcs[: args.bfs]:
     _, bs = g.bfs(int(src), out=par, profile=True)
