@@ -117,14 +117,10 @@ struct gi_graph_s {
   gi::DevBuf push_sum;    // double[n]: push-form accumulator
   // segmented pull (pr_segmented.cu); seg_Z == 0 until built
   int seg_Z = 0, seg_S = 0, seg_U = 0, seg_ctas = 0;  // segment size, segments, units, CTAs
-  int64_t seg_DB = 0, seg_P = 0, seg_C = 0;          // rows per destination block, pieces, chunks
-  gi::DevBuf seg_idx;      // build only: uint16 per edge slot: source - segment base (padding: Z)
-  gi::DevBuf seg_head;     // build only: uint32 bits: slot starts a piece
-  gi::DevBuf seg_cbase;    // build only: int32[C+1]: piece index of each chunk's first slot
-  gi::DevBuf seg_rec;      // chunk records: idx | head | cbase (pr_segmented.cu)
-  gi::DevBuf seg_pdst;     // int32[P]: local destination row of each piece
-  gi::DevBuf seg_unit_c0;  // int32[U+1]: first chunk of each (block, segment) unit
-  gi::DevBuf seg_cta;      // int32[CTAs+1]: cost-balanced chunk range of each CTA
+  int64_t seg_DB = 0, seg_P = 0, seg_C = 0;          // rows per destination block, pieces, records
+  gi::DevBuf seg_rec;      // records: long (lane-aligned) and short (lane-per-piece), pr_segmented.cu
+  gi::DevBuf seg_unit_c0;  // int32[U+1]: first record of each (block, segment) unit
+  gi::DevBuf seg_cta;      // int32[CTAs+1]: cost-balanced record range of each CTA
   gi::DevBuf seg_acc;      // float[2][seg_acc_stride]: per-row sums (ping-pong), L2-resident
   int64_t seg_acc_stride = 0;
   int seg_acc_cur = 0;     // buffer the next edge pass reduces into (all zero)

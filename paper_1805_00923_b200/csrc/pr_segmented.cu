@@ -4,38 +4,43 @@
 // partition the source range so each segment's
 // random reads hit cache, then merge the per-segment partial sums) retargeted
 // at the B200's 227 KB of shared memory per CTA. Measured on this part
-// (tools/microbench/, profiles/r01_gather_rates.txt, r01_red_rates.txt):
-// random 4-byte gathers run at ~1.0 per SM-clock from L2 but ~7 per SM-clock
-// from shared memory, so the pull edge pass (a4) gathers contrib from a staged
-// segment instead of from L2. A segment holds Z <= 65535 sources, so in-segment
-// source ids are 16-bit and the index stream is 2 bytes per edge.
+// (tools/microbench/, profiles/): random 4-byte gathers run at ~1.0 per
+// SM-clock from L2 but ~7 per SM-clock from shared memory, so the pull edge
+// pass (a4) gathers contrib from a staged segment instead of from L2. A
+// segment holds Z <= 65535 sources, so in-segment source ids are 16-bit and
+// the index stream is 2 bytes per edge.
 //
 // Layout (built once per graph):
-//   unit u = (destination block b, source segment s), u = b*S + s, holding the
-//            edges (v, w) with v in block b (rows [b*DB, (b+1)*DB)) and w in
-//            segment s (sources [s*Z, (s+1)*Z)), in (v, w) order. One block
-//            (DB = all rows) unless the accumulator would not fit in L2.
-//   piece    = (unit, destination) run: the partial sum the paper's segmented
-//              subgraphs merge ("SSG" partials).
-//   chunk    = 512 consecutive edge slots of one unit (32 lanes x 16); every
-//              unit is padded to whole chunks with the index Z (a shared-memory
-//              zero), so a chunk never spans two units.
-//   idx[]    uint16 per slot: w - s*Z
-//   head[]   1 bit per slot: the slot starts a piece
-//   cbase[c] piece index of chunk c's first slot
-//   pdst[p]  destination (local row) of piece p
+//   unit u  = (destination block b, source segment s), u = b*S + s: the edges
+//             (v, w) with v in rows [b*DB, (b+1)*DB) and w in sources
+//             [s*Z, (s+1)*Z). One block (DB = all rows) unless the per-row
+//             accumulator would not fit in L2.
+//   piece   = (unit, destination) run: the partial sum the paper's segmented
+//             subgraphs merge ("SSG" partials).
+//   record  = kRecBytes: a 16-byte header {type, L, groups} and one of
+//     long  (type 1): 512 edge slots of pieces with >= kLongPiece edges, each
+//           piece padded to whole 16-slot lanes (so a lane never holds two
+//           pieces): uint16 idx[512] | int32 dst[33] | uint32 mask.
+//           mask bit l: lane l starts a piece; dst[0]: the piece holding lane
+//           0, dst[q]: the q-th piece starting at lanes 1..31.
+//     short (type 2): pieces of exactly L < kLongPiece edges, 32 per group
+//           (one lane each), R_L groups: per group uint16 idx[L][32] |
+//           int32 dst[32]. Unused lanes read the zero slot and add into a
+//           trash row.
+//   A unit's records are its long records, then its short records by L.
 // Per iteration:
-//   k_pr_seg  persistent, one 512-thread CTA per SM over a cost-balanced
-//             range of chunks: stage the unit's contrib segment in shared
-//             memory (TMA bulk copy), then every warp reduces whole chunks on
-//             its own — 16 shared-memory gathers per lane, a warp segmented
-//             scan whose reset flags come from one ballot — and folds every
-//             piece that ends in the chunk (and the one still open at its end)
-//             into acc[v] with red.global.add.f32. acc (4 B per row of the
-//             block) stays in L2, so no partials go to HBM and no merge pass
-//             is needed; pieces cut by chunk boundaries need no carries.
+//   k_pr_seg  persistent, one CTA per SM over a cost-balanced range of
+//             records. A producer warp streams records into a kStages-deep
+//             shared-memory ring with bulk copies (TMA); the unit's contrib
+//             segment is staged with one more bulk copy. Each of kConsumers
+//             warps takes one record per stage: long: every lane sums its 16
+//             gathers, a warp segmented scan over lanes (resets from the
+//             mask) leaves each piece's sum in its last lane; short: every
+//             lane sums its piece's L gathers. The sums go into acc[v] with
+//             red.global.add.f32 — acc (4 B per row of the block) stays in
+//             L2, so no partials reach HBM and no merge pass is needed.
 //   k_pr_acc  r'[v] = (1-d)/n + d (acc[v] + D/n), contrib', dangling mass
-//             (fused vertex update a3); acc[v] reset to 0.
+//             (fused vertex update a3); zeroes the other (ping-pong) accumulator.
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
@@ -48,38 +53,35 @@
 namespace gi {
 namespace {
 
-constexpr int kConsumers = 16;                // consumer warps (one chunk each per stage)
+constexpr int kConsumers = 16;                      // consumer warps (one record each per stage)
 constexpr int kSegThreads = 32 * (kConsumers + 1);  // + one producer warp (TMA)
-constexpr int kLaneE = 16;                    // edge slots per lane per chunk
-constexpr int kChunkE = 32 * kLaneE;          // edge slots per chunk (one warp)
-constexpr int kChunkW = kChunkE / 32;         // head words per chunk
-// chunk record (interleaved so one bulk copy moves a run of chunks):
-//   uint16 idx[512] | uint32 head[16] | uint16 j0[32] | int32 cbase | pad
-// j0[l] = pieces closed in lanes < l (chunk-relative index of the piece open
-// at lane l's first slot)
-constexpr int kRecHead = 2 * kChunkE;         // byte offset of the head words
-constexpr int kRecJ0 = kRecHead + 4 * kChunkW;
-constexpr int kRecBase = kRecJ0 + 2 * 32;
-constexpr int kRecBytes = kRecBase + 16;      // 1168, a multiple of 16 (bulk-copy granule)
-constexpr int kStages = 4;                    // ring depth (stages in flight per CTA)
+constexpr int kLaneE = 16;                          // edge slots per lane (long records)
+constexpr int kChunkE = 32 * kLaneE;                // edge slots per long record
+constexpr int kLongPiece = 16;                      // pieces of >= 16 edges go to long records
+constexpr int kADst = 33;
+constexpr int kRecHdr = 16;
+constexpr int kRecPayload = 1168;
+constexpr int kRecBytes = kRecHdr + kRecPayload;    // 1184, a multiple of the 16-byte bulk-copy granule
+constexpr int kLDst = kRecHdr + 2 * kChunkE;        // long: dst[33]
+constexpr int kLMask = kLDst + 4 * kADst;           // long: mask
+static_assert(kLMask + 4 <= kRecBytes, "long record overflows");
+__host__ __device__ constexpr int short_group_bytes(int L) { return 64 * L + 128; }
+__host__ __device__ constexpr int short_groups(int L) { return kRecPayload / short_group_bytes(L); }
+constexpr int kStages = 4;                          // ring depth (stages in flight per CTA)
 constexpr int kStageBytes = kConsumers * kRecBytes;
-constexpr int kScratch = kChunkE + 32;        // floats of piece scratch per consumer warp
-constexpr int kChunkCost = 2 * kChunkE;       // CTA balance: a chunk costs 2 per slot ...
-constexpr int kPieceCost = 3;                 // ... plus 3 per piece (fitted from per-CTA timings)
-constexpr int64_t kStageCost = 99 * kChunkCost;  // a unit start ~ 99 chunks (staging + pipeline refill)
-constexpr int64_t kDefaultBlockRows = 8 << 20;  // 32 MB accumulator per destination block
+// CTA balance (costs in gather slots; fitted from per-CTA timings, tools/seg_timing.py)
+constexpr int kPieceCost = 1;
+constexpr int64_t kUnitCost = 40 * kChunkE;         // a unit start: segment staging + pipeline refill
+constexpr int64_t kDefaultBlockRows = 8 << 20;      // 32 MB accumulator per destination block
 
 struct SegArgs {
-  const uint8_t* __restrict__ rec;     // kRecBytes per chunk
-  const int32_t* __restrict__ cbase;   // C + 1 (consumers prefetch piece destinations ahead)
-  const int32_t* __restrict__ pdst;    // P (+ padding)
-  const int32_t* __restrict__ unit_c0; // U + 1: first chunk of each unit
-  const int32_t* __restrict__ cta_c0;  // grid + 1: first chunk of each CTA
+  const uint8_t* __restrict__ rec;     // kRecBytes per record
+  const int32_t* __restrict__ unit_c0; // U + 1: first record of each unit
+  const int32_t* __restrict__ cta_c0;  // grid + 1: first record of each CTA
   const float* __restrict__ cin;       // contrib, global ids, padded by >= 16 floats
-  float* __restrict__ acc;             // per local row
+  float* __restrict__ acc;             // per local row (+ trash row at nr)
   int64_t n;
   int Z, S, U;
-  // diagnostics (GI_SEG_MODE, template MODE): 0 full, 1 no REDs, 2 gathers only, 3 stream only
   unsigned long long* timing;  // diagnostics (GI_DEBUG_SEG_TIMING): per CTA [start, end, staging ns, units]
 };
 
@@ -118,134 +120,100 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
-__device__ __forceinline__ void prefetch_l2(const void* p) {
-  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
-}
-
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-// Reduce one chunk whose record sits in shared memory at `r`. SMEM: gather
-// from the staged segment `sc`; else from global `gsrc` (= cin + s*Z; the
-// padding index Z reads as 0). `sv` is this warp's scratch: the value of the
-// chunk's j-th piece (piece cbase + j) lands in sv[j], then the warp folds
-// them into acc with dense, coalesced REDs (a chunk's pieces have increasing
-// destinations). `empty`: the stage barrier to release once the record is
-// in registers.
-template <int MODE, bool SMEM>
-__device__ __forceinline__ void chunk_reduce(const SegArgs& A, const uint8_t* r, const float* sc, const float* gsrc,
-                                             float* sv, int lane, int Z, uint64_t* empty, int pd0, int pd1) {
-  const uint4 qa = *reinterpret_cast<const uint4*>(r + 32 * lane);
-  const uint4 qb = *reinterpret_cast<const uint4*>(r + 32 * lane + 16);
-  const uint32_t hw = *reinterpret_cast<const uint32_t*>(r + kRecHead + 4 * (lane >> 1));
-  const int cb = *reinterpret_cast<const int32_t*>(r + kRecBase);
-  const int j0 = *reinterpret_cast<const uint16_t*>(r + kRecJ0 + 2 * lane);
+// Long record: every lane's 16 slots belong to one piece, so a lane sums its
+// gathers; a warp segmented scan over lanes (reset where the mask marks a
+// piece start) leaves each piece's sum in its last lane, which folds it into acc.
+template <int MODE>
+__device__ __forceinline__ void reduce_long(const SegArgs& A, const uint8_t* r, const float* sc, int lane,
+                                            uint64_t* empty) {
+  const uint4 qa = *reinterpret_cast<const uint4*>(r + kRecHdr + 32 * lane);
+  const uint4 qb = *reinterpret_cast<const uint4*>(r + kRecHdr + 32 * lane + 16);
+  const uint32_t mask = *reinterpret_cast<const uint32_t*>(r + kLMask);
+  const int q = __popc(mask & ((2u << lane) - 1u) & ~1u);
+  const int dst = *reinterpret_cast<const int32_t*>(r + kLDst + 4 * q);
   __syncwarp();
   if (lane == 0) mbar_arrive(empty);  // the record may be overwritten now
   const uint32_t w[8] = {qa.x, qa.y, qa.z, qa.w, qb.x, qb.y, qb.z, qb.w};
-  if (MODE == 3) {  // diagnostics: stream only
-    if ((qa.x ^ qa.y ^ qa.z ^ qa.w ^ qb.x ^ qb.y ^ qb.z ^ qb.w ^ hw ^ pd0 ^ pd1) == 0x9e3779b9u) A.acc[lane] += 1.f;
-    return;
-  }
   float v[kLaneE];
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
-    const uint32_t i0 = w[j] & 0xFFFFu, i1 = w[j] >> 16;
-    if (SMEM) {
-      v[2 * j] = sc[i0];
-      v[2 * j + 1] = sc[i1];
-    } else {
-      v[2 * j] = i0 == (uint32_t)Z ? 0.f : __ldg(gsrc + i0);
-      v[2 * j + 1] = i1 == (uint32_t)Z ? 0.f : __ldg(gsrc + i1);
-    }
+    v[2 * j] = sc[w[j] & 0xFFFFu];
+    v[2 * j + 1] = sc[w[j] >> 16];
   }
-  if (MODE == 2) {  // diagnostics: stream + gathers, no segmentation
-    float s = 0.f;
 #pragma unroll
-    for (int k = 0; k < kLaneE; ++k) s += v[k];
-    if (s == -1.f) A.acc[lane + pd0 + pd1] += s;
+  for (int s = 1; s < kLaneE; s <<= 1)
+#pragma unroll
+    for (int k = 0; k < kLaneE; k += 2 * s) v[k] += v[k + s];
+  float X = v[0];
+  if (MODE == 1) {  // diagnostics: stream + gathers only
+    if (X == -1.f) A.acc[lane] += X;
     return;
   }
-  const uint32_t hb = (hw >> ((lane & 1) * 16)) & 0xFFFFu;  // bit k: slot lane*16+k starts a piece
-  // every head closes the piece before it, except at chunk position 0 (that
-  // piece has no slot in this chunk)
-  const uint32_t cl = lane == 0 ? (hb & ~1u) : hb;
-  const int cnt = __popc(cl);
-  // branch-free pass over the slots, as two independent halves: a closing
-  // stores the run it ends at sv[j] (j = chunk-relative index of the piece
-  // open at that slot) and restarts it. The lane's first closing ends the
-  // piece that began in an earlier lane: the scan's carry is added to it
-  // below. Half 1 starts as if no piece were open (run 0); if it has a
-  // closing, its first one is completed with half 0's open run.
-  constexpr int H = kLaneE / 2;
-  const uint32_t cl0 = cl & ((1u << H) - 1u), cl1 = cl >> H;
-  float run0 = 0.f, run1 = 0.f;
-  float* sp0 = sv + j0;
-  float* sp1 = sv + j0 + __popc(cl0);
-  float* first1 = sp1;
-#pragma unroll
-  for (int k = 0; k < H; ++k) {
-    const bool c0 = (cl0 >> k) & 1u, c1 = (cl1 >> k) & 1u;
-    if (c0) *sp0 = run0;
-    if (c1) *sp1 = run1;
-    sp0 += c0 ? 1 : 0;
-    sp1 += c1 ? 1 : 0;
-    run0 = (c0 ? 0.f : run0) + v[k];
-    run1 = (c1 ? 0.f : run1) + v[H + k];
-  }
-  float run;
-  if (cl1) {
-    *first1 += run0;  // half 1's first closing ends the run open at the end of half 0
-    run = run1;
-  } else {
-    run = run0 + run1;
-  }
-  // warp segmented inclusive scan of the runs open at each lane's end (`run`:
-  // after the lane's last head, or the whole lane); a lane with a head resets
-  // it (flags from one ballot)
-  const unsigned hm = __ballot_sync(0xffffffffu, hb != 0);
-  float X = run;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
     const float y = __shfl_up_sync(0xffffffffu, X, o);
-    if (lane >= o && ((hm >> (lane - o + 1)) & ((1u << o) - 1u)) == 0u) X = y + X;
+    if (lane >= o && ((mask >> (lane - o + 1)) & ((1u << o) - 1u)) == 0u) X = y + X;
   }
-  float carry = __shfl_up_sync(0xffffffffu, X, 1);  // run open at this lane's start
-  if (lane == 0) carry = 0.f;
-  if (cnt > 0) sv[j0] += carry;
-  const int np = __shfl_sync(0xffffffffu, j0 + cnt, 31);  // closed pieces; piece np is open at the end
-  if (lane == 31) sv[np] = X;
-  __syncwarp();
-  if (MODE == 1) {  // diagnostics: no REDs
-    if (sv[lane] == -1.f) A.acc[lane] += 1.f;
-    __syncwarp();
-    return;
-  }
-  // dense REDs: lane q folds piece cb + q (destinations of the first 64 in registers)
-  float* acc = A.acc;
-  if (lane <= np) atomicAdd(acc + pd0, sv[lane]);  // RED.E.ADD.F32
-  if (np >= 32) {
-    if (lane + 32 <= np) atomicAdd(acc + pd1, sv[lane + 32]);
-    for (int q = lane + 64; q <= np; q += 32) atomicAdd(acc + __ldg(&A.pdst[cb + q]), sv[q]);
-  }
-  __syncwarp();
+  const bool last = lane == 31 || ((mask >> (lane + 1)) & 1u);
+  if (last) atomicAdd(A.acc + dst, X);  // RED.E.ADD.F32
 }
 
-// Persistent CTA per SM over chunks [cta_c0[b], cta_c0[b+1]), unit by unit.
-// Warp kConsumers is the producer: one lane streams chunk records into a
+// Short record of pieces with exactly L edges: lane l of group g owns one
+// piece: L gathers, one RED.
+template <int MODE>
+__device__ __forceinline__ void reduce_short(const SegArgs& A, const uint8_t* r, const float* sc, int lane,
+                                             uint64_t* empty) {
+  const int L = *reinterpret_cast<const int32_t*>(r + 4);
+  const int ng = *reinterpret_cast<const int32_t*>(r + 8);
+  const int gb = short_group_bytes(L);
+  for (int g = 0; g < ng; ++g) {
+    const uint8_t* b = r + kRecHdr + g * gb + 2 * lane;
+    const int d = *reinterpret_cast<const int32_t*>(r + kRecHdr + g * gb + 64 * L + 4 * lane);
+    float s = 0.f;
+#pragma unroll 4
+    for (int k = 0; k < L; ++k) s += sc[*reinterpret_cast<const uint16_t*>(b + 64 * k)];
+    if (MODE == 1) {
+      if (s == -1.f) A.acc[lane] += s;
+    } else {
+      atomicAdd(A.acc + d, s);  // RED.E.ADD.F32
+    }
+  }
+  __syncwarp();
+  if (lane == 0) mbar_arrive(empty);
+}
+
+template <int MODE>
+__device__ __forceinline__ void reduce_record(const SegArgs& A, const uint8_t* r, const float* sc, int lane,
+                                              uint64_t* empty) {
+  const int type = *reinterpret_cast<const int32_t*>(r);
+  if (MODE == 2) {  // diagnostics: record stream only
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty);
+    if (type == 7) A.acc[lane] += 1.f;
+    return;
+  }
+  if (type == 1) reduce_long<MODE>(A, r, sc, lane, empty);
+  else reduce_short<MODE>(A, r, sc, lane, empty);
+}
+
+// Persistent CTA per SM over records [cta_c0[b], cta_c0[b+1]), unit by unit.
+// Warp kConsumers is the producer: one lane streams records into a
 // kStages-deep shared-memory ring with bulk copies (full[s]: bytes landed;
-// empty[s]: all consumer warps have taken their record). Consumer warp w
-// reduces record w of every stage. The unit's contrib segment is staged
-// with one more bulk copy when the unit is large enough to repay it.
+// empty[s]: every consumer warp has taken its record). Consumer warp w
+// reduces record w of every stage. The unit's contrib segment is staged with
+// one more bulk copy.
+// MODE (GI_SEG_MODE diagnostics): 0 full, 1 no REDs, 2 record stream only.
 template <int MODE>
 __global__ void __launch_bounds__(kSegThreads, 1) k_pr_seg(SegArgs A) {
-  extern __shared__ __align__(128) uint8_t smem[];
-  // [kStages][kStageBytes] ring | [kConsumers][kScratch] floats | Z + 4 floats of segment
+  extern __shared__ __align__(128) uint8_t smem[];  // [kStages][kStageBytes] ring | Z + 4 floats of segment
   __shared__ __align__(8) uint64_t full[kStages], empty[kStages], seg_bar;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   uint8_t* ring = smem;
-  float* scontrib = reinterpret_cast<float*>(smem + kStages * kStageBytes + kConsumers * kScratch * 4);
+  float* scontrib = reinterpret_cast<float*>(smem + kStages * kStageBytes);
   int c0 = A.cta_c0[blockIdx.x];
   const int c1 = A.cta_c0[blockIdx.x + 1];
   if (c0 >= c1) return;
@@ -269,16 +237,14 @@ __global__ void __launch_bounds__(kSegThreads, 1) k_pr_seg(SegArgs A) {
     }
     u = lo;
   }
-  // ring position: stage index and phase, advanced identically by producer and consumers
-  uint32_t it = 0;  // stages issued (producer) / consumed (consumers) so far, over all units
+  uint32_t it = 0;  // stages issued (producer) / consumed (consumers), over all units
   uint32_t seg_phase = 0;
   int staged_seg = -1;
   while (c0 < c1) {
     const int ue = min(c1, __ldg(&A.unit_c0[u + 1]));
     const int seg = u % A.S;
-    const bool stage_seg = (int64_t)(ue - c0) * kChunkE * 8 >= A.Z;
     const int nst = (ue - c0 + kConsumers - 1) / kConsumers;  // stages in this unit
-    const bool restage = stage_seg && seg != staged_seg;
+    const bool restage = seg != staged_seg;
     if (restage) {
       __syncthreads();  // every consumer is done with the previous segment
       if (tid == 0) {
@@ -306,42 +272,15 @@ __global__ void __launch_bounds__(kSegThreads, 1) k_pr_seg(SegArgs A) {
         mbar_wait(&seg_bar, seg_phase);
         if (A.timing && tid == 0) t_stage += globaltimer() - t0;
       }
-      const float* gsrc = A.cin + (int64_t)seg * A.Z;
-      float* sv = reinterpret_cast<float*>(smem + kStages * kStageBytes) + warp * kScratch;
-      // destinations of the first 64 pieces of this warp's chunks, loaded into
-      // registers one chunk ahead (their piece base cbase two chunks ahead);
-      // further lines of the next chunk's destinations prefetched into L2
-      auto cbase_of = [&](int k) { const int c = c0 + k * kConsumers + warp; return c < ue ? __ldg(&A.cbase[c]) : -1; };
-      int pd0 = 0, pd1 = 0;
-      {
-        const int cb = cbase_of(0);
-        if (cb >= 0) {
-          pd0 = __ldg(&A.pdst[cb + lane]);  // pdst is padded: always in bounds
-          pd1 = __ldg(&A.pdst[cb + 32 + lane]);
-        }
-      }
-      int cb_next = cbase_of(1);
       for (int k = 0; k < nst; ++k, ++it) {
         const uint32_t s = it % kStages, ph = (it / kStages) & 1u;
-        int npd0 = 0, npd1 = 0;
-        if (cb_next >= 0) {
-          npd0 = __ldg(&A.pdst[cb_next + lane]);
-          npd1 = __ldg(&A.pdst[cb_next + 32 + lane]);
-          if (lane >= 2 && lane < 16) prefetch_l2(A.pdst + cb_next + 32 * lane);
-        }
-        const int cb_nn = cbase_of(k + 2);
         mbar_wait(&full[s], ph);
         const int c = c0 + k * kConsumers + warp;
         const uint8_t* r = ring + s * kStageBytes + warp * kRecBytes;
-        if (c < ue) {
-          if (stage_seg) chunk_reduce<MODE, true>(A, r, scontrib, gsrc, sv, lane, A.Z, &empty[s], pd0, pd1);
-          else chunk_reduce<MODE, false>(A, r, scontrib, gsrc, sv, lane, A.Z, &empty[s], pd0, pd1);
-        } else if (lane == 0) {
+        if (c < ue) reduce_record<MODE>(A, r, scontrib, lane, &empty[s]);
+        else if (lane == 0) {
           mbar_arrive(&empty[s]);  // nothing to take from this slot
         }
-        pd0 = npd0;
-        pd1 = npd1;
-        cb_next = cb_nn;
       }
     }
     if (restage) seg_phase ^= 1u;
@@ -397,35 +336,8 @@ __global__ void __launch_bounds__(256) k_pr_acc(PrArgs A, const float* __restric
   if (threadIdx.x == 0 && bs != 0.0) atomicAdd(&A.dbuf[(A.it + 1) % 3], bs);
 }
 
+
 // ---------------------------------------------------------------- layout build
-// interleave idx / head / cbase into chunk records (kRecBytes each)
-__global__ void k_pack_records(const uint16_t* __restrict__ idx, const uint32_t* __restrict__ head,
-                               const int32_t* __restrict__ cbase, const int32_t* __restrict__ hc, int64_t C,
-                               uint8_t* __restrict__ rec) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < C * (kRecBytes / 4);
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t c = i / (kRecBytes / 4);
-    const int o = (int)(i % (kRecBytes / 4)) * 4;  // byte offset in the record
-    uint32_t w;
-    if (o < kRecHead) w = reinterpret_cast<const uint32_t*>(idx + c * kChunkE)[o / 4];
-    else if (o < kRecJ0) w = head[c * kChunkW + (o - kRecHead) / 4];
-    else if (o < kRecBase) {  // two lanes' j0: heads at chunk positions [1, 16 l)
-      const int l = (o - kRecJ0) / 2;
-      const int64_t p0 = c * kChunkE;
-      const uint32_t a = l == 0 ? 0u : (uint32_t)(hc[p0 + kLaneE * l - 1] - hc[p0]);
-      const uint32_t b = (uint32_t)(hc[p0 + kLaneE * (l + 1) - 1] - hc[p0]);
-      w = a | (b << 16);
-    }
-    else if (o == kRecBase) w = (uint32_t)cbase[c];
-    else w = 0;
-    reinterpret_cast<uint32_t*>(rec + c * kRecBytes)[o / 4] = w;
-  }
-}
-
-__global__ void k_fill_u16(uint16_t* __restrict__ p, int64_t n, uint16_t v) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) p[i] = v;
-}
-
 // row of every CSC edge (warp per row)
 template <typename OffT>
 __global__ void k_edge_rows(const OffT* __restrict__ off, int64_t n, int32_t* __restrict__ row) {
@@ -446,54 +358,172 @@ __global__ void k_unit_keys(const int32_t* __restrict__ idx, const int32_t* __re
   }
 }
 
-// unit_e[u] = first sorted position of unit u (lower bound of u in the sorted keys)
-__global__ void k_unit_starts(const uint32_t* __restrict__ skey, int64_t m, int U, int64_t* __restrict__ unit_e) {
-  for (int u = blockIdx.x * blockDim.x + threadIdx.x; u <= U; u += gridDim.x * blockDim.x) {
-    int64_t lo = 0, hi = m;
+// piece heads over the sorted edges: a new (unit, destination) run
+template <typename OffT>
+__global__ void k_sorted_heads(const uint32_t* __restrict__ skey, const OffT* __restrict__ order,
+                               const int32_t* __restrict__ row, int64_t m, int32_t* __restrict__ h) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+    h[i] = i == 0 || skey[i] != skey[i - 1] || row[(int64_t)order[i]] != row[(int64_t)order[i - 1]];
+}
+
+// per piece p (pid = inclusive head count): first sorted edge, unit, destination
+template <typename OffT>
+__global__ void k_piece_info(const int32_t* __restrict__ h, const int32_t* __restrict__ pid,
+                             const uint32_t* __restrict__ skey, const OffT* __restrict__ order,
+                             const int32_t* __restrict__ row, int64_t m, int64_t* __restrict__ pstart,
+                             int32_t* __restrict__ punit, int32_t* __restrict__ pdst) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+    if (h[i]) {
+      const int32_t p = pid[i] - 1;
+      pstart[p] = i;
+      punit[p] = (int32_t)skey[i];
+      pdst[p] = row[(int64_t)order[i]];
+    }
+}
+
+// long pieces: slots padded to whole lanes (else 0); short pieces: class key
+// u*16 + L (long: past every class), for the stable class sort
+__global__ void k_piece_class(const int64_t* __restrict__ pstart, const int32_t* __restrict__ punit, int64_t P,
+                              int64_t m, int64_t* __restrict__ asz, uint32_t* __restrict__ ckey,
+                              int32_t* __restrict__ pids, uint32_t sentinel) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < P; p += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t len = (p + 1 < P ? pstart[p + 1] : m) - pstart[p];
+    const bool lg = len >= kLongPiece;
+    asz[p] = lg ? (len + kLaneE - 1) / kLaneE * kLaneE : 0;
+    ckey[p] = lg ? sentinel : (uint32_t)punit[p] * 16u + (uint32_t)len;
+    pids[p] = (int32_t)p;
+  }
+}
+
+// lower bound of each value in a sorted array
+template <typename K>
+__global__ void k_lower_bounds(const K* __restrict__ a, int64_t n, int64_t nq, int64_t* __restrict__ out) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nq; q += (int64_t)gridDim.x * blockDim.x) {
+    int64_t lo = 0, hi = n;
     while (lo < hi) {
       const int64_t mid = (lo + hi) >> 1;
-      if (skey[mid] < (uint32_t)u) lo = mid + 1;
+      if ((int64_t)a[mid] < q) lo = mid + 1;
       else hi = mid;
     }
-    unit_e[u] = lo;
+    out[q] = lo;
   }
 }
 
-// place sorted edge i at its padded slot: index, head flag, destination
+// long record of each long piece's first slot, and the edges' index slots
 template <typename OffT>
-__global__ void k_place(const uint32_t* __restrict__ skey, const OffT* __restrict__ order, int64_t m,
-                        const int32_t* __restrict__ idx, const int32_t* __restrict__ row,
-                        const int64_t* __restrict__ unit_e, const int32_t* __restrict__ unit_c0, int Z, int S,
-                        uint16_t* __restrict__ sidx, int32_t* __restrict__ hflag, int32_t* __restrict__ srow) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t u = skey[i];
-    const int64_t e = (int64_t)order[i];
-    const int64_t pos = (int64_t)unit_c0[u] * kChunkE + (i - unit_e[u]);
-    const int32_t v = row[e];
-    const bool h = i == unit_e[u] || v != row[(int64_t)order[i - 1]];
-    sidx[pos] = (uint16_t)(idx[e] - (int64_t)(u % S) * Z);
-    hflag[pos] = h;
-    srow[pos] = v;
+__global__ void k_place_long(const int64_t* __restrict__ asz, const int64_t* __restrict__ aoff,
+                             const int32_t* __restrict__ punit, const int64_t* __restrict__ unit_p0,
+                             const int32_t* __restrict__ unit_c0, const int64_t* __restrict__ pstart,
+                             const uint32_t* __restrict__ skey, const OffT* __restrict__ order,
+                             const int32_t* __restrict__ idx, const int32_t* __restrict__ pdst, int64_t P, int64_t m,
+                             int Z, int S, uint8_t* __restrict__ rec) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < P; p += (int64_t)gridDim.x * blockDim.x) {
+    if (asz[p] == 0) continue;
+    const int u = punit[p];
+    const int64_t s0 = (int64_t)unit_c0[u] * kChunkE + (aoff[p] - aoff[unit_p0[u]]);  // slot in record units
+    const int64_t len = (p + 1 < P ? pstart[p + 1] : m) - pstart[p];
+    const int64_t base = (int64_t)(skey[pstart[p]] % (uint32_t)S) * Z;
+    for (int64_t o = 0; o < len; ++o) {
+      const int64_t s = s0 + o;
+      *reinterpret_cast<uint16_t*>(rec + (s / kChunkE) * kRecBytes + kRecHdr + 2 * (s % kChunkE)) =
+          (uint16_t)(idx[(int64_t)order[pstart[p] + o]] - base);
+    }
+    const int l0 = (int)((s0 % kChunkE) / kLaneE);
+    atomicOr(reinterpret_cast<uint32_t*>(rec + (s0 / kChunkE) * kRecBytes + kLMask), 1u << l0);
   }
 }
 
-// pack head flags into bits (one warp per 32 slots)
-__global__ void k_pack_heads(const int32_t* __restrict__ hflag, int64_t E, uint32_t* __restrict__ head) {
-  const int lane = threadIdx.x & 31;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i - lane < E; i += (int64_t)gridDim.x * blockDim.x) {
-    const unsigned b = __ballot_sync(0xffffffffu, i < E && hflag[i] != 0);
-    if (lane == 0) head[i >> 5] = b;
+// dst table of the long records (after every mask is complete)
+__global__ void k_long_dst(const int64_t* __restrict__ asz, const int64_t* __restrict__ aoff,
+                           const int32_t* __restrict__ punit, const int64_t* __restrict__ unit_p0,
+                           const int32_t* __restrict__ unit_c0, const int32_t* __restrict__ pdst, int64_t P,
+                           uint8_t* __restrict__ rec) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < P; p += (int64_t)gridDim.x * blockDim.x) {
+    if (asz[p] == 0) continue;
+    const int u = punit[p];
+    const int64_t s0 = (int64_t)unit_c0[u] * kChunkE + (aoff[p] - aoff[unit_p0[u]]), s1 = s0 + asz[p];
+    for (int64_t c = s0 / kChunkE; c * kChunkE < s1; ++c) {
+      uint8_t* r = rec + c * kRecBytes;
+      const int l = c * kChunkE >= s0 ? 0 : (int)((s0 % kChunkE) / kLaneE);
+      const uint32_t mask = *reinterpret_cast<const uint32_t*>(r + kLMask);
+      const int q = l == 0 ? 0 : __popc(mask & ((2u << l) - 1u) & ~1u);
+      *reinterpret_cast<int32_t*>(r + kLDst + 4 * q) = pdst[p];
+    }
   }
 }
 
-// hc = inclusive count of heads: pdst[hc-1] at heads, cbase[c] = hc[c*kChunkE] - 1
-__global__ void k_pieces(const int32_t* __restrict__ hflag, const int32_t* __restrict__ hc,
-                         const int32_t* __restrict__ srow, int64_t E, int32_t* __restrict__ pdst,
-                         int32_t* __restrict__ cbase) {
-  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < E; q += (int64_t)gridDim.x * blockDim.x) {
-    if (hflag[q]) pdst[hc[q] - 1] = srow[q];
-    if ((q % kChunkE) == 0) cbase[q / kChunkE] = hc[q] - 1;
+// headers of all records; short records also get padding lanes (index Z, trash row)
+__global__ void k_record_headers(const int32_t* __restrict__ rtype, const int32_t* __restrict__ rL,
+                                 const int32_t* __restrict__ rng, int64_t C, int Z, int trash,
+                                 uint8_t* __restrict__ rec) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < C * (kRecBytes / 4);
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = i / (kRecBytes / 4);
+    const int o = (int)(i % (kRecBytes / 4)) * 4;
+    uint32_t* w = reinterpret_cast<uint32_t*>(rec + c * kRecBytes + o);
+    const int type = rtype[c];
+    if (o == 0) *w = (uint32_t)type;
+    else if (o == 4) *w = (uint32_t)rL[c];
+    else if (o == 8) *w = (uint32_t)rng[c];
+    else if (o >= kRecHdr) {
+      if (type == 1) {
+        if (o < kLDst) *w = (uint32_t)Z | ((uint32_t)Z << 16);  // idx padding (overwritten by real slots)
+      } else {
+        const int L = rL[c], gb = short_group_bytes(L), g = (o - kRecHdr) / gb, go = (o - kRecHdr) % gb;
+        if (g < rng[c]) *w = go < 64 * L ? ((uint32_t)Z | ((uint32_t)Z << 16)) : (uint32_t)trash;
+      }
+    }
   }
+}
+
+// short pieces in class order: piece at class rank q -> record, group, lane
+template <typename OffT>
+__global__ void k_place_short(const uint32_t* __restrict__ sckey, const int32_t* __restrict__ spid, int64_t NS,
+                              const int64_t* __restrict__ cstart, const int32_t* __restrict__ crec0,
+                              const int64_t* __restrict__ pstart, const uint32_t* __restrict__ skey,
+                              const OffT* __restrict__ order, const int32_t* __restrict__ idx,
+                              const int32_t* __restrict__ pdst, int Z, int S, uint8_t* __restrict__ rec) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < NS; j += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t k = sckey[j];
+    const int L = (int)(k % 16u);
+    const int64_t q = j - cstart[k];
+    const int64_t grp = q / 32;
+    const int lane = (int)(q % 32), R = short_groups(L);
+    uint8_t* b = rec + (int64_t)(crec0[k] + grp / R) * kRecBytes + kRecHdr + (grp % R) * short_group_bytes(L);
+    const int32_t p = spid[j];
+    const int64_t base = (int64_t)(skey[pstart[p]] % (uint32_t)S) * Z;
+    for (int e = 0; e < L; ++e)
+      *reinterpret_cast<uint16_t*>(b + 64 * e + 2 * lane) = (uint16_t)(idx[(int64_t)order[pstart[p] + e]] - base);
+    *reinterpret_cast<int32_t*>(b + 64 * L + 4 * lane) = pdst[p];
+  }
+}
+
+template <typename T>
+static gi_status exclusive_scan(const T* in, T* out, int64_t n, DevBuf& tmp, cudaStream_t st) {
+  size_t tb = 0;
+  GI_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, in, out, n, st));
+  if (tmp.bytes < tb) GI_TRY(tmp.alloc(tb));
+  GI_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb, in, out, n, st));
+  return GI_OK;
+}
+
+template <typename T>
+static gi_status inclusive_scan(const T* in, T* out, int64_t n, DevBuf& tmp, cudaStream_t st) {
+  size_t tb = 0;
+  GI_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tb, in, out, n, st));
+  if (tmp.bytes < tb) GI_TRY(tmp.alloc(tb));
+  GI_CUDA(cub::DeviceScan::InclusiveSum(tmp.p, tb, in, out, n, st));
+  return GI_OK;
+}
+
+template <typename K, typename V>
+static gi_status sort_pairs(const K* ki, K* ko, const V* vi, V* vo, int64_t n, int bits, DevBuf& tmp,
+                            cudaStream_t st) {
+  size_t tb = 0;  // stable LSD radix sort
+  GI_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, ki, ko, vi, vo, n, 0, bits, st));
+  if (tmp.bytes < tb) GI_TRY(tmp.alloc(tb));
+  GI_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, ki, ko, vi, vo, n, 0, bits, st));
+  return GI_OK;
 }
 
 }  // namespace
@@ -506,11 +536,12 @@ static gi_status seg_build_t(gi_graph g, int Z, int64_t DB) {
   const int64_t n = g->nr, m = g->ml;  // CSC rows (owned destinations) and local edges
   const OffT* off = g->csc_off.as<OffT>();
   const int32_t* idx = g->csc_idx.as<int32_t>();
-  const int S = (int)ceil_div(g->n, Z);         // segments over all sources
-  const int B = (int)ceil_div(n, DB);           // destination blocks
-  if ((int64_t)B * S >= INT32_MAX / 2) return fail(GI_ERR_UNSUPPORTED, "segmented pull: too many units");
+  const int S = (int)ceil_div(g->n, Z);  // segments over all sources
+  const int B = (int)ceil_div(n, DB);    // destination blocks
+  if ((int64_t)B * S * 16 >= INT32_MAX / 2) return fail(GI_ERR_UNSUPPORTED, "segmented pull: too many units");
+  if (m >= INT32_MAX) return fail(GI_ERR_UNSUPPORTED, "segmented pull: more than 2^31 local edges");
   const int U = B * S;
-  DevBuf row, key, skey, eid, order, unit_e, tmp;
+  DevBuf row, key, skey, eid, order, tmp;
   GI_TRY(row.alloc(m * sizeof(int32_t)));
   k_edge_rows<OffT><<<grid_for(n * 32, 256, sms, 16), 256, 0, st>>>(off, n, row.as<int32_t>());
   GI_TRY(key.alloc(m * sizeof(uint32_t)));
@@ -521,79 +552,138 @@ static gi_status seg_build_t(gi_graph g, int Z, int64_t DB) {
                                                           eid.as<OffT>());
   int kbits = 1;
   while ((1ll << kbits) < U) ++kbits;
-  size_t tb = 0;  // stable LSD radix sort: (v, w) order is kept inside each unit
-  GI_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, key.as<uint32_t>(), skey.as<uint32_t>(), eid.as<OffT>(),
-                                          order.as<OffT>(), m, 0, kbits, st));
-  GI_TRY(tmp.alloc(tb));
-  GI_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, key.as<uint32_t>(), skey.as<uint32_t>(), eid.as<OffT>(),
-                                          order.as<OffT>(), m, 0, kbits, st));
+  // stable: (v, w) order is kept inside each unit
+  GI_TRY(sort_pairs(key.as<uint32_t>(), skey.as<uint32_t>(), eid.as<OffT>(), order.as<OffT>(), m, kbits, tmp, st));
   key.reset();
   eid.reset();
-  GI_TRY(unit_e.alloc((U + 1) * sizeof(int64_t)));
-  k_unit_starts<<<grid_for(U + 1, 256, sms), 256, 0, st>>>(skey.as<uint32_t>(), m, U, unit_e.as<int64_t>());
-  std::vector<int64_t> h_ue(U + 1);
-  GI_CUDA(cudaMemcpyAsync(h_ue.data(), unit_e.p, (U + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  // ---- pieces: (unit, destination) runs of the sorted edges
+  DevBuf h, pid, pstart, punit, pdst, asz, aoff, ckey, pids, sckey, spid, unit_p0;
+  GI_TRY(h.alloc(m * sizeof(int32_t)));
+  GI_TRY(pid.alloc(m * sizeof(int32_t)));
+  k_sorted_heads<OffT><<<grid_for(m, 256, sms), 256, 0, st>>>(skey.as<uint32_t>(), order.as<OffT>(), row.as<int32_t>(),
+                                                              m, h.as<int32_t>());
+  GI_TRY(inclusive_scan(h.as<int32_t>(), pid.as<int32_t>(), m, tmp, st));
+  int32_t Pi = 0;
+  GI_CUDA(cudaMemcpyAsync(&Pi, pid.as<int32_t>() + m - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
   GI_CUDA(cudaStreamSynchronize(st));
-  std::vector<int32_t> h_uc(U + 1);
-  int64_t C = 0;
+  const int64_t P = Pi;
+  GI_TRY(pstart.alloc((P + 1) * sizeof(int64_t)));
+  GI_TRY(punit.alloc((P + 1) * sizeof(int32_t)));
+  GI_TRY(pdst.alloc((P + 1) * sizeof(int32_t)));
+  k_piece_info<OffT><<<grid_for(m, 256, sms), 256, 0, st>>>(h.as<int32_t>(), pid.as<int32_t>(), skey.as<uint32_t>(),
+                                                            order.as<OffT>(), row.as<int32_t>(), m,
+                                                            pstart.as<int64_t>(), punit.as<int32_t>(),
+                                                            pdst.as<int32_t>());
+  h.reset();
+  pid.reset();
+  row.reset();
+  // ---- classes: long pieces (lane-aligned records) and short pieces by (unit, L)
+  const uint32_t sentinel = (uint32_t)U * 16u;
+  GI_TRY(asz.alloc((P + 1) * sizeof(int64_t)));
+  GI_TRY(aoff.alloc((P + 1) * sizeof(int64_t)));
+  GI_TRY(ckey.alloc((P + 1) * sizeof(uint32_t)));
+  GI_TRY(pids.alloc((P + 1) * sizeof(int32_t)));
+  GI_TRY(sckey.alloc((P + 1) * sizeof(uint32_t)));
+  GI_TRY(spid.alloc((P + 1) * sizeof(int32_t)));
+  k_piece_class<<<grid_for(P, 256, sms), 256, 0, st>>>(pstart.as<int64_t>(), punit.as<int32_t>(), P, m,
+                                                       asz.as<int64_t>(), ckey.as<uint32_t>(), pids.as<int32_t>(),
+                                                       sentinel);
+  GI_CUDA(cudaMemsetAsync(asz.as<int64_t>() + P, 0, sizeof(int64_t), st));
+  GI_TRY(exclusive_scan(asz.as<int64_t>(), aoff.as<int64_t>(), P + 1, tmp, st));
+  int cbits = 1;
+  while ((1ll << cbits) <= (int64_t)sentinel) ++cbits;
+  GI_TRY(sort_pairs(ckey.as<uint32_t>(), sckey.as<uint32_t>(), pids.as<int32_t>(), spid.as<int32_t>(), P, cbits, tmp,
+                    st));
+  ckey.reset();
+  pids.reset();
+  const int64_t NC = (int64_t)U * 16;  // short classes (L = 0 unused)
+  DevBuf cstart;
+  GI_TRY(cstart.alloc((NC + 1) * sizeof(int64_t)));
+  GI_TRY(unit_p0.alloc((U + 1) * sizeof(int64_t)));
+  k_lower_bounds<uint32_t><<<grid_for(NC + 1, 256, sms), 256, 0, st>>>(sckey.as<uint32_t>(), P, NC + 1,
+                                                                      cstart.as<int64_t>());
+  k_lower_bounds<int32_t><<<grid_for(U + 1, 256, sms), 256, 0, st>>>(punit.as<int32_t>(), P, U + 1,
+                                                                    unit_p0.as<int64_t>());
+  std::vector<int64_t> h_cs(NC + 1), h_up0(U + 1), h_ao(U + 1);
+  GI_CUDA(cudaMemcpyAsync(h_cs.data(), cstart.p, (NC + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  GI_CUDA(cudaMemcpyAsync(h_up0.data(), unit_p0.p, (U + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  GI_CUDA(cudaStreamSynchronize(st));
+  for (int u = 0; u <= U; ++u)
+    GI_CUDA(cudaMemcpyAsync(&h_ao[u], aoff.as<int64_t>() + h_up0[u], sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  GI_CUDA(cudaStreamSynchronize(st));
+  // ---- record layout: per unit, long records then short records by L
+  std::vector<int32_t> h_uc(U + 1), h_crec0(NC, 0), h_type, h_L, h_ng;
+  std::vector<int64_t> h_cost;  // per record, for the CTA balance
+  int64_t C = 0, CL = 0, NS = 0;
   for (int u = 0; u < U; ++u) {
     h_uc[u] = (int32_t)C;
-    C += ceil_div(h_ue[u + 1] - h_ue[u], kChunkE);
-    if (C >= INT32_MAX) return fail(GI_ERR_UNSUPPORTED, "segmented pull: more than 2^31 chunks");
+    const int64_t slots = h_ao[u + 1] - h_ao[u];
+    const int64_t nl = ceil_div(slots, kChunkE);
+    for (int64_t r = 0; r < nl; ++r) {
+      h_type.push_back(1);
+      h_L.push_back(0);
+      h_ng.push_back(0);
+      h_cost.push_back(kChunkE + 2 * kPieceCost);
+    }
+    C += nl;
+    CL += nl;
+    for (int L = 1; L < 16; ++L) {
+      const int64_t k = (int64_t)u * 16 + L;
+      const int64_t cnt = h_cs[k + 1] - h_cs[k];
+      NS += cnt;
+      h_crec0[k] = (int32_t)C;
+      const int64_t groups = ceil_div(cnt, 32), R = short_groups(L);
+      for (int64_t gq = 0; gq < groups; gq += R) {
+        const int ng = (int)std::min<int64_t>(R, groups - gq);
+        h_type.push_back(2);
+        h_L.push_back(L);
+        h_ng.push_back(ng);
+        h_cost.push_back((int64_t)ng * 32 * (L + kPieceCost));
+        ++C;
+      }
+    }
+    if (C >= INT32_MAX) return fail(GI_ERR_UNSUPPORTED, "segmented pull: more than 2^31 records");
   }
   h_uc[U] = (int32_t)C;
-  const int64_t E = C * kChunkE;
-  DevBuf unit_c0, hflag, hc, srow;
+  DevBuf unit_c0, crec0, rtype, rL, rng;
   GI_TRY(unit_c0.alloc((U + 1) * sizeof(int32_t)));
+  GI_TRY(crec0.alloc((NC + 1) * sizeof(int32_t)));
+  GI_TRY(rtype.alloc((C + 1) * sizeof(int32_t)));
+  GI_TRY(rL.alloc((C + 1) * sizeof(int32_t)));
+  GI_TRY(rng.alloc((C + 1) * sizeof(int32_t)));
   GI_CUDA(cudaMemcpyAsync(unit_c0.p, h_uc.data(), (U + 1) * sizeof(int32_t), cudaMemcpyHostToDevice, st));
-  GI_TRY(g->seg_idx.alloc(E * sizeof(uint16_t) + 16));
-  GI_TRY(hflag.alloc(E * sizeof(int32_t)));
-  GI_TRY(srow.alloc(E * sizeof(int32_t)));
-  // padding: index Z (reads 0), no head (joins the unit's last piece)
-  k_fill_u16<<<grid_for(E, 256, sms), 256, 0, st>>>(g->seg_idx.as<uint16_t>(), E, (uint16_t)Z);
-  GI_CUDA(cudaMemsetAsync(hflag.p, 0, E * sizeof(int32_t), st));
-  GI_CUDA(cudaMemsetAsync(srow.p, 0, E * sizeof(int32_t), st));
-  k_place<OffT><<<grid_for(m, 256, sms), 256, 0, st>>>(skey.as<uint32_t>(), order.as<OffT>(), m, idx,
-                                                       row.as<int32_t>(), unit_e.as<int64_t>(),
-                                                       unit_c0.as<int32_t>(), Z, S, g->seg_idx.as<uint16_t>(),
-                                                       hflag.as<int32_t>(), srow.as<int32_t>());
-  skey.reset();
-  order.reset();
-  row.reset();
-  GI_TRY(g->seg_head.alloc((E / 32) * sizeof(uint32_t) + 16));
-  k_pack_heads<<<grid_for(E, 256, sms), 256, 0, st>>>(hflag.as<int32_t>(), E, g->seg_head.as<uint32_t>());
-  GI_TRY(hc.alloc(E * sizeof(int32_t)));
-  tb = 0;
-  GI_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tb, hflag.as<int32_t>(), hc.as<int32_t>(), E, st));
-  GI_TRY(tmp.alloc(tb));
-  GI_CUDA(cub::DeviceScan::InclusiveSum(tmp.p, tb, hflag.as<int32_t>(), hc.as<int32_t>(), E, st));
-  int32_t P = 0;
-  GI_CUDA(cudaMemcpyAsync(&P, hc.as<int32_t>() + E - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-  GI_CUDA(cudaStreamSynchronize(st));
-  GI_TRY(g->seg_pdst.alloc(((int64_t)P + 32 * 32) * sizeof(int32_t)));
-  GI_CUDA(cudaMemsetAsync(g->seg_pdst.p, 0, ((int64_t)P + 32 * 32) * sizeof(int32_t), st));
-  GI_TRY(g->seg_cbase.alloc((C + 1) * sizeof(int32_t)));
-  k_pieces<<<grid_for(E, 256, sms), 256, 0, st>>>(hflag.as<int32_t>(), hc.as<int32_t>(), srow.as<int32_t>(), E,
-                                                  g->seg_pdst.as<int32_t>(), g->seg_cbase.as<int32_t>());
-  GI_CUDA(cudaMemcpyAsync(g->seg_cbase.as<int32_t>() + C, &P, sizeof(int32_t), cudaMemcpyHostToDevice, st));
+  GI_CUDA(cudaMemcpyAsync(crec0.p, h_crec0.data(), NC * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+  if (C > 0) {
+    GI_CUDA(cudaMemcpyAsync(rtype.p, h_type.data(), C * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+    GI_CUDA(cudaMemcpyAsync(rL.p, h_L.data(), C * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+    GI_CUDA(cudaMemcpyAsync(rng.p, h_ng.data(), C * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+  }
   GI_TRY(g->seg_rec.alloc(C * kRecBytes + 16));
-  k_pack_records<<<grid_for(C * (kRecBytes / 4), 256, sms), 256, 0, st>>>(
-      g->seg_idx.as<uint16_t>(), g->seg_head.as<uint32_t>(), g->seg_cbase.as<int32_t>(), hc.as<int32_t>(), C,
+  GI_CUDA(cudaMemsetAsync(g->seg_rec.p, 0, C * kRecBytes + 16, st));
+  const int trash = (int)n;  // accumulator row past the owned rows
+  k_record_headers<<<grid_for(C * (kRecBytes / 4), 256, sms), 256, 0, st>>>(
+      rtype.as<int32_t>(), rL.as<int32_t>(), rng.as<int32_t>(), C, Z, trash, g->seg_rec.as<uint8_t>());
+  k_place_long<OffT><<<grid_for(P, 256, sms), 256, 0, st>>>(
+      asz.as<int64_t>(), aoff.as<int64_t>(), punit.as<int32_t>(), unit_p0.as<int64_t>(), unit_c0.as<int32_t>(),
+      pstart.as<int64_t>(), skey.as<uint32_t>(), order.as<OffT>(), idx, pdst.as<int32_t>(), P, m, Z, S,
       g->seg_rec.as<uint8_t>());
-  // cost-balanced CTA ranges: a chunk costs its slots plus kPieceCost per
-  // piece ending in it; every unit start adds the cost of staging a segment
-  std::vector<int32_t> h_cb(C + 1);
-  GI_CUDA(cudaMemcpyAsync(h_cb.data(), g->seg_cbase.p, (C + 1) * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-  GI_CUDA(cudaStreamSynchronize(st));
+  k_long_dst<<<grid_for(P, 256, sms), 256, 0, st>>>(asz.as<int64_t>(), aoff.as<int64_t>(), punit.as<int32_t>(),
+                                                    unit_p0.as<int64_t>(), unit_c0.as<int32_t>(), pdst.as<int32_t>(),
+                                                    P, g->seg_rec.as<uint8_t>());
+  if (NS > 0)
+    k_place_short<OffT><<<grid_for(NS, 256, sms), 256, 0, st>>>(
+        sckey.as<uint32_t>(), spid.as<int32_t>(), NS, cstart.as<int64_t>(), crec0.as<int32_t>(), pstart.as<int64_t>(),
+        skey.as<uint32_t>(), order.as<OffT>(), idx, pdst.as<int32_t>(), Z, S, g->seg_rec.as<uint8_t>());
+  // ---- cost-balanced CTA ranges (every unit start adds kUnitCost)
   const int ctas = sms;
   std::vector<int32_t> h_cta(ctas + 1, (int32_t)C);
   {
     std::vector<int64_t> pre(C + 1, 0);
     int u = 0;
     for (int64_t c = 0; c < C; ++c) {
-      int64_t cost = kChunkCost + (int64_t)kPieceCost * (h_cb[c + 1] - h_cb[c]);
+      int64_t cost = h_cost[c];
       while (u < U && h_uc[u] < c) ++u;
-      if (u < U && h_uc[u] == c) cost += kStageCost;
+      if (u < U && h_uc[u] == c) cost += kUnitCost;
       pre[c + 1] = pre[c] + cost;
     }
     int64_t c = 0;
@@ -609,18 +699,17 @@ static gi_status seg_build_t(gi_graph g, int Z, int64_t DB) {
   GI_CUDA(cudaMemcpyAsync(g->seg_unit_c0.p, h_uc.data(), (U + 1) * sizeof(int32_t), cudaMemcpyHostToDevice, st));
   GI_TRY(g->seg_cta.alloc((ctas + 1) * sizeof(int32_t)));
   GI_CUDA(cudaMemcpyAsync(g->seg_cta.p, h_cta.data(), (ctas + 1) * sizeof(int32_t), cudaMemcpyHostToDevice, st));
-  g->seg_acc_stride = (n + 64) & ~31ll;
+  g->seg_acc_stride = (n + 64) & ~31ll;  // >= n + 1: row n is the trash row of padding lanes
   GI_TRY(g->seg_acc.alloc(2 * g->seg_acc_stride * sizeof(float)));
   GI_CUDA(cudaMemsetAsync(g->seg_acc.p, 0, 2 * g->seg_acc_stride * sizeof(float), st));
   g->seg_acc_cur = 0;
   GI_CUDA(cudaGetLastError());
   GI_CUDA(cudaStreamSynchronize(st));
-  g->seg_idx.reset();
-  g->seg_head.reset();
   if (const char* dbg = getenv("GI_DEBUG_SEG_LAYOUT")) {
     if (FILE* f = fopen(dbg, "a")) {
-      fprintf(f, "n=%lld m=%lld Z=%d S=%d B=%d U=%d C=%lld E=%lld P=%d pad=%.3f\n", (long long)n, (long long)m, Z, S,
-              B, U, (long long)C, (long long)E, P, m ? (double)E / (double)m - 1.0 : 0.0);
+      fprintf(f, "n=%lld m=%lld Z=%d S=%d B=%d U=%d records=%lld (long %lld, short %lld) bytes=%lld P=%lld "
+              "(short %lld)\n", (long long)n, (long long)m, Z, S, B, U, (long long)C, (long long)CL,
+              (long long)(C - CL), (long long)(C * kRecBytes), (long long)P, (long long)NS);
       fclose(f);
     }
   }
@@ -634,9 +723,7 @@ static gi_status seg_build_t(gi_graph g, int Z, int64_t DB) {
   return GI_OK;
 }
 
-static size_t seg_dyn_smem(int Z) {
-  return (size_t)kStages * kStageBytes + (size_t)kConsumers * kScratch * sizeof(float) + ((size_t)Z + 4) * sizeof(float);
-}
+static size_t seg_dyn_smem(int Z) { return (size_t)kStages * kStageBytes + ((size_t)Z + 4) * sizeof(float); }
 
 gi_status seg_build(gi_graph g, int segment_size, int64_t block_rows) {
   if (segment_size < 0 || block_rows < 0) return fail(GI_ERR_INVALID_ARGUMENT, "segment_size / dst_block < 0");
@@ -661,8 +748,6 @@ gi_status seg_edge_pass(gi_graph g, const float* cin) {
   cudaStream_t st = g->ctx->stream;
   SegArgs S;
   S.rec = g->seg_rec.as<uint8_t>();
-  S.cbase = g->seg_cbase.as<int32_t>();
-  S.pdst = g->seg_pdst.as<int32_t>();
   S.unit_c0 = g->seg_unit_c0.as<int32_t>();
   S.cta_c0 = g->seg_cta.as<int32_t>();
   S.cin = cin;
@@ -672,14 +757,13 @@ gi_status seg_edge_pass(gi_graph g, const float* cin) {
   S.S = g->seg_S;
   S.U = g->seg_U;
   static const int mode = getenv("GI_SEG_MODE") ? atoi(getenv("GI_SEG_MODE")) : 0;
-  void (*kern)(SegArgs) = mode == 1 ? k_pr_seg<1> : mode == 2 ? k_pr_seg<2> : mode == 3 ? k_pr_seg<3> : k_pr_seg<0>;
+  void (*kern)(SegArgs) = mode == 1 ? k_pr_seg<1> : mode == 2 ? k_pr_seg<2> : k_pr_seg<0>;
   const size_t dyn = seg_dyn_smem(g->seg_Z);
   static size_t attr_set = 0;  // largest dynamic smem size configured so far
   if (attr_set < dyn) {
     GI_CUDA(cudaFuncSetAttribute(k_pr_seg<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
     GI_CUDA(cudaFuncSetAttribute(k_pr_seg<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
     GI_CUDA(cudaFuncSetAttribute(k_pr_seg<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
-    GI_CUDA(cudaFuncSetAttribute(k_pr_seg<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
     attr_set = dyn;
   }
   static const char* dbg = getenv("GI_DEBUG_SEG_TIMING");  // diagnostics: file to append per-CTA timings to
@@ -698,14 +782,10 @@ gi_status seg_edge_pass(gi_graph g, const float* cin) {
     GI_CUDA(cudaMemcpyAsync(ht.data(), tbuf.p, ht.size() * 8, cudaMemcpyDeviceToHost, st));
     GI_CUDA(cudaMemcpyAsync(hc.data(), g->seg_cta.p, hc.size() * 4, cudaMemcpyDeviceToHost, st));
     GI_CUDA(cudaStreamSynchronize(st));
-    std::vector<int32_t> pc(g->seg_ctas + 1);  // piece index at each CTA boundary
-    for (int c = 0; c <= g->seg_ctas; ++c)
-      GI_CUDA(cudaMemcpyAsync(&pc[c], g->seg_cbase.as<int32_t>() + hc[c], 4, cudaMemcpyDeviceToHost, st));
-    GI_CUDA(cudaStreamSynchronize(st));
     if (FILE* f = fopen(dbg, "a")) {
       for (int c = 0; c < g->seg_ctas; ++c)
-        fprintf(f, "%d,%d,%d,%llu,%llu,%llu,%llu,%d\n", c, hc[c], hc[c + 1], ht[4 * c], ht[4 * c + 1], ht[4 * c + 2],
-                ht[4 * c + 3], pc[c + 1] - pc[c]);
+        fprintf(f, "%d,%d,%d,%llu,%llu,%llu,%llu\n", c, hc[c], hc[c + 1], ht[4 * c], ht[4 * c + 1], ht[4 * c + 2],
+                ht[4 * c + 3]);
       fclose(f);
     }
   }
