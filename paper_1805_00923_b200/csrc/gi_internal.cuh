@@ -121,6 +121,9 @@ struct gi_graph_s {
   gi::DevBuf seg_rec;      // records: long (lane-aligned) and short (lane-per-piece), pr_segmented.cu
   gi::DevBuf seg_unit_c0;  // int32[U+1]: first record of each (block, segment) unit
   gi::DevBuf seg_cta;      // int32[CTAs+1]: cost-balanced record range of each CTA
+  std::vector<int32_t> seg_h_cta;  // host copy of seg_cta
+  gi::DevBuf seg_time;     // uint64[4*CTAs]: per-CTA timings of the last calibrated launch
+  int seg_calib = 0;       // edge passes left that re-balance the CTA ranges from measured timings
   gi::DevBuf seg_acc;      // float[2][seg_acc_stride]: per-row sums (ping-pong), L2-resident
   int64_t seg_acc_stride = 0;
   int seg_acc_cur = 0;     // buffer the next edge pass reduces into (all zero)

@@ -69,10 +69,12 @@ __host__ __device__ constexpr int short_group_bytes(int L) { return 64 * L + 128
 __host__ __device__ constexpr int short_groups(int L) { return kRecPayload / short_group_bytes(L); }
 constexpr int kStages = 4;                          // ring depth (stages in flight per CTA)
 constexpr int kStageBytes = kConsumers * kRecBytes;
-// CTA balance (costs in gather slots; fitted from per-CTA timings, tools/seg_timing.py)
-constexpr int kPieceCost = 1;
+// CTA balance: an initial cost model (in gather slots), then refined from
+// measured per-CTA times over the first kCalibPasses edge passes (seg_rebalance)
+constexpr int kPieceCost = 4;
 constexpr int64_t kUnitCost = 40 * kChunkE;         // a unit start: segment staging + pipeline refill
 constexpr int64_t kDefaultBlockRows = 8 << 20;      // 32 MB accumulator per destination block
+constexpr int kCalibPasses = 3;
 
 struct SegArgs {
   const uint8_t* __restrict__ rec;     // kRecBytes per record
@@ -82,7 +84,7 @@ struct SegArgs {
   float* __restrict__ acc;             // per local row (+ trash row at nr)
   int64_t n;
   int Z, S, U;
-  unsigned long long* timing;  // diagnostics (GI_DEBUG_SEG_TIMING): per CTA [start, end, staging ns, units]
+  unsigned long long* timing;  // per CTA [start, end, staging ns, units] (balance calibration, diagnostics)
 };
 
 __device__ __forceinline__ unsigned long long globaltimer() {
@@ -699,6 +701,9 @@ static gi_status seg_build_t(gi_graph g, int Z, int64_t DB) {
   GI_CUDA(cudaMemcpyAsync(g->seg_unit_c0.p, h_uc.data(), (U + 1) * sizeof(int32_t), cudaMemcpyHostToDevice, st));
   GI_TRY(g->seg_cta.alloc((ctas + 1) * sizeof(int32_t)));
   GI_CUDA(cudaMemcpyAsync(g->seg_cta.p, h_cta.data(), (ctas + 1) * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+  g->seg_h_cta = h_cta;
+  GI_TRY(g->seg_time.alloc(4 * ctas * sizeof(unsigned long long)));
+  g->seg_calib = getenv("GI_SEG_NO_CALIB") ? 0 : kCalibPasses;
   g->seg_acc_stride = (n + 64) & ~31ll;  // >= n + 1: row n is the trash row of padding lanes
   GI_TRY(g->seg_acc.alloc(2 * g->seg_acc_stride * sizeof(float)));
   GI_CUDA(cudaMemsetAsync(g->seg_acc.p, 0, 2 * g->seg_acc_stride * sizeof(float), st));
@@ -720,6 +725,37 @@ static gi_status seg_build_t(gi_graph g, int Z, int64_t DB) {
   g->seg_P = P;
   g->seg_C = C;
   g->seg_ctas = ctas;
+  return GI_OK;
+}
+
+// Re-balance the CTA record ranges from one launch's measured per-CTA busy
+// times: every CTA's time is spread uniformly over its records, and the new
+// boundaries cut the resulting cumulative cost into equal shares.
+static gi_status seg_rebalance(gi_graph g, const std::vector<unsigned long long>& ht) {
+  const int ctas = g->seg_ctas;
+  std::vector<int32_t>& hc = g->seg_h_cta;
+  std::vector<double> T(ctas, 0.0);
+  double total = 0.0;
+  for (int k = 0; k < ctas; ++k) {
+    if (hc[k + 1] > hc[k] && ht[4 * k + 1] > ht[4 * k]) T[k] = (double)(ht[4 * k + 1] - ht[4 * k]);
+    total += T[k];
+  }
+  if (total <= 0.0) return GI_OK;
+  std::vector<int32_t> nc(ctas + 1);
+  nc[0] = 0;
+  nc[ctas] = hc[ctas];
+  int k = 0;
+  double before = 0.0;  // cost of CTA ranges < k
+  for (int j = 1; j < ctas; ++j) {
+    const double target = total * j / ctas;
+    while (k < ctas - 1 && before + T[k] < target) before += T[k++];
+    const int32_t len = hc[k + 1] - hc[k];
+    const double frac = T[k] > 0.0 ? (target - before) / T[k] : 0.0;
+    nc[j] = std::max(nc[j - 1], std::min(hc[k + 1], hc[k] + (int32_t)(frac * len + 0.5)));
+  }
+  hc = nc;
+  GI_CUDA(cudaMemcpyAsync(g->seg_cta.p, hc.data(), (ctas + 1) * sizeof(int32_t), cudaMemcpyHostToDevice,
+                          g->ctx->stream));
   return GI_OK;
 }
 
@@ -767,27 +803,31 @@ gi_status seg_edge_pass(gi_graph g, const float* cin) {
     attr_set = dyn;
   }
   static const char* dbg = getenv("GI_DEBUG_SEG_TIMING");  // diagnostics: file to append per-CTA timings to
-  DevBuf tbuf;
+  const bool timed = dbg || g->seg_calib > 0;
+  const int ctas = g->seg_ctas;
   S.timing = nullptr;
-  if (dbg) {
-    GI_TRY(tbuf.alloc(4 * g->seg_ctas * sizeof(unsigned long long)));
-    GI_CUDA(cudaMemsetAsync(tbuf.p, 0, 4 * g->seg_ctas * sizeof(unsigned long long), st));
-    S.timing = tbuf.as<unsigned long long>();
+  if (timed) {
+    GI_CUDA(cudaMemsetAsync(g->seg_time.p, 0, 4 * ctas * sizeof(unsigned long long), st));
+    S.timing = g->seg_time.as<unsigned long long>();
   }
-  kern<<<g->seg_ctas, kSegThreads, dyn, st>>>(S);
+  kern<<<ctas, kSegThreads, dyn, st>>>(S);
   GI_CUDA(cudaGetLastError());
+  if (!timed) return GI_OK;
+  std::vector<unsigned long long> ht(4 * ctas);
+  GI_CUDA(cudaMemcpyAsync(ht.data(), g->seg_time.p, ht.size() * 8, cudaMemcpyDeviceToHost, st));
+  GI_CUDA(cudaStreamSynchronize(st));
+  const std::vector<int32_t>& hc = g->seg_h_cta;
   if (dbg) {
-    std::vector<unsigned long long> ht(4 * g->seg_ctas);
-    std::vector<int32_t> hc(g->seg_ctas + 1);
-    GI_CUDA(cudaMemcpyAsync(ht.data(), tbuf.p, ht.size() * 8, cudaMemcpyDeviceToHost, st));
-    GI_CUDA(cudaMemcpyAsync(hc.data(), g->seg_cta.p, hc.size() * 4, cudaMemcpyDeviceToHost, st));
-    GI_CUDA(cudaStreamSynchronize(st));
     if (FILE* f = fopen(dbg, "a")) {
-      for (int c = 0; c < g->seg_ctas; ++c)
+      for (int c = 0; c < ctas; ++c)
         fprintf(f, "%d,%d,%d,%llu,%llu,%llu,%llu\n", c, hc[c], hc[c + 1], ht[4 * c], ht[4 * c + 1], ht[4 * c + 2],
                 ht[4 * c + 3]);
       fclose(f);
     }
+  }
+  if (g->seg_calib > 0) {
+    --g->seg_calib;
+    GI_TRY(seg_rebalance(g, ht));
   }
   return GI_OK;
 }

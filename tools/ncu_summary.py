@@ -6,6 +6,7 @@
 import csv
 import io
 import json
+import os
 import subprocess
 import sys
 
@@ -66,8 +67,8 @@ def main():
         agg = {}
         for d in launches:
             k = d["kernel"]
-            for key, name in (("k_pr_seg", "pr_seg"), ("k_pr_merge", "pr_merge"), ("k_pr_pull", "pr_direct"),
-                              ("k_bfs_pull_smem", "bfs_pull"), ("k_bfs_push_stamp", "bfs_push_stamp")):
+            for key, name in (("k_pr_seg", "pr_seg"), ("k_pr_acc", "pr_acc"), ("k_pr_pull", "pr_direct"),
+                              ("k_bfs_fused", "bfs_fused")):
                 if key in k:
                     a = agg.setdefault(name, {"launches": 0, "dram_bytes": 0.0, "duration_ns": 0.0})
                     a["launches"] += 1
@@ -76,12 +77,17 @@ def main():
         for a in agg.values():
             a["dram_bytes_per_launch"] = a["dram_bytes"] / a["launches"]
             a["duration_us_per_launch"] = a["duration_ns"] / a["launches"] / 1e3
-        if "pr_seg" in agg and "pr_merge" in agg:  # one pull iteration = segment pass + merge pass
+        if "pr_seg" in agg and "pr_acc" in agg:  # one pull iteration = segmented edge pass + vertex pass
             agg["pr_pull"] = {"dram_bytes_per_launch": agg["pr_seg"]["dram_bytes_per_launch"] +
-                              agg["pr_merge"]["dram_bytes_per_launch"],
-                              "note": "per PageRank iteration: k_pr_seg + k_pr_merge (k_fold_carries negligible)"}
-        agg["source"] = rep
-        json.dump(agg, open(js, "w"), indent=1)
+                              agg["pr_acc"]["dram_bytes_per_launch"],
+                              "note": "per PageRank iteration: k_pr_seg + k_pr_acc"}
+        old = json.load(open(js)) if os.path.exists(js) else {}
+        old.update(agg)  # merge with summaries of other captures (PR and BFS are captured separately)
+        old.setdefault("sources", [])
+        if rep not in old["sources"]:
+            old["sources"].append(rep)
+        old.pop("source", None)
+        json.dump(old, open(js, "w"), indent=1)
 
 
 if __name__ == "__main__":

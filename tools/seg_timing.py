@@ -5,7 +5,7 @@ import numpy as np
 
 rows = [list(map(int, l.split(","))) for l in open(sys.argv[1]) if l.strip()]
 ctas = max(r[0] for r in rows) + 1
-last = np.array(rows[-ctas:], dtype=np.float64)
+last = np.array(rows[-ctas:], dtype=np.float64)[:, :7]
 t0 = last[:, 3].min()
 start, end, stage, units = last[:, 3] - t0, last[:, 4] - t0, last[:, 5], last[:, 6]
 pieces = last[:, 7] if last.shape[1] > 7 else np.zeros(len(last))
