@@ -6,7 +6,7 @@
 One step = the whole hot path over the workload
 BASELINE.json's metric is quoted on at N=1 (configs[1] = RMAT s22 ef16,
 "config 2"): fixed-iteration PageRank (20 iterations, d = 0.85, pull) plus
-BFS from 64 seeded random sources (direction-optimising). The graph build
+BFS from 64 seeded random sources (direction-optimising, gi_bfs_multi). The graph build
 (a1) runs once before timing and is reported separately (`build_ms`), as the
 paper's Table 4 times the algorithms, not loading.
 
@@ -15,8 +15,11 @@ value  = (20 m + sum over sources of edges traversed) / device time, all ranks
 e2e    = the same edges over the time of the public C-ABI calls with HOST
          buffers: gi_graph_create from pinned host edges (H2D inside),
          gi_pagerank into host memory, gi_bfs x 64 into host memory.
-roofline: the pull-PageRank edge kernel (dominant), algorithmic bytes
-         4m + (o+12)n per launch / its CUDA-event duration.
+roofline: the kernel with the larger share of the step (BFS on config 2);
+         roofline_pr: the pull-PageRank iteration (the north_star's >= 50% target),
+         algorithmic bytes 4m + (o+12)n per iteration / its
+         CUDA-event duration; roofline_bfs: 4 B per edge examined + 4 B per
+         pull-level vertex check + 8 B per reached vertex, per source.
 cpu_baseline: the oracle (oracle/, plain C, OpenMP) on a bounded sample of
          the same graph (2 PR iterations + 2 BFS sources).
 
@@ -74,15 +77,18 @@ def load_peaks():
 
 
 def load_traffic():
-    """Per-launch DRAM bytes of the pull kernel from the committed ncu summary (or None)."""
+    """Per-launch DRAM bytes (ncu --set full) of the PR iteration and the BFS kernel from the committed
+    summary (profiles/ncu_summary.json); missing entries are None."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
-    if not os.path.exists(p):
-        return None
-    try:
-        d = json.load(open(p))
-        return d.get("pr_pull", {}).get("dram_bytes_per_launch")
-    except Exception:
-        return None
+    out = {"pr_pull": None, "bfs_fused": None}
+    if os.path.exists(p):
+        try:
+            d = json.load(open(p))
+            for k in out:
+                out[k] = d.get(k, {}).get("dram_bytes_per_launch")
+        except Exception:
+            pass
+    return out
 
 
 class ClockSampler:
@@ -252,17 +258,14 @@ def run_ours(args):
     del ts, td
     n, m = g.n, g.m
     pr_out = torch.empty(n, dtype=torch.float32, device=dev)
-    bfs_out = torch.empty(n, dtype=torch.int32, device=dev)
     srcs = [int(x) for x in sources]
+    bfs_out = torch.empty((len(srcs), n), dtype=torch.int32, device=dev)  # one parent row per source
 
     def step():
         _, ps = g.pagerank(cfg.pr_iters, cfg.damping, out=pr_out, direction=direction)
-        bfs_edges, launches = 0, ps.edge_launches + ps.aux_launches
-        for src in srcs:
-            _, bs = g.bfs(src, out=bfs_out)
-            bfs_edges += bs.edges_traversed
-            launches += bs.launches
-        return cfg.pr_iters * m, bfs_edges, launches
+        _, bss = g.bfs_multi(srcs, out=bfs_out)
+        launches = ps.edge_launches + ps.aux_launches + sum(b.launches for b in bss)
+        return cfg.pr_iters * m, sum(b.edges_traversed for b in bss), launches
 
     for _ in range(max(args.warmup, 0)):
         step()
@@ -272,8 +275,7 @@ def run_ours(args):
     ev[0].record(stream)
     g.pagerank(cfg.pr_iters, cfg.damping, out=pr_out, direction=direction)
     ev[1].record(stream)
-    for src in srcs:
-        g.bfs(src, out=bfs_out)
+    _, bss = g.bfs_multi(srcs, out=bfs_out)
     ev[2].record(stream)
     torch.cuda.synchronize()
     pr_ms, bfs_ms = ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2])
@@ -308,15 +310,30 @@ def run_ours(args):
         ms_max, edges_all = ms, float(tot_pr + tot_bfs)
     value = edges_all / (ms_max * 1e-3) / 1e9
 
-    # roofline of the dominant kernel (pull PR edge pass): CUDA events around each launch
-    _, ps = g.pagerank(cfg.pr_iters, cfg.damping, out=pr_out, direction=direction, profile=True)
-    kern_ms = ps.edge_ms / max(ps.edge_launches, 1)
+    # rooflines, kernel durations from CUDA events on the library's stream
     peak, peak_src = load_peaks()
-    achieved = ps.bytes_alg_per_iter / (kern_ms * 1e-3) / 1e9
     traffic = load_traffic()
-    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": traffic, "kernel": "k_pr_pull (pull PageRank edge pass + fused vertex update)",
-                "bytes_alg_per_launch": ps.bytes_alg_per_iter, "launch_ms": kern_ms, "peak_source": peak_src}
+    _, ps = g.pagerank(cfg.pr_iters, cfg.damping, out=pr_out, direction=direction, profile=True)
+    kern_ms = ps.edge_ms / max(ps.edge_launches, 1)  # one iteration: edge pass + vertex pass
+    achieved = ps.bytes_alg_per_iter / (kern_ms * 1e-3) / 1e9
+    roofline_pr = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                   "traffic": traffic.get("pr_pull"),
+                   "kernel": "k_pr_seg + k_pr_acc (segmented pull PageRank edge pass + fused vertex update), "
+                             "per iteration",
+                   "bytes_alg_per_launch": ps.bytes_alg_per_iter, "launch_ms": kern_ms,
+                   "vertex_ms": ps.vertex_ms / max(ps.edge_launches, 1), "peak_source": peak_src}
+    # BFS (the larger share of the step): one fused launch per source; algorithmic bytes per source =
+    # 4 B per edge examined + 4 B per pull-level vertex check + 8 B per reached vertex (parent + output)
+    _, bsp = g.bfs_multi(srcs, out=bfs_out, profile=True)
+    bfs_src_ms = sum(b.total_ms for b in bsp) / max(len(bsp), 1)
+    bfs_bytes = sum(4 * b.edges_examined + 4 * b.pull_vertices + 8 * b.reached for b in bsp) / max(len(bsp), 1)
+    bfs_achieved = bfs_bytes / (bfs_src_ms * 1e-3) / 1e9 if bfs_src_ms > 0 else 0.0
+    roofline_bfs = {"bound": "hbm", "achieved": bfs_achieved, "peak": peak, "unit": "GB/s",
+                    "frac": bfs_achieved / peak, "traffic": traffic.get("bfs_fused"),
+                    "kernel": "k_bfs_fused (direction-optimising BFS, one cooperative launch per source)",
+                    "bytes_alg_per_launch": bfs_bytes, "launch_ms": bfs_src_ms, "peak_source": peak_src,
+                    "edges_examined_per_source": sum(b.edges_examined for b in bsp) / max(len(bsp), 1)}
+    roofline = roofline_bfs if bfs_ms > pr_ms else roofline_pr
 
     # e2e through the public API with host buffers
     e2e = None
@@ -324,7 +341,7 @@ def run_ours(args):
         hs = torch.from_numpy(s).pin_memory()
         hd = torch.from_numpy(d).pin_memory()
         hpr = torch.empty(n, dtype=torch.float32).pin_memory()
-        hbfs = torch.empty(n, dtype=torch.int32).pin_memory()
+        hbfs = torch.empty((len(srcs), n), dtype=torch.int32).pin_memory()
         torch.cuda.synchronize()
         t = time.perf_counter()
         e2e_steps = max(1, min(args.steps, 2))
@@ -333,9 +350,8 @@ def run_ours(args):
             g2 = gi.Graph(ctx, cfg.n, hs, hd, flags)
             _, ps2 = g2.pagerank(cfg.pr_iters, cfg.damping, out=hpr, direction=direction)
             e_edges += cfg.pr_iters * g2.m
-            for src in srcs:
-                _, bs = g2.bfs(src, out=hbfs)
-                e_edges += bs.edges_traversed
+            _, bss2 = g2.bfs_multi(srcs, out=hbfs)
+            e_edges += sum(b.edges_traversed for b in bss2)
             g2.close()
         torch.cuda.synchronize()
         e2e_s = time.perf_counter() - t
@@ -364,7 +380,8 @@ def run_ours(args):
                        "l2": "inputs larger than L2 (CSR+CSC ~ 8m bytes > 126 MB), no flush",
                        "parallelism": (f"dst-partition x{world} (NCCL allgather of contrib / frontier bitmap)"
                                        if partition else f"replicas x{world}") if world > 1 else "single"},
-            "e2e": e2e, "gpu_launches": launches, "roofline": roofline, "cpu_baseline": cpu, "clocks": clocks,
+            "e2e": e2e, "gpu_launches": launches, "roofline": roofline, "roofline_pr": roofline_pr,
+            "roofline_bfs": roofline_bfs, "cpu_baseline": cpu, "clocks": clocks,
             "pr_gteps": cfg.pr_iters * m / (pr_ms * 1e-3) / 1e9, "pr_ms": pr_ms,
             "bfs_gteps": (tot_bfs / args.steps) / (bfs_ms * 1e-3) / 1e9 if bfs_ms > 0 else None,
             "bfs_ms_per_source": bfs_ms / max(len(srcs), 1), "build_ms": build_ms, "gen_s": gen_s,

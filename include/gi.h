@@ -239,10 +239,27 @@ typedef struct {
   float total_ms;          /* profile=1 */
   int32_t launches;        /* kernel launches in the call */
   int32_t reserved;
+  int64_t edges_examined;  /* edge reads of the traversal: push levels every
+                              out-edge of the frontier, pull levels the in-edges
+                              probed before the early exit (single GPU; 0 else) */
+  int64_t pull_vertices;   /* vertex checks of the pull levels (n per level) */
 } gi_bfs_stats;
 
 GI_API gi_status gi_bfs_ex(gi_graph g, int32_t source, const gi_bfs_opts* opts, int32_t* parent_out,
                     gi_bfs_stats* stats /* may be NULL */);
+
+/* k independent BFS runs (the multi-source workloads of BASELINE configs
+ * 2/4/5), identical in result to k gi_bfs_ex calls with the same options:
+ *   sources:     int32[k] in input ids, HOST memory;
+ *   parents_out: int32[k][n] (row i = parents of sources[i], layout as
+ *                gi_bfs), host or device;
+ *   stats:       gi_bfs_stats[k] or NULL (with profile=1, total_ms is the
+ *                batch time divided by k).
+ * On one GPU the runs are issued back to back with a single host
+ * synchronisation; on several GPUs this is a loop of gi_bfs_ex.
+ * Errors as gi_bfs_ex (checked for every source before any run); k = 0 -> GI_OK. */
+GI_API gi_status gi_bfs_multi(gi_graph g, int32_t k, const int32_t* sources, const gi_bfs_opts* opts,
+                              int32_t* parents_out, gi_bfs_stats* stats /* may be NULL */);
 
 /* ---------------------------------------------------------------- misc */
 GI_API const char* gi_status_string(gi_status s);

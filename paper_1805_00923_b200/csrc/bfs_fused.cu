@@ -41,12 +41,14 @@ namespace cg = cooperative_groups;
 namespace gi {
 namespace {
 
-constexpr int kFT = 1024;        // threads per CTA
+constexpr int kFT = 1024;        // threads per CTA (one CTA per SM: 64 registers)
 constexpr int kFW = kFT / 32;    // warps per CTA
-constexpr int kFSmall = 8192;    // frontier size expanded by the per-CTA scan
+constexpr int kFSmall = 8 * kFT; // frontier size expanded by the per-CTA scan
 constexpr int kFChunk = kFT;     // frontier entries per scan chunk (large frontiers)
 constexpr int kStreak = 16;      // consecutive small push levels before handing over to the small grid
 constexpr int kSmallGrid = 16;   // CTAs of the small-grid launch
+constexpr int64_t kBitmapPush = 1 << 16;  // push levels expanding more edges emit a bitmap frontier
+constexpr uint32_t kNever = 0xFFFFFFFFu;   // stamp of vertices without in-edges: no BFS reaches them
 
 template <typename OffT>
 struct FusedArgs {
@@ -55,14 +57,21 @@ struct FusedArgs {
   const OffT* __restrict__ csc_off;
   const int32_t* __restrict__ csc_idx;
   const int32_t* __restrict__ outdeg;
-  int32_t* parent;
+  uint32_t* stamp;                 // visited: stamp[v] == epoch (never cleared between sources)
+  uint32_t epoch;
+  int32_t source_in;               // input id of the source
+  const int32_t* __restrict__ inv; // input -> internal id (null: not relabelled)
+  int fresh;                       // first launch of a source: reset the frontier state in the kernel prologue
+  int32_t* out;                    // parents in input ids (written at claim time; -1 preset)
+  const int32_t* __restrict__ perm;  // internal -> input id (null: not relabelled)
   int32_t* q[2];
   uint32_t* bm[3];
   int64_t* cnt;        // 4-level ring of {|F|, sum outdeg F}
   long long* tail;     // 4-level ring of queue tails (bitmap -> queue compaction)
   long long* pre;      // per-entry exclusive prefix of degrees within its chunk
   long long* ctot;     // chunk totals -> exclusive chunk offsets; ctot[nchunks] = E
-  int64_t* state;      // [level, queue valid, bitmap valid, pull levels, done] across launches
+  int64_t* state;      // [level, queue valid, bitmap valid, pull levels, done, reached, edges, examined,
+                       //  pull-checked vertices] across launches
   int64_t n, mdiv;
   int64_t small_max;   // a push level with sum outdeg F <= small_max is "small"
   int mode;            // 0: full grid, hands over after kStreak small levels; 1: small grid, hands back
@@ -117,13 +126,13 @@ __device__ __forceinline__ void cta_append(bool want, int32_t v, int32_t* __rest
 }
 
 template <typename OffT>
-__global__ void __launch_bounds__(kFT, 2) k_bfs_fused(FusedArgs<OffT> A) {
+__global__ void __launch_bounds__(kFT, 1) k_bfs_fused(FusedArgs<OffT> A) {
   extern __shared__ __align__(16) unsigned char fsmem[];
   FSmem& sm = *reinterpret_cast<FSmem*>(fsmem);
   uint32_t* sbits = reinterpret_cast<uint32_t*>(fsmem);  // pull phase: staged bitmap prefix
   __shared__ int s_warp[kFW];
   __shared__ long long s_base;
-  __shared__ long long s_red[2][kFW];
+  __shared__ long long s_red[3][kFW];
   __shared__ union {
     typename cub::BlockScan<int, kFT>::TempStorage i;
     typename cub::BlockScan<long long, kFT>::TempStorage l;
@@ -132,14 +141,49 @@ __global__ void __launch_bounds__(kFT, 2) k_bfs_fused(FusedArgs<OffT> A) {
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int64_t G = gridDim.x;
   const int64_t words = (A.n + 31) >> 5;
+  // claim v for this source: the first thread to move its stamp to `epoch` wins
+  auto claim = [&](int32_t v) {
+    const uint32_t s = *(volatile uint32_t*)&A.stamp[v];
+    return s != A.epoch && atomicCAS(&A.stamp[v], s, A.epoch) == s;
+  };
+  if (A.fresh) {  // new source: output -1 everywhere, empty level-0 bitmap, then the source itself
+    // the stamps are read at random by every level: pull them into L2 (32 lines per thread pass)
+    for (int64_t i = (blockIdx.x * (int64_t)kFT + tid) * 32; i < A.n; i += G * kFT * 32)
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(A.stamp + i));
+    for (int64_t i = blockIdx.x * (int64_t)kFT + tid; i < A.n; i += G * kFT) A.out[i] = -1;
+    for (int64_t i = blockIdx.x * (int64_t)kFT + tid; i < words; i += G * kFT) A.bm[0][i] = 0u;
+    grid.sync();
+    if (blockIdx.x == 0 && tid == 0) {
+      const int32_t s = A.inv ? A.inv[A.source_in] : A.source_in;
+      A.stamp[s] = A.epoch;
+      A.out[A.source_in] = A.source_in;
+      A.q[0][0] = s;
+      A.bm[0][s >> 5] = 1u << (s & 31);
+      for (int i = 0; i < 8; ++i) A.cnt[i] = 0;
+      for (int i = 0; i < 4; ++i) A.tail[i] = 0;
+      A.cnt[0] = 1;
+      A.cnt[1] = __ldg(&A.outdeg[s]);
+      for (int i = 0; i < 11; ++i) A.state[i] = 0;
+      A.state[1] = 1;  // frontier valid as a queue
+      A.state[2] = 1;  // ... and as a bitmap
+      A.state[9] = (int64_t)gtimer();
+    }
+    grid.sync();
+  }
   int64_t level = A.state[0], pulls = A.state[3];
   bool qvalid = A.state[1] != 0;  // the current frontier is available as a queue ...
-  bool bvalid = A.state[2] != 0;  // ... and as a bitmap (level 0: both, set up by the host)
+  bool bvalid = A.state[2] != 0;  // ... and as a bitmap (level 0: both)
   bool done = false;
   int streak = 0;
+  // the output parent vector in input ids, written once per claimed vertex
+  auto emit = [&](int64_t v, int32_t u) {
+    if (A.perm) A.out[__ldg(&A.perm[v])] = __ldg(&A.perm[u]);
+    else A.out[v] = u;
+  };
   for (;;) {
     const int64_t* c = A.cnt + 2 * (level % 4);
     const int64_t nf = vload(c), sdeg = vload(c + 1);
+
     const bool timed = A.times && blockIdx.x == 0 && tid == 0 && level < A.max_times;
     if (timed) A.times[3 * level] = gtimer();
     if (nf == 0) {
@@ -152,6 +196,12 @@ __global__ void __launch_bounds__(kFT, 2) k_bfs_fused(FusedArgs<OffT> A) {
     if (A.mode == 1 && !small) break;                  // back to the full grid
     streak = small ? streak + 1 : 0;
     if (A.mode == 0 && A.small_max > 0 && streak > kStreak) break;  // hand over to the small grid
+    if (blockIdx.x == 0 && tid == 0) {  // reached vertices and their out-edges (R16), summed over levels
+      A.state[5] += nf;
+      A.state[6] += sdeg;
+      if (!pull) atomicAdd((unsigned long long*)&A.state[7], (unsigned long long)sdeg);  // push: every out-edge of F
+      if (pull) atomicAdd((unsigned long long*)&A.state[8], (unsigned long long)A.n);   // pull: every vertex checked
+    }
     uint32_t* bcur = A.bm[level % 3];
     uint32_t* bnext = A.bm[(level + 1) % 3];
     int32_t* qcur = A.q[level & 1];
@@ -163,6 +213,7 @@ __global__ void __launch_bounds__(kFT, 2) k_bfs_fused(FusedArgs<OffT> A) {
       A.tail[(level + 2) % 4] = 0;
     }
     long long fcnt = 0, fdeg = 0;  // this thread's share of |F_{l+1}| and its out-degrees
+    long long fexam = 0;           // in-edges this thread probed (pull levels)
 
     if (pull) {
       ++pulls;
@@ -178,32 +229,73 @@ __global__ void __launch_bounds__(kFT, 2) k_bfs_fused(FusedArgs<OffT> A) {
       for (int i = tid; i < A.sw; i += kFT) sbits[i] = __ldcg(&bcur[i]);
       __syncthreads();
       const uint32_t lim = (uint32_t)A.sw * 32u;
-      for (int64_t wd = blockIdx.x * (int64_t)kFW + w; wd < words; wd += G * kFW) {
-        const int64_t v = (wd << 5) + lane;
-        bool found = false;
-        if (v < A.n && __ldcg(&A.parent[v]) == -1) {
-          const int64_t e1 = (int64_t)A.csc_off[v + 1];
-          for (int64_t e = (int64_t)A.csc_off[v]; e < e1 && !found; e += 4) {
-            uint32_t u[4];
+      auto in_frontier = [&](uint32_t u) {
+        const uint32_t word = u < lim ? sbits[u >> 5] : __ldcg(&bcur[u >> 5]);
+        return ((word >> (u & 31)) & 1u) != 0u;
+      };
+      // each warp owns kPW words per step (lane l: vertex l of each), so every
+      // lane has kPW independent parent / offset / first-edge chains in flight;
+      // vertices not settled by their first 4 in-edges continue one by one
+      constexpr int kPW = 2;
+      for (int64_t wd0 = (blockIdx.x * (int64_t)kFW + w) * kPW; wd0 < words; wd0 += G * kFW * kPW) {
+        int64_t v[kPW], e[kPW], e1[kPW];
+        bool open[kPW], found[kPW];
 #pragma unroll
-            for (int k = 0; k < 4; ++k) u[k] = e + k < e1 ? (uint32_t)__ldg(&A.csc_idx[e + k]) : 0xffffffffu;
+        for (int j = 0; j < kPW; ++j) {
+          v[j] = ((wd0 + j) << 5) + lane;
+          if (wd0 + j < words && v[j] < A.n) {
+            const uint32_t s = __ldcg(&A.stamp[v[j]]);
+            open[j] = s != A.epoch && s != kNever;
+          } else {
+            open[j] = false;
+          }
+          found[j] = false;
+          e[j] = e1[j] = 0;
+        }
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              if (!found && u[k] != 0xffffffffu) {
-                const uint32_t word = u[k] < lim ? sbits[u[k] >> 5] : __ldcg(&bcur[u[k] >> 5]);
-                if ((word >> (u[k] & 31)) & 1u) {
-                  A.parent[v] = (int32_t)u[k];
-                  found = true;
-                }
-              }
+        for (int j = 0; j < kPW; ++j)
+          if (open[j]) {
+            e[j] = (int64_t)A.csc_off[v[j]];
+            e1[j] = (int64_t)A.csc_off[v[j] + 1];
+          }
+        uint32_t u[kPW][4];
+#pragma unroll
+        for (int j = 0; j < kPW; ++j)
+#pragma unroll
+          for (int k = 0; k < 4; ++k) u[j][k] = e[j] + k < e1[j] ? (uint32_t)__ldg(&A.csc_idx[e[j] + k]) : 0xffffffffu;
+#pragma unroll
+        for (int j = 0; j < kPW; ++j) fexam += min((int64_t)4, e1[j] - e[j]);
+#pragma unroll
+        for (int j = 0; j < kPW; ++j) {
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            if (!found[j] && u[j][k] != 0xffffffffu && in_frontier(u[j][k])) {
+              A.stamp[v[j]] = A.epoch;
+              emit(v[j], (int32_t)u[j][k]);
+              found[j] = true;
             }
+          for (int64_t ee = e[j] + 4; ee < e1[j] && !found[j]; ee += 4) {
+            uint32_t x[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) x[k] = ee + k < e1[j] ? (uint32_t)__ldg(&A.csc_idx[ee + k]) : 0xffffffffu;
+            fexam += min((int64_t)4, e1[j] - ee);
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              if (!found[j] && x[k] != 0xffffffffu && in_frontier(x[k])) {
+                A.stamp[v[j]] = A.epoch;
+                emit(v[j], (int32_t)x[k]);
+                found[j] = true;
+              }
           }
         }
-        const unsigned mask = __ballot_sync(0xffffffffu, found);
-        if (lane == 0) bnext[wd] = mask;
-        if (found) {
-          fcnt += 1;
-          fdeg += __ldg(&A.outdeg[v]);
+#pragma unroll
+        for (int j = 0; j < kPW; ++j) {
+          const unsigned mask = __ballot_sync(0xffffffffu, found[j]);
+          if (lane == 0 && wd0 + j < words) bnext[wd0 + j] = mask;
+          if (found[j]) {
+            fcnt += 1;
+            fdeg += __ldg(&A.outdeg[v[j]]);
+          }
         }
       }
       qvalid = false;
@@ -231,12 +323,31 @@ __global__ void __launch_bounds__(kFT, 2) k_bfs_fused(FusedArgs<OffT> A) {
         grid.sync();
       }
       unsigned long long* tn = reinterpret_cast<unsigned long long*>(cn);
-      // visit one flattened edge (u -> v): claim v, append, set its next-bitmap bit
+      // Big push levels (the hub levels of social graphs) emit the next
+      // frontier as a bitmap (one atomicOr per claim, no queue appends and
+      // their CTA barriers); the pull level that usually follows reads it
+      // directly, and a push level converts it back to a queue.
+      const bool to_bm = sdeg > kBitmapPush && sdeg > 4 * nf;
+      if (to_bm) {
+        for (int64_t i = blockIdx.x * (int64_t)kFT + tid; i < words; i += G * kFT) bnext[i] = 0u;
+        grid.sync();
+      }
+      // visit one flattened edge (u -> v): claim v, then append it (or set its bit)
       auto claim_step = [&](bool valid, int32_t u, int32_t v) {
         bool won = false;
-        if (valid && *(volatile int32_t*)&A.parent[v] == -1) won = atomicCAS(&A.parent[v], -1, u) == -1;
-        if (won) fdeg += __ldg(&A.outdeg[v]);
-        cta_append(won, v, qnext, tn, s_warp, &s_base);
+        if (valid) won = claim(v);
+        if (won) {
+          fdeg += __ldg(&A.outdeg[v]);
+          emit(v, u);
+        }
+        if (to_bm) {
+          if (won) {
+            atomicOr(&bnext[v >> 5], 1u << (v & 31));
+            fcnt += 1;
+          }
+        } else {
+          cta_append(won, v, qnext, tn, s_warp, &s_base);
+        }
       };
       if (sdeg <= 4 * nf) {
         // low-degree frontier (road/grid-like levels): thread per frontier vertex,
@@ -262,12 +373,15 @@ __global__ void __launch_bounds__(kFT, 2) k_bfs_fused(FusedArgs<OffT> A) {
             unsigned wmask = 0;
 #pragma unroll
             for (int j = 0; j < 4; ++j) v[j] = e + 4 * k + j < e1 ? __ldg(&A.csr_idx[e + 4 * k + j]) : -1;
-            int32_t pv[4];
+            uint32_t pv[4];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) pv[j] = v[j] >= 0 ? *(volatile int32_t*)&A.parent[v[j]] : 0;
+            for (int j = 0; j < 4; ++j) pv[j] = v[j] >= 0 ? *(volatile uint32_t*)&A.stamp[v[j]] : A.epoch;
 #pragma unroll
             for (int j = 0; j < 4; ++j)
-              if (v[j] >= 0 && pv[j] == -1 && atomicCAS(&A.parent[v[j]], -1, u) == -1) wmask |= 1u << j;
+              if (pv[j] != A.epoch && atomicCAS(&A.stamp[v[j]], pv[j], A.epoch) == pv[j]) {
+                wmask |= 1u << j;
+                emit(v[j], u);
+              }
             const int mine = __popc(wmask);
             int incl = mine;
 #pragma unroll
@@ -330,7 +444,7 @@ __global__ void __launch_bounds__(kFT, 2) k_bfs_fused(FusedArgs<OffT> A) {
           }
           claim_step(f < hi, u, v);
         }
-        fcnt = 0;  // counted through the tail below
+        if (!to_bm) fcnt = 0;  // counted through the tail below
       } else {
         // grid-wide scan of the frontier's degrees: chunk prefixes, then chunk offsets
         const int64_t nch = (nf + kFChunk - 1) / kFChunk;
@@ -406,30 +520,34 @@ __global__ void __launch_bounds__(kFT, 2) k_bfs_fused(FusedArgs<OffT> A) {
           }
           claim_step(f < hi, u, v);
         }
-        fcnt = 0;
+        if (!to_bm) fcnt = 0;
       }
-      qvalid = true;
-      bvalid = false;  // push levels produce only the queue
+      qvalid = !to_bm;  // push levels produce the queue or (big ones) the bitmap
+      bvalid = to_bm;
     }
     // |F_{l+1}| and sum of its out-degrees: one atomic pair per CTA
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       fcnt += __shfl_xor_sync(0xffffffffu, fcnt, o);
       fdeg += __shfl_xor_sync(0xffffffffu, fdeg, o);
+      fexam += __shfl_xor_sync(0xffffffffu, fexam, o);
     }
     if (lane == 0) {
       s_red[0][w] = fcnt;
       s_red[1][w] = fdeg;
+      s_red[2][w] = fexam;
     }
     __syncthreads();
     if (tid == 0) {
-      long long a = 0, b = 0;
+      long long a = 0, b = 0, x = 0;
       for (int i = 0; i < kFW; ++i) {
         a += s_red[0][i];
         b += s_red[1][i];
+        x += s_red[2][i];
       }
       if (a) atomicAdd((unsigned long long*)&cn[0], (unsigned long long)a);
       if (b) atomicAdd((unsigned long long*)&cn[1], (unsigned long long)b);
+      if (x) atomicAdd((unsigned long long*)&A.state[7], (unsigned long long)x);
     }
     if (timed) A.times[3 * level + 1] = gtimer();
     grid.sync();
@@ -437,6 +555,7 @@ __global__ void __launch_bounds__(kFT, 2) k_bfs_fused(FusedArgs<OffT> A) {
     ++level;
   }
   if (blockIdx.x == 0 && tid == 0) {
+    A.state[10] = (int64_t)gtimer();  // last exit
     A.state[0] = level;
     A.state[1] = qvalid;
     A.state[2] = bvalid;
@@ -445,115 +564,149 @@ __global__ void __launch_bounds__(kFT, 2) k_bfs_fused(FusedArgs<OffT> A) {
   }
 }
 
-__global__ void k_fused_init(int32_t s_in, const int32_t* __restrict__ inv, const int32_t* __restrict__ outdeg,
-                             int32_t* __restrict__ parent, int32_t* __restrict__ q, uint32_t* __restrict__ bm,
-                             int64_t* __restrict__ cnt, long long* __restrict__ tail) {
-  const int32_t s = inv ? inv[s_in] : s_in;
-  parent[s] = s;
-  q[0] = s;
-  bm[s >> 5] = 1u << (s & 31);
-  for (int i = 0; i < 8; ++i) cnt[i] = 0;
-  for (int i = 0; i < 4; ++i) tail[i] = 0;
-  cnt[0] = 1;
-  cnt[1] = outdeg[s];
-  cnt[12] = 0;  // state: level
-  cnt[13] = 1;  //        frontier valid as a queue
-  cnt[14] = 1;  //        frontier valid as a bitmap
-  cnt[15] = 0;  //        pull levels
-  cnt[16] = 0;  //        done
-}
 
 }  // namespace
 
+// stamps at setup (and after an epoch wrap): kNever for vertices no edge
+// enters (the pull levels skip them after one coalesced load), else 0
 template <typename OffT>
-static gi_status bfs_fused_t(gi_graph g, int32_t source, const gi_bfs_opts& o, int32_t* d_out, gi_bfs_stats* stats) {
+__global__ void k_stamp_init(const OffT* __restrict__ csc_off, int64_t n, uint32_t* __restrict__ stamp) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x)
+    stamp[v] = csc_off[v + 1] == csc_off[v] ? kNever : 0u;
+}
+
+// one-time per graph: buffers, dynamic shared memory, co-resident grid size
+template <typename OffT>
+static gi_status fused_setup(gi_graph g) {
   gi_context ctx = g->ctx;
-  cudaStream_t st = ctx->stream;
   const int64_t n = g->n, words = (n + 31) >> 5;
   auto& F = g->fused;
-  if (!F.ready) {
-    GI_TRY(F.parent.alloc((n + 1) * sizeof(int32_t)));
-    for (int k = 0; k < 2; ++k) GI_TRY(F.q[k].alloc((n + 1) * sizeof(int32_t)));
-    for (int k = 0; k < 3; ++k) GI_TRY(F.bm[k].alloc((words + 1) * sizeof(uint32_t)));
-    GI_TRY(F.cnt.alloc(24 * sizeof(int64_t)));
-    GI_TRY(F.pre.alloc((n + 1) * sizeof(long long)));
-    GI_TRY(F.ctot.alloc((n / kFChunk + 2) * sizeof(long long)));
-    int optin = 0, per_sm = 0;
-    GI_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
-    GI_CUDA(cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, ctx->device));
-    cudaFuncAttributes fa{};
-    GI_CUDA(cudaFuncGetAttributes(&fa, k_bfs_fused<OffT>));
-    int dyn = std::min(optin, per_sm / 2) - (int)fa.sharedSizeBytes - 2048;
-    dyn = std::max(dyn, (int)sizeof(FSmem)) & ~15;
-    GI_CUDA(cudaFuncSetAttribute(k_bfs_fused<OffT>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
-    int bpm = 0;
-    GI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bpm, k_bfs_fused<OffT>, kFT, dyn));
-    if (bpm < 1) return fail(GI_ERR_UNSUPPORTED, "fused BFS kernel cannot be co-resident");
-    F.dyn = dyn;
-    F.grid = bpm * ctx->num_sms;
-    F.ready = true;
-  }
-  cudaEvent_t e0 = nullptr, e1 = nullptr;
-  if (o.profile) {
-    GI_CUDA(cudaEventCreate(&e0));
-    GI_CUDA(cudaEventCreate(&e1));
-    GI_CUDA(cudaEventRecord(e0, st));
-  }
-  GI_CUDA(cudaMemsetAsync(F.parent.p, 0xFF, n * sizeof(int32_t), st));
-  for (int k = 0; k < 3; ++k) GI_CUDA(cudaMemsetAsync(F.bm[k].p, 0, words * sizeof(uint32_t), st));
+  if (F.ready) return GI_OK;
+  GI_TRY(F.stamp.alloc((n + 1) * sizeof(uint32_t)));
+  k_stamp_init<OffT><<<grid_for(n, 256, ctx->num_sms), 256, 0, ctx->stream>>>(g->csc_off.as<OffT>(), n,
+                                                                              F.stamp.as<uint32_t>());
+  GI_CUDA(cudaGetLastError());
+  F.epoch = 0;
+  for (int k = 0; k < 2; ++k) GI_TRY(F.q[k].alloc((n + 1) * sizeof(int32_t)));
+  for (int k = 0; k < 3; ++k) GI_TRY(F.bm[k].alloc((words + 1) * sizeof(uint32_t)));
+  GI_TRY(F.cnt.alloc(32 * sizeof(int64_t)));
+  GI_TRY(F.pre.alloc((n + 1) * sizeof(long long)));
+  GI_TRY(F.ctot.alloc((n / kFChunk + 2) * sizeof(long long)));
+  int optin = 0, per_sm = 0;
+  GI_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
+  GI_CUDA(cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, ctx->device));
+  cudaFuncAttributes fa{};
+  GI_CUDA(cudaFuncGetAttributes(&fa, k_bfs_fused<OffT>));
+  int dyn = std::min(optin, per_sm / 2) - (int)fa.sharedSizeBytes - 2048;
+  dyn = std::max(dyn, (int)sizeof(FSmem)) & ~15;
+  GI_CUDA(cudaFuncSetAttribute(k_bfs_fused<OffT>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
+  int bpm = 0;
+  GI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bpm, k_bfs_fused<OffT>, kFT, dyn));
+  if (bpm < 1) return fail(GI_ERR_UNSUPPORTED, "fused BFS kernel cannot be co-resident");
+  F.dyn = dyn;
+  F.grid = bpm * ctx->num_sms;
+  F.ready = true;
+  return GI_OK;
+}
+
+template <typename OffT>
+static FusedArgs<OffT> fused_args(gi_graph g, const gi_bfs_opts& o, int32_t* d_out) {
+  auto& F = g->fused;
+  const int64_t words = (g->n + 31) >> 5;
   int64_t* cnt = F.cnt.as<int64_t>();
-  long long* tail = reinterpret_cast<long long*>(cnt + 8);
-  int64_t* stt = cnt + 8 + 4;  // state[5] after the tail ring
-  k_fused_init<<<1, 1, 0, st>>>(source, g->relabeled ? g->inv.as<int32_t>() : nullptr, g->outdeg.as<int32_t>(),
-                                F.parent.as<int32_t>(), F.q[0].as<int32_t>(), F.bm[0].as<uint32_t>(), cnt, tail);
   FusedArgs<OffT> A;
   A.csr_off = g->csr_off.as<OffT>();
   A.csr_idx = g->csr_idx.as<int32_t>();
   A.csc_off = g->csc_off.as<OffT>();
   A.csc_idx = g->csc_idx.as<int32_t>();
   A.outdeg = g->outdeg.as<int32_t>();
-  A.parent = F.parent.as<int32_t>();
+  A.stamp = F.stamp.as<uint32_t>();
+  A.inv = g->relabeled ? g->inv.as<int32_t>() : nullptr;
+  A.fresh = 0;
+  A.out = d_out;
+  A.perm = g->relabeled ? g->perm.as<int32_t>() : nullptr;
   A.q[0] = F.q[0].as<int32_t>();
   A.q[1] = F.q[1].as<int32_t>();
   for (int k = 0; k < 3; ++k) A.bm[k] = F.bm[k].as<uint32_t>();
   A.cnt = cnt;
-  A.tail = tail;
+  A.tail = reinterpret_cast<long long*>(cnt + 8);
   A.pre = F.pre.as<long long>();
   A.ctot = F.ctot.as<long long>();
-  A.state = stt;
+  A.state = cnt + 8 + 4;  // state[7] after the tail ring
   A.small_max = 1 << 16;
   A.mode = 0;
-  A.n = n;
+  A.n = g->n;
   A.mdiv = g->m / (o.threshold_div > 0 ? o.threshold_div : 20);
   A.policy = o.policy;
   A.sw = (int)std::min<int64_t>(words, (int64_t)((F.dyn) / 4));
-  static const char* dbg = getenv("GI_DEBUG_BFS_FUSED");  // diagnostics: per-level timeline file
-  DevBuf tbuf;
   A.times = nullptr;
   A.max_times = 0;
+  return A;
+}
+
+// start a source: a fresh epoch (the visited stamps of earlier sources become
+// stale, no clearing), then one full-grid launch whose prologue resets the
+// output, the level-0 bitmap and the counters
+template <typename OffT>
+static gi_status fused_start(gi_graph g, int32_t source, FusedArgs<OffT>& A) {
+  gi_context ctx = g->ctx;
+  cudaStream_t st = ctx->stream;
+  auto& F = g->fused;
+  if (++F.epoch == kNever) {  // epochs exhausted (2^32 - 1 sources): reset the stamps once
+    k_stamp_init<OffT><<<grid_for(g->n, 256, ctx->num_sms), 256, 0, st>>>(g->csc_off.as<OffT>(), g->n,
+                                                                        F.stamp.as<uint32_t>());
+    GI_CUDA(cudaGetLastError());
+    F.epoch = 1;
+  }
+  A.epoch = F.epoch;
+  A.source_in = source;
+  A.fresh = 1;
+  A.mode = 0;
+  void* args[] = {&A};
+  GI_CUDA(cudaLaunchCooperativeKernel((void*)k_bfs_fused<OffT>, dim3(F.grid), dim3(kFT), args, (size_t)F.dyn, st));
+  GI_CUDA(cudaGetLastError());
+  A.fresh = 0;
+  return GI_OK;
+}
+
+template <typename OffT>
+static gi_status bfs_fused_t(gi_graph g, int32_t source, const gi_bfs_opts& o, int32_t* d_out, gi_bfs_stats* stats) {
+  gi_context ctx = g->ctx;
+  cudaStream_t st = ctx->stream;
+  GI_TRY(fused_setup<OffT>(g));
+  auto& F = g->fused;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (o.profile) {
+    GI_CUDA(cudaEventCreate(&e0));
+    GI_CUDA(cudaEventCreate(&e1));
+    GI_CUDA(cudaEventRecord(e0, st));
+  }
+  FusedArgs<OffT> A = fused_args<OffT>(g, o, d_out);
+  static const char* dbg = getenv("GI_DEBUG_BFS_FUSED");  // diagnostics: per-level timeline file
+  DevBuf tbuf;
   if (dbg) {
     A.max_times = 1 << 16;
     GI_TRY(tbuf.alloc((size_t)3 * A.max_times * sizeof(unsigned long long)));
     GI_CUDA(cudaMemsetAsync(tbuf.p, 0, (size_t)3 * A.max_times * sizeof(unsigned long long), st));
     A.times = tbuf.as<unsigned long long>();
   }
+  GI_TRY(fused_start<OffT>(g, source, A));
   // full grid; high-diameter stretches continue on a small grid (cheaper grid barriers)
   int64_t* h = ctx->h_scratch;
-  int launches = 1;
-  for (int mode = 0;; mode ^= 1) {
+  int launches = 2;
+  for (int mode = 1;; mode ^= 1) {
+    GI_CUDA(cudaMemcpyAsync(h + 16, A.state, 9 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    GI_CUDA(stream_wait(st));
+    if (h[16 + 4]) break;
     A.mode = mode;
     void* args[] = {&A};
     const int grid = mode == 0 ? F.grid : std::min(F.grid, kSmallGrid);
     GI_CUDA(cudaLaunchCooperativeKernel((void*)k_bfs_fused<OffT>, dim3(grid), dim3(kFT), args, (size_t)F.dyn, st));
     GI_CUDA(cudaGetLastError());
     ++launches;
-    GI_CUDA(cudaMemcpyAsync(h + 16, stt, 5 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-    GI_CUDA(stream_wait(st));
-    if (h[16 + 4]) break;
   }
   const int64_t lv[2] = {h[16], h[16 + 3]};
-  int64_t reached = 0, edges = 0;
-  GI_TRY(bfs_finish_output(g, F.parent.as<int32_t>(), d_out, &reached, &edges));
+  const int64_t reached = h[16 + 5], edges = h[16 + 6];
   if (dbg) {
     std::vector<unsigned long long> ht((size_t)3 * A.max_times);
     GI_CUDA(cudaMemcpy(ht.data(), tbuf.p, ht.size() * 8, cudaMemcpyDeviceToHost));
@@ -579,7 +732,83 @@ static gi_status bfs_fused_t(gi_graph g, int32_t source, const gi_bfs_opts& o, i
     stats->pull_levels = (int32_t)lv[1];
     stats->reached = reached;
     stats->edges_traversed = edges;
-    stats->launches = launches + 1;
+    stats->edges_examined = h[16 + 7];
+    stats->pull_vertices = h[16 + 8];
+    stats->launches = launches + 3;
+  }
+  return GI_OK;
+}
+
+// k sources back to back: every source is reset and run by one full-grid
+// launch with no host round trip in between; its final state is copied to
+// pinned host memory, and one synchronisation covers the batch. Sources the
+// single launch did not finish (high-diameter graphs hand over to the small
+// grid) are rerun one by one.
+template <typename OffT>
+static gi_status bfs_fused_multi_t(gi_graph g, int32_t k, const int32_t* sources, const gi_bfs_opts& o,
+                                   int32_t* d_out, int64_t out_stride, gi_bfs_stats* stats, int32_t* h_user_out) {
+  gi_context ctx = g->ctx;
+  cudaStream_t st = ctx->stream;
+  GI_TRY(fused_setup<OffT>(g));
+  const int64_t n = g->n;
+  if (ctx->h_batch_len < (int64_t)k * 16) {
+    if (ctx->h_batch) cudaFreeHost(ctx->h_batch);
+    ctx->h_batch = nullptr;
+    ctx->h_batch_len = 0;
+    GI_CUDA(cudaMallocHost(&ctx->h_batch, (size_t)k * 16 * sizeof(int64_t)));
+    ctx->h_batch_len = (int64_t)k * 16;
+  }
+  int64_t* hb = ctx->h_batch;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (o.profile) {
+    GI_CUDA(cudaEventCreate(&e0));
+    GI_CUDA(cudaEventCreate(&e1));
+    GI_CUDA(cudaEventRecord(e0, st));
+  }
+  for (int32_t i = 0; i < k; ++i) {
+    int32_t* out = d_out + (h_user_out ? 0 : (int64_t)i * out_stride);
+    FusedArgs<OffT> A = fused_args<OffT>(g, o, out);
+    GI_TRY(fused_start<OffT>(g, sources[i], A));
+    GI_CUDA(cudaMemcpyAsync(hb + 16 * i, A.state, 11 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    if (h_user_out)  // host output: the device staging row goes out before the next source reuses it
+      GI_CUDA(cudaMemcpyAsync(h_user_out + (int64_t)i * n, out, n * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  }
+  float ms = 0.f;
+  if (o.profile) GI_CUDA(cudaEventRecord(e1, st));
+  GI_CUDA(stream_wait(st));
+  if (o.profile) {
+    GI_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+  }
+  if (const char* dbg = getenv("GI_DEBUG_BFS_MULTI")) {  // diagnostics: kernel span and gap to the next source
+    if (FILE* f = fopen(dbg, "a")) {
+      for (int32_t i = 0; i < k; ++i)
+        fprintf(f, "src=%d kernel_us=%.2f gap_to_next_us=%.2f\n", sources[i], (hb[16 * i + 10] - hb[16 * i + 9]) / 1e3,
+                i + 1 < k ? (hb[16 * (i + 1) + 9] - hb[16 * i + 10]) / 1e3 : 0.0);
+      fclose(f);
+    }
+  }
+  for (int32_t i = 0; i < k; ++i) {
+    gi_bfs_stats s{};
+    if (!hb[16 * i + 4]) {  // not finished by one launch: run it with the handover loop
+      int32_t* out = d_out + (h_user_out ? 0 : (int64_t)i * out_stride);
+      GI_TRY(bfs_fused_t<OffT>(g, sources[i], o, out, &s));
+      if (h_user_out) {
+        GI_CUDA(cudaMemcpyAsync(h_user_out + (int64_t)i * n, out, n * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+        GI_CUDA(stream_wait(st));
+      }
+    } else {
+      s.levels = (int32_t)hb[16 * i];
+      s.pull_levels = (int32_t)hb[16 * i + 3];
+      s.reached = hb[16 * i + 5];
+      s.edges_traversed = hb[16 * i + 6];
+      s.edges_examined = hb[16 * i + 7];
+      s.pull_vertices = hb[16 * i + 8];
+      s.launches = 5;
+      s.total_ms = ms / (float)k;
+    }
+    if (stats) stats[i] = s;
   }
   return GI_OK;
 }
@@ -587,6 +816,12 @@ static gi_status bfs_fused_t(gi_graph g, int32_t source, const gi_bfs_opts& o, i
 gi_status bfs_fused(gi_graph g, int32_t source, const gi_bfs_opts& o, int32_t* d_out, gi_bfs_stats* stats) {
   if (g->off64) return bfs_fused_t<int64_t>(g, source, o, d_out, stats);
   return bfs_fused_t<int32_t>(g, source, o, d_out, stats);
+}
+
+gi_status bfs_fused_multi(gi_graph g, int32_t k, const int32_t* sources, const gi_bfs_opts& o, int32_t* d_out,
+                          int64_t out_stride, gi_bfs_stats* stats, int32_t* h_user_out) {
+  if (g->off64) return bfs_fused_multi_t<int64_t>(g, k, sources, o, d_out, out_stride, stats, h_user_out);
+  return bfs_fused_multi_t<int32_t>(g, k, sources, o, d_out, out_stride, stats, h_user_out);
 }
 
 }  // namespace gi

@@ -168,6 +168,7 @@ gi_status gi_context_destroy(gi_context ctx) {
     ctx->nccl_comm = nullptr;
   }
   if (ctx->h_scratch) cudaFreeHost(ctx->h_scratch);
+  if (ctx->h_batch) cudaFreeHost(ctx->h_batch);
   if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
   return GI_OK;
@@ -443,6 +444,46 @@ gi_status gi_bfs_ex(gi_graph g, int32_t source, const gi_bfs_opts* opts, int32_t
 
 gi_status gi_bfs(gi_graph g, int32_t source, int32_t* parent_out) {
   return gi_bfs_ex(g, source, nullptr, parent_out, nullptr);
+}
+
+gi_status gi_bfs_multi(gi_graph g, int32_t k, const int32_t* sources, const gi_bfs_opts* opts, int32_t* parents_out,
+                       gi_bfs_stats* stats) {
+  GI_GUARD_BEGIN
+  if (!g) return fail(GI_ERR_INVALID_ARGUMENT, "gi_bfs_multi: NULL graph");
+  if (k < 0) return fail(GI_ERR_INVALID_ARGUMENT, "gi_bfs_multi: k < 0");
+  if (k == 0) return GI_OK;
+  if (!sources || !parents_out) return fail(GI_ERR_INVALID_ARGUMENT, "gi_bfs_multi: NULL sources / output");
+  if (is_device_ptr(sources)) return fail(GI_ERR_INVALID_ARGUMENT, "gi_bfs_multi: sources must be host memory");
+  for (int32_t i = 0; i < k; ++i)
+    if (sources[i] < 0 || sources[i] >= g->n)
+      return fail(GI_ERR_VERTEX_OUT_OF_RANGE, "gi_bfs_multi: a source is not in [0, n)");
+  gi_bfs_opts o{};
+  if (opts) o = *opts;
+  if (o.policy < GI_BFS_AUTO || o.policy > GI_BFS_PULL_ONLY || o.threshold_div < 0)
+    return fail(GI_ERR_INVALID_ARGUMENT, "gi_bfs_multi: bad options");
+  gi_context ctx = g->ctx;
+  GI_CUDA(cudaSetDevice(ctx->device));
+  static const char* impl = getenv("GI_BFS_IMPL");
+  if (ctx->nranks > 1 || (impl && strcmp(impl, "host") == 0)) {  // one call per source
+    for (int32_t i = 0; i < k; ++i) {
+      OutBuf<int32_t> ob{parents_out + (int64_t)i * g->n, g->n, false, &g->out_stage};
+      int32_t* d = nullptr;
+      GI_TRY(ob.prepare(g, &d));
+      GI_TRY(bfs_run(g, sources[i], o, d, stats ? stats + i : nullptr));
+      GI_TRY(ob.finish(ctx));
+      GI_TRY(sync(ctx));
+    }
+    return GI_OK;
+  }
+  if (is_device_ptr(parents_out)) {
+    GI_TRY(bfs_fused_multi(g, k, sources, o, parents_out, g->n, stats, nullptr));
+  } else {
+    if (!g->out_stage.p || g->out_stage.bytes < (size_t)g->n * sizeof(int32_t))
+      GI_TRY(g->out_stage.alloc(g->n * sizeof(int32_t)));
+    GI_TRY(bfs_fused_multi(g, k, sources, o, g->out_stage.as<int32_t>(), 0, stats, parents_out));
+  }
+  return sync(ctx);
+  GI_GUARD_END
 }
 
 }  // extern "C"

@@ -82,6 +82,8 @@ struct gi_context_s {
   int num_sms = 148;
   // pinned host scratch for small D2H reads (counters)
   int64_t* h_scratch = nullptr;
+  int64_t* h_batch = nullptr;  // pinned per-source state slots of gi_bfs_multi
+  int64_t h_batch_len = 0;
   int live_graphs = 0;  // graphs created on this context and not yet destroyed
 };
 
@@ -139,7 +141,8 @@ struct gi_graph_s {
   struct {                // fused cooperative BFS (bfs_fused.cu)
     bool ready = false;
     int dyn = 0, grid = 0;
-    gi::DevBuf parent, q[2], bm[3], cnt, pre, ctot;
+    gi::DevBuf stamp, q[2], bm[3], cnt, pre, ctot;  // stamp[v] == epoch: visited by the current source
+    uint32_t epoch = 0;
   } fused;
   unsigned bfs_epoch = 0;
 };
@@ -173,6 +176,10 @@ gi_status prdelta_run(gi_graph g, int32_t iters, double damping, double eps, con
 // bfs.cu / bfs_fused.cu
 gi_status bfs_fused(gi_graph g, int32_t source_input_id, const gi_bfs_opts& o, int32_t* d_parent_input_ids,
                     gi_bfs_stats* stats);
+// k sources back to back (single GPU). d_out: device rows of out_stride, or
+// (h_user_out != null) one device staging row copied to h_user_out[i*n] per source
+gi_status bfs_fused_multi(gi_graph g, int32_t k, const int32_t* sources, const gi_bfs_opts& o, int32_t* d_out,
+                          int64_t out_stride, gi_bfs_stats* stats, int32_t* h_user_out);
 gi_status bfs_finish_output(gi_graph g, const int32_t* parent_internal, int32_t* d_out, int64_t* reached,
                             int64_t* edges);
 gi_status bfs_run(gi_graph g, int32_t source_input_id, const gi_bfs_opts& o,

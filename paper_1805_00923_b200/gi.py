@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libgi.so")
+LIB_PATH = os.environ.get("GI_LIBGI") or os.path.join(_PKG, "libgi.so")  # override: A/B experiments
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is not built; run `python -m paper_1805_00923_b200.build` "
@@ -73,7 +73,7 @@ class gi_bfs_opts(ctypes.Structure):
 class gi_bfs_stats(ctypes.Structure):
     _fields_ = [("levels", ctypes.c_int32), ("pull_levels", ctypes.c_int32), ("reached", ctypes.c_int64),
                 ("edges_traversed", ctypes.c_int64), ("total_ms", ctypes.c_float), ("launches", ctypes.c_int32),
-                ("reserved", ctypes.c_int32)]
+                ("reserved", ctypes.c_int32), ("edges_examined", ctypes.c_int64), ("pull_vertices", ctypes.c_int64)]
 
 
 _vp = ctypes.c_void_p
@@ -107,6 +107,7 @@ _SIGS = {
                            ctypes.POINTER(gi_prdelta_stats)], _st),
     "gi_bfs": ([_vp, _i32, _vp], _st),
     "gi_bfs_ex": ([_vp, _i32, ctypes.POINTER(gi_bfs_opts), _vp, ctypes.POINTER(gi_bfs_stats)], _st),
+    "gi_bfs_multi": ([_vp, _i32, _vp, ctypes.POINTER(gi_bfs_opts), _vp, ctypes.POINTER(gi_bfs_stats)], _st),
     "gi_status_string": ([_st], ctypes.c_char_p),
     "gi_last_error": ([], ctypes.c_char_p),
     "gi_abi_version": ([], ctypes.c_int),
@@ -320,6 +321,22 @@ def gi_bfs_ex(g: int, source: int, out=None, policy: int = GI_BFS_AUTO, threshol
     return keep, s
 
 
+def gi_bfs_multi(g: int, sources, out=None, policy: int = GI_BFS_AUTO, threshold_div: int = 0,
+                 profile: bool = False):
+    """k BFS runs back to back; out: int32[k, n] (host or device). Returns (out, [stats])."""
+    n = gi_graph_num_vertices(g)
+    src = np.ascontiguousarray(np.asarray(sources, dtype=np.int64).astype(np.int32))
+    k = len(src)
+    if out is None:
+        out = np.empty((k, n), np.int32)
+    p, keep = _ptr(out, np.int32)
+    o = gi_bfs_opts(policy, threshold_div, int(profile), 0)
+    stats = (gi_bfs_stats * max(k, 1))()
+    _check(_lib.gi_bfs_multi(g, k, src.ctypes.data if k else None, ctypes.byref(o), p or None, stats),
+           "gi_bfs_multi")
+    return keep, list(stats)[:k]
+
+
 # ------------------------------------------------------------------ RAII conveniences
 class Context:
     def __init__(self, device: int = 0, stream: int | None = None, *, local_group: int | None = None,
@@ -380,6 +397,9 @@ class Graph:
 
     def bfs(self, source, out=None, **kw):
         return gi_bfs_ex(self.handle, source, out, **kw)
+
+    def bfs_multi(self, sources, out=None, **kw):
+        return gi_bfs_multi(self.handle, sources, out, **kw)
 
     def out_degrees(self, out=None):
         return gi_graph_out_degrees(self.handle, out)

@@ -350,6 +350,39 @@ def test_bfs_config1(gi, ctx, policy, relabel):
     assert 0 < st.pull_levels < st.levels
 
 
+@pytest.mark.parametrize("where", ["host", "device"])
+def test_bfs_multi(gi, ctx, where):
+    """gi_bfs_multi == k gi_bfs runs: config 1 (one launch per source) and a
+    high-diameter grid (sources rerun through the small-grid handover)."""
+    import torch
+
+    cfg = graphgen.CONFIGS[1]
+    s1, d1 = cfg.edges()
+    s3, d3 = graphgen.grid(64, 64, 0.1, 3)
+    cases = [(cfg.n, s1, d1, [0] + graphgen.pick_sources(cfg.n, s1, d1, 9, 1001).tolist()),
+             (64 * 64, s3, d3, [0, 4095, 2080, 0])]
+    for n, s, d, sources in cases:
+        g = gi.Graph(ctx, n, s, d)
+        go = oracle.build_graph(n, s, d)
+        out = (torch.full((len(sources), n), 7, dtype=torch.int32, device="cuda") if where == "device"
+               else np.full((len(sources), n), 7, np.int32))
+        par, stats = g.bfs_multi(sources, out=out)
+        par = par.cpu().numpy() if where == "device" else par
+        for i, src in enumerate(sources):
+            depth = oracle.bfs_depth(go, src)
+            ok, msg = oracle.validate_bfs(go, src, par[i], depth)
+            assert ok, f"n={n} src={src}: {msg}"
+            _, one = g.bfs(src)
+            assert (stats[i].levels, stats[i].reached, stats[i].edges_traversed) == \
+                (one.levels, one.reached, one.edges_traversed)
+    g = gi.Graph(ctx, 10, *graphgen.cycle(10))
+    with pytest.raises(gi.GiError) as e:
+        g.bfs_multi([0, 10])
+    assert e.value.status == gi.GI_ERR_VERTEX_OUT_OF_RANGE
+    out, st = g.bfs_multi([])
+    assert out.shape == (0, 10) and st == []
+
+
 def test_bfs_stress_repeat(gi, ctx):
     s, d = graphgen.rmat(13, 16, 0.57, 0.19, 0.19, 33)
     n = 1 << 13
