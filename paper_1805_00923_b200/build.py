@@ -17,8 +17,11 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
-BUILD = os.path.join(PKG, "_build")
-LIB = os.path.join(PKG, "libgi.so")
+# GI_BUILD_DEFS / GI_BUILD_LIB / GI_BUILD_DIR: extra nvcc flags, library path and object directory of an
+# experimental variant (A/B runs load it through GI_LIBGI); the product build uses none of them
+BUILD = os.environ.get("GI_BUILD_DIR") or os.path.join(PKG, "_build")
+LIB = os.environ.get("GI_BUILD_LIB") or os.path.join(PKG, "libgi.so")
+EXTRA = os.environ.get("GI_BUILD_DEFS", "").split()
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
@@ -42,7 +45,7 @@ def _stale() -> bool:
 
 def _compile(src: str) -> tuple[str, str]:
     obj = os.path.join(BUILD, os.path.basename(src) + ".o")
-    cmd = [NVCC, *ARCH, *FLAGS, f"-I{INCLUDE}", f"-I{CSRC}", "-c", src, "-o", obj]
+    cmd = [NVCC, *ARCH, *FLAGS, *EXTRA, f"-I{INCLUDE}", f"-I{CSRC}", "-c", src, "-o", obj]
     p = subprocess.run(cmd, capture_output=True, text=True)
     if p.returncode != 0:
         raise RuntimeError(f"nvcc failed on {src}:\n{p.stdout}\n{p.stderr}")

@@ -49,6 +49,15 @@ constexpr int kStreak = 16;      // consecutive small push levels before handing
 constexpr int kSmallGrid = 16;   // CTAs of the small-grid launch
 constexpr int64_t kBitmapPush = 1 << 16;  // push levels expanding more edges emit a bitmap frontier
 constexpr uint32_t kNever = 0xFFFFFFFFu;   // stamp of vertices without in-edges: no BFS reaches them
+#ifndef GI_BFS_VINFO
+#define GI_BFS_VINFO 1  // claims read {input id, out-degree} with one 8-byte gather
+#endif
+#ifndef GI_BFS_KPW
+#define GI_BFS_KPW 4    // 32-vertex words per warp and pull step
+#endif
+#ifndef GI_BFS_SMEM_DIV
+#define GI_BFS_SMEM_DIV 4  // dynamic shared memory = 1/GI_BFS_SMEM_DIV of the SM's (the rest is L1)
+#endif
 
 template <typename OffT>
 struct FusedArgs {
@@ -64,6 +73,7 @@ struct FusedArgs {
   int fresh;                       // first launch of a source: reset the frontier state in the kernel prologue
   int32_t* out;                    // parents in input ids (written at claim time; -1 preset)
   const int32_t* __restrict__ perm;  // internal -> input id (null: not relabelled)
+  const int2* __restrict__ vinfo;    // {input id, out-degree} per internal id
   int32_t* q[2];
   uint32_t* bm[3];
   int64_t* cnt;        // 4-level ring of {|F|, sum outdeg F}
@@ -78,6 +88,7 @@ struct FusedArgs {
                        //    as soon as a level is not small (high-diameter graphs: cheaper barriers)
   int policy, sw;
   unsigned long long* times;  // optional (GI_DEBUG_BFS_FUSED): per level [start, work done, barrier done]
+  unsigned long long* ctimes; // optional: per level < 16 and CTA, the CTA's work-done time
   int max_times;
 };
 
@@ -175,10 +186,17 @@ __global__ void __launch_bounds__(kFT, 1) k_bfs_fused(FusedArgs<OffT> A) {
   bool bvalid = A.state[2] != 0;  // ... and as a bitmap (level 0: both)
   bool done = false;
   int streak = 0;
-  // the output parent vector in input ids, written once per claimed vertex
-  auto emit = [&](int64_t v, int32_t u) {
+  // a claimed vertex: its parent goes to the output vector in input ids; returns its out-degree
+  auto emit = [&](int64_t v, int32_t u) -> int {
+#if GI_BFS_VINFO
+    const int2 iv = __ldg(&A.vinfo[v]);  // {input id, out-degree}: one gather
+    A.out[iv.x] = A.perm ? __ldg(&A.perm[u]) : u;
+    return iv.y;
+#else
     if (A.perm) A.out[__ldg(&A.perm[v])] = __ldg(&A.perm[u]);
     else A.out[v] = u;
+    return __ldg(&A.outdeg[v]);
+#endif
   };
   for (;;) {
     const int64_t* c = A.cnt + 2 * (level % 4);
@@ -236,7 +254,7 @@ __global__ void __launch_bounds__(kFT, 1) k_bfs_fused(FusedArgs<OffT> A) {
       // each warp owns kPW words per step (lane l: vertex l of each), so every
       // lane has kPW independent parent / offset / first-edge chains in flight;
       // vertices not settled by their first 4 in-edges continue one by one
-      constexpr int kPW = 2;
+      constexpr int kPW = GI_BFS_KPW;
       for (int64_t wd0 = (blockIdx.x * (int64_t)kFW + w) * kPW; wd0 < words; wd0 += G * kFW * kPW) {
         int64_t v[kPW], e[kPW], e1[kPW];
         bool open[kPW], found[kPW];
@@ -271,7 +289,7 @@ __global__ void __launch_bounds__(kFT, 1) k_bfs_fused(FusedArgs<OffT> A) {
           for (int k = 0; k < 4; ++k)
             if (!found[j] && u[j][k] != 0xffffffffu && in_frontier(u[j][k])) {
               A.stamp[v[j]] = A.epoch;
-              emit(v[j], (int32_t)u[j][k]);
+              fdeg += emit(v[j], (int32_t)u[j][k]);
               found[j] = true;
             }
           for (int64_t ee = e[j] + 4; ee < e1[j] && !found[j]; ee += 4) {
@@ -283,7 +301,7 @@ __global__ void __launch_bounds__(kFT, 1) k_bfs_fused(FusedArgs<OffT> A) {
             for (int k = 0; k < 4; ++k)
               if (!found[j] && x[k] != 0xffffffffu && in_frontier(x[k])) {
                 A.stamp[v[j]] = A.epoch;
-                emit(v[j], (int32_t)x[k]);
+                fdeg += emit(v[j], (int32_t)x[k]);
                 found[j] = true;
               }
           }
@@ -292,10 +310,7 @@ __global__ void __launch_bounds__(kFT, 1) k_bfs_fused(FusedArgs<OffT> A) {
         for (int j = 0; j < kPW; ++j) {
           const unsigned mask = __ballot_sync(0xffffffffu, found[j]);
           if (lane == 0 && wd0 + j < words) bnext[wd0 + j] = mask;
-          if (found[j]) {
-            fcnt += 1;
-            fdeg += __ldg(&A.outdeg[v[j]]);
-          }
+          if (found[j]) fcnt += 1;
         }
       }
       qvalid = false;
@@ -337,8 +352,7 @@ __global__ void __launch_bounds__(kFT, 1) k_bfs_fused(FusedArgs<OffT> A) {
         bool won = false;
         if (valid) won = claim(v);
         if (won) {
-          fdeg += __ldg(&A.outdeg[v]);
-          emit(v, u);
+          fdeg += emit(v, u);
         }
         if (to_bm) {
           if (won) {
@@ -380,7 +394,7 @@ __global__ void __launch_bounds__(kFT, 1) k_bfs_fused(FusedArgs<OffT> A) {
             for (int j = 0; j < 4; ++j)
               if (pv[j] != A.epoch && atomicCAS(&A.stamp[v[j]], pv[j], A.epoch) == pv[j]) {
                 wmask |= 1u << j;
-                emit(v[j], u);
+                fdeg += emit(v[j], u);
               }
             const int mine = __popc(wmask);
             int incl = mine;
@@ -398,7 +412,6 @@ __global__ void __launch_bounds__(kFT, 1) k_bfs_fused(FusedArgs<OffT> A) {
               for (int j = 0; j < 4; ++j)
                 if ((wmask >> j) & 1u) {
                   qnext[pos++] = v[j];
-                  fdeg += __ldg(&A.outdeg[v[j]]);
                 }
             }
           }
@@ -550,6 +563,7 @@ __global__ void __launch_bounds__(kFT, 1) k_bfs_fused(FusedArgs<OffT> A) {
       if (x) atomicAdd((unsigned long long*)&A.state[7], (unsigned long long)x);
     }
     if (timed) A.times[3 * level + 1] = gtimer();
+    if (A.ctimes && tid == 0 && level < 16) A.ctimes[level * G + blockIdx.x] = gtimer();
     grid.sync();
     if (timed) A.times[3 * level + 2] = gtimer();
     ++level;
@@ -575,6 +589,12 @@ __global__ void k_stamp_init(const OffT* __restrict__ csc_off, int64_t n, uint32
     stamp[v] = csc_off[v + 1] == csc_off[v] ? kNever : 0u;
 }
 
+__global__ void k_vinfo(const int32_t* __restrict__ perm, const int32_t* __restrict__ outdeg, int64_t n,
+                        int2* __restrict__ vinfo) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x)
+    vinfo[v] = make_int2(perm ? perm[v] : (int32_t)v, outdeg[v]);
+}
+
 // one-time per graph: buffers, dynamic shared memory, co-resident grid size
 template <typename OffT>
 static gi_status fused_setup(gi_graph g) {
@@ -585,6 +605,9 @@ static gi_status fused_setup(gi_graph g) {
   GI_TRY(F.stamp.alloc((n + 1) * sizeof(uint32_t)));
   k_stamp_init<OffT><<<grid_for(n, 256, ctx->num_sms), 256, 0, ctx->stream>>>(g->csc_off.as<OffT>(), n,
                                                                               F.stamp.as<uint32_t>());
+  GI_TRY(F.vinfo.alloc((n + 1) * sizeof(int2)));
+  k_vinfo<<<grid_for(n, 256, ctx->num_sms), 256, 0, ctx->stream>>>(g->relabeled ? g->perm.as<int32_t>() : nullptr,
+                                                                  g->outdeg.as<int32_t>(), n, F.vinfo.as<int2>());
   GI_CUDA(cudaGetLastError());
   F.epoch = 0;
   for (int k = 0; k < 2; ++k) GI_TRY(F.q[k].alloc((n + 1) * sizeof(int32_t)));
@@ -597,7 +620,9 @@ static gi_status fused_setup(gi_graph g) {
   GI_CUDA(cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, ctx->device));
   cudaFuncAttributes fa{};
   GI_CUDA(cudaFuncGetAttributes(&fa, k_bfs_fused<OffT>));
-  int dyn = std::min(optin, per_sm / 2) - (int)fa.sharedSizeBytes - 2048;
+  // shared memory vs L1: the rest of the 256 KB stays L1, which the random
+  // gathers (offsets, vinfo, register spills) of every level lean on
+  int dyn = std::min(optin, per_sm / GI_BFS_SMEM_DIV) - (int)fa.sharedSizeBytes - 2048;
   dyn = std::max(dyn, (int)sizeof(FSmem)) & ~15;
   GI_CUDA(cudaFuncSetAttribute(k_bfs_fused<OffT>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
   int bpm = 0;
@@ -622,6 +647,7 @@ static FusedArgs<OffT> fused_args(gi_graph g, const gi_bfs_opts& o, int32_t* d_o
   A.outdeg = g->outdeg.as<int32_t>();
   A.stamp = F.stamp.as<uint32_t>();
   A.inv = g->relabeled ? g->inv.as<int32_t>() : nullptr;
+  A.vinfo = F.vinfo.as<int2>();
   A.fresh = 0;
   A.out = d_out;
   A.perm = g->relabeled ? g->perm.as<int32_t>() : nullptr;
@@ -640,6 +666,7 @@ static FusedArgs<OffT> fused_args(gi_graph g, const gi_bfs_opts& o, int32_t* d_o
   A.policy = o.policy;
   A.sw = (int)std::min<int64_t>(words, (int64_t)((F.dyn) / 4));
   A.times = nullptr;
+  A.ctimes = nullptr;
   A.max_times = 0;
   return A;
 }
@@ -683,12 +710,15 @@ static gi_status bfs_fused_t(gi_graph g, int32_t source, const gi_bfs_opts& o, i
   }
   FusedArgs<OffT> A = fused_args<OffT>(g, o, d_out);
   static const char* dbg = getenv("GI_DEBUG_BFS_FUSED");  // diagnostics: per-level timeline file
-  DevBuf tbuf;
+  DevBuf tbuf, cbuf;
   if (dbg) {
     A.max_times = 1 << 16;
     GI_TRY(tbuf.alloc((size_t)3 * A.max_times * sizeof(unsigned long long)));
     GI_CUDA(cudaMemsetAsync(tbuf.p, 0, (size_t)3 * A.max_times * sizeof(unsigned long long), st));
     A.times = tbuf.as<unsigned long long>();
+    GI_TRY(cbuf.alloc((size_t)16 * F.grid * sizeof(unsigned long long)));
+    GI_CUDA(cudaMemsetAsync(cbuf.p, 0, (size_t)16 * F.grid * sizeof(unsigned long long), st));
+    A.ctimes = cbuf.as<unsigned long long>();
   }
   GI_TRY(fused_start<OffT>(g, source, A));
   // full grid; high-diameter stretches continue on a small grid (cheaper grid barriers)
@@ -710,11 +740,22 @@ static gi_status bfs_fused_t(gi_graph g, int32_t source, const gi_bfs_opts& o, i
   if (dbg) {
     std::vector<unsigned long long> ht((size_t)3 * A.max_times);
     GI_CUDA(cudaMemcpy(ht.data(), tbuf.p, ht.size() * 8, cudaMemcpyDeviceToHost));
+    std::vector<unsigned long long> hc((size_t)16 * F.grid);
+    GI_CUDA(cudaMemcpy(hc.data(), cbuf.p, hc.size() * 8, cudaMemcpyDeviceToHost));
     if (FILE* f = fopen(dbg, "a")) {
-      for (int l = 0; l < A.max_times && ht[3 * l]; ++l)
-        fprintf(f, "src=%d level=%d work_us=%.2f barrier_us=%.2f\n", source, l,
+      for (int l = 0; l < A.max_times && ht[3 * l]; ++l) {
+        fprintf(f, "src=%d level=%d work_us=%.2f barrier_us=%.2f", source, l,
                 ht[3 * l + 1] ? (ht[3 * l + 1] - ht[3 * l]) / 1e3 : 0.0,
                 ht[3 * l + 2] ? (ht[3 * l + 2] - ht[3 * l + 1]) / 1e3 : 0.0);
+        if (l < 16 && ht[3 * l + 1]) {  // per-CTA work time: min / median / max
+          std::vector<double> w;
+          for (int c = 0; c < F.grid; ++c)
+            if (hc[(size_t)l * F.grid + c]) w.push_back((hc[(size_t)l * F.grid + c] - ht[3 * l]) / 1e3);
+          std::sort(w.begin(), w.end());
+          if (!w.empty()) fprintf(f, " cta_work_us min=%.2f med=%.2f max=%.2f", w.front(), w[w.size() / 2], w.back());
+        }
+        fprintf(f, "\n");
+      }
       fclose(f);
     }
   }

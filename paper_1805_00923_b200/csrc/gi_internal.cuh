@@ -142,6 +142,7 @@ struct gi_graph_s {
     bool ready = false;
     int dyn = 0, grid = 0;
     gi::DevBuf stamp, q[2], bm[3], cnt, pre, ctot;  // stamp[v] == epoch: visited by the current source
+    gi::DevBuf vinfo;                                // int2 {input id, out-degree} per internal id
     uint32_t epoch = 0;
   } fused;
   unsigned bfs_epoch = 0;
