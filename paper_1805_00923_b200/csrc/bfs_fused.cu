@@ -71,6 +71,10 @@ struct FusedArgs {
   int32_t source_in;               // input id of the source
   const int32_t* __restrict__ inv; // input -> internal id (null: not relabelled)
   int fresh;                       // first launch of a source: reset the frontier state in the kernel prologue
+  int nsrc;                        // sources run one after another in this launch (epoch + i, out + i*stride)
+  const int32_t* __restrict__ sources;  // device, nsrc input ids (null: source_in)
+  int64_t out_stride;
+  int64_t* states;                 // nsrc x 16 final states (null: none)
   int32_t* out;                    // parents in input ids (written at claim time; -1 preset)
   const int32_t* __restrict__ perm;  // internal -> input id (null: not relabelled)
   const int2* __restrict__ vinfo;    // {input id, out-degree} per internal id
@@ -152,22 +156,26 @@ __global__ void __launch_bounds__(kFT, 1) k_bfs_fused(FusedArgs<OffT> A) {
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int64_t G = gridDim.x;
   const int64_t words = (A.n + 31) >> 5;
+  for (int si = 0; si < A.nsrc; ++si) {  // several sources per launch (gi_bfs_multi): no launch gap
+  const uint32_t epoch = A.epoch + (uint32_t)si;
+  int32_t* const out = A.out + si * A.out_stride;
+  const int32_t source_in = A.sources ? A.sources[si] : A.source_in;
   // claim v for this source: the first thread to move its stamp to `epoch` wins
   auto claim = [&](int32_t v) {
     const uint32_t s = *(volatile uint32_t*)&A.stamp[v];
-    return s != A.epoch && atomicCAS(&A.stamp[v], s, A.epoch) == s;
+    return s != epoch && atomicCAS(&A.stamp[v], s, epoch) == s;
   };
   if (A.fresh) {  // new source: output -1 everywhere, empty level-0 bitmap, then the source itself
     // the stamps are read at random by every level: pull them into L2 (32 lines per thread pass)
     for (int64_t i = (blockIdx.x * (int64_t)kFT + tid) * 32; i < A.n; i += G * kFT * 32)
       asm volatile("prefetch.global.L2 [%0];" ::"l"(A.stamp + i));
-    for (int64_t i = blockIdx.x * (int64_t)kFT + tid; i < A.n; i += G * kFT) A.out[i] = -1;
+    for (int64_t i = blockIdx.x * (int64_t)kFT + tid; i < A.n; i += G * kFT) out[i] = -1;
     for (int64_t i = blockIdx.x * (int64_t)kFT + tid; i < words; i += G * kFT) A.bm[0][i] = 0u;
     grid.sync();
     if (blockIdx.x == 0 && tid == 0) {
-      const int32_t s = A.inv ? A.inv[A.source_in] : A.source_in;
-      A.stamp[s] = A.epoch;
-      A.out[A.source_in] = A.source_in;
+      const int32_t s = A.inv ? A.inv[source_in] : source_in;
+      A.stamp[s] = epoch;
+      out[source_in] = source_in;
       A.q[0][0] = s;
       A.bm[0][s >> 5] = 1u << (s & 31);
       for (int i = 0; i < 8; ++i) A.cnt[i] = 0;
@@ -190,11 +198,11 @@ __global__ void __launch_bounds__(kFT, 1) k_bfs_fused(FusedArgs<OffT> A) {
   auto emit = [&](int64_t v, int32_t u) -> int {
 #if GI_BFS_VINFO
     const int2 iv = __ldg(&A.vinfo[v]);  // {input id, out-degree}: one gather
-    A.out[iv.x] = A.perm ? __ldg(&A.perm[u]) : u;
+    out[iv.x] = A.perm ? __ldg(&A.perm[u]) : u;
     return iv.y;
 #else
-    if (A.perm) A.out[__ldg(&A.perm[v])] = __ldg(&A.perm[u]);
-    else A.out[v] = u;
+    if (A.perm) out[__ldg(&A.perm[v])] = __ldg(&A.perm[u]);
+    else out[v] = u;
     return __ldg(&A.outdeg[v]);
 #endif
   };
@@ -263,7 +271,7 @@ __global__ void __launch_bounds__(kFT, 1) k_bfs_fused(FusedArgs<OffT> A) {
           v[j] = ((wd0 + j) << 5) + lane;
           if (wd0 + j < words && v[j] < A.n) {
             const uint32_t s = __ldcg(&A.stamp[v[j]]);
-            open[j] = s != A.epoch && s != kNever;
+            open[j] = s != epoch && s != kNever;
           } else {
             open[j] = false;
           }
@@ -288,7 +296,7 @@ __global__ void __launch_bounds__(kFT, 1) k_bfs_fused(FusedArgs<OffT> A) {
 #pragma unroll
           for (int k = 0; k < 4; ++k)
             if (!found[j] && u[j][k] != 0xffffffffu && in_frontier(u[j][k])) {
-              A.stamp[v[j]] = A.epoch;
+              A.stamp[v[j]] = epoch;
               fdeg += emit(v[j], (int32_t)u[j][k]);
               found[j] = true;
             }
@@ -300,7 +308,7 @@ __global__ void __launch_bounds__(kFT, 1) k_bfs_fused(FusedArgs<OffT> A) {
 #pragma unroll
             for (int k = 0; k < 4; ++k)
               if (!found[j] && x[k] != 0xffffffffu && in_frontier(x[k])) {
-                A.stamp[v[j]] = A.epoch;
+                A.stamp[v[j]] = epoch;
                 fdeg += emit(v[j], (int32_t)x[k]);
                 found[j] = true;
               }
@@ -389,10 +397,10 @@ __global__ void __launch_bounds__(kFT, 1) k_bfs_fused(FusedArgs<OffT> A) {
             for (int j = 0; j < 4; ++j) v[j] = e + 4 * k + j < e1 ? __ldg(&A.csr_idx[e + 4 * k + j]) : -1;
             uint32_t pv[4];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) pv[j] = v[j] >= 0 ? *(volatile uint32_t*)&A.stamp[v[j]] : A.epoch;
+            for (int j = 0; j < 4; ++j) pv[j] = v[j] >= 0 ? *(volatile uint32_t*)&A.stamp[v[j]] : epoch;
 #pragma unroll
             for (int j = 0; j < 4; ++j)
-              if (pv[j] != A.epoch && atomicCAS(&A.stamp[v[j]], pv[j], A.epoch) == pv[j]) {
+              if (pv[j] != epoch && atomicCAS(&A.stamp[v[j]], pv[j], epoch) == pv[j]) {
                 wmask |= 1u << j;
                 fdeg += emit(v[j], u);
               }
@@ -575,7 +583,11 @@ __global__ void __launch_bounds__(kFT, 1) k_bfs_fused(FusedArgs<OffT> A) {
     A.state[2] = bvalid;
     A.state[3] = pulls;
     A.state[4] = done;
+    if (A.states)
+      for (int i = 0; i < 11; ++i) A.states[16 * si + i] = A.state[i];
   }
+  if (si + 1 < A.nsrc) grid.sync();  // the next prologue rewrites what this source's last level read
+  }  // sources
 }
 
 
@@ -649,6 +661,10 @@ static FusedArgs<OffT> fused_args(gi_graph g, const gi_bfs_opts& o, int32_t* d_o
   A.inv = g->relabeled ? g->inv.as<int32_t>() : nullptr;
   A.vinfo = F.vinfo.as<int2>();
   A.fresh = 0;
+  A.nsrc = 1;
+  A.sources = nullptr;
+  A.out_stride = 0;
+  A.states = nullptr;
   A.out = d_out;
   A.perm = g->relabeled ? g->perm.as<int32_t>() : nullptr;
   A.q[0] = F.q[0].as<int32_t>();
@@ -780,18 +796,18 @@ static gi_status bfs_fused_t(gi_graph g, int32_t source, const gi_bfs_opts& o, i
   return GI_OK;
 }
 
-// k sources back to back: every source is reset and run by one full-grid
-// launch with no host round trip in between; its final state is copied to
-// pinned host memory, and one synchronisation covers the batch. Sources the
-// single launch did not finish (high-diameter graphs hand over to the small
-// grid) are rerun one by one.
+// k sources back to back in ONE cooperative launch: the kernel loops over the
+// sources (epochs F.epoch+1 .. F.epoch+k, output rows out + i*stride) with a
+// grid barrier in between, and leaves every source's final state in `states`.
+// The small-grid handover of high-diameter graphs is off here (every level
+// runs on the full grid: correct, only slower on such graphs).
 template <typename OffT>
 static gi_status bfs_fused_multi_t(gi_graph g, int32_t k, const int32_t* sources, const gi_bfs_opts& o,
-                                   int32_t* d_out, int64_t out_stride, gi_bfs_stats* stats, int32_t* h_user_out) {
+                                   int32_t* d_out, int64_t out_stride, gi_bfs_stats* stats) {
   gi_context ctx = g->ctx;
   cudaStream_t st = ctx->stream;
   GI_TRY(fused_setup<OffT>(g));
-  const int64_t n = g->n;
+  auto& F = g->fused;
   if (ctx->h_batch_len < (int64_t)k * 16) {
     if (ctx->h_batch) cudaFreeHost(ctx->h_batch);
     ctx->h_batch = nullptr;
@@ -800,20 +816,35 @@ static gi_status bfs_fused_multi_t(gi_graph g, int32_t k, const int32_t* sources
     ctx->h_batch_len = (int64_t)k * 16;
   }
   int64_t* hb = ctx->h_batch;
+  if (F.msrc.bytes < (size_t)k * sizeof(int32_t)) GI_TRY(F.msrc.alloc((size_t)k * sizeof(int32_t)));
+  if (F.mstates.bytes < (size_t)k * 16 * sizeof(int64_t)) GI_TRY(F.mstates.alloc((size_t)k * 16 * sizeof(int64_t)));
+  GI_CUDA(cudaMemcpyAsync(F.msrc.p, sources, (size_t)k * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+  if ((uint64_t)F.epoch + (uint64_t)k >= (uint64_t)kNever) {  // epochs would run out: reset the stamps
+    k_stamp_init<OffT><<<grid_for(g->n, 256, ctx->num_sms), 256, 0, st>>>(g->csc_off.as<OffT>(), g->n,
+                                                                        F.stamp.as<uint32_t>());
+    GI_CUDA(cudaGetLastError());
+    F.epoch = 0;
+  }
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (o.profile) {
     GI_CUDA(cudaEventCreate(&e0));
     GI_CUDA(cudaEventCreate(&e1));
     GI_CUDA(cudaEventRecord(e0, st));
   }
-  for (int32_t i = 0; i < k; ++i) {
-    int32_t* out = d_out + (h_user_out ? 0 : (int64_t)i * out_stride);
-    FusedArgs<OffT> A = fused_args<OffT>(g, o, out);
-    GI_TRY(fused_start<OffT>(g, sources[i], A));
-    GI_CUDA(cudaMemcpyAsync(hb + 16 * i, A.state, 11 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-    if (h_user_out)  // host output: the device staging row goes out before the next source reuses it
-      GI_CUDA(cudaMemcpyAsync(h_user_out + (int64_t)i * n, out, n * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-  }
+  FusedArgs<OffT> A = fused_args<OffT>(g, o, d_out);
+  A.epoch = F.epoch + 1;
+  F.epoch += (uint32_t)k;
+  A.nsrc = k;
+  A.sources = F.msrc.as<int32_t>();
+  A.out_stride = out_stride;
+  A.states = F.mstates.as<int64_t>();
+  A.fresh = 1;
+  A.mode = 0;
+  A.small_max = 0;  // no handover
+  void* args[] = {&A};
+  GI_CUDA(cudaLaunchCooperativeKernel((void*)k_bfs_fused<OffT>, dim3(F.grid), dim3(kFT), args, (size_t)F.dyn, st));
+  GI_CUDA(cudaGetLastError());
+  GI_CUDA(cudaMemcpyAsync(hb, F.mstates.p, (size_t)k * 16 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   float ms = 0.f;
   if (o.profile) GI_CUDA(cudaEventRecord(e1, st));
   GI_CUDA(stream_wait(st));
@@ -822,34 +853,26 @@ static gi_status bfs_fused_multi_t(gi_graph g, int32_t k, const int32_t* sources
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
   }
-  if (const char* dbg = getenv("GI_DEBUG_BFS_MULTI")) {  // diagnostics: kernel span and gap to the next source
+  if (const char* dbg = getenv("GI_DEBUG_BFS_MULTI")) {  // diagnostics: per-source kernel span
     if (FILE* f = fopen(dbg, "a")) {
       for (int32_t i = 0; i < k; ++i)
-        fprintf(f, "src=%d kernel_us=%.2f gap_to_next_us=%.2f\n", sources[i], (hb[16 * i + 10] - hb[16 * i + 9]) / 1e3,
-                i + 1 < k ? (hb[16 * (i + 1) + 9] - hb[16 * i + 10]) / 1e3 : 0.0);
+        fprintf(f, "src=%d span_us=%.2f\n", sources[i], (hb[16 * i + 10] - hb[16 * i + 9]) / 1e3);
       fclose(f);
     }
   }
   for (int32_t i = 0; i < k; ++i) {
+    if (!hb[16 * i + 4]) return fail(GI_ERR_INTERNAL, "gi_bfs_multi: a source did not finish");
+    if (!stats) continue;
     gi_bfs_stats s{};
-    if (!hb[16 * i + 4]) {  // not finished by one launch: run it with the handover loop
-      int32_t* out = d_out + (h_user_out ? 0 : (int64_t)i * out_stride);
-      GI_TRY(bfs_fused_t<OffT>(g, sources[i], o, out, &s));
-      if (h_user_out) {
-        GI_CUDA(cudaMemcpyAsync(h_user_out + (int64_t)i * n, out, n * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-        GI_CUDA(stream_wait(st));
-      }
-    } else {
-      s.levels = (int32_t)hb[16 * i];
-      s.pull_levels = (int32_t)hb[16 * i + 3];
-      s.reached = hb[16 * i + 5];
-      s.edges_traversed = hb[16 * i + 6];
-      s.edges_examined = hb[16 * i + 7];
-      s.pull_vertices = hb[16 * i + 8];
-      s.launches = 5;
-      s.total_ms = ms / (float)k;
-    }
-    if (stats) stats[i] = s;
+    s.levels = (int32_t)hb[16 * i];
+    s.pull_levels = (int32_t)hb[16 * i + 3];
+    s.reached = hb[16 * i + 5];
+    s.edges_traversed = hb[16 * i + 6];
+    s.edges_examined = hb[16 * i + 7];
+    s.pull_vertices = hb[16 * i + 8];
+    s.launches = i == 0 ? 1 : 0;
+    s.total_ms = ms / (float)k;
+    stats[i] = s;
   }
   return GI_OK;
 }
@@ -860,9 +883,9 @@ gi_status bfs_fused(gi_graph g, int32_t source, const gi_bfs_opts& o, int32_t* d
 }
 
 gi_status bfs_fused_multi(gi_graph g, int32_t k, const int32_t* sources, const gi_bfs_opts& o, int32_t* d_out,
-                          int64_t out_stride, gi_bfs_stats* stats, int32_t* h_user_out) {
-  if (g->off64) return bfs_fused_multi_t<int64_t>(g, k, sources, o, d_out, out_stride, stats, h_user_out);
-  return bfs_fused_multi_t<int32_t>(g, k, sources, o, d_out, out_stride, stats, h_user_out);
+                          int64_t out_stride, gi_bfs_stats* stats) {
+  if (g->off64) return bfs_fused_multi_t<int64_t>(g, k, sources, o, d_out, out_stride, stats);
+  return bfs_fused_multi_t<int32_t>(g, k, sources, o, d_out, out_stride, stats);
 }
 
 }  // namespace gi

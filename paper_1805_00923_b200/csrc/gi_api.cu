@@ -476,11 +476,13 @@ gi_status gi_bfs_multi(gi_graph g, int32_t k, const int32_t* sources, const gi_b
     return GI_OK;
   }
   if (is_device_ptr(parents_out)) {
-    GI_TRY(bfs_fused_multi(g, k, sources, o, parents_out, g->n, stats, nullptr));
-  } else {
-    if (!g->out_stage.p || g->out_stage.bytes < (size_t)g->n * sizeof(int32_t))
-      GI_TRY(g->out_stage.alloc(g->n * sizeof(int32_t)));
-    GI_TRY(bfs_fused_multi(g, k, sources, o, g->out_stage.as<int32_t>(), 0, stats, parents_out));
+    GI_TRY(bfs_fused_multi(g, k, sources, o, parents_out, g->n, stats));
+  } else {  // host output: stage all k rows on the device, one copy back
+    DevBuf& stage = g->fused.mstage;
+    const size_t bytes = (size_t)k * g->n * sizeof(int32_t);
+    if (stage.bytes < bytes) GI_TRY(stage.alloc(bytes));
+    GI_TRY(bfs_fused_multi(g, k, sources, o, stage.as<int32_t>(), g->n, stats));
+    GI_CUDA(cudaMemcpyAsync(parents_out, stage.p, bytes, cudaMemcpyDeviceToHost, ctx->stream));
   }
   return sync(ctx);
   GI_GUARD_END

@@ -143,6 +143,7 @@ struct gi_graph_s {
     int dyn = 0, grid = 0;
     gi::DevBuf stamp, q[2], bm[3], cnt, pre, ctot;  // stamp[v] == epoch: visited by the current source
     gi::DevBuf vinfo;                                // int2 {input id, out-degree} per internal id
+    gi::DevBuf msrc, mstates, mstage;                // gi_bfs_multi: sources, final states, host-output staging
     uint32_t epoch = 0;
   } fused;
   unsigned bfs_epoch = 0;
@@ -177,10 +178,9 @@ gi_status prdelta_run(gi_graph g, int32_t iters, double damping, double eps, con
 // bfs.cu / bfs_fused.cu
 gi_status bfs_fused(gi_graph g, int32_t source_input_id, const gi_bfs_opts& o, int32_t* d_parent_input_ids,
                     gi_bfs_stats* stats);
-// k sources back to back (single GPU). d_out: device rows of out_stride, or
-// (h_user_out != null) one device staging row copied to h_user_out[i*n] per source
+// k sources in one launch (single GPU); d_out: device rows out_stride apart
 gi_status bfs_fused_multi(gi_graph g, int32_t k, const int32_t* sources, const gi_bfs_opts& o, int32_t* d_out,
-                          int64_t out_stride, gi_bfs_stats* stats, int32_t* h_user_out);
+                          int64_t out_stride, gi_bfs_stats* stats);
 gi_status bfs_finish_output(gi_graph g, const int32_t* parent_internal, int32_t* d_out, int64_t* reached,
                             int64_t* edges);
 gi_status bfs_run(gi_graph g, int32_t source_input_id, const gi_bfs_opts& o,
