@@ -322,7 +322,7 @@ def run_ours(args):
                              "per iteration",
                    "bytes_alg_per_launch": ps.bytes_alg_per_iter, "launch_ms": kern_ms,
                    "vertex_ms": ps.vertex_ms / max(ps.edge_launches, 1), "peak_source": peak_src}
-    # BFS (the larger share of the step): one fused launch per source; algorithmic bytes per source =
+    # BFS (the larger share of the step): the fused kernel, per source; algorithmic bytes per source =
     # 4 B per edge examined + 4 B per pull-level vertex check + 8 B per reached vertex (parent + output)
     _, bsp = g.bfs_multi(srcs, out=bfs_out, profile=True)
     bfs_src_ms = sum(b.total_ms for b in bsp) / max(len(bsp), 1)
@@ -330,7 +330,7 @@ def run_ours(args):
     bfs_achieved = bfs_bytes / (bfs_src_ms * 1e-3) / 1e9 if bfs_src_ms > 0 else 0.0
     roofline_bfs = {"bound": "hbm", "achieved": bfs_achieved, "peak": peak, "unit": "GB/s",
                     "frac": bfs_achieved / peak, "traffic": traffic.get("bfs_fused"),
-                    "kernel": "k_bfs_fused (direction-optimising BFS, one cooperative launch per source)",
+                    "kernel": "k_bfs_fused (direction-optimising BFS; gi_bfs_multi: one cooperative launch for all sources)",
                     "bytes_alg_per_launch": bfs_bytes, "launch_ms": bfs_src_ms, "peak_source": peak_src,
                     "edges_examined_per_source": sum(b.edges_examined for b in bsp) / max(len(bsp), 1)}
     roofline = roofline_bfs if bfs_ms > pr_ms else roofline_pr

@@ -53,7 +53,13 @@
 namespace gi {
 namespace {
 
-constexpr int kConsumers = 16;                      // consumer warps (one record each per stage)
+#ifndef GI_SEG_CONSUMERS
+#define GI_SEG_CONSUMERS 16
+#endif
+#ifndef GI_SEG_STAGES
+#define GI_SEG_STAGES 4
+#endif
+constexpr int kConsumers = GI_SEG_CONSUMERS;        // consumer warps (one record each per stage)
 constexpr int kSegThreads = 32 * (kConsumers + 1);  // + one producer warp (TMA)
 constexpr int kLaneE = 16;                          // edge slots per lane (long records)
 constexpr int kChunkE = 32 * kLaneE;                // edge slots per long record
@@ -67,14 +73,20 @@ constexpr int kLMask = kLDst + 4 * kADst;           // long: mask
 static_assert(kLMask + 4 <= kRecBytes, "long record overflows");
 __host__ __device__ constexpr int short_group_bytes(int L) { return 64 * L + 128; }
 __host__ __device__ constexpr int short_groups(int L) { return kRecPayload / short_group_bytes(L); }
-constexpr int kStages = 4;                          // ring depth (stages in flight per CTA)
+constexpr int kStages = GI_SEG_STAGES;              // ring depth (stages in flight per CTA)
 constexpr int kStageBytes = kConsumers * kRecBytes;
 // CTA balance: an initial cost model (in gather slots), then refined from
 // measured per-CTA times over the first kCalibPasses edge passes (seg_rebalance)
 constexpr int kPieceCost = 4;
 constexpr int64_t kUnitCost = 40 * kChunkE;         // a unit start: segment staging + pipeline refill
 constexpr int64_t kDefaultBlockRows = 8 << 20;      // 32 MB accumulator per destination block
-constexpr int kCalibPasses = 3;
+#ifndef GI_SEG_CALIB
+#define GI_SEG_CALIB 3
+#endif
+#ifndef GI_SEG_DAMP
+#define GI_SEG_DAMP 1.0  // fraction of the way each re-balance moves a boundary
+#endif
+constexpr int kCalibPasses = GI_SEG_CALIB;
 
 struct SegArgs {
   const uint8_t* __restrict__ rec;     // kRecBytes per record
@@ -753,6 +765,8 @@ static gi_status seg_rebalance(gi_graph g, const std::vector<unsigned long long>
     const double frac = T[k] > 0.0 ? (target - before) / T[k] : 0.0;
     nc[j] = std::max(nc[j - 1], std::min(hc[k + 1], hc[k] + (int32_t)(frac * len + 0.5)));
   }
+  for (int j = 1; j < ctas; ++j)  // damped move from the old boundary
+    nc[j] = std::max(nc[j - 1], (int32_t)(hc[j] + GI_SEG_DAMP * (nc[j] - hc[j]) + 0.5));
   hc = nc;
   GI_CUDA(cudaMemcpyAsync(g->seg_cta.p, hc.data(), (ctas + 1) * sizeof(int32_t), cudaMemcpyHostToDevice,
                           g->ctx->stream));
