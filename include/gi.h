@@ -102,8 +102,9 @@ enum {
                                      graph would be represented by duplicating
                                      the directed edges" P:3183 [draft] */
   GI_NO_RELABEL = 1u << 4         /* keep input vertex order internally (the
-                                     default relabels by out-degree; results are
-                                     always reported in input ids) */
+                                     default relabels by out-degree when the
+                                     degrees are skewed: max > 32 x mean, on one
+                                     GPU; results are always in input ids) */
 };
 
 /* Builds the edgeset from an edge list ("edges = load(...)"):

@@ -799,8 +799,8 @@ static gi_status bfs_fused_t(gi_graph g, int32_t source, const gi_bfs_opts& o, i
 // k sources back to back in ONE cooperative launch: the kernel loops over the
 // sources (epochs F.epoch+1 .. F.epoch+k, output rows out + i*stride) with a
 // grid barrier in between, and leaves every source's final state in `states`.
-// The small-grid handover of high-diameter graphs is off here (every level
-// runs on the full grid: correct, only slower on such graphs).
+// A source that reaches a long run of small levels (a high-diameter graph)
+// stops there and is rerun alone with the small-grid handover.
 template <typename OffT>
 static gi_status bfs_fused_multi_t(gi_graph g, int32_t k, const int32_t* sources, const gi_bfs_opts& o,
                                    int32_t* d_out, int64_t out_stride, gi_bfs_stats* stats) {
@@ -840,7 +840,6 @@ static gi_status bfs_fused_multi_t(gi_graph g, int32_t k, const int32_t* sources
   A.states = F.mstates.as<int64_t>();
   A.fresh = 1;
   A.mode = 0;
-  A.small_max = 0;  // no handover
   void* args[] = {&A};
   GI_CUDA(cudaLaunchCooperativeKernel((void*)k_bfs_fused<OffT>, dim3(F.grid), dim3(kFT), args, (size_t)F.dyn, st));
   GI_CUDA(cudaGetLastError());
@@ -861,7 +860,12 @@ static gi_status bfs_fused_multi_t(gi_graph g, int32_t k, const int32_t* sources
     }
   }
   for (int32_t i = 0; i < k; ++i) {
-    if (!hb[16 * i + 4]) return fail(GI_ERR_INTERNAL, "gi_bfs_multi: a source did not finish");
+    if (!hb[16 * i + 4]) {  // stopped before a long run of small levels: rerun it with the handover
+      gi_bfs_stats s{};
+      GI_TRY(bfs_fused_t<OffT>(g, sources[i], o, d_out + (int64_t)i * out_stride, &s));
+      if (stats) stats[i] = s;
+      continue;
+    }
     if (!stats) continue;
     gi_bfs_stats s{};
     s.levels = (int32_t)hb[16 * i];

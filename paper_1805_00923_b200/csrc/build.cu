@@ -19,6 +19,7 @@ namespace gi {
 namespace {
 
 constexpr uint64_t kSentinel = ~0ull;
+constexpr double kSkewRatio = 32.0;  // relabel when max out-degree > kSkewRatio x mean out-degree
 
 __global__ void k_validate(const int32_t* __restrict__ src, const int32_t* __restrict__ dst, int64_t m0,
                            int64_t n, int* __restrict__ bad) {
@@ -231,7 +232,23 @@ gi_status build_graph(gi_context ctx, int64_t n, int64_t m0, const int32_t* d_sr
   k_degrees<int64_t><<<grid_for(n, 256, sms), 256, 0, st>>>(off_in.as<int64_t>(), n, g->outdeg.as<int32_t>());
   GI_CUDA(cudaGetLastError());
 
-  // 7. relabel by out-degree (descending, stable)
+  // 7. relabel by out-degree (descending, stable) when the degrees are skewed:
+  // hub sources then form a dense prefix (segment 0 of the segmented pull, the
+  // staged bitmap prefix of the BFS pull). A flat degree distribution (a road
+  // grid) keeps its input order and with it its locality.
+  if (g->relabeled) {
+    DevBuf mx;
+    GI_TRY(mx.alloc(sizeof(int32_t)));
+    size_t b = 0;
+    GI_CUDA(cub::DeviceReduce::Max(nullptr, b, g->outdeg.as<int32_t>(), mx.as<int32_t>(), n, st));
+    GI_TRY(tmp.ensure(b));
+    GI_CUDA(cub::DeviceReduce::Max(tmp.buf.p, b, g->outdeg.as<int32_t>(), mx.as<int32_t>(), n, st));
+    int32_t hmax = 0;
+    GI_CUDA(cudaMemcpyAsync(&hmax, mx.p, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    GI_CUDA(cudaStreamSynchronize(st));
+    const double mean = n > 0 ? (double)m / (double)n : 0.0;
+    g->relabeled = (double)hmax > kSkewRatio * std::max(1.0, mean);
+  }
   const int32_t* inv = nullptr;
   if (g->relabeled) {
     DevBuf rk, rk2, ids;

@@ -110,6 +110,7 @@ struct gi_graph_s {
   gi::DevBuf outdeg;  // int32[n], internal ids
   // pull tiling: first/last row of each merge-path tile (int32 pairs)
   int64_t ntiles = 0;
+  int max_indeg = -1;  // longest CSC row (owned rows), computed on first use
   gi::DevBuf tile_rows;
   // PageRank workspace
   gi::DevBuf contrib[2];  // float[n]

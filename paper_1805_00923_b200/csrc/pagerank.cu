@@ -84,6 +84,73 @@ __global__ void __launch_bounds__(kPullThreads) k_pr_pull(PrArgs A) {
   if (tid == 0 && bs != 0.0) atomicAdd(&A.dbuf[(A.it + 1) % 3], bs);
 }
 
+// ---------------------------------------------------------------- pull, thread per row (flat graphs)
+// Graphs whose rows are all short (max in-degree <= kRowsMaxDeg: a road grid)
+// need no merge-path balancing: every thread sums kRowsPT rows spaced a block
+// apart (independent offset -> index -> contrib chains in flight), the
+// gathers stay local in input order, and the vertex update is fused.
+constexpr int kRowsPT = 4;
+constexpr int kRowsMaxDeg = 64;
+
+template <typename OffT>
+__global__ void __launch_bounds__(256) k_pr_rows(PrArgs A) {
+  __shared__ double sred[32];
+  const OffT* __restrict__ off = static_cast<const OffT*>(A.off);
+  if (blockIdx.x == 0 && threadIdx.x == 0) A.dbuf[(A.it + 2) % 3] = 0.0;
+  const double D = A.uniform ? A.dbuf[A.it % 3] : 0.0;
+  const float dn = (float)(D * A.inv_n);
+  double dpart = 0.0;
+  const int64_t span = (int64_t)blockDim.x * kRowsPT;
+  for (int64_t base = blockIdx.x * span; base < A.n; base += (int64_t)gridDim.x * span) {
+    int64_t a[kRowsPT], b[kRowsPT];
+#pragma unroll
+    for (int k = 0; k < kRowsPT; ++k) {
+      const int64_t r = base + threadIdx.x + (int64_t)k * blockDim.x;
+      a[k] = b[k] = 0;
+      if (r < A.n) {
+        a[k] = (int64_t)off[r];
+        b[k] = (int64_t)off[r + 1];
+      }
+    }
+    // 4 edges of each of the kRowsPT rows per step: 16 independent index loads,
+    // then 16 independent gathers
+    float s[kRowsPT];
+    int64_t len = 0;
+#pragma unroll
+    for (int k = 0; k < kRowsPT; ++k) {
+      s[k] = 0.f;
+      len = max(len, b[k] - a[k]);
+    }
+    for (int64_t j = 0; j < len; j += 4) {
+      int32_t u[kRowsPT][4];
+#pragma unroll
+      for (int k = 0; k < kRowsPT; ++k)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) u[k][q] = a[k] + j + q < b[k] ? __ldg(&A.idx[a[k] + j + q]) : -1;
+#pragma unroll
+      for (int k = 0; k < kRowsPT; ++k)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) s[k] += u[k][q] >= 0 ? __ldg(&A.cin[u[k][q]]) : 0.f;
+    }
+#pragma unroll
+    for (int k = 0; k < kRowsPT; ++k) {
+      const int64_t r = base + threadIdx.x + (int64_t)k * blockDim.x;
+      if (r < A.n) pr_epilogue(A, r, s[k], dn, dpart);
+    }
+  }
+  const double bs = block_sum(dpart, sred);
+  if (threadIdx.x == 0 && bs != 0.0) atomicAdd(&A.dbuf[(A.it + 1) % 3], bs);
+}
+
+template <typename OffT>
+__global__ void k_max_rowlen(const OffT* __restrict__ off, int64_t n, int* __restrict__ out) {
+  int mx = 0;
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x)
+    mx = max(mx, (int)min((int64_t)INT32_MAX, (int64_t)off[r + 1] - (int64_t)off[r]));
+  for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0 && mx) atomicMax(out, mx);
+}
+
 // ---------------------------------------------------------------- push (K5)
 template <typename OffT>
 __global__ void __launch_bounds__(256) k_pr_push(int64_t n, int64_t row0, const OffT* __restrict__ off,
@@ -154,7 +221,12 @@ gi_status pagerank_run(gi_graph g, int32_t iters, double damping, const gi_pr_op
   const bool dist = ctx->nranks > 1;
   gi_pr_stats S{};
   int kernel = o.direction;
-  if (kernel == GI_PR_PULL) kernel = (nr > 0 && ml > 0 && seg_build(g, o.segment_size, o.dst_block) == GI_OK) ? GI_PR_PULL_SEGMENTED : GI_PR_PULL_DIRECT;
+  // auto pull kernel: shared-memory segments for skewed (relabelled) graphs, whose
+  // hubs concentrate the gathers; the direct L2 gather keeps the input order's
+  // locality on flat-degree graphs (a grid's in-neighbours are +-1, +-width)
+  if (kernel == GI_PR_PULL)
+    kernel = (nr > 0 && ml > 0 && g->relabeled && seg_build(g, o.segment_size, o.dst_block) == GI_OK)
+                 ? GI_PR_PULL_SEGMENTED : GI_PR_PULL_DIRECT;
   else if (kernel == GI_PR_PULL_SEGMENTED) {
     if (nr > 0 && ml > 0) GI_TRY(seg_build(g, o.segment_size, o.dst_block));
     else kernel = GI_PR_PULL_DIRECT;
@@ -171,6 +243,19 @@ gi_status pagerank_run(gi_graph g, int32_t iters, double damping, const gi_pr_op
     if (o.direction == GI_PR_PULL && all != 0 && all != ctx->nranks) kernel = GI_PR_PULL_DIRECT;
   }
   S.kernel = kernel;
+  // direct pull: thread-per-row kernel when every row is short, else merge-path tiles
+  if (kernel == GI_PR_PULL_DIRECT && g->max_indeg < 0) {
+    DevBuf mx;
+    GI_TRY(mx.alloc(sizeof(int)));
+    GI_CUDA(cudaMemsetAsync(mx.p, 0, sizeof(int), st));
+    if (g->off64) k_max_rowlen<int64_t><<<grid_for(nr, 256, sms), 256, 0, st>>>(g->csc_off.as<int64_t>(), nr, mx.as<int>());
+    else k_max_rowlen<int32_t><<<grid_for(nr, 256, sms), 256, 0, st>>>(g->csc_off.as<int32_t>(), nr, mx.as<int>());
+    int h = 0;
+    GI_CUDA(cudaMemcpyAsync(&h, mx.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    GI_CUDA(cudaStreamSynchronize(st));
+    g->max_indeg = h;
+  }
+  const bool rows_kernel = kernel == GI_PR_PULL_DIRECT && g->max_indeg <= kRowsMaxDeg;
   const int osz = g->off64 ? 8 : 4;
   S.bytes_alg_per_iter = 4 * ml + (int64_t)(osz + 12) * nr;
   if (n == 0) {
@@ -261,12 +346,15 @@ gi_status pagerank_run(gi_graph g, int32_t iters, double damping, const gi_pr_op
     } else {
       A.tile_rows = g->tile_rows.as<int32_t>();
       A.idx = g->csc_idx.as<int32_t>();
+      const int rgrid = grid_for(ceil_div(nr, kRowsPT), 256, sms, 8);
       if (g->off64) {
         A.off = g->csc_off.as<int64_t>();
-        if (g->ntiles > 0) k_pr_pull<int64_t><<<(unsigned)g->ntiles, kPullThreads, 0, st>>>(A);
+        if (rows_kernel) k_pr_rows<int64_t><<<rgrid, 256, 0, st>>>(A);
+        else if (g->ntiles > 0) k_pr_pull<int64_t><<<(unsigned)g->ntiles, kPullThreads, 0, st>>>(A);
       } else {
         A.off = g->csc_off.as<int32_t>();
-        if (g->ntiles > 0) k_pr_pull<int32_t><<<(unsigned)g->ntiles, kPullThreads, 0, st>>>(A);
+        if (rows_kernel) k_pr_rows<int32_t><<<rgrid, 256, 0, st>>>(A);
+        else if (g->ntiles > 0) k_pr_pull<int32_t><<<(unsigned)g->ntiles, kPullThreads, 0, st>>>(A);
       }
       if (o.profile) GI_CUDA(cudaEventRecord(ev[1], st));
     }

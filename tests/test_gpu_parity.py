@@ -439,12 +439,16 @@ def test_full_config_parity(gi, ctx, full_graphs, cfg_idx):
     assert abs(got.astype(np.float64).sum() - 1.0) < 1e-5  # mass conserved (uniform rule)
     sources = cfg.sources(s, d)[:4].tolist() if cfg.source_seed else [0]
     par = torch.empty(cfg.n, dtype=torch.int32, device="cuda")
-    for src in sources:
+    multi = torch.empty((len(sources), cfg.n), dtype=torch.int32, device="cuda")
+    _, mst = g.bfs_multi(sources, out=multi)  # the call bench.py times
+    for i, src in enumerate(sources):
         _, bs = g.bfs(int(src), out=par)
         depth = oracle.bfs_depth(go, int(src))
-        ok, msg = oracle.validate_bfs(go, int(src), par.cpu().numpy(), depth)
-        assert ok, f"{cfg.name} src={src}: {msg}"
-        assert bs.edges_traversed == oracle.reached_out_edges(go, depth)
+        for what, p, st in (("gi_bfs", par, bs), ("gi_bfs_multi", multi[i], mst[i])):
+            ok, msg = oracle.validate_bfs(go, int(src), p.cpu().numpy(), depth)
+            assert ok, f"{cfg.name} {what} src={src}: {msg}"
+            assert st.edges_traversed == oracle.reached_out_edges(go, depth)
+            assert st.reached == int((depth >= 0).sum())
 
 
 # ---------------------------------------------------------------- PageRankDelta

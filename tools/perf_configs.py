@@ -1,0 +1,84 @@
+#!/usr/bin/env python3
+"""PageRank (20 iterations) and BFS timings of every single-GPU BASELINE config.
+
+    python tools/perf_configs.py [configs...]   (default: 1 2 3 4)
+
+Prints one JSON line per config: build ms, PR ms/iteration and GTEPS, the PR
+kernel chosen, BFS ms/source (gi_bfs_multi) and GTEPS, levels and edges
+examined per source. Inputs are the seeded generators (graphgen), device-resident.
+"""
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import graphgen  # noqa: E402
+from paper_1805_00923_b200 import gi  # noqa: E402
+
+cfgs = [int(a) for a in sys.argv[1:]] or [1, 2, 3, 4]
+ctx = gi.Context(0)
+for ci in cfgs:
+    cfg = graphgen.CONFIGS[ci]
+    if cfg.kind == "rmat" and ci == 4:
+        a, b, c, _ = cfg.abcd
+        ts, td = graphgen.rmat_device(cfg.scale, cfg.edge_factor, a, b, c, cfg.seed)
+        s = d = None
+    else:
+        s, d = cfg.edges()
+        ts, td = torch.from_numpy(s).cuda(), torch.from_numpy(d).cuda()
+    if cfg.source_seed:
+        if s is None:  # device-generated edges: draw the sources on the host from the degree array below
+            srcs = None
+        else:
+            srcs = [int(x) for x in cfg.sources(s, d)]
+    else:
+        srcs = [0]
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    flags = gi.GI_DEFAULT_FLAGS | gi.GI_EDGES_ON_DEVICE | (gi.GI_SYMMETRIZE if cfg.symmetrize else 0)
+    g = gi.Graph(ctx, cfg.n, ts, td, flags)
+    torch.cuda.synchronize()
+    build_ms = (time.perf_counter() - t) * 1e3
+    del ts, td
+    if srcs is None:
+        import numpy as np
+
+        od = g.out_degrees(torch.empty(cfg.n, dtype=torch.int32, device="cuda")).cpu().numpy()
+        cand = np.nonzero(od > 0)[0]  # internal? no: out_degrees are reported in input ids
+        rng = np.random.default_rng(cfg.source_seed)
+        srcs = [int(x) for x in rng.choice(cand, cfg.bfs_sources, replace=False)]
+    out = torch.empty(cfg.n, dtype=torch.float32, device="cuda")
+    t = time.perf_counter()
+    g.pagerank(cfg.pr_iters, cfg.damping, out=out)  # first call builds the layout + calibrates
+    torch.cuda.synchronize()
+    first_pr_ms = (time.perf_counter() - t) * 1e3
+    best = None
+    for _ in range(3):
+        _, st = g.pagerank(cfg.pr_iters, cfg.damping, out=out, profile=True)
+        if best is None or st.total_ms < best.total_ms:
+            best = st
+    par = torch.empty((len(srcs), cfg.n), dtype=torch.int32, device="cuda")
+    g.bfs_multi(srcs, out=par)
+    _, bst = g.bfs_multi(srcs, out=par, profile=True)
+    bfs_ms = sum(x.total_ms for x in bst) / len(bst)
+    trav = sum(x.edges_traversed for x in bst) / len(bst)
+    line = {"config": cfg.name, "n": cfg.n, "m": g.m, "build_ms": round(build_ms, 1),
+            "pr_first_call_ms": round(first_pr_ms, 1), "pr_kernel": {0: "pull", 1: "push", 2: "direct",
+                                                                    3: "segmented"}[best.kernel],
+            "pr_ms_per_iter": round(best.edge_ms / best.edge_launches, 4),
+            "pr_gteps": round(g.m * cfg.pr_iters / (best.total_ms * 1e-3) / 1e9, 1),
+            "pr_roofline_frac": round(best.bytes_alg_per_iter / (best.edge_ms / best.edge_launches * 1e-3) / 1e9
+                                      / json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"], 3)
+            if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else None,
+            "bfs_sources": len(srcs), "bfs_ms_per_source": round(bfs_ms, 4),
+            "bfs_gteps": round(trav / (bfs_ms * 1e-3) / 1e9, 1),
+            "bfs_levels": [x.levels for x in bst][:4], "bfs_edges_examined_per_source":
+                int(sum(x.edges_examined for x in bst) / len(bst))}
+    print(json.dumps(line), flush=True)
+    g.close()
+    torch.cuda.empty_cache()
