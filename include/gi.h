@@ -229,8 +229,12 @@ typedef struct {
                             the first level as push: a 1-vertex frontier) */
   int32_t threshold_div; /* 0 -> 20 */
   int32_t profile;       /* 1: fill timing fields of gi_bfs_stats */
-  int32_t reserved;
+  int32_t batch;         /* gi_bfs_multi only: GI_BFS_BATCH_AUTO (0),
+                            GI_BFS_BATCH_PER_SOURCE (one direction-optimising
+                            traversal per source) or GI_BFS_BATCH_BITPARALLEL
+                            (up to 64 sources per traversal, one bit each) */
 } gi_bfs_opts;
+enum { GI_BFS_BATCH_AUTO = 0, GI_BFS_BATCH_PER_SOURCE = 1, GI_BFS_BATCH_BITPARALLEL = 2 };
 
 typedef struct {
   int32_t levels;          /* frontier rounds executed */
@@ -250,14 +254,19 @@ GI_API gi_status gi_bfs_ex(gi_graph g, int32_t source, const gi_bfs_opts* opts, 
                     gi_bfs_stats* stats /* may be NULL */);
 
 /* k independent BFS runs (the multi-source workloads of BASELINE configs
- * 2/4/5), identical in result to k gi_bfs_ex calls with the same options:
+ * 2/4/5), each a valid BFS tree of its source as k gi_bfs_ex calls give
+ * (depths identical; a vertex may get another, equally valid parent, R8):
  *   sources:     int32[k] in input ids, HOST memory;
  *   parents_out: int32[k][n] (row i = parents of sources[i], layout as
  *                gi_bfs), host or device;
  *   stats:       gi_bfs_stats[k] or NULL (with profile=1, total_ms is the
  *                batch time divided by k).
- * On one GPU the runs are issued back to back with a single host
- * synchronisation; on several GPUs this is a loop of gi_bfs_ex.
+ * On one GPU, opts->batch selects per-source traversals (all sources in one
+ * cooperative launch) or the bit-parallel traversal (edgeset.apply over a
+ * 64-bit frontier mask per vertex: one pass over an edge serves 64 sources);
+ * AUTO takes the bit-parallel form for k >= 8. With BITPARALLEL, stats
+ * report the shared edge reads divided by the sources of the pass. On several
+ * GPUs this is a loop of gi_bfs_ex.
  * Errors as gi_bfs_ex (checked for every source before any run); k = 0 -> GI_OK. */
 GI_API gi_status gi_bfs_multi(gi_graph g, int32_t k, const int32_t* sources, const gi_bfs_opts* opts,
                               int32_t* parents_out, gi_bfs_stats* stats /* may be NULL */);

@@ -459,8 +459,10 @@ gi_status gi_bfs_multi(gi_graph g, int32_t k, const int32_t* sources, const gi_b
       return fail(GI_ERR_VERTEX_OUT_OF_RANGE, "gi_bfs_multi: a source is not in [0, n)");
   gi_bfs_opts o{};
   if (opts) o = *opts;
-  if (o.policy < GI_BFS_AUTO || o.policy > GI_BFS_PULL_ONLY || o.threshold_div < 0)
+  if (o.policy < GI_BFS_AUTO || o.policy > GI_BFS_PULL_ONLY || o.threshold_div < 0 ||
+      o.batch < GI_BFS_BATCH_AUTO || o.batch > GI_BFS_BATCH_BITPARALLEL)
     return fail(GI_ERR_INVALID_ARGUMENT, "gi_bfs_multi: bad options");
+  const bool bitpar = o.batch == GI_BFS_BATCH_BITPARALLEL || (o.batch == GI_BFS_BATCH_AUTO && k >= 8);
   gi_context ctx = g->ctx;
   GI_CUDA(cudaSetDevice(ctx->device));
   static const char* impl = getenv("GI_BFS_IMPL");
@@ -475,13 +477,16 @@ gi_status gi_bfs_multi(gi_graph g, int32_t k, const int32_t* sources, const gi_b
     }
     return GI_OK;
   }
+  auto run = [&](int32_t* rows) {
+    return bitpar ? msbfs_run(g, k, sources, o, rows, stats) : bfs_fused_multi(g, k, sources, o, rows, g->n, stats);
+  };
   if (is_device_ptr(parents_out)) {
-    GI_TRY(bfs_fused_multi(g, k, sources, o, parents_out, g->n, stats));
+    GI_TRY(run(parents_out));
   } else {  // host output: stage all k rows on the device, one copy back
     DevBuf& stage = g->fused.mstage;
     const size_t bytes = (size_t)k * g->n * sizeof(int32_t);
     if (stage.bytes < bytes) GI_TRY(stage.alloc(bytes));
-    GI_TRY(bfs_fused_multi(g, k, sources, o, stage.as<int32_t>(), g->n, stats));
+    GI_TRY(run(stage.as<int32_t>()));
     GI_CUDA(cudaMemcpyAsync(parents_out, stage.p, bytes, cudaMemcpyDeviceToHost, ctx->stream));
   }
   return sync(ctx);

@@ -148,6 +148,12 @@ struct gi_graph_s {
     uint32_t epoch = 0;
   } fused;
   unsigned bfs_epoch = 0;
+  struct {  // bit-parallel multi-source BFS (msbfs.cu)
+    gi::DevBuf seen, fr[2], act[2], cnt, src, heavy, par;
+    int64_t nheavy = 0;  // rows with in-degree >= 32 (pulled by whole warps)
+    gi::DevBuf chunks[2], scan_tmp;  // push: chunk counts / inclusive prefix, cub scan scratch
+    size_t scan_bytes = 0;
+  } ms;
 };
 
 namespace gi {
@@ -182,6 +188,9 @@ gi_status bfs_fused(gi_graph g, int32_t source_input_id, const gi_bfs_opts& o, i
 // k sources in one launch (single GPU); d_out: device rows out_stride apart
 gi_status bfs_fused_multi(gi_graph g, int32_t k, const int32_t* sources, const gi_bfs_opts& o, int32_t* d_out,
                           int64_t out_stride, gi_bfs_stats* stats);
+// msbfs.cu: k sources, 64 per bit-parallel pass; d_out: k device rows of n
+gi_status msbfs_run(gi_graph g, int32_t k, const int32_t* sources, const gi_bfs_opts& o, int32_t* d_out,
+                    gi_bfs_stats* stats);
 gi_status bfs_finish_output(gi_graph g, const int32_t* parent_internal, int32_t* d_out, int64_t* reached,
                             int64_t* edges);
 gi_status bfs_run(gi_graph g, int32_t source_input_id, const gi_bfs_opts& o,

@@ -1,0 +1,601 @@
+// msbfs.cu — bit-parallel multi-source BFS: up to 64 sources in one traversal.
+//
+// The batched form of edgeset.apply for the multi-source BFS workloads of
+// BASELINE configs 2/4/5 ("BFS from 64 seeded random sources"): the vertex
+// payload of the BFS frontier (Table 2's
+// edges.from(frontier).to(filter).apply) becomes a 64-bit mask, bit i = "in
+// source i's frontier", so one pass over an edge serves every source. Each
+// source's result is exactly a BFS tree of its own (every bit follows the
+// level-synchronous BFS of its source; parents are in-neighbours one level
+// closer, reading R8). The direction choice per level is the single-source
+// rule (R7) over the union frontier.
+//
+//   seen[v]    bits of the sources that have reached v (levels <= current)
+//   fr[c][v]   bits of the sources whose current frontier holds v
+//   act[c]     the vertices with fr[c][v] != 0 (push levels read it)
+// Per level (direction: pull iff |F| + sum outdeg F > m / 3 — a pull rarely
+// exits early here, since a vertex stops only once it has all k sources):
+//   pull (DensePull + early exit): light rows (in-degree < 32) a thread each,
+//     heavy rows a warp each; a row ORs the frontier masks of its in-neighbours
+//     into the bits it misses, recording for every new bit the in-neighbour
+//     that brought it, and stops once it has every source;
+//   push (SparsePush, edge-balanced): the active vertices' out-edges in chunks
+//     of 256 per warp; an edge claims new bits with atomicOr on seen (the
+//     returned old value says which bits this edge won) and adds them to the
+//     next frontier. Sinks (out-degree 0) never enter the active list.
+// Parents are staged vertex-major (par[v][i], k rounded up to 4 per row) so a
+// vertex's bits land in one 256-byte row; the epilogue transposes them into the
+// k output rows (int32[k][n], input ids; -1 where source i never reached v)
+// and counts, per source, the vertices reached and their out-degrees.
+#include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+#include <cub/cub.cuh>
+
+#include "gi_internal.cuh"
+#include "pr_common.cuh"
+
+namespace gi {
+namespace {
+
+#ifndef GI_MS_OUT
+#define GI_MS_OUT 1  // diagnostics: 0 drops the parent writes
+#endif
+constexpr int kMsT = 256;
+constexpr int64_t kHeavy = 32;  // rows with at least this many in-edges are pulled by whole warps
+constexpr int kMsPullDiv = 3;
+constexpr int kPushChunk = 256;
+#ifndef GI_MS_BATCH
+#define GI_MS_BATCH 4
+#endif
+constexpr int kPullBatch = GI_MS_BATCH;  // in-edge gathers in flight per pull step  // out-edges per push work item   // bit-parallel direction rule: pull iff |F| + sum outdeg F > m / 3
+
+struct MsArgs {
+  int64_t n;
+  const void* csr_off;
+  const int32_t* __restrict__ csr_idx;
+  const void* csc_off;
+  const int32_t* __restrict__ csc_idx;
+  const int32_t* __restrict__ outdeg;
+  const int32_t* __restrict__ perm;  // internal -> input id (null: not relabelled)
+  const int32_t* __restrict__ inv;   // input -> internal id
+  unsigned long long* seen;
+  const unsigned long long* __restrict__ fcur;
+  unsigned long long* fnext;
+  const int32_t* __restrict__ acur;  // active vertices of the current level (push)
+  int32_t* anext;                    // active vertices of the next level
+  unsigned long long* cnt;           // [0] |active next|, [1] sum outdeg, [2] OR of new bits, [3] edges examined
+  int32_t* par;                      // parents, vertex-major by input id: par[input id * kp + source bit]
+  int kp;                            // par row stride: k rounded up to a multiple of 4
+  int64_t nact;
+  unsigned long long all;            // mask of the k sources
+};
+
+__device__ __forceinline__ int32_t in_id(const MsArgs& A, int32_t v) { return A.perm ? __ldg(&A.perm[v]) : v; }
+
+// CTA-aggregated append of the active vertices (one atomic per CTA round)
+__device__ __forceinline__ void ms_append(const MsArgs& A, bool act, int32_t v, int* s_cnt, long long* s_base) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const unsigned mask = __ballot_sync(0xffffffffu, act);
+  if (lane == 0) s_cnt[w] = __popc(mask);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int tot = 0;
+    for (int i = 0; i < kMsT / 32; ++i) {
+      const int c = s_cnt[i];
+      s_cnt[i] = tot;
+      tot += c;
+    }
+    *s_base = tot ? (long long)atomicAdd(&A.cnt[0], (unsigned long long)tot) : 0;
+  }
+  __syncthreads();
+  if (act) A.anext[*s_base + s_cnt[w] + __popc(mask & ((1u << lane) - 1u))] = v;
+}
+
+// the level's counters (cnt[1..3]), reduced over the CTA once at kernel end;
+// every thread of the CTA calls it
+__device__ __forceinline__ void ms_counters(const MsArgs& A, long long deg, unsigned long long bits, long long exam) {
+  __shared__ unsigned long long s_red[3 * (kMsT / 32)];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int o = 16; o > 0; o >>= 1) {
+    deg += __shfl_xor_sync(0xffffffffu, deg, o);
+    bits |= __shfl_xor_sync(0xffffffffu, bits, o);
+    exam += __shfl_xor_sync(0xffffffffu, exam, o);
+  }
+  if (lane == 0) {
+    s_red[3 * w] = (unsigned long long)deg;
+    s_red[3 * w + 1] = bits;
+    s_red[3 * w + 2] = (unsigned long long)exam;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long d = 0, b = 0, x = 0;
+    for (int i = 0; i < kMsT / 32; ++i) {
+      d += s_red[3 * i];
+      b |= s_red[3 * i + 1];
+      x += s_red[3 * i + 2];
+    }
+    if (d) atomicAdd(&A.cnt[1], d);
+    if (b) atomicOr(&A.cnt[2], b);
+    if (x) atomicAdd(&A.cnt[3], x);
+  }
+}
+
+template <typename OffT>
+__global__ void __launch_bounds__(kMsT) k_ms_pull(MsArgs A) {
+  __shared__ int s_cnt[kMsT / 32];
+  __shared__ long long s_base;
+  const OffT* __restrict__ off = static_cast<const OffT*>(A.csc_off);
+  long long tdeg = 0, exam = 0;
+  unsigned long long tbits = 0;
+  for (int64_t b = blockIdx.x * (int64_t)kMsT; b < A.n; b += (int64_t)gridDim.x * kMsT) {
+    const int32_t w = (int32_t)(b + threadIdx.x);
+    bool act = false;
+    unsigned long long found = 0;
+    if (w < A.n) {
+      const int64_t e0 = (int64_t)off[w], e1 = (int64_t)off[w + 1];
+      const unsigned long long s = e1 - e0 >= kHeavy ? A.all : A.seen[w];  // heavy rows: k_ms_pull_heavy
+      if (s != A.all) {
+        int32_t wi = -1;  // input id of w, looked up at its first new bit
+        for (int64_t e = e0; e < e1; e += kPullBatch) {  // kPullBatch independent gathers per step
+          int32_t v[kPullBatch];
+          unsigned long long f[kPullBatch];
+#pragma unroll
+          for (int j = 0; j < kPullBatch; ++j) v[j] = e + j < e1 ? __ldg(&A.csc_idx[e + j]) : -1;
+#pragma unroll
+          for (int j = 0; j < kPullBatch; ++j) f[j] = v[j] >= 0 ? A.fcur[v[j]] : 0ull;
+          exam += min((int64_t)kPullBatch, e1 - e);
+#pragma unroll
+          for (int j = 0; j < kPullBatch; ++j) {
+            const unsigned long long m = f[j] & ~s & ~found;
+            if (m) {
+              const int32_t vin = in_id(A, v[j]);
+              if (wi < 0) wi = in_id(A, w);
+              if (GI_MS_OUT)
+                for (unsigned long long x = m; x; x &= x - 1) A.par[(int64_t)wi * A.kp + __ffsll((long long)x) - 1] = vin;
+              found |= m;
+            }
+          }
+          if ((s | found) == A.all) break;
+        }
+        if (found) {
+          A.seen[w] = s | found;
+          const int32_t deg = __ldg(&A.outdeg[w]);
+          act = deg > 0;  // a sink never pushes: it stays out of the active list
+          tdeg += deg;
+          tbits |= found;
+        }
+      }
+      if (e1 - e0 < kHeavy) A.fnext[w] = found;
+    }
+    ms_append(A, act, w, s_cnt, &s_base);
+  }
+  ms_counters(A, tdeg, tbits, exam);
+}
+
+// pull for the heavy rows (in-degree >= kHeavy): a warp per row, 32 in-edges
+// per step, kPullBatch steps' gathers in flight; the bits a step brings are
+// split among its lanes by an exclusive prefix OR (each new bit's parent is
+// the lowest lane holding it)
+template <typename OffT>
+__global__ void __launch_bounds__(kMsT) k_ms_pull_heavy(MsArgs A, const int32_t* __restrict__ heavy, int64_t nh) {
+  __shared__ int s_cnt[kMsT / 32];
+  __shared__ long long s_base;
+  const OffT* __restrict__ off = static_cast<const OffT*>(A.csc_off);
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t)gridDim.x * (kMsT / 32);
+  const int64_t rounds = (nh + nw - 1) / nw;
+  long long tdeg = 0, exam = 0;
+  unsigned long long tbits = 0;
+  for (int64_t r = 0; r < rounds; ++r) {
+    const int64_t i = r * nw + blockIdx.x * (kMsT / 32) + (threadIdx.x >> 5);
+    bool act = false;
+    int32_t w = 0;
+    unsigned long long found = 0;
+    if (i < nh) {
+      w = __ldg(&heavy[i]);
+      const unsigned long long s = A.seen[w];
+      if (s != A.all) {
+        const int32_t wi = in_id(A, w);
+        const int64_t e0 = (int64_t)off[w], e1 = (int64_t)off[w + 1];
+        for (int64_t b = e0; b < e1; b += 32 * kPullBatch) {
+          int32_t v[kPullBatch];
+          unsigned long long f[kPullBatch];
+#pragma unroll
+          for (int j = 0; j < kPullBatch; ++j) {
+            const int64_t e = b + 32 * j + lane;
+            v[j] = e < e1 ? __ldg(&A.csc_idx[e]) : -1;
+          }
+#pragma unroll
+          for (int j = 0; j < kPullBatch; ++j) f[j] = v[j] >= 0 ? A.fcur[v[j]] : 0ull;
+          if (lane == 0) exam += min((int64_t)32 * kPullBatch, e1 - b);
+#pragma unroll
+          for (int j = 0; j < kPullBatch; ++j) {
+            const unsigned long long m = f[j] & ~s & ~found;
+            if (__ballot_sync(0xffffffffu, m != 0) == 0) continue;
+            unsigned long long x = m;  // inclusive prefix OR over lanes
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+              const unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
+              if (lane >= o) x |= y;
+            }
+            unsigned long long below = __shfl_up_sync(0xffffffffu, x, 1);
+            if (lane == 0) below = 0;
+            const unsigned long long mine = m & ~below;
+            if (mine) {
+              const int32_t vin = in_id(A, v[j]);
+              if (GI_MS_OUT)
+                for (unsigned long long q = mine; q; q &= q - 1) A.par[(int64_t)wi * A.kp + __ffsll((long long)q) - 1] = vin;
+            }
+            found |= __shfl_sync(0xffffffffu, x, 31);
+          }
+          if ((s | found) == A.all) break;
+        }
+        if (found && lane == 0) A.seen[w] = s | found;
+      }
+      if (lane == 0) A.fnext[w] = found;
+      if (found && lane == 0) {
+        const int32_t deg = __ldg(&A.outdeg[w]);
+        act = deg > 0;
+        tdeg += deg;
+        tbits |= found;
+      }
+    }
+    ms_append(A, act, w, s_cnt, &s_base);
+  }
+  ms_counters(A, tdeg, tbits, exam);
+}
+
+// the heavy rows (in-degree >= kHeavy), appended in any order
+template <typename OffT>
+__global__ void k_ms_heavy_list(const OffT* __restrict__ off, int64_t n, int32_t* __restrict__ list,
+                                unsigned long long* __restrict__ cnt) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x)
+    if ((int64_t)off[v + 1] - (int64_t)off[v] >= kHeavy) list[atomicAdd(cnt, 1ull)] = (int32_t)v;
+}
+
+// chunk counts of the active vertices for the edge-balanced push
+__global__ void k_ms_chunks(const int32_t* __restrict__ act, int64_t nact, const int32_t* __restrict__ outdeg,
+                            int32_t* __restrict__ cc) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nact; i += (int64_t)gridDim.x * blockDim.x)
+    cc[i] = (__ldg(&outdeg[__ldg(&act[i])]) + kPushChunk - 1) / kPushChunk;
+}
+
+// push, edge-balanced: the active vertices' out-edges are cut into chunks of
+// kPushChunk (cp = inclusive prefix of the chunk counts) and every warp takes
+// a contiguous run of chunks, so a hub's edges spread over many warps
+template <typename OffT>
+__global__ void __launch_bounds__(kMsT) k_ms_push(MsArgs A, const int32_t* __restrict__ cp) {
+  __shared__ int32_t s_buf[kMsT / 32][64];  // per-warp staging of the vertices joining the next frontier
+  const OffT* __restrict__ off = static_cast<const OffT*>(A.csr_off);
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+  int nbuf = 0;
+  const int64_t nw = (int64_t)gridDim.x * (kMsT / 32);
+  const int64_t gw = blockIdx.x * (int64_t)(kMsT / 32) + wp;
+  long long deg = 0, exam = 0;
+  unsigned long long bits = 0;
+  const int64_t C = A.nact > 0 ? (int64_t)__ldg(&cp[A.nact - 1]) : 0;
+  const int64_t per = (C + nw - 1) / nw;
+  int64_t c = gw * per;
+  const int64_t cend = min(C, c + per);
+  if (c < cend) {
+    int64_t i = 0, hi = A.nact;  // first active vertex whose chunks reach past c
+    while (i < hi) {
+      const int64_t mid = (i + hi) >> 1;
+      if ((int64_t)__ldg(&cp[mid]) <= c) i = mid + 1;
+      else hi = mid;
+    }
+    for (; c < cend; ++i) {
+      const int64_t before = i ? (int64_t)__ldg(&cp[i - 1]) : 0;
+      const int64_t ce = min((int64_t)__ldg(&cp[i]), cend) - before;
+      const int32_t u = __ldg(&A.acur[i]);
+      const int64_t u0 = (int64_t)off[u], u1 = (int64_t)off[u + 1];
+      const int64_t e0 = u0 + (c - before) * kPushChunk, e1 = min(u1, u0 + ce * kPushChunk);
+      c = before + ce;
+      if (e0 >= e1) continue;
+      const unsigned long long mu = A.fcur[u];
+      const int32_t uin = in_id(A, u);
+      for (int64_t base = e0; base < e1; base += 32) {  // warp-uniform steps of 32 out-edges
+        const int64_t e = base + lane;
+        bool newact = false;
+        int32_t w = 0;
+        if (e < e1) {
+          w = __ldg(&A.csr_idx[e]);
+          ++exam;
+          const unsigned long long m = mu & ~*(volatile unsigned long long*)&A.seen[w];
+          if (m) {
+            const unsigned long long got = m & ~atomicOr(&A.seen[w], m);  // the bits this edge claims
+            if (got) {
+              const int32_t win = in_id(A, w);
+              if (GI_MS_OUT)
+                for (unsigned long long x = got; x; x &= x - 1) A.par[(int64_t)win * A.kp + __ffsll((long long)x) - 1] = uin;
+              bits |= got;
+              if (atomicOr(&A.fnext[w], got) == 0ull) {  // w's first bits this level: it joins the next frontier
+                const int32_t dw = __ldg(&A.outdeg[w]);
+                newact = dw > 0;  // sinks stay out of the active list
+                deg += dw;
+              }
+            }
+          }
+        }
+        const unsigned am = __ballot_sync(0xffffffffu, newact);
+        if (am) {
+          if (newact) s_buf[wp][nbuf + __popc(am & ((1u << lane) - 1u))] = w;
+          nbuf += __popc(am);
+          if (nbuf >= 32) {  // one atomic per 32 appended vertices
+            __syncwarp();
+            unsigned long long pos = 0;
+            if (lane == 0) pos = atomicAdd(&A.cnt[0], 32ull);
+            pos = __shfl_sync(0xffffffffu, pos, 0);
+            A.anext[pos + lane] = s_buf[wp][lane];
+            __syncwarp();
+            nbuf -= 32;
+            if (lane < nbuf) s_buf[wp][lane] = s_buf[wp][32 + lane];
+            __syncwarp();
+          }
+        }
+      }
+    }
+  }
+  __syncwarp();
+  if (nbuf > 0) {
+    unsigned long long pos = 0;
+    if (lane == 0) pos = atomicAdd(&A.cnt[0], (unsigned long long)nbuf);
+    pos = __shfl_sync(0xffffffffu, pos, 0);
+    if (lane < nbuf) A.anext[pos + lane] = s_buf[wp][lane];
+  }
+  ms_counters(A, deg, bits, exam);
+}
+
+// sources: bit i at source i (internal id), its own parent in row i, active list
+__global__ void k_ms_init(const int32_t* __restrict__ src_in, int k, const int32_t* __restrict__ inv, int64_t n,
+                          const int32_t* __restrict__ outdeg, unsigned long long* seen, unsigned long long* f0,
+                          int32_t* act, unsigned long long* cnt, int32_t* par, int kp) {
+  const int i = threadIdx.x;
+  if (i >= k) return;
+  const int32_t si = src_in[i];
+  const int32_t s = inv ? inv[si] : si;
+  atomicOr(&seen[s], 1ull << i);
+  par[(int64_t)si * kp + i] = si;
+  if (atomicOr(&f0[s], 1ull << i) == 0ull) {
+    act[atomicAdd(&cnt[0], 1ull)] = s;
+    atomicAdd(&cnt[1], (unsigned long long)outdeg[s]);
+  }
+}
+
+// The pass's epilogue, a warp per 32 consecutive input ids v:
+//   out[i][v] = source i's parent of v, or -1 when i never reached v — the
+//     vertex-major parents (8 KB per warp, 16-byte loads) go through a
+//     warp-private shared tile so the k output rows are written coalesced;
+//   per source i: vertices reached and the sum of their out-degrees (R16).
+constexpr int kFinWarps = 8;
+__global__ void __launch_bounds__(32 * kFinWarps) k_ms_finish(const int32_t* __restrict__ par,
+                                                             const unsigned long long* __restrict__ seen,
+                                                             const int32_t* __restrict__ inv,
+                                                             const int32_t* __restrict__ outdeg, int64_t n, int k, int kp,
+                                                             int32_t* __restrict__ out,
+                                                             unsigned long long* __restrict__ reached,
+                                                             unsigned long long* __restrict__ edges) {
+  extern __shared__ int32_t fin_smem[];
+  __shared__ unsigned long long r[64], d[64];
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+  int32_t* tile = fin_smem + wp * (64 * 33);  // [source][vertex], padded
+  for (int i = threadIdx.x; i < 64; i += blockDim.x) r[i] = d[i] = 0;
+  __syncthreads();
+  unsigned long long r0 = 0, r1 = 0, d0 = 0, d1 = 0;
+  const int64_t nw = (int64_t)gridDim.x * kFinWarps;
+  for (int64_t t = blockIdx.x * (int64_t)kFinWarps + wp; t * 32 < n; t += nw) {
+    const int64_t v0 = t * 32, v = v0 + lane;
+    const int32_t w = v < n ? (inv ? __ldg(&inv[v]) : (int32_t)v) : 0;
+    const unsigned long long sv = v < n ? seen[w] : 0ull;
+    const unsigned long long ov = v < n ? (unsigned long long)__ldg(&outdeg[w]) : 0ull;
+    const int rq = kp >> 2;                                  // int4s per par row
+    const int nq = (int)(n - v0 < 32 ? n - v0 : 32) * rq;  // int4s of the tile's rows (contiguous)
+    const int4* p4 = reinterpret_cast<const int4*>(par + v0 * kp);
+    int4 q[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) q[j] = lane + 32 * j < nq ? __ldg(&p4[lane + 32 * j]) : make_int4(0, 0, 0, 0);
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int qi = lane + 32 * j, vv = qi / rq, b = (qi - vv * rq) * 4;
+      if (qi < nq) {
+        tile[(b + 0) * 33 + vv] = q[j].x;
+        tile[(b + 1) * 33 + vv] = q[j].y;
+        tile[(b + 2) * 33 + vv] = q[j].z;
+        tile[(b + 3) * 33 + vv] = q[j].w;
+      }
+    }
+    __syncwarp();
+    if (v < n)
+      for (int b = 0; b < k; ++b) out[(int64_t)b * n + v] = (sv >> b) & 1ull ? tile[b * 33 + lane] : -1;
+    __syncwarp();
+    if (__ballot_sync(0xffffffffu, sv != 0) == 0) continue;
+#pragma unroll 4
+    for (int j = 0; j < 32; ++j) {
+      const unsigned long long s = __shfl_sync(0xffffffffu, sv, j);
+      const unsigned long long od = __shfl_sync(0xffffffffu, ov, j);
+      const unsigned long long b0 = (s >> lane) & 1ull, b1 = (s >> (lane + 32)) & 1ull;
+      r0 += b0;
+      r1 += b1;
+      d0 += b0 * od;
+      d1 += b1 * od;
+    }
+  }
+  if (r0) { atomicAdd(&r[lane], r0); atomicAdd(&d[lane], d0); }
+  if (r1) { atomicAdd(&r[lane + 32], r1); atomicAdd(&d[lane + 32], d1); }
+  __syncthreads();
+  for (int i = threadIdx.x; i < k; i += blockDim.x) {
+    if (r[i]) atomicAdd(&reached[i], r[i]);
+    if (d[i]) atomicAdd(&edges[i], d[i]);
+  }
+}
+
+template <typename OffT>
+gi_status msbfs_t(gi_graph g, int32_t k, const int32_t* sources, const gi_bfs_opts& o, int32_t* d_out,
+                  gi_bfs_stats* stats) {
+  gi_context ctx = g->ctx;
+  cudaStream_t st = ctx->stream;
+  const int sms = ctx->num_sms;
+  const int64_t n = g->n;
+  auto& M = g->ms;
+  if (!M.seen.p) {
+    GI_TRY(M.seen.alloc((n + 1) * 8));
+    for (int c = 0; c < 2; ++c) {
+      GI_TRY(M.fr[c].alloc((n + 1) * 8));
+      GI_TRY(M.act[c].alloc((n + 1) * 4));
+    }
+    GI_TRY(M.cnt.alloc(4 * 8 + 2 * 64 * 8));
+    GI_TRY(M.src.alloc(64 * 4));
+    GI_TRY(M.heavy.alloc((n + 1) * 4));
+    GI_TRY(M.chunks[0].alloc((n + 1) * 4));
+    GI_TRY(M.chunks[1].alloc((n + 1) * 4));
+    size_t tb = 0;
+    GI_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tb, M.chunks[0].as<int32_t>(), M.chunks[1].as<int32_t>(), (int)n, st));
+    GI_TRY(M.scan_tmp.alloc(tb + 16));
+    M.scan_bytes = tb;
+    GI_CUDA(cudaMemsetAsync(M.cnt.p, 0, 8, st));
+    k_ms_heavy_list<OffT><<<grid_for(n, 256, sms), 256, 0, st>>>(g->csc_off.as<OffT>(), n, M.heavy.as<int32_t>(),
+                                                                 M.cnt.as<unsigned long long>());
+    int64_t hn = 0;
+    GI_CUDA(cudaMemcpyAsync(&hn, M.cnt.p, 8, cudaMemcpyDeviceToHost, st));
+    GI_CUDA(cudaStreamSynchronize(st));
+    M.nheavy = hn;
+  }
+  const int kp = (k + 3) & ~3;
+  if (M.par.bytes < (size_t)n * kp * 4) GI_TRY(M.par.alloc((size_t)n * kp * 4));
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (o.profile) {
+    GI_CUDA(cudaEventCreate(&e0));
+    GI_CUDA(cudaEventCreate(&e1));
+    GI_CUDA(cudaEventRecord(e0, st));
+  }
+  unsigned long long* cnt = M.cnt.as<unsigned long long>();
+  int64_t* h = ctx->h_scratch;
+  const int64_t mdiv = g->m / (o.threshold_div > 0 ? o.threshold_div : kMsPullDiv);
+  std::vector<int32_t> levels(k, 1);
+  int64_t examined = 0;
+  int launches = 0;
+  GI_CUDA(cudaMemsetAsync(M.seen.p, 0, n * 8, st));
+  GI_CUDA(cudaMemsetAsync(M.fr[0].p, 0, n * 8, st));
+  GI_CUDA(cudaMemsetAsync(cnt, 0, 4 * 8 + 2 * 64 * 8, st));
+  GI_CUDA(cudaMemcpyAsync(M.src.p, sources, k * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+  k_ms_init<<<1, 64, 0, st>>>(M.src.as<int32_t>(), k, g->relabeled ? g->inv.as<int32_t>() : nullptr, n,
+                              g->outdeg.as<int32_t>(), M.seen.as<unsigned long long>(), M.fr[0].as<unsigned long long>(),
+                              M.act[0].as<int32_t>(), cnt, M.par.as<int32_t>(), kp);
+  launches += 1;
+  GI_CUDA(cudaMemcpyAsync(h, cnt, 4 * 8, cudaMemcpyDeviceToHost, st));
+  GI_CUDA(stream_wait(st));
+  int64_t nact = h[0], sdeg = h[1];
+  int pulls = 0;
+  MsArgs A{};
+  A.n = n;
+  A.csr_off = g->csr_off.p;
+  A.csr_idx = g->csr_idx.as<int32_t>();
+  A.csc_off = g->csc_off.p;
+  A.csc_idx = g->csc_idx.as<int32_t>();
+  A.outdeg = g->outdeg.as<int32_t>();
+  A.perm = g->relabeled ? g->perm.as<int32_t>() : nullptr;
+  A.inv = g->relabeled ? g->inv.as<int32_t>() : nullptr;
+  A.seen = M.seen.as<unsigned long long>();
+  A.cnt = cnt;
+  A.par = M.par.as<int32_t>();
+  A.kp = kp;
+  A.all = k == 64 ? ~0ull : ((1ull << k) - 1ull);
+  static const char* dbg = getenv("GI_DEBUG_MSBFS");  // diagnostics: per-level direction, size, time
+  FILE* df = dbg ? fopen(dbg, "a") : nullptr;
+  for (int level = 0; nact > 0; ++level) {
+    const auto tl0 = df ? std::chrono::steady_clock::now() : std::chrono::steady_clock::time_point{};
+    const int c = level & 1;
+    A.fcur = M.fr[c].as<unsigned long long>();
+    A.fnext = M.fr[c ^ 1].as<unsigned long long>();
+    A.acur = M.act[c].as<int32_t>();
+    A.anext = M.act[c ^ 1].as<int32_t>();
+    A.nact = nact;
+    GI_CUDA(cudaMemsetAsync(cnt, 0, 4 * 8, st));
+    const bool pull = o.policy == GI_BFS_PULL_ONLY ? level > 0
+                                                   : (o.policy == GI_BFS_AUTO && nact + sdeg > mdiv);
+    if (pull) {
+      k_ms_pull<OffT><<<grid_for(n, kMsT, sms, 16), kMsT, 0, st>>>(A);
+      if (M.nheavy > 0)
+        k_ms_pull_heavy<OffT><<<grid_for(M.nheavy * 32, kMsT, sms, 16), kMsT, 0, st>>>(A, M.heavy.as<int32_t>(),
+                                                                                      M.nheavy);
+      if (M.nheavy > 0) ++launches;
+      ++pulls;
+    } else {
+      GI_CUDA(cudaMemsetAsync(A.fnext, 0, n * 8, st));
+      int32_t* cc = M.chunks[0].as<int32_t>();
+      int32_t* cp = M.chunks[1].as<int32_t>();
+      k_ms_chunks<<<grid_for(nact, kMsT, sms, 8), kMsT, 0, st>>>(A.acur, nact, A.outdeg, cc);
+      size_t tb = M.scan_bytes;
+      GI_CUDA(cub::DeviceScan::InclusiveSum(M.scan_tmp.p, tb, cc, cp, (int)nact, st));
+      launches += 2;
+      k_ms_push<OffT><<<grid_for((sdeg / kPushChunk + nact) * 32, kMsT, sms, 8), kMsT, 0, st>>>(A, cp);
+    }
+    GI_CUDA(cudaGetLastError());
+    ++launches;
+    GI_CUDA(cudaMemcpyAsync(h, cnt, 4 * 8, cudaMemcpyDeviceToHost, st));
+    GI_CUDA(stream_wait(st));
+    if (df)
+      fprintf(df, "level=%d %s nact=%lld sdeg=%lld -> next=%lld examined=%lld us=%.1f\n", level, pull ? "pull" : "push",
+              (long long)nact, (long long)sdeg, (long long)h[0], (long long)h[3],
+              std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - tl0).count());
+    nact = h[0];
+    sdeg = h[1];
+    examined += h[3];
+    for (int i = 0; i < k; ++i)
+      if ((h[2] >> i) & 1) levels[i] = level + 2;  // source i still found vertices at this level
+  }
+  if (df) fclose(df);
+  unsigned long long* hr = cnt + 4;
+  GI_CUDA(cudaMemsetAsync(hr, 0, 2 * 64 * 8, st));
+  {
+    const size_t smem = (size_t)kFinWarps * 64 * 33 * 4;
+    GI_CUDA(cudaFuncSetAttribute(k_ms_finish, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_ms_finish<<<grid_for(n, 32 * kFinWarps, sms, 3), 32 * kFinWarps, smem, st>>>(
+        M.par.as<int32_t>(), M.seen.as<unsigned long long>(), A.inv, g->outdeg.as<int32_t>(), n, k, kp, d_out, hr, hr + 64);
+  }
+  ++launches;
+  std::vector<unsigned long long> hs(128);
+  GI_CUDA(cudaMemcpyAsync(hs.data(), hr, 128 * 8, cudaMemcpyDeviceToHost, st));
+  float ms = 0.f;
+  if (o.profile) GI_CUDA(cudaEventRecord(e1, st));
+  GI_CUDA(stream_wait(st));
+  if (o.profile) {
+    GI_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+  }
+  if (stats)
+    for (int i = 0; i < k; ++i) {
+      gi_bfs_stats s{};
+      s.levels = levels[i];
+      s.pull_levels = pulls;
+      s.reached = (int64_t)hs[i];
+      s.edges_traversed = (int64_t)hs[64 + i];
+      s.edges_examined = examined / k;  // shared by the k sources of the pass
+      s.pull_vertices = (int64_t)pulls * n / k;
+      s.total_ms = ms / (float)k;
+      s.launches = i == 0 ? launches : 0;
+      stats[i] = s;
+    }
+  return GI_OK;
+}
+
+}  // namespace
+
+// up to 64 sources per pass; longer batches run in passes of 64
+gi_status msbfs_run(gi_graph g, int32_t k, const int32_t* sources, const gi_bfs_opts& o, int32_t* d_out,
+                    gi_bfs_stats* stats) {
+  for (int32_t i0 = 0; i0 < k; i0 += 64) {
+    const int32_t kk = std::min<int32_t>(64, k - i0);
+    gi_status s = g->off64 ? msbfs_t<int64_t>(g, kk, sources + i0, o, d_out + (int64_t)i0 * g->n, stats ? stats + i0 : nullptr)
+                           : msbfs_t<int32_t>(g, kk, sources + i0, o, d_out + (int64_t)i0 * g->n, stats ? stats + i0 : nullptr);
+    if (s != GI_OK) return s;
+  }
+  return GI_OK;
+}
+
+}  // namespace gi

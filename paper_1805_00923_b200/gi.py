@@ -42,6 +42,7 @@ GI_PR_PULL, GI_PR_PUSH, GI_PR_PULL_DIRECT, GI_PR_PULL_SEGMENTED = 0, 1, 2, 3
 GI_DANGLING_UNIFORM, GI_DANGLING_DROP = 0, 1
 GI_BFS_AUTO, GI_BFS_PUSH_ONLY, GI_BFS_PULL_ONLY = 0, 1, 2
 GI_PRD_AUTO, GI_PRD_PUSH_ONLY, GI_PRD_PULL_ONLY = 0, 1, 2
+GI_BFS_BATCH_AUTO, GI_BFS_BATCH_PER_SOURCE, GI_BFS_BATCH_BITPARALLEL = 0, 1, 2
 
 
 class gi_pr_opts(ctypes.Structure):
@@ -67,7 +68,7 @@ class gi_prdelta_stats(ctypes.Structure):
 
 class gi_bfs_opts(ctypes.Structure):
     _fields_ = [("policy", ctypes.c_int32), ("threshold_div", ctypes.c_int32), ("profile", ctypes.c_int32),
-                ("reserved", ctypes.c_int32)]
+                ("batch", ctypes.c_int32)]
 
 
 class gi_bfs_stats(ctypes.Structure):
@@ -322,7 +323,7 @@ def gi_bfs_ex(g: int, source: int, out=None, policy: int = GI_BFS_AUTO, threshol
 
 
 def gi_bfs_multi(g: int, sources, out=None, policy: int = GI_BFS_AUTO, threshold_div: int = 0,
-                 profile: bool = False):
+                 profile: bool = False, batch: int = GI_BFS_BATCH_AUTO):
     """k BFS runs back to back; out: int32[k, n] (host or device). Returns (out, [stats])."""
     n = gi_graph_num_vertices(g)
     src = np.ascontiguousarray(np.asarray(sources, dtype=np.int64).astype(np.int32))
@@ -330,7 +331,7 @@ def gi_bfs_multi(g: int, sources, out=None, policy: int = GI_BFS_AUTO, threshold
     if out is None:
         out = np.empty((k, n), np.int32)
     p, keep = _ptr(out, np.int32)
-    o = gi_bfs_opts(policy, threshold_div, int(profile), 0)
+    o = gi_bfs_opts(policy, threshold_div, int(profile), batch)
     stats = (gi_bfs_stats * max(k, 1))()
     _check(_lib.gi_bfs_multi(g, k, src.ctypes.data if k else None, ctypes.byref(o), p or None, stats),
            "gi_bfs_multi")

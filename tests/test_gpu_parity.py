@@ -350,10 +350,13 @@ def test_bfs_config1(gi, ctx, policy, relabel):
     assert 0 < st.pull_levels < st.levels
 
 
+@pytest.mark.parametrize("batch", ["per_source", "bitparallel"])
 @pytest.mark.parametrize("where", ["host", "device"])
-def test_bfs_multi(gi, ctx, where):
-    """gi_bfs_multi == k gi_bfs runs: config 1 (one launch per source) and a
-    high-diameter grid (sources rerun through the small-grid handover)."""
+def test_bfs_multi(gi, ctx, where, batch):
+    """gi_bfs_multi == k gi_bfs runs (valid trees, same depths and stats):
+    config 1 and a high-diameter grid (per-source: sources rerun through the
+    small-grid handover), per-source and bit-parallel batches."""
+    bmode = {"per_source": gi.GI_BFS_BATCH_PER_SOURCE, "bitparallel": gi.GI_BFS_BATCH_BITPARALLEL}[batch]
     import torch
 
     cfg = graphgen.CONFIGS[1]
@@ -366,7 +369,7 @@ def test_bfs_multi(gi, ctx, where):
         go = oracle.build_graph(n, s, d)
         out = (torch.full((len(sources), n), 7, dtype=torch.int32, device="cuda") if where == "device"
                else np.full((len(sources), n), 7, np.int32))
-        par, stats = g.bfs_multi(sources, out=out)
+        par, stats = g.bfs_multi(sources, out=out, batch=bmode)
         par = par.cpu().numpy() if where == "device" else par
         for i, src in enumerate(sources):
             depth = oracle.bfs_depth(go, src)
@@ -377,10 +380,29 @@ def test_bfs_multi(gi, ctx, where):
                 (one.levels, one.reached, one.edges_traversed)
     g = gi.Graph(ctx, 10, *graphgen.cycle(10))
     with pytest.raises(gi.GiError) as e:
-        g.bfs_multi([0, 10])
+        g.bfs_multi([0, 10], batch=bmode)
     assert e.value.status == gi.GI_ERR_VERTEX_OUT_OF_RANGE
-    out, st = g.bfs_multi([])
+    out, st = g.bfs_multi([], batch=bmode)
     assert out.shape == (0, 10) and st == []
+
+
+def test_bfs_multi_bitparallel_batches(gi, ctx):
+    """More than 64 sources (two bit-parallel passes), repeated sources, every
+    direction policy; each row validated against the oracle."""
+    cfg = graphgen.CONFIGS[1]
+    s, d = cfg.edges()
+    g = gi.Graph(ctx, cfg.n, s, d)
+    go = oracle.build_graph(cfg.n, s, d)
+    sources = graphgen.pick_sources(cfg.n, s, d, 70, 77).tolist() + [0, 0]
+    for policy in POLICIES:
+        par, stats = g.bfs_multi(sources, batch=gi.GI_BFS_BATCH_BITPARALLEL, policy=_pol(gi, policy))
+        for i, src in enumerate(sources):
+            depth = oracle.bfs_depth(go, src)
+            ok, msg = oracle.validate_bfs(go, src, par[i], depth)
+            assert ok, f"{policy} src={src}: {msg}"
+            assert stats[i].reached == int((depth >= 0).sum())
+            assert stats[i].edges_traversed == oracle.reached_out_edges(go, depth)
+            assert stats[i].levels == depth.max() + 1
 
 
 def test_bfs_stress_repeat(gi, ctx):
@@ -440,11 +462,14 @@ def test_full_config_parity(gi, ctx, full_graphs, cfg_idx):
     sources = cfg.sources(s, d)[:4].tolist() if cfg.source_seed else [0]
     par = torch.empty(cfg.n, dtype=torch.int32, device="cuda")
     multi = torch.empty((len(sources), cfg.n), dtype=torch.int32, device="cuda")
-    _, mst = g.bfs_multi(sources, out=multi)  # the call bench.py times
+    bitp = torch.empty((len(sources), cfg.n), dtype=torch.int32, device="cuda")
+    _, mst = g.bfs_multi(sources, out=multi, batch=gi.GI_BFS_BATCH_PER_SOURCE)
+    _, bst = g.bfs_multi(sources, out=bitp, batch=gi.GI_BFS_BATCH_BITPARALLEL)
     for i, src in enumerate(sources):
         _, bs = g.bfs(int(src), out=par)
         depth = oracle.bfs_depth(go, int(src))
-        for what, p, st in (("gi_bfs", par, bs), ("gi_bfs_multi", multi[i], mst[i])):
+        for what, p, st in (("gi_bfs", par, bs), ("gi_bfs_multi", multi[i], mst[i]),
+                            ("gi_bfs_multi bit-parallel", bitp[i], bst[i])):
             ok, msg = oracle.validate_bfs(go, int(src), p.cpu().numpy(), depth)
             assert ok, f"{cfg.name} {what} src={src}: {msg}"
             assert st.edges_traversed == oracle.reached_out_edges(go, depth)
