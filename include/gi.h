@@ -243,12 +243,20 @@ typedef struct {
   int64_t edges_traversed; /* R16: sum of outdeg over reached vertices */
   float total_ms;          /* profile=1 */
   int32_t launches;        /* kernel launches in the call */
-  int32_t reserved;
+  float pull_ms;           /* profile=1, bit-parallel passes: device time of the
+                              pull-level kernels (0 for per-source traversals,
+                              whose pulls run inside the fused kernel) */
   int64_t edges_examined;  /* edge reads of the traversal: push levels every
                               out-edge of the frontier, pull levels the in-edges
                               probed before the early exit (single GPU; 0 else) */
   int64_t pull_vertices;   /* vertex checks of the pull levels (n per level) */
+  int64_t pull_edges_examined; /* the part of edges_examined read by pull levels
+                                  (bit-parallel passes; 0 for per-source) */
 } gi_bfs_stats;
+/* A bit-parallel pass serves up to 64 sources at once: its shared quantities
+ * (total_ms, pull_ms, edges_examined, pull_vertices, pull_edges_examined) are
+ * reported divided by the pass's source count, so summing over the sources of
+ * a call gives the call's totals. */
 
 GI_API gi_status gi_bfs_ex(gi_graph g, int32_t source, const gi_bfs_opts* opts, int32_t* parent_out,
                     gi_bfs_stats* stats /* may be NULL */);
@@ -264,9 +272,11 @@ GI_API gi_status gi_bfs_ex(gi_graph g, int32_t source, const gi_bfs_opts* opts, 
  * On one GPU, opts->batch selects per-source traversals (all sources in one
  * cooperative launch) or the bit-parallel traversal (edgeset.apply over a
  * 64-bit frontier mask per vertex: one pass over an edge serves 64 sources);
- * AUTO takes the bit-parallel form for k >= 8. With BITPARALLEL, stats
- * report the shared edge reads divided by the sources of the pass. On several
- * GPUs this is a loop of gi_bfs_ex.
+ * AUTO takes the bit-parallel form for k >= 8. With BITPARALLEL, stats report
+ * the shared quantities divided by the sources of the pass. Bit-parallel
+ * scratch: 8 bytes x 3 + 4 x 3 + 4 x round8(min(k, 64)) bytes per vertex, kept
+ * with the graph.
+ * On several GPUs this is a loop of gi_bfs_ex.
  * Errors as gi_bfs_ex (checked for every source before any run); k = 0 -> GI_OK. */
 GI_API gi_status gi_bfs_multi(gi_graph g, int32_t k, const int32_t* sources, const gi_bfs_opts* opts,
                               int32_t* parents_out, gi_bfs_stats* stats /* may be NULL */);

@@ -151,6 +151,8 @@ struct gi_graph_s {
   struct {  // bit-parallel multi-source BFS (msbfs.cu)
     gi::DevBuf seen, fr[2], act[2], cnt, src, heavy, par;
     int64_t nheavy = 0;  // rows with in-degree >= 32 (pulled by whole warps)
+    gi::DevBuf hch;      // their chunks: int2 (row, first in-edge offset)
+    int64_t nhch = 0;
     gi::DevBuf chunks[2], scan_tmp;  // push: chunk counts / inclusive prefix, cub scan scratch
     size_t scan_bytes = 0;
   } ms;

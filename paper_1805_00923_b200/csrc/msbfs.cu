@@ -23,7 +23,7 @@
 //     of 256 per warp; an edge claims new bits with atomicOr on seen (the
 //     returned old value says which bits this edge won) and adds them to the
 //     next frontier. Sinks (out-degree 0) never enter the active list.
-// Parents are staged vertex-major (par[v][i], k rounded up to 4 per row) so a
+// Parents are staged vertex-major (par[v][i], k rounded up to 8 per row) so a
 // vertex's bits land in one 256-byte row; the epilogue transposes them into the
 // k output rows (int32[k][n], input ids; -1 where source i never reached v)
 // and counts, per source, the vertices reached and their out-degrees.
@@ -45,13 +45,20 @@ namespace {
 #define GI_MS_OUT 1  // diagnostics: 0 drops the parent writes
 #endif
 constexpr int kMsT = 256;
-constexpr int64_t kHeavy = 32;  // rows with at least this many in-edges are pulled by whole warps
+#ifndef GI_MS_HEAVY
+#define GI_MS_HEAVY 32
+#endif
+constexpr int64_t kHeavy = GI_MS_HEAVY;  // rows with at least this many in-edges are pulled by whole warps
 constexpr int kMsPullDiv = 3;
 constexpr int kPushChunk = 256;
 #ifndef GI_MS_BATCH
 #define GI_MS_BATCH 4
 #endif
-constexpr int kPullBatch = GI_MS_BATCH;  // in-edge gathers in flight per pull step  // out-edges per push work item   // bit-parallel direction rule: pull iff |F| + sum outdeg F > m / 3
+constexpr int kPullBatch = GI_MS_BATCH;
+#ifndef GI_MS_HCHUNK
+#define GI_MS_HCHUNK 1024
+#endif
+constexpr int kHChunk = GI_MS_HCHUNK;  // heavy-row in-edges per pull work item  // in-edge gathers in flight per pull step  // out-edges per push work item   // bit-parallel direction rule: pull iff |F| + sum outdeg F > m / 3
 
 struct MsArgs {
   int64_t n;
@@ -69,12 +76,51 @@ struct MsArgs {
   int32_t* anext;                    // active vertices of the next level
   unsigned long long* cnt;           // [0] |active next|, [1] sum outdeg, [2] OR of new bits, [3] edges examined
   int32_t* par;                      // parents, vertex-major by input id: par[input id * kp + source bit]
-  int kp;                            // par row stride: k rounded up to a multiple of 4
+  int kp;                            // par row stride: k rounded up to a multiple of 8
   int64_t nact;
   unsigned long long all;            // mask of the k sources
 };
 
 __device__ __forceinline__ int32_t in_id(const MsArgs& A, int32_t v) { return A.perm ? __ldg(&A.perm[v]) : v; }
+
+// par row entries of the bits in m := val, a 32-byte sector (8 sources) at a
+// time. A sector none of whose bits is known yet (known = bits with a parent
+// already, or being written concurrently) is stored whole with one 256-bit
+// store — its other entries get val as a placeholder, overwritten when their
+// bit is found and masked by seen in the epilogue — so the sector's first
+// write is never a partial one (no read-modify-write of a partially written
+// line in HBM). Sectors with known bits get per-entry stores. UNIQUE: the
+// caller is the only writer of this row in the launch (else only sectors
+// whose 8 bits are all in m are stored whole).
+template <bool UNIQUE>
+__device__ __forceinline__ void par_put(int32_t* row, unsigned long long m, unsigned long long known, int32_t val) {
+  while (m) {
+    const int g = (__ffsll((long long)m) - 1) >> 3;
+    const unsigned nm = (unsigned)(m >> (8 * g)) & 0xFFu;
+    const unsigned kn = (unsigned)(known >> (8 * g)) & 0xFFu;
+    if (UNIQUE ? kn == 0u : nm == 0xFFu) {
+      asm volatile("st.global.v8.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1};" ::"l"(row + 8 * g), "r"(val) : "memory");
+    } else if (UNIQUE) {  // halves / pairs without known bits go as one vector store each
+      for (int h = 0; h < 8; h += 4) {
+        const unsigned n4 = (nm >> h) & 0xFu, k4 = (kn >> h) & 0xFu;
+        if (!n4) continue;
+        if (!k4) {
+          *reinterpret_cast<int4*>(row + 8 * g + h) = make_int4(val, val, val, val);
+          continue;
+        }
+        for (int p = h; p < h + 4; p += 2) {
+          const unsigned n2 = (nm >> p) & 3u, k2 = (kn >> p) & 3u;
+          if (!n2) continue;
+          if (!k2) *reinterpret_cast<int2*>(row + 8 * g + p) = make_int2(val, val);
+          else row[8 * g + p + (n2 & 1u ? 0 : 1)] = val;  // one of the pair is known, the other new
+        }
+      }
+    } else {
+      for (unsigned q = nm; q; q &= q - 1) row[8 * g + __ffs(q) - 1] = val;
+    }
+    m &= ~(0xFFull << (8 * g));
+  }
+}
 
 // CTA-aggregated append of the active vertices (one atomic per CTA round)
 __device__ __forceinline__ void ms_append(const MsArgs& A, bool act, int32_t v, int* s_cnt, long long* s_base) {
@@ -154,8 +200,7 @@ __global__ void __launch_bounds__(kMsT) k_ms_pull(MsArgs A) {
             if (m) {
               const int32_t vin = in_id(A, v[j]);
               if (wi < 0) wi = in_id(A, w);
-              if (GI_MS_OUT)
-                for (unsigned long long x = m; x; x &= x - 1) A.par[(int64_t)wi * A.kp + __ffsll((long long)x) - 1] = vin;
+              if (GI_MS_OUT) par_put<true>(A.par + (int64_t)wi * A.kp, m, s | found, vin);
               found |= m;
             }
           }
@@ -169,84 +214,155 @@ __global__ void __launch_bounds__(kMsT) k_ms_pull(MsArgs A) {
           tbits |= found;
         }
       }
-      if (e1 - e0 < kHeavy) A.fnext[w] = found;
+      A.fnext[w] = found;  // heavy rows: 0 here, k_ms_pull_heavy ORs into it
     }
     ms_append(A, act, w, s_cnt, &s_base);
   }
   ms_counters(A, tdeg, tbits, exam);
 }
 
-// pull for the heavy rows (in-degree >= kHeavy): a warp per row, 32 in-edges
-// per step, kPullBatch steps' gathers in flight; the bits a step brings are
-// split among its lanes by an exclusive prefix OR (each new bit's parent is
-// the lowest lane holding it)
-template <typename OffT>
-__global__ void __launch_bounds__(kMsT) k_ms_pull_heavy(MsArgs A, const int32_t* __restrict__ heavy, int64_t nh) {
-  __shared__ int s_cnt[kMsT / 32];
-  __shared__ long long s_base;
-  const OffT* __restrict__ off = static_cast<const OffT*>(A.csc_off);
+// pull for the heavy rows (in-degree >= kHeavy), edge-balanced: the rows are
+// cut into chunks of kHChunk in-edges (built once per graph; a row of at most
+// kHChunk in-edges is one chunk) and every warp takes a contiguous run of
+// chunks, kPullBatch x 32 gathers in flight per step. Chunks of one row may run
+// concurrently: each ORs what it found into seen / fnext with atomics, and the
+// chunk whose atomicOr on fnext returns 0 appends the row to the next frontier.
+// A chunk stops early once seen (as of its start) plus its own finds hold
+// every source. A new bit's parent is the lowest lane bringing it in its step;
+// lane L holds the parents of sources L and 32 + L, so a row's parents leave
+// in two coalesced stores at the end of the chunk (chunks of a split row race
+// on a bit found by both; either store is a valid parent).
+// 32x32 bit-matrix transpose across a warp: on return bit l of lane L's word
+// is bit L of lane l's input word
+__device__ __forceinline__ unsigned warp_transpose32(unsigned x) {
   const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int j = 16, i = 0; j > 0; j >>= 1, ++i) {
+    const unsigned mk = i == 0 ? 0x0000FFFFu : i == 1 ? 0x00FF00FFu : i == 2 ? 0x0F0F0F0Fu : i == 3 ? 0x33333333u : 0x55555555u;
+    const unsigned y = __shfl_xor_sync(0xffffffffu, x, j);
+    x = (lane & j) ? (x & ~mk) | ((y >> j) & mk) : (x & mk) | ((y << j) & ~mk);
+  }
+  return x;
+}
+
+template <typename OffT>
+__global__ void __launch_bounds__(kMsT) k_ms_pull_heavy(MsArgs A, const int2* __restrict__ hch, int64_t C) {
+  __shared__ int32_t s_buf[kMsT / 32][32];  // per-warp staging of the rows joining the next frontier
+  const OffT* __restrict__ off = static_cast<const OffT*>(A.csc_off);
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
   const int64_t nw = (int64_t)gridDim.x * (kMsT / 32);
-  const int64_t rounds = (nh + nw - 1) / nw;
+  const int64_t gw = blockIdx.x * (int64_t)(kMsT / 32) + wp;
+  const int64_t per = (C + nw - 1) / nw;
+  const int64_t c1 = min(C, (gw + 1) * per);
   long long tdeg = 0, exam = 0;
   unsigned long long tbits = 0;
-  for (int64_t r = 0; r < rounds; ++r) {
-    const int64_t i = r * nw + blockIdx.x * (kMsT / 32) + (threadIdx.x >> 5);
-    bool act = false;
-    int32_t w = 0;
-    unsigned long long found = 0;
-    if (i < nh) {
-      w = __ldg(&heavy[i]);
-      const unsigned long long s = A.seen[w];
-      if (s != A.all) {
-        const int32_t wi = in_id(A, w);
-        const int64_t e0 = (int64_t)off[w], e1 = (int64_t)off[w + 1];
-        for (int64_t b = e0; b < e1; b += 32 * kPullBatch) {
-          int32_t v[kPullBatch];
-          unsigned long long f[kPullBatch];
+  int nbuf = 0;
+  for (int64_t c = gw * per; c < c1; ++c) {
+    const int2 ch = __ldg(&hch[c]);
+    const int32_t w = ch.x;
+    const unsigned long long s = *(volatile unsigned long long*)&A.seen[w];
+    bool newact = false;
+    if (s != A.all) {
+      const int32_t wi = in_id(A, w);
+      const int64_t rb = (int64_t)off[w], re = (int64_t)off[w + 1];
+      const int64_t e0 = rb + ch.y, e1 = min(re, e0 + kHChunk);
+      const bool whole = re - rb <= kHChunk;  // the warp is the row's only writer this launch
+      int32_t* prow = A.par + (int64_t)wi * A.kp;
+      // lane L keeps the parents of sources L (plo) and 32 + L (phi)
+      int32_t plo = 0, phi = 0;
+      unsigned long long found = 0;
+      for (int64_t b = e0; b < e1; b += 32 * kPullBatch) {
+        int32_t v[kPullBatch];
+        unsigned long long f[kPullBatch];
 #pragma unroll
-          for (int j = 0; j < kPullBatch; ++j) {
-            const int64_t e = b + 32 * j + lane;
-            v[j] = e < e1 ? __ldg(&A.csc_idx[e]) : -1;
-          }
-#pragma unroll
-          for (int j = 0; j < kPullBatch; ++j) f[j] = v[j] >= 0 ? A.fcur[v[j]] : 0ull;
-          if (lane == 0) exam += min((int64_t)32 * kPullBatch, e1 - b);
-#pragma unroll
-          for (int j = 0; j < kPullBatch; ++j) {
-            const unsigned long long m = f[j] & ~s & ~found;
-            if (__ballot_sync(0xffffffffu, m != 0) == 0) continue;
-            unsigned long long x = m;  // inclusive prefix OR over lanes
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-              const unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
-              if (lane >= o) x |= y;
-            }
-            unsigned long long below = __shfl_up_sync(0xffffffffu, x, 1);
-            if (lane == 0) below = 0;
-            const unsigned long long mine = m & ~below;
-            if (mine) {
-              const int32_t vin = in_id(A, v[j]);
-              if (GI_MS_OUT)
-                for (unsigned long long q = mine; q; q &= q - 1) A.par[(int64_t)wi * A.kp + __ffsll((long long)q) - 1] = vin;
-            }
-            found |= __shfl_sync(0xffffffffu, x, 31);
-          }
-          if ((s | found) == A.all) break;
+        for (int j = 0; j < kPullBatch; ++j) {
+          const int64_t e = b + 32 * j + lane;
+          v[j] = e < e1 ? __ldg(&A.csc_idx[e]) : -1;
         }
-        if (found && lane == 0) A.seen[w] = s | found;
+#pragma unroll
+        for (int j = 0; j < kPullBatch; ++j) f[j] = v[j] >= 0 ? A.fcur[v[j]] : 0ull;
+        if (lane == 0) exam += min((int64_t)32 * kPullBatch, e1 - b);
+#pragma unroll
+        for (int j = 0; j < kPullBatch; ++j) {
+          const unsigned long long mj = f[j] & ~s & ~found;
+          const unsigned lo = __reduce_or_sync(0xffffffffu, (unsigned)mj);
+          const unsigned hi = __reduce_or_sync(0xffffffffu, (unsigned)(mj >> 32));
+          if ((lo | hi) == 0u) continue;  // warp-uniform: nothing new from this batch slot
+          const int32_t vin = mj ? in_id(A, v[j]) : 0;
+          // each new bit's parent: the lowest lane bringing it (bit-matrix transpose of the lanes' masks)
+          if (lo) {
+            const unsigned tl = warp_transpose32((unsigned)mj);
+            const int32_t p = __shfl_sync(0xffffffffu, vin, tl ? __ffs(tl) - 1 : 0);
+            if (tl) plo = p;
+          }
+          if (hi) {
+            const unsigned th = warp_transpose32((unsigned)(mj >> 32));
+            const int32_t p = __shfl_sync(0xffffffffu, vin, th ? __ffs(th) - 1 : 0);
+            if (th) phi = p;
+          }
+          found |= ((unsigned long long)hi << 32) | lo;
+        }
+        if ((s | found) == A.all) break;
       }
-      if (lane == 0) A.fnext[w] = found;
+      if (GI_MS_OUT && found) {
+        // whole row: a sector without known bits is written in full (placeholders
+        // for its unfound sources), else only the new entries; split rows: new entries
+        const unsigned kl = (unsigned)s, kh = (unsigned)(s >> 32);
+        const unsigned nl = (unsigned)found, nh = (unsigned)(found >> 32);
+        const int sh = lane & ~7;
+        const bool wl = (nl >> lane) & 1u || (whole && ((nl >> sh) & 0xFFu) && !((kl >> sh) & 0xFFu));
+        const bool wh = (nh >> lane) & 1u || (whole && ((nh >> sh) & 0xFFu) && !((kh >> sh) & 0xFFu));
+        if (wl && lane < A.kp) prow[lane] = plo;
+        if (wh && 32 + lane < A.kp) prow[32 + lane] = phi;
+      }
       if (found && lane == 0) {
-        const int32_t deg = __ldg(&A.outdeg[w]);
-        act = deg > 0;
-        tdeg += deg;
+        atomicOr(&A.seen[w], found);
         tbits |= found;
+        if (atomicOr(&A.fnext[w], found) == 0ull) {  // the row's first bits this level
+          const int32_t d = __ldg(&A.outdeg[w]);
+          tdeg += d;
+          newact = d > 0;
+        }
       }
     }
-    ms_append(A, act, w, s_cnt, &s_base);
+    if (__shfl_sync(0xffffffffu, newact, 0)) {
+      if (lane == 0) s_buf[wp][nbuf] = w;
+      if (++nbuf == 32) {  // one atomic per 32 appended rows
+        __syncwarp();
+        unsigned long long pos = 0;
+        if (lane == 0) pos = atomicAdd(&A.cnt[0], 32ull);
+        pos = __shfl_sync(0xffffffffu, pos, 0);
+        A.anext[pos + lane] = s_buf[wp][lane];
+        __syncwarp();
+        nbuf = 0;
+      }
+    }
+  }
+  __syncwarp();
+  if (nbuf > 0) {
+    unsigned long long pos = 0;
+    if (lane == 0) pos = atomicAdd(&A.cnt[0], (unsigned long long)nbuf);
+    pos = __shfl_sync(0xffffffffu, pos, 0);
+    if (lane < nbuf) A.anext[pos + lane] = s_buf[wp][lane];
   }
   ms_counters(A, tdeg, tbits, exam);
+}
+
+// heavy-row chunks: cc[i] = chunks of heavy row i; then (row, first in-edge offset) per chunk
+template <typename OffT>
+__global__ void k_ms_hchunk_count(const OffT* __restrict__ off, const int32_t* __restrict__ heavy, int64_t nh,
+                                  int32_t* __restrict__ cc) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nh; i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t w = heavy[i];
+    cc[i] = (int32_t)(((int64_t)off[w + 1] - (int64_t)off[w] + kHChunk - 1) / kHChunk);
+  }
+}
+__global__ void k_ms_hchunk_fill(const int32_t* __restrict__ heavy, int64_t nh, const int32_t* __restrict__ cc,
+                                 const int32_t* __restrict__ cp, int2* __restrict__ hch) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nh; i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t w = heavy[i], c = cc[i], base = cp[i] - c;
+    for (int32_t j = 0; j < c; ++j) hch[base + j] = make_int2(w, j * kHChunk);
+  }
 }
 
 // the heavy rows (in-degree >= kHeavy), appended in any order
@@ -310,8 +426,7 @@ __global__ void __launch_bounds__(kMsT) k_ms_push(MsArgs A, const int32_t* __res
             const unsigned long long got = m & ~atomicOr(&A.seen[w], m);  // the bits this edge claims
             if (got) {
               const int32_t win = in_id(A, w);
-              if (GI_MS_OUT)
-                for (unsigned long long x = got; x; x &= x - 1) A.par[(int64_t)win * A.kp + __ffsll((long long)x) - 1] = uin;
+              if (GI_MS_OUT) par_put<false>(A.par + (int64_t)win * A.kp, got, 0ull, uin);
               bits |= got;
               if (atomicOr(&A.fnext[w], got) == 0ull) {  // w's first bits this level: it joins the next frontier
                 const int32_t dw = __ldg(&A.outdeg[w]);
@@ -463,13 +578,31 @@ gi_status msbfs_t(gi_graph g, int32_t k, const int32_t* sources, const gi_bfs_op
     GI_CUDA(cudaMemcpyAsync(&hn, M.cnt.p, 8, cudaMemcpyDeviceToHost, st));
     GI_CUDA(cudaStreamSynchronize(st));
     M.nheavy = hn;
+    M.nhch = 0;
+    if (hn > 0) {
+      int32_t* cc = M.chunks[0].as<int32_t>();
+      int32_t* cp = M.chunks[1].as<int32_t>();
+      k_ms_hchunk_count<OffT><<<grid_for(hn, 256, sms), 256, 0, st>>>(g->csc_off.as<OffT>(), M.heavy.as<int32_t>(), hn, cc);
+      size_t tb2 = M.scan_bytes;
+      GI_CUDA(cub::DeviceScan::InclusiveSum(M.scan_tmp.p, tb2, cc, cp, (int)hn, st));
+      int32_t hc = 0;
+      GI_CUDA(cudaMemcpyAsync(&hc, cp + hn - 1, 4, cudaMemcpyDeviceToHost, st));
+      GI_CUDA(cudaStreamSynchronize(st));
+      GI_TRY(M.hch.alloc((size_t)hc * 8));
+      k_ms_hchunk_fill<<<grid_for(hn, 256, sms), 256, 0, st>>>(M.heavy.as<int32_t>(), hn, cc, cp, M.hch.as<int2>());
+      M.nhch = hc;
+    }
   }
-  const int kp = (k + 3) & ~3;
+  const int kp = (k + 7) & ~7;  // whole 32-byte sectors per row
   if (M.par.bytes < (size_t)n * kp * 4) GI_TRY(M.par.alloc((size_t)n * kp * 4));
-  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  cudaEvent_t e0 = nullptr, e1 = nullptr, pe0 = nullptr, pe1 = nullptr;
+  int64_t pull_examined = 0;
+  float pull_ms = 0.f;
   if (o.profile) {
     GI_CUDA(cudaEventCreate(&e0));
     GI_CUDA(cudaEventCreate(&e1));
+    GI_CUDA(cudaEventCreate(&pe0));
+    GI_CUDA(cudaEventCreate(&pe1));
     GI_CUDA(cudaEventRecord(e0, st));
   }
   unsigned long long* cnt = M.cnt.as<unsigned long long>();
@@ -517,12 +650,14 @@ gi_status msbfs_t(gi_graph g, int32_t k, const int32_t* sources, const gi_bfs_op
     GI_CUDA(cudaMemsetAsync(cnt, 0, 4 * 8, st));
     const bool pull = o.policy == GI_BFS_PULL_ONLY ? level > 0
                                                    : (o.policy == GI_BFS_AUTO && nact + sdeg > mdiv);
+    if (pull && o.profile) GI_CUDA(cudaEventRecord(pe0, st));
     if (pull) {
       k_ms_pull<OffT><<<grid_for(n, kMsT, sms, 16), kMsT, 0, st>>>(A);
-      if (M.nheavy > 0)
-        k_ms_pull_heavy<OffT><<<grid_for(M.nheavy * 32, kMsT, sms, 16), kMsT, 0, st>>>(A, M.heavy.as<int32_t>(),
-                                                                                      M.nheavy);
-      if (M.nheavy > 0) ++launches;
+      if (M.nhch > 0) {
+        k_ms_pull_heavy<OffT><<<grid_for(M.nhch * 32, kMsT, sms, 8), kMsT, 0, st>>>(A, M.hch.as<int2>(), M.nhch);
+        ++launches;
+      }
+      if (o.profile) GI_CUDA(cudaEventRecord(pe1, st));
       ++pulls;
     } else {
       GI_CUDA(cudaMemsetAsync(A.fnext, 0, n * 8, st));
@@ -545,6 +680,14 @@ gi_status msbfs_t(gi_graph g, int32_t k, const int32_t* sources, const gi_bfs_op
     nact = h[0];
     sdeg = h[1];
     examined += h[3];
+    if (pull) {
+      pull_examined += h[3];
+      if (o.profile) {
+        float pm = 0.f;
+        GI_CUDA(cudaEventElapsedTime(&pm, pe0, pe1));
+        pull_ms += pm;
+      }
+    }
     for (int i = 0; i < k; ++i)
       if ((h[2] >> i) & 1) levels[i] = level + 2;  // source i still found vertices at this level
   }
@@ -567,6 +710,8 @@ gi_status msbfs_t(gi_graph g, int32_t k, const int32_t* sources, const gi_bfs_op
     GI_CUDA(cudaEventElapsedTime(&ms, e0, e1));
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
+    cudaEventDestroy(pe0);
+    cudaEventDestroy(pe1);
   }
   if (stats)
     for (int i = 0; i < k; ++i) {
@@ -578,6 +723,8 @@ gi_status msbfs_t(gi_graph g, int32_t k, const int32_t* sources, const gi_bfs_op
       s.edges_examined = examined / k;  // shared by the k sources of the pass
       s.pull_vertices = (int64_t)pulls * n / k;
       s.total_ms = ms / (float)k;
+      s.pull_ms = pull_ms / (float)k;
+      s.pull_edges_examined = pull_examined / k;
       s.launches = i == 0 ? launches : 0;
       stats[i] = s;
     }

@@ -74,7 +74,8 @@ class gi_bfs_opts(ctypes.Structure):
 class gi_bfs_stats(ctypes.Structure):
     _fields_ = [("levels", ctypes.c_int32), ("pull_levels", ctypes.c_int32), ("reached", ctypes.c_int64),
                 ("edges_traversed", ctypes.c_int64), ("total_ms", ctypes.c_float), ("launches", ctypes.c_int32),
-                ("reserved", ctypes.c_int32), ("edges_examined", ctypes.c_int64), ("pull_vertices", ctypes.c_int64)]
+                ("pull_ms", ctypes.c_float), ("edges_examined", ctypes.c_int64), ("pull_vertices", ctypes.c_int64),
+                ("pull_edges_examined", ctypes.c_int64)]
 
 
 _vp = ctypes.c_void_p
