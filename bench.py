@@ -14,12 +14,12 @@ value  = (20 m + sum over sources of edges traversed) / device time, all ranks
          (GTEPS), inputs resident in HBM, CUDA events on the library's stream.
 e2e    = the same edges over the time of the public C-ABI calls with HOST
          buffers: gi_graph_create from pinned host edges (H2D inside),
-         gi_pagerank into host memory, gi_bfs x 64 into host memory.
-roofline: the kernel with the larger share of the step (BFS on config 2);
+         gi_pagerank into host memory, gi_bfs_multi (64 sources) into host memory.
+roofline: the kernel with the larger summed device time per step;
          roofline_pr: the pull-PageRank iteration (the north_star's >= 50% target),
          algorithmic bytes 4m + (o+12)n per iteration / its
-         CUDA-event duration; roofline_bfs: 4 B per edge examined + 4 B per
-         pull-level vertex check + 8 B per reached vertex, per source.
+         CUDA-event duration; roofline_bfs: the bit-parallel pull level
+         (k_ms_pull + k_ms_pull_heavy), 4 B per in-edge read + 20 B per vertex.
 cpu_baseline: the oracle (oracle/, plain C, OpenMP) on a bounded sample of
          the same graph (2 PR iterations + 2 BFS sources).
 
@@ -80,7 +80,7 @@ def load_traffic():
     """Per-launch DRAM bytes (ncu --set full) of the PR iteration and the BFS kernel from the committed
     summary (profiles/ncu_summary.json); missing entries are None."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
-    out = {"pr_pull": None, "bfs_fused": None}
+    out = {"pr_pull": None, "bfs_fused": None, "bfs_pull": None}
     if os.path.exists(p):
         try:
             d = json.load(open(p))
@@ -322,18 +322,36 @@ def run_ours(args):
                              "per iteration",
                    "bytes_alg_per_launch": ps.bytes_alg_per_iter, "launch_ms": kern_ms,
                    "vertex_ms": ps.vertex_ms / max(ps.edge_launches, 1), "peak_source": peak_src}
-    # BFS (the larger share of the step): the fused kernel, per source; algorithmic bytes per source =
-    # 4 B per edge examined + 4 B per pull-level vertex check + 8 B per reached vertex (parent + output)
+    # BFS: gi_bfs_multi over the 64 sources runs one bit-parallel pass (SURVEY §8 a7-a9 over a 64-bit
+    # frontier mask); its dominant kernels are the pull levels (k_ms_pull + k_ms_pull_heavy). Algorithmic
+    # bytes per pull level = 4 B per in-edge read (CSC index stream) + 20 B per vertex (row offset 4 B,
+    # seen mask 8 B read, next-frontier mask 8 B written); the 8 B frontier-mask gathers hit L2 (n x 8 B
+    # = 32 MB resident), so they are not HBM bytes. Per-source runs (k < 8): the fused kernel, per source.
     _, bsp = g.bfs_multi(srcs, out=bfs_out, profile=True)
-    bfs_src_ms = sum(b.total_ms for b in bsp) / max(len(bsp), 1)
-    bfs_bytes = sum(4 * b.edges_examined + 4 * b.pull_vertices + 8 * b.reached for b in bsp) / max(len(bsp), 1)
-    bfs_achieved = bfs_bytes / (bfs_src_ms * 1e-3) / 1e9 if bfs_src_ms > 0 else 0.0
+    bfs_pass_ms = sum(b.total_ms for b in bsp)
+    pull_ms = sum(b.pull_ms for b in bsp)
+    if pull_ms > 0:
+        pull_levels = max(b.pull_levels for b in bsp)
+        pull_edges = sum(b.pull_edges_examined for b in bsp)
+        bfs_bytes = (4 * pull_edges + 20 * n * pull_levels) / pull_levels
+        bfs_launch_ms = pull_ms / pull_levels
+        bfs_kernel = ("k_ms_pull + k_ms_pull_heavy (bit-parallel multi-source BFS, one pull level over "
+                      f"{len(srcs)} sources)")
+        bfs_total_ms = pull_ms
+    else:
+        bfs_launch_ms = bfs_pass_ms / max(len(bsp), 1)
+        bfs_bytes = sum(4 * b.edges_examined + 4 * b.pull_vertices + 8 * b.reached for b in bsp) / max(len(bsp), 1)
+        bfs_kernel = "k_bfs_fused (direction-optimising BFS, per source)"
+        bfs_total_ms = bfs_pass_ms
+    bfs_achieved = bfs_bytes / (bfs_launch_ms * 1e-3) / 1e9 if bfs_launch_ms > 0 else 0.0
     roofline_bfs = {"bound": "hbm", "achieved": bfs_achieved, "peak": peak, "unit": "GB/s",
-                    "frac": bfs_achieved / peak, "traffic": traffic.get("bfs_fused"),
-                    "kernel": "k_bfs_fused (direction-optimising BFS; gi_bfs_multi: one cooperative launch for all sources)",
-                    "bytes_alg_per_launch": bfs_bytes, "launch_ms": bfs_src_ms, "peak_source": peak_src,
+                    "frac": bfs_achieved / peak, "traffic": traffic.get("bfs_pull"),
+                    "kernel": bfs_kernel, "bytes_alg_per_launch": bfs_bytes, "launch_ms": bfs_launch_ms,
+                    "launches_per_step": (max(b.pull_levels for b in bsp) if pull_ms > 0 else len(bsp)),
+                    "pass_ms": bfs_pass_ms, "peak_source": peak_src,
                     "edges_examined_per_source": sum(b.edges_examined for b in bsp) / max(len(bsp), 1)}
-    roofline = roofline_bfs if bfs_ms > pr_ms else roofline_pr
+    # the dominant kernel: the larger summed device time per step (PR edge pass x 20 vs the BFS pull levels)
+    roofline = roofline_bfs if bfs_total_ms > ps.edge_ms else roofline_pr
 
     # e2e through the public API with host buffers
     e2e = None
@@ -376,7 +394,7 @@ def run_ours(args):
             "data": "synthetic (seeded counter-based RMAT; stands in for LiveJournal, paper datasets unavailable)",
             "config": {"workload": f"{cfg.name} (BASELINE configs[{cfg.idx - 1}])", "n": n, "m": m,
                        "pr_iters": cfg.pr_iters, "damping": cfg.damping, "bfs_sources": len(srcs),
-                       "pr_direction": args.pr_direction, "bfs_policy": "auto (m/20)",
+                       "pr_direction": args.pr_direction, "bfs_policy": "auto: bit-parallel pass of 64 sources, pull iff |F| + sum outdeg F > m/3",
                        "l2": "inputs larger than L2 (CSR+CSC ~ 8m bytes > 126 MB), no flush",
                        "parallelism": (f"dst-partition x{world} (NCCL allgather of contrib / frontier bitmap)"
                                        if partition else f"replicas x{world}") if world > 1 else "single"},

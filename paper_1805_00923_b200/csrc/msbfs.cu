@@ -23,12 +23,13 @@
 //     of 256 per warp; an edge claims new bits with atomicOr on seen (the
 //     returned old value says which bits this edge won) and adds them to the
 //     next frontier. Sinks (out-degree 0) never enter the active list.
-// Parents are staged vertex-major (par[v][i], k rounded up to 8 per row) so a
+// Parents are staged vertex-major (par[v][i], rows of k rounded up to a power of two >= 8) so a
 // vertex's bits land in one 256-byte row; the epilogue transposes them into the
 // k output rows (int32[k][n], input ids; -1 where source i never reached v)
 // and counts, per source, the vertices reached and their out-degrees.
 #include <algorithm>
 #include <chrono>
+#include <climits>
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
@@ -76,7 +77,7 @@ struct MsArgs {
   int32_t* anext;                    // active vertices of the next level
   unsigned long long* cnt;           // [0] |active next|, [1] sum outdeg, [2] OR of new bits, [3] edges examined
   int32_t* par;                      // parents, vertex-major by input id: par[input id * kp + source bit]
-  int kp;                            // par row stride: k rounded up to a multiple of 8
+  int kp;                            // par row stride: k rounded up to a power of two >= 8
   int64_t nact;
   unsigned long long all;            // mask of the k sources
 };
@@ -373,18 +374,21 @@ __global__ void k_ms_heavy_list(const OffT* __restrict__ off, int64_t n, int32_t
     if ((int64_t)off[v + 1] - (int64_t)off[v] >= kHeavy) list[atomicAdd(cnt, 1ull)] = (int32_t)v;
 }
 
-// chunk counts of the active vertices for the edge-balanced push
-__global__ void k_ms_chunks(const int32_t* __restrict__ act, int64_t nact, const int32_t* __restrict__ outdeg,
-                            int32_t* __restrict__ cc) {
+// out-degrees of the active vertices (their inclusive prefix drives the push)
+__global__ void k_ms_degs(const int32_t* __restrict__ act, int64_t nact, const int32_t* __restrict__ outdeg,
+                          long long* __restrict__ dd) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nact; i += (int64_t)gridDim.x * blockDim.x)
-    cc[i] = (__ldg(&outdeg[__ldg(&act[i])]) + kPushChunk - 1) / kPushChunk;
+    dd[i] = __ldg(&outdeg[__ldg(&act[i])]);
 }
 
-// push, edge-balanced: the active vertices' out-edges are cut into chunks of
-// kPushChunk (cp = inclusive prefix of the chunk counts) and every warp takes
-// a contiguous run of chunks, so a hub's edges spread over many warps
+// push, edge-parallel: the active vertices' out-edges, concatenated (dp =
+// inclusive prefix of their out-degrees), are split evenly over the warps and
+// walked 32 at a time, a lane per edge. A warp keeps a window of 32 prefix
+// entries; each lane finds its edge's vertex in it by a 5-step search over
+// shuffles, so low-degree vertices share a step and a hub spreads over many
+// warps.
 template <typename OffT>
-__global__ void __launch_bounds__(kMsT) k_ms_push(MsArgs A, const int32_t* __restrict__ cp) {
+__global__ void __launch_bounds__(kMsT) k_ms_push(MsArgs A, const long long* __restrict__ dp) {
   __shared__ int32_t s_buf[kMsT / 32][64];  // per-warp staging of the vertices joining the next frontier
   const OffT* __restrict__ off = static_cast<const OffT*>(A.csr_off);
   const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
@@ -393,66 +397,67 @@ __global__ void __launch_bounds__(kMsT) k_ms_push(MsArgs A, const int32_t* __res
   const int64_t gw = blockIdx.x * (int64_t)(kMsT / 32) + wp;
   long long deg = 0, exam = 0;
   unsigned long long bits = 0;
-  const int64_t C = A.nact > 0 ? (int64_t)__ldg(&cp[A.nact - 1]) : 0;
-  const int64_t per = (C + nw - 1) / nw;
-  int64_t c = gw * per;
-  const int64_t cend = min(C, c + per);
-  if (c < cend) {
-    int64_t i = 0, hi = A.nact;  // first active vertex whose chunks reach past c
-    while (i < hi) {
-      const int64_t mid = (i + hi) >> 1;
-      if ((int64_t)__ldg(&cp[mid]) <= c) i = mid + 1;
+  const long long E = A.nact > 0 ? __ldg(&dp[A.nact - 1]) : 0;
+  const long long per = (E + nw - 1) / nw;
+  long long e = gw * per;
+  const long long eend = min(E, e + per);
+  if (e < eend) {
+    int64_t i0 = 0, hi = A.nact;  // the active vertex holding edge e: first i with dp[i] > e
+    while (i0 < hi) {
+      const int64_t mid = (i0 + hi) >> 1;
+      if (__ldg(&dp[mid]) <= e) i0 = mid + 1;
       else hi = mid;
     }
-    for (; c < cend; ++i) {
-      const int64_t before = i ? (int64_t)__ldg(&cp[i - 1]) : 0;
-      const int64_t ce = min((int64_t)__ldg(&cp[i]), cend) - before;
-      const int32_t u = __ldg(&A.acur[i]);
-      const int64_t u0 = (int64_t)off[u], u1 = (int64_t)off[u + 1];
-      const int64_t e0 = u0 + (c - before) * kPushChunk, e1 = min(u1, u0 + ce * kPushChunk);
-      c = before + ce;
-      if (e0 >= e1) continue;
-      const unsigned long long mu = A.fcur[u];
-      const int32_t uin = in_id(A, u);
-      for (int64_t base = e0; base < e1; base += 32) {  // warp-uniform steps of 32 out-edges
-        const int64_t e = base + lane;
-        bool newact = false;
-        int32_t w = 0;
-        if (e < e1) {
-          w = __ldg(&A.csr_idx[e]);
-          ++exam;
-          const unsigned long long m = mu & ~*(volatile unsigned long long*)&A.seen[w];
-          if (m) {
-            const unsigned long long got = m & ~atomicOr(&A.seen[w], m);  // the bits this edge claims
-            if (got) {
-              const int32_t win = in_id(A, w);
-              if (GI_MS_OUT) par_put<false>(A.par + (int64_t)win * A.kp, got, 0ull, uin);
-              bits |= got;
-              if (atomicOr(&A.fnext[w], got) == 0ull) {  // w's first bits this level: it joins the next frontier
-                const int32_t dw = __ldg(&A.outdeg[w]);
-                newact = dw > 0;  // sinks stay out of the active list
-                deg += dw;
-              }
+    while (e < eend) {  // warp-uniform
+      const long long P = i0 + lane < A.nact ? __ldg(&dp[i0 + lane]) : LLONG_MAX;
+      const long long Pprev = i0 > 0 ? __ldg(&dp[i0 - 1]) : 0;
+      const long long stop = min(eend, min(e + 32, (long long)__shfl_sync(0xffffffffu, P, 31)));
+      const long long my = e + lane;
+      int pos = 0;  // my edge's vertex: i0 + #{l : P_l <= my}
+#pragma unroll
+      for (int s = 16; s > 0; s >>= 1)
+        if (__shfl_sync(0xffffffffu, P, pos + s - 1) <= my) pos += s;
+      const long long pl = __shfl_sync(0xffffffffu, P, pos > 0 ? pos - 1 : 0);  // every lane takes part
+      const long long start = pos ? pl : Pprev;
+      bool newact = false;
+      int32_t w = 0;
+      if (my < stop) {
+        const int32_t u = __ldg(&A.acur[i0 + pos]);
+        w = __ldg(&A.csr_idx[(int64_t)off[u] + (my - start)]);
+        ++exam;
+        const unsigned long long m = A.fcur[u] & ~*(volatile unsigned long long*)&A.seen[w];
+        if (m) {
+          const unsigned long long got = m & ~atomicOr(&A.seen[w], m);  // the bits this edge claims
+          if (got) {
+            const int32_t win = in_id(A, w);
+            if (GI_MS_OUT) par_put<false>(A.par + (int64_t)win * A.kp, got, 0ull, in_id(A, u));
+            bits |= got;
+            if (atomicOr(&A.fnext[w], got) == 0ull) {  // w's first bits this level: it joins the next frontier
+              const int32_t dw = __ldg(&A.outdeg[w]);
+              newact = dw > 0;  // sinks stay out of the active list
+              deg += dw;
             }
           }
         }
-        const unsigned am = __ballot_sync(0xffffffffu, newact);
-        if (am) {
-          if (newact) s_buf[wp][nbuf + __popc(am & ((1u << lane) - 1u))] = w;
-          nbuf += __popc(am);
-          if (nbuf >= 32) {  // one atomic per 32 appended vertices
-            __syncwarp();
-            unsigned long long pos = 0;
-            if (lane == 0) pos = atomicAdd(&A.cnt[0], 32ull);
-            pos = __shfl_sync(0xffffffffu, pos, 0);
-            A.anext[pos + lane] = s_buf[wp][lane];
-            __syncwarp();
-            nbuf -= 32;
-            if (lane < nbuf) s_buf[wp][lane] = s_buf[wp][32 + lane];
-            __syncwarp();
-          }
+      }
+      const unsigned am = __ballot_sync(0xffffffffu, newact);
+      if (am) {
+        if (newact) s_buf[wp][nbuf + __popc(am & ((1u << lane) - 1u))] = w;
+        nbuf += __popc(am);
+        if (nbuf >= 32) {  // one atomic per 32 appended vertices
+          __syncwarp();
+          unsigned long long pos2 = 0;
+          if (lane == 0) pos2 = atomicAdd(&A.cnt[0], 32ull);
+          pos2 = __shfl_sync(0xffffffffu, pos2, 0);
+          A.anext[pos2 + lane] = s_buf[wp][lane];
+          __syncwarp();
+          nbuf -= 32;
+          if (lane < nbuf) s_buf[wp][lane] = s_buf[wp][32 + lane];
+          __syncwarp();
         }
       }
+      i0 += __popc(__ballot_sync(0xffffffffu, P <= stop));
+      e = stop;
     }
   }
   __syncwarp();
@@ -481,68 +486,88 @@ __global__ void k_ms_init(const int32_t* __restrict__ src_in, int k, const int32
   }
 }
 
-// The pass's epilogue, a warp per 32 consecutive input ids v:
+// The pass's epilogue, a CTA per tile of kFinV consecutive input ids v:
 //   out[i][v] = source i's parent of v, or -1 when i never reached v — the
-//     vertex-major parents (8 KB per warp, 16-byte loads) go through a
-//     warp-private shared tile so the k output rows are written coalesced;
+//     tile's vertex-major parents (kFinV rows of kp, contiguous, 16-byte
+//     loads) are transposed through shared memory so each of the k output
+//     rows gets one contiguous 4 x kFinV-byte segment;
 //   per source i: vertices reached and the sum of their out-degrees (R16).
-constexpr int kFinWarps = 8;
-__global__ void __launch_bounds__(32 * kFinWarps) k_ms_finish(const int32_t* __restrict__ par,
-                                                             const unsigned long long* __restrict__ seen,
-                                                             const int32_t* __restrict__ inv,
-                                                             const int32_t* __restrict__ outdeg, int64_t n, int k, int kp,
-                                                             int32_t* __restrict__ out,
-                                                             unsigned long long* __restrict__ reached,
-                                                             unsigned long long* __restrict__ edges) {
-  extern __shared__ int32_t fin_smem[];
+constexpr int kFinV = 128;  // vertices per tile
+constexpr int kFinT = 256;  // threads per CTA
+__global__ void __launch_bounds__(kFinT) k_ms_finish(const int32_t* __restrict__ par,
+                                                    const unsigned long long* __restrict__ seen,
+                                                    const int32_t* __restrict__ inv,
+                                                    const int32_t* __restrict__ outdeg, int64_t n, int k, int lkp,
+                                                    int32_t* __restrict__ out,
+                                                    unsigned long long* __restrict__ reached,
+                                                    unsigned long long* __restrict__ edges) {
+  extern __shared__ int32_t tile[];  // [64][kFinV + 1]
+  __shared__ unsigned long long sv[kFinV];
   __shared__ unsigned long long r[64], d[64];
   const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
-  int32_t* tile = fin_smem + wp * (64 * 33);  // [source][vertex], padded
-  for (int i = threadIdx.x; i < 64; i += blockDim.x) r[i] = d[i] = 0;
-  __syncthreads();
+  const int kp = 1 << lkp, lrq = lkp - 2;  // par row: kp ints = 2^lrq int4s
+  for (int i = threadIdx.x; i < 64; i += kFinT) r[i] = d[i] = 0;
   unsigned long long r0 = 0, r1 = 0, d0 = 0, d1 = 0;
-  const int64_t nw = (int64_t)gridDim.x * kFinWarps;
-  for (int64_t t = blockIdx.x * (int64_t)kFinWarps + wp; t * 32 < n; t += nw) {
-    const int64_t v0 = t * 32, v = v0 + lane;
-    const int32_t w = v < n ? (inv ? __ldg(&inv[v]) : (int32_t)v) : 0;
-    const unsigned long long sv = v < n ? seen[w] : 0ull;
-    const unsigned long long ov = v < n ? (unsigned long long)__ldg(&outdeg[w]) : 0ull;
-    const int rq = kp >> 2;                                  // int4s per par row
-    const int nq = (int)(n - v0 < 32 ? n - v0 : 32) * rq;  // int4s of the tile's rows (contiguous)
+  for (int64_t v0 = blockIdx.x * (int64_t)kFinV; v0 < n; v0 += (int64_t)gridDim.x * kFinV) {
+    const int nv = (int)(n - v0 < kFinV ? n - v0 : kFinV);
+    const int nq = nv << lrq;  // int4s of the tile's rows
     const int4* p4 = reinterpret_cast<const int4*>(par + v0 * kp);
-    int4 q[16];
+    unsigned long long ov = 0;
+    if (threadIdx.x < kFinV) {
+      const int64_t v = v0 + threadIdx.x;
+      const int32_t w = v < n ? (inv ? __ldg(&inv[v]) : (int32_t)v) : 0;
+      sv[threadIdx.x] = v < n ? seen[w] : 0ull;
+      ov = v < n ? (unsigned long long)__ldg(&outdeg[w]) : 0ull;
+    }
+    __syncthreads();
+    int4 q[kFinV * 16 / kFinT];
 #pragma unroll
-    for (int j = 0; j < 16; ++j) q[j] = lane + 32 * j < nq ? __ldg(&p4[lane + 32 * j]) : make_int4(0, 0, 0, 0);
+    for (int j = 0; j < kFinV * 16 / kFinT; ++j) {  // rows of vertices no source reached are never read
+      const int qi = threadIdx.x + kFinT * j;
+      q[j] = qi < nq && sv[qi >> lrq] ? __ldg(&p4[qi]) : make_int4(0, 0, 0, 0);
+    }
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      const int qi = lane + 32 * j, vv = qi / rq, b = (qi - vv * rq) * 4;
+    for (int j = 0; j < kFinV * 16 / kFinT; ++j) {
+      const int qi = threadIdx.x + kFinT * j;
       if (qi < nq) {
-        tile[(b + 0) * 33 + vv] = q[j].x;
-        tile[(b + 1) * 33 + vv] = q[j].y;
-        tile[(b + 2) * 33 + vv] = q[j].z;
-        tile[(b + 3) * 33 + vv] = q[j].w;
+        const int vv = qi >> lrq, b = (qi & ((1 << lrq) - 1)) * 4;
+        tile[(b + 0) * (kFinV + 1) + vv] = q[j].x;
+        tile[(b + 1) * (kFinV + 1) + vv] = q[j].y;
+        tile[(b + 2) * (kFinV + 1) + vv] = q[j].z;
+        tile[(b + 3) * (kFinV + 1) + vv] = q[j].w;
       }
     }
-    __syncwarp();
-    if (v < n)
-      for (int b = 0; b < k; ++b) out[(int64_t)b * n + v] = (sv >> b) & 1ull ? tile[b * 33 + lane] : -1;
-    __syncwarp();
-    if (__ballot_sync(0xffffffffu, sv != 0) == 0) continue;
-#pragma unroll 4
-    for (int j = 0; j < 32; ++j) {
-      const unsigned long long s = __shfl_sync(0xffffffffu, sv, j);
-      const unsigned long long od = __shfl_sync(0xffffffffu, ov, j);
-      const unsigned long long b0 = (s >> lane) & 1ull, b1 = (s >> (lane + 32)) & 1ull;
-      r0 += b0;
-      r1 += b1;
-      d0 += b0 * od;
-      d1 += b1 * od;
+    __syncthreads();
+    // rows: warp wp writes rows wp, wp + 8, ...; a row's segment is kFinV / 32 coalesced stores
+    for (int b = wp; b < k; b += kFinT / 32) {
+#pragma unroll
+      for (int c = 0; c < kFinV / 32; ++c) {
+        const int vv = c * 32 + lane;
+        if (vv < nv) out[(int64_t)b * n + v0 + vv] = (sv[vv] >> b) & 1ull ? tile[b * (kFinV + 1) + vv] : -1;
+      }
     }
+    // stats: warps 0..3 take 32 vertices each; lane counts sources lane and lane + 32
+    if (threadIdx.x < kFinV) {
+      const unsigned long long s_me = sv[threadIdx.x];
+      if (__ballot_sync(0xffffffffu, s_me != 0) != 0) {
+#pragma unroll 4
+        for (int j = 0; j < 32; ++j) {
+          const unsigned long long s = __shfl_sync(0xffffffffu, s_me, j);
+          const unsigned long long od = __shfl_sync(0xffffffffu, ov, j);
+          const unsigned long long b0 = (s >> lane) & 1ull, b1 = (s >> (lane + 32)) & 1ull;
+          r0 += b0;
+          r1 += b1;
+          d0 += b0 * od;
+          d1 += b1 * od;
+        }
+      }
+    }
+    __syncthreads();
   }
   if (r0) { atomicAdd(&r[lane], r0); atomicAdd(&d[lane], d0); }
   if (r1) { atomicAdd(&r[lane + 32], r1); atomicAdd(&d[lane + 32], d1); }
   __syncthreads();
-  for (int i = threadIdx.x; i < k; i += blockDim.x) {
+  for (int i = threadIdx.x; i < k; i += kFinT) {
     if (r[i]) atomicAdd(&reached[i], r[i]);
     if (d[i]) atomicAdd(&edges[i], d[i]);
   }
@@ -565,10 +590,13 @@ gi_status msbfs_t(gi_graph g, int32_t k, const int32_t* sources, const gi_bfs_op
     GI_TRY(M.cnt.alloc(4 * 8 + 2 * 64 * 8));
     GI_TRY(M.src.alloc(64 * 4));
     GI_TRY(M.heavy.alloc((n + 1) * 4));
-    GI_TRY(M.chunks[0].alloc((n + 1) * 4));
-    GI_TRY(M.chunks[1].alloc((n + 1) * 4));
-    size_t tb = 0;
+    GI_TRY(M.chunks[0].alloc((n + 1) * 8));
+    GI_TRY(M.chunks[1].alloc((n + 1) * 8));
+    size_t tb = 0, tb64 = 0;
     GI_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tb, M.chunks[0].as<int32_t>(), M.chunks[1].as<int32_t>(), (int)n, st));
+    GI_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tb64, M.chunks[0].as<long long>(), M.chunks[1].as<long long>(),
+                                          (int)n, st));
+    tb = std::max(tb, tb64);
     GI_TRY(M.scan_tmp.alloc(tb + 16));
     M.scan_bytes = tb;
     GI_CUDA(cudaMemsetAsync(M.cnt.p, 0, 8, st));
@@ -593,7 +621,9 @@ gi_status msbfs_t(gi_graph g, int32_t k, const int32_t* sources, const gi_bfs_op
       M.nhch = hc;
     }
   }
-  const int kp = (k + 7) & ~7;  // whole 32-byte sectors per row
+  int lkp = 3;  // par row: kp = 2^lkp >= k ints (whole 32-byte sectors, power-of-two tiles in the epilogue)
+  while ((1 << lkp) < k) ++lkp;
+  const int kp = 1 << lkp;
   if (M.par.bytes < (size_t)n * kp * 4) GI_TRY(M.par.alloc((size_t)n * kp * 4));
   cudaEvent_t e0 = nullptr, e1 = nullptr, pe0 = nullptr, pe1 = nullptr;
   int64_t pull_examined = 0;
@@ -661,13 +691,13 @@ gi_status msbfs_t(gi_graph g, int32_t k, const int32_t* sources, const gi_bfs_op
       ++pulls;
     } else {
       GI_CUDA(cudaMemsetAsync(A.fnext, 0, n * 8, st));
-      int32_t* cc = M.chunks[0].as<int32_t>();
-      int32_t* cp = M.chunks[1].as<int32_t>();
-      k_ms_chunks<<<grid_for(nact, kMsT, sms, 8), kMsT, 0, st>>>(A.acur, nact, A.outdeg, cc);
+      long long* dd = M.chunks[0].as<long long>();
+      long long* dp = M.chunks[1].as<long long>();
+      k_ms_degs<<<grid_for(nact, kMsT, sms, 8), kMsT, 0, st>>>(A.acur, nact, A.outdeg, dd);
       size_t tb = M.scan_bytes;
-      GI_CUDA(cub::DeviceScan::InclusiveSum(M.scan_tmp.p, tb, cc, cp, (int)nact, st));
+      GI_CUDA(cub::DeviceScan::InclusiveSum(M.scan_tmp.p, tb, dd, dp, (int)nact, st));
       launches += 2;
-      k_ms_push<OffT><<<grid_for((sdeg / kPushChunk + nact) * 32, kMsT, sms, 8), kMsT, 0, st>>>(A, cp);
+      k_ms_push<OffT><<<grid_for((sdeg + kPushChunk - 1) / kPushChunk * 32, kMsT, sms, 8), kMsT, 0, st>>>(A, dp);
     }
     GI_CUDA(cudaGetLastError());
     ++launches;
@@ -695,10 +725,11 @@ gi_status msbfs_t(gi_graph g, int32_t k, const int32_t* sources, const gi_bfs_op
   unsigned long long* hr = cnt + 4;
   GI_CUDA(cudaMemsetAsync(hr, 0, 2 * 64 * 8, st));
   {
-    const size_t smem = (size_t)kFinWarps * 64 * 33 * 4;
+    const size_t smem = (size_t)64 * (kFinV + 1) * 4;
     GI_CUDA(cudaFuncSetAttribute(k_ms_finish, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_ms_finish<<<grid_for(n, 32 * kFinWarps, sms, 3), 32 * kFinWarps, smem, st>>>(
-        M.par.as<int32_t>(), M.seen.as<unsigned long long>(), A.inv, g->outdeg.as<int32_t>(), n, k, kp, d_out, hr, hr + 64);
+    k_ms_finish<<<grid_for(n, kFinV, sms, 6), kFinT, smem, st>>>(
+        M.par.as<int32_t>(), M.seen.as<unsigned long long>(), A.inv, g->outdeg.as<int32_t>(), n, k, lkp, d_out, hr,
+        hr + 64);
   }
   ++launches;
   std::vector<unsigned long long> hs(128);

@@ -2,7 +2,7 @@
 # per-kernel durations of one bit-parallel multi-source BFS batch (config 2)
 bash tools/gpu/bfs_batch_ab.sh bitparallel
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/msbfs_launches.csv \
-  python /tmp/bb.py 2 bitparallel > /dev/null 2>&1
+  python tools/bfs_batch.py 2 bitparallel > /dev/null 2>&1
 python - <<'PY'
 import csv, collections
 import io

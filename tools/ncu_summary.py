@@ -68,12 +68,15 @@ def main():
         for d in launches:
             k = d["kernel"]
             for key, name in (("k_pr_seg", "pr_seg"), ("k_pr_acc", "pr_acc"), ("k_pr_pull", "pr_direct"),
-                              ("k_bfs_fused", "bfs_fused")):
+                              ("k_bfs_fused", "bfs_fused"), ("k_ms_pull_heavy", "ms_pull_heavy"),
+                              ("k_ms_pull<", "ms_pull_light"), ("k_ms_push", "ms_push"),
+                              ("k_ms_finish", "ms_finish")):
                 if key in k:
                     a = agg.setdefault(name, {"launches": 0, "dram_bytes": 0.0, "duration_ns": 0.0})
                     a["launches"] += 1
                     a["dram_bytes"] += d.get("dram_read", 0) + d.get("dram_write", 0)
                     a["duration_ns"] += d.get("duration_ns", 0)
+                    break
         for a in agg.values():
             a["dram_bytes_per_launch"] = a["dram_bytes"] / a["launches"]
             a["duration_us_per_launch"] = a["duration_ns"] / a["launches"] / 1e3
@@ -81,6 +84,11 @@ def main():
             agg["pr_pull"] = {"dram_bytes_per_launch": agg["pr_seg"]["dram_bytes_per_launch"] +
                               agg["pr_acc"]["dram_bytes_per_launch"],
                               "note": "per PageRank iteration: k_pr_seg + k_pr_acc"}
+        if "ms_pull_light" in agg:  # one bit-parallel pull level = light-row kernel + heavy-row kernel
+            lv = agg["ms_pull_light"]["launches"]
+            tot = agg["ms_pull_light"]["dram_bytes"] + agg.get("ms_pull_heavy", {}).get("dram_bytes", 0.0)
+            agg["bfs_pull"] = {"dram_bytes_per_launch": tot / lv, "levels": lv,
+                               "note": "per bit-parallel pull level: k_ms_pull + k_ms_pull_heavy"}
         old = json.load(open(js)) if os.path.exists(js) else {}
         old.update(agg)  # merge with summaries of other captures (PR and BFS are captured separately)
         old.setdefault("sources", [])
