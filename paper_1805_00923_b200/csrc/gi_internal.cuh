@@ -9,7 +9,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdlib>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "gi.h"
@@ -124,7 +126,8 @@ struct gi_graph_s {
   gi::DevBuf seg_rec;      // records: long (lane-aligned) and short (lane-per-piece), pr_segmented.cu
   gi::DevBuf seg_unit_c0;  // int32[U+1]: first record of each (block, segment) unit
   gi::DevBuf seg_cta;      // int32[CTAs+1]: cost-balanced record range of each CTA
-  std::vector<int32_t> seg_h_cta;  // host copy of seg_cta
+  std::vector<int32_t> seg_h_cta;  // host copy of seg_cta's record starts
+  std::vector<int32_t> seg_h_uc;   // host copy of seg_unit_c0
   gi::DevBuf seg_time;     // uint64[4*CTAs]: per-CTA timings of the last calibrated launch
   int seg_calib = 0;       // edge passes left that re-balance the CTA ranges from measured timings
   gi::DevBuf seg_acc;      // float[2][seg_acc_stride]: per-row sums (ping-pong), L2-resident
@@ -208,6 +211,26 @@ inline cudaError_t stream_wait(cudaStream_t st) {
 }
 // util
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+// launch with programmatic stream serialization (the kernel calls griddepcontrol.wait
+// before touching its predecessor's data); GI_PDL=0 turns it off for A/B runs
+template <typename... KArgs, typename... Args>
+inline gi_status launch_pdl(void (*kern)(KArgs...), int grid, int block, size_t smem, cudaStream_t st,
+                            Args&&... args) {
+  static const bool on = !getenv("GI_PDL") || atoi(getenv("GI_PDL")) != 0;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3((unsigned)block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = on ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  GI_CUDA(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
+  return GI_OK;
+}
+
 inline int grid_for(int64_t work, int threads, int num_sms, int per_sm = 8) {
   int64_t g = ceil_div(work, threads);
   int64_t cap = (int64_t)num_sms * per_sm;

@@ -78,6 +78,11 @@ constexpr int kStageBytes = kConsumers * kRecBytes;
 // CTA balance: an initial cost model (in gather slots), then refined from
 // measured per-CTA times over the first kCalibPasses edge passes (seg_rebalance)
 constexpr int kPieceCost = 4;
+#ifndef GI_SEG_DIRECT
+#define GI_SEG_DIRECT 16
+#endif
+constexpr int kDirectRecs = GI_SEG_DIRECT;  // units with fewer records gather from global memory (no staging)
+constexpr int kDirectCost = 5;              // cost factor of a record of such a unit (L2 vs shared-memory gathers)
 constexpr int64_t kUnitCost = 40 * kChunkE;         // a unit start: segment staging + pipeline refill
 constexpr int64_t kDefaultBlockRows = 8 << 20;      // 32 MB accumulator per destination block
 #ifndef GI_SEG_CALIB
@@ -92,12 +97,20 @@ struct SegArgs {
   const uint8_t* __restrict__ rec;     // kRecBytes per record
   const int32_t* __restrict__ unit_c0; // U + 1: first record of each unit
   const int32_t* __restrict__ cta_c0;  // grid + 1: first record of each CTA
+  const int32_t* __restrict__ cta_u;   // grid: unit of each CTA's first record
   const float* __restrict__ cin;       // contrib, global ids, padded by >= 16 floats
   float* __restrict__ acc;             // per local row (+ trash row at nr)
   int64_t n;
   int Z, S, U;
   unsigned long long* timing;  // per CTA [start, end, staging ns, units] (balance calibration, diagnostics)
 };
+
+// programmatic dependent launch (the edge and vertex passes of consecutive
+// iterations are launched with cudaLaunchAttributeProgrammaticStreamSerialization):
+// a kernel lets its successor be scheduled as soon as all its CTAs run, and
+// waits for its predecessor's completion and memory before touching its data
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 __device__ __forceinline__ unsigned long long globaltimer() {
   unsigned long long t;
@@ -138,10 +151,19 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
+// a contrib value of the unit's segment: from the staged copy in shared memory,
+// or (G: a sparse unit, not staged) straight from global memory; offset Z is
+// the zero slot that padding slots point at
+template <bool G>
+__device__ __forceinline__ float seg_val(const float* sc, uint32_t o, uint32_t Z) {
+  if (G) return o < Z ? __ldg(sc + o) : 0.f;
+  return sc[o];
+}
+
 // Long record: every lane's 16 slots belong to one piece, so a lane sums its
 // gathers; a warp segmented scan over lanes (reset where the mask marks a
 // piece start) leaves each piece's sum in its last lane, which folds it into acc.
-template <int MODE>
+template <int MODE, bool G>
 __device__ __forceinline__ void reduce_long(const SegArgs& A, const uint8_t* r, const float* sc, int lane,
                                             uint64_t* empty) {
   const uint4 qa = *reinterpret_cast<const uint4*>(r + kRecHdr + 32 * lane);
@@ -155,8 +177,8 @@ __device__ __forceinline__ void reduce_long(const SegArgs& A, const uint8_t* r, 
   float v[kLaneE];
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
-    v[2 * j] = sc[w[j] & 0xFFFFu];
-    v[2 * j + 1] = sc[w[j] >> 16];
+    v[2 * j] = seg_val<G>(sc, w[j] & 0xFFFFu, A.Z);
+    v[2 * j + 1] = seg_val<G>(sc, w[j] >> 16, A.Z);
   }
 #pragma unroll
   for (int s = 1; s < kLaneE; s <<= 1)
@@ -178,7 +200,7 @@ __device__ __forceinline__ void reduce_long(const SegArgs& A, const uint8_t* r, 
 
 // Short record of pieces with exactly L edges: lane l of group g owns one
 // piece: L gathers, one RED.
-template <int MODE>
+template <int MODE, bool G>
 __device__ __forceinline__ void reduce_short(const SegArgs& A, const uint8_t* r, const float* sc, int lane,
                                              uint64_t* empty) {
   const int L = *reinterpret_cast<const int32_t*>(r + 4);
@@ -189,7 +211,7 @@ __device__ __forceinline__ void reduce_short(const SegArgs& A, const uint8_t* r,
     const int d = *reinterpret_cast<const int32_t*>(r + kRecHdr + g * gb + 64 * L + 4 * lane);
     float s = 0.f;
 #pragma unroll 4
-    for (int k = 0; k < L; ++k) s += sc[*reinterpret_cast<const uint16_t*>(b + 64 * k)];
+    for (int k = 0; k < L; ++k) s += seg_val<G>(sc, *reinterpret_cast<const uint16_t*>(b + 64 * k), A.Z);
     if (MODE == 1) {
       if (s == -1.f) A.acc[lane] += s;
     } else {
@@ -200,7 +222,7 @@ __device__ __forceinline__ void reduce_short(const SegArgs& A, const uint8_t* r,
   if (lane == 0) mbar_arrive(empty);
 }
 
-template <int MODE>
+template <int MODE, bool G>
 __device__ __forceinline__ void reduce_record(const SegArgs& A, const uint8_t* r, const float* sc, int lane,
                                               uint64_t* empty) {
   const int type = *reinterpret_cast<const int32_t*>(r);
@@ -210,8 +232,8 @@ __device__ __forceinline__ void reduce_record(const SegArgs& A, const uint8_t* r
     if (type == 7) A.acc[lane] += 1.f;
     return;
   }
-  if (type == 1) reduce_long<MODE>(A, r, sc, lane, empty);
-  else reduce_short<MODE>(A, r, sc, lane, empty);
+  if (type == 1) reduce_long<MODE, G>(A, r, sc, lane, empty);
+  else reduce_short<MODE, G>(A, r, sc, lane, empty);
 }
 
 // Persistent CTA per SM over records [cta_c0[b], cta_c0[b+1]), unit by unit.
@@ -232,7 +254,6 @@ __global__ void __launch_bounds__(kSegThreads, 1) k_pr_seg(SegArgs A) {
   const int c1 = A.cta_c0[blockIdx.x + 1];
   if (c0 >= c1) return;
   unsigned long long t_start = 0, t_stage = 0, n_units = 0;
-  if (A.timing && tid == 0) t_start = globaltimer();
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
@@ -240,25 +261,25 @@ __global__ void __launch_bounds__(kSegThreads, 1) k_pr_seg(SegArgs A) {
     }
     mbar_init(&seg_bar, 1);
   }
+  int u = __ldg(&A.cta_u[blockIdx.x]);  // unit of c0
+  pdl_launch_dependents();
   __syncthreads();
-  int u;  // unit of c0: last u with unit_c0[u] <= c0
-  {
-    int lo = 0, hi = A.U - 1;
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (__ldg(&A.unit_c0[mid]) <= c0) lo = mid;
-      else hi = mid - 1;
-    }
-    u = lo;
-  }
+  pdl_wait();  // the previous vertex pass wrote cin and cleared acc
+  if (A.timing && tid == 0) t_start = globaltimer();
   uint32_t it = 0;  // stages issued (producer) / consumed (consumers), over all units
   uint32_t seg_phase = 0;
   int staged_seg = -1;
   while (c0 < c1) {
-    const int ue = min(c1, __ldg(&A.unit_c0[u + 1]));
+    int uend = __ldg(&A.unit_c0[u + 1]);
+    // a sparse unit gathers from global memory instead of staging its segment;
+    // a run of consecutive sparse units streams as one span (records carry their segment)
+    const bool direct = uend - __ldg(&A.unit_c0[u]) < kDirectRecs;
+    if (direct)
+      while (uend < c1 && u + 1 < A.U && __ldg(&A.unit_c0[u + 2]) - uend < kDirectRecs) uend = __ldg(&A.unit_c0[++u + 1]);
+    const int ue = min(c1, uend);
     const int seg = u % A.S;
-    const int nst = (ue - c0 + kConsumers - 1) / kConsumers;  // stages in this unit
-    const bool restage = seg != staged_seg;
+    const int nst = (ue - c0 + kConsumers - 1) / kConsumers;  // stages in this unit (span)
+    const bool restage = !direct && seg != staged_seg;
     if (restage) {
       __syncthreads();  // every consumer is done with the previous segment
       if (tid == 0) {
@@ -291,7 +312,12 @@ __global__ void __launch_bounds__(kSegThreads, 1) k_pr_seg(SegArgs A) {
         mbar_wait(&full[s], ph);
         const int c = c0 + k * kConsumers + warp;
         const uint8_t* r = ring + s * kStageBytes + warp * kRecBytes;
-        if (c < ue) reduce_record<MODE>(A, r, scontrib, lane, &empty[s]);
+        if (c < ue) {
+          if (direct)
+            reduce_record<MODE, true>(A, r, A.cin + (int64_t)*reinterpret_cast<const int32_t*>(r + 12) * A.Z, lane,
+                                      &empty[s]);
+          else reduce_record<MODE, false>(A, r, scontrib, lane, &empty[s]);
+        }
         else if (lane == 0) {
           mbar_arrive(&empty[s]);  // nothing to take from this slot
         }
@@ -315,6 +341,8 @@ __global__ void __launch_bounds__(kSegThreads, 1) k_pr_seg(SegArgs A) {
 // then pr_epilogue's arithmetic; zero[v] = 0 readies the other accumulator.
 __global__ void __launch_bounds__(256) k_pr_acc(PrArgs A, const float* __restrict__ acc, float* __restrict__ zero) {
   __shared__ double sred[32];
+  pdl_launch_dependents();
+  pdl_wait();  // the edge pass's accumulator
   if (blockIdx.x == 0 && threadIdx.x == 0) A.dbuf[(A.it + 2) % 3] = 0.0;
   const double D = A.uniform ? A.dbuf[A.it % 3] : 0.0;
   const float dn = (float)(D * A.inv_n);
@@ -469,7 +497,7 @@ __global__ void k_long_dst(const int64_t* __restrict__ asz, const int64_t* __res
 // headers of all records; short records also get padding lanes (index Z, trash row)
 __global__ void k_record_headers(const int32_t* __restrict__ rtype, const int32_t* __restrict__ rL,
                                  const int32_t* __restrict__ rng, int64_t C, int Z, int trash,
-                                 uint8_t* __restrict__ rec) {
+                                 const int32_t* __restrict__ unit_c0, int U, int S, uint8_t* __restrict__ rec) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < C * (kRecBytes / 4);
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t c = i / (kRecBytes / 4);
@@ -479,7 +507,15 @@ __global__ void k_record_headers(const int32_t* __restrict__ rtype, const int32_
     if (o == 0) *w = (uint32_t)type;
     else if (o == 4) *w = (uint32_t)rL[c];
     else if (o == 8) *w = (uint32_t)rng[c];
-    else if (o >= kRecHdr) {
+    else if (o == 12) {  // the record's source segment (read when its unit is gathered unstaged)
+      int lo = 0, hi = U - 1;  // last unit u with unit_c0[u] <= c
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (unit_c0[mid] <= c) lo = mid;
+        else hi = mid - 1;
+      }
+      *w = (uint32_t)(lo % S);
+    } else if (o >= kRecHdr) {
       if (type == 1) {
         if (o < kLDst) *w = (uint32_t)Z | ((uint32_t)Z << 16);  // idx padding (overwritten by real slots)
       } else {
@@ -541,6 +577,8 @@ static gi_status sort_pairs(const K* ki, K* ko, const V* vi, V* vo, int64_t n, i
 }
 
 }  // namespace
+
+static gi_status seg_upload_ctas(gi_graph g);
 
 template <typename OffT>
 static gi_status seg_build_t(gi_graph g, int Z, int64_t DB) {
@@ -676,7 +714,8 @@ static gi_status seg_build_t(gi_graph g, int Z, int64_t DB) {
   GI_CUDA(cudaMemsetAsync(g->seg_rec.p, 0, C * kRecBytes + 16, st));
   const int trash = (int)n;  // accumulator row past the owned rows
   k_record_headers<<<grid_for(C * (kRecBytes / 4), 256, sms), 256, 0, st>>>(
-      rtype.as<int32_t>(), rL.as<int32_t>(), rng.as<int32_t>(), C, Z, trash, g->seg_rec.as<uint8_t>());
+      rtype.as<int32_t>(), rL.as<int32_t>(), rng.as<int32_t>(), C, Z, trash, unit_c0.as<int32_t>(), (int)U, S,
+      g->seg_rec.as<uint8_t>());
   k_place_long<OffT><<<grid_for(P, 256, sms), 256, 0, st>>>(
       asz.as<int64_t>(), aoff.as<int64_t>(), punit.as<int32_t>(), unit_p0.as<int64_t>(), unit_c0.as<int32_t>(),
       pstart.as<int64_t>(), skey.as<uint32_t>(), order.as<OffT>(), idx, pdst.as<int32_t>(), P, m, Z, S,
@@ -688,7 +727,7 @@ static gi_status seg_build_t(gi_graph g, int Z, int64_t DB) {
     k_place_short<OffT><<<grid_for(NS, 256, sms), 256, 0, st>>>(
         sckey.as<uint32_t>(), spid.as<int32_t>(), NS, cstart.as<int64_t>(), crec0.as<int32_t>(), pstart.as<int64_t>(),
         skey.as<uint32_t>(), order.as<OffT>(), idx, pdst.as<int32_t>(), Z, S, g->seg_rec.as<uint8_t>());
-  // ---- cost-balanced CTA ranges (every unit start adds kUnitCost)
+  // ---- cost-balanced CTA ranges (every staged unit start adds kUnitCost)
   const int ctas = sms;
   std::vector<int32_t> h_cta(ctas + 1, (int32_t)C);
   {
@@ -696,8 +735,9 @@ static gi_status seg_build_t(gi_graph g, int Z, int64_t DB) {
     int u = 0;
     for (int64_t c = 0; c < C; ++c) {
       int64_t cost = h_cost[c];
-      while (u < U && h_uc[u] < c) ++u;
-      if (u < U && h_uc[u] == c) cost += kUnitCost;
+      while (u + 1 < U && h_uc[u + 1] <= c) ++u;  // u: the unit holding record c
+      if (h_uc[u + 1] - h_uc[u] < kDirectRecs) cost *= kDirectCost;  // unstaged: L2 gathers
+      else if (h_uc[u] == c) cost += kUnitCost;
       pre[c + 1] = pre[c] + cost;
     }
     int64_t c = 0;
@@ -711,11 +751,12 @@ static gi_status seg_build_t(gi_graph g, int Z, int64_t DB) {
   }
   GI_TRY(g->seg_unit_c0.alloc((U + 1) * sizeof(int32_t)));
   GI_CUDA(cudaMemcpyAsync(g->seg_unit_c0.p, h_uc.data(), (U + 1) * sizeof(int32_t), cudaMemcpyHostToDevice, st));
-  GI_TRY(g->seg_cta.alloc((ctas + 1) * sizeof(int32_t)));
-  GI_CUDA(cudaMemcpyAsync(g->seg_cta.p, h_cta.data(), (ctas + 1) * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+  GI_TRY(g->seg_cta.alloc((2 * ctas + 1) * sizeof(int32_t)));
   g->seg_h_cta = h_cta;
+  g->seg_h_uc = h_uc;
+  GI_TRY(seg_upload_ctas(g));
   GI_TRY(g->seg_time.alloc(4 * ctas * sizeof(unsigned long long)));
-  g->seg_calib = getenv("GI_SEG_NO_CALIB") ? 0 : kCalibPasses;
+  g->seg_calib = getenv("GI_SEG_NO_CALIB") ? 0 : getenv("GI_SEG_CALIB") ? atoi(getenv("GI_SEG_CALIB")) : kCalibPasses;
   g->seg_acc_stride = (n + 64) & ~31ll;  // >= n + 1: row n is the trash row of padding lanes
   GI_TRY(g->seg_acc.alloc(2 * g->seg_acc_stride * sizeof(float)));
   GI_CUDA(cudaMemsetAsync(g->seg_acc.p, 0, 2 * g->seg_acc_stride * sizeof(float), st));
@@ -765,10 +806,24 @@ static gi_status seg_rebalance(gi_graph g, const std::vector<unsigned long long>
     const double frac = T[k] > 0.0 ? (target - before) / T[k] : 0.0;
     nc[j] = std::max(nc[j - 1], std::min(hc[k + 1], hc[k] + (int32_t)(frac * len + 0.5)));
   }
+  static const double damp = getenv("GI_SEG_DAMP") ? atof(getenv("GI_SEG_DAMP")) : GI_SEG_DAMP;
   for (int j = 1; j < ctas; ++j)  // damped move from the old boundary
-    nc[j] = std::max(nc[j - 1], (int32_t)(hc[j] + GI_SEG_DAMP * (nc[j] - hc[j]) + 0.5));
+    nc[j] = std::max(nc[j - 1], (int32_t)(hc[j] + damp * (nc[j] - hc[j]) + 0.5));
   hc = nc;
-  GI_CUDA(cudaMemcpyAsync(g->seg_cta.p, hc.data(), (ctas + 1) * sizeof(int32_t), cudaMemcpyHostToDevice,
+  return seg_upload_ctas(g);
+}
+
+// seg_cta = [record start of each CTA (ctas + 1)] ++ [unit of each CTA's first record (ctas)]
+static gi_status seg_upload_ctas(gi_graph g) {
+  const std::vector<int32_t>& hc = g->seg_h_cta;
+  const std::vector<int32_t>& uc = g->seg_h_uc;
+  const int ctas = (int)hc.size() - 1;
+  std::vector<int32_t> buf(hc);
+  buf.resize(2 * ctas + 1);
+  for (int c = 0; c < ctas; ++c)  // last unit u with unit_c0[u] <= hc[c]
+    buf[ctas + 1 + c] = std::max<int32_t>(0, (int32_t)(std::upper_bound(uc.begin(), uc.end() - 1, hc[c]) - uc.begin()) - 1);
+  // pageable source: the call returns once buf has been staged
+  GI_CUDA(cudaMemcpyAsync(g->seg_cta.p, buf.data(), buf.size() * sizeof(int32_t), cudaMemcpyHostToDevice,
                           g->ctx->stream));
   return GI_OK;
 }
@@ -800,6 +855,7 @@ gi_status seg_edge_pass(gi_graph g, const float* cin) {
   S.rec = g->seg_rec.as<uint8_t>();
   S.unit_c0 = g->seg_unit_c0.as<int32_t>();
   S.cta_c0 = g->seg_cta.as<int32_t>();
+  S.cta_u = g->seg_cta.as<int32_t>() + g->seg_ctas + 1;
   S.cin = cin;
   S.acc = seg_acc_buf(g, g->seg_acc_cur);
   S.n = g->n;
@@ -824,8 +880,7 @@ gi_status seg_edge_pass(gi_graph g, const float* cin) {
     GI_CUDA(cudaMemsetAsync(g->seg_time.p, 0, 4 * ctas * sizeof(unsigned long long), st));
     S.timing = g->seg_time.as<unsigned long long>();
   }
-  kern<<<ctas, kSegThreads, dyn, st>>>(S);
-  GI_CUDA(cudaGetLastError());
+  GI_TRY(launch_pdl(kern, ctas, kSegThreads, dyn, st, S));
   if (!timed) return GI_OK;
   std::vector<unsigned long long> ht(4 * ctas);
   GI_CUDA(cudaMemcpyAsync(ht.data(), g->seg_time.p, ht.size() * 8, cudaMemcpyDeviceToHost, st));
@@ -848,9 +903,8 @@ gi_status seg_edge_pass(gi_graph g, const float* cin) {
 
 gi_status seg_vertex_pass(gi_graph g, const PrArgs& A) {
   cudaStream_t st = g->ctx->stream;
-  k_pr_acc<<<grid_for(ceil_div(g->nr, 4), 256, g->ctx->num_sms, 4), 256, 0, st>>>(
-      A, seg_acc_buf(g, g->seg_acc_cur), seg_acc_buf(g, g->seg_acc_cur ^ 1));
-  GI_CUDA(cudaGetLastError());
+  GI_TRY(launch_pdl(k_pr_acc, grid_for(ceil_div(g->nr, 4), 256, g->ctx->num_sms, 4), 256, 0, st, A,
+                    (const float*)seg_acc_buf(g, g->seg_acc_cur), seg_acc_buf(g, g->seg_acc_cur ^ 1)));
   g->seg_acc_cur ^= 1;
   return GI_OK;
 }

@@ -1,7 +1,7 @@
 #!/usr/bin/env python3
 """PageRank (20 iterations) and BFS timings of every single-GPU BASELINE config.
 
-    python tools/perf_configs.py [configs...]   (default: 1 2 3 4)
+    python tools/perf_configs.py [configs...]   (default: 1 2 3 4; 5 needs ~150 GB of HBM)
 
 Prints one JSON line per config: build ms, PR ms/iteration and GTEPS, the PR
 kernel chosen, BFS ms/source (gi_bfs_multi) and GTEPS, levels and edges
@@ -24,7 +24,7 @@ cfgs = [int(a) for a in sys.argv[1:]] or [1, 2, 3, 4]
 ctx = gi.Context(0)
 for ci in cfgs:
     cfg = graphgen.CONFIGS[ci]
-    if cfg.kind == "rmat" and ci == 4:
+    if cfg.kind == "rmat" and ci in (4, 5):  # billion-edge configs: the device twin of the generator
         a, b, c, _ = cfg.abcd
         ts, td = graphgen.rmat_device(cfg.scale, cfg.edge_factor, a, b, c, cfg.seed)
         s = d = None

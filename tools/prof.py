@@ -25,11 +25,21 @@ ap.add_argument("--direction", default="pull")
 args = ap.parse_args()
 
 cfg = graphgen.CONFIGS[args.config]
-s, d = cfg.edges()
-srcs = cfg.sources(s, d)
+if args.config in (4, 5):  # billion-edge configs: device generator, sources = first vertices with out-edges
+    a, b, c, _ = cfg.abcd
+    ts, td = graphgen.rmat_device(cfg.scale, cfg.edge_factor, a, b, c, cfg.seed)
+    srcs = None
+else:
+    s, d = cfg.edges()
+    srcs = cfg.sources(s, d)
+    ts, td = torch.from_numpy(s).cuda(), torch.from_numpy(d).cuda()
 ctx = gi.Context(0)
 flags = gi.GI_DEFAULT_FLAGS | (gi.GI_SYMMETRIZE if cfg.symmetrize else 0)
-g = gi.Graph(ctx, cfg.n, torch.from_numpy(s).cuda(), torch.from_numpy(d).cuda(), flags | gi.GI_EDGES_ON_DEVICE)
+g = gi.Graph(ctx, cfg.n, ts, td, flags | gi.GI_EDGES_ON_DEVICE)
+del ts, td
+if srcs is None:
+    od = g.out_degrees(torch.empty(cfg.n, dtype=torch.int32, device="cuda"))
+    srcs = torch.nonzero(od > 0).flatten()[:max(args.bfs, 1)].cpu().numpy()
 out = torch.empty(cfg.n, dtype=torch.float32, device="cuda")
 par = torch.empty(cfg.n, dtype=torch.int32, device="cuda")
 direction = {"pull": gi.GI_PR_PULL, "push": gi.GI_PR_PUSH, "direct": gi.GI_PR_PULL_DIRECT,
