@@ -128,6 +128,7 @@ struct gi_graph_s {
   gi::DevBuf seg_cta;      // int32[CTAs+1]: cost-balanced record range of each CTA
   std::vector<int32_t> seg_h_cta;  // host copy of seg_cta's record starts
   std::vector<int32_t> seg_h_uc;   // host copy of seg_unit_c0
+  std::vector<int64_t> seg_h_model;  // prefix of the per-record cost model (C + 1)
   gi::DevBuf seg_time;     // uint64[4*CTAs]: per-CTA timings of the last calibrated launch
   int seg_calib = 0;       // edge passes left that re-balance the CTA ranges from measured timings
   gi::DevBuf seg_acc;      // float[2][seg_acc_stride]: per-row sums (ping-pong), L2-resident

@@ -748,6 +748,7 @@ static gi_status seg_build_t(gi_graph g, int Z, int64_t DB) {
       h_cta[k] = (int32_t)c;
     }
     h_cta[ctas] = (int32_t)C;
+    g->seg_h_model.swap(pre);  // the model's prefix: the shape of cost inside a range when re-balancing
   }
   GI_TRY(g->seg_unit_c0.alloc((U + 1) * sizeof(int32_t)));
   GI_CUDA(cudaMemcpyAsync(g->seg_unit_c0.p, h_uc.data(), (U + 1) * sizeof(int32_t), cudaMemcpyHostToDevice, st));
@@ -797,14 +798,20 @@ static gi_status seg_rebalance(gi_graph g, const std::vector<unsigned long long>
   std::vector<int32_t> nc(ctas + 1);
   nc[0] = 0;
   nc[ctas] = hc[ctas];
+  // inside CTA k's range the measured time T[k] is spread over the records in
+  // proportion to the build's cost model (dense staged records, sparse unstaged
+  // ones and segment stagings cost very differently)
+  const std::vector<int64_t>& pm = g->seg_h_model;
   int k = 0;
   double before = 0.0;  // cost of CTA ranges < k
   for (int j = 1; j < ctas; ++j) {
     const double target = total * j / ctas;
     while (k < ctas - 1 && before + T[k] < target) before += T[k++];
-    const int32_t len = hc[k + 1] - hc[k];
     const double frac = T[k] > 0.0 ? (target - before) / T[k] : 0.0;
-    nc[j] = std::max(nc[j - 1], std::min(hc[k + 1], hc[k] + (int32_t)(frac * len + 0.5)));
+    const double mk = (double)(pm[hc[k + 1]] - pm[hc[k]]);
+    const int64_t want = pm[hc[k]] + (int64_t)(frac * mk);  // model position of the cut
+    const int32_t cut = (int32_t)(std::lower_bound(pm.begin() + hc[k], pm.begin() + hc[k + 1], want) - pm.begin());
+    nc[j] = std::max(nc[j - 1], std::min(hc[k + 1], cut));
   }
   static const double damp = getenv("GI_SEG_DAMP") ? atof(getenv("GI_SEG_DAMP")) : GI_SEG_DAMP;
   for (int j = 1; j < ctas; ++j)  // damped move from the old boundary
@@ -888,9 +895,21 @@ gi_status seg_edge_pass(gi_graph g, const float* cin) {
   const std::vector<int32_t>& hc = g->seg_h_cta;
   if (dbg) {
     if (FILE* f = fopen(dbg, "a")) {
-      for (int c = 0; c < ctas; ++c)
-        fprintf(f, "%d,%d,%d,%llu,%llu,%llu,%llu\n", c, hc[c], hc[c + 1], ht[4 * c], ht[4 * c + 1], ht[4 * c + 2],
-                ht[4 * c + 3]);
+      const std::vector<int32_t>& uc = g->seg_h_uc;
+      for (int c = 0; c < ctas; ++c) {
+        // + records in unstaged (sparse) units, staged units touched, first unit, last unit
+        int u = std::max<int>(0, (int)(std::upper_bound(uc.begin(), uc.end() - 1, hc[c]) - uc.begin()) - 1);
+        const int ufirst = u;
+        long long drec = 0, su = 0;
+        for (int32_t r = hc[c]; r < hc[c + 1]; ++r) {
+          while (u + 1 < (int)uc.size() - 1 && uc[u + 1] <= r) ++u;
+          const bool direct = uc[u + 1] - uc[u] < kDirectRecs;
+          if (direct) ++drec;
+          else if (r == hc[c] || uc[u] == r) ++su;
+        }
+        fprintf(f, "%d,%d,%d,%llu,%llu,%llu,%llu,%lld,%lld,%d,%d\n", c, hc[c], hc[c + 1], ht[4 * c], ht[4 * c + 1],
+                ht[4 * c + 2], ht[4 * c + 3], drec, su, ufirst, u);
+      }
       fclose(f);
     }
   }

@@ -5,7 +5,8 @@ import numpy as np
 
 rows = [list(map(int, l.split(","))) for l in open(sys.argv[1]) if l.strip()]
 ctas = max(r[0] for r in rows) + 1
-last = np.array(rows[-ctas:], dtype=np.float64)[:, :7]
+full = np.array(rows[-ctas:], dtype=np.float64)
+last = full[:, :7]
 t0 = last[:, 3].min()
 start, end, stage, units = last[:, 3] - t0, last[:, 4] - t0, last[:, 5], last[:, 6]
 pieces = last[:, 7] if last.shape[1] > 7 else np.zeros(len(last))
@@ -26,3 +27,9 @@ coef, *_ = np.linalg.lstsq(X, dur, rcond=None)
 pred = X @ coef
 print(f"fit busy ~ {coef[0]:.1f} ns/chunk + {coef[1]:.2f} ns/piece + {coef[2]:.0f} ns/unit; "
       f"rms err {np.sqrt(np.mean((pred - dur) ** 2)) / 1e3:.2f} us; balanced span ~ {dur.sum() / len(dur) / 1e3:.1f} us")
+
+if full.shape[1] >= 11:  # + unstaged records, staged units, first and last unit per CTA
+    order = np.argsort(-dur)[:8]
+    print("slowest CTAs: cta busy_us records unstaged_records staged_units units[first..last]")
+    for q in order:
+        print(f"  {q:3d} {dur[q] / 1e3:7.1f} {chunks[q]:6.0f} {full[q, 7]:6.0f} {full[q, 8]:4.0f} [{full[q, 9]:.0f}..{full[q, 10]:.0f}]")
