@@ -86,7 +86,7 @@ constexpr int kDirectCost = 5;              // cost factor of a record of such a
 constexpr int64_t kUnitCost = 40 * kChunkE;         // a unit start: segment staging + pipeline refill
 constexpr int64_t kDefaultBlockRows = 8 << 20;      // 32 MB accumulator per destination block
 #ifndef GI_SEG_CALIB
-#define GI_SEG_CALIB 3
+#define GI_SEG_CALIB 8
 #endif
 #ifndef GI_SEG_DAMP
 #define GI_SEG_DAMP 1.0  // fraction of the way each re-balance moves a boundary

@@ -1,5 +1,4 @@
-# config 2/4 PR ms/iter: parity subset, then calibration pass counts
-timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -m gpu -k "pr or prdelta" 2>&1 | tail -1
+# config 2/4 PR ms/iter for several calibration pass counts
 for c in 2 4; do
-  for k in 3 8; do echo -n "cfg$c calib=$k  "; GI_SEG_CALIB=$k timeout 600 python tools/prof.py --config $c --pr-iters 20 --pr-reps 2 --bfs 0 2>&1 | tail -1; done
+  for k in 3 5 8; do echo -n "cfg$c calib=$k  "; GI_SEG_CALIB=$k timeout 600 python tools/prof.py --config $c --pr-iters 20 --pr-reps 2 --bfs 0 2>&1 | tail -1; done
 done
