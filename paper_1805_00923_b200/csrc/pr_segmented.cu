@@ -85,6 +85,7 @@ constexpr int kDirectRecs = GI_SEG_DIRECT;  // units with fewer records gather f
 constexpr int kDirectCost = 5;              // cost factor of a record of such a unit (L2 vs shared-memory gathers)
 constexpr int64_t kUnitCost = 40 * kChunkE;         // a unit start: segment staging + pipeline refill
 constexpr int64_t kDefaultBlockRows = 8 << 20;      // 32 MB accumulator per destination block
+constexpr int64_t kBlockEdges = (1ll << 31) - (1ll << 20);  // and fewer edges than the build's 32-bit sorts take
 #ifndef GI_SEG_CALIB
 #define GI_SEG_CALIB 8
 #endif
@@ -382,12 +383,14 @@ __global__ void __launch_bounds__(256) k_pr_acc(PrArgs A, const float* __restric
 // ---------------------------------------------------------------- layout build
 // row of every CSC edge (warp per row)
 template <typename OffT>
-__global__ void k_edge_rows(const OffT* __restrict__ off, int64_t n, int32_t* __restrict__ row) {
+// (rows [r0, r0 + n) of the CSC, whose edges start at e0: row[e - e0] = r0 + v)
+__global__ void k_edge_rows(const OffT* __restrict__ off, int64_t n, int64_t e0, int64_t r0,
+                            int32_t* __restrict__ row) {
   const int lane = threadIdx.x & 31;
   const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t v = w0; v < n; v += nw)
-    for (int64_t e = (int64_t)off[v] + lane; e < (int64_t)off[v + 1]; e += 32) row[e] = (int32_t)v;
+    for (int64_t e = (int64_t)off[v] + lane; e < (int64_t)off[v + 1]; e += 32) row[e - e0] = (int32_t)(r0 + v);
 }
 
 // unit key of every edge and its position (the sort payload)
@@ -580,22 +583,46 @@ static gi_status sort_pairs(const K* ki, K* ko, const V* vi, V* vo, int64_t n, i
 
 static gi_status seg_upload_ctas(gi_graph g);
 
+// the records of one destination block (CSC rows [r0, r1), fewer than 2^31
+// edges): units (block, segment) for every segment, in segment order
+struct SegBlock {
+  DevBuf rec;                   // C records
+  std::vector<int32_t> uc;      // S + 1: first record of each unit (block-local)
+  std::vector<int64_t> cost;    // per record, for the CTA balance
+  int64_t C = 0, CL = 0, NS = 0, P = 0;
+};
+
 template <typename OffT>
-static gi_status seg_build_t(gi_graph g, int Z, int64_t DB) {
+static gi_status seg_build_block(gi_graph g, int Z, int S, int64_t r0, int64_t r1, SegBlock& out) {
   gi_context ctx = g->ctx;
   cudaStream_t st = ctx->stream;
   const int sms = ctx->num_sms;
-  const int64_t n = g->nr, m = g->ml;  // CSC rows (owned destinations) and local edges
-  const OffT* off = g->csc_off.as<OffT>();
-  const int32_t* idx = g->csc_idx.as<int32_t>();
-  const int S = (int)ceil_div(g->n, Z);  // segments over all sources
-  const int B = (int)ceil_div(n, DB);    // destination blocks
-  if ((int64_t)B * S * 16 >= INT32_MAX / 2) return fail(GI_ERR_UNSUPPORTED, "segmented pull: too many units");
-  if (m >= INT32_MAX) return fail(GI_ERR_UNSUPPORTED, "segmented pull: more than 2^31 local edges");
-  const int U = B * S;
+  const int64_t nb = r1 - r0;
+  int64_t e0 = 0, e1 = 0;
+  GI_CUDA(cudaMemcpyAsync(&e0, g->csc_off.as<OffT>() + r0, sizeof(OffT), cudaMemcpyDeviceToHost, st));
+  GI_CUDA(cudaMemcpyAsync(&e1, g->csc_off.as<OffT>() + r1, sizeof(OffT), cudaMemcpyDeviceToHost, st));
+  GI_CUDA(cudaStreamSynchronize(st));
+  if (sizeof(OffT) == 4) {  // the copies filled the low halves
+    e0 = (int64_t)(int32_t)e0;
+    e1 = (int64_t)(int32_t)e1;
+  }
+  const int64_t m = e1 - e0;
+  if (m >= INT32_MAX) return fail(GI_ERR_INTERNAL, "segmented pull: block of 2^31 edges");
+  const OffT* off = g->csc_off.as<OffT>() + r0;
+  const int32_t* idx = g->csc_idx.as<int32_t>() + e0;
+  const int U = S;  // this block's units
+  const int64_t DB = INT64_MAX;  // one block: the unit key is the segment
+  out.rec.reset();
+  out.uc.clear();
+  out.cost.clear();
+  out.C = out.CL = out.NS = out.P = 0;
+  if (m == 0) {
+    out.uc.assign(S + 1, 0);
+    return GI_OK;
+  }
   DevBuf row, key, skey, eid, order, tmp;
   GI_TRY(row.alloc(m * sizeof(int32_t)));
-  k_edge_rows<OffT><<<grid_for(n * 32, 256, sms, 16), 256, 0, st>>>(off, n, row.as<int32_t>());
+  k_edge_rows<OffT><<<grid_for(nb * 32, 256, sms, 16), 256, 0, st>>>(off, nb, e0, r0, row.as<int32_t>());
   GI_TRY(key.alloc(m * sizeof(uint32_t)));
   GI_TRY(skey.alloc(m * sizeof(uint32_t)));
   GI_TRY(eid.alloc(m * sizeof(OffT)));
@@ -710,23 +737,93 @@ static gi_status seg_build_t(gi_graph g, int Z, int64_t DB) {
     GI_CUDA(cudaMemcpyAsync(rL.p, h_L.data(), C * sizeof(int32_t), cudaMemcpyHostToDevice, st));
     GI_CUDA(cudaMemcpyAsync(rng.p, h_ng.data(), C * sizeof(int32_t), cudaMemcpyHostToDevice, st));
   }
-  GI_TRY(g->seg_rec.alloc(C * kRecBytes + 16));
-  GI_CUDA(cudaMemsetAsync(g->seg_rec.p, 0, C * kRecBytes + 16, st));
-  const int trash = (int)n;  // accumulator row past the owned rows
+  GI_TRY(out.rec.alloc(C * kRecBytes + 16));
+  GI_CUDA(cudaMemsetAsync(out.rec.p, 0, C * kRecBytes + 16, st));
+  const int trash = (int)g->nr;  // accumulator row past the owned rows
   k_record_headers<<<grid_for(C * (kRecBytes / 4), 256, sms), 256, 0, st>>>(
       rtype.as<int32_t>(), rL.as<int32_t>(), rng.as<int32_t>(), C, Z, trash, unit_c0.as<int32_t>(), (int)U, S,
-      g->seg_rec.as<uint8_t>());
+      out.rec.as<uint8_t>());
   k_place_long<OffT><<<grid_for(P, 256, sms), 256, 0, st>>>(
       asz.as<int64_t>(), aoff.as<int64_t>(), punit.as<int32_t>(), unit_p0.as<int64_t>(), unit_c0.as<int32_t>(),
       pstart.as<int64_t>(), skey.as<uint32_t>(), order.as<OffT>(), idx, pdst.as<int32_t>(), P, m, Z, S,
-      g->seg_rec.as<uint8_t>());
+      out.rec.as<uint8_t>());
   k_long_dst<<<grid_for(P, 256, sms), 256, 0, st>>>(asz.as<int64_t>(), aoff.as<int64_t>(), punit.as<int32_t>(),
                                                     unit_p0.as<int64_t>(), unit_c0.as<int32_t>(), pdst.as<int32_t>(),
-                                                    P, g->seg_rec.as<uint8_t>());
+                                                    P, out.rec.as<uint8_t>());
   if (NS > 0)
     k_place_short<OffT><<<grid_for(NS, 256, sms), 256, 0, st>>>(
         sckey.as<uint32_t>(), spid.as<int32_t>(), NS, cstart.as<int64_t>(), crec0.as<int32_t>(), pstart.as<int64_t>(),
-        skey.as<uint32_t>(), order.as<OffT>(), idx, pdst.as<int32_t>(), Z, S, g->seg_rec.as<uint8_t>());
+        skey.as<uint32_t>(), order.as<OffT>(), idx, pdst.as<int32_t>(), Z, S, out.rec.as<uint8_t>());
+  GI_CUDA(cudaGetLastError());
+  GI_CUDA(cudaStreamSynchronize(st));  // the temporaries are freed on return
+  out.uc = std::move(h_uc);
+  out.cost = std::move(h_cost);
+  out.C = C;
+  out.CL = CL;
+  out.NS = NS;
+  out.P = P;
+  return GI_OK;
+}
+
+template <typename OffT>
+static gi_status seg_build_t(gi_graph g, int Z, int64_t DB) {
+  gi_context ctx = g->ctx;
+  cudaStream_t st = ctx->stream;
+  const int sms = ctx->num_sms;
+  const int64_t n = g->nr, m = g->ml;  // CSC rows (owned destinations) and local edges
+  const int S = (int)ceil_div(g->n, Z);  // segments over all sources
+  if ((int64_t)S * 16 >= INT32_MAX / 2) return fail(GI_ERR_UNSUPPORTED, "segmented pull: too many units");
+  // destination blocks: at most DB rows (the accumulator range kept in L2) and
+  // fewer than 2^31 edges each (the build's sorts and piece ids are 32-bit)
+  std::vector<OffT> hoff(n + 1);
+  GI_CUDA(cudaMemcpyAsync(hoff.data(), g->csc_off.p, (n + 1) * sizeof(OffT), cudaMemcpyDeviceToHost, st));
+  GI_CUDA(cudaStreamSynchronize(st));
+  std::vector<int64_t> br{0};
+  {
+    static const int64_t emax = getenv("GI_SEG_BLOCK_EDGES") ? atoll(getenv("GI_SEG_BLOCK_EDGES")) : kBlockEdges;
+    int64_t r = 0;
+    while (r < n) {
+      int64_t r1 = std::min<int64_t>(n, r + DB);
+      if ((int64_t)hoff[r1] - (int64_t)hoff[r] > emax)  // last row keeping the block under emax edges
+        r1 = std::max<int64_t>(r + 1, (int64_t)(std::upper_bound(hoff.begin() + r, hoff.begin() + r1 + 1,
+                                                                 (OffT)((int64_t)hoff[r] + emax)) - hoff.begin()) - 1);
+      br.push_back(r1);
+      r = r1;
+    }
+    if (n == 0) br.push_back(0);
+  }
+  const int B = (int)br.size() - 1;
+  if ((int64_t)B * S >= INT32_MAX / 2) return fail(GI_ERR_UNSUPPORTED, "segmented pull: too many units");
+  const int U = B * S;
+  std::vector<SegBlock> blocks(B);
+  int64_t C = 0, CL = 0, NS = 0, P = 0;
+  for (int b = 0; b < B; ++b) {
+    GI_TRY(seg_build_block<OffT>(g, Z, S, br[b], br[b + 1], blocks[b]));
+    C += blocks[b].C;
+    CL += blocks[b].CL;
+    NS += blocks[b].NS;
+    P += blocks[b].P;
+    if (C >= INT32_MAX) return fail(GI_ERR_UNSUPPORTED, "segmented pull: more than 2^31 records");
+  }
+  // concatenate the blocks' records; unit u = b * S + segment
+  std::vector<int32_t> h_uc(U + 1);
+  std::vector<int64_t> h_cost;
+  h_cost.reserve(C);
+  GI_TRY(g->seg_rec.alloc(C * kRecBytes + 16));
+  GI_CUDA(cudaMemsetAsync(g->seg_rec.as<uint8_t>() + C * kRecBytes, 0, 16, st));
+  int64_t cb = 0;
+  for (int b = 0; b < B; ++b) {
+    SegBlock& k = blocks[b];
+    for (int s = 0; s < S; ++s) h_uc[b * S + s] = (int32_t)(cb + k.uc[s]);
+    h_cost.insert(h_cost.end(), k.cost.begin(), k.cost.end());
+    if (k.C > 0)
+      GI_CUDA(cudaMemcpyAsync(g->seg_rec.as<uint8_t>() + cb * kRecBytes, k.rec.p, k.C * kRecBytes,
+                              cudaMemcpyDeviceToDevice, st));
+    cb += k.C;
+  }
+  h_uc[U] = (int32_t)C;
+  GI_CUDA(cudaStreamSynchronize(st));
+  blocks.clear();
   // ---- cost-balanced CTA ranges (every staged unit start adds kUnitCost)
   const int ctas = sms;
   std::vector<int32_t> h_cta(ctas + 1, (int32_t)C);
