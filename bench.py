@@ -364,13 +364,22 @@ def run_ours(args):
         t = time.perf_counter()
         e2e_steps = max(1, min(args.steps, 2))
         e_edges = 0
+        dbg = os.environ.get("GI_BENCH_E2E_DEBUG")
         for _ in range(e2e_steps):
+            tp = [time.perf_counter()]
             g2 = gi.Graph(ctx, cfg.n, hs, hd, flags)
+            tp.append(time.perf_counter())
             _, ps2 = g2.pagerank(cfg.pr_iters, cfg.damping, out=hpr, direction=direction)
+            tp.append(time.perf_counter())
             e_edges += cfg.pr_iters * g2.m
             _, bss2 = g2.bfs_multi(srcs, out=hbfs)
+            tp.append(time.perf_counter())
             e_edges += sum(b.edges_traversed for b in bss2)
             g2.close()
+            tp.append(time.perf_counter())
+            if dbg:
+                print("e2e step: create %.1f pagerank %.1f bfs_multi %.1f close %.1f ms"
+                      % tuple((b - a) * 1e3 for a, b in zip(tp, tp[1:])), file=sys.stderr)
         torch.cuda.synchronize()
         e2e_s = time.perf_counter() - t
         if world > 1:

@@ -143,6 +143,14 @@ gi_status gi_context_create(int device, void* cuda_stream, gi_context* out) {
     }
     c->own_stream = true;
   }
+  if (pool_enabled()) {  // keep freed blocks cached (up to kPoolKeep) for the next graph or layout build
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      uint64_t keep = kPoolKeep;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    cudaGetLastError();
+  }
   cudaError_t he = cudaMallocHost(&c->h_scratch, 64 * sizeof(int64_t));
   if (he != cudaSuccess) {
     if (c->own_stream) cudaStreamDestroy(c->stream);
@@ -194,6 +202,7 @@ gi_status gi_graph_create(gi_context ctx, int64_t n, int64_t m0, const int32_t* 
   if (flags & ~known) return fail(GI_ERR_INVALID_ARGUMENT, "gi_graph_create: unknown flag bits");
   if (n == 0 && m0 > 0) return fail(GI_ERR_VERTEX_OUT_OF_RANGE, "gi_graph_create: edges given but n = 0");
   GI_CUDA(cudaSetDevice(ctx->device));
+  AllocScope as_(ctx->stream);
   if ((flags & GI_EDGES_ON_DEVICE) && m0 > 0 && !(is_device_ptr(src) && is_device_ptr(dst)))
     return fail(GI_ERR_INVALID_ARGUMENT, "gi_graph_create: GI_EDGES_ON_DEVICE but edges are host memory");
   DevBuf hs, hd;
@@ -219,7 +228,7 @@ gi_status gi_graph_destroy(gi_graph g) {
   cudaSetDevice(g->ctx->device);
   cudaStreamSynchronize(g->ctx->stream);
   g->ctx->live_graphs--;
-  delete g;
+  delete g;  // pooled buffers go back to the pool (stream-ordered frees)
   return GI_OK;
 }
 
@@ -281,6 +290,7 @@ gi_status gi_graph_out_degrees(gi_graph g, int32_t* outdeg) {
   if (!g || (!outdeg && g->n > 0)) return fail(GI_ERR_INVALID_ARGUMENT, "gi_graph_out_degrees: NULL argument");
   gi_context ctx = g->ctx;
   GI_CUDA(cudaSetDevice(ctx->device));
+  AllocScope as_(ctx->stream);
   if (g->n == 0) return GI_OK;
   OutBuf<int32_t> ob{outdeg, g->n, false, &g->out_stage};
   int32_t* d = nullptr;
@@ -299,6 +309,7 @@ gi_status gi_graph_in_degrees(gi_graph g, int32_t* indeg) {
   if (g->ctx->nranks > 1) return fail(GI_ERR_UNSUPPORTED, "gi_graph_in_degrees: single-GPU graphs only");
   gi_context ctx = g->ctx;
   GI_CUDA(cudaSetDevice(ctx->device));
+  AllocScope as_(ctx->stream);
   if (g->n == 0) return GI_OK;
   OutBuf<int32_t> ob{indeg, g->n, false, &g->out_stage};
   int32_t* d = nullptr;
@@ -321,6 +332,7 @@ gi_status gi_graph_csr(gi_graph g, int64_t* off, int32_t* idx) {
   gi_context ctx = g->ctx;
   cudaStream_t st = ctx->stream;
   GI_CUDA(cudaSetDevice(ctx->device));
+  AllocScope as_(ctx->stream);
   const int64_t n = g->n, m = g->m;
   const int sms = ctx->num_sms;
   DevBuf deg, doff, didx, didx2, tmp;
@@ -382,6 +394,7 @@ gi_status gi_pagerank_ex(gi_graph g, int32_t iters, double damping, const gi_pr_
     return fail(GI_ERR_INVALID_ARGUMENT, "gi_pagerank: segment_size / dst_block < 0");
   gi_context ctx = g->ctx;
   GI_CUDA(cudaSetDevice(ctx->device));
+  AllocScope as_(ctx->stream);
   OutBuf<float> ob{out, g->n, false, &g->out_stage};
   float* d = nullptr;
   if (g->n > 0) GI_TRY(ob.prepare(g, &d));
@@ -405,6 +418,7 @@ gi_status gi_pagerank_delta(gi_graph g, int32_t iters, double damping, double ep
     return fail(GI_ERR_INVALID_ARGUMENT, "gi_pagerank_delta: bad options");
   gi_context ctx = g->ctx;
   GI_CUDA(cudaSetDevice(ctx->device));
+  AllocScope as_(ctx->stream);
   if (g->n == 0) {
     if (stats) *stats = gi_prdelta_stats{};
     return GI_OK;
@@ -433,6 +447,7 @@ gi_status gi_bfs_ex(gi_graph g, int32_t source, const gi_bfs_opts* opts, int32_t
     return fail(GI_ERR_INVALID_ARGUMENT, "gi_bfs: bad options");
   gi_context ctx = g->ctx;
   GI_CUDA(cudaSetDevice(ctx->device));
+  AllocScope as_(ctx->stream);
   OutBuf<int32_t> ob{parent_out, g->n, false, &g->out_stage};
   int32_t* d = nullptr;
   GI_TRY(ob.prepare(g, &d));
@@ -465,6 +480,7 @@ gi_status gi_bfs_multi(gi_graph g, int32_t k, const int32_t* sources, const gi_b
   const bool bitpar = o.batch == GI_BFS_BATCH_BITPARALLEL || (o.batch == GI_BFS_BATCH_AUTO && k >= 8);
   gi_context ctx = g->ctx;
   GI_CUDA(cudaSetDevice(ctx->device));
+  AllocScope as_(ctx->stream);
   static const char* impl = getenv("GI_BFS_IMPL");
   if (ctx->nranks > 1 || (impl && strcmp(impl, "host") == 0)) {  // one call per source
     for (int32_t i = 0; i < k; ++i) {

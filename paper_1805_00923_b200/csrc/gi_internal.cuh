@@ -37,24 +37,62 @@ gi_status cuda_fail(cudaError_t e, const char* what, const char* file, int line)
 
 // ------------------------------------------------------------------ device buffer
 // RAII device allocation (cudaMalloc; freed on destruction).
+// Allocations inside a library call are stream-ordered on the context's stream
+// (cudaMallocAsync / cudaFreeAsync from the device's pool, which keeps up to
+// kPoolKeep bytes cached), so the temporaries of a graph build or a layout
+// build, and a graph's buffers after gi_graph_destroy, are reused instead of
+// going back to cudaMalloc / cudaFree. AllocScope sets the stream for the
+// calling thread; outside a scope (or with GI_POOL=0) DevBuf uses cudaMalloc.
+constexpr uint64_t kPoolKeep = 16ull << 30;
+inline cudaStream_t& tl_alloc_stream() {
+  static thread_local cudaStream_t s = nullptr;
+  return s;
+}
+inline bool pool_enabled() {
+  static const bool on = !getenv("GI_POOL") || atoi(getenv("GI_POOL")) != 0;
+  return on;
+}
+struct AllocScope {
+  cudaStream_t prev;
+  explicit AllocScope(cudaStream_t s) : prev(tl_alloc_stream()) { tl_alloc_stream() = s; }
+  ~AllocScope() { tl_alloc_stream() = prev; }
+  AllocScope(const AllocScope&) = delete;
+  AllocScope& operator=(const AllocScope&) = delete;
+};
+
 struct DevBuf {
   void* p = nullptr;
   size_t bytes = 0;
+  cudaStream_t s = nullptr;  // stream of a pooled allocation (freed on it)
+  bool pooled = false;
   DevBuf() = default;
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
   ~DevBuf() { reset(); }
   void reset() {
-    if (p) cudaFree(p);
+    if (p) {
+      if (pooled) cudaFreeAsync(p, s);
+      else cudaFree(p);
+    }
     p = nullptr;
     bytes = 0;
+    pooled = false;
   }
   gi_status alloc(size_t nbytes) {
     reset();
     if (nbytes == 0) nbytes = 16;
-    cudaError_t e = cudaMalloc(&p, nbytes);
+    const cudaStream_t st = tl_alloc_stream();
+    cudaError_t e;
+    if (st && pool_enabled()) {
+      e = cudaMallocAsync(&p, nbytes, st);
+      pooled = e == cudaSuccess;
+      s = st;
+    } else {
+      e = cudaMalloc(&p, nbytes);
+    }
     if (e != cudaSuccess) {
       p = nullptr;
+      pooled = false;
       cudaGetLastError();
       return fail(GI_ERR_OUT_OF_MEMORY, "cudaMalloc of " + std::to_string(nbytes) + " bytes failed: " +
                                             cudaGetErrorString(e));

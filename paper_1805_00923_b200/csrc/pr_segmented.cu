@@ -42,6 +42,7 @@
 //   k_pr_acc  r'[v] = (1-d)/n + d (acc[v] + D/n), contrib', dangling mass
 //             (fused vertex update a3); zeroes the other (ping-pong) accumulator.
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <cub/cub.cuh>
@@ -773,6 +774,7 @@ static gi_status seg_build_t(gi_graph g, int Z, int64_t DB) {
   const int64_t n = g->nr, m = g->ml;  // CSC rows (owned destinations) and local edges
   const int S = (int)ceil_div(g->n, Z);  // segments over all sources
   if ((int64_t)S * 16 >= INT32_MAX / 2) return fail(GI_ERR_UNSUPPORTED, "segmented pull: too many units");
+  const auto tb0 = std::chrono::steady_clock::now();
   // destination blocks: at most DB rows (the accumulator range kept in L2) and
   // fewer than 2^31 edges each (the build's sorts and piece ids are 32-bit)
   std::vector<OffT> hoff(n + 1);
@@ -824,6 +826,7 @@ static gi_status seg_build_t(gi_graph g, int Z, int64_t DB) {
   h_uc[U] = (int32_t)C;
   GI_CUDA(cudaStreamSynchronize(st));
   blocks.clear();
+  const auto tb1 = std::chrono::steady_clock::now();
   // ---- cost-balanced CTA ranges (every staged unit start adds kUnitCost)
   const int ctas = sms;
   std::vector<int32_t> h_cta(ctas + 1, (int32_t)C);
@@ -863,9 +866,13 @@ static gi_status seg_build_t(gi_graph g, int Z, int64_t DB) {
   GI_CUDA(cudaStreamSynchronize(st));
   if (const char* dbg = getenv("GI_DEBUG_SEG_LAYOUT")) {
     if (FILE* f = fopen(dbg, "a")) {
+      const auto tb2 = std::chrono::steady_clock::now();
       fprintf(f, "n=%lld m=%lld Z=%d S=%d B=%d U=%d records=%lld (long %lld, short %lld) bytes=%lld P=%lld "
-              "(short %lld)\n", (long long)n, (long long)m, Z, S, B, U, (long long)C, (long long)CL,
-              (long long)(C - CL), (long long)(C * kRecBytes), (long long)P, (long long)NS);
+              "(short %lld) build %.1f ms (blocks %.1f, ranges + upload %.1f)\n", (long long)n, (long long)m, Z, S, B,
+              U, (long long)C, (long long)CL, (long long)(C - CL), (long long)(C * kRecBytes), (long long)P,
+              (long long)NS, std::chrono::duration<double, std::milli>(tb2 - tb0).count(),
+              std::chrono::duration<double, std::milli>(tb1 - tb0).count(),
+              std::chrono::duration<double, std::milli>(tb2 - tb1).count());
       fclose(f);
     }
   }

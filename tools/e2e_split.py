@@ -1,0 +1,37 @@
+"""Phase split of one bench e2e step on config 2: graph create from pinned host edges (H2D inside),
+first PageRank call (segmented layout build + calibration + 20 iterations, host output),
+a second PageRank call, bfs_multi of the 64 sources into pinned host rows.
+
+usage: python tools/e2e_split.py [CONFIG]
+"""
+import os
+import sys
+import time
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import graphgen  # noqa: E402
+from paper_1805_00923_b200 import gi  # noqa: E402
+
+cfg = graphgen.CONFIGS[int(sys.argv[1]) if len(sys.argv) > 1 else 2]
+s, d = cfg.edges()
+srcs = [int(x) for x in cfg.sources(s, d)]
+ctx = gi.Context(0)
+hs, hd = torch.from_numpy(s).pin_memory(), torch.from_numpy(d).pin_memory()
+hpr = torch.empty(cfg.n, dtype=torch.float32).pin_memory()
+hbfs = torch.empty((len(srcs), cfg.n), dtype=torch.int32).pin_memory()
+for rep in range(3):
+    t = [time.perf_counter()]
+    g = gi.Graph(ctx, cfg.n, hs, hd, gi.GI_DEFAULT_FLAGS)
+    torch.cuda.synchronize(); t.append(time.perf_counter())
+    g.pagerank(cfg.pr_iters, cfg.damping, out=hpr)
+    t.append(time.perf_counter())
+    g.pagerank(cfg.pr_iters, cfg.damping, out=hpr)
+    t.append(time.perf_counter())
+    g.bfs_multi(srcs, out=hbfs)
+    t.append(time.perf_counter())
+    g.close()
+    t.append(time.perf_counter())
+    ms = [(b - a) * 1e3 for a, b in zip(t, t[1:])]
+    print("create %.1f  pr#1 %.1f  pr#2 %.1f  bfs_multi(host) %.1f  close %.1f ms" % tuple(ms))
