@@ -59,7 +59,15 @@ constexpr int kPullBatch = GI_MS_BATCH;
 #ifndef GI_MS_HCHUNK
 #define GI_MS_HCHUNK 1024
 #endif
-constexpr int kHChunk = GI_MS_HCHUNK;  // heavy-row in-edges per pull work item  // in-edge gathers in flight per pull step  // out-edges per push work item   // bit-parallel direction rule: pull iff |F| + sum outdeg F > m / 3
+constexpr int kHChunk = GI_MS_HCHUNK;  // heavy-row in-edges per pull work item
+#ifndef GI_MS_HPER
+#define GI_MS_HPER 4
+#endif
+constexpr int kHeavyPer = GI_MS_HPER;  // heavy chunks per warp
+#ifndef GI_MS_LPERSM
+#define GI_MS_LPERSM 16
+#endif
+constexpr int kLightPerSM = GI_MS_LPERSM;  // light-row pull CTAs per SM (grid-stride beyond)  // in-edge gathers in flight per pull step  // out-edges per push work item   // bit-parallel direction rule: pull iff |F| + sum outdeg F > m / 3
 
 struct MsArgs {
   int64_t n;
@@ -682,9 +690,12 @@ gi_status msbfs_t(gi_graph g, int32_t k, const int32_t* sources, const gi_bfs_op
                                                    : (o.policy == GI_BFS_AUTO && nact + sdeg > mdiv);
     if (pull && o.profile) GI_CUDA(cudaEventRecord(pe0, st));
     if (pull) {
-      k_ms_pull<OffT><<<grid_for(n, kMsT, sms, 16), kMsT, 0, st>>>(A);
+      k_ms_pull<OffT><<<grid_for(n, kMsT, sms, kLightPerSM), kMsT, 0, st>>>(A);
       if (M.nhch > 0) {
-        k_ms_pull_heavy<OffT><<<grid_for(M.nhch * 32, kMsT, sms, 8), kMsT, 0, st>>>(A, M.hch.as<int2>(), M.nhch);
+        // a few chunks per warp and many CTAs: the block scheduler balances the uneven chunks
+        const int64_t hw = (M.nhch + kHeavyPer - 1) / kHeavyPer;
+        k_ms_pull_heavy<OffT><<<(unsigned)std::max<int64_t>(1, (hw + kMsT / 32 - 1) / (kMsT / 32)), kMsT, 0, st>>>(
+            A, M.hch.as<int2>(), M.nhch);
         ++launches;
       }
       if (o.profile) GI_CUDA(cudaEventRecord(pe1, st));
