@@ -90,6 +90,7 @@ struct FusedArgs {
   int64_t small_max;   // a push level with sum outdeg F <= small_max is "small"
   int mode;            // 0: full grid, hands over after kStreak small levels; 1: small grid, hands back
                        //    as soon as a level is not small (high-diameter graphs: cheaper barriers)
+  int clustered;       // the launch is one thread-block cluster: barriers are cluster barriers (hardware)
   int policy, sw;
   unsigned long long* times;  // optional (GI_DEBUG_BFS_FUSED): per level [start, work done, barrier done]
   unsigned long long* ctimes; // optional: per level < 16 and CTA, the CTA's work-done time
@@ -153,6 +154,12 @@ __global__ void __launch_bounds__(kFT, 1) k_bfs_fused(FusedArgs<OffT> A) {
     typename cub::BlockScan<long long, kFT>::TempStorage l;
   } scan_tmp;
   cg::grid_group grid = cg::this_grid();
+  // the barrier between phases: the grid's (cooperative launch) or, for the
+  // small grid launched as one cluster, the cluster's hardware barrier
+  auto gsync = [&]() {
+    if (A.clustered) cg::this_cluster().sync();
+    else grid.sync();
+  };
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int64_t G = gridDim.x;
   const int64_t words = (A.n + 31) >> 5;
@@ -171,7 +178,7 @@ __global__ void __launch_bounds__(kFT, 1) k_bfs_fused(FusedArgs<OffT> A) {
       asm volatile("prefetch.global.L2 [%0];" ::"l"(A.stamp + i));
     for (int64_t i = blockIdx.x * (int64_t)kFT + tid; i < A.n; i += G * kFT) out[i] = -1;
     for (int64_t i = blockIdx.x * (int64_t)kFT + tid; i < words; i += G * kFT) A.bm[0][i] = 0u;
-    grid.sync();
+    gsync();
     if (blockIdx.x == 0 && tid == 0) {
       const int32_t s = A.inv ? A.inv[source_in] : source_in;
       A.stamp[s] = epoch;
@@ -187,7 +194,7 @@ __global__ void __launch_bounds__(kFT, 1) k_bfs_fused(FusedArgs<OffT> A) {
       A.state[2] = 1;  // ... and as a bitmap
       A.state[9] = (int64_t)gtimer();
     }
-    grid.sync();
+    gsync();
   }
   int64_t level = A.state[0], pulls = A.state[3];
   bool qvalid = A.state[1] != 0;  // the current frontier is available as a queue ...
@@ -245,12 +252,12 @@ __global__ void __launch_bounds__(kFT, 1) k_bfs_fused(FusedArgs<OffT> A) {
       ++pulls;
       if (!bvalid) {  // frontier only as a queue (after push levels): build its bitmap
         for (int64_t i = blockIdx.x * (int64_t)kFT + tid; i < words; i += G * kFT) bcur[i] = 0u;
-        grid.sync();
+        gsync();
         for (int64_t i = blockIdx.x * (int64_t)kFT + tid; i < nf; i += G * kFT) {
           const int32_t u = __ldcg(&qcur[i]);
           atomicOr(&bcur[u >> 5], 1u << (u & 31));
         }
-        grid.sync();
+        gsync();
       }
       for (int i = tid; i < A.sw; i += kFT) sbits[i] = __ldcg(&bcur[i]);
       __syncthreads();
@@ -343,7 +350,7 @@ __global__ void __launch_bounds__(kFT, 1) k_bfs_fused(FusedArgs<OffT> A) {
           }
           __syncthreads();
         }
-        grid.sync();
+        gsync();
       }
       unsigned long long* tn = reinterpret_cast<unsigned long long*>(cn);
       // Big push levels (the hub levels of social graphs) emit the next
@@ -353,7 +360,7 @@ __global__ void __launch_bounds__(kFT, 1) k_bfs_fused(FusedArgs<OffT> A) {
       const bool to_bm = sdeg > kBitmapPush && sdeg > 4 * nf;
       if (to_bm) {
         for (int64_t i = blockIdx.x * (int64_t)kFT + tid; i < words; i += G * kFT) bnext[i] = 0u;
-        grid.sync();
+        gsync();
       }
       // visit one flattened edge (u -> v): claim v, then append it (or set its bit)
       auto claim_step = [&](bool valid, int32_t u, int32_t v) {
@@ -482,7 +489,7 @@ __global__ void __launch_bounds__(kFT, 1) k_bfs_fused(FusedArgs<OffT> A) {
           if (tid == 0) A.ctot[ch] = tot;
           __syncthreads();
         }
-        grid.sync();
+        gsync();
         if (blockIdx.x == 0) {
           long long carry = 0;
           for (int64_t b = 0; b < nch; b += kFT) {
@@ -496,7 +503,7 @@ __global__ void __launch_bounds__(kFT, 1) k_bfs_fused(FusedArgs<OffT> A) {
           }
           if (tid == 0) A.ctot[nch] = carry;
         }
-        grid.sync();
+        gsync();
         const long long E = vload(A.ctot + nch);
         auto gpre = [&](int64_t i) { return vload(A.ctot + i / kFChunk) + vload(A.pre + i); };
         auto owner = [&](long long f) {  // last i with gpre(i) <= f
@@ -572,7 +579,7 @@ __global__ void __launch_bounds__(kFT, 1) k_bfs_fused(FusedArgs<OffT> A) {
     }
     if (timed) A.times[3 * level + 1] = gtimer();
     if (A.ctimes && tid == 0 && level < 16) A.ctimes[level * G + blockIdx.x] = gtimer();
-    grid.sync();
+    gsync();
     if (timed) A.times[3 * level + 2] = gtimer();
     ++level;
   }
@@ -586,7 +593,7 @@ __global__ void __launch_bounds__(kFT, 1) k_bfs_fused(FusedArgs<OffT> A) {
     if (A.states)
       for (int i = 0; i < 11; ++i) A.states[16 * si + i] = A.state[i];
   }
-  if (si + 1 < A.nsrc) grid.sync();  // the next prologue rewrites what this source's last level read
+  if (si + 1 < A.nsrc) gsync();  // the next prologue rewrites what this source's last level read
   }  // sources
 }
 
@@ -642,6 +649,26 @@ static gi_status fused_setup(gi_graph g) {
   if (bpm < 1) return fail(GI_ERR_UNSUPPORTED, "fused BFS kernel cannot be co-resident");
   F.dyn = dyn;
   F.grid = bpm * ctx->num_sms;
+  // the small grid as one cluster of kSmallGrid CTAs (non-portable size), if the device can hold one
+  F.cluster = false;
+  static const bool cl_env = !getenv("GI_BFS_CLUSTER") || atoi(getenv("GI_BFS_CLUSTER")) != 0;
+  if (cl_env && cudaFuncSetAttribute(k_bfs_fused<OffT>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
+                    cudaSuccess) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(kSmallGrid);
+    cfg.blockDim = dim3(kFT);
+    cfg.dynamicSmemBytes = (size_t)dyn;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = kSmallGrid;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int nc = 0;
+    if (cudaOccupancyMaxActiveClusters(&nc, k_bfs_fused<OffT>, &cfg) == cudaSuccess && nc >= 1) F.cluster = true;
+  }
+  cudaGetLastError();
   F.ready = true;
   return GI_OK;
 }
@@ -677,6 +704,7 @@ static FusedArgs<OffT> fused_args(gi_graph g, const gi_bfs_opts& o, int32_t* d_o
   A.state = cnt + 8 + 4;  // state[7] after the tail ring
   A.small_max = 1 << 16;
   A.mode = 0;
+  A.clustered = 0;
   A.n = g->n;
   A.mdiv = g->m / (o.threshold_div > 0 ? o.threshold_div : 20);
   A.policy = o.policy;
@@ -705,6 +733,7 @@ static gi_status fused_start(gi_graph g, int32_t source, FusedArgs<OffT>& A) {
   A.source_in = source;
   A.fresh = 1;
   A.mode = 0;
+  A.clustered = 0;
   void* args[] = {&A};
   GI_CUDA(cudaLaunchCooperativeKernel((void*)k_bfs_fused<OffT>, dim3(F.grid), dim3(kFT), args, (size_t)F.dyn, st));
   GI_CUDA(cudaGetLastError());
@@ -745,9 +774,26 @@ static gi_status bfs_fused_t(gi_graph g, int32_t source, const gi_bfs_opts& o, i
     GI_CUDA(stream_wait(st));
     if (h[16 + 4]) break;
     A.mode = mode;
+    A.clustered = mode == 1 && F.cluster;
     void* args[] = {&A};
     const int grid = mode == 0 ? F.grid : std::min(F.grid, kSmallGrid);
-    GI_CUDA(cudaLaunchCooperativeKernel((void*)k_bfs_fused<OffT>, dim3(grid), dim3(kFT), args, (size_t)F.dyn, st));
+    if (A.clustered) {  // one cluster: hardware barriers between the phases of a level
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3(kSmallGrid);
+      cfg.blockDim = dim3(kFT);
+      cfg.dynamicSmemBytes = (size_t)F.dyn;
+      cfg.stream = st;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = kSmallGrid;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      GI_CUDA(cudaLaunchKernelEx(&cfg, k_bfs_fused<OffT>, A));
+    } else {
+      GI_CUDA(cudaLaunchCooperativeKernel((void*)k_bfs_fused<OffT>, dim3(grid), dim3(kFT), args, (size_t)F.dyn, st));
+    }
     GI_CUDA(cudaGetLastError());
     ++launches;
   }
@@ -840,6 +886,7 @@ static gi_status bfs_fused_multi_t(gi_graph g, int32_t k, const int32_t* sources
   A.states = F.mstates.as<int64_t>();
   A.fresh = 1;
   A.mode = 0;
+  A.clustered = 0;
   void* args[] = {&A};
   GI_CUDA(cudaLaunchCooperativeKernel((void*)k_bfs_fused<OffT>, dim3(F.grid), dim3(kFT), args, (size_t)F.dyn, st));
   GI_CUDA(cudaGetLastError());

@@ -183,6 +183,7 @@ struct gi_graph_s {
   gi::DevBuf bfs_cand;    // uint64[n]: (epoch << 32 | parent candidate), stamp + collect push
   struct {                // fused cooperative BFS (bfs_fused.cu)
     bool ready = false;
+    bool cluster = false;  // the small grid runs as one thread-block cluster
     int dyn = 0, grid = 0;
     gi::DevBuf stamp, q[2], bm[3], cnt, pre, ctot;  // stamp[v] == epoch: visited by the current source
     gi::DevBuf vinfo;                                // int2 {input id, out-degree} per internal id
