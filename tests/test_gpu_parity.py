@@ -405,6 +405,53 @@ def test_bfs_multi_bitparallel_batches(gi, ctx):
             assert stats[i].levels == depth.max() + 1
 
 
+def test_bfs_multi_bitparallel_edge_cases(gi, ctx):
+    """Bit-parallel passes on degenerate inputs: no edges; isolated and sink
+    sources; k = 1, 64 and 65; a 100k-leaf star under every direction policy —
+    pull-only makes the hub's 100k in-edges a split heavy row whose chunks race
+    on the same bits."""
+    bp = gi.GI_BFS_BATCH_BITPARALLEL
+    # no edges: every row holds only its own source
+    g = gi.Graph(ctx, 100, np.zeros(0, np.int32), np.zeros(0, np.int32))
+    srcs = [3, 7, 7, 99, 0, 50, 51, 52, 53, 54]
+    par, st = g.bfs_multi(srcs, batch=bp)
+    for i, s in enumerate(srcs):
+        want = np.full(100, -1, np.int32)
+        want[s] = s
+        assert (par[i] == want).all()
+        assert (st[i].reached, st[i].levels, st[i].edges_traversed) == (1, 1, 0)
+    # RMAT: isolated vertices and sinks as sources, k = 1 / 64 / 65
+    cfg = graphgen.CONFIGS[1]
+    s, d = cfg.edges()
+    g = gi.Graph(ctx, cfg.n, s, d)
+    go = oracle.build_graph(cfg.n, s, d)
+    outdeg = np.bincount(s[s != d], minlength=cfg.n)
+    indeg = np.bincount(d[s != d], minlength=cfg.n)
+    isolated = np.nonzero((outdeg == 0) & (indeg == 0))[0][:3].tolist()
+    sinks = np.nonzero((outdeg == 0) & (indeg > 0))[0][:3].tolist()
+    live = graphgen.pick_sources(cfg.n, s, d, 70, 5).tolist()
+    for srcs in ([live[0]], isolated + sinks + live[:58], live[:65]):
+        par, st = g.bfs_multi(srcs, batch=bp)
+        for i, src in enumerate(srcs):
+            depth = oracle.bfs_depth(go, src)
+            ok, msg = oracle.validate_bfs(go, src, par[i], depth)
+            assert ok, f"k={len(srcs)} src={src}: {msg}"
+            assert st[i].reached == int((depth >= 0).sum())
+            assert st[i].levels == depth.max() + 1
+    # 100k-leaf bidirectional star, sources = 64 leaves (+ the hub)
+    L = 100_000
+    s, d = graphgen.star_bidirectional(L)
+    g = gi.Graph(ctx, L + 1, s, d)
+    go = oracle.build_graph(L + 1, s, d)
+    srcs = list(range(1, 64)) + [0]
+    for policy in POLICIES:
+        par, st = g.bfs_multi(srcs, batch=bp, policy=_pol(gi, policy))
+        for i, src in enumerate(srcs):
+            depth = oracle.bfs_depth(go, src)
+            ok, msg = oracle.validate_bfs(go, src, par[i], depth)
+            assert ok, f"star {policy} src={src}: {msg}"
+
+
 def test_bfs_stress_repeat(gi, ctx):
     s, d = graphgen.rmat(13, 16, 0.57, 0.19, 0.19, 33)
     n = 1 << 13
