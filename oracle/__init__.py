@@ -65,6 +65,8 @@ def _get():
             lib.or_reached_out_edges.restype = ctypes.c_int64
             lib.or_pagerank_delta.argtypes = [vp, ctypes.c_int, ctypes.c_double, ctypes.c_double, f64p, vp]
             lib.or_pagerank_delta.restype = ctypes.c_int
+            lib.or_cc_labels.argtypes = [vp, i32p]
+            lib.or_cc_labels.restype = ctypes.c_int
             _lib = lib
     return _lib
 
@@ -176,3 +178,14 @@ def pagerank_delta(g: Graph, iters: int = 10, damping: float = 0.85, epsilon: fl
     if rc != 0:
         raise OracleError(f"or_pagerank_delta failed ({rc})")
     return (r[: g.n], fs[:iters]) if return_frontiers else r[: g.n]
+
+
+def cc_labels(g: Graph) -> np.ndarray:
+    """Label propagation's fixed point (P:3440-3472 [punt]): label[v] = the
+    smallest u with u = v or a directed path u ->* v (symmetric graph: the smallest
+    vertex of v's component)."""
+    out = np.empty(max(g.n, 1), np.int32)
+    rc = _get().or_cc_labels(g._h, out)
+    if rc != 0:
+        raise OracleError(f"or_cc_labels failed ({rc})")
+    return out[: g.n]

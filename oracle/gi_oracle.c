@@ -1,5 +1,5 @@
 /*
- * gi_oracle.c — the CPU ORACLE for the edgeset.apply hot path (PageRank, BFS).
+ * gi_oracle.c — the CPU ORACLE for the edgeset.apply hot path (PageRank, BFS, CC).
  *
  * TEST INFRASTRUCTURE ONLY. Only tests/, __graft_entry__.smoke() and
  * bench.py's cpu_baseline / --impl reference legs may load this library.
@@ -35,6 +35,10 @@
  *      directed path s ->* v along out-edges, -1 if unreachable; FIFO queue.
  *      Parent vector semantics: parent = -1 initially P:2093-2099; each vertex
  *      inserted once P:1021-1025; parent[source] = source S:509 (R8, R9).
+ *
+ *  CC (or_cc_labels): label propagation IDs[dst] min= IDs[src] from
+ *      IDs[v] = v (P:3440-3472 [punt]) written out as its fixed point
+ *      IDs[v] = min{u : u = v or u ->* v} (see the function).
  *
  *  Validator (or_validate_bfs): Graph500-style. A parent vector is valid iff
  *      parent[s] = s; parent[v] = -1 <=> depth(v) = -1; otherwise
@@ -279,5 +283,45 @@ int or_pagerank_delta(const or_graph* g, int iters, double damp, double eps, dou
   free(delta);
   free(dsum);
   free(inF);
+  return 0;
+}
+
+/* Connected components by label propagation (or_cc_labels).
+ * The paper's CC: IDs[v] = v (init), then rounds of
+ *   frontier = edges.from(frontier).apply(updateEdge).modified(IDs)
+ * with updateEdge: IDs[dst] min= IDs[src]      P:3440-3472 [punt]
+ * ("synchronous label propagation" P:2237; "initially operates on the whole
+ * graph and in subsequent iterations only ... the vertices whose data changed"
+ * P:2249 [punt]), until the frontier is empty. Every round only lowers labels
+ * and a lowered label is pushed on, so the rounds stop exactly at the fixed
+ * point
+ *   IDs[v] = min { u : u = v or there is a directed path u ->* v }
+ * (on a symmetric graph: the smallest vertex of v's connected component).
+ * That plain definition is what this function writes out: for u = 0..n-1 in
+ * increasing order, every vertex reachable from u along out-edges that has no
+ * label yet gets label u (a vertex labelled earlier by some u' < u has all it
+ * reaches labelled too, so the walk stops there). Labels are vertex ids. */
+int or_cc_labels(const or_graph* g, int32_t* label) {
+  const int64_t n = g->n;
+  int32_t* q = (int32_t*)malloc((size_t)(n > 0 ? n : 1) * sizeof(int32_t));
+  if (!q) return -3;
+  for (int64_t v = 0; v < n; ++v) label[v] = -1;
+  for (int64_t u = 0; u < n; ++u) {
+    if (label[u] >= 0) continue;
+    int64_t head = 0, tail = 0;
+    label[u] = (int32_t)u;
+    q[tail++] = (int32_t)u;
+    while (head < tail) {
+      const int32_t x = q[head++];
+      for (int64_t j = g->csr_off[x]; j < g->csr_off[x + 1]; ++j) {
+        const int32_t y = g->csr_idx[j];
+        if (label[y] < 0) {
+          label[y] = (int32_t)u;
+          q[tail++] = y;
+        }
+      }
+    }
+  }
+  free(q);
   return 0;
 }

@@ -404,3 +404,86 @@ def test_prdelta_cycle_symmetry_and_frontier_shrinks():
     assert fs[0] == 1 << 12 and fs[-1] < fs[1]  # the active set shrinks as ranks converge
     rpr = oracle.pagerank(g, 12, 0.85, oracle.DROP)
     assert np.abs(r - rpr).sum() < 0.05 * rpr.sum()  # an approximation of PageRank
+
+
+# ---------------------------------------------------------------- connected components (NEXT #4)
+def _cc_paper_rounds(n, src, dst):
+    """The paper's CC program literally (P:3440-3472 [punt]): IDs[v] = v, frontier =
+    all vertices, then rounds of edges.from(frontier).apply(IDs[dst] min= IDs[src])
+    .modified(IDs), synchronous (every edge reads the labels of the round's start),
+    until the frontier is empty. Pure Python, small graphs only."""
+    ids = list(range(n))
+    frontier = set(range(n))
+    edges = [(int(s), int(d)) for s, d in zip(src, dst)]
+    rounds = 0
+    while frontier:
+        new = list(ids)
+        for s, d in edges:
+            if s in frontier and ids[s] < new[d]:
+                new[d] = ids[s]
+        frontier = {v for v in range(n) if new[v] != ids[v]}
+        ids = new
+        rounds += 1
+    return np.array(ids, np.int32), rounds
+
+
+def test_cc_closed_forms():
+    n = 9
+    path = (np.arange(n - 1, dtype=np.int32), np.arange(1, n, dtype=np.int32))
+    g = oracle.build_graph(n, *path)
+    assert (oracle.cc_labels(g) == 0).all()                     # 0 reaches everything
+    g = oracle.build_graph(n, path[1], path[0])                   # reversed: nothing reaches v from below
+    assert (oracle.cc_labels(g) == np.arange(n)).all()
+    s, d = graphgen.cycle(n)
+    assert (oracle.cc_labels(oracle.build_graph(n, s, d)) == 0).all()
+    # two directed cycles {0..4}, {5..8} plus isolated 9, 10
+    s = np.array([0, 1, 2, 3, 4, 5, 6, 7, 8], np.int32)
+    d = np.array([1, 2, 3, 4, 0, 6, 7, 8, 5], np.int32)
+    lab = oracle.cc_labels(oracle.build_graph(11, s, d))
+    assert lab.tolist() == [0] * 5 + [5] * 4 + [9, 10]
+    # m = 0: every vertex is its own label
+    assert oracle.cc_labels(oracle.build_graph(5, np.zeros(0, np.int32), np.zeros(0, np.int32))).tolist() == [0, 1, 2, 3, 4]
+
+
+def test_cc_symmetric_matches_components():
+    """On symmetric graphs the fixed point is the smallest vertex of each connected
+    component: checked against scipy's connected_components (a library routine)."""
+    from scipy.sparse import coo_matrix
+    from scipy.sparse.csgraph import connected_components
+
+    rng = np.random.default_rng(11)
+    for trial in range(40):
+        n = int(rng.integers(1, 300))
+        m = int(rng.integers(0, 2 * n + 1))
+        s = rng.integers(0, n, m).astype(np.int32)
+        d = rng.integers(0, n, m).astype(np.int32)
+        g = oracle.build_graph(n, s, d, symmetrize=True)
+        lab = oracle.cc_labels(g)
+        a = coo_matrix((np.ones(m), (s, d)), shape=(n, n))
+        nc, comp = connected_components(a, directed=True, connection="weak")
+        want = np.full(nc, n, np.int64)
+        np.minimum.at(want, comp, np.arange(n))
+        assert (lab == want[comp]).all(), trial
+
+
+def test_cc_directed_brute_force_and_paper_rounds():
+    """Directed graphs: label[v] = min{u : u = v or u ->* v} from a Floyd-Warshall
+    style boolean closure, and the paper's synchronous rounds reach the same
+    labels."""
+    rng = np.random.default_rng(12)
+    for trial in range(120):
+        n = int(rng.integers(1, 9))
+        m = int(rng.integers(0, n * n + 1))
+        s = rng.integers(0, n, m).astype(np.int32)
+        d = rng.integers(0, n, m).astype(np.int32)
+        g = oracle.build_graph(n, s, d)
+        lab = oracle.cc_labels(g)
+        reach = np.eye(n, dtype=bool)
+        reach[s, d] = True
+        for k in range(n):
+            reach |= reach[:, [k]] & reach[[k], :]
+        want = np.array([min(u for u in range(n) if reach[u, v]) for v in range(n)], np.int32)
+        assert (lab == want).all(), trial
+        keep = s != d
+        paper, _ = _cc_paper_rounds(n, s[keep], d[keep])
+        assert (paper == want).all(), trial
