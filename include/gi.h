@@ -281,6 +281,36 @@ GI_API gi_status gi_bfs_ex(gi_graph g, int32_t source, const gi_bfs_opts* opts, 
 GI_API gi_status gi_bfs_multi(gi_graph g, int32_t k, const int32_t* sources, const gi_bfs_opts* opts,
                               int32_t* parents_out, gi_bfs_stats* stats /* may be NULL */);
 
+/* ---------------------------------------------------------------- connected components (NEXT #4)
+ * Label propagation, the paper's CC (P:3440-3472 [punt], P:3600-3615;
+ * "synchronous label propagation" P:2237): IDs[v] = v, frontier = every
+ * vertex, then rounds of
+ *   frontier = edges.from(frontier).apply(IDs[dst] min= IDs[src]).modified(IDs)
+ * until the frontier is empty; each round runs pull (DensePull over the frontier
+ * bitmap) iff |F| + sum outdeg(F) > m / threshold_div, else push (SparsePush with
+ * atomicMin), as BFS (R7).
+ *   labels_out: int32[n], host or device; labels_out[v] = the fixed point
+ *     min{ u : u = v or a directed path u ->* v } in input ids (reading R22);
+ *     on a graph built with GI_SYMMETRIZE that is the smallest vertex id of v's
+ *     connected component.
+ * Errors: GI_ERR_INVALID_ARGUMENT (NULL graph/output, bad options),
+ * GI_ERR_UNSUPPORTED on a multi-GPU context. n = 0 -> GI_OK. */
+typedef struct {
+  int32_t policy;        /* GI_BFS_AUTO / GI_BFS_PUSH_ONLY / GI_BFS_PULL_ONLY */
+  int32_t threshold_div; /* 0 -> 20 */
+  int32_t profile;       /* 1: fill total_ms */
+  int32_t reserved;
+} gi_cc_opts;
+typedef struct {
+  int32_t rounds;          /* label-propagation rounds (the last one changes nothing) */
+  int32_t pull_rounds;     /* rounds run in the pull direction */
+  int64_t edges_examined;  /* in-edges read by pull rounds + out-edges by push rounds */
+  float total_ms;          /* profile = 1 */
+  int32_t launches;        /* kernel launches in the call */
+} gi_cc_stats;
+GI_API gi_status gi_cc(gi_graph g, int32_t* labels_out);
+GI_API gi_status gi_cc_ex(gi_graph g, const gi_cc_opts* opts, int32_t* labels_out, gi_cc_stats* stats);
+
 /* ---------------------------------------------------------------- misc */
 GI_API const char* gi_status_string(gi_status s);
 GI_API const char* gi_last_error(void); /* thread-local; valid until the next call */

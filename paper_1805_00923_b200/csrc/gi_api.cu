@@ -436,6 +436,33 @@ gi_status gi_pagerank(gi_graph g, int32_t iters, double damping, float* out) {
   return gi_pagerank_ex(g, iters, damping, nullptr, out, nullptr);
 }
 
+gi_status gi_cc_ex(gi_graph g, const gi_cc_opts* opts, int32_t* labels_out, gi_cc_stats* stats) {
+  GI_GUARD_BEGIN
+  if (!g) return fail(GI_ERR_INVALID_ARGUMENT, "gi_cc: NULL graph");
+  if (!labels_out && g->n > 0) return fail(GI_ERR_INVALID_ARGUMENT, "gi_cc: NULL output");
+  gi_cc_opts o{};
+  if (opts) o = *opts;
+  if (o.policy < GI_BFS_AUTO || o.policy > GI_BFS_PULL_ONLY || o.threshold_div < 0)
+    return fail(GI_ERR_INVALID_ARGUMENT, "gi_cc: bad options");
+  gi_context ctx = g->ctx;
+  if (ctx->nranks > 1) return fail(GI_ERR_UNSUPPORTED, "gi_cc: single-GPU contexts only");
+  if (g->n == 0) {
+    if (stats) *stats = gi_cc_stats{};
+    return GI_OK;
+  }
+  GI_CUDA(cudaSetDevice(ctx->device));
+  AllocScope as_(ctx->stream);
+  OutBuf<int32_t> ob{labels_out, g->n, false, &g->out_stage};
+  int32_t* d = nullptr;
+  GI_TRY(ob.prepare(g, &d));
+  GI_TRY(cc_run(g, o, d, stats));
+  GI_TRY(ob.finish(ctx));
+  return sync(ctx);
+  GI_GUARD_END
+}
+
+gi_status gi_cc(gi_graph g, int32_t* labels_out) { return gi_cc_ex(g, nullptr, labels_out, nullptr); }
+
 gi_status gi_bfs_ex(gi_graph g, int32_t source, const gi_bfs_opts* opts, int32_t* parent_out, gi_bfs_stats* stats) {
   GI_GUARD_BEGIN
   if (!g) return fail(GI_ERR_INVALID_ARGUMENT, "gi_bfs: NULL graph");

@@ -581,14 +581,15 @@ __global__ void __launch_bounds__(kFinT) k_ms_finish(const int32_t* __restrict__
   }
 }
 
+// The traversal state shared by the bit-parallel BFS and CC (cc.cu), allocated
+// once per graph: masks, active lists, degree-prefix scratch and the heavy-row
+// chunks of the CSC (rows of >= kHeavy in-edges cut into <= kHChunk pieces).
 template <typename OffT>
-gi_status msbfs_t(gi_graph g, int32_t k, const int32_t* sources, const gi_bfs_opts& o, int32_t* d_out,
-                  gi_bfs_stats* stats) {
-  gi_context ctx = g->ctx;
-  cudaStream_t st = ctx->stream;
-  const int sms = ctx->num_sms;
-  const int64_t n = g->n;
+static gi_status ms_prepare_t(gi_graph g) {
   auto& M = g->ms;
+  cudaStream_t st = g->ctx->stream;
+  const int sms = g->ctx->num_sms;
+  const int64_t n = g->n;
   if (!M.seen.p) {
     GI_TRY(M.seen.alloc((n + 1) * 8));
     for (int c = 0; c < 2; ++c) {
@@ -629,6 +630,24 @@ gi_status msbfs_t(gi_graph g, int32_t k, const int32_t* sources, const gi_bfs_op
       M.nhch = hc;
     }
   }
+  return GI_OK;
+}
+
+}  // namespace
+
+gi_status ms_prepare(gi_graph g) { return g->off64 ? ms_prepare_t<int64_t>(g) : ms_prepare_t<int32_t>(g); }
+
+namespace {
+
+template <typename OffT>
+gi_status msbfs_t(gi_graph g, int32_t k, const int32_t* sources, const gi_bfs_opts& o, int32_t* d_out,
+                  gi_bfs_stats* stats) {
+  gi_context ctx = g->ctx;
+  cudaStream_t st = ctx->stream;
+  const int sms = ctx->num_sms;
+  const int64_t n = g->n;
+  auto& M = g->ms;
+  GI_TRY(ms_prepare(g));
   int lkp = 3;  // par row: kp = 2^lkp >= k ints (whole 32-byte sectors, power-of-two tiles in the epilogue)
   while ((1 << lkp) < k) ++lkp;
   const int kp = 1 << lkp;

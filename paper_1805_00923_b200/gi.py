@@ -71,6 +71,16 @@ class gi_bfs_opts(ctypes.Structure):
                 ("batch", ctypes.c_int32)]
 
 
+class gi_cc_opts(ctypes.Structure):
+    _fields_ = [("policy", ctypes.c_int32), ("threshold_div", ctypes.c_int32), ("profile", ctypes.c_int32),
+                ("reserved", ctypes.c_int32)]
+
+
+class gi_cc_stats(ctypes.Structure):
+    _fields_ = [("rounds", ctypes.c_int32), ("pull_rounds", ctypes.c_int32), ("edges_examined", ctypes.c_int64),
+                ("total_ms", ctypes.c_float), ("launches", ctypes.c_int32)]
+
+
 class gi_bfs_stats(ctypes.Structure):
     _fields_ = [("levels", ctypes.c_int32), ("pull_levels", ctypes.c_int32), ("reached", ctypes.c_int64),
                 ("edges_traversed", ctypes.c_int64), ("total_ms", ctypes.c_float), ("launches", ctypes.c_int32),
@@ -109,6 +119,8 @@ _SIGS = {
                            ctypes.POINTER(gi_prdelta_stats)], _st),
     "gi_bfs": ([_vp, _i32, _vp], _st),
     "gi_bfs_ex": ([_vp, _i32, ctypes.POINTER(gi_bfs_opts), _vp, ctypes.POINTER(gi_bfs_stats)], _st),
+    "gi_cc": ([_vp, _vp], _st),
+    "gi_cc_ex": ([_vp, ctypes.POINTER(gi_cc_opts), _vp, ctypes.POINTER(gi_cc_stats)], _st),
     "gi_bfs_multi": ([_vp, _i32, _vp, ctypes.POINTER(gi_bfs_opts), _vp, ctypes.POINTER(gi_bfs_stats)], _st),
     "gi_status_string": ([_st], ctypes.c_char_p),
     "gi_last_error": ([], ctypes.c_char_p),
@@ -323,6 +335,18 @@ def gi_bfs_ex(g: int, source: int, out=None, policy: int = GI_BFS_AUTO, threshol
     return keep, s
 
 
+def gi_cc_ex(g: int, out=None, policy: int = GI_BFS_AUTO, threshold_div: int = 0, profile: bool = False):
+    """Label-propagation components: out[v] = min input id u with u = v or u ->* v."""
+    n = gi_graph_num_vertices(g)
+    if out is None:
+        out = np.empty(n, np.int32)
+    p, keep = _ptr(out, np.int32)
+    o = gi_cc_opts(policy, threshold_div, int(profile), 0)
+    s = gi_cc_stats()
+    _check(_lib.gi_cc_ex(g, ctypes.byref(o), p or None, ctypes.byref(s)), "gi_cc_ex")
+    return keep, s
+
+
 def gi_bfs_multi(g: int, sources, out=None, policy: int = GI_BFS_AUTO, threshold_div: int = 0,
                  profile: bool = False, batch: int = GI_BFS_BATCH_AUTO):
     """k BFS runs back to back; out: int32[k, n] (host or device). Returns (out, [stats])."""
@@ -399,6 +423,9 @@ class Graph:
 
     def bfs(self, source, out=None, **kw):
         return gi_bfs_ex(self.handle, source, out, **kw)
+
+    def cc(self, out=None, **kw):
+        return gi_cc_ex(self.handle, out, **kw)
 
     def bfs_multi(self, sources, out=None, **kw):
         return gi_bfs_multi(self.handle, sources, out, **kw)

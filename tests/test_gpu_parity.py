@@ -563,3 +563,57 @@ def test_prdelta_equals_pagerank_drop_at_eps0(gi, ctx):
     want = oracle.pagerank(oracle.build_graph(cfg.n, s, d), 12, 0.85, oracle.DROP)
     got, _ = g.pagerank_delta(12, 0.85, 0.0)
     _pr_check(got, want, "prdelta eps=0 vs PR drop")
+
+
+# ---------------------------------------------------------------- connected components (NEXT #4)
+def _cc_cases():
+    cfg = graphgen.CONFIGS[1]
+    s1, d1 = cfg.edges()
+    sr, dr = graphgen.rmat(18, 8, 0.57, 0.19, 0.19, 21)
+    s3, d3 = graphgen.grid(128, 128, 0.3, 5)  # dropped edges split the grid into pieces
+    ps = np.arange(999, dtype=np.int32)
+    return [
+        ("config1", cfg.n, s1, d1, False),
+        ("config1-sym", cfg.n, s1, d1, True),
+        ("rmat18-sym", 1 << 18, sr, dr, True),
+        ("grid128", 128 * 128, s3, d3, False),
+        ("path", 1000, ps, ps + 1, False),
+        ("path-reversed", 1000, ps + 1, ps, False),
+        ("star", 100_001, *graphgen.star_bidirectional(100_000), False),
+        ("edgeless", 17, np.zeros(0, np.int32), np.zeros(0, np.int32), False),
+    ]
+
+
+@pytest.mark.parametrize("policy", POLICIES)
+def test_cc_parity(gi, ctx, policy):
+    """gi_cc == the oracle's fixed point (min input id over ancestors), exactly,
+    on directed and symmetrised RMAT, a fragmented grid, paths, a 100k-leaf star
+    and an edgeless graph, under every direction policy."""
+    for name, n, s, d, sym in _cc_cases():
+        flags = gi.GI_DEFAULT_FLAGS | (gi.GI_SYMMETRIZE if sym else 0)
+        g = gi.Graph(ctx, n, s, d, flags)
+        go = oracle.build_graph(n, s, d, symmetrize=sym)
+        want = oracle.cc_labels(go)
+        got, st = g.cc(policy=_pol(gi, policy))
+        assert (got == want).all(), f"{name} {policy}: {int((got != want).sum())} labels differ"
+        assert st.rounds >= 1 or n == 0
+        g.close()
+
+
+def test_cc_device_output_and_errors(gi, ctx):
+    import torch
+
+    cfg = graphgen.CONFIGS[1]
+    s, d = cfg.edges()
+    g = gi.Graph(ctx, cfg.n, s, d, gi.GI_DEFAULT_FLAGS | gi.GI_SYMMETRIZE)
+    want = oracle.cc_labels(oracle.build_graph(cfg.n, s, d, symmetrize=True))
+    out = torch.full((cfg.n,), -7, dtype=torch.int32, device="cuda")
+    got, st = g.cc(out=out, profile=True)
+    assert (got.cpu().numpy() == want).all()
+    assert st.total_ms > 0 and st.launches >= 2
+    # repeated calls reuse the state
+    got2, _ = g.cc()
+    assert (got2 == want).all()
+    with pytest.raises(gi.GiError) as e:
+        g.cc(policy=7)
+    assert e.value.status == gi.GI_ERR_INVALID_ARGUMENT
