@@ -10,7 +10,7 @@
 // graph the smallest vertex id of v's component). Labels are INPUT ids, so the
 // result does not depend on the internal relabelling.
 //
-// Per round, direction by the BFS rule (R7): pull iff |F| + sum outdeg F > m/20.
+// Per round, direction: pull iff |F| + sum outdeg F > m/3 (R23; BFS's rule with m/3).
 //   pull (DensePull): every row takes the min label of its in-neighbours in F
 //     (frontier bitmap); light rows (in-degree < 32) a thread each, heavy rows in
 //     chunks of <= 1024 in-edges a warp each (chunks of one row race through
@@ -33,6 +33,12 @@ namespace {
 constexpr int kCT = 256;
 constexpr int kCcHeavy = 32;      // rows of at least this many in-edges: the heavy kernel (ms_prepare's chunks)
 constexpr int kCcHChunk = 1024;   // in-edges per heavy chunk (as ms_prepare cuts them)
+// direction rule: pull iff |F| + sum outdeg F > m / 3. A CC pull row has no
+// early exit (it needs the minimum over all its in-neighbours in F), so a pull
+// round costs all m in-edges; a push round costs the frontier's out-edges with
+// an atomic each (reading R23; BFS's m/20 made the grid graph's label waves run
+// thousands of full pull rounds)
+constexpr int kCcPullDiv = 3;
 
 struct CcArgs {
   int64_t n;
@@ -52,17 +58,33 @@ struct CcArgs {
 
 __device__ __forceinline__ int32_t vload(const int32_t* p) { return *(volatile const int32_t*)p; }
 
-// warp-aggregated append of the rows whose bit this warp set, + their degrees
-__device__ __forceinline__ void cc_append(const CcArgs& A, bool add, int32_t w, unsigned long long& deg) {
+// append the rows whose bit this warp set (+ their degrees) through a per-warp
+// shared-memory buffer: one atomicAdd on the queue tail per 32 rows (a tail
+// shared by every warp is a serialisation point)
+__device__ __forceinline__ void cc_flush(const CcArgs& A, int32_t* buf, int cnt) {
+  const int lane = threadIdx.x & 31;
+  __syncwarp();
+  unsigned long long pos = 0;
+  if (lane == 0) pos = atomicAdd(&A.cnt[0], (unsigned long long)cnt);
+  pos = __shfl_sync(0xffffffffu, pos, 0);
+  if (lane < cnt) A.qnext[pos + lane] = buf[lane];
+  __syncwarp();
+}
+__device__ __forceinline__ void cc_append(const CcArgs& A, bool add, int32_t w, unsigned long long& deg,
+                                          int32_t* buf, int& nbuf) {
   const int lane = threadIdx.x & 31;
   const unsigned am = __ballot_sync(0xffffffffu, add);
   if (!am) return;
-  unsigned long long pos = 0;
-  if (lane == 0) pos = atomicAdd(&A.cnt[0], (unsigned long long)__popc(am));
-  pos = __shfl_sync(0xffffffffu, pos, 0);
   if (add) {
-    A.qnext[pos + __popc(am & ((1u << lane) - 1u))] = w;
+    buf[nbuf + __popc(am & ((1u << lane) - 1u))] = w;
     deg += (unsigned long long)__ldg(&A.outdeg[w]);
+  }
+  nbuf += __popc(am);
+  if (nbuf >= 32) {
+    cc_flush(A, buf, 32);
+    nbuf -= 32;
+    if (lane < nbuf) buf[lane] = buf[32 + lane];
+    __syncwarp();
   }
 }
 
@@ -96,8 +118,11 @@ __global__ void k_cc_init(int32_t* __restrict__ ids, const int32_t* __restrict__
 // (one atomicOr sets their bits in the next bitmap)
 template <typename OffT>
 __global__ void __launch_bounds__(kCT) k_cc_pull(CcArgs A) {
+  __shared__ int32_t s_buf[kCT / 32][64];
   const OffT* __restrict__ off = static_cast<const OffT*>(A.csc_off);
   const int lane = threadIdx.x & 31;
+  int32_t* buf = s_buf[threadIdx.x >> 5];
+  int nbuf = 0;
   unsigned long long deg = 0, exam = 0;
   for (int64_t b = (blockIdx.x * (int64_t)kCT + threadIdx.x) & ~31ll; b < A.n; b += (int64_t)gridDim.x * kCT) {
     const int64_t w = b + lane;
@@ -123,16 +148,20 @@ __global__ void __launch_bounds__(kCT) k_cc_pull(CcArgs A) {
     }
     const unsigned word = __ballot_sync(0xffffffffu, changed);
     if (word && lane == 0) atomicOr(&A.bnext[b >> 5], word);  // (b is a multiple of 32)
-    cc_append(A, changed, (int32_t)w, deg);
+    cc_append(A, changed, (int32_t)w, deg, buf, nbuf);
   }
+  if (nbuf > 0) cc_flush(A, buf, nbuf);
   cc_counters(A, deg, exam);
 }
 
 // pull over the heavy rows: a warp per chunk (row, first in-edge)
 template <typename OffT>
 __global__ void __launch_bounds__(kCT) k_cc_pull_heavy(CcArgs A, const int2* __restrict__ hch, int64_t C) {
+  __shared__ int32_t s_buf[kCT / 32][64];
   const OffT* __restrict__ off = static_cast<const OffT*>(A.csc_off);
   const int lane = threadIdx.x & 31;
+  int32_t* buf = s_buf[threadIdx.x >> 5];
+  int nbuf = 0;
   const int64_t nw = (int64_t)gridDim.x * (kCT / 32);
   unsigned long long deg = 0, exam = 0;
   for (int64_t c = blockIdx.x * (int64_t)(kCT / 32) + (threadIdx.x >> 5); c < C; c += nw) {
@@ -158,8 +187,9 @@ __global__ void __launch_bounds__(kCT) k_cc_pull_heavy(CcArgs A, const int2* __r
       const uint32_t bit = 1u << (w & 31);
       add = !(atomicOr(&A.bnext[w >> 5], bit) & bit);
     }
-    cc_append(A, add, w, deg);
+    cc_append(A, add, w, deg, buf, nbuf);
   }
+  if (nbuf > 0) cc_flush(A, buf, nbuf);
   cc_counters(A, deg, exam);
 }
 
@@ -174,8 +204,11 @@ __global__ void k_cc_degs(const int32_t* __restrict__ q, int64_t nf, const int32
 // a window of 32 prefix entries by a 5-step shuffle search
 template <typename OffT>
 __global__ void __launch_bounds__(kCT) k_cc_push(CcArgs A, const long long* __restrict__ dp) {
+  __shared__ int32_t s_buf[kCT / 32][64];
   const OffT* __restrict__ off = static_cast<const OffT*>(A.csr_off);
   const int lane = threadIdx.x & 31;
+  int32_t* buf = s_buf[threadIdx.x >> 5];
+  int nbuf = 0;
   const int64_t nw = (int64_t)gridDim.x * (kCT / 32);
   const int64_t gw = blockIdx.x * (int64_t)(kCT / 32) + (threadIdx.x >> 5);
   unsigned long long deg = 0, exam = 0;
@@ -213,11 +246,12 @@ __global__ void __launch_bounds__(kCT) k_cc_push(CcArgs A, const long long* __re
           add = !(atomicOr(&A.bnext[w >> 5], bit) & bit);
         }
       }
-      cc_append(A, add, w, deg);
+      cc_append(A, add, w, deg, buf, nbuf);
       i0 += __popc(__ballot_sync(0xffffffffu, P <= stop));
       e = stop;
     }
   }
+  if (nbuf > 0) cc_flush(A, buf, nbuf);
   cc_counters(A, deg, exam);
 }
 
@@ -247,7 +281,7 @@ gi_status cc_t(gi_graph g, const gi_cc_opts& o, int32_t* d_out, gi_cc_stats* sta
     GI_CUDA(cudaEventCreate(&e1));
     GI_CUDA(cudaEventRecord(e0, st));
   }
-  const int64_t mdiv = g->m / (o.threshold_div > 0 ? o.threshold_div : 20);
+  const int64_t mdiv = g->m / (o.threshold_div > 0 ? o.threshold_div : kCcPullDiv);
   const int32_t* perm = g->relabeled ? g->perm.as<int32_t>() : nullptr;
   unsigned long long* cnt = M.cnt.as<unsigned long long>();
   int64_t* h = ctx->h_scratch;
