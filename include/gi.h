@@ -288,7 +288,7 @@ GI_API gi_status gi_bfs_multi(gi_graph g, int32_t k, const int32_t* sources, con
  *   frontier = edges.from(frontier).apply(IDs[dst] min= IDs[src]).modified(IDs)
  * until the frontier is empty; each round runs pull (DensePull over the frontier
  * bitmap) iff |F| + sum outdeg(F) > m / threshold_div, else push (SparsePush with
- * atomicMin) — BFS's rule, with threshold_div 3 by default (R23).
+ * atomicMin), as BFS (R7).
  *   labels_out: int32[n], host or device; labels_out[v] = the fixed point
  *     min{ u : u = v or a directed path u ->* v } in input ids (reading R22);
  *     on a graph built with GI_SYMMETRIZE that is the smallest vertex id of v's
@@ -297,7 +297,7 @@ GI_API gi_status gi_bfs_multi(gi_graph g, int32_t k, const int32_t* sources, con
  * GI_ERR_UNSUPPORTED on a multi-GPU context. n = 0 -> GI_OK. */
 typedef struct {
   int32_t policy;        /* GI_BFS_AUTO / GI_BFS_PUSH_ONLY / GI_BFS_PULL_ONLY */
-  int32_t threshold_div; /* 0 -> 3 */
+  int32_t threshold_div; /* 0 -> 20 */
   int32_t profile;       /* 1: fill total_ms */
   int32_t reserved;
 } gi_cc_opts;

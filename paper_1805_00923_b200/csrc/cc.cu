@@ -10,7 +10,7 @@
 // graph the smallest vertex id of v's component). Labels are INPUT ids, so the
 // result does not depend on the internal relabelling.
 //
-// Per round, direction: pull iff |F| + sum outdeg F > m/3 (R23; BFS's rule with m/3).
+// Per round, direction by the BFS rule (R7): pull iff |F| + sum outdeg F > m/20.
 //   pull (DensePull): every row takes the min label of its in-neighbours in F
 //     (frontier bitmap); light rows (in-degree < 32) a thread each, heavy rows in
 //     chunks of <= 1024 in-edges a warp each (chunks of one row race through
@@ -33,12 +33,10 @@ namespace {
 constexpr int kCT = 256;
 constexpr int kCcHeavy = 32;      // rows of at least this many in-edges: the heavy kernel (ms_prepare's chunks)
 constexpr int kCcHChunk = 1024;   // in-edges per heavy chunk (as ms_prepare cuts them)
-// direction rule: pull iff |F| + sum outdeg F > m / 3. A CC pull row has no
-// early exit (it needs the minimum over all its in-neighbours in F), so a pull
-// round costs all m in-edges; a push round costs the frontier's out-edges with
-// an atomic each (reading R23; BFS's m/20 made the grid graph's label waves run
-// thousands of full pull rounds)
-constexpr int kCcPullDiv = 3;
+// direction rule: BFS's (R7), pull iff |F| + sum outdeg F > m / 20. A CC pull
+// row has no early exit, but the pull streams the CSC while the push scatters
+// atomics: m/3 and m/8 measured slower or equal on RMAT and the grid
+constexpr int kCcPullDiv = 20;
 
 struct CcArgs {
   int64_t n;
