@@ -45,6 +45,9 @@ namespace {
 #ifndef GI_MS_OUT
 #define GI_MS_OUT 1  // diagnostics: 0 drops the parent writes
 #endif
+#ifndef GI_MS_RMW
+#define GI_MS_RMW 1  // partially known sectors (unique writer) are read, merged and written whole
+#endif
 constexpr int kMsT = 256;
 #ifndef GI_MS_HEAVY
 #define GI_MS_HEAVY 32
@@ -109,6 +112,17 @@ __device__ __forceinline__ void par_put(int32_t* row, unsigned long long m, unsi
     const unsigned kn = (unsigned)(known >> (8 * g)) & 0xFFu;
     if (UNIQUE ? kn == 0u : nm == 0xFFu) {
       asm volatile("st.global.v8.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1};" ::"l"(row + 8 * g), "r"(val) : "memory");
+    } else if (UNIQUE && GI_MS_RMW) {  // read the sector, merge the new entries, write it whole
+      int32_t x[8];
+      asm volatile("ld.global.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                   : "=r"(x[0]), "=r"(x[1]), "=r"(x[2]), "=r"(x[3]), "=r"(x[4]), "=r"(x[5]), "=r"(x[6]), "=r"(x[7])
+                   : "l"(row + 8 * g));
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if ((nm >> j) & 1u) x[j] = val;
+      asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(row + 8 * g), "r"(x[0]), "r"(x[1]),
+                   "r"(x[2]), "r"(x[3]), "r"(x[4]), "r"(x[5]), "r"(x[6]), "r"(x[7])
+                   : "memory");
     } else if (UNIQUE) {  // halves / pairs without known bits go as one vector store each
       for (int h = 0; h < 8; h += 4) {
         const unsigned n4 = (nm >> h) & 0xFu, k4 = (kn >> h) & 0xFu;
