@@ -514,7 +514,10 @@ __global__ void k_ms_init(const int32_t* __restrict__ src_in, int k, const int32
 //     loads) are transposed through shared memory so each of the k output
 //     rows gets one contiguous 4 x kFinV-byte segment;
 //   per source i: vertices reached and the sum of their out-degrees (R16).
-constexpr int kFinV = 128;  // vertices per tile
+#ifndef GI_MS_FINV
+#define GI_MS_FINV 128
+#endif
+constexpr int kFinV = GI_MS_FINV;  // vertices per tile
 constexpr int kFinT = 256;  // threads per CTA
 __global__ void __launch_bounds__(kFinT) k_ms_finish(const int32_t* __restrict__ par,
                                                     const unsigned long long* __restrict__ seen,
@@ -524,7 +527,7 @@ __global__ void __launch_bounds__(kFinT) k_ms_finish(const int32_t* __restrict__
                                                     unsigned long long* __restrict__ reached,
                                                     unsigned long long* __restrict__ edges) {
   extern __shared__ int32_t tile[];  // [64][kFinV + 1]
-  __shared__ unsigned long long sv[kFinV];
+  __shared__ unsigned long long sv[kFinV], sod[kFinV];
   __shared__ unsigned long long r[64], d[64];
   const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
   const int kp = 1 << lkp, lrq = lkp - 2;  // par row: kp ints = 2^lrq int4s
@@ -534,12 +537,11 @@ __global__ void __launch_bounds__(kFinT) k_ms_finish(const int32_t* __restrict__
     const int nv = (int)(n - v0 < kFinV ? n - v0 : kFinV);
     const int nq = nv << lrq;  // int4s of the tile's rows
     const int4* p4 = reinterpret_cast<const int4*>(par + v0 * kp);
-    unsigned long long ov = 0;
     if (threadIdx.x < kFinV) {
       const int64_t v = v0 + threadIdx.x;
       const int32_t w = v < n ? (inv ? __ldg(&inv[v]) : (int32_t)v) : 0;
       sv[threadIdx.x] = v < n ? seen[w] : 0ull;
-      ov = v < n ? (unsigned long long)__ldg(&outdeg[w]) : 0ull;
+      sod[threadIdx.x] = v < n ? (unsigned long long)__ldg(&outdeg[w]) : 0ull;
     }
     __syncthreads();
     int4 q[kFinV * 16 / kFinT];
@@ -568,20 +570,17 @@ __global__ void __launch_bounds__(kFinT) k_ms_finish(const int32_t* __restrict__
         if (vv < nv) out[(int64_t)b * n + v0 + vv] = (sv[vv] >> b) & 1ull ? tile[b * (kFinV + 1) + vv] : -1;
       }
     }
-    // stats: warps 0..3 take 32 vertices each; lane counts sources lane and lane + 32
-    if (threadIdx.x < kFinV) {
-      const unsigned long long s_me = sv[threadIdx.x];
-      if (__ballot_sync(0xffffffffu, s_me != 0) != 0) {
+    // stats: every warp takes kFinV / 8 vertices; lane counts sources lane and lane + 32
+    {
+      constexpr int kPer = kFinV / (kFinT / 32);
 #pragma unroll 4
-        for (int j = 0; j < 32; ++j) {
-          const unsigned long long s = __shfl_sync(0xffffffffu, s_me, j);
-          const unsigned long long od = __shfl_sync(0xffffffffu, ov, j);
-          const unsigned long long b0 = (s >> lane) & 1ull, b1 = (s >> (lane + 32)) & 1ull;
-          r0 += b0;
-          r1 += b1;
-          d0 += b0 * od;
-          d1 += b1 * od;
-        }
+      for (int j = 0; j < kPer; ++j) {
+        const unsigned long long s = sv[wp * kPer + j], od = sod[wp * kPer + j];  // (broadcast reads)
+        const unsigned long long b0 = (s >> lane) & 1ull, b1 = (s >> (lane + 32)) & 1ull;
+        r0 += b0;
+        r1 += b1;
+        d0 += b0 * od;
+        d1 += b1 * od;
       }
     }
     __syncthreads();
