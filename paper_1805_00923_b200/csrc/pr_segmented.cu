@@ -976,12 +976,13 @@ gi_status seg_edge_pass(gi_graph g, const float* cin) {
   static const int mode = getenv("GI_SEG_MODE") ? atoi(getenv("GI_SEG_MODE")) : 0;
   void (*kern)(SegArgs) = mode == 1 ? k_pr_seg<1> : mode == 2 ? k_pr_seg<2> : k_pr_seg<0>;
   const size_t dyn = seg_dyn_smem(g->seg_Z);
-  static size_t attr_set = 0;  // largest dynamic smem size configured so far
-  if (attr_set < dyn) {
+  static size_t attr_set[64] = {};  // per device: largest dynamic smem size configured so far
+  const int dev = g->ctx->device & 63;
+  if (attr_set[dev] < dyn) {
     GI_CUDA(cudaFuncSetAttribute(k_pr_seg<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
     GI_CUDA(cudaFuncSetAttribute(k_pr_seg<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
     GI_CUDA(cudaFuncSetAttribute(k_pr_seg<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
-    attr_set = dyn;
+    attr_set[dev] = dyn;
   }
   static const char* dbg = getenv("GI_DEBUG_SEG_TIMING");  // diagnostics: file to append per-CTA timings to
   const bool timed = dbg || g->seg_calib > 0;
