@@ -23,11 +23,13 @@ roofline: the kernel with the larger summed device time per step;
 cpu_baseline: the oracle (oracle/, plain C, OpenMP) on a bounded sample of
          the same graph (2 PR iterations + 2 BFS sources).
 
-Multi-GPU (torchrun, one process per GPU): by default the graph is
-destination-partitioned over the N GPUs (each rank passes a share of the
-edge list; NCCL allgather of contrib slices / frontier bitmaps each iteration
-or level, SURVEY §8(e)) and the same single job is timed (strong scaling);
---mode replicas runs N independent copies instead (weak scaling).
+Multi-GPU (torchrun, one process per GPU): by default N replicas, each rank
+running the step on its own copy of the graph with its own seeded batch of 64
+BFS sources (independent problems, no collective; weak scaling). --mode
+partition times the destination-partitioned job instead (each rank passes a
+share of the edge list; NCCL allgather of contrib slices / frontier bitmaps each
+iteration or level; strong scaling; its BFS is a loop of
+single-source traversals).
 """
 from __future__ import annotations
 
@@ -58,9 +60,10 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--pr-direction", default="pull", choices=["pull", "push", "direct", "segmented"])
-    ap.add_argument("--mode", default="partition", choices=["partition", "replicas"],
-                    help="N > 1: destination-partitioned graph over NCCL (strong scaling, SURVEY §8(e)) or "
-                         "independent replicas (weak scaling)")
+    ap.add_argument("--mode", default="replicas", choices=["partition", "replicas"],
+                    help="N > 1: independent replicas, each rank its own batch of BFS sources (weak scaling, "
+                         "the default: the step's BFS sources are independent problems) or the "
+                         "destination-partitioned graph over NCCL (strong scaling, SURVEY §8(e))")
     return ap.parse_args()
 
 
@@ -242,6 +245,11 @@ def run_ours(args):
     else:
         ctx = gi.Context(dev, stream.cuda_stream)
     cfg, s, d, sources, gen_s = workload(args.config)
+    if world > 1 and not partition and rank > 0 and cfg.source_seed:
+        # replicas: every rank traverses its own seeded batch of sources (rank 0 keeps the N = 1 batch)
+        import graphgen
+
+        sources = graphgen.pick_sources(cfg.n, s, d, cfg.bfs_sources, cfg.source_seed + rank)
     if partition:  # every rank passes its own share of the edge list; the graph is the union
         s, d = s[rank::world].copy(), d[rank::world].copy()
     flags = gi.GI_DEFAULT_FLAGS | (gi.GI_SYMMETRIZE if cfg.symmetrize else 0)
@@ -387,11 +395,16 @@ def run_ours(args):
                       % tuple((b - a) * 1e3 for a, b in zip(tp, tp[1:])), file=sys.stderr)
         torch.cuda.synchronize()
         e2e_s = time.perf_counter() - t
+        e_all = float(e_edges)
         if world > 1:
             te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
             torch.distributed.all_reduce(te, op=torch.distributed.ReduceOp.MAX)
             e2e_s = float(te[0])
-        e2e = {"value": e_edges / e2e_s / 1e9 * (1 if partition else world), "unit": "GTEPS",
+            if not partition:  # replicas: every rank's own edges (its own sources)
+                ta = torch.tensor([e_all], dtype=torch.float64, device=dev)
+                torch.distributed.all_reduce(ta, op=torch.distributed.ReduceOp.SUM)
+                e_all = float(ta[0])
+        e2e = {"value": e_all / e2e_s / 1e9, "unit": "GTEPS",
                "h2d_bytes_per_step": int(8 * len(s)),
                "d2h_bytes_per_step": int(4 * n * (1 + len(srcs))), "steps": e2e_steps,
                "includes": "gi_graph_create from pinned host edges + gi_pagerank + gi_bfs_multi over the sources, host outputs; one untimed warm-up step"}
