@@ -70,6 +70,8 @@ def _get():
             lib.gg_edge_checksum.restype = ctypes.c_uint64
             lib.gg_uniform.argtypes = [ctypes.c_uint64, ctypes.c_uint64]
             lib.gg_uniform.restype = ctypes.c_double
+            lib.gg_edge_weights.argtypes = [ctypes.c_uint64, ctypes.c_int64, i32p, i32p, i32p]
+            lib.gg_edge_weights.restype = None
             _lib = lib
     return _lib
 
@@ -114,6 +116,16 @@ def pick_sources(n: int, src: np.ndarray, dst: np.ndarray, k: int, seed: int) ->
 def edge_checksum(src: np.ndarray, dst: np.ndarray) -> int:
     return int(_get().gg_edge_checksum(len(src), np.ascontiguousarray(src, np.int32),
                                        np.ascontiguousarray(dst, np.int32)))
+
+
+def edge_weights(seed: int, u: np.ndarray, v: np.ndarray) -> np.ndarray:
+    """Synthetic integer weights in [1, 255] of the directed edges (u[i], v[i]) (input ids):
+    1 + mix64(mix64(seed) + (u << 32 | v)) % 255 (SSSP inputs, reading R24)."""
+    u = np.ascontiguousarray(u, np.int32)
+    v = np.ascontiguousarray(v, np.int32)
+    w = np.empty(len(u), np.int32)
+    _get().gg_edge_weights(seed, len(u), u, v, w)
+    return w
 
 
 # ---------------------------------------------------------------- small families

@@ -129,3 +129,15 @@ uint64_t gg_edge_checksum(int64_t m, const int32_t* src, const int32_t* dst) {
     h += mix64(((uint64_t)(uint32_t)src[i] << 32) | (uint32_t)dst[i]);
   return h;
 }
+
+/* Synthetic edge weights (SSSP inputs, reading R24): the weight of directed edge
+ * (u, v), u and v input ids, is 1 + mix64(mix64(seed) + (u << 32 | v)) % 255,
+ * an integer in [1, 255]: a pure function of (seed, u, v), so the CUDA library
+ * draws the same weights from its own copy of this counter-based generator. */
+uint32_t gg_edge_weight(uint64_t seed, int32_t u, int32_t v) {
+  return 1u + (uint32_t)(mix64(mix64(seed) + (((uint64_t)(uint32_t)u << 32) | (uint32_t)v)) % 255u);
+}
+
+void gg_edge_weights(uint64_t seed, int64_t m, const int32_t* u, const int32_t* v, int32_t* w) {
+  for (int64_t i = 0; i < m; ++i) w[i] = (int32_t)gg_edge_weight(seed, u[i], v[i]);
+}

@@ -67,6 +67,8 @@ def _get():
             lib.or_pagerank_delta.restype = ctypes.c_int
             lib.or_cc_labels.argtypes = [vp, i32p]
             lib.or_cc_labels.restype = ctypes.c_int
+            lib.or_sssp.argtypes = [vp, ctypes.c_int32, i32p, i64p]
+            lib.or_sssp.restype = ctypes.c_int
             _lib = lib
     return _lib
 
@@ -189,3 +191,24 @@ def cc_labels(g: Graph) -> np.ndarray:
     if rc != 0:
         raise OracleError(f"or_cc_labels failed ({rc})")
     return out[: g.n]
+
+
+def sssp(g: Graph, source: int, w_csr) -> np.ndarray:
+    """Shortest-path distances from source along out-edges, w_csr[j] = weight of CSR edge j
+    (Dijkstra: the fixed point of the paper's frontier Bellman-Ford); -1 = unreachable."""
+    w = np.ascontiguousarray(w_csr, np.int32)
+    if w.shape != (g.m,):
+        raise ValueError("one weight per CSR edge")
+    dist = np.empty(max(g.n, 1), np.int64)
+    rc = _get().or_sssp(g._h, source, w if g.m else np.zeros(1, np.int32), dist)
+    if rc != 0:
+        raise OracleError(f"or_sssp failed ({rc})")
+    return dist[: g.n]
+
+
+def csr_weights(g: Graph, seed: int) -> np.ndarray:
+    """The synthetic weight (graphgen.edge_weights, input ids) of every CSR edge of g."""
+    import graphgen
+
+    rows = np.repeat(np.arange(g.n, dtype=np.int32), np.diff(g.csr_off).astype(np.int64))
+    return graphgen.edge_weights(seed, rows, g.csr_idx)

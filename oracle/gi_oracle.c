@@ -1,5 +1,5 @@
 /*
- * gi_oracle.c — the CPU ORACLE for the edgeset.apply hot path (PageRank, BFS, CC).
+ * gi_oracle.c — the CPU ORACLE for the edgeset.apply hot path (PageRank, BFS, CC, SSSP).
  *
  * TEST INFRASTRUCTURE ONLY. Only tests/, __graft_entry__.smoke() and
  * bench.py's cpu_baseline / --impl reference legs may load this library.
@@ -39,6 +39,9 @@
  *  CC (or_cc_labels): label propagation IDs[dst] min= IDs[src] from
  *      IDs[v] = v (P:3440-3472 [punt]) written out as its fixed point
  *      IDs[v] = min{u : u = v or u ->* v} (see the function).
+ *
+ *  SSSP (or_sssp): the shortest-path distances the paper's frontier
+ *      Bellman-Ford reaches, written out with Dijkstra.
  *
  *  Validator (or_validate_bfs): Graph500-style. A parent vector is valid iff
  *      parent[s] = s; parent[v] = -1 <=> depth(v) = -1; otherwise
@@ -323,5 +326,71 @@ int or_cc_labels(const or_graph* g, int32_t* label) {
     }
   }
   free(q);
+  return 0;
+}
+
+/* Single-source shortest paths (or_sssp). The paper's SSSP is a frontier-based
+ * Bellman-Ford ("an active set-based version of Bellman-Ford"
+ * P:2246-2247 [punt]): dist[s] = 0, frontier = {s}, rounds of
+ *   frontier = edges.from(frontier).apply(dist[dst] min= dist[src] + w).modified(dist)
+ * until empty. With non-negative weights it stops at the shortest-path
+ * distances, which is what this function writes out: Dijkstra's algorithm with
+ * a binary heap (a textbook routine) over out-edges. w[j] is the weight of CSR
+ * edge j (int32 >= 0); dist[v] = -1 when v is unreachable. int64 sums. */
+typedef struct {
+  int64_t d;
+  int32_t v;
+} or_heap_item;
+
+static void heap_push(or_heap_item* h, int64_t* size, int64_t d, int32_t v) {
+  int64_t i = (*size)++;
+  while (i > 0) {
+    const int64_t p = (i - 1) / 2;
+    if (h[p].d <= d) break;
+    h[i] = h[p];
+    i = p;
+  }
+  h[i].d = d;
+  h[i].v = v;
+}
+
+static or_heap_item heap_pop(or_heap_item* h, int64_t* size) {
+  const or_heap_item top = h[0];
+  const or_heap_item last = h[--(*size)];
+  int64_t i = 0;
+  for (;;) {
+    int64_t c = 2 * i + 1;
+    if (c >= *size) break;
+    if (c + 1 < *size && h[c + 1].d < h[c].d) ++c;
+    if (last.d <= h[c].d) break;
+    h[i] = h[c];
+    i = c;
+  }
+  if (*size > 0) h[i] = last;
+  return top;
+}
+
+int or_sssp(const or_graph* g, int32_t source, const int32_t* w, int64_t* dist) {
+  const int64_t n = g->n;
+  if (source < 0 || source >= n) return -2;
+  or_heap_item* h = (or_heap_item*)malloc((size_t)(g->m + 1) * sizeof(or_heap_item));
+  if (!h) return -3;
+  for (int64_t v = 0; v < n; ++v) dist[v] = -1;
+  int64_t size = 0;
+  dist[source] = 0;
+  heap_push(h, &size, 0, source);
+  while (size > 0) {
+    const or_heap_item it = heap_pop(h, &size);
+    if (it.d != dist[it.v]) continue; /* stale entry */
+    for (int64_t j = g->csr_off[it.v]; j < g->csr_off[it.v + 1]; ++j) {
+      const int32_t y = g->csr_idx[j];
+      const int64_t nd = it.d + w[j];
+      if (dist[y] < 0 || nd < dist[y]) {
+        dist[y] = nd;
+        heap_push(h, &size, nd, y);
+      }
+    }
+  }
+  free(h);
   return 0;
 }

@@ -487,3 +487,88 @@ def test_cc_directed_brute_force_and_paper_rounds():
         keep = s != d
         paper, _ = _cc_paper_rounds(n, s[keep], d[keep])
         assert (paper == want).all(), trial
+
+
+# ---------------------------------------------------------------- SSSP (NEXT #4)
+def _mix64(z):
+    M = (1 << 64) - 1
+    z = (z + 0x9E3779B97F4A7C15) & M
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & M
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & M
+    return z ^ (z >> 31)
+
+
+def test_edge_weight_generator():
+    """graphgen's synthetic weights: 1 + mix64(mix64(seed) + (u << 32 | v)) % 255 (R24),
+    deterministic, in [1, 255], seed-dependent, direction-dependent."""
+    rng = np.random.default_rng(3)
+    u = rng.integers(0, 1 << 31, 500).astype(np.int32)
+    v = rng.integers(0, 1 << 31, 500).astype(np.int32)
+    w = graphgen.edge_weights(9, u, v)
+    want = [1 + (_mix64((_mix64(9) + ((int(a) << 32) | int(b))) & ((1 << 64) - 1)) % 255) for a, b in zip(u, v)]
+    assert w.tolist() == want
+    assert w.min() >= 1 and w.max() <= 255
+    assert (graphgen.edge_weights(10, u, v) != w).mean() > 0.9
+    assert (graphgen.edge_weights(9, v, u) != w).mean() > 0.9
+
+
+def _bellman_ford_paper(n, src, dst, w, source):
+    """The paper's SSSP literally: frontier-based Bellman-Ford, synchronous
+    rounds of edges.from(frontier).apply(dist[dst] min= dist[src] + w).modified(dist)."""
+    INF = float("inf")
+    dist = [INF] * n
+    dist[source] = 0
+    frontier = {source}
+    while frontier:
+        new = list(dist)
+        for s, d, ww in zip(src, dst, w):
+            if s in frontier and dist[s] + ww < new[d]:
+                new[d] = dist[s] + ww
+        frontier = {v for v in range(n) if new[v] != dist[v]}
+        dist = new
+    return [(-1 if x == INF else int(x)) for x in dist]
+
+
+def test_sssp_unit_weights_are_bfs_depths():
+    for seed in range(6):
+        s, d = graphgen.random_digraph(200, 700, seed)
+        g = oracle.build_graph(200, s, d)
+        for src in (0, 17, 199):
+            dist = oracle.sssp(g, src, np.ones(g.m, np.int32))
+            assert (dist == oracle.bfs_depth(g, src)).all()
+
+
+def test_sssp_weighted_path_closed_form():
+    n = 12
+    s, d = graphgen.path(n)
+    g = oracle.build_graph(n, s, d)
+    w = np.arange(1, g.m + 1, dtype=np.int32)  # edge k -> k+1 weighs k+1
+    dist = oracle.sssp(g, 0, w)
+    assert dist.tolist() == [k * (k + 1) // 2 for k in range(n)]
+    dist = oracle.sssp(g, 5, w)
+    assert dist.tolist() == [-1] * 5 + [sum(range(6, 6 + j)) for j in range(n - 5)]
+
+
+def test_sssp_brute_force_and_paper_rounds():
+    """Tiny weighted digraphs: min-plus closure (Floyd-Warshall) and the paper's
+    frontier Bellman-Ford give the oracle's distances."""
+    rng = np.random.default_rng(13)
+    for trial in range(100):
+        n = int(rng.integers(1, 9))
+        m = int(rng.integers(0, n * n + 1))
+        s = rng.integers(0, n, m).astype(np.int32)
+        d = rng.integers(0, n, m).astype(np.int32)
+        g = oracle.build_graph(n, s, d)
+        w = oracle.csr_weights(g, trial)
+        rows = np.repeat(np.arange(n), np.diff(g.csr_off))
+        D = np.full((n, n), np.inf)
+        np.fill_diagonal(D, 0)
+        for a, b, ww in zip(rows, g.csr_idx, w):
+            D[a, b] = min(D[a, b], ww)
+        for k in range(n):
+            D = np.minimum(D, D[:, [k]] + D[[k], :])
+        for src in range(n):
+            dist = oracle.sssp(g, src, w)
+            want = np.where(np.isinf(D[src]), -1, D[src]).astype(np.int64)
+            assert (dist == want).all(), trial
+            assert dist.tolist() == _bellman_ford_paper(n, rows.tolist(), g.csr_idx.tolist(), w.tolist(), src)
