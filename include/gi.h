@@ -311,6 +311,26 @@ typedef struct {
 GI_API gi_status gi_cc(gi_graph g, int32_t* labels_out);
 GI_API gi_status gi_cc_ex(gi_graph g, const gi_cc_opts* opts, int32_t* labels_out, gi_cc_stats* stats);
 
+/* ---------------------------------------------------------------- SSSP (NEXT #4)
+ * Single-source shortest paths, the paper's frontier-based Bellman-Ford
+ * (P:2246-2247 [punt]): dist[source] = 0, frontier = {source},
+ * rounds of edges.from(frontier).apply(dist[dst] min= dist[src] + w).modified(dist)
+ * until the frontier is empty, each round pull or push by the BFS rule (R7).
+ * Edge weights are synthetic (the graph carries none, reading R24): the weight
+ * of directed edge (u, v), input ids, is 1 + mix64(mix64(weight_seed) +
+ * (u << 32 | v)) % 255 (graphgen.edge_weights draws the same values; mix64 =
+ * the splitmix64 finaliser). Weights are computed on the device once per
+ * (graph, seed) and kept with the graph (8 bytes per edge).
+ *   dist_out: int32[n], host or device: the shortest-path distance from
+ *     `source` along out-edges (exact integers), -1 when unreachable.
+ * Errors: as gi_bfs_ex (source out of range: GI_ERR_VERTEX_OUT_OF_RANGE);
+ * GI_ERR_UNSUPPORTED on a multi-GPU context. */
+typedef gi_cc_opts gi_sssp_opts;   /* policy, threshold_div (0 -> 20), profile */
+typedef gi_cc_stats gi_sssp_stats; /* rounds, pull_rounds, edges_examined, total_ms, launches */
+GI_API gi_status gi_sssp(gi_graph g, int32_t source, uint64_t weight_seed, int32_t* dist_out);
+GI_API gi_status gi_sssp_ex(gi_graph g, int32_t source, uint64_t weight_seed, const gi_sssp_opts* opts,
+                            int32_t* dist_out, gi_sssp_stats* stats);
+
 /* ---------------------------------------------------------------- misc */
 GI_API const char* gi_status_string(gi_status s);
 GI_API const char* gi_last_error(void); /* thread-local; valid until the next call */

@@ -52,6 +52,8 @@ struct CcArgs {
   int32_t* qnext;                       // next frontier queue
   unsigned long long* cnt;              // [0] |F'|, [1] sum outdeg F', [2] edges examined
   int64_t nf;                           // |F| (push)
+  const int32_t* __restrict__ wcsr;     // SSSP: edge weights in CSR / CSC order
+  const int32_t* __restrict__ wcsc;
 };
 
 __device__ __forceinline__ int32_t vload(const int32_t* p) { return *(volatile const int32_t*)p; }
@@ -114,7 +116,9 @@ __global__ void k_cc_init(int32_t* __restrict__ ids, const int32_t* __restrict__
 
 // pull over the light rows: a thread per row, a warp per 32 consecutive rows
 // (one atomicOr sets their bits in the next bitmap)
-template <typename OffT>
+// W (SSSP): the value a frontier in-neighbour u offers over edge e is
+// dist[u] + w(e); otherwise (CC) its label
+template <typename OffT, bool W>
 __global__ void __launch_bounds__(kCT) k_cc_pull(CcArgs A) {
   __shared__ int32_t s_buf[kCT / 32][64];
   const OffT* __restrict__ off = static_cast<const OffT*>(A.csc_off);
@@ -135,7 +139,8 @@ __global__ void __launch_bounds__(kCT) k_cc_pull(CcArgs A) {
           for (int j = 0; j < 4; ++j) u[j] = e + j < e1 ? __ldg(&A.csc_idx[e + j]) : -1;
 #pragma unroll
           for (int j = 0; j < 4; ++j)
-            if (u[j] >= 0 && ((__ldg(&A.bcur[u[j] >> 5]) >> (u[j] & 31)) & 1u)) best = min(best, vload(&A.ids[u[j]]));
+            if (u[j] >= 0 && ((__ldg(&A.bcur[u[j] >> 5]) >> (u[j] & 31)) & 1u))
+              best = min(best, vload(&A.ids[u[j]]) + (W ? __ldg(&A.wcsc[e + j]) : 0));
         }
         exam += (unsigned long long)(e1 - e0);
         if (best < vload(&A.ids[w])) {  // the only writer of a light row in a pull round
@@ -153,7 +158,7 @@ __global__ void __launch_bounds__(kCT) k_cc_pull(CcArgs A) {
 }
 
 // pull over the heavy rows: a warp per chunk (row, first in-edge)
-template <typename OffT>
+template <typename OffT, bool W>
 __global__ void __launch_bounds__(kCT) k_cc_pull_heavy(CcArgs A, const int2* __restrict__ hch, int64_t C) {
   __shared__ int32_t s_buf[kCT / 32][64];
   const OffT* __restrict__ off = static_cast<const OffT*>(A.csc_off);
@@ -176,7 +181,8 @@ __global__ void __launch_bounds__(kCT) k_cc_pull_heavy(CcArgs A, const int2* __r
       }
 #pragma unroll
       for (int j = 0; j < 4; ++j)
-        if (u[j] >= 0 && ((__ldg(&A.bcur[u[j] >> 5]) >> (u[j] & 31)) & 1u)) best = min(best, vload(&A.ids[u[j]]));
+        if (u[j] >= 0 && ((__ldg(&A.bcur[u[j] >> 5]) >> (u[j] & 31)) & 1u))
+          best = min(best, vload(&A.ids[u[j]]) + (W ? __ldg(&A.wcsc[b + 32 * j + lane]) : 0));
     }
     if (lane == 0) exam += (unsigned long long)(e1 - e0);
     best = __reduce_min_sync(0xffffffffu, best);
@@ -200,7 +206,7 @@ __global__ void k_cc_degs(const int32_t* __restrict__ q, int64_t nf, const int32
 // push: the frontier's out-edges (dp = inclusive prefix of their out-degrees)
 // split evenly over the warps, 32 per step; a lane finds its edge's vertex in
 // a window of 32 prefix entries by a 5-step shuffle search
-template <typename OffT>
+template <typename OffT, bool W>
 __global__ void __launch_bounds__(kCT) k_cc_push(CcArgs A, const long long* __restrict__ dp) {
   __shared__ int32_t s_buf[kCT / 32][64];
   const OffT* __restrict__ off = static_cast<const OffT*>(A.csr_off);
@@ -236,9 +242,10 @@ __global__ void __launch_bounds__(kCT) k_cc_push(CcArgs A, const long long* __re
       int32_t w = 0;
       if (my < stop) {
         const int32_t u = __ldg(&A.qcur[i0 + pos]);
-        w = __ldg(&A.csr_idx[(int64_t)off[u] + (my - start)]);
+        const int64_t ei = (int64_t)off[u] + (my - start);
+        w = __ldg(&A.csr_idx[ei]);
         ++exam;
-        const int32_t lu = vload(&A.ids[u]);
+        const int32_t lu = vload(&A.ids[u]) + (W ? __ldg(&A.wcsr[ei]) : 0);
         if (lu < vload(&A.ids[w]) && lu < atomicMin(&A.ids[w], lu)) {  // this edge lowered w's label
           const uint32_t bit = 1u << (w & 31);
           add = !(atomicOr(&A.bnext[w >> 5], bit) & bit);
@@ -260,8 +267,67 @@ __global__ void k_cc_out(const int32_t* __restrict__ ids, const int32_t* __restr
     out[perm ? __ldg(&perm[v]) : v] = ids[v];
 }
 
+// SSSP: out[input id of v] = dist[v], -1 when unreachable
+__global__ void k_sssp_out(const int32_t* __restrict__ dist, const int32_t* __restrict__ perm, int64_t n,
+                           int32_t* __restrict__ out) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t d = dist[v];
+    out[perm ? __ldg(&perm[v]) : v] = d == INT_MAX ? -1 : d;
+  }
+}
+
+// SSSP: dist = "infinity" except the source; frontier {source}
+__global__ void k_sssp_init(int32_t* __restrict__ dist, int64_t n, int32_t s, uint32_t* __restrict__ bm,
+                            int32_t* __restrict__ q) {
+  const int64_t words = (n + 31) >> 5;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n || i < words;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (i < n) dist[i] = i == s ? 0 : INT_MAX;
+    if (i < words) bm[i] = i == (s >> 5) ? 1u << (s & 31) : 0u;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) q[0] = s;
+}
+
+// The synthetic weight of edge (u, v), input ids: the library's copy of
+// graphgen's counter-based generator (R24), 1 + mix64(mix64(seed) + (u << 32 | v)) % 255
+__device__ __forceinline__ uint64_t w_mix64(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+__device__ __forceinline__ int32_t edge_weight(uint64_t key, int32_t u, int32_t v) {
+  return 1 + (int32_t)(w_mix64(key + (((uint64_t)(uint32_t)u << 32) | (uint32_t)v)) % 255u);
+}
+
+// weights of every edge of a CSR (src_is_row) or CSC layout, a warp per row
 template <typename OffT>
-gi_status cc_t(gi_graph g, const gi_cc_opts& o, int32_t* d_out, gi_cc_stats* stats) {
+__global__ void k_edge_weights(const OffT* __restrict__ off, const int32_t* __restrict__ idx, int64_t n,
+                               const int32_t* __restrict__ perm, uint64_t key, bool src_is_row,
+                               int32_t* __restrict__ w) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; r < n; r += nw) {
+    const int32_t ri = perm ? __ldg(&perm[r]) : (int32_t)r;
+    for (int64_t e = (int64_t)off[r] + lane; e < (int64_t)off[r + 1]; e += 32) {
+      const int32_t x = __ldg(&idx[e]);
+      const int32_t xi = perm ? __ldg(&perm[x]) : x;
+      w[e] = src_is_row ? edge_weight(key, ri, xi) : edge_weight(key, xi, ri);
+    }
+  }
+}
+
+// host side of graphgen's key: mix64(seed)
+static uint64_t h_mix64(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+// CC (W = false) or SSSP from `source` (W = true, weights drawn with `seed`)
+template <typename OffT, bool W>
+gi_status cc_t(gi_graph g, const gi_cc_opts& o, int32_t source, uint64_t seed, int32_t* d_out, gi_cc_stats* stats) {
   gi_context ctx = g->ctx;
   cudaStream_t st = ctx->stream;
   const int sms = ctx->num_sms;
@@ -283,12 +349,41 @@ gi_status cc_t(gi_graph g, const gi_cc_opts& o, int32_t* d_out, gi_cc_stats* sta
   const int32_t* perm = g->relabeled ? g->perm.as<int32_t>() : nullptr;
   unsigned long long* cnt = M.cnt.as<unsigned long long>();
   int64_t* h = ctx->h_scratch;
-  // round 0: every vertex in the frontier (|F| = n, sum outdeg = m)
-  const bool first_push = o.policy == GI_BFS_PUSH_ONLY;
-  k_cc_init<<<grid_for(std::max(n, words), 256, sms), 256, 0, st>>>(K.ids.as<int32_t>(), perm, n, K.bm[0].as<uint32_t>(),
-                                                                  M.act[0].as<int32_t>(), first_push ? 1 : 0);
   int launches = 1, rounds = 0, pulls = 0;
   int64_t nf = n, sdeg = g->m, examined = 0;
+  if (W) {  // weights of this seed (cached with the graph), dist, frontier {source}
+    if (!K.w_ready || K.w_seed != seed) {
+      if (!K.wcsr.p) {
+        GI_TRY(K.wcsr.alloc((g->m + 1) * 4));
+        GI_TRY(K.wcsc.alloc((g->m + 1) * 4));
+      }
+      const uint64_t key = h_mix64(seed);
+      k_edge_weights<OffT><<<grid_for(n * 32, 256, sms, 16), 256, 0, st>>>(
+          g->csr_off.as<OffT>(), g->csr_idx.as<int32_t>(), n, perm, key, true, K.wcsr.as<int32_t>());
+      k_edge_weights<OffT><<<grid_for(n * 32, 256, sms, 16), 256, 0, st>>>(
+          g->csc_off.as<OffT>(), g->csc_idx.as<int32_t>(), n, perm, key, false, K.wcsc.as<int32_t>());
+      launches += 2;
+      K.w_ready = true;
+      K.w_seed = seed;
+    }
+    int32_t s = source;  // internal id of the source
+    if (g->relabeled) {
+      GI_CUDA(cudaMemcpyAsync(&s, g->inv.as<int32_t>() + source, 4, cudaMemcpyDeviceToHost, st));
+      GI_CUDA(cudaStreamSynchronize(st));
+    }
+    k_sssp_init<<<grid_for(std::max(n, words), 256, sms), 256, 0, st>>>(K.ids.as<int32_t>(), n, s,
+                                                                       K.bm[0].as<uint32_t>(), M.act[0].as<int32_t>());
+    int32_t od = 0;
+    GI_CUDA(cudaMemcpyAsync(&od, g->outdeg.as<int32_t>() + s, 4, cudaMemcpyDeviceToHost, st));
+    GI_CUDA(cudaStreamSynchronize(st));
+    nf = 1;
+    sdeg = od;
+  } else {  // CC round 0: every vertex in the frontier (|F| = n, sum outdeg = m)
+    const bool first_push = o.policy == GI_BFS_PUSH_ONLY;
+    k_cc_init<<<grid_for(std::max(n, words), 256, sms), 256, 0, st>>>(K.ids.as<int32_t>(), perm, n,
+                                                                    K.bm[0].as<uint32_t>(), M.act[0].as<int32_t>(),
+                                                                    first_push ? 1 : 0);
+  }
   CcArgs A{};
   A.n = n;
   A.csr_off = g->csr_off.p;
@@ -298,6 +393,8 @@ gi_status cc_t(gi_graph g, const gi_cc_opts& o, int32_t* d_out, gi_cc_stats* sta
   A.outdeg = g->outdeg.as<int32_t>();
   A.ids = K.ids.as<int32_t>();
   A.cnt = cnt;
+  A.wcsr = W ? K.wcsr.as<int32_t>() : nullptr;
+  A.wcsc = W ? K.wcsc.as<int32_t>() : nullptr;
   for (int r = 0; nf > 0; ++r) {
     const int c = r & 1;
     A.bcur = K.bm[c].as<uint32_t>();
@@ -307,12 +404,12 @@ gi_status cc_t(gi_graph g, const gi_cc_opts& o, int32_t* d_out, gi_cc_stats* sta
     A.nf = nf;
     GI_CUDA(cudaMemsetAsync(A.bnext, 0, words * 4, st));
     GI_CUDA(cudaMemsetAsync(cnt, 0, 3 * 8, st));
-    const bool pull = o.policy == GI_BFS_PULL_ONLY || (o.policy == GI_BFS_AUTO && nf + sdeg > mdiv);
+    const bool pull = (o.policy == GI_BFS_PULL_ONLY && (r > 0 || !W)) || (o.policy == GI_BFS_AUTO && nf + sdeg > mdiv);
     if (pull) {
-      k_cc_pull<OffT><<<grid_for(n, kCT, sms, 16), kCT, 0, st>>>(A);
+      k_cc_pull<OffT, W><<<grid_for(n, kCT, sms, 16), kCT, 0, st>>>(A);
       ++launches;
       if (M.nhch > 0) {
-        k_cc_pull_heavy<OffT><<<grid_for(M.nhch * 32, kCT, sms, 16), kCT, 0, st>>>(A, M.hch.as<int2>(), M.nhch);
+        k_cc_pull_heavy<OffT, W><<<grid_for(M.nhch * 32, kCT, sms, 16), kCT, 0, st>>>(A, M.hch.as<int2>(), M.nhch);
         ++launches;
       }
       ++pulls;
@@ -322,7 +419,7 @@ gi_status cc_t(gi_graph g, const gi_cc_opts& o, int32_t* d_out, gi_cc_stats* sta
       k_cc_degs<<<grid_for(nf, kCT, sms, 8), kCT, 0, st>>>(A.qcur, nf, A.outdeg, dd);
       size_t tb = M.scan_bytes;
       GI_CUDA(cub::DeviceScan::InclusiveSum(M.scan_tmp.p, tb, dd, dp, (int)nf, st));
-      k_cc_push<OffT><<<grid_for((sdeg + 255) / 256 * 32, kCT, sms, 8), kCT, 0, st>>>(A, dp);
+      k_cc_push<OffT, W><<<grid_for((sdeg + 255) / 256 * 32, kCT, sms, 8), kCT, 0, st>>>(A, dp);
       launches += 3;
     }
     GI_CUDA(cudaGetLastError());
@@ -333,7 +430,8 @@ gi_status cc_t(gi_graph g, const gi_cc_opts& o, int32_t* d_out, gi_cc_stats* sta
     examined += h[2];
     ++rounds;
   }
-  k_cc_out<<<grid_for(n, 256, sms), 256, 0, st>>>(K.ids.as<int32_t>(), perm, n, d_out);
+  if (W) k_sssp_out<<<grid_for(n, 256, sms), 256, 0, st>>>(K.ids.as<int32_t>(), perm, n, d_out);
+  else k_cc_out<<<grid_for(n, 256, sms), 256, 0, st>>>(K.ids.as<int32_t>(), perm, n, d_out);
   ++launches;
   GI_CUDA(cudaGetLastError());
   float ms = 0.f;
@@ -363,7 +461,13 @@ gi_status cc_run(gi_graph g, const gi_cc_opts& o, int32_t* d_out, gi_cc_stats* s
     if (stats) *stats = gi_cc_stats{};
     return GI_OK;
   }
-  return g->off64 ? cc_t<int64_t>(g, o, d_out, stats) : cc_t<int32_t>(g, o, d_out, stats);
+  return g->off64 ? cc_t<int64_t, false>(g, o, 0, 0, d_out, stats) : cc_t<int32_t, false>(g, o, 0, 0, d_out, stats);
+}
+
+gi_status sssp_run(gi_graph g, int32_t source, uint64_t seed, const gi_cc_opts& o, int32_t* d_out,
+                   gi_cc_stats* stats) {
+  return g->off64 ? cc_t<int64_t, true>(g, o, source, seed, d_out, stats)
+                  : cc_t<int32_t, true>(g, o, source, seed, d_out, stats);
 }
 
 }  // namespace gi

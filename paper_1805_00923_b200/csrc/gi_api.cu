@@ -463,6 +463,33 @@ gi_status gi_cc_ex(gi_graph g, const gi_cc_opts* opts, int32_t* labels_out, gi_c
 
 gi_status gi_cc(gi_graph g, int32_t* labels_out) { return gi_cc_ex(g, nullptr, labels_out, nullptr); }
 
+gi_status gi_sssp_ex(gi_graph g, int32_t source, uint64_t weight_seed, const gi_sssp_opts* opts, int32_t* dist_out,
+                     gi_sssp_stats* stats) {
+  GI_GUARD_BEGIN
+  if (!g) return fail(GI_ERR_INVALID_ARGUMENT, "gi_sssp: NULL graph");
+  if (!dist_out) return fail(GI_ERR_INVALID_ARGUMENT, "gi_sssp: NULL output");
+  if (source < 0 || source >= g->n) return fail(GI_ERR_VERTEX_OUT_OF_RANGE, "gi_sssp: source not in [0, n)");
+  gi_sssp_opts o{};
+  if (opts) o = *opts;
+  if (o.policy < GI_BFS_AUTO || o.policy > GI_BFS_PULL_ONLY || o.threshold_div < 0)
+    return fail(GI_ERR_INVALID_ARGUMENT, "gi_sssp: bad options");
+  gi_context ctx = g->ctx;
+  if (ctx->nranks > 1) return fail(GI_ERR_UNSUPPORTED, "gi_sssp: single-GPU contexts only");
+  GI_CUDA(cudaSetDevice(ctx->device));
+  AllocScope as_(ctx->stream);
+  OutBuf<int32_t> ob{dist_out, g->n, false, &g->out_stage};
+  int32_t* d = nullptr;
+  GI_TRY(ob.prepare(g, &d));
+  GI_TRY(sssp_run(g, source, weight_seed, o, d, stats));
+  GI_TRY(ob.finish(ctx));
+  return sync(ctx);
+  GI_GUARD_END
+}
+
+gi_status gi_sssp(gi_graph g, int32_t source, uint64_t weight_seed, int32_t* dist_out) {
+  return gi_sssp_ex(g, source, weight_seed, nullptr, dist_out, nullptr);
+}
+
 gi_status gi_bfs_ex(gi_graph g, int32_t source, const gi_bfs_opts* opts, int32_t* parent_out, gi_bfs_stats* stats) {
   GI_GUARD_BEGIN
   if (!g) return fail(GI_ERR_INVALID_ARGUMENT, "gi_bfs: NULL graph");

@@ -199,8 +199,10 @@ struct gi_graph_s {
     gi::DevBuf chunks[2], scan_tmp;  // push: chunk counts / inclusive prefix, cub scan scratch
     size_t scan_bytes = 0;
   } ms;
-  struct {  // connected components (cc.cu): labels and the frontier bitmaps
-    gi::DevBuf ids, bm[2];
+  struct {  // connected components / SSSP (cc.cu): labels or distances, frontier bitmaps, edge weights
+    gi::DevBuf ids, bm[2], wcsr, wcsc;
+    bool w_ready = false;
+    uint64_t w_seed = 0;
   } ccs;
 };
 
@@ -225,6 +227,8 @@ gi_status seg_edge_pass(gi_graph g, const float* cin);
 // bit-parallel BFS / CC shared state (g->ms): masks, active lists, heavy-row chunks
 gi_status ms_prepare(gi_graph g);
 gi_status cc_run(gi_graph g, const gi_cc_opts& o, int32_t* d_out, gi_cc_stats* stats);  // cc.cu
+gi_status sssp_run(gi_graph g, int32_t source, uint64_t seed, const gi_cc_opts& o, int32_t* d_out,
+                   gi_cc_stats* stats);  // cc.cu
 // the two accumulators: cur holds the sums of the last edge pass; the other is zero
 inline float* seg_acc_buf(gi_graph g, int which) { return g->seg_acc.as<float>() + which * g->seg_acc_stride; }
 // vertex update from the current accumulator; zeroes the other one (never a

@@ -120,6 +120,8 @@ _SIGS = {
     "gi_bfs": ([_vp, _i32, _vp], _st),
     "gi_bfs_ex": ([_vp, _i32, ctypes.POINTER(gi_bfs_opts), _vp, ctypes.POINTER(gi_bfs_stats)], _st),
     "gi_cc": ([_vp, _vp], _st),
+    "gi_sssp": ([_vp, _i32, ctypes.c_uint64, _vp], _st),
+    "gi_sssp_ex": ([_vp, _i32, ctypes.c_uint64, ctypes.POINTER(gi_cc_opts), _vp, ctypes.POINTER(gi_cc_stats)], _st),
     "gi_cc_ex": ([_vp, ctypes.POINTER(gi_cc_opts), _vp, ctypes.POINTER(gi_cc_stats)], _st),
     "gi_bfs_multi": ([_vp, _i32, _vp, ctypes.POINTER(gi_bfs_opts), _vp, ctypes.POINTER(gi_bfs_stats)], _st),
     "gi_status_string": ([_st], ctypes.c_char_p),
@@ -347,6 +349,20 @@ def gi_cc_ex(g: int, out=None, policy: int = GI_BFS_AUTO, threshold_div: int = 0
     return keep, s
 
 
+def gi_sssp_ex(g: int, source: int, seed: int, out=None, policy: int = GI_BFS_AUTO, threshold_div: int = 0,
+               profile: bool = False):
+    """Shortest-path distances from source (frontier Bellman-Ford) with graphgen's synthetic weights
+    of `seed`; -1 = unreachable."""
+    n = gi_graph_num_vertices(g)
+    if out is None:
+        out = np.empty(n, np.int32)
+    p, keep = _ptr(out, np.int32)
+    o = gi_cc_opts(policy, threshold_div, int(profile), 0)
+    s = gi_cc_stats()
+    _check(_lib.gi_sssp_ex(g, source, seed, ctypes.byref(o), p or None, ctypes.byref(s)), "gi_sssp_ex")
+    return keep, s
+
+
 def gi_bfs_multi(g: int, sources, out=None, policy: int = GI_BFS_AUTO, threshold_div: int = 0,
                  profile: bool = False, batch: int = GI_BFS_BATCH_AUTO):
     """k BFS runs back to back; out: int32[k, n] (host or device). Returns (out, [stats])."""
@@ -426,6 +442,9 @@ class Graph:
 
     def cc(self, out=None, **kw):
         return gi_cc_ex(self.handle, out, **kw)
+
+    def sssp(self, source, seed=1, out=None, **kw):
+        return gi_sssp_ex(self.handle, source, seed, out, **kw)
 
     def bfs_multi(self, sources, out=None, **kw):
         return gi_bfs_multi(self.handle, sources, out, **kw)

@@ -617,3 +617,49 @@ def test_cc_device_output_and_errors(gi, ctx):
     with pytest.raises(gi.GiError) as e:
         g.cc(policy=7)
     assert e.value.status == gi.GI_ERR_INVALID_ARGUMENT
+
+
+# ---------------------------------------------------------------- SSSP (NEXT #4)
+@pytest.mark.parametrize("policy", POLICIES)
+def test_sssp_parity(gi, ctx, policy):
+    """gi_sssp == Dijkstra on the oracle's graph with graphgen's weights (exact
+    integers): directed and symmetrised RMAT, a fragmented grid, a path, a 100k-leaf
+    star; every direction policy; several sources and weight seeds."""
+    cfg = graphgen.CONFIGS[1]
+    s1, d1 = cfg.edges()
+    s3, d3 = graphgen.grid(96, 96, 0.2, 7)
+    ps = np.arange(499, dtype=np.int32)
+    cases = [("config1", cfg.n, s1, d1, False, [0, 5, 777]),
+             ("config1-sym", cfg.n, s1, d1, True, [3]),
+             ("grid96", 96 * 96, s3, d3, False, [0, 4000]),
+             ("path", 500, ps, ps + 1, False, [0, 250, 499]),
+             ("star", 100_001, *graphgen.star_bidirectional(100_000), False, [0, 77])]
+    for name, n, s, d, sym, srcs in cases:
+        flags = gi.GI_DEFAULT_FLAGS | (gi.GI_SYMMETRIZE if sym else 0)
+        g = gi.Graph(ctx, n, s, d, flags)
+        go = oracle.build_graph(n, s, d, symmetrize=sym)
+        for seed in (1, 99):
+            w = oracle.csr_weights(go, seed)
+            for src in srcs:
+                want = oracle.sssp(go, src, w)
+                got, st = g.sssp(src, seed=seed, policy=_pol(gi, policy))
+                assert (got.astype(np.int64) == want).all(), \
+                    f"{name} seed={seed} src={src} {policy}: {int((got != want).sum())} distances differ"
+        g.close()
+
+
+def test_sssp_device_output_and_errors(gi, ctx):
+    import torch
+
+    s, d = graphgen.rmat(12, 8, 0.57, 0.19, 0.19, 4)
+    n = 1 << 12
+    g = gi.Graph(ctx, n, s, d)
+    go = oracle.build_graph(n, s, d)
+    want = oracle.sssp(go, 0, oracle.csr_weights(go, 5))
+    out = torch.full((n,), -9, dtype=torch.int32, device="cuda")
+    got, st = g.sssp(0, seed=5, out=out, profile=True)
+    assert (got.cpu().numpy().astype(np.int64) == want).all()
+    assert st.total_ms > 0 and st.rounds >= 1
+    with pytest.raises(gi.GiError) as e:
+        g.sssp(n)
+    assert e.value.status == gi.GI_ERR_VERTEX_OUT_OF_RANGE
