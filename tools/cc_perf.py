@@ -1,6 +1,6 @@
-"""Connected-components timings: configs 2 (directed and symmetrised), 3, 4 (directed).
+"""Connected-components and SSSP timings: configs 2 (directed and symmetrised), 3, 4 (directed).
 
-usage: python tools/cc_perf.py [configs...]
+usage: python tools/cc_perf.py [configs...]   (a trailing s = symmetrised)
 """
 import json
 import os
@@ -32,12 +32,23 @@ for arg in sys.argv[1:] or ["2", "2s", "3", "4"]:
         _, st = g.cc(out=out, profile=True)
         if best is None or st.total_ms < best.total_ms:
             best = st
+    ssrc = 0 if cfg.source_seed == 0 else int(torch.nonzero(g.out_degrees(torch.empty(cfg.n, dtype=torch.int32,
+                                                                                       device="cuda")) > 0)[0])
+    g.sssp(ssrc, seed=1, out=out)
+    sbest = None
+    for _ in range(3):
+        _, sst = g.sssp(ssrc, seed=1, out=out, profile=True)
+        if sbest is None or sst.total_ms < sbest.total_ms:
+            sbest = sst
+    g.cc(out=out)
     labels = out.cpu()
     comps = int((labels == torch.arange(cfg.n, dtype=torch.int32)).sum())  # vertices that are their own label
     print(json.dumps({"config": cfg.name + (" sym" if sym else ""), "n": cfg.n, "m": g.m, "cc_ms": round(best.total_ms, 3),
                       "rounds": best.rounds, "pull_rounds": best.pull_rounds,
                       "edges_examined": best.edges_examined,
                       "gteps_examined": round(best.edges_examined / (best.total_ms * 1e-3) / 1e9, 1),
-                      "roots": comps}), flush=True)
+                      "roots": comps, "sssp_ms": round(sbest.total_ms, 3), "sssp_rounds": sbest.rounds,
+                      "sssp_pull_rounds": sbest.pull_rounds, "sssp_edges_examined": sbest.edges_examined}),
+          flush=True)
     g.close()
     torch.cuda.empty_cache()
