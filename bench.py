@@ -145,6 +145,17 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def bench_config(cfg, n, m, k, args, world, partition):
+    """The `config` object of the JSON line (both arms print the same one)."""
+    return {"workload": f"{cfg.name} (BASELINE configs[{cfg.idx - 1}])", "n": n, "m": m,
+            "pr_iters": cfg.pr_iters, "damping": cfg.damping, "bfs_sources": k,
+            "pr_direction": args.pr_direction,
+            "bfs_policy": "auto: bit-parallel pass of 64 sources, pull iff |F| + sum outdeg F > m/3",
+            "l2": "inputs larger than L2 (CSR+CSC ~ 8m bytes > 126 MB), no flush",
+            "parallelism": (f"dst-partition x{world} (NCCL allgather of contrib / frontier bitmap)"
+                            if partition else f"replicas x{world}") if world > 1 else "single"}
+
+
 def workload(cfg_idx):
     import graphgen
 
@@ -194,7 +205,7 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot_t / args.steps * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded RMAT/grid generators; paper datasets not available)",
-        "config": {"workload": cfg.name, "n": cfg.n, "m": g.m},
+        "config": bench_config(cfg, cfg.n, g.m, len(sources), args, world, world > 1 and args.mode == "partition"),
         "cpu_baseline": {"value": gteps, "unit": "GTEPS", "cores": cores, "kind": "oracle", "sample": sample},
         "e2e": {"value": gteps, "unit": "GTEPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -419,12 +430,7 @@ def run_ours(args):
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
             "scaling": "strong" if partition else "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded counter-based RMAT; stands in for LiveJournal, paper datasets unavailable)",
-            "config": {"workload": f"{cfg.name} (BASELINE configs[{cfg.idx - 1}])", "n": n, "m": m,
-                       "pr_iters": cfg.pr_iters, "damping": cfg.damping, "bfs_sources": len(srcs),
-                       "pr_direction": args.pr_direction, "bfs_policy": "auto: bit-parallel pass of 64 sources, pull iff |F| + sum outdeg F > m/3",
-                       "l2": "inputs larger than L2 (CSR+CSC ~ 8m bytes > 126 MB), no flush",
-                       "parallelism": (f"dst-partition x{world} (NCCL allgather of contrib / frontier bitmap)"
-                                       if partition else f"replicas x{world}") if world > 1 else "single"},
+            "config": bench_config(cfg, n, m, len(srcs), args, world, partition),
             "e2e": e2e, "gpu_launches": launches, "roofline": roofline, "roofline_pr": roofline_pr,
             "roofline_bfs": roofline_bfs, "cpu_baseline": cpu, "clocks": clocks,
             "pr_gteps": cfg.pr_iters * m / (pr_ms * 1e-3) / 1e9, "pr_ms": pr_ms,
