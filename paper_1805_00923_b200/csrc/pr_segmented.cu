@@ -79,6 +79,9 @@ constexpr int kStageBytes = kConsumers * kRecBytes;
 // CTA balance: an initial cost model (in gather slots), then refined from
 // measured per-CTA times over the first kCalibPasses edge passes (seg_rebalance)
 constexpr int kPieceCost = 4;
+#ifndef GI_ACC_PER_SM
+#define GI_ACC_PER_SM 4  // vertex-pass CTAs per SM
+#endif
 #ifndef GI_SEG_DIRECT
 #define GI_SEG_DIRECT 16
 #endif
@@ -1027,7 +1030,7 @@ gi_status seg_edge_pass(gi_graph g, const float* cin) {
 
 gi_status seg_vertex_pass(gi_graph g, const PrArgs& A) {
   cudaStream_t st = g->ctx->stream;
-  GI_TRY(launch_pdl(k_pr_acc, grid_for(ceil_div(g->nr, 4), 256, g->ctx->num_sms, 4), 256, 0, st, A,
+  GI_TRY(launch_pdl(k_pr_acc, grid_for(ceil_div(g->nr, 4), 256, g->ctx->num_sms, GI_ACC_PER_SM), 256, 0, st, A,
                     (const float*)seg_acc_buf(g, g->seg_acc_cur), seg_acc_buf(g, g->seg_acc_cur ^ 1)));
   g->seg_acc_cur ^= 1;
   return GI_OK;
