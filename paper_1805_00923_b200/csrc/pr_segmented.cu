@@ -79,6 +79,9 @@ constexpr int kStageBytes = kConsumers * kRecBytes;
 // CTA balance: an initial cost model (in gather slots), then refined from
 // measured per-CTA times over the first kCalibPasses edge passes (seg_rebalance)
 constexpr int kPieceCost = 4;
+#ifndef GI_SEG_EVICT_FIRST
+#define GI_SEG_EVICT_FIRST 1  // the record stream carries an L2 evict_first hint (keeps acc and contrib in L2)
+#endif
 #ifndef GI_ACC_PER_SM
 #define GI_ACC_PER_SM 4  // vertex-pass CTAs per SM
 #endif
@@ -138,6 +141,19 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t
                    smem_u32(dst)),
                "l"(src), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
+}
+
+// the same bulk copy with an L2 eviction-priority hint (the streamed records
+// are read once per pass: evict_first keeps the accumulator and contrib in L2)
+__device__ __forceinline__ void tma_load_1d_hint(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                                 uint64_t policy) {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
 }
 
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
@@ -297,12 +313,21 @@ __global__ void __launch_bounds__(kSegThreads, 1) k_pr_seg(SegArgs A) {
     }
     if (warp == kConsumers) {
       if (lane == 0) {  // producer
+#if GI_SEG_EVICT_FIRST
+        uint64_t rec_policy;
+        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(rec_policy));
+#endif
         for (int k = 0; k < nst; ++k, ++it) {
           const uint32_t s = it % kStages, ph = (it / kStages) & 1u;
           if (it >= kStages) mbar_wait(&empty[s], ph ^ 1u);  // consumers released this slot's last use
           const int cs = c0 + k * kConsumers;
           const int nc = min(kConsumers, ue - cs);
+#if GI_SEG_EVICT_FIRST
+          tma_load_1d_hint(ring + s * kStageBytes, A.rec + (int64_t)cs * kRecBytes, (uint32_t)(nc * kRecBytes),
+                           &full[s], rec_policy);
+#else
           tma_load_1d(ring + s * kStageBytes, A.rec + (int64_t)cs * kRecBytes, (uint32_t)(nc * kRecBytes), &full[s]);
+#endif
         }
       }
       it = __shfl_sync(0xffffffffu, it, 0);
