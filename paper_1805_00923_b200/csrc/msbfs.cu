@@ -45,6 +45,9 @@ namespace {
 #ifndef GI_MS_OUT
 #define GI_MS_OUT 1  // diagnostics: 0 drops the parent writes
 #endif
+#ifndef GI_MS_CS
+#define GI_MS_CS 0
+#endif
 #ifndef GI_MS_RMW
 #define GI_MS_RMW 1  // partially known sectors (unique writer) are read, merged and written whole
 #endif
@@ -94,6 +97,16 @@ struct MsArgs {
 };
 
 __device__ __forceinline__ int32_t in_id(const MsArgs& A, int32_t v) { return A.perm ? __ldg(&A.perm[v]) : v; }
+
+// edge-index streams are read once per level: evict-first (ld.global.cs) keeps
+// the frontier masks, seen and the parent rows in L2
+__device__ __forceinline__ int32_t ms_idx(const int32_t* p) {
+#if GI_MS_CS
+  return __ldcs(p);
+#else
+  return __ldg(p);
+#endif
+}
 
 // par row entries of the bits in m := val, a 32-byte sector (8 sources) at a
 // time. A sector none of whose bits is known yet (known = bits with a parent
@@ -213,7 +226,7 @@ __global__ void __launch_bounds__(kMsT) k_ms_pull(MsArgs A) {
           int32_t v[kPullBatch];
           unsigned long long f[kPullBatch];
 #pragma unroll
-          for (int j = 0; j < kPullBatch; ++j) v[j] = e + j < e1 ? __ldg(&A.csc_idx[e + j]) : -1;
+          for (int j = 0; j < kPullBatch; ++j) v[j] = e + j < e1 ? ms_idx(&A.csc_idx[e + j]) : -1;
 #pragma unroll
           for (int j = 0; j < kPullBatch; ++j) f[j] = v[j] >= 0 ? A.fcur[v[j]] : 0ull;
           exam += min((int64_t)kPullBatch, e1 - e);
@@ -300,7 +313,7 @@ __global__ void __launch_bounds__(kMsT) k_ms_pull_heavy(MsArgs A, const int2* __
 #pragma unroll
         for (int j = 0; j < kPullBatch; ++j) {
           const int64_t e = b + 32 * j + lane;
-          v[j] = e < e1 ? __ldg(&A.csc_idx[e]) : -1;
+          v[j] = e < e1 ? ms_idx(&A.csc_idx[e]) : -1;
         }
 #pragma unroll
         for (int j = 0; j < kPullBatch; ++j) f[j] = v[j] >= 0 ? A.fcur[v[j]] : 0ull;
@@ -445,7 +458,7 @@ __global__ void __launch_bounds__(kMsT) k_ms_push(MsArgs A, const long long* __r
       int32_t w = 0;
       if (my < stop) {
         const int32_t u = __ldg(&A.acur[i0 + pos]);
-        w = __ldg(&A.csr_idx[(int64_t)off[u] + (my - start)]);
+        w = ms_idx(&A.csr_idx[(int64_t)off[u] + (my - start)]);
         ++exam;
         const unsigned long long m = A.fcur[u] & ~*(volatile unsigned long long*)&A.seen[w];
         if (m) {
