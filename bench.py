@@ -379,14 +379,15 @@ def run_ours(args):
         hd = torch.from_numpy(d).pin_memory()
         hpr = torch.empty(n, dtype=torch.float32).pin_memory()
         hbfs = torch.empty((len(srcs), n), dtype=torch.int32).pin_memory()
-        # one untimed end-to-end step first (first-touch of pinned buffers and of the allocation pool)
-        gw = gi.Graph(ctx, cfg.n, hs, hd, flags)
-        gw.pagerank(cfg.pr_iters, cfg.damping, out=hpr, direction=direction)
-        gw.bfs_multi(srcs, out=hbfs)
-        gw.close()
+        # two untimed end-to-end steps first (first-touch of pinned buffers and of the allocation pool)
+        for _ in range(2):
+            gw = gi.Graph(ctx, cfg.n, hs, hd, flags)
+            gw.pagerank(cfg.pr_iters, cfg.damping, out=hpr, direction=direction)
+            gw.bfs_multi(srcs, out=hbfs)
+            gw.close()
         torch.cuda.synchronize()
         t = time.perf_counter()
-        e2e_steps = max(1, min(args.steps, 2))
+        e2e_steps = max(1, min(args.steps, 5))
         e_edges = 0
         dbg = os.environ.get("GI_BENCH_E2E_DEBUG")
         for _ in range(e2e_steps):
@@ -418,7 +419,7 @@ def run_ours(args):
         e2e = {"value": e_all / e2e_s / 1e9, "unit": "GTEPS",
                "h2d_bytes_per_step": int(8 * len(s)),
                "d2h_bytes_per_step": int(4 * n * (1 + len(srcs))), "steps": e2e_steps,
-               "includes": "gi_graph_create from pinned host edges + gi_pagerank + gi_bfs_multi over the sources, host outputs; one untimed warm-up step"}
+               "includes": "gi_graph_create from pinned host edges + gi_pagerank + gi_bfs_multi over the sources, host outputs; two untimed warm-up steps"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
