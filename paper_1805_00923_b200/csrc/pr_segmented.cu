@@ -491,19 +491,25 @@ __global__ void k_place_long(const int64_t* __restrict__ asz, const int64_t* __r
                              const uint32_t* __restrict__ skey, const OffT* __restrict__ order,
                              const int32_t* __restrict__ idx, const int32_t* __restrict__ pdst, int64_t P, int64_t m,
                              int Z, int S, uint8_t* __restrict__ rec) {
-  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < P; p += (int64_t)gridDim.x * blockDim.x) {
+  // a warp per piece, its lanes striding over the piece's edges (a hub's piece
+  // holds up to ~10^5 edges: one thread per piece serialised the build on them)
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t p = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; p < P; p += nw) {
     if (asz[p] == 0) continue;
     const int u = punit[p];
     const int64_t s0 = (int64_t)unit_c0[u] * kChunkE + (aoff[p] - aoff[unit_p0[u]]);  // slot in record units
     const int64_t len = (p + 1 < P ? pstart[p + 1] : m) - pstart[p];
     const int64_t base = (int64_t)(skey[pstart[p]] % (uint32_t)S) * Z;
-    for (int64_t o = 0; o < len; ++o) {
+    for (int64_t o = lane; o < len; o += 32) {
       const int64_t s = s0 + o;
       *reinterpret_cast<uint16_t*>(rec + (s / kChunkE) * kRecBytes + kRecHdr + 2 * (s % kChunkE)) =
           (uint16_t)(idx[(int64_t)order[pstart[p] + o]] - base);
     }
-    const int l0 = (int)((s0 % kChunkE) / kLaneE);
-    atomicOr(reinterpret_cast<uint32_t*>(rec + (s0 / kChunkE) * kRecBytes + kLMask), 1u << l0);
+    if (lane == 0) {
+      const int l0 = (int)((s0 % kChunkE) / kLaneE);
+      atomicOr(reinterpret_cast<uint32_t*>(rec + (s0 / kChunkE) * kRecBytes + kLMask), 1u << l0);
+    }
   }
 }
 
@@ -772,7 +778,7 @@ static gi_status seg_build_block(gi_graph g, int Z, int S, int64_t r0, int64_t r
   k_record_headers<<<grid_for(C * (kRecBytes / 4), 256, sms), 256, 0, st>>>(
       rtype.as<int32_t>(), rL.as<int32_t>(), rng.as<int32_t>(), C, Z, trash, unit_c0.as<int32_t>(), (int)U, S,
       out.rec.as<uint8_t>());
-  k_place_long<OffT><<<grid_for(P, 256, sms), 256, 0, st>>>(
+  k_place_long<OffT><<<grid_for(P * 32, 256, sms, 16), 256, 0, st>>>(
       asz.as<int64_t>(), aoff.as<int64_t>(), punit.as<int32_t>(), unit_p0.as<int64_t>(), unit_c0.as<int32_t>(),
       pstart.as<int64_t>(), skey.as<uint32_t>(), order.as<OffT>(), idx, pdst.as<int32_t>(), P, m, Z, S,
       out.rec.as<uint8_t>());
