@@ -37,13 +37,16 @@ gi_status cuda_fail(cudaError_t e, const char* what, const char* file, int line)
 
 // ------------------------------------------------------------------ device buffer
 // RAII device allocation (cudaMalloc; freed on destruction).
-// Allocations inside a library call are stream-ordered on the context's stream
-// (cudaMallocAsync / cudaFreeAsync from the device's pool, which keeps up to
-// kPoolKeep bytes cached), so the temporaries of a graph build or a layout
+// Allocations of up to kPoolMaxBlock bytes inside a library call are
+// stream-ordered on the context's stream (cudaMallocAsync / cudaFreeAsync from
+// the device's pool, which keeps up to kPoolKeep bytes cached), so the temporaries of a graph build or a layout
 // build, and a graph's buffers after gi_graph_destroy, are reused instead of
 // going back to cudaMalloc / cudaFree. AllocScope sets the stream for the
 // calling thread; outside a scope (or with GI_POOL=0) DevBuf uses cudaMalloc.
 constexpr uint64_t kPoolKeep = 16ull << 30;
+// larger buffers (the temporaries of a billion-edge build) use cudaMalloc: the
+// pool would release and re-map them around every synchronisation
+constexpr size_t kPoolMaxBlock = 2ull << 30;
 inline cudaStream_t& tl_alloc_stream() {
   static thread_local cudaStream_t s = nullptr;
   return s;
@@ -83,7 +86,7 @@ struct DevBuf {
     if (nbytes == 0) nbytes = 16;
     const cudaStream_t st = tl_alloc_stream();
     cudaError_t e;
-    if (st && pool_enabled()) {
+    if (st && pool_enabled() && nbytes <= kPoolMaxBlock) {
       e = cudaMallocAsync(&p, nbytes, st);
       pooled = e == cudaSuccess;
       s = st;

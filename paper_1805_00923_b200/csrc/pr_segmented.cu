@@ -46,6 +46,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cub/cub.cuh>
+#include <string>
 #include <vector>
 
 #include "gi_internal.cuh"
@@ -643,6 +644,19 @@ static gi_status seg_build_block(gi_graph g, int Z, int S, int64_t r0, int64_t r
   }
   const int64_t m = e1 - e0;
   if (m >= INT32_MAX) return fail(GI_ERR_INTERNAL, "segmented pull: block of 2^31 edges");
+  // diagnostics (GI_DEBUG_SEG_LAYOUT): synchronised phase times of this block's build
+  static const char* ldbg = getenv("GI_DEBUG_SEG_LAYOUT");
+  auto tp = std::chrono::steady_clock::now();
+  std::string phases;
+  auto mark = [&](const char* name) {
+    if (!ldbg) return;
+    cudaStreamSynchronize(st);
+    const auto t2 = std::chrono::steady_clock::now();
+    char b[64];
+    snprintf(b, sizeof(b), " %s=%.1f", name, std::chrono::duration<double, std::milli>(t2 - tp).count());
+    phases += b;
+    tp = t2;
+  };
   const OffT* off = g->csc_off.as<OffT>() + r0;
   const int32_t* idx = g->csc_idx.as<int32_t>() + e0;
   const int U = S;  // this block's units
@@ -664,10 +678,12 @@ static gi_status seg_build_block(gi_graph g, int Z, int S, int64_t r0, int64_t r
   GI_TRY(order.alloc(m * sizeof(OffT)));
   k_unit_keys<OffT><<<grid_for(m, 256, sms), 256, 0, st>>>(idx, row.as<int32_t>(), m, Z, S, DB, key.as<uint32_t>(),
                                                           eid.as<OffT>());
+  mark("keys");
   int kbits = 1;
   while ((1ll << kbits) < U) ++kbits;
   // stable: (v, w) order is kept inside each unit
   GI_TRY(sort_pairs(key.as<uint32_t>(), skey.as<uint32_t>(), eid.as<OffT>(), order.as<OffT>(), m, kbits, tmp, st));
+  mark("sort1");
   key.reset();
   eid.reset();
   // ---- pieces: (unit, destination) runs of the sorted edges
@@ -688,6 +704,7 @@ static gi_status seg_build_block(gi_graph g, int Z, int S, int64_t r0, int64_t r
                                                             order.as<OffT>(), row.as<int32_t>(), m,
                                                             pstart.as<int64_t>(), punit.as<int32_t>(),
                                                             pdst.as<int32_t>());
+  mark("pieces");
   h.reset();
   pid.reset();
   row.reset();
@@ -708,6 +725,7 @@ static gi_status seg_build_block(gi_graph g, int Z, int S, int64_t r0, int64_t r
   while ((1ll << cbits) <= (int64_t)sentinel) ++cbits;
   GI_TRY(sort_pairs(ckey.as<uint32_t>(), sckey.as<uint32_t>(), pids.as<int32_t>(), spid.as<int32_t>(), P, cbits, tmp,
                     st));
+  mark("classes");
   ckey.reset();
   pids.reset();
   const int64_t NC = (int64_t)U * 16;  // short classes (L = 0 unused)
@@ -725,6 +743,7 @@ static gi_status seg_build_block(gi_graph g, int Z, int S, int64_t r0, int64_t r
   for (int u = 0; u <= U; ++u)
     GI_CUDA(cudaMemcpyAsync(&h_ao[u], aoff.as<int64_t>() + h_up0[u], sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   GI_CUDA(cudaStreamSynchronize(st));
+  mark("bounds");
   // ---- record layout: per unit, long records then short records by L
   std::vector<int32_t> h_uc(U + 1), h_crec0(NC, 0), h_type, h_L, h_ng;
   std::vector<int64_t> h_cost;  // per record, for the CTA balance
@@ -759,6 +778,7 @@ static gi_status seg_build_block(gi_graph g, int Z, int S, int64_t r0, int64_t r
     if (C >= INT32_MAX) return fail(GI_ERR_UNSUPPORTED, "segmented pull: more than 2^31 records");
   }
   h_uc[U] = (int32_t)C;
+  mark("host_layout");
   DevBuf unit_c0, crec0, rtype, rL, rng;
   GI_TRY(unit_c0.alloc((U + 1) * sizeof(int32_t)));
   GI_TRY(crec0.alloc((NC + 1) * sizeof(int32_t)));
@@ -778,10 +798,12 @@ static gi_status seg_build_block(gi_graph g, int Z, int S, int64_t r0, int64_t r
   k_record_headers<<<grid_for(C * (kRecBytes / 4), 256, sms), 256, 0, st>>>(
       rtype.as<int32_t>(), rL.as<int32_t>(), rng.as<int32_t>(), C, Z, trash, unit_c0.as<int32_t>(), (int)U, S,
       out.rec.as<uint8_t>());
+  mark("headers");
   k_place_long<OffT><<<grid_for(P * 32, 256, sms, 16), 256, 0, st>>>(
       asz.as<int64_t>(), aoff.as<int64_t>(), punit.as<int32_t>(), unit_p0.as<int64_t>(), unit_c0.as<int32_t>(),
       pstart.as<int64_t>(), skey.as<uint32_t>(), order.as<OffT>(), idx, pdst.as<int32_t>(), P, m, Z, S,
       out.rec.as<uint8_t>());
+  mark("place_long");
   k_long_dst<<<grid_for(P, 256, sms), 256, 0, st>>>(asz.as<int64_t>(), aoff.as<int64_t>(), punit.as<int32_t>(),
                                                     unit_p0.as<int64_t>(), unit_c0.as<int32_t>(), pdst.as<int32_t>(),
                                                     P, out.rec.as<uint8_t>());
@@ -789,6 +811,12 @@ static gi_status seg_build_block(gi_graph g, int Z, int S, int64_t r0, int64_t r
     k_place_short<OffT><<<grid_for(NS, 256, sms), 256, 0, st>>>(
         sckey.as<uint32_t>(), spid.as<int32_t>(), NS, cstart.as<int64_t>(), crec0.as<int32_t>(), pstart.as<int64_t>(),
         skey.as<uint32_t>(), order.as<OffT>(), idx, pdst.as<int32_t>(), Z, S, out.rec.as<uint8_t>());
+  mark("long_dst+short");
+  if (ldbg && !phases.empty())
+    if (FILE* f = fopen(ldbg, "a")) {
+      fprintf(f, "block rows [%lld, %lld) edges %lld:%s\n", (long long)r0, (long long)r1, (long long)m, phases.c_str());
+      fclose(f);
+    }
   GI_CUDA(cudaGetLastError());
   GI_CUDA(cudaStreamSynchronize(st));  // the temporaries are freed on return
   out.uc = std::move(h_uc);

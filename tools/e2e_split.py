@@ -21,7 +21,7 @@ ctx = gi.Context(0)
 hs, hd = torch.from_numpy(s).pin_memory(), torch.from_numpy(d).pin_memory()
 hpr = torch.empty(cfg.n, dtype=torch.float32).pin_memory()
 hbfs = torch.empty((len(srcs), cfg.n), dtype=torch.int32).pin_memory()
-for rep in range(3):
+for rep in range(int(os.environ.get("E2E_REPS", "3"))):
     t = [time.perf_counter()]
     g = gi.Graph(ctx, cfg.n, hs, hd, gi.GI_DEFAULT_FLAGS)
     torch.cuda.synchronize(); t.append(time.perf_counter())
