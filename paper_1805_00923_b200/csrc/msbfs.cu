@@ -15,18 +15,22 @@
 //   act[c]     the vertices with fr[c][v] != 0 (push levels read it)
 // Per level (direction: pull iff |F| + sum outdeg F > m / 3 — a pull rarely
 // exits early here, since a vertex stops only once it has all k sources):
-//   pull (DensePull + early exit): light rows (in-degree < 32) a thread each,
-//     heavy rows a warp each; a row ORs the frontier masks of its in-neighbours
-//     into the bits it misses, recording for every new bit the in-neighbour
-//     that brought it, and stops once it has every source;
-//   push (SparsePush, edge-balanced): the active vertices' out-edges in chunks
-//     of 256 per warp; an edge claims new bits with atomicOr on seen (the
-//     returned old value says which bits this edge won) and adds them to the
-//     next frontier. Sinks (out-degree 0) never enter the active list.
+//   pull (DensePull + early exit): light rows (in-degree < 32) a thread each;
+//     heavy rows cut into chunks of <= 1024 in-edges, a warp per chunk (chunks
+//     of one row race through atomicOr on seen / fr_next, R8 parents either
+//     way); a row ORs the frontier masks of its in-neighbours into the bits it
+//     misses, recording for every new bit an in-neighbour that brought it, and
+//     stops once it has every source;
+//   push (SparsePush): the active vertices' out-edges, concatenated by an
+//     inclusive prefix of their out-degrees and walked 32 at a time, a lane per
+//     edge; an edge claims new bits with atomicOr on seen (the returned old
+//     value says which bits this edge won) and adds them to the next frontier.
+//     Sinks (out-degree 0) never enter the active list.
 // Parents are staged vertex-major (par[v][i], rows of k rounded up to a power of two >= 8) so a
-// vertex's bits land in one 256-byte row; the epilogue transposes them into the
-// k output rows (int32[k][n], input ids; -1 where source i never reached v)
-// and counts, per source, the vertices reached and their out-degrees.
+// vertex's bits land in one 256-byte row; the epilogue (registers, a lane per
+// vertex) writes them into the k output rows (int32[k][n], input ids; -1 where
+// source i never reached v) and counts, per source, the vertices reached and
+// their out-degrees.
 #include <algorithm>
 #include <chrono>
 #include <climits>
@@ -521,87 +525,65 @@ __global__ void k_ms_init(const int32_t* __restrict__ src_in, int k, const int32
   }
 }
 
-// The pass's epilogue, a CTA per tile of kFinV consecutive input ids v:
-//   out[i][v] = source i's parent of v, or -1 when i never reached v — the
-//     tile's vertex-major parents (kFinV rows of kp, contiguous, 16-byte
-//     loads) are transposed through shared memory so each of the k output
-//     rows gets one contiguous 4 x kFinV-byte segment;
-//   per source i: vertices reached and the sum of their out-degrees (R16).
-#ifndef GI_MS_FINV
-#define GI_MS_FINV 128
-#endif
-constexpr int kFinV = GI_MS_FINV;  // vertices per tile
-constexpr int kFinT = 256;  // threads per CTA
-__global__ void __launch_bounds__(kFinT) k_ms_finish(const int32_t* __restrict__ par,
-                                                    const unsigned long long* __restrict__ seen,
-                                                    const int32_t* __restrict__ inv,
-                                                    const int32_t* __restrict__ outdeg, int64_t n, int k, int lkp,
-                                                    int32_t* __restrict__ out,
-                                                    unsigned long long* __restrict__ reached,
-                                                    unsigned long long* __restrict__ edges) {
-  extern __shared__ int32_t tile[];  // [64][kFinV + 1]
-  __shared__ unsigned long long sv[kFinV], sod[kFinV];
+// The pass's epilogue: out[i][v] (input ids) = source i's parent of v, or -1
+// when i never reached v, and per source the vertices reached and the sum of
+// their out-degrees (R16). A warp per 32 consecutive input ids, lane l owns
+// vertex v0 + l. The lane reads its vertex's parent row (whole 32-byte sectors,
+// 16 sources per pass) into registers; then for each source b the warp stores
+// out[b][v0 .. v0+31] — lane l's register b — as one coalesced 128-byte row
+// segment. No shared-memory transpose, no block barrier.
+template <int KP>
+__global__ void __launch_bounds__(256) k_ms_finish_reg(const int32_t* __restrict__ par,
+                                                      const unsigned long long* __restrict__ seen,
+                                                      const int32_t* __restrict__ inv,
+                                                      const int32_t* __restrict__ outdeg, int64_t n, int k,
+                                                      int32_t* __restrict__ out,
+                                                      unsigned long long* __restrict__ reached,
+                                                      unsigned long long* __restrict__ edges) {
   __shared__ unsigned long long r[64], d[64];
-  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
-  const int kp = 1 << lkp, lrq = lkp - 2;  // par row: kp ints = 2^lrq int4s
-  for (int i = threadIdx.x; i < 64; i += kFinT) r[i] = d[i] = 0;
+  const int lane = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < 64; i += blockDim.x) r[i] = d[i] = 0;
+  __syncthreads();
   unsigned long long r0 = 0, r1 = 0, d0 = 0, d1 = 0;
-  for (int64_t v0 = blockIdx.x * (int64_t)kFinV; v0 < n; v0 += (int64_t)gridDim.x * kFinV) {
-    const int nv = (int)(n - v0 < kFinV ? n - v0 : kFinV);
-    const int nq = nv << lrq;  // int4s of the tile's rows
-    const int4* p4 = reinterpret_cast<const int4*>(par + v0 * kp);
-    if (threadIdx.x < kFinV) {
-      const int64_t v = v0 + threadIdx.x;
-      const int32_t w = v < n ? (inv ? __ldg(&inv[v]) : (int32_t)v) : 0;
-      sv[threadIdx.x] = v < n ? seen[w] : 0ull;
-      sod[threadIdx.x] = v < n ? (unsigned long long)__ldg(&outdeg[w]) : 0ull;
-    }
-    __syncthreads();
-    int4 q[kFinV * 16 / kFinT];
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; t * 32 < n; t += nw) {
+    const int64_t v = t * 32 + lane;
+    const bool in = v < n;
+    const int32_t w = in ? (inv ? __ldg(&inv[v]) : (int32_t)v) : 0;
+    const unsigned long long sv = in ? seen[w] : 0ull;
+    const unsigned long long ov = in ? (unsigned long long)__ldg(&outdeg[w]) : 0ull;
+    const int4* row = reinterpret_cast<const int4*>(par + v * KP);
 #pragma unroll
-    for (int j = 0; j < kFinV * 16 / kFinT; ++j) {  // rows of vertices no source reached are never read
-      const int qi = threadIdx.x + kFinT * j;
-      q[j] = qi < nq && sv[qi >> lrq] ? __ldg(&p4[qi]) : make_int4(0, 0, 0, 0);
-    }
+    for (int b0 = 0; b0 < KP; b0 += 16) {
+      if (b0 >= k) break;
+      int4 q[4];
 #pragma unroll
-    for (int j = 0; j < kFinV * 16 / kFinT; ++j) {
-      const int qi = threadIdx.x + kFinT * j;
-      if (qi < nq) {
-        const int vv = qi >> lrq, b = (qi & ((1 << lrq) - 1)) * 4;
-        tile[(b + 0) * (kFinV + 1) + vv] = q[j].x;
-        tile[(b + 1) * (kFinV + 1) + vv] = q[j].y;
-        tile[(b + 2) * (kFinV + 1) + vv] = q[j].z;
-        tile[(b + 3) * (kFinV + 1) + vv] = q[j].w;
+      for (int j = 0; j < 4; ++j)  // unreached vertices' rows are never read
+        q[j] = sv ? __ldg(&row[b0 / 4 + j]) : make_int4(-1, -1, -1, -1);
+      const int32_t x[16] = {q[0].x, q[0].y, q[0].z, q[0].w, q[1].x, q[1].y, q[1].z, q[1].w,
+                             q[2].x, q[2].y, q[2].z, q[2].w, q[3].x, q[3].y, q[3].z, q[3].w};
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const int b = b0 + j;
+        if (b < k && in) out[(int64_t)b * n + v] = (sv >> b) & 1ull ? x[j] : -1;
       }
     }
-    __syncthreads();
-    // rows: warp wp writes rows wp, wp + 8, ...; a row's segment is kFinV / 32 coalesced stores
-    for (int b = wp; b < k; b += kFinT / 32) {
-#pragma unroll
-      for (int c = 0; c < kFinV / 32; ++c) {
-        const int vv = c * 32 + lane;
-        if (vv < nv) out[(int64_t)b * n + v0 + vv] = (sv[vv] >> b) & 1ull ? tile[b * (kFinV + 1) + vv] : -1;
-      }
-    }
-    // stats: every warp takes kFinV / 8 vertices; lane counts sources lane and lane + 32
-    {
-      constexpr int kPer = kFinV / (kFinT / 32);
+    if (__ballot_sync(0xffffffffu, sv != 0) == 0) continue;
 #pragma unroll 4
-      for (int j = 0; j < kPer; ++j) {
-        const unsigned long long s = sv[wp * kPer + j], od = sod[wp * kPer + j];  // (broadcast reads)
-        const unsigned long long b0 = (s >> lane) & 1ull, b1 = (s >> (lane + 32)) & 1ull;
-        r0 += b0;
-        r1 += b1;
-        d0 += b0 * od;
-        d1 += b1 * od;
-      }
+    for (int j = 0; j < 32; ++j) {
+      const unsigned long long s = __shfl_sync(0xffffffffu, sv, j);
+      const unsigned long long od = __shfl_sync(0xffffffffu, ov, j);
+      const unsigned long long b0 = (s >> lane) & 1ull, b1 = (s >> (lane + 32)) & 1ull;
+      r0 += b0;
+      r1 += b1;
+      d0 += b0 * od;
+      d1 += b1 * od;
     }
-    __syncthreads();
   }
   if (r0) { atomicAdd(&r[lane], r0); atomicAdd(&d[lane], d0); }
   if (r1) { atomicAdd(&r[lane + 32], r1); atomicAdd(&d[lane + 32], d1); }
   __syncthreads();
-  for (int i = threadIdx.x; i < k; i += kFinT) {
+  for (int i = threadIdx.x; i < k; i += blockDim.x) {
     if (r[i]) atomicAdd(&reached[i], r[i]);
     if (d[i]) atomicAdd(&edges[i], d[i]);
   }
@@ -780,12 +762,11 @@ gi_status msbfs_t(gi_graph g, int32_t k, const int32_t* sources, const gi_bfs_op
   if (df) fclose(df);
   unsigned long long* hr = cnt + 4;
   GI_CUDA(cudaMemsetAsync(hr, 0, 2 * 64 * 8, st));
-  {
-    const size_t smem = (size_t)64 * (kFinV + 1) * 4;
-    GI_CUDA(cudaFuncSetAttribute(k_ms_finish, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_ms_finish<<<grid_for(n, kFinV, sms, 6), kFinT, smem, st>>>(
-        M.par.as<int32_t>(), M.seen.as<unsigned long long>(), A.inv, g->outdeg.as<int32_t>(), n, k, lkp, d_out, hr,
-        hr + 64);
+  {  // epilogue: transpose into the k output rows + per-source counts (R16)
+    auto* fk = kp == 8 ? k_ms_finish_reg<8> : kp == 16 ? k_ms_finish_reg<16> : kp == 32 ? k_ms_finish_reg<32>
+                                                                                      : k_ms_finish_reg<64>;
+    fk<<<grid_for(n, 256, sms, 8), 256, 0, st>>>(M.par.as<int32_t>(), M.seen.as<unsigned long long>(), A.inv,
+                                                 g->outdeg.as<int32_t>(), n, k, d_out, hr, hr + 64);
   }
   ++launches;
   std::vector<unsigned long long> hs(128);
