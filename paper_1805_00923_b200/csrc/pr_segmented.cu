@@ -744,6 +744,7 @@ static gi_status seg_build_block(gi_graph g, int Z, int S, int64_t r0, int64_t r
     GI_CUDA(cudaMemcpyAsync(&h_ao[u], aoff.as<int64_t>() + h_up0[u], sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   GI_CUDA(cudaStreamSynchronize(st));
   mark("bounds");
+  int64_t hist_L[16] = {};  // short pieces by length (layout diagnostics)
   // ---- record layout: per unit, long records then short records by L
   std::vector<int32_t> h_uc(U + 1), h_crec0(NC, 0), h_type, h_L, h_ng;
   std::vector<int64_t> h_cost;  // per record, for the CTA balance
@@ -764,6 +765,7 @@ static gi_status seg_build_block(gi_graph g, int Z, int S, int64_t r0, int64_t r
       const int64_t k = (int64_t)u * 16 + L;
       const int64_t cnt = h_cs[k + 1] - h_cs[k];
       NS += cnt;
+      hist_L[L] += cnt;
       h_crec0[k] = (int32_t)C;
       const int64_t groups = ceil_div(cnt, 32), R = short_groups(L);
       for (int64_t gq = 0; gq < groups; gq += R) {
@@ -814,7 +816,10 @@ static gi_status seg_build_block(gi_graph g, int Z, int S, int64_t r0, int64_t r
   mark("long_dst+short");
   if (ldbg && !phases.empty())
     if (FILE* f = fopen(ldbg, "a")) {
-      fprintf(f, "block rows [%lld, %lld) edges %lld:%s\n", (long long)r0, (long long)r1, (long long)m, phases.c_str());
+      fprintf(f, "block rows [%lld, %lld) edges %lld:%s\n  short pieces by L:", (long long)r0, (long long)r1,
+              (long long)m, phases.c_str());
+      for (int L = 1; L < 16; ++L) fprintf(f, " %d:%lld", L, (long long)hist_L[L]);
+      fprintf(f, "\n");
       fclose(f);
     }
   GI_CUDA(cudaGetLastError());
