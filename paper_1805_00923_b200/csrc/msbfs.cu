@@ -60,12 +60,12 @@ constexpr int kMsT = 256;
 #define GI_MS_HEAVY 32
 #endif
 constexpr int64_t kHeavy = GI_MS_HEAVY;  // rows with at least this many in-edges are pulled by whole warps
-constexpr int kMsPullDiv = 3;
-constexpr int kPushChunk = 256;
+constexpr int kMsPullDiv = 3;     // bit-parallel direction rule: pull iff |F| + sum outdeg F > m / 3 (R21)
+constexpr int kPushChunk = 256;   // push: out-edges per warp at least
 #ifndef GI_MS_BATCH
 #define GI_MS_BATCH 4
 #endif
-constexpr int kPullBatch = GI_MS_BATCH;
+constexpr int kPullBatch = GI_MS_BATCH;  // in-edge gathers in flight per pull step
 #ifndef GI_MS_HCHUNK
 #define GI_MS_HCHUNK 1024
 #endif
@@ -77,7 +77,7 @@ constexpr int kHeavyPer = GI_MS_HPER;  // heavy chunks per warp
 #ifndef GI_MS_LPERSM
 #define GI_MS_LPERSM 16
 #endif
-constexpr int kLightPerSM = GI_MS_LPERSM;  // light-row pull CTAs per SM (grid-stride beyond)  // in-edge gathers in flight per pull step  // out-edges per push work item   // bit-parallel direction rule: pull iff |F| + sum outdeg F > m / 3
+constexpr int kLightPerSM = GI_MS_LPERSM;  // light-row pull CTAs per SM (grid-stride beyond)
 
 struct MsArgs {
   int64_t n;
