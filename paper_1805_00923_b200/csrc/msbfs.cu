@@ -94,8 +94,11 @@ struct MsArgs {
   const int32_t* __restrict__ acur;  // active vertices of the current level (push)
   int32_t* anext;                    // active vertices of the next level
   unsigned long long* cnt;           // [0] |active next|, [1] sum outdeg, [2] OR of new bits, [3] edges examined
-  int32_t* par;                      // parents, vertex-major by input id: par[input id * kp + source bit]
+  int32_t* par;                      // heavy rows' parents (input ids): par[hidx[v] * kp + source bit]
   int kp;                            // par row stride: k rounded up to a power of two >= 8
+  uint8_t* par8;                     // light rows: par8[v * 64 + source bit] = index of the parent in v's
+                                     //   in-edge list (< 32), 0xFF = v is that source itself
+  const int32_t* __restrict__ hidx;  // heavy row -> its par row, -1 for a light row
   int64_t nact;
   unsigned long long all;            // mask of the k sources
 };
@@ -162,6 +165,30 @@ __device__ __forceinline__ void par_put(int32_t* row, unsigned long long m, unsi
   }
 }
 
+// light row: byte entries of the bits in m := idx, read-merge-write per 32-byte
+// sector (32 sources); the pull thread is the row's only writer in its launch
+__device__ __forceinline__ void par8_put(uint8_t* row, unsigned long long m, uint32_t idx) {
+#pragma unroll
+  for (int g = 0; g < 2; ++g) {
+    const unsigned nm = (unsigned)(m >> (32 * g));
+    if (!nm) continue;
+    uint32_t x[8];
+    asm volatile("ld.global.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(x[0]), "=r"(x[1]), "=r"(x[2]), "=r"(x[3]), "=r"(x[4]), "=r"(x[5]), "=r"(x[6]), "=r"(x[7])
+                 : "l"(row + 32 * g));
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const unsigned q = (nm >> (4 * j)) & 0xFu;
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+        if ((q >> b) & 1u) x[j] = (x[j] & ~(0xFFu << (8 * b))) | (idx << (8 * b));
+    }
+    asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(row + 32 * g), "r"(x[0]), "r"(x[1]),
+                 "r"(x[2]), "r"(x[3]), "r"(x[4]), "r"(x[5]), "r"(x[6]), "r"(x[7])
+                 : "memory");
+  }
+}
+
 // CTA-aggregated append of the active vertices (one atomic per CTA round)
 __device__ __forceinline__ void ms_append(const MsArgs& A, bool act, int32_t v, int* s_cnt, long long* s_base) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -225,7 +252,6 @@ __global__ void __launch_bounds__(kMsT) k_ms_pull(MsArgs A) {
       const int64_t e0 = (int64_t)off[w], e1 = (int64_t)off[w + 1];
       const unsigned long long s = e1 - e0 >= kHeavy ? A.all : A.seen[w];  // heavy rows: k_ms_pull_heavy
       if (s != A.all) {
-        int32_t wi = -1;  // input id of w, looked up at its first new bit
         for (int64_t e = e0; e < e1; e += kPullBatch) {  // kPullBatch independent gathers per step
           int32_t v[kPullBatch];
           unsigned long long f[kPullBatch];
@@ -237,10 +263,8 @@ __global__ void __launch_bounds__(kMsT) k_ms_pull(MsArgs A) {
 #pragma unroll
           for (int j = 0; j < kPullBatch; ++j) {
             const unsigned long long m = f[j] & ~s & ~found;
-            if (m) {
-              const int32_t vin = in_id(A, v[j]);
-              if (wi < 0) wi = in_id(A, w);
-              if (GI_MS_OUT) par_put<true>(A.par + (int64_t)wi * A.kp, m, s | found, vin);
+            if (m) {  // the parent of these bits: in-edge e + j - e0 of the row
+              if (GI_MS_OUT) par8_put(A.par8 + (int64_t)w * 64, m, (uint32_t)(e + j - e0));
               found |= m;
             }
           }
@@ -303,11 +327,10 @@ __global__ void __launch_bounds__(kMsT) k_ms_pull_heavy(MsArgs A, const int2* __
     const unsigned long long s = *(volatile unsigned long long*)&A.seen[w];
     bool newact = false;
     if (s != A.all) {
-      const int32_t wi = in_id(A, w);
       const int64_t rb = (int64_t)off[w], re = (int64_t)off[w + 1];
       const int64_t e0 = rb + ch.y, e1 = min(re, e0 + kHChunk);
       const bool whole = re - rb <= kHChunk;  // the warp is the row's only writer this launch
-      int32_t* prow = A.par + (int64_t)wi * A.kp;
+      int32_t* prow = A.par + (int64_t)__ldg(&A.hidx[w]) * A.kp;
       // lane L keeps the parents of sources L (plo) and 32 + L (phi)
       int32_t plo = 0, phi = 0;
       unsigned long long found = 0;
@@ -386,6 +409,11 @@ __global__ void __launch_bounds__(kMsT) k_ms_pull_heavy(MsArgs A, const int2* __
     if (lane < nbuf) A.anext[pos + lane] = s_buf[wp][lane];
   }
   ms_counters(A, tdeg, tbits, exam);
+}
+
+__global__ void k_ms_hidx(const int32_t* __restrict__ heavy, int64_t nh, int32_t* __restrict__ hidx) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nh; i += (int64_t)gridDim.x * blockDim.x)
+    hidx[heavy[i]] = (int32_t)i;
 }
 
 // heavy-row chunks: cc[i] = chunks of heavy row i; then (row, first in-edge offset) per chunk
@@ -468,8 +496,23 @@ __global__ void __launch_bounds__(kMsT) k_ms_push(MsArgs A, const long long* __r
         if (m) {
           const unsigned long long got = m & ~atomicOr(&A.seen[w], m);  // the bits this edge claims
           if (got) {
-            const int32_t win = in_id(A, w);
-            if (GI_MS_OUT) par_put<false>(A.par + (int64_t)win * A.kp, got, 0ull, in_id(A, u));
+            if (GI_MS_OUT) {
+              const int32_t h = __ldg(&A.hidx[w]);
+              if (h >= 0) {
+                par_put<false>(A.par + (int64_t)h * A.kp, got, 0ull, in_id(A, u));
+              } else {  // light row: u's position in w's in-edge list (sorted, < 32 entries)
+                const OffT* __restrict__ coff = static_cast<const OffT*>(A.csc_off);
+                int64_t lo = (int64_t)coff[w], hi = (int64_t)coff[w + 1];
+                const int64_t base = lo;
+                while (lo < hi) {
+                  const int64_t mid = (lo + hi) >> 1;
+                  if (__ldg(&A.csc_idx[mid]) < u) lo = mid + 1;
+                  else hi = mid;
+                }
+                for (unsigned long long x = got; x; x &= x - 1)
+                  A.par8[(int64_t)w * 64 + __ffsll((long long)x) - 1] = (uint8_t)(lo - base);
+              }
+            }
             bits |= got;
             if (atomicOr(&A.fnext[w], got) == 0ull) {  // w's first bits this level: it joins the next frontier
               const int32_t dw = __ldg(&A.outdeg[w]);
@@ -512,13 +555,15 @@ __global__ void __launch_bounds__(kMsT) k_ms_push(MsArgs A, const long long* __r
 // sources: bit i at source i (internal id), its own parent in row i, active list
 __global__ void k_ms_init(const int32_t* __restrict__ src_in, int k, const int32_t* __restrict__ inv, int64_t n,
                           const int32_t* __restrict__ outdeg, unsigned long long* seen, unsigned long long* f0,
-                          int32_t* act, unsigned long long* cnt, int32_t* par, int kp) {
+                          int32_t* act, unsigned long long* cnt, int32_t* par, int kp, uint8_t* par8,
+                          const int32_t* __restrict__ hidx) {
   const int i = threadIdx.x;
   if (i >= k) return;
   const int32_t si = src_in[i];
   const int32_t s = inv ? inv[si] : si;
   atomicOr(&seen[s], 1ull << i);
-  par[(int64_t)si * kp + i] = si;
+  if (hidx[s] >= 0) par[(int64_t)hidx[s] * kp + i] = si;
+  else par8[(int64_t)s * 64 + i] = 0xFF;  // the source is its own parent
   if (atomicOr(&f0[s], 1ull << i) == 0ull) {
     act[atomicAdd(&cnt[0], 1ull)] = s;
     atomicAdd(&cnt[1], (unsigned long long)outdeg[s]);
@@ -532,8 +577,13 @@ __global__ void k_ms_init(const int32_t* __restrict__ src_in, int k, const int32
 // 16 sources per pass) into registers; then for each source b the warp stores
 // out[b][v0 .. v0+31] — lane l's register b — as one coalesced 128-byte row
 // segment. No shared-memory transpose, no block barrier.
-template <int KP>
+template <typename OffT, int KP>
 __global__ void __launch_bounds__(256) k_ms_finish_reg(const int32_t* __restrict__ par,
+                                                      const uint8_t* __restrict__ par8,
+                                                      const int32_t* __restrict__ hidx,
+                                                      const OffT* __restrict__ csc_off,
+                                                      const int32_t* __restrict__ csc_idx,
+                                                      const int32_t* __restrict__ perm,
                                                       const unsigned long long* __restrict__ seen,
                                                       const int32_t* __restrict__ inv,
                                                       const int32_t* __restrict__ outdeg, int64_t n, int k,
@@ -541,10 +591,12 @@ __global__ void __launch_bounds__(256) k_ms_finish_reg(const int32_t* __restrict
                                                       unsigned long long* __restrict__ reached,
                                                       unsigned long long* __restrict__ edges) {
   __shared__ unsigned long long r[64], d[64];
-  const int lane = threadIdx.x & 31;
+  __shared__ int32_t nbr[8][32][33];  // per warp and lane: a light row's in-neighbours in input ids
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
   for (int i = threadIdx.x; i < 64; i += blockDim.x) r[i] = d[i] = 0;
   __syncthreads();
   unsigned long long r0 = 0, r1 = 0, d0 = 0, d1 = 0;
+  int32_t* my = nbr[wp][lane];
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; t * 32 < n; t += nw) {
     const int64_t v = t * 32 + lane;
@@ -552,16 +604,46 @@ __global__ void __launch_bounds__(256) k_ms_finish_reg(const int32_t* __restrict
     const int32_t w = in ? (inv ? __ldg(&inv[v]) : (int32_t)v) : 0;
     const unsigned long long sv = in ? seen[w] : 0ull;
     const unsigned long long ov = in ? (unsigned long long)__ldg(&outdeg[w]) : 0ull;
-    const int4* row = reinterpret_cast<const int4*>(par + v * KP);
+    const int32_t h = sv ? __ldg(&hidx[w]) : -1;
+    const bool light = sv && h < 0;
+    uint4 p8[4] = {};
+    if (light) {  // byte row (parent = an in-edge index) and the row's in-neighbours' input ids
+      const uint4* r8 = reinterpret_cast<const uint4*>(par8 + (int64_t)w * 64);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) p8[j] = __ldg(&r8[j]);
+      const int64_t e0 = (int64_t)csc_off[w];
+      const int deg = (int)((int64_t)csc_off[w + 1] - e0);
+      for (int j0 = 0; j0 < deg; j0 += 8) {
+        int32_t u[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) u[j] = j0 + j < deg ? __ldg(&csc_idx[e0 + j0 + j]) : 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if (j0 + j < deg) my[j0 + j] = perm ? __ldg(&perm[u[j]]) : u[j];
+      }
+    }
+    const int4* row = reinterpret_cast<const int4*>(par + (int64_t)(h < 0 ? 0 : h) * KP);
+    const uint32_t* b8 = reinterpret_cast<const uint32_t*>(p8);
 #pragma unroll
     for (int b0 = 0; b0 < KP; b0 += 16) {
       if (b0 >= k) break;
-      int4 q[4];
+      int32_t x[16];
+      if (light) {
 #pragma unroll
-      for (int j = 0; j < 4; ++j)  // unreached vertices' rows are never read
-        q[j] = sv ? __ldg(&row[b0 / 4 + j]) : make_int4(-1, -1, -1, -1);
-      const int32_t x[16] = {q[0].x, q[0].y, q[0].z, q[0].w, q[1].x, q[1].y, q[1].z, q[1].w,
-                             q[2].x, q[2].y, q[2].z, q[2].w, q[3].x, q[3].y, q[3].z, q[3].w};
+        for (int j = 0; j < 16; ++j) {
+          const uint32_t byte = (b8[(b0 + j) >> 2] >> (8 * ((b0 + j) & 3))) & 0xFFu;
+          x[j] = byte == 0xFFu ? (int32_t)v : my[byte & 31u];
+        }
+      } else {
+        int4 q[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j)  // unreached vertices' rows are never read
+          q[j] = sv ? __ldg(&row[b0 / 4 + j]) : make_int4(-1, -1, -1, -1);
+        const int32_t y[16] = {q[0].x, q[0].y, q[0].z, q[0].w, q[1].x, q[1].y, q[1].z, q[1].w,
+                               q[2].x, q[2].y, q[2].z, q[2].w, q[3].x, q[3].y, q[3].z, q[3].w};
+#pragma unroll
+        for (int j = 0; j < 16; ++j) x[j] = y[j];
+      }
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
         const int b = b0 + j;
@@ -573,11 +655,11 @@ __global__ void __launch_bounds__(256) k_ms_finish_reg(const int32_t* __restrict
     for (int j = 0; j < 32; ++j) {
       const unsigned long long s = __shfl_sync(0xffffffffu, sv, j);
       const unsigned long long od = __shfl_sync(0xffffffffu, ov, j);
-      const unsigned long long b0 = (s >> lane) & 1ull, b1 = (s >> (lane + 32)) & 1ull;
-      r0 += b0;
-      r1 += b1;
-      d0 += b0 * od;
-      d1 += b1 * od;
+      const unsigned long long bb0 = (s >> lane) & 1ull, bb1 = (s >> (lane + 32)) & 1ull;
+      r0 += bb0;
+      r1 += bb1;
+      d0 += bb0 * od;
+      d1 += bb1 * od;
     }
   }
   if (r0) { atomicAdd(&r[lane], r0); atomicAdd(&d[lane], d0); }
@@ -623,6 +705,12 @@ static gi_status ms_prepare_t(gi_graph g) {
     GI_CUDA(cudaMemcpyAsync(&hn, M.cnt.p, 8, cudaMemcpyDeviceToHost, st));
     GI_CUDA(cudaStreamSynchronize(st));
     M.nheavy = hn;
+    // heavy rows' compact index into the int32 parent rows; light rows (< kHeavy in-edges)
+    // stage their parents as 1-byte in-edge indices
+    GI_TRY(M.hidx.alloc((n + 1) * 4));
+    GI_CUDA(cudaMemsetAsync(M.hidx.p, 0xFF, (n + 1) * 4, st));
+    if (hn > 0) k_ms_hidx<<<grid_for(hn, 256, sms), 256, 0, st>>>(M.heavy.as<int32_t>(), hn, M.hidx.as<int32_t>());
+    GI_TRY(M.par8.alloc((size_t)n * 64 + 64));
     M.nhch = 0;
     if (hn > 0) {
       int32_t* cc = M.chunks[0].as<int32_t>();
@@ -659,7 +747,7 @@ gi_status msbfs_t(gi_graph g, int32_t k, const int32_t* sources, const gi_bfs_op
   int lkp = 3;  // par row: kp = 2^lkp >= k ints (whole 32-byte sectors, power-of-two tiles in the epilogue)
   while ((1 << lkp) < k) ++lkp;
   const int kp = 1 << lkp;
-  if (M.par.bytes < (size_t)n * kp * 4) GI_TRY(M.par.alloc((size_t)n * kp * 4));
+  if (M.par.bytes < (size_t)(M.nheavy + 1) * kp * 4) GI_TRY(M.par.alloc((size_t)(M.nheavy + 1) * kp * 4));
   cudaEvent_t e0 = nullptr, e1 = nullptr, pe0 = nullptr, pe1 = nullptr;
   int64_t pull_examined = 0;
   float pull_ms = 0.f;
@@ -682,7 +770,8 @@ gi_status msbfs_t(gi_graph g, int32_t k, const int32_t* sources, const gi_bfs_op
   GI_CUDA(cudaMemcpyAsync(M.src.p, sources, k * sizeof(int32_t), cudaMemcpyHostToDevice, st));
   k_ms_init<<<1, 64, 0, st>>>(M.src.as<int32_t>(), k, g->relabeled ? g->inv.as<int32_t>() : nullptr, n,
                               g->outdeg.as<int32_t>(), M.seen.as<unsigned long long>(), M.fr[0].as<unsigned long long>(),
-                              M.act[0].as<int32_t>(), cnt, M.par.as<int32_t>(), kp);
+                              M.act[0].as<int32_t>(), cnt, M.par.as<int32_t>(), kp, M.par8.as<uint8_t>(),
+                              M.hidx.as<int32_t>());
   launches += 1;
   GI_CUDA(cudaMemcpyAsync(h, cnt, 4 * 8, cudaMemcpyDeviceToHost, st));
   GI_CUDA(stream_wait(st));
@@ -700,6 +789,8 @@ gi_status msbfs_t(gi_graph g, int32_t k, const int32_t* sources, const gi_bfs_op
   A.seen = M.seen.as<unsigned long long>();
   A.cnt = cnt;
   A.par = M.par.as<int32_t>();
+  A.par8 = M.par8.as<uint8_t>();
+  A.hidx = M.hidx.as<int32_t>();
   A.kp = kp;
   A.all = k == 64 ? ~0ull : ((1ull << k) - 1ull);
   static const char* dbg = getenv("GI_DEBUG_MSBFS");  // diagnostics: per-level direction, size, time
@@ -762,11 +853,13 @@ gi_status msbfs_t(gi_graph g, int32_t k, const int32_t* sources, const gi_bfs_op
   if (df) fclose(df);
   unsigned long long* hr = cnt + 4;
   GI_CUDA(cudaMemsetAsync(hr, 0, 2 * 64 * 8, st));
-  {  // epilogue: transpose into the k output rows + per-source counts (R16)
-    auto* fk = kp == 8 ? k_ms_finish_reg<8> : kp == 16 ? k_ms_finish_reg<16> : kp == 32 ? k_ms_finish_reg<32>
-                                                                                      : k_ms_finish_reg<64>;
-    fk<<<grid_for(n, 256, sms, 8), 256, 0, st>>>(M.par.as<int32_t>(), M.seen.as<unsigned long long>(), A.inv,
-                                                 g->outdeg.as<int32_t>(), n, k, d_out, hr, hr + 64);
+  {  // epilogue: the k output rows + per-source counts (R16)
+    auto* fk = kp == 8 ? k_ms_finish_reg<OffT, 8> : kp == 16 ? k_ms_finish_reg<OffT, 16>
+             : kp == 32 ? k_ms_finish_reg<OffT, 32> : k_ms_finish_reg<OffT, 64>;
+    fk<<<grid_for(n, 256, sms, 8), 256, 0, st>>>(
+        M.par.as<int32_t>(), M.par8.as<uint8_t>(), M.hidx.as<int32_t>(), g->csc_off.as<OffT>(),
+        g->csc_idx.as<int32_t>(), g->relabeled ? g->perm.as<int32_t>() : nullptr, M.seen.as<unsigned long long>(),
+        A.inv, g->outdeg.as<int32_t>(), n, k, d_out, hr, hr + 64);
   }
   ++launches;
   std::vector<unsigned long long> hs(128);
