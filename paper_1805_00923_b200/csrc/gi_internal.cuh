@@ -195,7 +195,7 @@ struct gi_graph_s {
   } fused;
   unsigned bfs_epoch = 0;
   struct {  // bit-parallel multi-source BFS (msbfs.cu)
-    gi::DevBuf seen, fr[2], act[2], cnt, src, heavy, par, par8, hidx;
+    gi::DevBuf seen, fr[2], act[2], cnt, src, heavy, par, par8, hidx, csc_in;
     int64_t nheavy = 0;  // rows with in-degree >= 32 (pulled by whole warps)
     gi::DevBuf hch;      // their chunks: int2 (row, first in-edge offset)
     int64_t nhch = 0;

@@ -411,6 +411,12 @@ __global__ void __launch_bounds__(kMsT) k_ms_pull_heavy(MsArgs A, const int2* __
   ms_counters(A, tdeg, tbits, exam);
 }
 
+__global__ void k_ms_csc_in(const int32_t* __restrict__ idx, int64_t m, const int32_t* __restrict__ perm,
+                            int32_t* __restrict__ out) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x)
+    out[e] = perm ? __ldg(&perm[idx[e]]) : idx[e];
+}
+
 __global__ void k_ms_hidx(const int32_t* __restrict__ heavy, int64_t nh, int32_t* __restrict__ hidx) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nh; i += (int64_t)gridDim.x * blockDim.x)
     hidx[heavy[i]] = (int32_t)i;
@@ -582,8 +588,7 @@ __global__ void __launch_bounds__(256) k_ms_finish_reg(const int32_t* __restrict
                                                       const uint8_t* __restrict__ par8,
                                                       const int32_t* __restrict__ hidx,
                                                       const OffT* __restrict__ csc_off,
-                                                      const int32_t* __restrict__ csc_idx,
-                                                      const int32_t* __restrict__ perm,
+                                                      const int32_t* __restrict__ csc_in,
                                                       const unsigned long long* __restrict__ seen,
                                                       const int32_t* __restrict__ inv,
                                                       const int32_t* __restrict__ outdeg, int64_t n, int k,
@@ -613,13 +618,13 @@ __global__ void __launch_bounds__(256) k_ms_finish_reg(const int32_t* __restrict
       for (int j = 0; j < 4; ++j) p8[j] = __ldg(&r8[j]);
       const int64_t e0 = (int64_t)csc_off[w];
       const int deg = (int)((int64_t)csc_off[w + 1] - e0);
-      for (int j0 = 0; j0 < deg; j0 += 8) {
+      for (int j0 = 0; j0 < deg; j0 += 8) {  // csc_in: the CSC's sources already in input ids
         int32_t u[8];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) u[j] = j0 + j < deg ? __ldg(&csc_idx[e0 + j0 + j]) : 0;
+        for (int j = 0; j < 8; ++j) u[j] = j0 + j < deg ? __ldg(&csc_in[e0 + j0 + j]) : 0;
 #pragma unroll
         for (int j = 0; j < 8; ++j)
-          if (j0 + j < deg) my[j0 + j] = perm ? __ldg(&perm[u[j]]) : u[j];
+          if (j0 + j < deg) my[j0 + j] = u[j];
       }
     }
     const int4* row = reinterpret_cast<const int4*>(par + (int64_t)(h < 0 ? 0 : h) * KP);
@@ -711,6 +716,11 @@ static gi_status ms_prepare_t(gi_graph g) {
     GI_CUDA(cudaMemsetAsync(M.hidx.p, 0xFF, (n + 1) * 4, st));
     if (hn > 0) k_ms_hidx<<<grid_for(hn, 256, sms), 256, 0, st>>>(M.heavy.as<int32_t>(), hn, M.hidx.as<int32_t>());
     GI_TRY(M.par8.alloc((size_t)n * 64 + 64));
+    // the CSC's sources in input ids (the epilogue resolves light rows' parent indices through it)
+    GI_TRY(M.csc_in.alloc((size_t)(g->ml + 1) * 4));
+    k_ms_csc_in<<<grid_for(g->ml, 256, sms), 256, 0, st>>>(g->csc_idx.as<int32_t>(), g->ml,
+                                                          g->relabeled ? g->perm.as<int32_t>() : nullptr,
+                                                          M.csc_in.as<int32_t>());
     M.nhch = 0;
     if (hn > 0) {
       int32_t* cc = M.chunks[0].as<int32_t>();
@@ -858,7 +868,7 @@ gi_status msbfs_t(gi_graph g, int32_t k, const int32_t* sources, const gi_bfs_op
              : kp == 32 ? k_ms_finish_reg<OffT, 32> : k_ms_finish_reg<OffT, 64>;
     fk<<<grid_for(n, 256, sms, 8), 256, 0, st>>>(
         M.par.as<int32_t>(), M.par8.as<uint8_t>(), M.hidx.as<int32_t>(), g->csc_off.as<OffT>(),
-        g->csc_idx.as<int32_t>(), g->relabeled ? g->perm.as<int32_t>() : nullptr, M.seen.as<unsigned long long>(),
+        M.csc_in.as<int32_t>(), M.seen.as<unsigned long long>(),
         A.inv, g->outdeg.as<int32_t>(), n, k, d_out, hr, hr + 64);
   }
   ++launches;
