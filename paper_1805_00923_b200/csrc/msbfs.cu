@@ -506,17 +506,20 @@ __global__ void __launch_bounds__(kMsT) k_ms_push(MsArgs A, const long long* __r
               const int32_t h = __ldg(&A.hidx[w]);
               if (h >= 0) {
                 par_put<false>(A.par + (int64_t)h * A.kp, got, 0ull, in_id(A, u));
-              } else {  // light row: u's position in w's in-edge list (sorted, < 32 entries)
+              } else {  // light row: u's position in w's in-edge list (< 32 entries, scanned 8 at a time)
                 const OffT* __restrict__ coff = static_cast<const OffT*>(A.csc_off);
-                int64_t lo = (int64_t)coff[w], hi = (int64_t)coff[w + 1];
-                const int64_t base = lo;
-                while (lo < hi) {
-                  const int64_t mid = (lo + hi) >> 1;
-                  if (__ldg(&A.csc_idx[mid]) < u) lo = mid + 1;
-                  else hi = mid;
+                const int64_t lo = (int64_t)coff[w], hi = (int64_t)coff[w + 1];
+                int pos = 0;
+                for (int64_t e = lo; e < hi; e += 8) {
+                  int32_t x[8];
+#pragma unroll
+                  for (int j = 0; j < 8; ++j) x[j] = e + j < hi ? __ldg(&A.csc_idx[e + j]) : -1;
+#pragma unroll
+                  for (int j = 0; j < 8; ++j)
+                    if (x[j] == u) pos = (int)(e + j - lo);
                 }
                 for (unsigned long long x = got; x; x &= x - 1)
-                  A.par8[(int64_t)w * 64 + __ffsll((long long)x) - 1] = (uint8_t)(lo - base);
+                  A.par8[(int64_t)w * 64 + __ffsll((long long)x) - 1] = (uint8_t)pos;
               }
             }
             bits |= got;
