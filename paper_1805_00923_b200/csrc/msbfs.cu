@@ -52,9 +52,6 @@ namespace {
 #ifndef GI_MS_CS
 #define GI_MS_CS 0
 #endif
-#ifndef GI_MS_RMW
-#define GI_MS_RMW 1  // partially known sectors (unique writer) are read, merged and written whole
-#endif
 constexpr int kMsT = 256;
 #ifndef GI_MS_HEAVY
 #define GI_MS_HEAVY 32
@@ -115,49 +112,15 @@ __device__ __forceinline__ int32_t ms_idx(const int32_t* p) {
 #endif
 }
 
-// par row entries of the bits in m := val, a 32-byte sector (8 sources) at a
-// time. A sector none of whose bits is known yet (known = bits with a parent
-// already, or being written concurrently) is stored whole with one 256-bit
-// store — its other entries get val as a placeholder, overwritten when their
-// bit is found and masked by seen in the epilogue — so the sector's first
-// write is never a partial one (no read-modify-write of a partially written
-// line in HBM). Sectors with known bits get per-entry stores. UNIQUE: the
-// caller is the only writer of this row in the launch (else only sectors
-// whose 8 bits are all in m are stored whole).
-template <bool UNIQUE>
-__device__ __forceinline__ void par_put(int32_t* row, unsigned long long m, unsigned long long known, int32_t val) {
+// heavy row (several writers may claim bits of it concurrently): entries of
+// the bits in m := val; a sector whose 8 bits are all in m is stored whole
+// with one 256-bit store, other bits one entry at a time
+__device__ __forceinline__ void par_put(int32_t* row, unsigned long long m, int32_t val) {
   while (m) {
     const int g = (__ffsll((long long)m) - 1) >> 3;
     const unsigned nm = (unsigned)(m >> (8 * g)) & 0xFFu;
-    const unsigned kn = (unsigned)(known >> (8 * g)) & 0xFFu;
-    if (UNIQUE ? kn == 0u : nm == 0xFFu) {
+    if (nm == 0xFFu) {
       asm volatile("st.global.v8.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1};" ::"l"(row + 8 * g), "r"(val) : "memory");
-    } else if (UNIQUE && GI_MS_RMW) {  // read the sector, merge the new entries, write it whole
-      int32_t x[8];
-      asm volatile("ld.global.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                   : "=r"(x[0]), "=r"(x[1]), "=r"(x[2]), "=r"(x[3]), "=r"(x[4]), "=r"(x[5]), "=r"(x[6]), "=r"(x[7])
-                   : "l"(row + 8 * g));
-#pragma unroll
-      for (int j = 0; j < 8; ++j)
-        if ((nm >> j) & 1u) x[j] = val;
-      asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(row + 8 * g), "r"(x[0]), "r"(x[1]),
-                   "r"(x[2]), "r"(x[3]), "r"(x[4]), "r"(x[5]), "r"(x[6]), "r"(x[7])
-                   : "memory");
-    } else if (UNIQUE) {  // halves / pairs without known bits go as one vector store each
-      for (int h = 0; h < 8; h += 4) {
-        const unsigned n4 = (nm >> h) & 0xFu, k4 = (kn >> h) & 0xFu;
-        if (!n4) continue;
-        if (!k4) {
-          *reinterpret_cast<int4*>(row + 8 * g + h) = make_int4(val, val, val, val);
-          continue;
-        }
-        for (int p = h; p < h + 4; p += 2) {
-          const unsigned n2 = (nm >> p) & 3u, k2 = (kn >> p) & 3u;
-          if (!n2) continue;
-          if (!k2) *reinterpret_cast<int2*>(row + 8 * g + p) = make_int2(val, val);
-          else row[8 * g + p + (n2 & 1u ? 0 : 1)] = val;  // one of the pair is known, the other new
-        }
-      }
     } else {
       for (unsigned q = nm; q; q &= q - 1) row[8 * g + __ffs(q) - 1] = val;
     }
@@ -505,7 +468,7 @@ __global__ void __launch_bounds__(kMsT) k_ms_push(MsArgs A, const long long* __r
             if (GI_MS_OUT) {
               const int32_t h = __ldg(&A.hidx[w]);
               if (h >= 0) {
-                par_put<false>(A.par + (int64_t)h * A.kp, got, 0ull, in_id(A, u));
+                par_put(A.par + (int64_t)h * A.kp, got, in_id(A, u));
               } else {  // light row: u's position in w's in-edge list (< 32 entries, scanned 8 at a time)
                 const OffT* __restrict__ coff = static_cast<const OffT*>(A.csc_off);
                 const int64_t lo = (int64_t)coff[w], hi = (int64_t)coff[w + 1];
