@@ -260,6 +260,33 @@ __global__ void __launch_bounds__(kCT) k_cc_push(CcArgs A, const long long* __re
   cc_counters(A, deg, exam);
 }
 
+// after a segmented min pass (every in-neighbour, not only F's: the labels only
+// fall, so the fixed point is the same): IDs[v] = min(IDs[v], acc[v]); a row
+// whose label dropped joins the next frontier
+__global__ void __launch_bounds__(kCT) k_cc_apply(CcArgs A, const int32_t* __restrict__ acc) {
+  __shared__ int32_t s_buf[kCT / 32][64];
+  const int lane = threadIdx.x & 31;
+  int32_t* buf = s_buf[threadIdx.x >> 5];
+  int nbuf = 0;
+  unsigned long long deg = 0;
+  for (int64_t b = (blockIdx.x * (int64_t)kCT + threadIdx.x) & ~31ll; b < A.n; b += (int64_t)gridDim.x * kCT) {
+    const int64_t w = b + lane;
+    bool changed = false;
+    if (w < A.n) {
+      const int32_t a = acc[w];
+      if (a < A.ids[w]) {
+        A.ids[w] = a;
+        changed = true;
+      }
+    }
+    const unsigned word = __ballot_sync(0xffffffffu, changed);
+    if (word && lane == 0) A.bnext[b >> 5] = word;
+    cc_append(A, changed, (int32_t)w, deg, buf, nbuf);
+  }
+  if (nbuf > 0) cc_flush(A, buf, nbuf);
+  cc_counters(A, deg, 0);
+}
+
 // out[input id of v] = IDs[v]
 __global__ void k_cc_out(const int32_t* __restrict__ ids, const int32_t* __restrict__ perm, int64_t n,
                          int32_t* __restrict__ out) {
@@ -351,6 +378,14 @@ gi_status cc_t(gi_graph g, const gi_cc_opts& o, int32_t source, uint64_t seed, i
   int64_t* h = ctx->h_scratch;
   int launches = 1, rounds = 0, pulls = 0;
   int64_t nf = n, sdeg = g->m, examined = 0;
+  // CC pull rounds use the segmented layout when the graph has one (skewed,
+  // relabelled graphs; built on first use, shared with PageRank)
+  static const bool seg_env = !getenv("GI_CC_SEG") || atoi(getenv("GI_CC_SEG")) != 0;
+  bool seg = false;
+  if (!W && seg_env && g->relabeled && g->ctx->nranks == 1 && g->ml > 0 && seg_build(g, 0, 0) == GI_OK) {
+    seg = true;
+    if (!K.acc.p) GI_TRY(K.acc.alloc((n + 64) * 4));
+  }
   if (W) {  // weights of this seed (cached with the graph), dist, frontier {source}
     if (!K.w_ready || K.w_seed != seed) {
       if (!K.wcsr.p) {
@@ -405,7 +440,14 @@ gi_status cc_t(gi_graph g, const gi_cc_opts& o, int32_t source, uint64_t seed, i
     GI_CUDA(cudaMemsetAsync(A.bnext, 0, words * 4, st));
     GI_CUDA(cudaMemsetAsync(cnt, 0, 3 * 8, st));
     const bool pull = (o.policy == GI_BFS_PULL_ONLY && (r > 0 || !W)) || (o.policy == GI_BFS_AUTO && nf + sdeg > mdiv);
-    if (pull) {
+    if (pull && seg) {  // CC: a min pass over the segmented layout, then the label update
+      GI_CUDA(cudaMemsetAsync(K.acc.p, 0x7F, (n + 64) * 4, st));  // 0x7F7F7F7F exceeds every label
+      GI_TRY(seg_min_pass(g, K.ids.as<int32_t>(), K.acc.as<int32_t>()));
+      k_cc_apply<<<grid_for(n, kCT, sms, 16), kCT, 0, st>>>(A, K.acc.as<int32_t>());
+      launches += 2;
+      examined += g->m;
+      ++pulls;
+    } else if (pull) {
       k_cc_pull<OffT, W><<<grid_for(n, kCT, sms, 16), kCT, 0, st>>>(A);
       ++launches;
       if (M.nhch > 0) {

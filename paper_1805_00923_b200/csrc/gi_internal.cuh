@@ -203,7 +203,7 @@ struct gi_graph_s {
     size_t scan_bytes = 0;
   } ms;
   struct {  // connected components / SSSP (cc.cu): labels or distances, frontier bitmaps, edge weights
-    gi::DevBuf ids, bm[2], wcsr, wcsc;
+    gi::DevBuf ids, bm[2], wcsr, wcsc, acc;
     bool w_ready = false;
     uint64_t w_seed = 0;
   } ccs;
@@ -227,6 +227,8 @@ struct PrArgs;
 gi_status seg_build(gi_graph g, int segment_size, int64_t block_rows);
 // seg_acc_buf(g, cur)[v] = sum of cin over v's in-edges (the buffer is zero before the pass)
 gi_status seg_edge_pass(gi_graph g, const float* cin);
+// a min pass over the segmented layout: acc[v] = min(acc[v], labels[u] over in-edges (u, v)) (CC, cc.cu)
+gi_status seg_min_pass(gi_graph g, const int32_t* labels, int32_t* acc);
 // bit-parallel BFS / CC shared state (g->ms): masks, active lists, heavy-row chunks
 gi_status ms_prepare(gi_graph g);
 gi_status cc_run(gi_graph g, const gi_cc_opts& o, int32_t* d_out, gi_cc_stats* stats);  // cc.cu

@@ -42,6 +42,7 @@
 //   k_pr_acc  r'[v] = (1-d)/n + d (acc[v] + D/n), contrib', dangling mass
 //             (fused vertex update a3); zeroes the other (ping-pong) accumulator.
 #include <algorithm>
+#include <climits>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -173,21 +174,38 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-// a contrib value of the unit's segment: from the staged copy in shared memory,
-// or (G: a sparse unit, not staged) straight from global memory; offset Z is
-// the zero slot that padding slots point at
-template <bool G>
-__device__ __forceinline__ float seg_val(const float* sc, uint32_t o, uint32_t Z) {
-  if (G) return o < Z ? __ldg(sc + o) : 0.f;
+// The reduction a pass folds over a destination's in-edges: PageRank's sum of
+// fp32 contributions (RED.ADD.F32), or connected components' min of int32
+// labels (RED.MIN.S32) — the same records, gathers and piece structure.
+struct OpSum {
+  using T = float;
+  static __device__ __forceinline__ T id() { return 0.f; }
+  static __device__ __forceinline__ T op(T a, T b) { return a + b; }
+  static __device__ __forceinline__ void red(T* p, T v) { atomicAdd(p, v); }
+};
+struct OpMin {
+  using T = int32_t;
+  static __device__ __forceinline__ T id() { return INT_MAX; }
+  static __device__ __forceinline__ T op(T a, T b) { return min(a, b); }
+  static __device__ __forceinline__ void red(T* p, T v) { atomicMin(p, v); }
+};
+
+// a value of the unit's segment: from the staged copy in shared memory, or (G:
+// a sparse unit, not staged) straight from global memory; offset Z is the
+// identity slot that padding slots point at
+template <bool G, class OP>
+__device__ __forceinline__ typename OP::T seg_val(const typename OP::T* sc, uint32_t o, uint32_t Z) {
+  if (G) return o < Z ? __ldg(sc + o) : OP::id();
   return sc[o];
 }
 
 // Long record: every lane's 16 slots belong to one piece, so a lane sums its
 // gathers; a warp segmented scan over lanes (reset where the mask marks a
 // piece start) leaves each piece's sum in its last lane, which folds it into acc.
-template <int MODE, bool G>
-__device__ __forceinline__ void reduce_long(const SegArgs& A, const uint8_t* r, const float* sc, int lane,
+template <int MODE, bool G, class OP>
+__device__ __forceinline__ void reduce_long(const SegArgs& A, const uint8_t* r, const typename OP::T* sc, int lane,
                                             uint64_t* empty) {
+  using T = typename OP::T;
   const uint4 qa = *reinterpret_cast<const uint4*>(r + kRecHdr + 32 * lane);
   const uint4 qb = *reinterpret_cast<const uint4*>(r + kRecHdr + 32 * lane + 16);
   const uint32_t mask = *reinterpret_cast<const uint32_t*>(r + kLMask);
@@ -196,56 +214,57 @@ __device__ __forceinline__ void reduce_long(const SegArgs& A, const uint8_t* r, 
   __syncwarp();
   if (lane == 0) mbar_arrive(empty);  // the record may be overwritten now
   const uint32_t w[8] = {qa.x, qa.y, qa.z, qa.w, qb.x, qb.y, qb.z, qb.w};
-  float v[kLaneE];
+  T v[kLaneE];
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
-    v[2 * j] = seg_val<G>(sc, w[j] & 0xFFFFu, A.Z);
-    v[2 * j + 1] = seg_val<G>(sc, w[j] >> 16, A.Z);
+    v[2 * j] = seg_val<G, OP>(sc, w[j] & 0xFFFFu, A.Z);
+    v[2 * j + 1] = seg_val<G, OP>(sc, w[j] >> 16, A.Z);
   }
 #pragma unroll
   for (int s = 1; s < kLaneE; s <<= 1)
 #pragma unroll
-    for (int k = 0; k < kLaneE; k += 2 * s) v[k] += v[k + s];
-  float X = v[0];
+    for (int k = 0; k < kLaneE; k += 2 * s) v[k] = OP::op(v[k], v[k + s]);
+  T X = v[0];
   if (MODE == 1) {  // diagnostics: stream + gathers only
-    if (X == -1.f) A.acc[lane] += X;
+    if (X == (T)-1) A.acc[lane] += (float)X;
     return;
   }
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
-    const float y = __shfl_up_sync(0xffffffffu, X, o);
-    if (lane >= o && ((mask >> (lane - o + 1)) & ((1u << o) - 1u)) == 0u) X = y + X;
+    const T y = __shfl_up_sync(0xffffffffu, X, o);
+    if (lane >= o && ((mask >> (lane - o + 1)) & ((1u << o) - 1u)) == 0u) X = OP::op(y, X);
   }
   const bool last = lane == 31 || ((mask >> (lane + 1)) & 1u);
-  if (last) atomicAdd(A.acc + dst, X);  // RED.E.ADD.F32
+  if (last) OP::red(reinterpret_cast<T*>(A.acc) + dst, X);  // RED.E.ADD.F32 / RED.E.MIN.S32
 }
 
 // Short record of pieces with exactly L edges: lane l of group g owns one
 // piece: L gathers, one RED.
-template <int MODE, bool G>
-__device__ __forceinline__ void reduce_short(const SegArgs& A, const uint8_t* r, const float* sc, int lane,
+template <int MODE, bool G, class OP>
+__device__ __forceinline__ void reduce_short(const SegArgs& A, const uint8_t* r, const typename OP::T* sc, int lane,
                                              uint64_t* empty) {
+  using T = typename OP::T;
   const int L = *reinterpret_cast<const int32_t*>(r + 4);
   const int ng = *reinterpret_cast<const int32_t*>(r + 8);
   const int gb = short_group_bytes(L);
   for (int g = 0; g < ng; ++g) {
     const uint8_t* b = r + kRecHdr + g * gb + 2 * lane;
     const int d = *reinterpret_cast<const int32_t*>(r + kRecHdr + g * gb + 64 * L + 4 * lane);
-    float s = 0.f;
+    T s = OP::id();
 #pragma unroll 4
-    for (int k = 0; k < L; ++k) s += seg_val<G>(sc, *reinterpret_cast<const uint16_t*>(b + 64 * k), A.Z);
+    for (int k = 0; k < L; ++k) s = OP::op(s, seg_val<G, OP>(sc, *reinterpret_cast<const uint16_t*>(b + 64 * k), A.Z));
     if (MODE == 1) {
-      if (s == -1.f) A.acc[lane] += s;
+      if (s == (T)-1) A.acc[lane] += (float)s;
     } else {
-      atomicAdd(A.acc + d, s);  // RED.E.ADD.F32
+      OP::red(reinterpret_cast<T*>(A.acc) + d, s);  // RED.E.ADD.F32 / RED.E.MIN.S32
     }
   }
   __syncwarp();
   if (lane == 0) mbar_arrive(empty);
 }
 
-template <int MODE, bool G>
-__device__ __forceinline__ void reduce_record(const SegArgs& A, const uint8_t* r, const float* sc, int lane,
+template <int MODE, bool G, class OP>
+__device__ __forceinline__ void reduce_record(const SegArgs& A, const uint8_t* r, const typename OP::T* sc, int lane,
                                               uint64_t* empty) {
   const int type = *reinterpret_cast<const int32_t*>(r);
   if (MODE == 2) {  // diagnostics: record stream only
@@ -254,8 +273,8 @@ __device__ __forceinline__ void reduce_record(const SegArgs& A, const uint8_t* r
     if (type == 7) A.acc[lane] += 1.f;
     return;
   }
-  if (type == 1) reduce_long<MODE, G>(A, r, sc, lane, empty);
-  else reduce_short<MODE, G>(A, r, sc, lane, empty);
+  if (type == 1) reduce_long<MODE, G, OP>(A, r, sc, lane, empty);
+  else reduce_short<MODE, G, OP>(A, r, sc, lane, empty);
 }
 
 // Persistent CTA per SM over records [cta_c0[b], cta_c0[b+1]), unit by unit.
@@ -265,13 +284,14 @@ __device__ __forceinline__ void reduce_record(const SegArgs& A, const uint8_t* r
 // reduces record w of every stage. The unit's contrib segment is staged with
 // one more bulk copy.
 // MODE (GI_SEG_MODE diagnostics): 0 full, 1 no REDs, 2 record stream only.
-template <int MODE>
+template <int MODE, class OP>
 __global__ void __launch_bounds__(kSegThreads, 1) k_pr_seg(SegArgs A) {
+  using T = typename OP::T;
   extern __shared__ __align__(128) uint8_t smem[];  // [kStages][kStageBytes] ring | Z + 4 floats of segment
   __shared__ __align__(8) uint64_t full[kStages], empty[kStages], seg_bar;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   uint8_t* ring = smem;
-  float* scontrib = reinterpret_cast<float*>(smem + kStages * kStageBytes);
+  T* scontrib = reinterpret_cast<T*>(smem + kStages * kStageBytes);
   int c0 = A.cta_c0[blockIdx.x];
   const int c1 = A.cta_c0[blockIdx.x + 1];
   if (c0 >= c1) return;
@@ -307,7 +327,7 @@ __global__ void __launch_bounds__(kSegThreads, 1) k_pr_seg(SegArgs A) {
       if (tid == 0) {
         const int64_t base = (int64_t)seg * A.Z;
         const int64_t zlen = min((int64_t)A.Z, A.n - base);
-        scontrib[A.Z] = 0.f;
+        scontrib[A.Z] = OP::id();
         tma_load_1d(scontrib, A.cin + base, (uint32_t)(((zlen * 4) + 15) & ~15ll), &seg_bar);
       }
       staged_seg = seg;
@@ -345,9 +365,10 @@ __global__ void __launch_bounds__(kSegThreads, 1) k_pr_seg(SegArgs A) {
         const uint8_t* r = ring + s * kStageBytes + warp * kRecBytes;
         if (c < ue) {
           if (direct)
-            reduce_record<MODE, true>(A, r, A.cin + (int64_t)*reinterpret_cast<const int32_t*>(r + 12) * A.Z, lane,
-                                      &empty[s]);
-          else reduce_record<MODE, false>(A, r, scontrib, lane, &empty[s]);
+            reduce_record<MODE, true, OP>(
+                A, r, reinterpret_cast<const T*>(A.cin) + (int64_t)*reinterpret_cast<const int32_t*>(r + 12) * A.Z,
+                lane, &empty[s]);
+          else reduce_record<MODE, false, OP>(A, r, scontrib, lane, &empty[s]);
         }
         else if (lane == 0) {
           mbar_arrive(&empty[s]);  // nothing to take from this slot
@@ -1013,7 +1034,7 @@ gi_status seg_build(gi_graph g, int segment_size, int64_t block_rows) {
   int optin = 0;
   GI_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, g->ctx->device));
   cudaFuncAttributes a{};
-  GI_CUDA(cudaFuncGetAttributes(&a, k_pr_seg<0>));
+  GI_CUDA(cudaFuncGetAttributes(&a, k_pr_seg<0, OpSum>));
   int Z = (optin - (int)a.sharedSizeBytes - 64 - (int)seg_dyn_smem(0)) / 4;
   Z = std::min(Z, 65535) & ~31;
   if (Z < 1024) return fail(GI_ERR_UNSUPPORTED, "segmented pull: not enough shared memory");
@@ -1025,6 +1046,34 @@ gi_status seg_build(gi_graph g, int segment_size, int64_t block_rows) {
   if (g->ml == 0 || g->nr == 0) return fail(GI_ERR_UNSUPPORTED, "segmented pull: empty graph");
   if (g->off64) return seg_build_t<int64_t>(g, Z, DB);
   return seg_build_t<int32_t>(g, Z, DB);
+}
+
+// One min pass over the segmented layout (connected components, cc.cu):
+// acc[v] = min over v's in-edges (u, v) of labels[u]; acc must hold the
+// identity-or-larger (INT_MAX-ish) values for rows 0..n (row n: padding lanes).
+gi_status seg_min_pass(gi_graph g, const int32_t* labels, int32_t* acc) {
+  cudaStream_t st = g->ctx->stream;
+  SegArgs S;
+  S.rec = g->seg_rec.as<uint8_t>();
+  S.unit_c0 = g->seg_unit_c0.as<int32_t>();
+  S.cta_c0 = g->seg_cta.as<int32_t>();
+  S.cta_u = g->seg_cta.as<int32_t>() + g->seg_ctas + 1;
+  S.cin = reinterpret_cast<const float*>(labels);  // raw 4-byte words: the kernel reads them as int32
+  S.acc = reinterpret_cast<float*>(acc);
+  S.n = g->n;
+  S.Z = g->seg_Z;
+  S.S = g->seg_S;
+  S.U = g->seg_U;
+  S.timing = nullptr;
+  const size_t dyn = seg_dyn_smem(g->seg_Z);
+  static size_t attr_min[64] = {};
+  const int dev = g->ctx->device & 63;
+  if (attr_min[dev] < dyn) {
+    GI_CUDA(cudaFuncSetAttribute(k_pr_seg<0, OpMin>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+    attr_min[dev] = dyn;
+  }
+  GI_TRY(launch_pdl(k_pr_seg<0, OpMin>, g->seg_ctas, kSegThreads, dyn, st, S));
+  return GI_OK;
 }
 
 gi_status seg_edge_pass(gi_graph g, const float* cin) {
@@ -1041,14 +1090,14 @@ gi_status seg_edge_pass(gi_graph g, const float* cin) {
   S.S = g->seg_S;
   S.U = g->seg_U;
   static const int mode = getenv("GI_SEG_MODE") ? atoi(getenv("GI_SEG_MODE")) : 0;
-  void (*kern)(SegArgs) = mode == 1 ? k_pr_seg<1> : mode == 2 ? k_pr_seg<2> : k_pr_seg<0>;
+  void (*kern)(SegArgs) = mode == 1 ? k_pr_seg<1, OpSum> : mode == 2 ? k_pr_seg<2, OpSum> : k_pr_seg<0, OpSum>;
   const size_t dyn = seg_dyn_smem(g->seg_Z);
   static size_t attr_set[64] = {};  // per device: largest dynamic smem size configured so far
   const int dev = g->ctx->device & 63;
   if (attr_set[dev] < dyn) {
-    GI_CUDA(cudaFuncSetAttribute(k_pr_seg<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
-    GI_CUDA(cudaFuncSetAttribute(k_pr_seg<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
-    GI_CUDA(cudaFuncSetAttribute(k_pr_seg<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+    GI_CUDA(cudaFuncSetAttribute(k_pr_seg<0, OpSum>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+    GI_CUDA(cudaFuncSetAttribute(k_pr_seg<1, OpSum>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+    GI_CUDA(cudaFuncSetAttribute(k_pr_seg<2, OpSum>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
     attr_set[dev] = dyn;
   }
   static const char* dbg = getenv("GI_DEBUG_SEG_TIMING");  // diagnostics: file to append per-CTA timings to
