@@ -235,14 +235,22 @@ def run_ours(args):
     import torch
 
     rank, world, local = dist_env()
+    # diagnostics: GI_BENCH_DEVICE pins every rank to one GPU and GI_BENCH_DIST_BACKEND=gloo runs the
+    # host-side collectives on CPU tensors, so the replicas path can be exercised functionally on one GPU
+    gpu = int(os.environ.get("GI_BENCH_DEVICE", local))
+    backend = os.environ.get("GI_BENCH_DIST_BACKEND", "nccl")
     if world > 1:
         import torch.distributed as dist
 
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        torch.cuda.set_device(gpu)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", gpu))
+        else:
+            dist.init_process_group(backend)
     else:
         torch.cuda.set_device(0)
     dev = torch.cuda.current_device()
+    cdev = dev if backend == "nccl" else "cpu"  # where the timing reductions live
     from paper_1805_00923_b200 import gi
 
     stream = torch.cuda.Stream()
@@ -319,7 +327,7 @@ def run_ours(args):
     clocks = sampler.stop()
     ms = e0.elapsed_time(e1)
     if world > 1:
-        tt = torch.tensor([ms, tot_pr + tot_bfs], dtype=torch.float64, device=dev)
+        tt = torch.tensor([ms, tot_pr + tot_bfs], dtype=torch.float64, device=cdev)
         mx = tt.clone()
         torch.distributed.all_reduce(mx[:1], op=torch.distributed.ReduceOp.MAX)
         torch.distributed.all_reduce(tt[1:], op=torch.distributed.ReduceOp.SUM)
@@ -409,11 +417,11 @@ def run_ours(args):
         e2e_s = time.perf_counter() - t
         e_all = float(e_edges)
         if world > 1:
-            te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+            te = torch.tensor([e2e_s], dtype=torch.float64, device=cdev)
             torch.distributed.all_reduce(te, op=torch.distributed.ReduceOp.MAX)
             e2e_s = float(te[0])
             if not partition:  # replicas: every rank's own edges (its own sources)
-                ta = torch.tensor([e_all], dtype=torch.float64, device=dev)
+                ta = torch.tensor([e_all], dtype=torch.float64, device=cdev)
                 torch.distributed.all_reduce(ta, op=torch.distributed.ReduceOp.SUM)
                 e_all = float(ta[0])
         e2e = {"value": e_all / e2e_s / 1e9, "unit": "GTEPS",
