@@ -152,23 +152,29 @@ __device__ __forceinline__ void par8_put(uint8_t* row, unsigned long long m, uin
   }
 }
 
-// CTA-aggregated append of the active vertices (one atomic per CTA round)
-__device__ __forceinline__ void ms_append(const MsArgs& A, bool act, int32_t v, int* s_cnt, long long* s_base) {
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const unsigned mask = __ballot_sync(0xffffffffu, act);
-  if (lane == 0) s_cnt[w] = __popc(mask);
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int tot = 0;
-    for (int i = 0; i < kMsT / 32; ++i) {
-      const int c = s_cnt[i];
-      s_cnt[i] = tot;
-      tot += c;
-    }
-    *s_base = tot ? (long long)atomicAdd(&A.cnt[0], (unsigned long long)tot) : 0;
+// warp-level append through a shared-memory buffer: one tail atomic per 32
+// appended rows, no block barrier (the rows of a CTA round finish unevenly)
+__device__ __forceinline__ void ms_warp_flush(const MsArgs& A, int32_t* buf, int cnt) {
+  const int lane = threadIdx.x & 31;
+  __syncwarp();
+  unsigned long long pos = 0;
+  if (lane == 0) pos = atomicAdd(&A.cnt[0], (unsigned long long)cnt);
+  pos = __shfl_sync(0xffffffffu, pos, 0);
+  if (lane < cnt) A.anext[pos + lane] = buf[lane];
+  __syncwarp();
+}
+__device__ __forceinline__ void ms_warp_append(const MsArgs& A, bool act, int32_t v, int32_t* buf, int& nbuf) {
+  const int lane = threadIdx.x & 31;
+  const unsigned am = __ballot_sync(0xffffffffu, act);
+  if (!am) return;
+  if (act) buf[nbuf + __popc(am & ((1u << lane) - 1u))] = v;
+  nbuf += __popc(am);
+  if (nbuf >= 32) {
+    ms_warp_flush(A, buf, 32);
+    nbuf -= 32;
+    if (lane < nbuf) buf[lane] = buf[32 + lane];
+    __syncwarp();
   }
-  __syncthreads();
-  if (act) A.anext[*s_base + s_cnt[w] + __popc(mask & ((1u << lane) - 1u))] = v;
 }
 
 // the level's counters (cnt[1..3]), reduced over the CTA once at kernel end;
@@ -202,8 +208,9 @@ __device__ __forceinline__ void ms_counters(const MsArgs& A, long long deg, unsi
 
 template <typename OffT>
 __global__ void __launch_bounds__(kMsT) k_ms_pull(MsArgs A) {
-  __shared__ int s_cnt[kMsT / 32];
-  __shared__ long long s_base;
+  __shared__ int32_t s_buf[kMsT / 32][64];  // per-warp staging of the rows joining the next frontier
+  int32_t* wbuf = s_buf[threadIdx.x >> 5];
+  int nbuf = 0;
   const OffT* __restrict__ off = static_cast<const OffT*>(A.csc_off);
   long long tdeg = 0, exam = 0;
   unsigned long long tbits = 0;
@@ -243,8 +250,9 @@ __global__ void __launch_bounds__(kMsT) k_ms_pull(MsArgs A) {
       }
       A.fnext[w] = found;  // heavy rows: 0 here, k_ms_pull_heavy ORs into it
     }
-    ms_append(A, act, w, s_cnt, &s_base);
+    ms_warp_append(A, act, w, wbuf, nbuf);
   }
+  if (nbuf > 0) ms_warp_flush(A, wbuf, nbuf);
   ms_counters(A, tdeg, tbits, exam);
 }
 
