@@ -1,4 +1,5 @@
-// cc.cu — connected components by label propagation.
+// cc.cu — connected components by label propagation and SSSP by frontier
+// Bellman-Ford: one min-propagation engine.
 //
 // The paper's CC (P:3440-3472 [punt]; "synchronous label
 // propagation" P:2237): IDs[v] = v, frontier = every vertex, then rounds of
@@ -11,10 +12,14 @@
 // result does not depend on the internal relabelling.
 //
 // Per round, direction by the BFS rule (R7): pull iff |F| + sum outdeg F > m/20.
-//   pull (DensePull): every row takes the min label of its in-neighbours in F
-//     (frontier bitmap); light rows (in-degree < 32) a thread each, heavy rows in
-//     chunks of <= 1024 in-edges a warp each (chunks of one row race through
-//     atomicMin; the one whose atomicMin lowered the label marks the row);
+//   pull (DensePull), CC on a graph with the segmented layout: one pass of the
+//     PageRank edge kernel with an int32-min reduction (seg_min_pass) over every
+//     in-neighbour's label, then k_cc_apply lowers the labels and builds the
+//     next frontier; otherwise (and for SSSP) every row takes the min over its
+//     in-neighbours in F (frontier bitmap): light rows (in-degree < 32) a thread
+//     each, heavy rows in chunks of <= 1024 in-edges a warp each (chunks of one
+//     row race through atomicMin; the one whose atomicMin lowered the label
+//     marks the row);
 //   push (SparsePush): the frontier's out-edges, concatenated by an inclusive
 //     prefix of their out-degrees and walked 32 at a time, a lane per edge:
 //     atomicMin on the destination's label; a lowered label sets the row's bit
