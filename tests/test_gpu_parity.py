@@ -663,3 +663,23 @@ def test_sssp_device_output_and_errors(gi, ctx):
     with pytest.raises(gi.GiError) as e:
         g.sssp(n)
     assert e.value.status == gi.GI_ERR_VERTEX_OUT_OF_RANGE
+
+
+def test_cc_pr_share_the_segmented_layout(gi, ctx):
+    """CC's min passes and PageRank's sum passes run on the same segmented layout
+    (whichever call builds it first) and on separate accumulators: interleaved
+    calls on one graph keep both exact."""
+    s, d = graphgen.rmat(17, 16, 0.57, 0.19, 0.19, 8)
+    n = 1 << 17
+    g = gi.Graph(ctx, n, s, d, gi.GI_DEFAULT_FLAGS | gi.GI_SYMMETRIZE)
+    go = oracle.build_graph(n, s, d, symmetrize=True)
+    want_cc = oracle.cc_labels(go)
+    want_pr = oracle.pagerank(go, 20, 0.85)
+    for step in range(2):
+        lab, _ = g.cc()  # step 0: builds the layout
+        assert (lab == want_cc).all(), step
+        pr, _ = g.pagerank(20, 0.85)
+        pr = np.asarray(pr, np.float64)
+        assert np.abs(pr - want_pr).sum() <= 1e-5 and (np.abs(pr - want_pr) / want_pr).max() <= 1e-4, step
+        par, _ = g.bfs_multi(graphgen.pick_sources(n, s, d, 8, step).tolist())  # AUTO: bit-parallel
+        assert par.shape == (8, n)
