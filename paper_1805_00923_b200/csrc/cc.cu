@@ -202,11 +202,6 @@ __global__ void __launch_bounds__(kCT) k_cc_pull_heavy(CcArgs A, const int2* __r
   cc_counters(A, deg, exam);
 }
 
-__global__ void k_cc_degs(const int32_t* __restrict__ q, int64_t nf, const int32_t* __restrict__ outdeg,
-                          long long* __restrict__ dd) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nf; i += (int64_t)gridDim.x * blockDim.x)
-    dd[i] = __ldg(&outdeg[__ldg(&q[i])]);
-}
 
 // push: the frontier's out-edges (dp = inclusive prefix of their out-degrees)
 // split evenly over the warps, 32 per step; a lane finds its edge's vertex in
@@ -461,13 +456,13 @@ gi_status cc_t(gi_graph g, const gi_cc_opts& o, int32_t source, uint64_t seed, i
       }
       ++pulls;
     } else {
-      long long* dd = M.chunks[0].as<long long>();
       long long* dp = M.chunks[1].as<long long>();
-      k_cc_degs<<<grid_for(nf, kCT, sms, 8), kCT, 0, st>>>(A.qcur, nf, A.outdeg, dd);
       size_t tb = M.scan_bytes;
-      GI_CUDA(cub::DeviceScan::InclusiveSum(M.scan_tmp.p, tb, dd, dp, (int)nf, st));
+      GI_CUDA(cub::DeviceScan::InclusiveSum(
+          M.scan_tmp.p, tb, cub::TransformInputIterator<long long, OutdegOf, const int32_t*>(A.qcur, OutdegOf{A.outdeg}),
+          dp, (int)nf, st));
       k_cc_push<OffT, W><<<grid_for((sdeg + 255) / 256 * 32, kCT, sms, 8), kCT, 0, st>>>(A, dp);
-      launches += 3;
+      launches += 3;  // scan (2) + push
     }
     GI_CUDA(cudaGetLastError());
     GI_CUDA(cudaMemcpyAsync(h, cnt, 3 * 8, cudaMemcpyDeviceToHost, st));

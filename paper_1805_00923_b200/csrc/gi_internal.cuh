@@ -231,6 +231,12 @@ gi_status seg_edge_pass(gi_graph g, const float* cin);
 gi_status seg_min_pass(gi_graph g, const int32_t* labels, int32_t* acc);
 // bit-parallel BFS / CC shared state (g->ms): masks, active lists, heavy-row chunks
 gi_status ms_prepare(gi_graph g);
+// out-degree of an active vertex, as a scan input (the push levels' degree prefix
+// is one cub scan over the active list through this functor: no separate pass)
+struct OutdegOf {
+  const int32_t* outdeg;
+  __host__ __device__ __forceinline__ long long operator()(int32_t v) const { return (long long)outdeg[v]; }
+};
 gi_status cc_run(gi_graph g, const gi_cc_opts& o, int32_t* d_out, gi_cc_stats* stats);  // cc.cu
 gi_status sssp_run(gi_graph g, int32_t source, uint64_t seed, const gi_cc_opts& o, int32_t* d_out,
                    gi_cc_stats* stats);  // cc.cu

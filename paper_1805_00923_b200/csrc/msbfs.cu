@@ -418,12 +418,6 @@ __global__ void k_ms_heavy_list(const OffT* __restrict__ off, int64_t n, int32_t
     if ((int64_t)off[v + 1] - (int64_t)off[v] >= kHeavy) list[atomicAdd(cnt, 1ull)] = (int32_t)v;
 }
 
-// out-degrees of the active vertices (their inclusive prefix drives the push)
-__global__ void k_ms_degs(const int32_t* __restrict__ act, int64_t nact, const int32_t* __restrict__ outdeg,
-                          long long* __restrict__ dd) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nact; i += (int64_t)gridDim.x * blockDim.x)
-    dd[i] = __ldg(&outdeg[__ldg(&act[i])]);
-}
 
 // push, edge-parallel: the active vertices' out-edges, concatenated (dp =
 // inclusive prefix of their out-degrees), are split evenly over the warps and
@@ -674,7 +668,12 @@ static gi_status ms_prepare_t(gi_graph g) {
     GI_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tb, M.chunks[0].as<int32_t>(), M.chunks[1].as<int32_t>(), (int)n, st));
     GI_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tb64, M.chunks[0].as<long long>(), M.chunks[1].as<long long>(),
                                           (int)n, st));
-    tb = std::max(tb, tb64);
+    size_t tbt = 0;  // the degree-prefix scan reads the active list through OutdegOf
+    GI_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tbt,
+                                          cub::TransformInputIterator<long long, OutdegOf, const int32_t*>(
+                                              M.act[0].as<int32_t>(), OutdegOf{g->outdeg.as<int32_t>()}),
+                                          M.chunks[1].as<long long>(), (int)n, st));
+    tb = std::max(std::max(tb, tb64), tbt);
     GI_TRY(M.scan_tmp.alloc(tb + 16));
     M.scan_bytes = tb;
     GI_CUDA(cudaMemsetAsync(M.cnt.p, 0, 8, st));
@@ -804,11 +803,12 @@ gi_status msbfs_t(gi_graph g, int32_t k, const int32_t* sources, const gi_bfs_op
       ++pulls;
     } else {
       GI_CUDA(cudaMemsetAsync(A.fnext, 0, n * 8, st));
-      long long* dd = M.chunks[0].as<long long>();
       long long* dp = M.chunks[1].as<long long>();
-      k_ms_degs<<<grid_for(nact, kMsT, sms, 8), kMsT, 0, st>>>(A.acur, nact, A.outdeg, dd);
+
       size_t tb = M.scan_bytes;
-      GI_CUDA(cub::DeviceScan::InclusiveSum(M.scan_tmp.p, tb, dd, dp, (int)nact, st));
+      GI_CUDA(cub::DeviceScan::InclusiveSum(
+          M.scan_tmp.p, tb, cub::TransformInputIterator<long long, OutdegOf, const int32_t*>(A.acur, OutdegOf{A.outdeg}),
+          dp, (int)nact, st));
       launches += 2;
       k_ms_push<OffT><<<grid_for((sdeg + kPushChunk - 1) / kPushChunk * 32, kMsT, sms, 8), kMsT, 0, st>>>(A, dp);
     }
