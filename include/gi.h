@@ -148,20 +148,25 @@ GI_API gi_status gi_graph_csr(gi_graph g, int64_t* off, int32_t* idx);
  * n = 0 -> GI_OK, nothing written. */
 GI_API gi_status gi_pagerank(gi_graph g, int32_t iters, double damping, float* out);
 
-enum { GI_PR_PULL = 0, GI_PR_PUSH = 1, GI_PR_PULL_DIRECT = 2, GI_PR_PULL_SEGMENTED = 3 };
+enum { GI_PR_PULL = 0, GI_PR_PUSH = 1, GI_PR_PULL_DIRECT = 2, GI_PR_PULL_SEGMENTED = 3, GI_PR_PULL_PARTITIONED = 4 };
 enum { GI_DANGLING_UNIFORM = 0, GI_DANGLING_DROP = 1 };
 typedef struct {
   int32_t direction; /* GI_PR_PULL (auto-selected pull kernel), GI_PR_PUSH
                         (DensePush with atomics, the parity form),
                         GI_PR_PULL_DIRECT (CSC gather via L1/L2),
-                        GI_PR_PULL_SEGMENTED (shared-memory source segments) */
+                        GI_PR_PULL_SEGMENTED (shared-memory source segments),
+                        GI_PR_PULL_PARTITIONED (the CSC split by source
+                        range into L2-sized partitions, one gather pass per
+                        partition: the paper's cache partitioning) */
   int32_t dangling;  /* GI_DANGLING_UNIFORM (default) or GI_DANGLING_DROP
                         (paper-literal: no D term) */
   int32_t profile;   /* 1: fill gi_pr_stats kernel timings (CUDA events on the
                         context stream around every edge-pass launch) */
   int32_t segment_size; /* GI_PR_PULL_SEGMENTED: sources per shared-memory
                         segment; 0 = as many as fit in one CTA's shared memory
-                        (smaller values exercise many segments in tests) */
+                        (smaller values exercise many segments in tests).
+                        GI_PR_PULL_PARTITIONED: sources per partition, rounded
+                        up to a power of two; 0 = sized to the L2 cache */
   int32_t dst_block;    /* GI_PR_PULL_SEGMENTED: destination rows per block
                         (the per-row accumulator of one block stays in L2);
                         0 = automatic */

@@ -611,4 +611,17 @@ gi_status build_graph_dist(gi_context ctx, int64_t n, int64_t m0, const int32_t*
   return GI_OK;
 }
 
+gi_status tile_rows_launch(const void* off, bool off64, int64_t n, int64_t m, int64_t ntiles, int32_t* rows,
+                           cudaStream_t st, int sms) {
+  if (ntiles <= 0) return GI_OK;
+  if (off64)
+    k_tile_rows<int64_t><<<grid_for(2 * ntiles, 256, sms), 256, 0, st>>>(static_cast<const int64_t*>(off), n, m, ntiles,
+                                                                        kPullTile, rows);
+  else
+    k_tile_rows<int32_t><<<grid_for(2 * ntiles, 256, sms), 256, 0, st>>>(static_cast<const int32_t*>(off), n, m, ntiles,
+                                                                        kPullTile, rows);
+  GI_CUDA(cudaGetLastError());
+  return GI_OK;
+}
+
 }  // namespace gi

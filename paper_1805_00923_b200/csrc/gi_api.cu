@@ -386,7 +386,7 @@ gi_status gi_pagerank_ex(gi_graph g, int32_t iters, double damping, const gi_pr_
   if (!(damping >= 0.0 && damping <= 1.0)) return fail(GI_ERR_INVALID_ARGUMENT, "gi_pagerank: damping not in [0,1]");
   gi_pr_opts o{};
   if (opts) o = *opts;
-  if (o.direction < GI_PR_PULL || o.direction > GI_PR_PULL_SEGMENTED)
+  if (o.direction < GI_PR_PULL || o.direction > GI_PR_PULL_PARTITIONED)
     return fail(GI_ERR_INVALID_ARGUMENT, "gi_pagerank: bad direction");
   if (o.dangling != GI_DANGLING_UNIFORM && o.dangling != GI_DANGLING_DROP)
     return fail(GI_ERR_INVALID_ARGUMENT, "gi_pagerank: bad dangling rule");

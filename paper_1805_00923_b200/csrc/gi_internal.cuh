@@ -175,6 +175,15 @@ struct gi_graph_s {
   gi::DevBuf seg_acc;      // float[2][seg_acc_stride]: per-row sums (ping-pong), L2-resident
   int64_t seg_acc_stride = 0;
   int seg_acc_cur = 0;     // buffer the next edge pass reduces into (all zero)
+  // source-partitioned pull (pagerank.cu; the paper's cache partitioning):
+  // the CSC's edges grouped by source range [p << sp_shift, (p+1) << sp_shift),
+  // each group a CSC of its own (offsets sp_off + p * (nr+1), edges sp_idx +
+  // sp_base[p], merge-path tiles sp_tiles + 2 * sp_tile0[p]); sp_P == 0 until built
+  int sp_P = 0, sp_shift = 0;
+  bool sp_off64 = false;
+  std::vector<int64_t> sp_m, sp_base, sp_ntiles, sp_tile0;
+  gi::DevBuf sp_idx, sp_off, sp_tiles, sp_acc;
+  int pr_auto = -1;       // auto-selected pull kernel, decided on first use
   gi::DevBuf out_stage;   // float/int32[n]: output staging in input ids
   // BFS workspace
   gi::DevBuf parent;      // int32[n], internal ids
@@ -225,6 +234,9 @@ gi_status pagerank_run(gi_graph g, int32_t iters, double damping, const gi_pr_op
 struct PrArgs;
 // segment_size / block_rows: 0 = automatic (tests pass small values)
 gi_status seg_build(gi_graph g, int segment_size, int64_t block_rows);
+// merge-path tile rows of a CSC (build.cu); rows: int32[2 * ntiles]
+gi_status tile_rows_launch(const void* off, bool off64, int64_t n, int64_t m, int64_t ntiles, int32_t* rows,
+                           cudaStream_t st, int sms);
 // seg_acc_buf(g, cur)[v] = sum of cin over v's in-edges (the buffer is zero before the pass)
 gi_status seg_edge_pass(gi_graph g, const float* cin);
 // a min pass over the segmented layout: acc[v] = min(acc[v], labels[u] over in-edges (u, v)) (CC, cc.cu)

@@ -17,6 +17,10 @@
 #include "pr_common.cuh"
 #include "comm.cuh"
 
+#include <algorithm>
+#include <climits>
+#include <cub/device/device_scan.cuh>
+
 namespace gi {
 namespace {
 
@@ -27,6 +31,16 @@ namespace {
 // of P:598-599, through L1/L2); phase B is the merge-path walk with the fused
 // vertex update; rows that cross tiles add a double partial and an arrival
 // count, and the last arriving tile finishes them (pieces = tiles touched).
+// Row r's sum s over this pass's edges: the whole in-row (pmode 0), or the
+// part from one source partition (cache partitioning):
+// partial sums merge in pacc and the last partition's pass finishes the row.
+__device__ __forceinline__ void pr_part_finish(const PrArgs& A, int64_t r, float s, float dn, double& dpart) {
+  if (A.pmode == 0) pr_epilogue(A, r, s, dn, dpart);
+  else if (A.pmode == 1) A.pacc[r] = s;
+  else if (A.pmode == 2) A.pacc[r] += s;
+  else pr_epilogue(A, r, A.pacc[r] + s, dn, dpart);
+}
+
 template <typename OffT>
 __global__ void __launch_bounds__(kPullThreads) k_pr_pull(PrArgs A) {
   constexpr int NT = kPullThreads, IPT = kPullItemsPerThread, T = kPullTile;
@@ -64,7 +78,7 @@ __global__ void __launch_bounds__(kPullThreads) k_pr_pull(PrArgs A) {
 
   double dpart = 0.0;
   tile_walk<NT, IPT>(
-      loff, R, items, sval, scratch, [&](int i, float v) { pr_epilogue(A, r0 + i, v, dn, dpart); },
+      loff, R, items, sval, scratch, [&](int i, float v) { pr_part_finish(A, r0 + i, v, dn, dpart); },
       [&](int i, float v) {
         const int64_t r = r0 + i;
         const int64_t sp = r + (int64_t)off[r], ep = r + (int64_t)off[r + 1];
@@ -75,7 +89,7 @@ __global__ void __launch_bounds__(kPullThreads) k_pr_pull(PrArgs A) {
         if (prev == pieces - 1) {
           __threadfence();
           const double tot = atomicAdd(&A.split_acc[r], 0.0);
-          pr_epilogue(A, r, (float)tot, dn, dpart);
+          pr_part_finish(A, r, (float)tot, dn, dpart);
           A.split_acc[r] = 0.0;
           A.split_cnt[r] = 0;
         }
@@ -209,7 +223,147 @@ __global__ void k_fill(float* __restrict__ out, int64_t n, float v) {
     out[i] = v;
 }
 
+// ---------------------------------------------------------------- source-partitioned CSC (cache partitioning)
+// "incoming edges (src, dst) are assigned to SSG_i if src
+// in V_i, and sorted by dst"; V_i = [i << shift, (i+1) << shift). A warp per
+// CSC row counts its edges per partition (k_sp_count), then places them
+// (k_sp_fill) keeping their order inside the row: lanes of one step holding
+// the same partition take consecutive slots by rank (__match_any_sync).
+constexpr int kSpMax = 32;  // partitions at most (one histogram bin per lane)
+
+template <typename OffT>
+__global__ void __launch_bounds__(256) k_sp_count(const OffT* __restrict__ off, const int32_t* __restrict__ idx,
+                                                  int64_t nr, int shift, int P, int64_t* __restrict__ cnt) {
+  __shared__ int hist[8][kSpMax];
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+  for (int64_t w = blockIdx.x * 8ll + wp; w < nr; w += gridDim.x * 8ll) {
+    hist[wp][lane] = 0;
+    __syncwarp();
+    for (int64_t e = (int64_t)off[w] + lane; e < (int64_t)off[w + 1]; e += 32) atomicAdd(&hist[wp][idx[e] >> shift], 1);
+    __syncwarp();
+    if (lane < P) cnt[lane * (nr + 1) + w] = hist[wp][lane];
+    __syncwarp();
+  }
+}
+
+template <typename OffT>
+__global__ void __launch_bounds__(256) k_sp_fill(const OffT* __restrict__ off, const int32_t* __restrict__ idx,
+                                                 int64_t nr, int shift, const int64_t* __restrict__ poff,
+                                                 const int64_t* __restrict__ base, int32_t* __restrict__ out) {
+  __shared__ int cur[8][kSpMax + 1];
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+  for (int64_t w = blockIdx.x * 8ll + wp; w < nr; w += gridDim.x * 8ll) {
+    cur[wp][lane] = 0;
+    __syncwarp();
+    const int64_t e0 = (int64_t)off[w], e1 = (int64_t)off[w + 1];
+    for (int64_t b = e0; b < e1; b += 32) {
+      const int64_t e = b + lane;
+      const int32_t v = e < e1 ? idx[e] : -1;
+      const int p = v >= 0 ? v >> shift : kSpMax;
+      const unsigned peers = __match_any_sync(0xffffffffu, p);
+      const int rank = __popc(peers & ((1u << lane) - 1u));
+      const int c = cur[wp][p];
+      if (v >= 0) out[base[p] + poff[p * (nr + 1) + w] + c + rank] = v;
+      __syncwarp();
+      if (rank == 0) cur[wp][p] = c + __popc(peers);
+      __syncwarp();
+    }
+  }
+}
+
+__global__ void k_narrow_off(const int64_t* __restrict__ in, int64_t n, int32_t* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (int32_t)in[i];
+}
+
 }  // namespace
+
+// Builds the source-partitioned CSC once per graph (single GPU).
+static gi_status sp_build(gi_graph g, int sources_per_part) {
+  gi_context ctx = g->ctx;
+  cudaStream_t st = ctx->stream;
+  const int sms = ctx->num_sms;
+  const int64_t n = g->n, nr = g->nr, m = g->ml;
+  int64_t z = sources_per_part;
+  if (z <= 0) {  // a partition's contrib slice: ~3/8 of L2 (the record stream and the row sums share it)
+    int l2 = 0;
+    GI_CUDA(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, ctx->device));
+    z = std::max<int64_t>((int64_t)l2 * 3 / 8 / 4, 1024);
+  }
+  int shift = 0;
+  if (sources_per_part > 0)
+    while ((1ll << shift) < z) ++shift;  // round up
+  else
+    while ((2ll << shift) <= z) ++shift;  // round down
+  while (((n + (1ll << shift) - 1) >> shift) > kSpMax) ++shift;
+  const int P = (int)std::max<int64_t>(1, (n + (1ll << shift) - 1) >> shift);
+  if (g->sp_P == P && g->sp_shift == shift) return GI_OK;
+  g->sp_P = 0;
+  const int64_t stride = nr + 1;
+  DevBuf cnt, poff, dbase, tmp;
+  GI_TRY(cnt.alloc((size_t)P * stride * sizeof(int64_t)));
+  GI_TRY(poff.alloc((size_t)P * stride * sizeof(int64_t)));
+  GI_CUDA(cudaMemsetAsync(cnt.p, 0, (size_t)P * stride * sizeof(int64_t), st));
+  const int grid = grid_for(ceil_div(nr, 8), 256, sms, 8);
+  if (nr > 0) {
+    if (g->off64) k_sp_count<int64_t><<<grid, 256, 0, st>>>(g->csc_off.as<int64_t>(), g->csc_idx.as<int32_t>(), nr, shift, P, cnt.as<int64_t>());
+    else k_sp_count<int32_t><<<grid, 256, 0, st>>>(g->csc_off.as<int32_t>(), g->csc_idx.as<int32_t>(), nr, shift, P, cnt.as<int64_t>());
+    GI_CUDA(cudaGetLastError());
+  }
+  size_t tb = 0;
+  GI_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt.as<int64_t>(), poff.as<int64_t>(), stride, st));
+  GI_TRY(tmp.alloc(tb));
+  for (int p = 0; p < P; ++p)
+    GI_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb, cnt.as<int64_t>() + p * stride, poff.as<int64_t>() + p * stride,
+                                          stride, st));
+  std::vector<int64_t> mp(P);
+  for (int p = 0; p < P; ++p)
+    GI_CUDA(cudaMemcpyAsync(&mp[p], poff.as<int64_t>() + p * stride + nr, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  GI_CUDA(cudaStreamSynchronize(st));
+  g->sp_m = mp;
+  g->sp_base.assign(P + 1, 0);
+  g->sp_ntiles.assign(P, 0);
+  g->sp_tile0.assign(P + 1, 0);
+  bool wide = false;
+  for (int p = 0; p < P; ++p) {
+    g->sp_base[p + 1] = g->sp_base[p] + mp[p];
+    wide = wide || mp[p] > INT32_MAX - 1;
+    g->sp_ntiles[p] = nr > 0 ? ceil_div(nr + mp[p], kPullTile) : 0;
+    g->sp_tile0[p + 1] = g->sp_tile0[p] + g->sp_ntiles[p];
+  }
+  if (g->sp_base[P] != m) return fail(GI_ERR_INTERNAL, "source partitions do not cover the CSC");
+  GI_TRY(dbase.alloc(P * sizeof(int64_t)));
+  GI_CUDA(cudaMemcpyAsync(dbase.p, g->sp_base.data(), P * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  GI_TRY(g->sp_idx.alloc(std::max<int64_t>(m, 1) * sizeof(int32_t)));
+  if (nr > 0) {
+    if (g->off64)
+      k_sp_fill<int64_t><<<grid, 256, 0, st>>>(g->csc_off.as<int64_t>(), g->csc_idx.as<int32_t>(), nr, shift,
+                                               poff.as<int64_t>(), dbase.as<int64_t>(), g->sp_idx.as<int32_t>());
+    else
+      k_sp_fill<int32_t><<<grid, 256, 0, st>>>(g->csc_off.as<int32_t>(), g->csc_idx.as<int32_t>(), nr, shift,
+                                               poff.as<int64_t>(), dbase.as<int64_t>(), g->sp_idx.as<int32_t>());
+    GI_CUDA(cudaGetLastError());
+  }
+  g->sp_off64 = wide;
+  if (wide) {
+    GI_TRY(g->sp_off.alloc((size_t)P * stride * sizeof(int64_t)));
+    GI_CUDA(cudaMemcpyAsync(g->sp_off.p, poff.p, (size_t)P * stride * sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
+  } else {
+    GI_TRY(g->sp_off.alloc((size_t)P * stride * sizeof(int32_t)));
+    k_narrow_off<<<grid_for(P * stride, 256, sms), 256, 0, st>>>(poff.as<int64_t>(), P * stride, g->sp_off.as<int32_t>());
+    GI_CUDA(cudaGetLastError());
+  }
+  GI_TRY(g->sp_tiles.alloc(2 * std::max<int64_t>(g->sp_tile0[P], 1) * sizeof(int32_t)));
+  const size_t osz = wide ? 8 : 4;
+  for (int p = 0; p < P; ++p)
+    GI_TRY(tile_rows_launch(static_cast<const char*>(g->sp_off.p) + (size_t)p * stride * osz, wide, nr, mp[p],
+                            g->sp_ntiles[p], g->sp_tiles.as<int32_t>() + 2 * g->sp_tile0[p], st, sms));
+  GI_TRY(g->sp_acc.alloc(std::max<int64_t>(nr, 1) * sizeof(float)));
+  GI_CUDA(cudaStreamSynchronize(st));
+  g->sp_P = P;
+  g->sp_shift = shift;
+  return GI_OK;
+}
 
 gi_status pagerank_run(gi_graph g, int32_t iters, double damping, const gi_pr_opts& o, float* d_out,
                        gi_pr_stats* stats) {
@@ -224,10 +378,21 @@ gi_status pagerank_run(gi_graph g, int32_t iters, double damping, const gi_pr_op
   // auto pull kernel: shared-memory segments for skewed (relabelled) graphs, whose
   // hubs concentrate the gathers; the direct L2 gather keeps the input order's
   // locality on flat-degree graphs (a grid's in-neighbours are +-1, +-width)
-  if (kernel == GI_PR_PULL)
+  // auto pull: segmented on relabelled graphs, else direct (decided once per graph).
+  // The source-partitioned pull (cache partitioning) is explicit only: on B200 a
+  // random 4-byte gather costs the same whether its sector hits L2 or HBM
+  // (DESIGN.md §5), so partitions sized to L2 measured no faster than the
+  // direct gather on configs 2, 4 and 5.
+  if (kernel == GI_PR_PULL && g->pr_auto >= 0 && !dist) kernel = g->pr_auto;
+  if (kernel == GI_PR_PULL) {
     kernel = (nr > 0 && ml > 0 && g->relabeled && seg_build(g, o.segment_size, o.dst_block) == GI_OK)
                  ? GI_PR_PULL_SEGMENTED : GI_PR_PULL_DIRECT;
-  else if (kernel == GI_PR_PULL_SEGMENTED) {
+    if (!dist) g->pr_auto = kernel;
+  }
+  if (kernel == GI_PR_PULL_PARTITIONED) {
+    if (dist || nr == 0 || ml == 0) kernel = GI_PR_PULL_DIRECT;
+    else GI_TRY(sp_build(g, o.segment_size));
+  } else if (kernel == GI_PR_PULL_SEGMENTED) {
     if (nr > 0 && ml > 0) GI_TRY(seg_build(g, o.segment_size, o.dst_block));
     else kernel = GI_PR_PULL_DIRECT;
   }
@@ -342,6 +507,26 @@ gi_status pagerank_run(gi_graph g, int32_t iters, double damping, const gi_pr_op
       if (o.profile) GI_CUDA(cudaEventRecord(ev[2], st));
       GI_TRY(seg_vertex_pass(g, A));
       S.aux_launches++;
+      if (o.profile) GI_CUDA(cudaEventRecord(ev[1], st));
+    } else if (kernel == GI_PR_PULL_PARTITIONED) {  // one merge-path pass per source partition
+      const int P = g->sp_P;
+      A.pacc = g->sp_acc.as<float>();
+      for (int p = 0; p < P; ++p) {
+        A.pmode = P == 1 ? 0 : p == 0 ? 1 : p == P - 1 ? 3 : 2;
+        A.m = g->sp_m[p];
+        A.idx = g->sp_idx.as<int32_t>() + g->sp_base[p];
+        A.tile_rows = g->sp_tiles.as<int32_t>() + 2 * g->sp_tile0[p];
+        if (g->sp_ntiles[p] == 0) continue;
+        if (g->sp_off64) {
+          A.off = g->sp_off.as<int64_t>() + p * (nr + 1);
+          k_pr_pull<int64_t><<<(unsigned)g->sp_ntiles[p], kPullThreads, 0, st>>>(A);
+        } else {
+          A.off = g->sp_off.as<int32_t>() + p * (nr + 1);
+          k_pr_pull<int32_t><<<(unsigned)g->sp_ntiles[p], kPullThreads, 0, st>>>(A);
+        }
+      }
+      A.pmode = 0;
+      A.m = ml;
       if (o.profile) GI_CUDA(cudaEventRecord(ev[1], st));
     } else {
       A.tile_rows = g->tile_rows.as<int32_t>();

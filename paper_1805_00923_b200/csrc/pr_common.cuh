@@ -32,6 +32,10 @@ struct PrArgs {
   int32_t* split_cnt;
   float* rank_out;  // non-null on the final iteration (input ids)
   const int32_t* __restrict__ perm;
+  // source-partitioned pull: pmode 0 = one pass (finish every row), 1 = first
+  // partition (pacc = s), 2 = middle (pacc += s), 3 = last (finish with pacc + s)
+  float* pacc;
+  int pmode;
 };
 
 // vertex update (a3): r' = base + d (s + D/n); contrib' = r'/outdeg; dangling partial

@@ -38,7 +38,7 @@ GI_SYMMETRIZE = 1 << 3
 GI_NO_RELABEL = 1 << 4
 GI_DEFAULT_FLAGS = GI_REMOVE_SELF_LOOPS | GI_DEDUP
 
-GI_PR_PULL, GI_PR_PUSH, GI_PR_PULL_DIRECT, GI_PR_PULL_SEGMENTED = 0, 1, 2, 3
+GI_PR_PULL, GI_PR_PUSH, GI_PR_PULL_DIRECT, GI_PR_PULL_SEGMENTED, GI_PR_PULL_PARTITIONED = 0, 1, 2, 3, 4
 GI_DANGLING_UNIFORM, GI_DANGLING_DROP = 0, 1
 GI_BFS_AUTO, GI_BFS_PUSH_ONLY, GI_BFS_PULL_ONLY = 0, 1, 2
 GI_PRD_AUTO, GI_PRD_PUSH_ONLY, GI_PRD_PULL_ONLY = 0, 1, 2

@@ -132,12 +132,12 @@ def test_build_device_edges_and_errors(gi, ctx):
 
 
 # ---------------------------------------------------------------- PageRank (a3-a5)
-PR_DIRS = ["pull", "push", "direct", "segmented"]
+PR_DIRS = ["pull", "push", "direct", "segmented", "partitioned"]
 
 
 def _dir(gi, name):
     return {"pull": gi.GI_PR_PULL, "push": gi.GI_PR_PUSH, "direct": gi.GI_PR_PULL_DIRECT,
-            "segmented": gi.GI_PR_PULL_SEGMENTED}[name]
+            "segmented": gi.GI_PR_PULL_SEGMENTED, "partitioned": gi.GI_PR_PULL_PARTITIONED}[name]
 
 
 @pytest.mark.parametrize("direction", PR_DIRS)
@@ -230,6 +230,26 @@ def test_pr_segmented_many_segments(gi, ctx, seg, dblk):
                                  dst_block=dblk)
             assert st.kernel == gi.GI_PR_PULL_SEGMENTED
             _pr_check(got, oracle.pagerank(go, 20, 0.85, dangling), f"seg={seg} dblk={dblk} n={n}")
+
+
+@pytest.mark.parametrize("z", [1, 1000, 4096, 30000, 0])
+def test_pr_partitioned_many_partitions(gi, ctx, z):
+    """Cache partitioning: the CSC split by source range
+    into 2^k-vertex partitions (up to 32), one merge-path pass per partition;
+    rows empty in a partition, hubs split across tiles, a single partition (z=0)."""
+    cases = [(graphgen.CONFIGS[1].n, *graphgen.CONFIGS[1].edges()),
+             (70001, *graphgen.random_digraph(70001, 1000003, 5)),
+             (100001, *graphgen.in_star(100000)),
+             (100001, *graphgen.star_bidirectional(100000)),
+             (5, np.zeros(0, np.int32), np.zeros(0, np.int32))]
+    for n, s, d in cases:
+        g = gi.Graph(ctx, n, s, d)
+        go = oracle.build_graph(n, s, d)
+        for dangling in (0, 1):
+            got, st = g.pagerank(20, 0.85, direction=gi.GI_PR_PULL_PARTITIONED, dangling=dangling, segment_size=z)
+            if go.m > 0:
+                assert st.kernel == gi.GI_PR_PULL_PARTITIONED
+            _pr_check(got, oracle.pagerank(go, 20, 0.85, dangling), f"z={z} n={n}")
 
 
 def test_pr_device_output_and_damping_edges(gi, ctx):
