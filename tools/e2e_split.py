@@ -22,16 +22,24 @@ hs, hd = torch.from_numpy(s).pin_memory(), torch.from_numpy(d).pin_memory()
 hpr = torch.empty(cfg.n, dtype=torch.float32).pin_memory()
 hbfs = torch.empty((len(srcs), cfg.n), dtype=torch.int32).pin_memory()
 for rep in range(int(os.environ.get("E2E_REPS", "3"))):
-    t = [time.perf_counter()]
+    # wall time and this process's CPU time (user + system) per phase: a stall
+    # with little CPU time is a wait (driver / DMA / scheduling), one with
+    # system time is the kernel working for us (page faults, pinning)
+    def now():
+        o = os.times()
+        return time.perf_counter(), o.user + o.system
+
+    t = [now()]
     g = gi.Graph(ctx, cfg.n, hs, hd, gi.GI_DEFAULT_FLAGS)
-    torch.cuda.synchronize(); t.append(time.perf_counter())
+    torch.cuda.synchronize(); t.append(now())
     g.pagerank(cfg.pr_iters, cfg.damping, out=hpr)
-    t.append(time.perf_counter())
+    t.append(now())
     g.pagerank(cfg.pr_iters, cfg.damping, out=hpr)
-    t.append(time.perf_counter())
+    t.append(now())
     g.bfs_multi(srcs, out=hbfs)
-    t.append(time.perf_counter())
+    t.append(now())
     g.close()
-    t.append(time.perf_counter())
-    ms = [(b - a) * 1e3 for a, b in zip(t, t[1:])]
-    print("create %.1f  pr#1 %.1f  pr#2 %.1f  bfs_multi(host) %.1f  close %.1f ms" % tuple(ms))
+    t.append(now())
+    ms = [((b[0] - a[0]) * 1e3, (b[1] - a[1]) * 1e3) for a, b in zip(t, t[1:])]
+    print("create %.1f/%.0f  pr#1 %.1f/%.0f  pr#2 %.1f/%.0f  bfs_multi(host) %.1f/%.0f  close %.1f/%.0f ms (wall/cpu)"
+          % tuple(x for p in ms for x in p), flush=True)
