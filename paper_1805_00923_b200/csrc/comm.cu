@@ -37,6 +37,46 @@ class NcclComm : public Comm {
   gi_status allreduce_f64(double* d, int64_t count, cudaStream_t st) override {
     return red(d, count, ncclFloat64, st);
   }
+  // CUDA IPC handles of every rank's buffer, exchanged with an allgather;
+  // failure anywhere (another node, pooled memory) -> all ranks fall back
+  gi_status peer_map(void* local, std::vector<void*>& peers, std::vector<void*>& opened, cudaStream_t st) override {
+    const int64_t hs = (int64_t)sizeof(cudaIpcMemHandle_t);
+    std::vector<cudaIpcMemHandle_t> h(nranks);
+    int32_t bad = cudaIpcGetMemHandle(&h[rank], local) != cudaSuccess;
+    cudaGetLastError();
+    DevBuf hb, flag;
+    GI_TRY(hb.alloc(nranks * hs));
+    GI_TRY(flag.alloc(sizeof(int32_t)));
+    GI_CUDA(cudaMemcpyAsync(hb.as<char>() + rank * hs, &h[rank], hs, cudaMemcpyHostToDevice, st));
+    std::vector<int64_t> off(nranks + 1);
+    for (int q = 0; q <= nranks; ++q) off[q] = q * hs;
+    GI_TRY(allgatherv(hb.p, off, st));
+    GI_CUDA(cudaMemcpyAsync(h.data(), hb.p, nranks * hs, cudaMemcpyDeviceToHost, st));
+    GI_CUDA(cudaStreamSynchronize(st));
+    peers.assign(nranks, nullptr);
+    peers[rank] = local;
+    for (int q = 0; q < nranks && !bad; ++q) {
+      if (q == rank) continue;
+      void* p = nullptr;
+      if (cudaIpcOpenMemHandle(&p, h[q], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+        cudaGetLastError();
+        bad = 1;
+        break;
+      }
+      peers[q] = p;
+      opened.push_back(p);
+    }
+    GI_CUDA(cudaMemcpyAsync(flag.p, &bad, sizeof(int32_t), cudaMemcpyHostToDevice, st));
+    GI_TRY(allreduce_i32(flag.as<int32_t>(), 1, st));
+    int32_t any = 0;
+    GI_CUDA(cudaMemcpyAsync(&any, flag.p, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    GI_CUDA(cudaStreamSynchronize(st));
+    if (any) {
+      peer_unmap(opened);
+      return fail(GI_ERR_CUDA, "peer_map: CUDA IPC mapping unavailable on some rank");
+    }
+    return GI_OK;
+  }
   gi_status allgatherv(void* buf, const std::vector<int64_t>& off, cudaStream_t st) override {
     const NcclApi* a = nccl_api();
     if (!a) return GI_ERR_NCCL;
@@ -83,6 +123,16 @@ class LocalComm : public Comm {
   gi_status allreduce_i32(int32_t* d, int64_t count, cudaStream_t st) override { return red<int32_t>(d, count, st); }
   gi_status allreduce_i64(int64_t* d, int64_t count, cudaStream_t st) override { return red<int64_t>(d, count, st); }
   gi_status allreduce_f64(double* d, int64_t count, cudaStream_t st) override { return red<double>(d, count, st); }
+  // in-process ranks: the buffers are directly addressable
+  gi_status peer_map(void* local, std::vector<void*>& peers, std::vector<void*>&, cudaStream_t st) override {
+    GI_CUDA(cudaStreamSynchronize(st));
+    g_->ptr[rank] = local;
+    g_->barrier();
+    peers.assign(nranks, nullptr);
+    for (int q = 0; q < nranks; ++q) peers[q] = const_cast<void*>(g_->ptr[q]);
+    g_->barrier();
+    return GI_OK;
+  }
   gi_status allgatherv(void* buf, const std::vector<int64_t>& off, cudaStream_t st) override {
     GI_CUDA(cudaStreamSynchronize(st));
     g_->ptr[rank] = buf;
@@ -142,5 +192,10 @@ Comm* make_nccl_comm(void* nccl_comm, int rank, int nranks) {
 }
 
 Comm* make_local_comm(LocalGroup* g, int rank) { return new LocalComm(g, rank); }
+
+void peer_unmap(std::vector<void*>& opened) {
+  for (void* p : opened) cudaIpcCloseMemHandle(p);
+  opened.clear();
+}
 
 }  // namespace gi

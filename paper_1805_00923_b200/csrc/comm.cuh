@@ -32,7 +32,14 @@ struct Comm {
   // recv + roff[p] (counts must agree pairwise)
   virtual gi_status alltoallv(const void* send, const std::vector<int64_t>& soff, void* recv,
                               const std::vector<int64_t>& roff, cudaStream_t st) = 0;
+  // Collective: every rank passes a buffer of the same size (cudaMalloc'd);
+  // on GI_OK peers[q] is rank q's buffer addressable from this device
+  // (peers[rank] = local) and `opened` lists mappings to release with
+  // peer_unmap. Any rank failing makes every rank return GI_ERR_CUDA.
+  virtual gi_status peer_map(void* local, std::vector<void*>& peers, std::vector<void*>& opened,
+                             cudaStream_t st) = 0;
 };
+void peer_unmap(std::vector<void*>& opened);
 
 // Shared state of an in-process group of simulated ranks.
 struct LocalGroup {

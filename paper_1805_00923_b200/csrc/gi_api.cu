@@ -228,6 +228,7 @@ gi_status gi_graph_destroy(gi_graph g) {
   cudaSetDevice(g->ctx->device);
   cudaStreamSynchronize(g->ctx->stream);
   g->ctx->live_graphs--;
+  peer_unmap(g->peer_opened);
   delete g;  // pooled buffers go back to the pool (stream-ordered frees)
   return GI_OK;
 }

@@ -81,12 +81,13 @@ struct DevBuf {
     bytes = 0;
     pooled = false;
   }
-  gi_status alloc(size_t nbytes) {
+  // plain = true: always cudaMalloc (memory that is exported to peers by CUDA IPC)
+  gi_status alloc(size_t nbytes, bool plain = false) {
     reset();
     if (nbytes == 0) nbytes = 16;
     const cudaStream_t st = tl_alloc_stream();
     cudaError_t e;
-    if (st && pool_enabled() && nbytes <= kPoolMaxBlock) {
+    if (!plain && st && pool_enabled() && nbytes <= kPoolMaxBlock) {
       e = cudaMallocAsync(&p, nbytes, st);
       pooled = e == cudaSuccess;
       s = st;
@@ -184,6 +185,11 @@ struct gi_graph_s {
   std::vector<int64_t> sp_m, sp_base, sp_ntiles, sp_tile0;
   gi::DevBuf sp_idx, sp_off, sp_tiles, sp_acc;
   int pr_auto = -1;       // auto-selected pull kernel, decided on first use
+  // multi-GPU PageRank with peer stores: every rank's
+  // contrib[k] replica as seen from this rank (index = rank; own entry = local)
+  int peer_state = 0;                 // 0 unknown, 1 mapped, -1 unavailable (allgather path)
+  std::vector<void*> peer_c[2];
+  std::vector<void*> peer_opened;     // CUDA IPC mappings to close on destroy
   gi::DevBuf out_stage;   // float/int32[n]: output staging in input ids
   // BFS workspace
   gi::DevBuf parent;      // int32[n], internal ids

@@ -19,6 +19,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <cstring>
 #include <cub/device/device_scan.cuh>
 
 namespace gi {
@@ -436,7 +437,7 @@ gi_status pagerank_run(gi_graph g, int32_t iters, double damping, const gi_pr_op
   }
   // workspace (lazily allocated, reused across calls)
   for (int k = 0; k < 2; ++k)
-    if (!g->contrib[k].p) GI_TRY(g->contrib[k].alloc((n + 16) * sizeof(float)));
+    if (!g->contrib[k].p) GI_TRY(g->contrib[k].alloc((n + 16) * sizeof(float), /*plain=*/dist));
   if (!g->dbuf.p) GI_TRY(g->dbuf.alloc(4 * sizeof(double)));
   if (kernel == GI_PR_PUSH) {
     if (!g->push_sum.p) {
@@ -459,6 +460,20 @@ gi_status pagerank_run(gi_graph g, int32_t iters, double damping, const gi_pr_op
     GI_TRY(rank_int.alloc(n * sizeof(float)));
   }
 
+  // multi-GPU: map every rank's contrib replicas once per graph; the vertex
+  // update then stores each owned row's new contrib into all replicas over
+  // NVLink, and the per-iteration allgather goes away.
+  // The dangling-mass allreduce that follows every vertex pass orders those
+  // stores before any rank's next edge pass. GI_PR_PEER=0: allgather path.
+  const char* peer_env = getenv("GI_PR_PEER");
+  const bool want_peer = dist && ctx->nranks <= 8 && !(peer_env && strcmp(peer_env, "0") == 0);
+  if (want_peer && g->peer_state == 0) {
+    gi_status e0 = ctx->comm->peer_map(g->contrib[0].p, g->peer_c[0], g->peer_opened, st);
+    gi_status e1 = e0 == GI_OK ? ctx->comm->peer_map(g->contrib[1].p, g->peer_c[1], g->peer_opened, st) : e0;
+    g->peer_state = e1 == GI_OK ? 1 : -1;
+    if (e1 != GI_OK) peer_unmap(g->peer_opened);
+  }
+  const bool peer = want_peer && g->peer_state == 1;
   cudaEvent_t ev[3] = {nullptr, nullptr, nullptr}, tot[2] = {nullptr, nullptr};
   if (o.profile) {
     for (int k = 0; k < 3; ++k) GI_CUDA(cudaEventCreate(&ev[k]));
@@ -489,6 +504,10 @@ gi_status pagerank_run(gi_graph g, int32_t iters, double damping, const gi_pr_op
     A.cin = g->contrib[it & 1].as<float>();
     A.cout = g->contrib[(it + 1) & 1].as<float>();
     A.rank_out = (it == iters - 1) ? (dist ? rank_int.as<float>() : d_out) : nullptr;
+    A.npeer = 0;
+    if (peer)
+      for (int q = 0; q < ctx->nranks; ++q)
+        if (q != ctx->rank) A.peer[A.npeer++] = static_cast<float*>(g->peer_c[(it + 1) & 1][q]);
     if (o.profile) GI_CUDA(cudaEventRecord(ev[0], st));
     if (dist) GI_CUDA(cudaMemsetAsync(A.dbuf + (it + 1) % 3, 0, sizeof(double), st));  // ranks without rows
     if (kernel == GI_PR_PUSH) {
@@ -547,7 +566,7 @@ gi_status pagerank_run(gi_graph g, int32_t iters, double damping, const gi_pr_op
     S.edge_launches++;
     if (dist) {  // dangling partials (allreduce) + contrib slices (allgatherv)
       GI_TRY(ctx->comm->allreduce_f64(A.dbuf + (it + 1) % 3, 1, st));
-      GI_TRY(ctx->comm->allgatherv(A.cout, cb, st));
+      if (!peer) GI_TRY(ctx->comm->allgatherv(A.cout, cb, st));
       if (it == iters - 1) {
         std::vector<int64_t> rb = cb;
         GI_TRY(ctx->comm->allgatherv(rank_int.p, rb, st));

@@ -36,6 +36,10 @@ struct PrArgs {
   // partition (pacc = s), 2 = middle (pacc += s), 3 = last (finish with pacc + s)
   float* pacc;
   int pmode;
+  // multi-GPU peer stores: the new contrib of an owned row is also written
+  // into the other ranks' replicas (replaces the per-iteration allgather)
+  float* peer[7];
+  int npeer;
 };
 
 // vertex update (a3): r' = base + d (s + D/n); contrib' = r'/outdeg; dangling partial
@@ -44,7 +48,9 @@ __device__ __forceinline__ void pr_epilogue(const PrArgs& A, int64_t r, float s,
   const int64_t v = A.row0 + r;
   const float rn = A.base + A.damp * (s + dn);
   const int od = __ldg(&A.outdeg[v]);
-  A.cout[v] = od > 0 ? rn / (float)od : 0.f;
+  const float c = od > 0 ? rn / (float)od : 0.f;
+  A.cout[v] = c;
+  for (int q = 0; q < A.npeer; ++q) A.peer[q][v] = c;
   if (od == 0) dpart += (double)rn;
   if (A.rank_out) A.rank_out[A.perm ? __ldg(&A.perm[v]) : v] = rn;
 }

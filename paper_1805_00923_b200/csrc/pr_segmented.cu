@@ -419,6 +419,7 @@ __global__ void __launch_bounds__(256) k_pr_acc(PrArgs A, const float* __restric
       if (A.rank_out) A.rank_out[A.perm ? __ldg(&A.perm[v0 + k]) : v0 + k] = rn;
     }
     *reinterpret_cast<float4*>(A.cout + v0) = make_float4(c[0], c[1], c[2], c[3]);
+    for (int p = 0; p < A.npeer; ++p) *reinterpret_cast<float4*>(A.peer[p] + v0) = make_float4(c[0], c[1], c[2], c[3]);
   }
   for (int64_t r = (vec ? 4 * nq : 0) + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < A.n;
        r += (int64_t)gridDim.x * blockDim.x) {

@@ -141,10 +141,15 @@ CASES = [
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("peer", ["1", "0"])
 @pytest.mark.parametrize("P", [2, 3, 4])
 @pytest.mark.parametrize("name,n,make", CASES)
-def test_partitioned_pagerank_and_bfs(gi, P, name, n, make):
+def test_partitioned_pagerank_and_bfs(gi, P, name, n, make, peer, monkeypatch):
+    """peer=1: the vertex update stores each owned row's contrib into every
+    rank's replica (peer stores, SURVEY §8(f) NEXT #3); peer=0: the allgather."""
     import torch
+
+    monkeypatch.setenv("GI_PR_PEER", peer)
 
     if not torch.cuda.is_available():
         pytest.fail("needs a CUDA device")
