@@ -65,7 +65,12 @@ GI_API gi_status gi_context_create(int device, void* cuda_stream, gi_context* ou
 /* Multi-GPU (one process per GPU): rank 0 calls
  * gi_nccl_unique_id, broadcasts the 128 bytes (e.g. with torch.distributed),
  * then every rank calls gi_context_create_dist. NCCL is loaded at run time
- * (dlopen "libnccl.so.2"); GI_ERR_NCCL if it cannot be. */
+ * (dlopen "libnccl.so.2"); GI_ERR_NCCL if it cannot be.
+ * PageRank on such a context maps every rank's contrib replicas once per graph
+ * (CUDA IPC) and stores new contrib values straight into them from the vertex
+ * update (no per-iteration allgather); if any rank cannot map them, or the
+ * environment sets GI_PR_PEER=0, every rank uses an NCCL allgatherv instead.
+ * Graphs must then be destroyed on all ranks (the mappings are closed there). */
 GI_API gi_status gi_nccl_unique_id(unsigned char id[128]);
 GI_API gi_status gi_context_create_dist(int device, void* cuda_stream, int rank, int nranks,
                                  const unsigned char id[128], gi_context* out);
