@@ -91,3 +91,19 @@ def test_product_does_not_import_oracle():
                 txt = open(os.path.join(dirpath, f), errors="replace").read()
                 assert "import oracle" not in txt and "from oracle" not in txt, f
                 assert "gi_oracle" not in txt, f
+
+
+def test_binding_constants_match_header(gi):
+    """Every enum constant of include/gi.h the binding defines has the header's value."""
+    src = open(os.path.join(ROOT, "include", "gi.h")).read()
+    consts = {}
+    for body in re.findall(r"enum\s*\{([^}]*)\}", src):
+        for name, val in re.findall(r"\b(GI_[A-Z0-9_]+)\s*=\s*(-?\d+)\s*(?=,|/|$)", body.strip()):
+            consts[name] = int(val)
+    assert consts["GI_PR_PULL_PARTITIONED"] == 4
+    checked = 0
+    for name, val in consts.items():
+        if hasattr(gi, name):
+            assert getattr(gi, name) == val, name
+            checked += 1
+    assert checked >= 10
