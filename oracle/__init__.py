@@ -58,6 +58,8 @@ def _get():
             lib.or_pagerank.restype = ctypes.c_int
             lib.or_bfs_depth.argtypes = [vp, ctypes.c_int32, i32p]
             lib.or_bfs_depth.restype = ctypes.c_int
+            lib.or_bfs_depth_levels.argtypes = [vp, ctypes.c_int32, i32p]
+            lib.or_bfs_depth_levels.restype = ctypes.c_int
             lib.or_validate_bfs.argtypes = [vp, ctypes.c_int32, i32p, i32p,
                                             ctypes.POINTER(ctypes.c_int64)]
             lib.or_validate_bfs.restype = ctypes.c_int
@@ -148,6 +150,15 @@ def bfs_depth(g: Graph, source: int) -> np.ndarray:
     rc = _get().or_bfs_depth(g._h, source, d)
     if rc != 0:
         raise OracleError(f"or_bfs_depth failed ({rc})")
+    return d[: g.n]
+
+
+def bfs_depth_levels(g: Graph, source: int) -> np.ndarray:
+    """The same depths as bfs_depth, computed level by level with OpenMP (billion-edge configs)."""
+    d = np.empty(max(g.n, 1), np.int32)
+    rc = _get().or_bfs_depth_levels(g._h, source, d)
+    if rc != 0:
+        raise OracleError(f"or_bfs_depth_levels failed ({rc})")
     return d[: g.n]
 
 

@@ -14,7 +14,8 @@
  *      CSR/CSC P:3183 [draft]. V = {0..n-1} with n given explicitly (R4);
  *      self-loops removed and duplicates removed on request (R5); optional
  *      symmetrisation "duplicating the directed edges" P:3183 [draft].
- *      Sort = qsort of 64-bit (u<<32|v) keys (a library primitive).
+ *      Rows by counting sort, each row sorted with qsort (a library
+ *      primitive), repeats dropped inside the sorted row.
  *
  *  PageRank (or_pagerank), fp64, Jacobi, fixed iteration count:
  *      edge update  new_rank[dst] += old_rank[src] / out_degree[src]
@@ -36,6 +37,9 @@
  *      Parent vector semantics: parent = -1 initially P:2093-2099; each vertex
  *      inserted once P:1021-1025; parent[source] = source S:509 (R8, R9).
  *
+ *      or_bfs_depth_levels: the same depths level by level (OpenMP), for the
+ *      billion-edge configs; pinned to or_bfs_depth.
+ *
  *  CC (or_cc_labels): label propagation IDs[dst] min= IDs[src] from
  *      IDs[v] = v (P:3440-3472 [punt]) written out as its fixed point
  *      IDs[v] = min{u : u = v or u ->* v} (see the function).
@@ -53,6 +57,7 @@
 #include <stdlib.h>
 #include <math.h>
 #include <string.h>
+#include <omp.h>
 
 typedef struct {
   int64_t n, m;
@@ -62,57 +67,155 @@ typedef struct {
   int32_t* csc_idx; /* m, ascending within each row */
 } or_graph;
 
-static int cmp_u64(const void* a, const void* b) {
-  const uint64_t x = *(const uint64_t*)a, y = *(const uint64_t*)b;
+void or_graph_free(or_graph* g);
+
+static int cmp_i32(const void* a, const void* b) {
+  const int32_t x = *(const int32_t*)a, y = *(const int32_t*)b;
   return x < y ? -1 : (x > y ? 1 : 0);
 }
 
+/* Bucket the pairs (key[i], val[i]), i < k, by key into rows of a CSR over n
+ * keys (counting sort), then sort every row (qsort, a library primitive) and,
+ * with dedup, keep one copy of each repeated value. Returns the number of
+ * entries kept, or -3 (out of memory); *off (n+1) and *idx are malloc'd; key
+ * and val are freed. The counting sort runs in two passes so that no two
+ * threads ever write the same counter: (1) each thread moves its slice of the
+ * pairs into NB key ranges ("coarse buckets") at offsets from a prefix over
+ * (bucket, thread) counts; (2) each coarse bucket is counting-sorted by key on
+ * its own. Rows are independent, so the OpenMP loops change nothing but speed. */
+#define OR_NB 256
+static int64_t bucket_rows(int64_t n, int64_t k, int32_t* key, int32_t* val, int dedup,
+                           int64_t** off_out, int32_t** idx_out) {
+  const int64_t width = n / OR_NB + 1; /* keys per coarse bucket */
+  const int nt = omp_get_max_threads();
+  int64_t* hist = (int64_t*)calloc((size_t)nt * OR_NB + 1, sizeof(int64_t));
+  int32_t* ck = (int32_t*)malloc((size_t)(k > 0 ? k : 1) * sizeof(int32_t));
+  int32_t* cv = (int32_t*)malloc((size_t)(k > 0 ? k : 1) * sizeof(int32_t));
+  int64_t* cnt = (int64_t*)calloc((size_t)n + 1, sizeof(int64_t));
+  if (!hist || !ck || !cv || !cnt) { free(hist); free(ck); free(cv); free(cnt); free(key); free(val); return -3; }
+  /* pass 1: hist[b * nt + t] = pairs of thread t's slice in bucket b */
+#pragma omp parallel num_threads(nt)
+  {
+    const int t = omp_get_thread_num();
+    const int64_t lo = k * t / nt, hi = k * (t + 1) / nt;
+    int64_t* h = (int64_t*)calloc(OR_NB, sizeof(int64_t));
+    for (int64_t i = lo; i < hi; ++i) h[key[i] / width]++;
+    for (int b = 0; b < OR_NB; ++b) hist[(int64_t)b * nt + t] = h[b];
+#pragma omp barrier
+#pragma omp single
+    {
+      int64_t run = 0;
+      for (int64_t j = 0; j < (int64_t)nt * OR_NB; ++j) {
+        const int64_t c = hist[j];
+        hist[j] = run;
+        run += c;
+      }
+      hist[(int64_t)nt * OR_NB] = run;
+    }
+    for (int b = 0; b < OR_NB; ++b) h[b] = hist[(int64_t)b * nt + t];
+    for (int64_t i = lo; i < hi; ++i) {
+      const int64_t at = h[key[i] / width]++;
+      ck[at] = key[i];
+      cv[at] = val[i];
+    }
+    free(h);
+  }
+  free(key);
+  free(val);
+  /* row lengths: cnt[x + 1] = pairs with key x (each bucket's keys counted by one thread) */
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int b = 0; b < OR_NB; ++b)
+    for (int64_t i = hist[(int64_t)b * nt]; i < hist[(int64_t)(b + 1) * nt]; ++i) cnt[ck[i] + 1]++;
+  for (int64_t x = 0; x < n; ++x) cnt[x + 1] += cnt[x]; /* cnt = row starts */
+  int32_t* buf = (int32_t*)malloc((size_t)(k > 0 ? k : 1) * sizeof(int32_t));
+  int64_t* pos = (int64_t*)malloc(((size_t)n + 1) * sizeof(int64_t));
+  if (!buf || !pos) { free(hist); free(ck); free(cv); free(cnt); free(buf); free(pos); return -3; }
+  memcpy(pos, cnt, ((size_t)n + 1) * sizeof(int64_t));
+  /* pass 2: scatter each bucket into its rows */
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int b = 0; b < OR_NB; ++b)
+    for (int64_t i = hist[(int64_t)b * nt]; i < hist[(int64_t)(b + 1) * nt]; ++i) buf[pos[ck[i]]++] = cv[i];
+  free(hist);
+  free(ck);
+  free(cv);
+  /* sort each row; pos[x] = entries kept in row x */
+#pragma omp parallel for schedule(dynamic, 1024)
+  for (int64_t x = 0; x < n; ++x) {
+    int32_t* row = buf + cnt[x];
+    const int64_t len = cnt[x + 1] - cnt[x];
+    qsort(row, (size_t)len, sizeof(int32_t), cmp_i32);
+    int64_t kept = len;
+    if (dedup && len > 1) {
+      kept = 1;
+      for (int64_t j = 1; j < len; ++j)
+        if (row[j] != row[kept - 1]) row[kept++] = row[j];
+    }
+    pos[x] = kept;
+  }
+  int64_t* off = (int64_t*)malloc(((size_t)n + 1) * sizeof(int64_t));
+  if (!off) { free(cnt); free(pos); free(buf); return -3; }
+  off[0] = 0;
+  for (int64_t x = 0; x < n; ++x) off[x + 1] = off[x] + pos[x];
+  const int64_t m = off[n];
+  int32_t* idx = (int32_t*)malloc((size_t)(m > 0 ? m : 1) * sizeof(int32_t));
+  if (!idx) { free(cnt); free(pos); free(buf); free(off); return -3; }
+#pragma omp parallel for schedule(dynamic, 1024)
+  for (int64_t x = 0; x < n; ++x) memcpy(idx + off[x], buf + cnt[x], (size_t)pos[x] * sizeof(int32_t));
+  free(cnt);
+  free(pos);
+  free(buf);
+  *off_out = off;
+  *idx_out = idx;
+  return m;
+}
+
 /* Returns m >= 0 and *out, or -1 (bad argument) / -2 (vertex out of range) /
- * -3 (out of memory). */
+ * -3 (out of memory).
+ * E = the input pairs without self-loops (remove_self_loops), plus (v,u) for
+ * every (u,v) (symmetrize), without repeats (dedup). CSR: E bucketed by source,
+ * each row sorted; CSC: the CSR's pairs bucketed by destination, each row
+ * sorted (the transpose). */
 int64_t or_build(int64_t n, int64_t m0, const int32_t* src, const int32_t* dst,
                  int remove_self_loops, int dedup, int symmetrize, or_graph** out) {
   *out = NULL;
   if (n < 0 || m0 < 0 || n > 2147483647LL) return -1;
+  int bad = 0;
+#pragma omp parallel for reduction(| : bad)
   for (int64_t i = 0; i < m0; ++i)
-    if (src[i] < 0 || src[i] >= n || dst[i] < 0 || dst[i] >= n) return -2;
+    if (src[i] < 0 || src[i] >= n || dst[i] < 0 || dst[i] >= n) bad = 1;
+  if (bad) return -2;
+  /* the cleaned pair list (u[i], v[i]) */
   const int64_t cap = symmetrize ? 2 * m0 : m0;
-  uint64_t* key = (uint64_t*)malloc((size_t)(cap > 0 ? cap : 1) * sizeof(uint64_t));
-  if (!key) return -3;
+  int32_t* u = (int32_t*)malloc((size_t)(cap > 0 ? cap : 1) * sizeof(int32_t));
+  int32_t* v = (int32_t*)malloc((size_t)(cap > 0 ? cap : 1) * sizeof(int32_t));
+  if (!u || !v) { free(u); free(v); return -3; }
   int64_t k = 0;
   for (int64_t i = 0; i < m0; ++i) {
-    const uint32_t u = (uint32_t)src[i], v = (uint32_t)dst[i];
-    if (remove_self_loops && u == v) continue;
-    key[k++] = ((uint64_t)u << 32) | v;
-    if (symmetrize) key[k++] = ((uint64_t)v << 32) | u;
-  }
-  qsort(key, (size_t)k, sizeof(uint64_t), cmp_u64);
-  int64_t m = 0;
-  for (int64_t i = 0; i < k; ++i) {
-    if (dedup && m > 0 && key[m - 1] == key[i]) continue;
-    key[m++] = key[i];
+    if (remove_self_loops && src[i] == dst[i]) continue;
+    u[k] = src[i];
+    v[k++] = dst[i];
+    if (symmetrize) {
+      u[k] = dst[i];
+      v[k++] = src[i];
+    }
   }
   or_graph* g = (or_graph*)calloc(1, sizeof(or_graph));
+  if (!g) { free(u); free(v); return -3; }
   g->n = n;
+  const int64_t m = bucket_rows(n, k, u, v, dedup, &g->csr_off, &g->csr_idx); /* frees u, v */
+  if (m < 0) { free(g); return m; }
   g->m = m;
-  g->csr_off = (int64_t*)calloc((size_t)n + 1, sizeof(int64_t));
-  g->csc_off = (int64_t*)calloc((size_t)n + 1, sizeof(int64_t));
-  g->csr_idx = (int32_t*)malloc((size_t)(m > 0 ? m : 1) * sizeof(int32_t));
-  g->csc_idx = (int32_t*)malloc((size_t)(m > 0 ? m : 1) * sizeof(int32_t));
-  /* CSR: keys are sorted by (u, v). */
-  for (int64_t i = 0; i < m; ++i) {
-    g->csr_off[(key[i] >> 32) + 1]++;
-    g->csr_idx[i] = (int32_t)(key[i] & 0xFFFFFFFFu);
-  }
-  for (int64_t v = 0; v < n; ++v) g->csr_off[v + 1] += g->csr_off[v];
-  /* CSC: re-key as (v, u) and sort again. */
-  for (int64_t i = 0; i < m; ++i) key[i] = (key[i] << 32) | (key[i] >> 32);
-  qsort(key, (size_t)m, sizeof(uint64_t), cmp_u64);
-  for (int64_t i = 0; i < m; ++i) {
-    g->csc_off[(key[i] >> 32) + 1]++;
-    g->csc_idx[i] = (int32_t)(key[i] & 0xFFFFFFFFu);
-  }
-  for (int64_t v = 0; v < n; ++v) g->csc_off[v + 1] += g->csc_off[v];
-  free(key);
+  /* CSC: the same m pairs keyed by destination */
+  int32_t* row = (int32_t*)malloc((size_t)(m > 0 ? m : 1) * sizeof(int32_t));
+  if (!row) { or_graph_free(g); return -3; }
+#pragma omp parallel for schedule(dynamic, 1024)
+  for (int64_t x = 0; x < n; ++x)
+    for (int64_t j = g->csr_off[x]; j < g->csr_off[x + 1]; ++j) row[j] = (int32_t)x;
+  int32_t* col = (int32_t*)malloc((size_t)(m > 0 ? m : 1) * sizeof(int32_t));
+  if (!col) { free(row); or_graph_free(g); return -3; }
+  memcpy(col, g->csr_idx, (size_t)m * sizeof(int32_t));
+  const int64_t mt = bucket_rows(n, m, col, row, 0, &g->csc_off, &g->csc_idx); /* frees col, row */
+  if (mt != m) { or_graph_free(g); return mt < 0 ? mt : -3; }
   *out = g;
   return m;
 }
@@ -142,7 +245,8 @@ int or_pagerank(const or_graph* g, int iters, double damp, int dangling_rule, do
   double* r = rank;
   double* nr = (double*)malloc((size_t)n * sizeof(double));
   double* outdeg = (double*)malloc((size_t)n * sizeof(double));
-  if (!nr || !outdeg) { free(nr); free(outdeg); return -3; }
+  double* w = (double*)malloc((size_t)n * sizeof(double));
+  if (!nr || !outdeg || !w) { free(nr); free(outdeg); free(w); return -3; }
   for (int64_t u = 0; u < n; ++u) outdeg[u] = (double)(g->csr_off[u + 1] - g->csr_off[u]);
   for (int64_t v = 0; v < n; ++v) r[v] = 1.0 / (double)n;
   const double base = (1.0 - damp) / (double)n;
@@ -151,12 +255,16 @@ int or_pagerank(const or_graph* g, int iters, double damp, int dangling_rule, do
     for (int64_t u = 0; u < n; ++u)
       if (outdeg[u] == 0.0) D += r[u];
     const double spread = dangling_rule == 0 ? D / (double)n : 0.0;
+    /* w[u] = r[u] / outdeg[u], the edge weight of every out-edge of u (the
+     * same IEEE quotient the edge loop would form per edge, formed once) */
+#pragma omp parallel for schedule(static)
+    for (int64_t u = 0; u < n; ++u) w[u] = outdeg[u] > 0.0 ? r[u] / outdeg[u] : 0.0;
 #pragma omp parallel for schedule(dynamic, 4096)
     for (int64_t v = 0; v < n; ++v) {
       double s = 0.0;
       for (int64_t j = g->csc_off[v]; j < g->csc_off[v + 1]; ++j) {
         const int32_t u = g->csc_idx[j];
-        s += r[u] / outdeg[u];
+        s += w[u];
       }
       nr[v] = base + damp * (s + spread);
     }
@@ -164,6 +272,7 @@ int or_pagerank(const or_graph* g, int iters, double damp, int dangling_rule, do
   }
   free(nr);
   free(outdeg);
+  free(w);
   return 0;
 }
 
@@ -191,6 +300,50 @@ int or_bfs_depth(const or_graph* g, int32_t source, int32_t* depth) {
   return 0;
 }
 
+/* The same depths, level by level (level-synchronous, top-down): the
+ * frontier F_L = {v : depth(v) = L}; F_{L+1} = the out-neighbours of F_L with
+ * no depth yet. Depths are unique, so the order in which a level's vertices
+ * are discovered (OpenMP threads racing on a compare-and-swap) changes
+ * nothing. For the billion-edge configs, whose FIFO run is minutes per source
+ * (BASELINE.md CPU-baseline plan); pinned to or_bfs_depth. */
+int or_bfs_depth_levels(const or_graph* g, int32_t source, int32_t* depth) {
+  const int64_t n = g->n;
+  if (source < 0 || source >= n) return -2;
+  int32_t* cur = (int32_t*)malloc((size_t)n * sizeof(int32_t));
+  int32_t* nxt = (int32_t*)malloc((size_t)n * sizeof(int32_t));
+  if (!cur || !nxt) { free(cur); free(nxt); return -3; }
+#pragma omp parallel for schedule(static)
+  for (int64_t v = 0; v < n; ++v) depth[v] = -1;
+  depth[source] = 0;
+  cur[0] = source;
+  int64_t ncur = 1;
+  for (int32_t level = 0; ncur > 0; ++level) {
+    int64_t nnext = 0;
+#pragma omp parallel for schedule(dynamic, 64)
+    for (int64_t i = 0; i < ncur; ++i) {
+      const int32_t u = cur[i];
+      for (int64_t j = g->csr_off[u]; j < g->csr_off[u + 1]; ++j) {
+        const int32_t v = g->csr_idx[j];
+        int32_t unseen = -1;
+        if (__atomic_load_n(&depth[v], __ATOMIC_RELAXED) == -1 &&
+            __atomic_compare_exchange_n(&depth[v], &unseen, level + 1, 0, __ATOMIC_RELAXED, __ATOMIC_RELAXED)) {
+          int64_t at;
+#pragma omp atomic capture
+          at = nnext++;
+          nxt[at] = v;
+        }
+      }
+    }
+    int32_t* t = cur;
+    cur = nxt;
+    nxt = t;
+    ncur = nnext;
+  }
+  free(cur);
+  free(nxt);
+  return 0;
+}
+
 static int has_edge(const or_graph* g, int32_t u, int32_t v) {
   int64_t lo = g->csr_off[u], hi = g->csr_off[u + 1];
   while (lo < hi) {
@@ -209,22 +362,36 @@ int or_validate_bfs(const or_graph* g, int32_t source, const int32_t* depth,
   const int64_t n = g->n;
   *bad_vertex = -1;
   if (parent[source] != source) { *bad_vertex = source; return 1; }
+  /* every vertex is checked on its own; the smallest failing vertex is reported */
+  int64_t first = n;
+#pragma omp parallel for schedule(dynamic, 65536) reduction(min : first)
   for (int64_t v = 0; v < n; ++v) {
-    if (v == source) continue;
+    if (v == source || v >= first) continue;
     const int32_t p = parent[v];
-    if ((p == -1) != (depth[v] == -1)) { *bad_vertex = v; return 2; }
-    if (p == -1) continue;
-    if (p < 0 || p >= n) { *bad_vertex = v; return 3; }
-    if (!has_edge(g, p, (int32_t)v)) { *bad_vertex = v; return 4; }
-    if (depth[p] != depth[v] - 1) { *bad_vertex = v; return 5; }
+    int bad = 0;
+    if ((p == -1) != (depth[v] == -1)) bad = 1;
+    else if (p == -1) bad = 0;
+    else if (p < 0 || p >= n) bad = 1;
+    else if (!has_edge(g, p, (int32_t)v)) bad = 1;
+    else if (depth[p] != depth[v] - 1) bad = 1;
+    if (bad && v < first) first = v;
   }
-  return 0;
+  if (first == n) return 0;
+  /* the rule the first failing vertex breaks */
+  const int64_t v = first;
+  const int32_t p = parent[v];
+  *bad_vertex = v;
+  if ((p == -1) != (depth[v] == -1)) return 2;
+  if (p < 0 || p >= n) return 3;
+  if (!has_edge(g, p, (int32_t)v)) return 4;
+  return 5;
 }
 
 /* Edge count examined by a BFS tree in TEPS terms (R16): sum of outdeg over
  * reached vertices. */
 int64_t or_reached_out_edges(const or_graph* g, const int32_t* depth) {
   int64_t s = 0;
+#pragma omp parallel for reduction(+ : s)
   for (int64_t v = 0; v < g->n; ++v)
     if (depth[v] >= 0) s += g->csr_off[v + 1] - g->csr_off[v];
   return s;

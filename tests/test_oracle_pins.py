@@ -20,6 +20,8 @@ that a dropped term, wrong sign/index or transposed operand fails one of them:
     edge, disconnected, Floyd-Warshall brute force on n <= 8
   - validator vs. exhaustive enumeration of parent vectors with a walk-based
     definition of a shortest-path tree
+  - level-synchronous depths (OpenMP, billion-edge configs) = the FIFO depths
+  - TEPS count (R16) = sum of raw out-degrees over the Floyd-Warshall reachable set
 * Build: edge set = numpy.unique of the cleaned pairs; CSC = transpose of CSR.
 """
 from __future__ import annotations
@@ -267,6 +269,33 @@ def test_bfs_brute_force_small():
         D = _floyd_warshall(n, s, t)
         for src in range(n):
             assert oracle.bfs_depth(g, src).tolist() == D[src].tolist()
+            assert oracle.bfs_depth_levels(g, src).tolist() == D[src].tolist()
+
+
+def test_bfs_levels_equals_fifo_on_rmat():
+    """or_bfs_depth_levels (OpenMP, level-synchronous) = the FIFO BFS on graphs with many levels
+    and wide frontiers (RMAT, a ragged grid, a path)."""
+    cases = [(1 << 12, *graphgen.rmat(12, 8, 0.57, 0.19, 0.19, 21)),
+             (64 * 64, *graphgen.grid(64, 64, 0.3, 5)), (500, *graphgen.path(500))]
+    for n, s, t in cases:
+        g = oracle.build_graph(n, s, t)
+        for src in [0, 1, n // 3, n - 1]:
+            assert np.array_equal(oracle.bfs_depth_levels(g, src), oracle.bfs_depth(g, src)), (n, src)
+
+
+def test_reached_out_edges_brute_force():
+    """R16's TEPS count = sum of out-degrees (counted from the raw cleaned pairs) over the vertices
+    Floyd-Warshall says are reachable."""
+    for trial in range(200):
+        n = 1 + trial % 8
+        s, t = graphgen.random_digraph(n, (trial * 5) % (3 * n + 1), 7000 + trial)
+        g = oracle.build_graph(n, s, t)
+        D = _floyd_warshall(n, s, t)
+        pairs = {(int(a), int(b)) for a, b in zip(s, t) if a != b}
+        outdeg = [sum(1 for (a, _) in pairs if a == u) for u in range(n)]
+        for src in range(n):
+            want = sum(outdeg[v] for v in range(n) if D[src][v] >= 0)
+            assert oracle.reached_out_edges(g, oracle.bfs_depth(g, src)) == want
 
 
 def _walk_valid(n, edges, dist, s, parent):
@@ -362,6 +391,25 @@ def test_build_matches_numpy_unique():
             for u in range(n):
                 row = g.csr_idx[g.csr_off[u]:g.csr_off[u + 1]]
                 assert np.all(np.diff(row) > 0)
+
+
+def test_build_matches_numpy_unique_rmat():
+    """The same pin on a skewed graph large enough for every thread to hold pairs of every key range."""
+    n = 1 << 14
+    s, t = graphgen.rmat(14, 16, 0.57, 0.19, 0.19, 31)
+    for sym in (False, True):
+        g = oracle.build_graph(n, s, t, symmetrize=sym)
+        a, b = s.astype(np.int64), t.astype(np.int64)
+        k = a != b
+        a, b = a[k], b[k]
+        if sym:
+            a, b = np.concatenate([a, b]), np.concatenate([b, a])
+        key = np.unique(a * n + b)
+        assert g.m == len(key)
+        assert np.array_equal(np.repeat(np.arange(n), np.diff(g.csr_off)) * n + g.csr_idx, key)
+        keyt = np.sort(b * n + a)
+        keyt = np.unique(keyt)
+        assert np.array_equal(np.repeat(np.arange(n), np.diff(g.csc_off)) * n + g.csc_idx, keyt)
 
 
 def test_build_out_of_range():
