@@ -113,6 +113,24 @@ def pick_sources(n: int, src: np.ndarray, dst: np.ndarray, k: int, seed: int) ->
     return out[:got].copy()
 
 
+def has_out_edge(n: int, src: np.ndarray, dst: np.ndarray) -> np.ndarray:
+    """uint8[n]: 1 where v is the source of a non-self-loop pair of this edge list (or share of it)."""
+    elig = np.empty(max(n, 1), np.uint8)
+    _get().gg_has_out_edge(n, len(src), np.ascontiguousarray(src, np.int32), np.ascontiguousarray(dst, np.int32),
+                           elig)
+    return elig[:n]
+
+
+def pick_sources_from_mask(n: int, eligible: np.ndarray, k: int, seed: int) -> np.ndarray:
+    """pick_sources given the eligibility mask (e.g. OR-reduced over ranks holding shares of the edges)."""
+    elig = np.ascontiguousarray(np.asarray(eligible) != 0, np.uint8)
+    if len(elig) == 0:
+        elig = np.zeros(1, np.uint8)
+    out = np.empty(max(k, 1), np.int32)
+    got = _get().gg_pick_sources(n, elig, k, seed, max(64 * k, 1 << 20), out)
+    return out[:got].copy()
+
+
 def edge_checksum(src: np.ndarray, dst: np.ndarray) -> int:
     return int(_get().gg_edge_checksum(len(src), np.ascontiguousarray(src, np.int32),
                                        np.ascontiguousarray(dst, np.int32)))

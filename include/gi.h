@@ -66,16 +66,51 @@ GI_API gi_status gi_context_create(int device, void* cuda_stream, gi_context* ou
  * gi_nccl_unique_id, broadcasts the 128 bytes (e.g. with torch.distributed),
  * then every rank calls gi_context_create_dist. NCCL is loaded at run time
  * (dlopen "libnccl.so.2"); GI_ERR_NCCL if it cannot be.
- * PageRank on such a context maps every rank's contrib replicas once per graph
- * (CUDA IPC) and stores new contrib values straight into them from the vertex
- * update (no per-iteration allgather); if any rank cannot map them, or the
- * environment sets GI_PR_PEER=0, every rank uses an NCCL allgatherv instead.
- * Graphs must then be destroyed on all ranks (the mappings are closed there). */
+ * PageRank exchanges contrib slices with an NCCL allgatherv every iteration.
+ * With GI_PR_PEER=1 it instead maps every rank's contrib replicas once per
+ * graph (CUDA IPC) and stores new contrib values straight into them from the
+ * vertex update (no per-iteration allgather); the ranks
+ * agree on the choice (an allreduce: peer stores only if every rank asks for
+ * them and every rank can map), else all use the allgatherv. Peer stores are
+ * tested across processes sharing one GPU (gi_context_create_hostcomm) and
+ * with in-process ranks, NOT across GPUs over NVLink (no multi-GPU box here).
+ * gi_graph_destroy is then collective: every rank closes its mappings, then
+ * all ranks meet at a barrier before any frees the mapped buffers. */
 GI_API gi_status gi_nccl_unique_id(unsigned char id[128]);
 GI_API gi_status gi_context_create_dist(int device, void* cuda_stream, int rank, int nranks,
                                  const unsigned char id[128], gi_context* out);
 GI_API gi_status gi_context_destroy(gi_context ctx);
 GI_API gi_status gi_context_rank(gi_context ctx, int* rank, int* nranks);
+
+/* Multi-process contexts over ANY transport: the multi-GPU path's collectives
+ * (allreduce of degree histograms and scalars, allgatherv of
+ * contrib / bitmap / parent slices, alltoallv of the build's owner shuffle)
+ * staged through host memory and performed by the caller's callbacks, e.g.
+ * torch.distributed over gloo. Each callback returns 0 on success; it is
+ * called on the thread making the library call, with host buffers valid for
+ * the duration of the callback:
+ *   allreduce(user, buf, count, dtype): in-place element-wise SUM over ranks of
+ *     `count` elements, dtype GI_DT_INT32 / GI_DT_INT64 / GI_DT_F64;
+ *   allgatherv(user, buf, off, nranks): `buf` holds off[nranks] bytes; on
+ *     return bytes [off[q], off[q+1]) must hold rank q's bytes (this rank's
+ *     own range is filled on entry);
+ *   alltoallv(user, send, soff, recv, roff, nranks): send bytes
+ *     [soff[q], soff[q+1]) to rank q; receive rank q's bytes into
+ *     recv + [roff[q], roff[q+1]) (counts agree pairwise).
+ * Ranks may share a device (no kernel waits on another rank: every collective
+ * synchronises the stream first). PageRank peer stores (CUDA IPC, handles
+ * exchanged through allgatherv) are used only with GI_PR_PEER=1 on every rank.
+ * The struct is copied; `user` must stay valid until gi_context_destroy. */
+enum { GI_DT_INT32 = 0, GI_DT_INT64 = 1, GI_DT_F64 = 2 };
+typedef struct {
+  void* user;
+  int (*allreduce)(void* user, void* buf, int64_t count, int32_t dtype);
+  int (*allgatherv)(void* user, void* buf, const int64_t* off, int32_t nranks);
+  int (*alltoallv)(void* user, const void* send, const int64_t* soff, void* recv, const int64_t* roff,
+                   int32_t nranks);
+} gi_host_comm;
+GI_API gi_status gi_context_create_hostcomm(int device, void* cuda_stream, int rank, int nranks,
+                                            const gi_host_comm* comm, gi_context* out);
 
 /* Test hook for the partitioned path on ONE GPU: nranks simulated ranks,
  * each driven by its own host thread with its own context created by
@@ -106,10 +141,14 @@ enum {
   GI_SYMMETRIZE = 1u << 3,        /* add (v,u) for every (u,v): "an undirected
                                      graph would be represented by duplicating
                                      the directed edges" P:3183 [draft] */
-  GI_NO_RELABEL = 1u << 4         /* keep input vertex order internally (the
+  GI_NO_RELABEL = 1u << 4,        /* keep input vertex order internally (the
                                      default relabels by out-degree when the
                                      degrees are skewed: max > 32 x mean, on one
                                      GPU; results are always in input ids) */
+  GI_OFFSETS64 = 1u << 5          /* store CSR/CSC row offsets as int64 even when
+                                     m < 2^31 (they are int64 anyway from 2^31
+                                     edges on, e.g. config 5): runs
+                                     the wide-offset kernels on small graphs */
 };
 
 /* Builds the edgeset from an edge list ("edges = load(...)"):
@@ -185,7 +224,11 @@ typedef struct {
   int32_t kernel;          /* GI_PR_* kernel actually used */
   float vertex_ms;         /* segmented pull: part of edge_ms spent in the
                               vertex-update kernel (profile=1) */
-  int64_t bytes_alg_per_iter; /* 4m + (o+12)n for pull */
+  int64_t bytes_alg_per_iter; /* 4m + (o+12)n for pull (this rank's rows) */
+  int32_t exchange;        /* multi-GPU contrib exchange: 0 none (one rank),
+                              1 allgatherv per iteration, 2 peer stores */
+  float exchange_ms;       /* profile=1: device time of the per-iteration
+                              collectives (dangling allreduce + allgatherv) */
 } gi_pr_stats;
 
 GI_API gi_status gi_pagerank_ex(gi_graph g, int32_t iters, double damping, const gi_pr_opts* opts,

@@ -71,8 +71,15 @@ def _get():
             lib.or_cc_labels.restype = ctypes.c_int
             lib.or_sssp.argtypes = [vp, ctypes.c_int32, i32p, i64p]
             lib.or_sssp.restype = ctypes.c_int
+            lib.or_set_threads.argtypes = [ctypes.c_int]
+            lib.or_set_threads.restype = ctypes.c_int
             _lib = lib
     return _lib
+
+
+def set_threads(t: int) -> int:
+    """OpenMP threads of the oracle's loops (t <= 0: unchanged); returns the previous count."""
+    return int(_get().or_set_threads(int(t)))
 
 
 class OracleError(RuntimeError):

@@ -69,6 +69,14 @@ typedef struct {
 
 void or_graph_free(or_graph* g);
 
+/* OpenMP threads the oracle's parallel loops use (the CPU baseline times it on
+ * all host cores and on one); returns the previous setting. */
+int or_set_threads(int t) {
+  const int prev = omp_get_max_threads();
+  if (t > 0) omp_set_num_threads(t);
+  return prev;
+}
+
 static int cmp_i32(const void* a, const void* b) {
   const int32_t x = *(const int32_t*)a, y = *(const int32_t*)b;
   return x < y ? -1 : (x > y ? 1 : 0);

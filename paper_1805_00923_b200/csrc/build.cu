@@ -222,7 +222,7 @@ gi_status build_graph(gi_context ctx, int64_t n, int64_t m0, const int32_t* d_sr
   g->ml = m;
   g->r0 = 0;
   g->nr = n;
-  g->off64 = m >= (int64_t)INT32_MAX;
+  g->off64 = m >= (int64_t)INT32_MAX || (flags & GI_OFFSETS64);
 
   // 6. out-degrees in input ids (from the input-id CSR)
   DevBuf off_in;
@@ -572,7 +572,7 @@ gi_status build_graph_dist(gi_context ctx, int64_t n, int64_t m0, const int32_t*
     std::swap(pc, pa);
   }
   g->ml = ml;
-  g->off64 = ml >= (int64_t)INT32_MAX;
+  g->off64 = ml >= (int64_t)INT32_MAX || (flags & GI_OFFSETS64);
   if (g->off64) GI_TRY(csr_from_sorted<int64_t>(g, pc->as<uint64_t>(), ml, bits, n, g->csr_off, g->csr_idx));
   else GI_TRY(csr_from_sorted<int32_t>(g, pc->as<uint64_t>(), ml, bits, n, g->csr_off, g->csr_idx));
   // exact out-degrees: local row lengths summed over ranks

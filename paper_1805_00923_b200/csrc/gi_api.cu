@@ -198,7 +198,7 @@ gi_status gi_graph_create(gi_context ctx, int64_t n, int64_t m0, const int32_t* 
   if (n < 0 || n > INT32_MAX) return fail(GI_ERR_INVALID_ARGUMENT, "gi_graph_create: n must be in [0, 2^31-1]");
   if (m0 < 0 || m0 >= (1ll << 40)) return fail(GI_ERR_INVALID_ARGUMENT, "gi_graph_create: bad edge count");
   if (m0 > 0 && (!src || !dst)) return fail(GI_ERR_INVALID_ARGUMENT, "gi_graph_create: NULL edge array");
-  const uint32_t known = GI_EDGES_ON_DEVICE | GI_REMOVE_SELF_LOOPS | GI_DEDUP | GI_SYMMETRIZE | GI_NO_RELABEL;
+  const uint32_t known = GI_EDGES_ON_DEVICE | GI_REMOVE_SELF_LOOPS | GI_DEDUP | GI_SYMMETRIZE | GI_NO_RELABEL | GI_OFFSETS64;
   if (flags & ~known) return fail(GI_ERR_INVALID_ARGUMENT, "gi_graph_create: unknown flag bits");
   if (n == 0 && m0 > 0) return fail(GI_ERR_VERTEX_OUT_OF_RANGE, "gi_graph_create: edges given but n = 0");
   GI_CUDA(cudaSetDevice(ctx->device));
@@ -228,9 +228,17 @@ gi_status gi_graph_destroy(gi_graph g) {
   cudaSetDevice(g->ctx->device);
   cudaStreamSynchronize(g->ctx->stream);
   g->ctx->live_graphs--;
+  gi_status s = GI_OK;
+  if (g->peer_state == 1 && g->ctx->comm) {
+    // other ranks store into (and map) this rank's contrib buffers: every rank
+    // closes its mappings, and no rank frees before all have (collective)
+    peer_unmap(g->peer_opened);
+    AllocScope as_(g->ctx->stream);
+    s = g->ctx->comm->barrier(g->ctx->stream);
+  }
   peer_unmap(g->peer_opened);
   delete g;  // pooled buffers go back to the pool (stream-ordered frees)
-  return GI_OK;
+  return s;
 }
 
 gi_status gi_graph_num_vertices(gi_graph g, int64_t* n) {
@@ -606,6 +614,8 @@ gi_status gi_local_group_create(int nranks, gi_local_group* out) {
   grp->g.n = nranks;
   grp->g.ptr.assign(nranks, nullptr);
   grp->g.offs.assign(nranks, {});
+  grp->g.dev.assign(nranks, -1);
+  grp->g.flag.assign(nranks, 0);
   *out = grp;
   return GI_OK;
   GI_GUARD_END
@@ -627,6 +637,24 @@ gi_status gi_context_create_local(int device, void* cuda_stream, gi_local_group 
   c->rank = rank;
   c->nranks = grp->g.n;
   if (c->nranks > 1) c->comm = make_local_comm(&grp->g, rank);
+  *out = c;
+  return GI_OK;
+  GI_GUARD_END
+}
+
+gi_status gi_context_create_hostcomm(int device, void* cuda_stream, int rank, int nranks, const gi_host_comm* comm,
+                                     gi_context* out) {
+  GI_GUARD_BEGIN
+  if (!out || !comm || !comm->allreduce || !comm->allgatherv || !comm->alltoallv)
+    return fail(GI_ERR_INVALID_ARGUMENT, "gi_context_create_hostcomm: NULL argument or callback");
+  *out = nullptr;
+  if (nranks < 1 || rank < 0 || rank >= nranks)
+    return fail(GI_ERR_INVALID_ARGUMENT, "gi_context_create_hostcomm: bad rank / nranks");
+  gi_context c = nullptr;
+  GI_TRY(gi_context_create(device, cuda_stream, &c));
+  c->rank = rank;
+  c->nranks = nranks;
+  if (nranks > 1) c->comm = make_host_comm(*comm, rank, nranks);
   *out = c;
   return GI_OK;
   GI_GUARD_END

@@ -95,6 +95,7 @@ __global__ void __launch_bounds__(kPullThreads) k_pr_pull(PrArgs A) {
           A.split_cnt[r] = 0;
         }
       });
+  if (A.npeer) __threadfence_system();  // peer stores ordered before the next collective
   const double bs = block_sum(dpart, sred);
   if (tid == 0 && bs != 0.0) atomicAdd(&A.dbuf[(A.it + 1) % 3], bs);
 }
@@ -153,6 +154,7 @@ __global__ void __launch_bounds__(256) k_pr_rows(PrArgs A) {
       if (r < A.n) pr_epilogue(A, r, s[k], dn, dpart);
     }
   }
+  if (A.npeer) __threadfence_system();  // peer stores ordered before the next collective
   const double bs = block_sum(dpart, sred);
   if (threadIdx.x == 0 && bs != 0.0) atomicAdd(&A.dbuf[(A.it + 1) % 3], bs);
 }
@@ -194,6 +196,7 @@ __global__ void __launch_bounds__(256) k_pr_vertex(PrArgs A, double* __restrict_
     acc[v] = 0.0;
     pr_epilogue(A, v, s, dn, dpart);
   }
+  if (A.npeer) __threadfence_system();  // peer stores ordered before the next collective
   const double bs = block_sum(dpart, sred);
   if (threadIdx.x == 0 && bs != 0.0) atomicAdd(&A.dbuf[(A.it + 1) % 3], bs);
 }
@@ -397,16 +400,23 @@ gi_status pagerank_run(gi_graph g, int32_t iters, double damping, const gi_pr_op
     if (nr > 0 && ml > 0) GI_TRY(seg_build(g, o.segment_size, o.dst_block));
     else kernel = GI_PR_PULL_DIRECT;
   }
-  if (dist) {  // every rank must run the same kernel family (collective call sequence)
+  // multi-GPU peer stores: asked for by GI_PR_PEER=1
+  // (=0 forbids them; unset: the comm's default, on only for in-process ranks)
+  const char* peer_env = getenv("GI_PR_PEER");
+  const bool ask_peer = dist && ctx->nranks <= 8 &&
+                        (peer_env ? strcmp(peer_env, "0") != 0 : ctx->comm->peer_stores_default());
+  bool want_peer = false;
+  if (dist) {  // every rank must run the same kernel family and exchange (collective call sequence)
     DevBuf kk;
-    GI_TRY(kk.alloc(sizeof(int32_t)));
-    int32_t mine = kernel == GI_PR_PULL_SEGMENTED ? 1 : 0;
-    GI_CUDA(cudaMemcpyAsync(kk.p, &mine, sizeof(int32_t), cudaMemcpyHostToDevice, st));
-    GI_TRY(ctx->comm->allreduce_i32(kk.as<int32_t>(), 1, st));
-    int32_t all = 0;
-    GI_CUDA(cudaMemcpyAsync(&all, kk.p, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    GI_TRY(kk.alloc(2 * sizeof(int32_t)));
+    int32_t mine[2] = {kernel == GI_PR_PULL_SEGMENTED ? 1 : 0, ask_peer ? 1 : 0};
+    GI_CUDA(cudaMemcpyAsync(kk.p, mine, sizeof mine, cudaMemcpyHostToDevice, st));
+    GI_TRY(ctx->comm->allreduce_i32(kk.as<int32_t>(), 2, st));
+    int32_t all[2] = {0, 0};
+    GI_CUDA(cudaMemcpyAsync(all, kk.p, sizeof all, cudaMemcpyDeviceToHost, st));
     GI_CUDA(cudaStreamSynchronize(st));
-    if (o.direction == GI_PR_PULL && all != 0 && all != ctx->nranks) kernel = GI_PR_PULL_DIRECT;
+    if (o.direction == GI_PR_PULL && all[0] != 0 && all[0] != ctx->nranks) kernel = GI_PR_PULL_DIRECT;
+    want_peer = all[1] == ctx->nranks;  // every rank asked
   }
   S.kernel = kernel;
   // direct pull: thread-per-row kernel when every row is short, else merge-path tiles
@@ -465,19 +475,23 @@ gi_status pagerank_run(gi_graph g, int32_t iters, double damping, const gi_pr_op
   // NVLink, and the per-iteration allgather goes away.
   // The dangling-mass allreduce that follows every vertex pass orders those
   // stores before any rank's next edge pass. GI_PR_PEER=0: allgather path.
-  const char* peer_env = getenv("GI_PR_PEER");
-  const bool want_peer = dist && ctx->nranks <= 8 && !(peer_env && strcmp(peer_env, "0") == 0);
   if (want_peer && g->peer_state == 0) {
+    // both maps always run on every rank (a failed map is agreed on inside)
     gi_status e0 = ctx->comm->peer_map(g->contrib[0].p, g->peer_c[0], g->peer_opened, st);
-    gi_status e1 = e0 == GI_OK ? ctx->comm->peer_map(g->contrib[1].p, g->peer_c[1], g->peer_opened, st) : e0;
-    g->peer_state = e1 == GI_OK ? 1 : -1;
-    if (e1 != GI_OK) peer_unmap(g->peer_opened);
+    gi_status e1 = ctx->comm->peer_map(g->contrib[1].p, g->peer_c[1], g->peer_opened, st);
+    g->peer_state = (e0 == GI_OK && e1 == GI_OK) ? 1 : -1;
+    if (g->peer_state != 1) {
+      peer_unmap(g->peer_opened);
+      set_error("");  // the allgather fallback serves the call: no stale message
+    }
   }
   const bool peer = want_peer && g->peer_state == 1;
-  cudaEvent_t ev[3] = {nullptr, nullptr, nullptr}, tot[2] = {nullptr, nullptr};
+  S.exchange = dist ? (peer ? 2 : 1) : 0;
+  cudaEvent_t ev[3] = {nullptr, nullptr, nullptr}, tot[2] = {nullptr, nullptr}, xev[2] = {nullptr, nullptr};
   if (o.profile) {
     for (int k = 0; k < 3; ++k) GI_CUDA(cudaEventCreate(&ev[k]));
     for (int k = 0; k < 2; ++k) GI_CUDA(cudaEventCreate(&tot[k]));
+    for (int k = 0; k < 2; ++k) GI_CUDA(cudaEventCreate(&xev[k]));
     GI_CUDA(cudaEventRecord(tot[0], st));
   }
   GI_CUDA(cudaMemsetAsync(g->dbuf.p, 0, 4 * sizeof(double), st));
@@ -565,8 +579,16 @@ gi_status pagerank_run(gi_graph g, int32_t iters, double damping, const gi_pr_op
     GI_CUDA(cudaGetLastError());
     S.edge_launches++;
     if (dist) {  // dangling partials (allreduce) + contrib slices (allgatherv)
+      if (o.profile) GI_CUDA(cudaEventRecord(xev[0], st));
       GI_TRY(ctx->comm->allreduce_f64(A.dbuf + (it + 1) % 3, 1, st));
       if (!peer) GI_TRY(ctx->comm->allgatherv(A.cout, cb, st));
+      if (o.profile) {
+        GI_CUDA(cudaEventRecord(xev[1], st));
+        GI_CUDA(cudaEventSynchronize(xev[1]));
+        float xm = 0.f;
+        GI_CUDA(cudaEventElapsedTime(&xm, xev[0], xev[1]));
+        S.exchange_ms += xm;
+      }
       if (it == iters - 1) {
         std::vector<int64_t> rb = cb;
         GI_TRY(ctx->comm->allgatherv(rank_int.p, rb, st));
@@ -594,6 +616,7 @@ gi_status pagerank_run(gi_graph g, int32_t iters, double damping, const gi_pr_op
     S.vertex_ms = vertex_ms;
     for (int k = 0; k < 3; ++k) cudaEventDestroy(ev[k]);
     for (int k = 0; k < 2; ++k) cudaEventDestroy(tot[k]);
+    for (int k = 0; k < 2; ++k) cudaEventDestroy(xev[k]);
   }
   if (stats) *stats = S;
   return GI_OK;

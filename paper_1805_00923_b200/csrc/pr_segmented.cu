@@ -427,6 +427,7 @@ __global__ void __launch_bounds__(256) k_pr_acc(PrArgs A, const float* __restric
     zero[r] = 0.f;
     pr_epilogue(A, r, s, dn, dpart);
   }
+  if (A.npeer) __threadfence_system();  // peer stores ordered before the next collective
   const double bs = block_sum(dpart, sred);
   if (threadIdx.x == 0 && bs != 0.0) atomicAdd(&A.dbuf[(A.it + 1) % 3], bs);
 }

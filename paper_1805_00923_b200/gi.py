@@ -36,6 +36,7 @@ GI_REMOVE_SELF_LOOPS = 1 << 1
 GI_DEDUP = 1 << 2
 GI_SYMMETRIZE = 1 << 3
 GI_NO_RELABEL = 1 << 4
+GI_OFFSETS64 = 1 << 5
 GI_DEFAULT_FLAGS = GI_REMOVE_SELF_LOOPS | GI_DEDUP
 
 GI_PR_PULL, GI_PR_PUSH, GI_PR_PULL_DIRECT, GI_PR_PULL_SEGMENTED, GI_PR_PULL_PARTITIONED = 0, 1, 2, 3, 4
@@ -53,7 +54,20 @@ class gi_pr_opts(ctypes.Structure):
 class gi_pr_stats(ctypes.Structure):
     _fields_ = [("edge_launches", ctypes.c_int32), ("aux_launches", ctypes.c_int32), ("edge_ms", ctypes.c_float),
                 ("total_ms", ctypes.c_float), ("kernel", ctypes.c_int32), ("vertex_ms", ctypes.c_float),
-                ("bytes_alg_per_iter", ctypes.c_int64)]
+                ("bytes_alg_per_iter", ctypes.c_int64), ("exchange", ctypes.c_int32), ("exchange_ms", ctypes.c_float)]
+
+
+GI_DT_INT32, GI_DT_INT64, GI_DT_F64 = 0, 1, 2
+_ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32)
+_ALLGATHERV_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(ctypes.c_int64),
+                                  ctypes.c_int32)
+_ALLTOALLV_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(ctypes.c_int64),
+                                 ctypes.c_void_p, ctypes.POINTER(ctypes.c_int64), ctypes.c_int32)
+
+
+class gi_host_comm(ctypes.Structure):
+    _fields_ = [("user", ctypes.c_void_p), ("allreduce", _ALLREDUCE_FN), ("allgatherv", _ALLGATHERV_FN),
+                ("alltoallv", _ALLTOALLV_FN)]
 
 
 class gi_prdelta_opts(ctypes.Structure):
@@ -103,6 +117,8 @@ _SIGS = {
     "gi_local_group_create": ([ctypes.c_int, ctypes.POINTER(_vp)], _st),
     "gi_local_group_destroy": ([_vp], _st),
     "gi_context_create_local": ([ctypes.c_int, _vp, _vp, ctypes.c_int, ctypes.POINTER(_vp)], _st),
+    "gi_context_create_hostcomm": ([ctypes.c_int, _vp, ctypes.c_int, ctypes.c_int, ctypes.POINTER(gi_host_comm),
+                                    ctypes.POINTER(_vp)], _st),
     "gi_partition_ranges": ([_i64, ctypes.c_int, _vp, _vp], _st),
     "gi_graph_partition": ([_vp, ctypes.POINTER(_i64), ctypes.POINTER(_i64), ctypes.POINTER(_i64)], _st),
     "gi_graph_create": ([_vp, _i64, _i64, _vp, _vp, ctypes.c_uint32, ctypes.POINTER(_vp)], _st),
@@ -207,6 +223,48 @@ def gi_context_create_local(device: int, stream: int | None, grp: int, rank: int
     _check(_lib.gi_context_create_local(device, stream or None, grp, rank, ctypes.byref(out)),
            "gi_context_create_local")
     return out.value
+
+
+def gi_context_create_hostcomm(device: int, stream: int | None, rank: int, nranks: int, comm) -> tuple[int, object]:
+    """comm: an object with allreduce(buf: np.ndarray) (in-place sum; int32 / int64 / float64 view),
+    allgatherv(buf: np.ndarray[uint8], off: list[int]) and alltoallv(send, soff, recv, roff) (uint8 views).
+    Returns (context handle, keep-alive of the callback trampolines)."""
+    dts = {GI_DT_INT32: np.int32, GI_DT_INT64: np.int64, GI_DT_F64: np.float64}
+
+    def _u8(ptr, nbytes):
+        return np.ctypeslib.as_array((ctypes.c_uint8 * max(int(nbytes), 1)).from_address(ptr))[: int(nbytes)] \
+            if nbytes else np.empty(0, np.uint8)
+
+    def ar(_u, buf, count, dtype):
+        try:
+            dt = dts[dtype]
+            comm.allreduce(_u8(buf, count * np.dtype(dt).itemsize).view(dt))
+            return 0
+        except Exception:  # pragma: no cover - reported as GI_ERR_NCCL by the library
+            return 1
+
+    def ag(_u, buf, off, p):
+        try:
+            offs = [off[i] for i in range(p + 1)]
+            comm.allgatherv(_u8(buf, offs[-1]), offs)
+            return 0
+        except Exception:  # pragma: no cover
+            return 1
+
+    def a2a(_u, send, soff, recv, roff, p):
+        try:
+            so = [soff[i] for i in range(p + 1)]
+            ro = [roff[i] for i in range(p + 1)]
+            comm.alltoallv(_u8(send, so[-1]), so, _u8(recv, ro[-1]), ro)
+            return 0
+        except Exception:  # pragma: no cover
+            return 1
+
+    cb = gi_host_comm(None, _ALLREDUCE_FN(ar), _ALLGATHERV_FN(ag), _ALLTOALLV_FN(a2a))
+    out = _vp()
+    _check(_lib.gi_context_create_hostcomm(device, stream or None, rank, nranks, ctypes.byref(cb), ctypes.byref(out)),
+           "gi_context_create_hostcomm")
+    return out.value, (cb, ar, ag, a2a, comm)
 
 
 def gi_partition_ranges(n: int, nranks: int, weight_prefix) -> np.ndarray:
@@ -382,11 +440,16 @@ def gi_bfs_multi(g: int, sources, out=None, policy: int = GI_BFS_AUTO, threshold
 # ------------------------------------------------------------------ RAII conveniences
 class Context:
     def __init__(self, device: int = 0, stream: int | None = None, *, local_group: int | None = None,
-                 rank: int = 0, nccl: tuple | None = None):
-        """local_group: simulated ranks in this process (tests); nccl: (rank, nranks, unique_id)."""
+                 rank: int = 0, nccl: tuple | None = None, hostcomm: tuple | None = None):
+        """local_group: simulated ranks in this process (tests); nccl: (rank, nranks, unique_id);
+        hostcomm: (rank, nranks, comm) with comm as gi_context_create_hostcomm takes it."""
         import weakref
 
-        if local_group is not None:
+        self._keep = None
+        if hostcomm is not None:
+            self.handle, self._keep = gi_context_create_hostcomm(device, stream, hostcomm[0], hostcomm[1],
+                                                                 hostcomm[2])
+        elif local_group is not None:
             self.handle = gi_context_create_local(device, stream, local_group, rank)
         elif nccl is not None:
             self.handle = gi_context_create_dist(device, stream, nccl[0], nccl[1], nccl[2])

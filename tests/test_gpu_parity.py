@@ -21,14 +21,33 @@ PR_L1 = 1e-5
 PR_REL = 1e-4
 
 
-@pytest.fixture(scope="module")
-def gi():
+class _WideOffsets:
+    """The binding with every graph built with GI_OFFSETS64: int64 CSR/CSC offsets, the layout
+    of graphs past 2^31 edges (config 5), so the whole suite also runs the
+    int64-offset kernel instantiations."""
+
+    def __init__(self, mod):
+        self._mod = mod
+
+        class Graph(mod.Graph):
+            def __init__(self, ctx, n, src, dst, flags=mod.GI_DEFAULT_FLAGS):
+                super().__init__(ctx, n, src, dst, flags | mod.GI_OFFSETS64)
+
+        self.Graph = Graph
+        self.wide = True
+
+    def __getattr__(self, k):
+        return getattr(self._mod, k)
+
+
+@pytest.fixture(scope="module", params=["off32", "off64"])
+def gi(request):
     from paper_1805_00923_b200 import build
 
     build.build()
     from paper_1805_00923_b200 import gi as _gi
 
-    return _gi
+    return _WideOffsets(_gi) if request.param == "off64" else _gi
 
 
 @pytest.fixture(scope="module")
@@ -500,6 +519,17 @@ def test_bfs_errors_and_device_output(gi, ctx):
     assert out.cpu().tolist() == [9, 0, 1, 3, 3, 4, 5, 6, 7, 8]
 
 
+def test_offsets_width_takes_effect(gi, ctx):
+    """B_alg = 4m + (o+12)n reports the offset width o the graph was built with."""
+    s, d = graphgen.CONFIGS[1].edges()
+    n = graphgen.CONFIGS[1].n
+    g = gi.Graph(ctx, n, s, d)
+    _, st = g.pagerank(2, 0.85)
+    o = 8 if getattr(gi, "wide", False) else 4
+    assert st.bytes_alg_per_iter == 4 * g.m + (o + 12) * n
+    g.close()
+
+
 # ---------------------------------------------------------------- full-size configs (BASELINE configs[1], [2])
 @pytest.fixture(scope="module")
 def full_graphs():
@@ -526,17 +556,25 @@ def test_full_config_parity(gi, ctx, full_graphs, cfg_idx):
     got = out.cpu().numpy()
     _pr_check(got, want, cfg.name)
     assert abs(got.astype(np.float64).sum() - 1.0) < 1e-5  # mass conserved (uniform rule)
-    sources = cfg.sources(s, d)[:4].tolist() if cfg.source_seed else [0]
+    sources = cfg.sources(s, d).tolist() if cfg.source_seed else [0]
+    # the bench's exact call: every source of the workload (64 on config 2) in one gi_bfs_multi
+    # (AUTO: one bit-parallel pass of 64 sources), all rows validated
+    allp = torch.empty((len(sources), cfg.n), dtype=torch.int32, device="cuda")
+    _, ast = g.bfs_multi(sources, out=allp)
+    few = sources[:4]
     par = torch.empty(cfg.n, dtype=torch.int32, device="cuda")
-    multi = torch.empty((len(sources), cfg.n), dtype=torch.int32, device="cuda")
-    bitp = torch.empty((len(sources), cfg.n), dtype=torch.int32, device="cuda")
-    _, mst = g.bfs_multi(sources, out=multi, batch=gi.GI_BFS_BATCH_PER_SOURCE)
-    _, bst = g.bfs_multi(sources, out=bitp, batch=gi.GI_BFS_BATCH_BITPARALLEL)
+    multi = torch.empty((len(few), cfg.n), dtype=torch.int32, device="cuda")
+    bitp = torch.empty((len(few), cfg.n), dtype=torch.int32, device="cuda")
+    _, mst = g.bfs_multi(few, out=multi, batch=gi.GI_BFS_BATCH_PER_SOURCE)
+    _, bst = g.bfs_multi(few, out=bitp, batch=gi.GI_BFS_BATCH_BITPARALLEL)
     for i, src in enumerate(sources):
-        _, bs = g.bfs(int(src), out=par)
-        depth = oracle.bfs_depth(go, int(src))
-        for what, p, st in (("gi_bfs", par, bs), ("gi_bfs_multi", multi[i], mst[i]),
-                            ("gi_bfs_multi bit-parallel", bitp[i], bst[i])):
+        depth = oracle.bfs_depth_levels(go, int(src))
+        runs = [("gi_bfs_multi (bench call)", allp[i], ast[i])]
+        if i < len(few):
+            _, bs = g.bfs(int(src), out=par)
+            runs += [("gi_bfs", par, bs), ("gi_bfs_multi per-source", multi[i], mst[i]),
+                     ("gi_bfs_multi bit-parallel", bitp[i], bst[i])]
+        for what, p, st in runs:
             ok, msg = oracle.validate_bfs(go, int(src), p.cpu().numpy(), depth)
             assert ok, f"{cfg.name} {what} src={src}: {msg}"
             assert st.edges_traversed == oracle.reached_out_edges(go, depth)
