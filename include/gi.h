@@ -192,7 +192,8 @@ GI_API gi_status gi_graph_csr(gi_graph g, int64_t* off, int32_t* idx);
  * n = 0 -> GI_OK, nothing written. */
 GI_API gi_status gi_pagerank(gi_graph g, int32_t iters, double damping, float* out);
 
-enum { GI_PR_PULL = 0, GI_PR_PUSH = 1, GI_PR_PULL_DIRECT = 2, GI_PR_PULL_SEGMENTED = 3, GI_PR_PULL_PARTITIONED = 4 };
+enum { GI_PR_PULL = 0, GI_PR_PUSH = 1, GI_PR_PULL_DIRECT = 2, GI_PR_PULL_SEGMENTED = 3, GI_PR_PULL_PARTITIONED = 4,
+       GI_PR_PULL_BLOCKED = 5 };
 enum { GI_DANGLING_UNIFORM = 0, GI_DANGLING_DROP = 1 };
 typedef struct {
   int32_t direction; /* GI_PR_PULL (auto-selected pull kernel), GI_PR_PUSH
@@ -201,7 +202,14 @@ typedef struct {
                         GI_PR_PULL_SEGMENTED (shared-memory source segments),
                         GI_PR_PULL_PARTITIONED (the CSC split by source
                         range into L2-sized partitions, one gather pass per
-                        partition: the paper's cache partitioning) */
+                        partition: the paper's cache partitioning),
+                        GI_PR_PULL_BLOCKED (propagation blocking, the
+                        write-side counterpart the paper cites at P:755:
+                        contributions binned by (source chunk, destination
+                        block) in a streaming pass, summed per block in
+                        shared memory in a second; chosen by GI_PR_PULL when
+                        the segmented pull's pieces hold < 2.5 edges and
+                        contrib exceeds 64 MB, e.g. config 5) */
   int32_t dangling;  /* GI_DANGLING_UNIFORM (default) or GI_DANGLING_DROP
                         (paper-literal: no D term) */
   int32_t profile;   /* 1: fill gi_pr_stats kernel timings (CUDA events on the
@@ -381,6 +389,17 @@ GI_API gi_status gi_cc_ex(gi_graph g, const gi_cc_opts* opts, int32_t* labels_ou
 typedef gi_cc_opts gi_sssp_opts;   /* policy, threshold_div (0 -> 20), profile */
 typedef gi_cc_stats gi_sssp_stats; /* rounds, pull_rounds, edges_examined, total_ms, launches */
 GI_API gi_status gi_sssp(gi_graph g, int32_t source, uint64_t weight_seed, int32_t* dist_out);
+/* SSSP over the caller's edge weights (the paper runs SSSP on weighted
+ * datasets):
+ *   weights: int32[m], host or device, one per edge of the CLEANED graph in
+ *     gi_graph_csr's order (input ids: rows by source ascending, neighbours
+ *     ascending within a row); every weight >= 0 (GI_ERR_INVALID_ARGUMENT
+ *     otherwise); every shortest-path length must be < 2^31 - 1.
+ *   dist_out: int32[n] as gi_sssp.
+ * The weights are moved into the library's CSR and CSC order on every call
+ * (one binary search per edge) and replace any cached synthetic weights. */
+GI_API gi_status gi_sssp_weighted(gi_graph g, int32_t source, const int32_t* weights, const gi_sssp_opts* opts,
+                                  int32_t* dist_out, gi_sssp_stats* stats);
 GI_API gi_status gi_sssp_ex(gi_graph g, int32_t source, uint64_t weight_seed, const gi_sssp_opts* opts,
                             int32_t* dist_out, gi_sssp_stats* stats);
 

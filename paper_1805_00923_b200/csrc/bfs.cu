@@ -291,6 +291,15 @@ __global__ void __launch_bounds__(256) k_bfs_pull(const uint32_t* __restrict__ f
   }
 }
 
+// Multi-GPU BFS with peer stores (SURVEY §8(f) NEXT #3 for the frontier): the
+// next-frontier words a rank produces for its owned range are also written into
+// every other rank's replica of the bitmap (mapped through CUDA IPC), so no
+// per-level allgather is needed. np = 0: local bitmap only.
+struct PeerBits {
+  uint32_t* p[7];
+  int np;
+};
+
 // Pull level with the hot prefix of the frontier bitmap staged in shared
 // memory (the north_star's "bitmap staged in shared memory"): vertices are
 // relabelled hottest-first, so the first `sw` words (up to ~1.8 M vertices)
@@ -303,7 +312,8 @@ __global__ void __launch_bounds__(1024, 2) k_bfs_pull_smem(const uint32_t* __res
                                                            const OffT* __restrict__ off,
                                                            const int32_t* __restrict__ idx,
                                                            const int32_t* __restrict__ outdeg, int64_t n, int sw,
-                                                           int64_t* __restrict__ cnext, int64_t r0) {
+                                                           int64_t* __restrict__ cnext, int64_t r0,
+                                                           PeerBits peers) {
   // n = CSC rows held here, r0 = global id of row 0 (a multiple of 32);
   // parent is indexed by local row, fnext / outdeg by global id
   extern __shared__ uint32_t sbits[];
@@ -339,12 +349,13 @@ __global__ void __launch_bounds__(1024, 2) k_bfs_pull_smem(const uint32_t* __res
       }
     }
     const unsigned mask = __ballot_sync(0xffffffffu, found);
-    if (lane == 0) fnext[(r0 >> 5) + w] = mask;
+    if (lane < 1 + peers.np) (lane == 0 ? fnext : peers.p[lane - 1])[(r0 >> 5) + w] = mask;
     if (found) {
       cnt += 1;
       sdeg += __ldg(&outdeg[r0 + v]);
     }
   }
+  if (peers.np) __threadfence_system();  // peer stores ordered before the level's allreduce
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
@@ -717,7 +728,8 @@ static gi_status bfs_impl(gi_graph g, int32_t source, const gi_bfs_opts& o, int3
         const int sw = (int)std::min<int64_t>(words, smem_words);
         k_bfs_pull_smem<OffT><<<2 * sms, 1024, (size_t)sw * 4, st>>>(g->bitmap[bc].as<uint32_t>(),
                                                                  g->bitmap[bc ^ 1].as<uint32_t>(), parent, csc_off,
-                                                                 g->csc_idx.as<int32_t>(), outdeg, n, sw, nxt, 0);
+                                                                 g->csc_idx.as<int32_t>(), outdeg, n, sw, nxt, 0,
+                                                                 PeerBits{});
       }
       bc ^= 1;
       in_bitmap = true;
@@ -821,7 +833,8 @@ __global__ void __launch_bounds__(256) k_dist_push(const int32_t* __restrict__ q
                                                    const long long* __restrict__ pre, long long E,
                                                    const OffT* __restrict__ off, const int32_t* __restrict__ idx,
                                                    const int32_t* __restrict__ outdeg, int32_t* parent, int64_t r0,
-                                                   uint32_t* __restrict__ fnext, int64_t* __restrict__ cnext) {
+                                                   uint32_t* __restrict__ fnext, int64_t* __restrict__ cnext,
+                                                   PeerBits peers) {
   __shared__ FlatSmem sm;
   long long cnt = 0, sdeg = 0;
   flat_edges<OffT>(q, nf, pre, E, off, idx, sm, [&](bool valid, int32_t u, int32_t v) {
@@ -829,11 +842,13 @@ __global__ void __launch_bounds__(256) k_dist_push(const int32_t* __restrict__ q
       int32_t* p = &parent[v - r0];
       if (*(volatile int32_t*)p == -1 && atomicCAS(p, -1, u) == -1) {
         atomicOr(&fnext[v >> 5], 1u << (v & 31));
+        for (int k = 0; k < peers.np; ++k) atomicOr_system(&peers.p[k][v >> 5], 1u << (v & 31));
         cnt += 1;
         sdeg += __ldg(&outdeg[v]);
       }
     }
   });
+  if (peers.np) __threadfence_system();
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
@@ -856,6 +871,8 @@ __global__ void k_dist_init(int32_t s_in, const int32_t* __restrict__ inv, const
 }
 
 }  // namespace
+
+static bool all_peer_ok(gi_graph g, int P, bool ask) { return ask && P > 1 && g->bfs_peer_state == 1; }
 
 template <typename OffT>
 static gi_status bfs_dist_impl(gi_graph g, int32_t source, const gi_bfs_opts& o, int32_t* d_out, gi_bfs_stats* stats) {
@@ -894,11 +911,52 @@ static gi_status bfs_dist_impl(gi_graph g, int32_t source, const gi_bfs_opts& o,
     pslice[p] = g->bounds[p] * 4;
   }
   gi_bfs_stats S{};
-  int bc = 0;
+  // peer stores of the next-frontier words (GI_BFS_PEER=1, or the comm's default;
+  // every rank must ask and every rank must map, agreed by allreduce): a ring of
+  // three bitmaps, so the one a level writes into on every replica was zeroed
+  // by its owner a level earlier, before that level's allreduce (which no rank
+  // passes before every rank has reached it)
+  const char* peer_env = getenv("GI_BFS_PEER");
+  const bool ask = P <= 8 && (peer_env ? strcmp(peer_env, "0") != 0 : C->peer_stores_default());
+  {
+    int64_t mine = ask ? 1 : 0;
+    GI_CUDA(cudaMemcpyAsync(cnt + 2, &mine, sizeof mine, cudaMemcpyHostToDevice, st));
+    GI_TRY(C->allreduce_i64(cnt + 2, 1, st));
+    int64_t all = 0;
+    GI_CUDA(cudaMemcpyAsync(&all, cnt + 2, sizeof all, cudaMemcpyDeviceToHost, st));
+    GI_CUDA(cudaStreamSynchronize(st));
+    if (all == P && g->bfs_peer_state == 0) {
+      bool ok = true;
+      for (int k = 0; k < 3 && ok; ++k) ok = g->bfs_ring[k].alloc((words + 1) * sizeof(uint32_t), /*plain=*/true) == GI_OK;
+      int32_t bad = ok ? 0 : 1;  // every rank reaches the maps' collectives
+      GI_CUDA(cudaMemcpyAsync(cnt + 2, &bad, sizeof bad, cudaMemcpyHostToDevice, st));
+      GI_TRY(C->allreduce_i32(reinterpret_cast<int32_t*>(cnt + 2), 1, st));
+      GI_CUDA(cudaMemcpyAsync(&bad, cnt + 2, sizeof bad, cudaMemcpyDeviceToHost, st));
+      GI_CUDA(cudaStreamSynchronize(st));
+      bool mapped = bad == 0;
+      for (int k = 0; k < 3 && mapped; ++k)
+        mapped = C->peer_map(g->bfs_ring[k].p, g->bfs_peer_bm[k], g->bfs_peer_opened, st) == GI_OK;
+      g->bfs_peer_state = mapped ? 1 : -1;
+      if (!mapped) {
+        peer_unmap(g->bfs_peer_opened);
+        set_error("");  // the allgather serves the call
+      }
+    }
+  }
+  const bool peer = all_peer_ok(g, P, ask);
   GI_CUDA(cudaMemsetAsync(parent, 0xFF, (nr + 1) * sizeof(int32_t), st));
-  GI_CUDA(cudaMemsetAsync(g->bitmap[bc].p, 0, words * sizeof(uint32_t), st));
+  uint32_t* ring[3] = {g->bitmap[0].as<uint32_t>(), g->bitmap[1].as<uint32_t>(), nullptr};
+  if (peer) {
+    for (int k = 0; k < 3; ++k) {
+      ring[k] = g->bfs_ring[k].as<uint32_t>();
+      GI_CUDA(cudaMemsetAsync(ring[k], 0, words * sizeof(uint32_t), st));
+    }
+    GI_TRY(C->barrier(st));  // every replica zeroed before any rank's level-0 stores
+  } else {
+    GI_CUDA(cudaMemsetAsync(ring[0], 0, words * sizeof(uint32_t), st));
+  }
   k_dist_init<<<1, 1, 0, st>>>(source, g->relabeled ? g->inv.as<int32_t>() : nullptr, outdeg, r0, nr, parent,
-                               g->bitmap[bc].as<uint32_t>(), cnt);
+                               ring[0], cnt);
   S.launches++;
   static int smem_words = -1;
   if (smem_words < 0) {
@@ -917,19 +975,28 @@ static gi_status bfs_dist_impl(gi_graph g, int32_t source, const gi_bfs_opts& o,
     if (o.policy == GI_BFS_PUSH_ONLY) pull = false;
     else if (o.policy == GI_BFS_PULL_ONLY) pull = level > 0;
     else pull = (nf + sdeg) > m / div;
+    uint32_t* fcur = peer ? ring[level % 3] : ring[level & 1];
+    uint32_t* fnext = peer ? ring[(level + 1) % 3] : ring[(level + 1) & 1];
+    PeerBits pb{};
+    if (peer) {
+      for (int q = 0; q < P; ++q)
+        if (q != C->rank) pb.p[pb.np++] = static_cast<uint32_t*>(g->bfs_peer_bm[(level + 1) % 3][q]);
+      // the bitmap peers write into two levels from now (see above)
+      GI_CUDA(cudaMemsetAsync(ring[(level + 2) % 3], 0, words * sizeof(uint32_t), st));
+    } else {
+      GI_CUDA(cudaMemsetAsync(fnext, 0, words * sizeof(uint32_t), st));
+    }
     GI_CUDA(cudaMemsetAsync(cnt, 0, 2 * sizeof(int64_t), st));
-    GI_CUDA(cudaMemsetAsync(g->bitmap[bc ^ 1].p, 0, words * sizeof(uint32_t), st));
     if (pull) {
       const int sw = (int)std::min<int64_t>(words, smem_words);
       if (nr > 0)
-        k_bfs_pull_smem<OffT><<<2 * sms, 1024, (size_t)sw * 4, st>>>(g->bitmap[bc].as<uint32_t>(),
-                                                                     g->bitmap[bc ^ 1].as<uint32_t>(), parent, csc_off,
-                                                                     g->csc_idx.as<int32_t>(), outdeg, nr, sw, cnt, r0);
+        k_bfs_pull_smem<OffT><<<2 * sms, 1024, (size_t)sw * 4, st>>>(fcur, fnext, parent, csc_off,
+                                                                     g->csc_idx.as<int32_t>(), outdeg, nr, sw, cnt, r0,
+                                                                     pb);
       S.pull_levels++;
     } else {
       GI_CUDA(cudaMemsetAsync(aux, 0, sizeof(unsigned long long), st));
-      k_b2q<<<grid_for(words, 256, sms), 256, 0, st>>>(g->bitmap[bc].as<uint32_t>(), words, g->queue[0].as<int32_t>(),
-                                                       aux);
+      k_b2q<<<grid_for(words, 256, sms), 256, 0, st>>>(fcur, words, g->queue[0].as<int32_t>(), aux);
       cub::TransformInputIterator<long long, LocalFrontierDegree<OffT>, cub::CountingInputIterator<int64_t>> it(
           cub::CountingInputIterator<int64_t>(0), LocalFrontierDegree<OffT>{csr_off, g->queue[0].as<int32_t>(), nf});
       size_t tb = g->bfs_scan_tmp.bytes;
@@ -940,15 +1007,13 @@ static gi_status bfs_dist_impl(gi_graph g, int32_t source, const gi_bfs_opts& o,
       if (E > 0) {
         const int grid = (int)std::min<int64_t>(ceil_div(E, kFlatCH), (int64_t)sms * 8);
         k_dist_push<OffT><<<grid, 256, 0, st>>>(g->queue[0].as<int32_t>(), nf, g->bfs_pre.as<long long>(), E, csr_off,
-                                                g->csr_idx.as<int32_t>(), outdeg, parent, r0,
-                                                g->bitmap[bc ^ 1].as<uint32_t>(), cnt);
+                                                g->csr_idx.as<int32_t>(), outdeg, parent, r0, fnext, cnt, pb);
       }
       S.launches += 2;
     }
     GI_CUDA(cudaGetLastError());
-    GI_TRY(C->allgatherv(g->bitmap[bc ^ 1].p, wslice, st));
+    if (!peer) GI_TRY(C->allgatherv(fnext, wslice, st));
     GI_TRY(C->allreduce_i64(cnt, 2, st));
-    bc ^= 1;
     S.launches++;
     S.levels++;
   }

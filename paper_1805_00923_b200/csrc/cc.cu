@@ -344,6 +344,33 @@ __global__ void k_edge_weights(const OffT* __restrict__ off, const int32_t* __re
   }
 }
 
+// caller weights (w_user: int32[m] in the input-id CSR order, rows ascending,
+// neighbours ascending) moved to the internal CSR (src_is_row) or CSC layout: a
+// warp per internal row, each edge's input-id CSR position by binary search
+template <typename OffT>
+__global__ void k_map_weights(const OffT* __restrict__ off, const int32_t* __restrict__ idx, int64_t n,
+                              const int32_t* __restrict__ perm, const int64_t* __restrict__ ioff,
+                              const int32_t* __restrict__ iidx, const int32_t* __restrict__ w_user, bool src_is_row,
+                              int32_t* __restrict__ w) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; r < n; r += nw) {
+    const int32_t ri = perm ? __ldg(&perm[r]) : (int32_t)r;
+    for (int64_t e = (int64_t)off[r] + lane; e < (int64_t)off[r + 1]; e += 32) {
+      const int32_t x = __ldg(&idx[e]);
+      const int32_t xi = perm ? __ldg(&perm[x]) : x;
+      const int32_t u = src_is_row ? ri : xi, v = src_is_row ? xi : ri;
+      int64_t lo = ioff[u], hi = ioff[u + 1];
+      while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (__ldg(&iidx[mid]) < v) lo = mid + 1;
+        else hi = mid;
+      }
+      w[e] = __ldg(&w_user[lo]);
+    }
+  }
+}
+
 // host side of graphgen's key: mix64(seed)
 static uint64_t h_mix64(uint64_t z) {
   z += 0x9E3779B97F4A7C15ull;
@@ -354,7 +381,8 @@ static uint64_t h_mix64(uint64_t z) {
 
 // CC (W = false) or SSSP from `source` (W = true, weights drawn with `seed`)
 template <typename OffT, bool W>
-gi_status cc_t(gi_graph g, const gi_cc_opts& o, int32_t source, uint64_t seed, int32_t* d_out, gi_cc_stats* stats) {
+gi_status cc_t(gi_graph g, const gi_cc_opts& o, int32_t source, uint64_t seed, int32_t* d_out, gi_cc_stats* stats,
+               const int32_t* w_user = nullptr) {
   gi_context ctx = g->ctx;
   cudaStream_t st = ctx->stream;
   const int sms = ctx->num_sms;
@@ -386,8 +414,24 @@ gi_status cc_t(gi_graph g, const gi_cc_opts& o, int32_t source, uint64_t seed, i
     seg = true;
     if (!K.acc.p) GI_TRY(K.acc.alloc((n + 64) * 4));
   }
-  if (W) {  // weights of this seed (cached with the graph), dist, frontier {source}
-    if (!K.w_ready || K.w_seed != seed) {
+  if (W) {  // weights of this seed (cached with the graph) or the caller's, dist, frontier {source}
+    if (w_user) {  // explicit weights in input-id CSR order -> internal CSR and CSC order
+      if (!K.wcsr.p) {
+        GI_TRY(K.wcsr.alloc((g->m + 1) * 4));
+        GI_TRY(K.wcsc.alloc((g->m + 1) * 4));
+      }
+      DevBuf ioff, iidx;
+      GI_TRY(csr_input_ids(g, ioff, iidx));
+      k_map_weights<OffT><<<grid_for(n * 32, 256, sms, 16), 256, 0, st>>>(
+          g->csr_off.as<OffT>(), g->csr_idx.as<int32_t>(), n, perm, ioff.as<int64_t>(), iidx.as<int32_t>(), w_user,
+          true, K.wcsr.as<int32_t>());
+      k_map_weights<OffT><<<grid_for(n * 32, 256, sms, 16), 256, 0, st>>>(
+          g->csc_off.as<OffT>(), g->csc_idx.as<int32_t>(), n, perm, ioff.as<int64_t>(), iidx.as<int32_t>(), w_user,
+          false, K.wcsc.as<int32_t>());
+      GI_CUDA(cudaStreamSynchronize(st));  // ioff / iidx are released below
+      launches += 2;
+      K.w_ready = false;  // the cache no longer holds a seed's weights
+    } else if (!K.w_ready || K.w_seed != seed) {
       if (!K.wcsr.p) {
         GI_TRY(K.wcsr.alloc((g->m + 1) * 4));
         GI_TRY(K.wcsc.alloc((g->m + 1) * 4));
@@ -506,10 +550,10 @@ gi_status cc_run(gi_graph g, const gi_cc_opts& o, int32_t* d_out, gi_cc_stats* s
   return g->off64 ? cc_t<int64_t, false>(g, o, 0, 0, d_out, stats) : cc_t<int32_t, false>(g, o, 0, 0, d_out, stats);
 }
 
-gi_status sssp_run(gi_graph g, int32_t source, uint64_t seed, const gi_cc_opts& o, int32_t* d_out,
-                   gi_cc_stats* stats) {
-  return g->off64 ? cc_t<int64_t, true>(g, o, source, seed, d_out, stats)
-                  : cc_t<int32_t, true>(g, o, source, seed, d_out, stats);
+gi_status sssp_run(gi_graph g, int32_t source, uint64_t seed, const int32_t* w_user, const gi_cc_opts& o,
+                   int32_t* d_out, gi_cc_stats* stats) {
+  return g->off64 ? cc_t<int64_t, true>(g, o, source, seed, d_out, stats, w_user)
+                  : cc_t<int32_t, true>(g, o, source, seed, d_out, stats, w_user);
 }
 
 }  // namespace gi

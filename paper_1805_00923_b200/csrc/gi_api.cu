@@ -229,14 +229,16 @@ gi_status gi_graph_destroy(gi_graph g) {
   cudaStreamSynchronize(g->ctx->stream);
   g->ctx->live_graphs--;
   gi_status s = GI_OK;
-  if (g->peer_state == 1 && g->ctx->comm) {
-    // other ranks store into (and map) this rank's contrib buffers: every rank
-    // closes its mappings, and no rank frees before all have (collective)
+  if ((g->peer_state == 1 || g->bfs_peer_state == 1) && g->ctx->comm) {
+    // other ranks store into (and map) this rank's contrib / frontier buffers:
+    // every rank closes its mappings, and no rank frees before all have (collective)
     peer_unmap(g->peer_opened);
+    peer_unmap(g->bfs_peer_opened);
     AllocScope as_(g->ctx->stream);
     s = g->ctx->comm->barrier(g->ctx->stream);
   }
   peer_unmap(g->peer_opened);
+  peer_unmap(g->bfs_peer_opened);
   delete g;  // pooled buffers go back to the pool (stream-ordered frees)
   return s;
 }
@@ -271,6 +273,15 @@ __global__ void k_indeg(const OffT* __restrict__ off, const int32_t* __restrict_
 }
 
 // CSR in input ids: row lengths first (scan on host side of the caller), then
+// *out = min(*out, a[0..n)) (the caller initialises *out)
+__global__ void k_min_i32(const int32_t* __restrict__ a, int64_t n, int32_t* __restrict__ out) {
+  int32_t v = INT32_MAX;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    v = min(v, a[i]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
+  if ((threadIdx.x & 31) == 0 && v != INT32_MAX) atomicMin(out, v);
+}
 // rows copied with ids mapped back and sorted per row.
 template <typename OffT>
 __global__ void k_csr_export(const OffT* __restrict__ off, const int32_t* __restrict__ idx,
@@ -289,8 +300,58 @@ __global__ void k_csr_export(const OffT* __restrict__ off, const int32_t* __rest
 }  // namespace
 }  // namespace gi
 
+
 #include <cub/device/device_scan.cuh>
 #include <cub/device/device_segmented_radix_sort.cuh>
+
+namespace gi {
+// The cleaned CSR in input ids (rows ascending, neighbours ascending):
+// off int64[n+1], idx int32[m], device buffers (gi_graph_csr, explicit SSSP weights).
+gi_status csr_input_ids(gi_graph g, DevBuf& doff, DevBuf& didx) {
+  gi_context ctx = g->ctx;
+  cudaStream_t st = ctx->stream;
+  const int64_t n = g->n, m = g->m;
+  const int sms = ctx->num_sms;
+  DevBuf deg, didx2, tmp;
+  GI_TRY(deg.alloc((n + 1) * sizeof(int32_t)));
+  GI_TRY(doff.alloc((n + 1) * sizeof(int64_t)));
+  GI_TRY(didx.alloc(m * sizeof(int32_t)));
+  GI_TRY(didx2.alloc(m * sizeof(int32_t)));
+  const int32_t* perm = g->relabeled ? g->perm.as<int32_t>() : nullptr;
+  const int32_t* inv = g->relabeled ? g->inv.as<int32_t>() : nullptr;
+  GI_CUDA(cudaMemsetAsync(deg.p, 0, (n + 1) * sizeof(int32_t), st));
+  if (n > 0)
+    k_degree_out<<<grid_for(n, 256, sms), 256, 0, st>>>(g->outdeg.as<int32_t>(), perm, n, deg.as<int32_t>());
+  size_t tb = 0;
+  GI_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, deg.as<int32_t>(), doff.as<int64_t>(), n + 1, st));
+  GI_TRY(tmp.alloc(tb));
+  GI_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb, deg.as<int32_t>(), doff.as<int64_t>(), n + 1, st));
+  if (n > 0 && m > 0) {
+    if (g->off64)
+      k_csr_export<int64_t><<<grid_for(n * 32, 256, sms), 256, 0, st>>>(g->csr_off.as<int64_t>(), g->csr_idx.as<int32_t>(),
+                                                                     perm, inv, n, doff.as<int64_t>(), didx.as<int32_t>());
+    else
+      k_csr_export<int32_t><<<grid_for(n * 32, 256, sms), 256, 0, st>>>(g->csr_off.as<int32_t>(), g->csr_idx.as<int32_t>(),
+                                                                     perm, inv, n, doff.as<int64_t>(), didx.as<int32_t>());
+    if (perm) {  // rows must be ascending in input ids
+      size_t sb = 0;
+      GI_CUDA(cub::DeviceSegmentedRadixSort::SortKeys(nullptr, sb, didx.as<int32_t>(), didx2.as<int32_t>(), m, n,
+                                                      doff.as<int64_t>(), doff.as<int64_t>() + 1, 0, 32, st));
+      DevBuf tmp2;
+      GI_TRY(tmp2.alloc(sb));
+      GI_CUDA(cub::DeviceSegmentedRadixSort::SortKeys(tmp2.p, sb, didx.as<int32_t>(), didx2.as<int32_t>(), m, n,
+                                                      doff.as<int64_t>(), doff.as<int64_t>() + 1, 0, 32, st));
+      GI_CUDA(cudaStreamSynchronize(st));
+      std::swap(didx.p, didx2.p);
+      std::swap(didx.bytes, didx2.bytes);
+      std::swap(didx.pooled, didx2.pooled);
+      std::swap(didx.s, didx2.s);
+    }
+  }
+  GI_CUDA(cudaGetLastError());
+  return GI_OK;
+}
+}  // namespace gi
 
 extern "C" {
 
@@ -343,42 +404,8 @@ gi_status gi_graph_csr(gi_graph g, int64_t* off, int32_t* idx) {
   GI_CUDA(cudaSetDevice(ctx->device));
   AllocScope as_(ctx->stream);
   const int64_t n = g->n, m = g->m;
-  const int sms = ctx->num_sms;
-  DevBuf deg, doff, didx, didx2, tmp;
-  GI_TRY(deg.alloc((n + 1) * sizeof(int32_t)));
-  GI_TRY(doff.alloc((n + 1) * sizeof(int64_t)));
-  GI_TRY(didx.alloc(m * sizeof(int32_t)));
-  GI_TRY(didx2.alloc(m * sizeof(int32_t)));
-  const int32_t* perm = g->relabeled ? g->perm.as<int32_t>() : nullptr;
-  const int32_t* inv = g->relabeled ? g->inv.as<int32_t>() : nullptr;
-  GI_CUDA(cudaMemsetAsync(deg.p, 0, (n + 1) * sizeof(int32_t), st));
-  if (n > 0)
-    k_degree_out<<<grid_for(n, 256, sms), 256, 0, st>>>(g->outdeg.as<int32_t>(), perm, n, deg.as<int32_t>());
-  size_t tb = 0;
-  GI_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, deg.as<int32_t>(), doff.as<int64_t>(), n + 1, st));
-  GI_TRY(tmp.alloc(tb));
-  GI_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb, deg.as<int32_t>(), doff.as<int64_t>(), n + 1, st));
-  if (n > 0 && m > 0) {
-    if (g->off64)
-      k_csr_export<int64_t><<<grid_for(n * 32, 256, sms), 256, 0, st>>>(g->csr_off.as<int64_t>(), g->csr_idx.as<int32_t>(),
-                                                                     perm, inv, n, doff.as<int64_t>(), didx.as<int32_t>());
-    else
-      k_csr_export<int32_t><<<grid_for(n * 32, 256, sms), 256, 0, st>>>(g->csr_off.as<int32_t>(), g->csr_idx.as<int32_t>(),
-                                                                     perm, inv, n, doff.as<int64_t>(), didx.as<int32_t>());
-    if (perm) {  // rows must be ascending in input ids
-      size_t sb = 0;
-      GI_CUDA(cub::DeviceSegmentedRadixSort::SortKeys(nullptr, sb, didx.as<int32_t>(), didx2.as<int32_t>(), m, n,
-                                                      doff.as<int64_t>(), doff.as<int64_t>() + 1, 0, 32, st));
-      DevBuf tmp2;
-      GI_TRY(tmp2.alloc(sb));
-      GI_CUDA(cub::DeviceSegmentedRadixSort::SortKeys(tmp2.p, sb, didx.as<int32_t>(), didx2.as<int32_t>(), m, n,
-                                                      doff.as<int64_t>(), doff.as<int64_t>() + 1, 0, 32, st));
-      GI_CUDA(cudaStreamSynchronize(st));
-      std::swap(didx.p, didx2.p);
-      std::swap(didx.bytes, didx2.bytes);
-    }
-  }
-  GI_CUDA(cudaGetLastError());
+  DevBuf doff, didx;
+  GI_TRY(csr_input_ids(g, doff, didx));
   GI_CUDA(cudaMemcpyAsync(off, doff.p, (n + 1) * sizeof(int64_t), is_device_ptr(off) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
   if (m > 0)
     GI_CUDA(cudaMemcpyAsync(idx, didx.p, m * sizeof(int32_t), is_device_ptr(idx) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
@@ -395,7 +422,7 @@ gi_status gi_pagerank_ex(gi_graph g, int32_t iters, double damping, const gi_pr_
   if (!(damping >= 0.0 && damping <= 1.0)) return fail(GI_ERR_INVALID_ARGUMENT, "gi_pagerank: damping not in [0,1]");
   gi_pr_opts o{};
   if (opts) o = *opts;
-  if (o.direction < GI_PR_PULL || o.direction > GI_PR_PULL_PARTITIONED)
+  if (o.direction < GI_PR_PULL || o.direction > GI_PR_PULL_BLOCKED)
     return fail(GI_ERR_INVALID_ARGUMENT, "gi_pagerank: bad direction");
   if (o.dangling != GI_DANGLING_UNIFORM && o.dangling != GI_DANGLING_DROP)
     return fail(GI_ERR_INVALID_ARGUMENT, "gi_pagerank: bad dangling rule");
@@ -489,7 +516,43 @@ gi_status gi_sssp_ex(gi_graph g, int32_t source, uint64_t weight_seed, const gi_
   OutBuf<int32_t> ob{dist_out, g->n, false, &g->out_stage};
   int32_t* d = nullptr;
   GI_TRY(ob.prepare(g, &d));
-  GI_TRY(sssp_run(g, source, weight_seed, o, d, stats));
+  GI_TRY(sssp_run(g, source, weight_seed, nullptr, o, d, stats));
+  GI_TRY(ob.finish(ctx));
+  return sync(ctx);
+  GI_GUARD_END
+}
+
+gi_status gi_sssp_weighted(gi_graph g, int32_t source, const int32_t* weights, const gi_sssp_opts* opts,
+                           int32_t* dist_out, gi_sssp_stats* stats) {
+  GI_GUARD_BEGIN
+  if (!g) return fail(GI_ERR_INVALID_ARGUMENT, "gi_sssp_weighted: NULL graph");
+  if (!dist_out) return fail(GI_ERR_INVALID_ARGUMENT, "gi_sssp_weighted: NULL output");
+  if (!weights && g->m > 0) return fail(GI_ERR_INVALID_ARGUMENT, "gi_sssp_weighted: NULL weights");
+  if (source < 0 || source >= g->n) return fail(GI_ERR_VERTEX_OUT_OF_RANGE, "gi_sssp_weighted: source not in [0, n)");
+  gi_sssp_opts o{};
+  if (opts) o = *opts;
+  if (o.policy < GI_BFS_AUTO || o.policy > GI_BFS_PULL_ONLY || o.threshold_div < 0)
+    return fail(GI_ERR_INVALID_ARGUMENT, "gi_sssp_weighted: bad options");
+  gi_context ctx = g->ctx;
+  if (ctx->nranks > 1) return fail(GI_ERR_UNSUPPORTED, "gi_sssp_weighted: single-GPU contexts only");
+  GI_CUDA(cudaSetDevice(ctx->device));
+  AllocScope as_(ctx->stream);
+  DevBuf hold, mn;
+  const int32_t* dw = nullptr;
+  GI_TRY(to_device(ctx, weights, g->m, hold, &dw));
+  if (g->m > 0) {  // weights must be >= 0 (the frontier Bellman-Ford's fixed point is then the shortest paths)
+    GI_TRY(mn.alloc(sizeof(int32_t)));
+    GI_CUDA(cudaMemsetAsync(mn.p, 0x7F, sizeof(int32_t), ctx->stream));
+    k_min_i32<<<grid_for(g->m, 256, ctx->num_sms), 256, 0, ctx->stream>>>(dw, g->m, mn.as<int32_t>());
+    int32_t hmin = 0;
+    GI_CUDA(cudaMemcpyAsync(&hmin, mn.p, sizeof hmin, cudaMemcpyDeviceToHost, ctx->stream));
+    GI_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (hmin < 0) return fail(GI_ERR_INVALID_ARGUMENT, "gi_sssp_weighted: negative edge weight");
+  }
+  OutBuf<int32_t> ob{dist_out, g->n, false, &g->out_stage};
+  int32_t* d = nullptr;
+  GI_TRY(ob.prepare(g, &d));
+  GI_TRY(sssp_run(g, source, 0, dw, o, d, stats));
   GI_TRY(ob.finish(ctx));
   return sync(ctx);
   GI_GUARD_END

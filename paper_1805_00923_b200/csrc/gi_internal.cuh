@@ -185,11 +185,22 @@ struct gi_graph_s {
   std::vector<int64_t> sp_m, sp_base, sp_ntiles, sp_tile0;
   gi::DevBuf sp_idx, sp_off, sp_tiles, sp_acc;
   int pr_auto = -1;       // auto-selected pull kernel, decided on first use
+  // propagation-blocked pull (pr_blocked.cu); pb_Ks == 0 until built
+  int pb_Ks = 0, pb_Kd = 0, pb_nitems = 0;
+  int64_t pb_mp = 0;
+  double pb_epp = 0.0;    // edges per segmented-pull piece (the auto choice's statistic)
+  gi::DevBuf pb_rb, pb_tstart, pb_src, pb_dst, pb_vals, pb_items;
   // multi-GPU PageRank with peer stores: every rank's
   // contrib[k] replica as seen from this rank (index = rank; own entry = local)
   int peer_state = 0;                 // 0 unknown, 1 mapped, -1 unavailable (allgather path)
   std::vector<void*> peer_c[2];
   std::vector<void*> peer_opened;     // CUDA IPC mappings to close on destroy
+  // multi-GPU BFS with peer stores: a ring of 3 frontier bitmaps (cudaMalloc, IPC-exported)
+  // and every rank's replicas of them
+  int bfs_peer_state = 0;             // 0 unknown, 1 mapped, -1 unavailable (allgather path)
+  gi::DevBuf bfs_ring[3];
+  std::vector<void*> bfs_peer_bm[3];
+  std::vector<void*> bfs_peer_opened;
   gi::DevBuf out_stage;   // float/int32[n]: output staging in input ids
   // BFS workspace
   gi::DevBuf parent;      // int32[n], internal ids
@@ -238,6 +249,13 @@ gi_status pagerank_run(gi_graph g, int32_t iters, double damping, const gi_pr_op
                        float* d_out_input_ids, gi_pr_stats* stats);
 // pr_segmented.cu
 struct PrArgs;
+// the segment size the segmented pull uses on this device
+gi_status seg_default_Z(gi_graph g, int* Z);
+// pr_blocked.cu: propagation-blocked pull (layout once per graph; one iteration = 2 launches)
+gi_status pb_build(gi_graph g);
+gi_status pb_count_pieces(gi_graph g, int Z, int64_t* pieces);
+// mid: recorded between the scatter and the gather (profiling; may be null)
+gi_status pb_iteration(gi_graph g, const PrArgs& A, cudaEvent_t mid);
 // segment_size / block_rows: 0 = automatic (tests pass small values)
 gi_status seg_build(gi_graph g, int segment_size, int64_t block_rows);
 // merge-path tile rows of a CSC (build.cu); rows: int32[2 * ntiles]
@@ -256,8 +274,12 @@ struct OutdegOf {
   __host__ __device__ __forceinline__ long long operator()(int32_t v) const { return (long long)outdeg[v]; }
 };
 gi_status cc_run(gi_graph g, const gi_cc_opts& o, int32_t* d_out, gi_cc_stats* stats);  // cc.cu
-gi_status sssp_run(gi_graph g, int32_t source, uint64_t seed, const gi_cc_opts& o, int32_t* d_out,
-                   gi_cc_stats* stats);  // cc.cu
+// SSSP weights: synthetic from `seed` (R24), or w_user != nullptr: device int32[m]
+// in the edge order of csr_input_ids / gi_graph_csr
+gi_status sssp_run(gi_graph g, int32_t source, uint64_t seed, const int32_t* w_user, const gi_cc_opts& o,
+                   int32_t* d_out, gi_cc_stats* stats);  // cc.cu
+// the cleaned CSR in input ids on the device (gi_api.cu)
+gi_status csr_input_ids(gi_graph g, DevBuf& doff, DevBuf& didx);
 // the two accumulators: cur holds the sums of the last edge pass; the other is zero
 inline float* seg_acc_buf(gi_graph g, int which) { return g->seg_acc.as<float>() + which * g->seg_acc_stride; }
 // vertex update from the current accumulator; zeroes the other one (never a

@@ -19,11 +19,17 @@
 
 #include <algorithm>
 #include <climits>
+#include <cstdio>
 #include <cstring>
 #include <cub/device/device_scan.cuh>
 
 namespace gi {
 namespace {
+
+// auto choice of the propagation-blocked pull: fewer edges per segmented-pull
+// piece than this, and a contrib vector larger than this (bytes)
+constexpr double kBlockedEpp = 2.5;
+constexpr int64_t kBlockedMinContrib = 64ll << 20;
 
 // ---------------------------------------------------------------- pull, direct gather (K4)
 // Tile b covers merge positions [bT, (b+1)T) of the CSC item sequence
@@ -389,9 +395,47 @@ gi_status pagerank_run(gi_graph g, int32_t iters, double damping, const gi_pr_op
   // direct gather on configs 2, 4 and 5.
   if (kernel == GI_PR_PULL && g->pr_auto >= 0 && !dist) kernel = g->pr_auto;
   if (kernel == GI_PR_PULL) {
-    kernel = (nr > 0 && ml > 0 && g->relabeled && seg_build(g, o.segment_size, o.dst_block) == GI_OK)
-                 ? GI_PR_PULL_SEGMENTED : GI_PR_PULL_DIRECT;
+    // skewed (relabelled) graphs: the segmented pull, unless its (row, segment)
+    // pieces hold so few edges that its one RED per piece dominates (config 5's
+    // flat, symmetrised RMAT: ~1.6 edges per piece) and contrib exceeds what L2
+    // keeps: then the propagation-blocked pull (pr_blocked.cu). Decided from
+    // global counts, so every rank picks the same family.
+    kernel = GI_PR_PULL_DIRECT;
+    if (g->relabeled && o.segment_size == 0) {
+      int Z = 0;
+      int64_t cnt[2] = {0, 0};  // pieces, edges
+      if (nr > 0 && ml > 0 && seg_default_Z(g, &Z) == GI_OK) {
+        GI_TRY(pb_count_pieces(g, Z, &cnt[0]));
+        cnt[1] = ml;
+      }
+      if (dist) {
+        DevBuf cb2;
+        GI_TRY(cb2.alloc(sizeof cnt));
+        GI_CUDA(cudaMemcpyAsync(cb2.p, cnt, sizeof cnt, cudaMemcpyHostToDevice, st));
+        GI_TRY(ctx->comm->allreduce_i64(cb2.as<int64_t>(), 2, st));
+        GI_CUDA(cudaMemcpyAsync(cnt, cb2.p, sizeof cnt, cudaMemcpyDeviceToHost, st));
+        GI_CUDA(cudaStreamSynchronize(st));
+      }
+      static const double epp_min = getenv("GI_PB_EPP") ? atof(getenv("GI_PB_EPP")) : kBlockedEpp;
+      const double epp = cnt[0] > 0 ? (double)cnt[1] / (double)cnt[0] : 1e30;
+      g->pb_epp = epp;
+      if (const char* dbg = getenv("GI_DEBUG_SEG_LAYOUT"))
+        if (FILE* f = fopen(dbg, "a")) {
+          fprintf(f, "auto pull: Z=%d pieces=%lld edges=%lld edges/piece=%.3f\n", Z, (long long)cnt[0],
+                  (long long)cnt[1], epp);
+          fclose(f);
+        }
+      if (epp < epp_min && (int64_t)n * 4 > kBlockedMinContrib && nr > 0 && ml > 0 && pb_build(g) == GI_OK)
+        kernel = GI_PR_PULL_BLOCKED;
+    }
+    if (kernel == GI_PR_PULL_DIRECT && nr > 0 && ml > 0 && g->relabeled &&
+        seg_build(g, o.segment_size, o.dst_block) == GI_OK)
+      kernel = GI_PR_PULL_SEGMENTED;
     if (!dist) g->pr_auto = kernel;
+  }
+  if (kernel == GI_PR_PULL_BLOCKED) {
+    if (nr > 0 && ml > 0) GI_TRY(pb_build(g));
+    else kernel = GI_PR_PULL_DIRECT;
   }
   if (kernel == GI_PR_PULL_PARTITIONED) {
     if (dist || nr == 0 || ml == 0) kernel = GI_PR_PULL_DIRECT;
@@ -408,14 +452,15 @@ gi_status pagerank_run(gi_graph g, int32_t iters, double damping, const gi_pr_op
   bool want_peer = false;
   if (dist) {  // every rank must run the same kernel family and exchange (collective call sequence)
     DevBuf kk;
-    GI_TRY(kk.alloc(2 * sizeof(int32_t)));
-    int32_t mine[2] = {kernel == GI_PR_PULL_SEGMENTED ? 1 : 0, ask_peer ? 1 : 0};
+    GI_TRY(kk.alloc(3 * sizeof(int32_t)));
+    int32_t mine[3] = {kernel == GI_PR_PULL_SEGMENTED ? 1 : 0, ask_peer ? 1 : 0, kernel == GI_PR_PULL_BLOCKED ? 1 : 0};
     GI_CUDA(cudaMemcpyAsync(kk.p, mine, sizeof mine, cudaMemcpyHostToDevice, st));
-    GI_TRY(ctx->comm->allreduce_i32(kk.as<int32_t>(), 2, st));
-    int32_t all[2] = {0, 0};
+    GI_TRY(ctx->comm->allreduce_i32(kk.as<int32_t>(), 3, st));
+    int32_t all[3] = {0, 0, 0};
     GI_CUDA(cudaMemcpyAsync(all, kk.p, sizeof all, cudaMemcpyDeviceToHost, st));
     GI_CUDA(cudaStreamSynchronize(st));
-    if (o.direction == GI_PR_PULL && all[0] != 0 && all[0] != ctx->nranks) kernel = GI_PR_PULL_DIRECT;
+    const bool mixed = (all[0] != 0 && all[0] != ctx->nranks) || (all[2] != 0 && all[2] != ctx->nranks);
+    if (o.direction == GI_PR_PULL && mixed) kernel = GI_PR_PULL_DIRECT;
     want_peer = all[1] == ctx->nranks;  // every rank asked
   }
   S.kernel = kernel;
@@ -535,6 +580,10 @@ gi_status pagerank_run(gi_graph g, int32_t iters, double damping, const gi_pr_op
       if (o.profile) GI_CUDA(cudaEventRecord(ev[1], st));
       k_pr_vertex<<<grid_for(nr, 256, sms), 256, 0, st>>>(A, g->push_sum.as<double>());
       S.aux_launches++;
+    } else if (kernel == GI_PR_PULL_BLOCKED) {  // scatter to bins + gather with fused vertex update
+      GI_TRY(pb_iteration(g, A, o.profile ? ev[2] : nullptr));
+      S.aux_launches++;
+      if (o.profile) GI_CUDA(cudaEventRecord(ev[1], st));
     } else if (kernel == GI_PR_PULL_SEGMENTED) {
       GI_TRY(seg_edge_pass(g, A.cin));
       if (o.profile) GI_CUDA(cudaEventRecord(ev[2], st));
@@ -602,7 +651,7 @@ gi_status pagerank_run(gi_graph g, int32_t iters, double damping, const gi_pr_op
       float ms = 0.f;
       GI_CUDA(cudaEventElapsedTime(&ms, ev[0], ev[1]));
       edge_ms += ms;
-      if (kernel == GI_PR_PULL_SEGMENTED) {
+      if (kernel == GI_PR_PULL_SEGMENTED || kernel == GI_PR_PULL_BLOCKED) {
         GI_CUDA(cudaEventElapsedTime(&ms, ev[2], ev[1]));
         vertex_ms += ms;
       }

@@ -433,6 +433,7 @@ __global__ void __launch_bounds__(256) k_pr_acc(PrArgs A, const float* __restric
 }
 
 
+
 // ---------------------------------------------------------------- layout build
 // row of every CSC edge (warp per row)
 template <typename OffT>
@@ -1031,8 +1032,7 @@ static gi_status seg_upload_ctas(gi_graph g) {
 
 static size_t seg_dyn_smem(int Z) { return (size_t)kStages * kStageBytes + ((size_t)Z + 4) * sizeof(float); }
 
-gi_status seg_build(gi_graph g, int segment_size, int64_t block_rows) {
-  if (segment_size < 0 || block_rows < 0) return fail(GI_ERR_INVALID_ARGUMENT, "segment_size / dst_block < 0");
+gi_status seg_default_Z(gi_graph g, int* Zout) {
   int optin = 0;
   GI_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, g->ctx->device));
   cudaFuncAttributes a{};
@@ -1040,6 +1040,14 @@ gi_status seg_build(gi_graph g, int segment_size, int64_t block_rows) {
   int Z = (optin - (int)a.sharedSizeBytes - 64 - (int)seg_dyn_smem(0)) / 4;
   Z = std::min(Z, 65535) & ~31;
   if (Z < 1024) return fail(GI_ERR_UNSUPPORTED, "segmented pull: not enough shared memory");
+  *Zout = Z;
+  return GI_OK;
+}
+
+gi_status seg_build(gi_graph g, int segment_size, int64_t block_rows) {
+  if (segment_size < 0 || block_rows < 0) return fail(GI_ERR_INVALID_ARGUMENT, "segment_size / dst_block < 0");
+  int Z = 0;
+  GI_TRY(seg_default_Z(g, &Z));
   if (segment_size > 0) Z = std::max(32, std::min(Z, segment_size) & ~3);
   int64_t DB = block_rows > 0 ? block_rows : kDefaultBlockRows;
   DB = std::max<int64_t>(1, std::min<int64_t>(DB, std::max<int64_t>(g->nr, 1)));

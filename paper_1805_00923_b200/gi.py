@@ -39,7 +39,7 @@ GI_NO_RELABEL = 1 << 4
 GI_OFFSETS64 = 1 << 5
 GI_DEFAULT_FLAGS = GI_REMOVE_SELF_LOOPS | GI_DEDUP
 
-GI_PR_PULL, GI_PR_PUSH, GI_PR_PULL_DIRECT, GI_PR_PULL_SEGMENTED, GI_PR_PULL_PARTITIONED = 0, 1, 2, 3, 4
+GI_PR_PULL, GI_PR_PUSH, GI_PR_PULL_DIRECT, GI_PR_PULL_SEGMENTED, GI_PR_PULL_PARTITIONED, GI_PR_PULL_BLOCKED = 0, 1, 2, 3, 4, 5
 GI_DANGLING_UNIFORM, GI_DANGLING_DROP = 0, 1
 GI_BFS_AUTO, GI_BFS_PUSH_ONLY, GI_BFS_PULL_ONLY = 0, 1, 2
 GI_PRD_AUTO, GI_PRD_PUSH_ONLY, GI_PRD_PULL_ONLY = 0, 1, 2
@@ -138,6 +138,7 @@ _SIGS = {
     "gi_cc": ([_vp, _vp], _st),
     "gi_sssp": ([_vp, _i32, ctypes.c_uint64, _vp], _st),
     "gi_sssp_ex": ([_vp, _i32, ctypes.c_uint64, ctypes.POINTER(gi_cc_opts), _vp, ctypes.POINTER(gi_cc_stats)], _st),
+    "gi_sssp_weighted": ([_vp, _i32, _vp, ctypes.POINTER(gi_cc_opts), _vp, ctypes.POINTER(gi_cc_stats)], _st),
     "gi_cc_ex": ([_vp, ctypes.POINTER(gi_cc_opts), _vp, ctypes.POINTER(gi_cc_stats)], _st),
     "gi_bfs_multi": ([_vp, _i32, _vp, ctypes.POINTER(gi_bfs_opts), _vp, ctypes.POINTER(gi_bfs_stats)], _st),
     "gi_status_string": ([_st], ctypes.c_char_p),
@@ -421,6 +422,24 @@ def gi_sssp_ex(g: int, source: int, seed: int, out=None, policy: int = GI_BFS_AU
     return keep, s
 
 
+def gi_sssp_weighted(g: int, source: int, weights, out=None, policy: int = GI_BFS_AUTO, threshold_div: int = 0,
+                     profile: bool = False):
+    """Shortest-path distances from source over caller weights: int32[m] in gi_graph_csr's edge order
+    (input ids, rows and neighbours ascending), all >= 0; -1 = unreachable."""
+    n, m = gi_graph_num_vertices(g), gi_graph_num_edges(g)
+    pw, kw = _ptr(weights, np.int32)
+    if (len(kw) if kw is not None else 0) != m:
+        raise ValueError("one weight per edge of the cleaned graph")
+    if out is None:
+        out = np.empty(n, np.int32)
+    p, keep = _ptr(out, np.int32)
+    o = gi_cc_opts(policy, threshold_div, int(profile), 0)
+    s = gi_cc_stats()
+    _check(_lib.gi_sssp_weighted(g, source, pw or None, ctypes.byref(o), p or None, ctypes.byref(s)),
+           "gi_sssp_weighted")
+    return keep, s
+
+
 def gi_bfs_multi(g: int, sources, out=None, policy: int = GI_BFS_AUTO, threshold_div: int = 0,
                  profile: bool = False, batch: int = GI_BFS_BATCH_AUTO):
     """k BFS runs back to back; out: int32[k, n] (host or device). Returns (out, [stats])."""
@@ -508,6 +527,9 @@ class Graph:
 
     def sssp(self, source, seed=1, out=None, **kw):
         return gi_sssp_ex(self.handle, source, seed, out, **kw)
+
+    def sssp_weighted(self, source, weights, out=None, **kw):
+        return gi_sssp_weighted(self.handle, source, weights, out, **kw)
 
     def bfs_multi(self, sources, out=None, **kw):
         return gi_bfs_multi(self.handle, sources, out, **kw)

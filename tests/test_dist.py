@@ -189,7 +189,7 @@ def _hostcomm_library_worker(rank, world, port, q, peer):
     import sys
     import traceback
 
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), GI_PR_PEER=peer)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), GI_PR_PEER=peer, GI_BFS_PEER=peer)
     try:
         import torch
         import torch.distributed as dist
@@ -211,7 +211,7 @@ def _hostcomm_library_worker(rank, world, port, q, peer):
             g = G.Graph(ctx, n, s[sel].copy(), d[sel].copy())
             if g.m != go.m:
                 bad.append((name, "m", g.m, go.m))
-            for direction in (G.GI_PR_PULL, G.GI_PR_PULL_DIRECT, G.GI_PR_PUSH):
+            for direction in (G.GI_PR_PULL, G.GI_PR_PULL_DIRECT, G.GI_PR_PUSH, G.GI_PR_PULL_BLOCKED):
                 for dg in (0, 1):
                     got, st = g.pagerank(20, 0.85, direction=direction, dangling=dg, profile=True)
                     want = orc.pagerank(go, 20, 0.85, dg)
@@ -303,11 +303,13 @@ CASES = [
 @pytest.mark.parametrize("P", [2, 3, 4])
 @pytest.mark.parametrize("name,n,make", CASES)
 def test_partitioned_pagerank_and_bfs(gi, P, name, n, make, peer, monkeypatch):
-    """peer=1: the vertex update stores each owned row's contrib into every
-    rank's replica (peer stores, SURVEY §8(f) NEXT #3); peer=0: the allgather."""
+    """peer=1: the vertex update stores each owned row's contrib, and the BFS level
+    kernels each owned next-frontier word, into every rank's replica (peer stores,
+    SURVEY §8(f) NEXT #3); peer=0: the allgathers."""
     import torch
 
     monkeypatch.setenv("GI_PR_PEER", peer)
+    monkeypatch.setenv("GI_BFS_PEER", peer)
 
     if not torch.cuda.is_available():
         pytest.fail("needs a CUDA device")
@@ -324,7 +326,7 @@ def test_partitioned_pagerank_and_bfs(gi, P, name, n, make, peer, monkeypatch):
         sel = owner == r
         g = gi.Graph(ctx, n, s[sel], d[sel])
         res = {"m": g.m, "part": g.partition()}
-        for direction in (gi.GI_PR_PULL, gi.GI_PR_PULL_DIRECT, gi.GI_PR_PUSH):
+        for direction in (gi.GI_PR_PULL, gi.GI_PR_PULL_DIRECT, gi.GI_PR_PUSH, gi.GI_PR_PULL_BLOCKED):
             for dg in (0, 1):
                 res[("pr", direction, dg)] = g.pagerank(20, 0.85, direction=direction, dangling=dg)[0]
         res[("pr", "seg-small", 0)] = g.pagerank(20, 0.85, direction=gi.GI_PR_PULL_SEGMENTED, segment_size=1000)[0]

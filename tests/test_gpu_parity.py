@@ -151,12 +151,13 @@ def test_build_device_edges_and_errors(gi, ctx):
 
 
 # ---------------------------------------------------------------- PageRank (a3-a5)
-PR_DIRS = ["pull", "push", "direct", "segmented", "partitioned"]
+PR_DIRS = ["pull", "push", "direct", "segmented", "partitioned", "blocked"]
 
 
 def _dir(gi, name):
     return {"pull": gi.GI_PR_PULL, "push": gi.GI_PR_PUSH, "direct": gi.GI_PR_PULL_DIRECT,
-            "segmented": gi.GI_PR_PULL_SEGMENTED, "partitioned": gi.GI_PR_PULL_PARTITIONED}[name]
+            "segmented": gi.GI_PR_PULL_SEGMENTED, "partitioned": gi.GI_PR_PULL_PARTITIONED,
+            "blocked": gi.GI_PR_PULL_BLOCKED}[name]
 
 
 @pytest.mark.parametrize("direction", PR_DIRS)
@@ -269,6 +270,24 @@ def test_pr_partitioned_many_partitions(gi, ctx, z):
             if go.m > 0:
                 assert st.kernel == gi.GI_PR_PULL_PARTITIONED
             _pr_check(got, oracle.pagerank(go, 20, 0.85, dangling), f"z={z} n={n}")
+
+
+def test_pr_blocked_hub_blocks_and_chunks(gi, ctx):
+    """The propagation-blocked pull where its layout has many source chunks (n > 49152 per
+    chunk), row blocks cut by edge count (a 200k-in-edge hub row, a 30k-leaf in-star) and
+    sparse tiles: against the oracle under both dangling rules."""
+    n = 150_001
+    s0, d0 = graphgen.random_digraph(n, 400_000, 21)
+    hub_src = np.arange(1, 200_001, dtype=np.int32) % n
+    s = np.concatenate([s0, hub_src, np.arange(30_000, dtype=np.int32) + 100_000])
+    d = np.concatenate([d0, np.zeros(len(hub_src), np.int32), np.full(30_000, 99_999, np.int32)])
+    go = oracle.build_graph(n, s, d)
+    g = gi.Graph(ctx, n, s, d)
+    for dg in (0, 1):
+        got, st = g.pagerank(20, 0.85, direction=gi.GI_PR_PULL_BLOCKED, dangling=dg)
+        assert st.kernel == gi.GI_PR_PULL_BLOCKED
+        _pr_check(got, oracle.pagerank(go, 20, 0.85, dg), f"blocked dangling={dg}")
+    g.close()
 
 
 def test_pr_device_output_and_damping_edges(gi, ctx):
@@ -703,6 +722,52 @@ def test_sssp_parity(gi, ctx, policy):
                 got, st = g.sssp(src, seed=seed, policy=_pol(gi, policy))
                 assert (got.astype(np.int64) == want).all(), \
                     f"{name} seed={seed} src={src} {policy}: {int((got != want).sum())} distances differ"
+        g.close()
+
+
+@pytest.mark.parametrize("policy", POLICIES)
+def test_sssp_weighted_parity(gi, ctx, policy):
+    """gi_sssp_weighted (the caller's weights, gi_graph_csr's edge order) == Dijkstra on the
+    oracle's graph: random weights in [0, 1000] (zeros included), heavy-tailed weights, and
+    graphgen's weights (which must also reproduce gi_sssp with that seed)."""
+    import torch
+
+    cfg = graphgen.CONFIGS[1]
+    s1, d1 = cfg.edges()
+    s3, d3 = graphgen.grid(64, 64, 0.2, 9)
+    cases = [("config1", cfg.n, s1, d1, False, [0, 5]), ("config1-sym", cfg.n, s1, d1, True, [7]),
+             ("grid64", 64 * 64, s3, d3, False, [0, 2000]),
+             ("random", 3001, *graphgen.random_digraph(3001, 30000, 5), False, [0, 3000])]
+    rng = np.random.default_rng(11)
+    for name, n, s, d, sym, srcs in cases:
+        flags = gi.GI_DEFAULT_FLAGS | (gi.GI_SYMMETRIZE if sym else 0)
+        g = gi.Graph(ctx, n, s, d, flags)
+        go = oracle.build_graph(n, s, d, symmetrize=sym)
+        off, idx = g.csr()
+        assert np.array_equal(off, go.csr_off) and np.array_equal(idx, go.csr_idx)  # the documented order
+        for kind in ("uniform", "heavy", "graphgen"):
+            if kind == "uniform":
+                w = rng.integers(0, 1001, go.m).astype(np.int32)
+            elif kind == "heavy":
+                w = np.minimum(rng.pareto(1.2, go.m) * 50, 1e6).astype(np.int32)
+            else:
+                w = oracle.csr_weights(go, 5)
+            for src in srcs:
+                want = oracle.sssp(go, src, w)
+                for where in ("host", "device"):
+                    ww = w if where == "host" else torch.from_numpy(w).cuda()
+                    got, _ = g.sssp_weighted(src, ww, policy=_pol(gi, policy))
+                    assert (got.astype(np.int64) == want).all(), \
+                        f"{name} {kind} src={src} {policy} {where}: {int((got != want).sum())} differ"
+                if kind == "graphgen":
+                    got2, _ = g.sssp(src, seed=5, policy=_pol(gi, policy))
+                    assert (got2.astype(np.int64) == want).all()
+        bad = np.zeros(go.m, np.int32)
+        bad[go.m // 2] = -1
+        with pytest.raises(gi.GiError):
+            g.sssp_weighted(0, bad)
+        with pytest.raises(ValueError):
+            g.sssp_weighted(0, bad[:-1])
         g.close()
 
 
