@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <new>
 #include <string>
 
@@ -29,6 +30,80 @@ gi_status cuda_fail(cudaError_t e, const char* what, const char* file, int line)
   t_last_error = buf;
   if (e == cudaErrorMemoryAllocation) return GI_ERR_OUT_OF_MEMORY;
   return GI_ERR_CUDA;
+}
+
+// ---------------------------------------------------------------- big-buffer cache (gi_internal.cuh)
+namespace {
+struct BigEntry {
+  void* p;
+  size_t bytes;
+  cudaStream_t s;
+  int dev;
+};
+std::mutex g_big_mu;
+std::vector<BigEntry> g_big;
+size_t g_big_total = 0;
+size_t big_cap() {
+  static const size_t v = (getenv("GI_BIGCACHE_GB") ? (size_t)atoll(getenv("GI_BIGCACHE_GB")) : 64) << 30;
+  return v;
+}
+}  // namespace
+
+void* big_cache_get(size_t nbytes, cudaStream_t s, size_t* got) {
+  int dev = -1;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(g_big_mu);
+  int best = -1;
+  for (int i = 0; i < (int)g_big.size(); ++i) {
+    const BigEntry& e = g_big[i];
+    if (e.s == s && e.dev == dev && e.bytes >= nbytes && e.bytes <= 2 * nbytes &&
+        (best < 0 || e.bytes < g_big[best].bytes))
+      best = i;
+  }
+  if (best < 0) return nullptr;
+  void* p = g_big[best].p;
+  *got = g_big[best].bytes;
+  g_big_total -= g_big[best].bytes;
+  g_big.erase(g_big.begin() + best);
+  return p;
+}
+
+void big_cache_put(void* p, size_t bytes, cudaStream_t s) {
+  int dev = -1;
+  cudaGetDevice(&dev);
+  std::vector<void*> drop;
+  {
+    std::lock_guard<std::mutex> lk(g_big_mu);
+    if (bytes > big_cap()) {
+      drop.push_back(p);
+    } else {
+      while (g_big_total + bytes > big_cap() && !g_big.empty()) {  // oldest first
+        drop.push_back(g_big.front().p);
+        g_big_total -= g_big.front().bytes;
+        g_big.erase(g_big.begin());
+      }
+      g_big.push_back(BigEntry{p, bytes, s, dev});
+      g_big_total += bytes;
+    }
+  }
+  for (void* q : drop) cudaFree(q);
+}
+
+void big_cache_flush(cudaStream_t s) {
+  int dev = -1;
+  cudaGetDevice(&dev);
+  std::vector<void*> drop;
+  {
+    std::lock_guard<std::mutex> lk(g_big_mu);
+    for (int i = (int)g_big.size() - 1; i >= 0; --i)
+      if (g_big[i].dev == dev && (!s || g_big[i].s == s)) {
+        drop.push_back(g_big[i].p);
+        g_big_total -= g_big[i].bytes;
+        g_big.erase(g_big.begin() + i);
+      }
+  }
+  if (!drop.empty()) cudaDeviceSynchronize();  // blocks of other streams may still be in use
+  for (void* q : drop) cudaFree(q);
 }
 
 static bool is_device_ptr(const void* p) {
@@ -146,7 +221,7 @@ gi_status gi_context_create(int device, void* cuda_stream, gi_context* out) {
   if (pool_enabled()) {  // keep freed blocks cached (up to kPoolKeep) for the next graph or layout build
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
-      uint64_t keep = kPoolKeep;
+      uint64_t keep = pool_keep();
       cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
     }
     cudaGetLastError();
@@ -168,6 +243,7 @@ gi_status gi_context_destroy(gi_context ctx) {
     return fail(GI_ERR_INVALID_ARGUMENT, "gi_context_destroy: destroy the context's graphs first");
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
+  big_cache_flush(ctx->stream);  // the stream's cached blocks (the stream may be destroyed below)
   delete ctx->comm;
   ctx->comm = nullptr;
   if (ctx->nccl_comm) {
@@ -344,7 +420,9 @@ gi_status csr_input_ids(gi_graph g, DevBuf& doff, DevBuf& didx) {
       GI_CUDA(cudaStreamSynchronize(st));
       std::swap(didx.p, didx2.p);
       std::swap(didx.bytes, didx2.bytes);
+      std::swap(didx.cap, didx2.cap);
       std::swap(didx.pooled, didx2.pooled);
+      std::swap(didx.cached, didx2.cached);
       std::swap(didx.s, didx2.s);
     }
   }

@@ -43,10 +43,18 @@ gi_status cuda_fail(cudaError_t e, const char* what, const char* file, int line)
 // build, and a graph's buffers after gi_graph_destroy, are reused instead of
 // going back to cudaMalloc / cudaFree. AllocScope sets the stream for the
 // calling thread; outside a scope (or with GI_POOL=0) DevBuf uses cudaMalloc.
-constexpr uint64_t kPoolKeep = 16ull << 30;
+constexpr uint64_t kPoolKeepDefault = 16ull << 30;
+inline uint64_t pool_keep() {  // GI_POOL_KEEP_GB overrides (A/B runs)
+  static const uint64_t v = getenv("GI_POOL_KEEP_GB") ? (uint64_t)atoll(getenv("GI_POOL_KEEP_GB")) << 30 : kPoolKeepDefault;
+  return v;
+}
 // larger buffers (the temporaries of a billion-edge build) use cudaMalloc: the
 // pool would release and re-map them around every synchronisation
-constexpr size_t kPoolMaxBlock = 2ull << 30;
+constexpr size_t kPoolMaxBlockDefault = 2ull << 30;
+inline size_t pool_max_block() {  // GI_POOL_MAX_GB overrides (A/B runs)
+  static const size_t v = getenv("GI_POOL_MAX_GB") ? (size_t)atoll(getenv("GI_POOL_MAX_GB")) << 30 : kPoolMaxBlockDefault;
+  return v;
+}
 inline cudaStream_t& tl_alloc_stream() {
   static thread_local cudaStream_t s = nullptr;
   return s;
@@ -63,11 +71,25 @@ struct AllocScope {
   AllocScope& operator=(const AllocScope&) = delete;
 };
 
+// Large buffers (above the pool's block limit: the temporaries of a
+// billion-edge build or layout build) are cudaMalloc'd; freeing one returns it
+// to a per-process cache keyed by (device, stream) instead of cudaFree, and an
+// allocation on the same stream reuses a cached block of 1 to 2x its size.
+// Reuse is stream-ordered (every user of a block is on the same stream), so no
+// synchronisation is needed; cudaMalloc / cudaFree of multi-GB blocks cost
+// 10-400 ms each and stall the device (DESIGN §6 e2e). The cache holds at most
+// GI_BIGCACHE_GB (default 64) GB, is emptied when an allocation fails, and the
+// blocks of a stream are freed when its context is destroyed.
+void* big_cache_get(size_t nbytes, cudaStream_t s, size_t* got);
+void big_cache_put(void* p, size_t bytes, cudaStream_t s);
+void big_cache_flush(cudaStream_t s);  // s = nullptr: every stream of the current device
+
 struct DevBuf {
   void* p = nullptr;
   size_t bytes = 0;
-  cudaStream_t s = nullptr;  // stream of a pooled allocation (freed on it)
+  cudaStream_t s = nullptr;  // stream of a pooled / cached allocation (freed on / returned for it)
   bool pooled = false;
+  bool cached = false;       // a large block owned by the big-buffer cache protocol
   DevBuf() = default;
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
@@ -75,35 +97,58 @@ struct DevBuf {
   void reset() {
     if (p) {
       if (pooled) cudaFreeAsync(p, s);
+      else if (cached) big_cache_put(p, cap, s);
       else cudaFree(p);
     }
     p = nullptr;
     bytes = 0;
+    cap = 0;
     pooled = false;
+    cached = false;
   }
   // plain = true: always cudaMalloc (memory that is exported to peers by CUDA IPC)
   gi_status alloc(size_t nbytes, bool plain = false) {
     reset();
     if (nbytes == 0) nbytes = 16;
     const cudaStream_t st = tl_alloc_stream();
-    cudaError_t e;
-    if (!plain && st && pool_enabled() && nbytes <= kPoolMaxBlock) {
+    cudaError_t e = cudaSuccess;
+    if (!plain && st && pool_enabled() && nbytes <= pool_max_block()) {
       e = cudaMallocAsync(&p, nbytes, st);
       pooled = e == cudaSuccess;
       s = st;
+    } else if (!plain && st && pool_enabled()) {
+      size_t got = 0;
+      p = big_cache_get(nbytes, st, &got);
+      if (!p) {
+        e = cudaMalloc(&p, nbytes);
+        if (e != cudaSuccess) {  // memory held by the cache: release it and retry once
+          cudaGetLastError();
+          big_cache_flush(nullptr);
+          e = cudaMalloc(&p, nbytes);
+        }
+        got = nbytes;
+      }
+      if (e == cudaSuccess) {
+        cached = true;
+        cap = got;
+        s = st;
+      }
     } else {
       e = cudaMalloc(&p, nbytes);
     }
     if (e != cudaSuccess) {
       p = nullptr;
       pooled = false;
+      cached = false;
       cudaGetLastError();
       return fail(GI_ERR_OUT_OF_MEMORY, "cudaMalloc of " + std::to_string(nbytes) + " bytes failed: " +
                                             cudaGetErrorString(e));
     }
     bytes = nbytes;
+    if (!cached) cap = nbytes;
     return GI_OK;
   }
+  size_t cap = 0;  // bytes of the underlying block (>= bytes for a reused cached block)
   template <typename T>
   T* as() const { return static_cast<T*>(p); }
 };
@@ -222,6 +267,7 @@ struct gi_graph_s {
   unsigned bfs_epoch = 0;
   struct {  // bit-parallel multi-source BFS (msbfs.cu)
     gi::DevBuf seen, fr[2], act[2], cnt, src, heavy, par, par8, hidx, csc_in;
+    gi::DevBuf fc;       // the frontier masks narrowed to 16 / 32 bits for the pull gathers (k <= 32)
     int64_t nheavy = 0;  // rows with in-degree >= 32 (pulled by whole warps)
     gi::DevBuf hch;      // their chunks: int2 (row, first in-edge offset)
     int64_t nhch = 0;

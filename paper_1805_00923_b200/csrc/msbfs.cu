@@ -87,6 +87,9 @@ struct MsArgs {
   const int32_t* __restrict__ inv;   // input -> internal id
   unsigned long long* seen;
   const unsigned long long* __restrict__ fcur;
+  const void* fc;                    // the frontier masks the pull levels gather: fcur itself, or a copy
+                                     //   narrowed to 16 / 32 bits when k <= 16 / 32 (4x / 2x smaller, so a
+                                     //   billion-edge graph's gathered array stays in L2)
   unsigned long long* fnext;
   const int32_t* __restrict__ acur;  // active vertices of the current level (push)
   int32_t* anext;                    // active vertices of the next level
@@ -206,7 +209,18 @@ __device__ __forceinline__ void ms_counters(const MsArgs& A, long long deg, unsi
   }
 }
 
-template <typename OffT>
+// narrowed frontier masks for the pull gathers (k <= 8 * sizeof(FM) sources)
+template <typename FM>
+__global__ void k_ms_narrow(const unsigned long long* __restrict__ f, int64_t n, FM* __restrict__ out) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x)
+    out[v] = (FM)f[v];
+}
+template <typename FM>
+__device__ __forceinline__ unsigned long long ms_fget(const MsArgs& A, int32_t v) {
+  return (unsigned long long)reinterpret_cast<const FM*>(A.fc)[v];
+}
+
+template <typename OffT, typename FM>
 __global__ void __launch_bounds__(kMsT) k_ms_pull(MsArgs A) {
   __shared__ int32_t s_buf[kMsT / 32][64];  // per-warp staging of the rows joining the next frontier
   int32_t* wbuf = s_buf[threadIdx.x >> 5];
@@ -228,7 +242,7 @@ __global__ void __launch_bounds__(kMsT) k_ms_pull(MsArgs A) {
 #pragma unroll
           for (int j = 0; j < kPullBatch; ++j) v[j] = e + j < e1 ? ms_idx(&A.csc_idx[e + j]) : -1;
 #pragma unroll
-          for (int j = 0; j < kPullBatch; ++j) f[j] = v[j] >= 0 ? A.fcur[v[j]] : 0ull;
+          for (int j = 0; j < kPullBatch; ++j) f[j] = v[j] >= 0 ? ms_fget<FM>(A, v[j]) : 0ull;
           exam += min((int64_t)kPullBatch, e1 - e);
 #pragma unroll
           for (int j = 0; j < kPullBatch; ++j) {
@@ -280,7 +294,7 @@ __device__ __forceinline__ unsigned warp_transpose32(unsigned x) {
   return x;
 }
 
-template <typename OffT>
+template <typename OffT, typename FM>
 __global__ void __launch_bounds__(kMsT) k_ms_pull_heavy(MsArgs A, const int2* __restrict__ hch, int64_t C) {
   __shared__ int32_t s_buf[kMsT / 32][32];  // per-warp staging of the rows joining the next frontier
   const OffT* __restrict__ off = static_cast<const OffT*>(A.csc_off);
@@ -314,7 +328,7 @@ __global__ void __launch_bounds__(kMsT) k_ms_pull_heavy(MsArgs A, const int2* __
           v[j] = e < e1 ? ms_idx(&A.csc_idx[e]) : -1;
         }
 #pragma unroll
-        for (int j = 0; j < kPullBatch; ++j) f[j] = v[j] >= 0 ? A.fcur[v[j]] : 0ull;
+        for (int j = 0; j < kPullBatch; ++j) f[j] = v[j] >= 0 ? ms_fget<FM>(A, v[j]) : 0ull;
         if (lane == 0) exam += min((int64_t)32 * kPullBatch, e1 - b);
 #pragma unroll
         for (int j = 0; j < kPullBatch; ++j) {
@@ -731,6 +745,7 @@ gi_status msbfs_t(gi_graph g, int32_t k, const int32_t* sources, const gi_bfs_op
   while ((1 << lkp) < k) ++lkp;
   const int kp = 1 << lkp;
   if (M.par.bytes < (size_t)(M.nheavy + 1) * kp * 4) GI_TRY(M.par.alloc((size_t)(M.nheavy + 1) * kp * 4));
+  if (k <= 32 && M.fc.bytes < (size_t)(n + 1) * (k <= 16 ? 2 : 4)) GI_TRY(M.fc.alloc((size_t)(n + 1) * (k <= 16 ? 2 : 4)));
   cudaEvent_t e0 = nullptr, e1 = nullptr, pe0 = nullptr, pe1 = nullptr;
   int64_t pull_examined = 0;
   float pull_ms = 0.f;
@@ -791,14 +806,29 @@ gi_status msbfs_t(gi_graph g, int32_t k, const int32_t* sources, const gi_bfs_op
                                                    : (o.policy == GI_BFS_AUTO && nact + sdeg > mdiv);
     if (pull && o.profile) GI_CUDA(cudaEventRecord(pe0, st));
     if (pull) {
-      k_ms_pull<OffT><<<grid_for(n, kMsT, sms, kLightPerSM), kMsT, 0, st>>>(A);
-      if (M.nhch > 0) {
-        // a few chunks per warp and many CTAs: the block scheduler balances the uneven chunks
-        const int64_t hw = (M.nhch + kHeavyPer - 1) / kHeavyPer;
-        k_ms_pull_heavy<OffT><<<(unsigned)std::max<int64_t>(1, (hw + kMsT / 32 - 1) / (kMsT / 32)), kMsT, 0, st>>>(
-            A, M.hch.as<int2>(), M.nhch);
+      const int fw = k <= 16 ? 2 : k <= 32 ? 4 : 8;  // bytes per gathered frontier mask
+      const int lg = grid_for(n, kMsT, sms, kLightPerSM);
+      const int64_t hw = (M.nhch + kHeavyPer - 1) / kHeavyPer;
+      const unsigned hg = (unsigned)std::max<int64_t>(1, (hw + kMsT / 32 - 1) / (kMsT / 32));
+      // a few chunks per warp and many CTAs: the block scheduler balances the uneven chunks
+      if (fw == 8) {
+        A.fc = A.fcur;
+        k_ms_pull<OffT, unsigned long long><<<lg, kMsT, 0, st>>>(A);
+        if (M.nhch > 0) k_ms_pull_heavy<OffT, unsigned long long><<<hg, kMsT, 0, st>>>(A, M.hch.as<int2>(), M.nhch);
+      } else if (fw == 4) {
+        k_ms_narrow<uint32_t><<<grid_for(n, 256, sms, 8), 256, 0, st>>>(A.fcur, n, M.fc.as<uint32_t>());
+        A.fc = M.fc.p;
+        k_ms_pull<OffT, uint32_t><<<lg, kMsT, 0, st>>>(A);
+        if (M.nhch > 0) k_ms_pull_heavy<OffT, uint32_t><<<hg, kMsT, 0, st>>>(A, M.hch.as<int2>(), M.nhch);
+        ++launches;
+      } else {
+        k_ms_narrow<uint16_t><<<grid_for(n, 256, sms, 8), 256, 0, st>>>(A.fcur, n, M.fc.as<uint16_t>());
+        A.fc = M.fc.p;
+        k_ms_pull<OffT, uint16_t><<<lg, kMsT, 0, st>>>(A);
+        if (M.nhch > 0) k_ms_pull_heavy<OffT, uint16_t><<<hg, kMsT, 0, st>>>(A, M.hch.as<int2>(), M.nhch);
         ++launches;
       }
+      if (M.nhch > 0) ++launches;
       if (o.profile) GI_CUDA(cudaEventRecord(pe1, st));
       ++pulls;
     } else {

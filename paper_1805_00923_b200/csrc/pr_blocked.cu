@@ -14,7 +14,7 @@
 //
 //   tile (s, d) = the in-edges whose source lies in chunk s (C consecutive
 //   sources, staged in shared memory) and whose destination lies in row block
-//   d (at most C rows, at most ~2 m / (rows / C) edges: blocks are cut by edge
+//   d (at most B rows, at most ~2 m / (rows / B) edges: blocks are cut by edge
 //   count too, so hub rows do not make one block the whole pass). Tiles are laid
 //   out chunk-major, [s][d], each padded to a multiple of 8 edges:
 //     src16[e]  = source - s*C (16 bits; C for padding: the zero slot)
@@ -26,9 +26,12 @@
 //                 streaming map (2 B read + 4 B written per edge).
 //   k_pb_gather   CTA per row block d: acc[rows] in shared memory; the block's
 //                 runs (s, d) over all s, flattened into one group space split
-//                 evenly over the warps, added with shared-memory atomics
-//                 (4 B + 2 B read per edge); then the fused vertex update a3
-//                 (pr_epilogue) for the block's rows.
+//                 evenly over the warps (4 B + 2 B read per edge), runs of one
+//                 destination summed in registers and across lanes, then added
+//                 as 64-bit fixed point with native 32-bit shared atomics (low
+//                 word + carry into the high word: exact integer sums, where
+//                 an fp32 shared atomic add is a CAS loop); then the fused
+//                 vertex update a3 (pr_epilogue) for the block's rows.
 // 12 bytes per edge of HBM traffic, all sequential, instead of one random
 // 32-byte sector (gather) or one random RED (segmented) per edge.
 #include <algorithm>
@@ -44,7 +47,8 @@ namespace gi {
 namespace {
 
 constexpr int kPbThreads = 1024;
-constexpr int kPbC = 49152;          // sources per chunk = rows per block (16-bit local ids, 192 KB of smem)
+constexpr int kPbC = 49152;          // sources per chunk (16-bit local ids; 192 KB of staged contrib)
+constexpr int kPbB = 24576;          // rows per block (two 32-bit accumulator words per row: 192 KB)
 constexpr int kPbMaxChunks = 2048;   // k_pb_gather keeps one run start + prefix per chunk in smem
 constexpr int kPbGroup = 8;          // edges per group (one 16-byte index load, two 16-byte value stores)
 
@@ -106,14 +110,28 @@ __global__ void __launch_bounds__(kPbThreads, 1) k_pb_scatter(PbArgs P) {
 // phase 2: CTA per row block; acc in smem, runs (s, d) flattened over the warps,
 // then the fused vertex update of the block's rows
 __global__ void __launch_bounds__(kPbThreads, 1) k_pb_gather(PbArgs P, PrArgs A) {
-  extern __shared__ __align__(16) float acc[];  // kPbC + 4 floats | Ks + 1 int32 prefix | Ks int64 starts
+  // row sums as 64-bit fixed point (2^-62 units, exact integer adds) in two 32-bit words:
+  // shared memory has a native 32-bit atomic add but none for fp32 (a CAS loop)
+  extern __shared__ __align__(16) uint32_t lo[];  // kPbB + 4 low words | kPbB + 4 high words | prefix | starts
   __shared__ double sred[32];
-  int32_t* pre = reinterpret_cast<int32_t*>(acc + kPbC + 4);
+  uint32_t* hi = lo + kPbB + 4;
+  int32_t* pre = reinterpret_cast<int32_t*>(hi + kPbB + 4);
   int64_t* rs = reinterpret_cast<int64_t*>(pre + ((P.Ks + 2) & ~1));
   const int d = blockIdx.x;
   const int64_t r0 = P.rb[d], nrow = P.rb[d + 1] - r0;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int i = tid; i <= kPbC; i += kPbThreads) acc[i] = 0.f;
+  for (int i = tid; i <= kPbB; i += kPbThreads) {
+    lo[i] = 0u;
+    hi[i] = 0u;
+  }
+  // add X >= 0 (X * 2^62 < 2^64: a row's sum never exceeds the total rank mass 1)
+  auto add = [&](uint32_t k, float X) {
+    const unsigned long long x = __float2ull_rn(X * 0x1p62f);
+    const uint32_t l = (uint32_t)x, h = (uint32_t)(x >> 32);
+    const uint32_t old = atomicAdd(&lo[k], l);
+    const uint32_t c = (uint32_t)(old + l < old);  // carry out of the low word
+    if (h + c) atomicAdd(&hi[k], h + c);
+  };
   // group counts of the block's runs, then an exclusive prefix (one warp)
   for (int s = tid; s < P.Ks; s += kPbThreads) {
     const int64_t a = P.tstart[(int64_t)s * P.Kd + d], b = P.tstart[(int64_t)s * P.Kd + d + 1];
@@ -151,8 +169,7 @@ __global__ void __launch_bounds__(kPbThreads, 1) k_pb_gather(PbArgs P, PrArgs A)
     }
     s = lo;
   }
-  // two groups per lane in flight: the next group's loads are issued before this
-  // group's shared-memory atomics (CAS loops: fp32 has no native shared add)
+  // the next group's loads are issued before this group's shared-memory atomics
   auto locate = [&](int32_t g) -> int64_t {
     while (pre[s + 1] <= g) ++s;  // the run (s, d) holding group g (monotone within the lane)
     return rs[s] + (int64_t)(g - pre[s]) * kPbGroup;
@@ -190,7 +207,7 @@ __global__ void __launch_bounds__(kPbThreads, 1) k_pb_gather(PbArgs P, PrArgs A)
         if (k8[k] == key) {
           X += v8[k];
         } else {
-          atomicAdd(&acc[key], X);
+          add(key, X);
           key = k8[k];
           X = v8[k];
         }
@@ -206,7 +223,7 @@ __global__ void __launch_bounds__(kPbThreads, 1) k_pb_gather(PbArgs P, PrArgs A)
       if (lane >= o && ((heads >> (lane - o + 1)) & ((1u << o) - 1u)) == 0u) X += y;
     }
     const bool last = lane == 31 || ((heads >> (lane + 1)) & 1u);
-    if (last && key != 0xFFFFFFFFu) atomicAdd(&acc[key], X);
+    if (last && key != 0xFFFFFFFFu) add(key, X);
   }
   __syncthreads();
   // vertex update (a3) of rows [r0, r0 + nrow)
@@ -214,7 +231,8 @@ __global__ void __launch_bounds__(kPbThreads, 1) k_pb_gather(PbArgs P, PrArgs A)
   const double D = A.uniform ? A.dbuf[A.it % 3] : 0.0;
   const float dn = (float)(D * A.inv_n);
   double dpart = 0.0;
-  for (int64_t i = tid; i < nrow; i += kPbThreads) pr_epilogue(A, r0 + i, acc[i], dn, dpart);
+  for (int64_t i = tid; i < nrow; i += kPbThreads)
+    pr_epilogue(A, r0 + i, (float)(((double)hi[i] * 4294967296.0 + (double)lo[i]) * 0x1p-62), dn, dpart);
   if (A.npeer) __threadfence_system();  // peer stores ordered before the next collective
   const double bs = block_sum(dpart, sred);
   if (tid == 0 && bs != 0.0) atomicAdd(&A.dbuf[(A.it + 1) % 3], bs);
@@ -327,14 +345,14 @@ gi_status pb_build_t(gi_graph g) {
   const int64_t nr = g->nr, m = g->ml, n = g->n;
   const int Ks = (int)ceil_div(n, kPbC);
   if (Ks > kPbMaxChunks) return fail(GI_ERR_UNSUPPORTED, "blocked pull: too many source chunks");
-  // row blocks: <= kPbC rows and <= W2 edges (a block of one row may hold more)
+  // row blocks: <= kPbB rows and <= W2 edges (a block of one row may hold more)
   std::vector<OffT> hoff(nr + 1);
   GI_CUDA(cudaMemcpyAsync(hoff.data(), g->csc_off.p, (nr + 1) * sizeof(OffT), cudaMemcpyDeviceToHost, st));
   GI_CUDA(cudaStreamSynchronize(st));
-  const int64_t W2 = std::max<int64_t>(2 * m / std::max<int64_t>(ceil_div(nr, kPbC), 1), 1 << 16);
+  const int64_t W2 = std::max<int64_t>(2 * m / std::max<int64_t>(ceil_div(nr, kPbB), 1), 1 << 16);
   std::vector<int64_t> rb{0};
   for (int64_t r = 0; r < nr;) {
-    int64_t r1 = std::min<int64_t>(nr, r + kPbC);
+    int64_t r1 = std::min<int64_t>(nr, r + kPbB);
     if ((int64_t)hoff[r1] - (int64_t)hoff[r] > W2)
       r1 = std::max<int64_t>(r + 1, (int64_t)(std::upper_bound(hoff.begin() + r, hoff.begin() + r1 + 1,
                                                                 (OffT)((int64_t)hoff[r] + W2)) - hoff.begin()) - 1);
@@ -369,7 +387,7 @@ gi_status pb_build_t(gi_graph g) {
   GI_TRY(g->pb_dst.alloc((mp + 8) * sizeof(uint16_t)));
   GI_TRY(g->pb_vals.alloc((mp + 8) * sizeof(float)));
   k_pb_fill<<<grid_for(mp + 8, 256, sms, 16), 256, 0, st>>>(g->pb_src.as<uint16_t>(), mp + 8, (uint16_t)kPbC);
-  k_pb_fill<<<grid_for(mp + 8, 256, sms, 16), 256, 0, st>>>(g->pb_dst.as<uint16_t>(), mp + 8, (uint16_t)kPbC);
+  k_pb_fill<<<grid_for(mp + 8, 256, sms, 16), 256, 0, st>>>(g->pb_dst.as<uint16_t>(), mp + 8, (uint16_t)kPbB);
   k_pb_place<OffT><<<Kd, 32, (size_t)Ks * sizeof(int32_t), st>>>(g->csc_off.as<OffT>(), g->csc_idx.as<int32_t>(),
                                                                  g->pb_rb.as<int64_t>(), Ks, Kd,
                                                                  g->pb_tstart.as<int64_t>(), g->pb_src.as<uint16_t>(),
@@ -404,7 +422,7 @@ gi_status pb_build_t(gi_graph g) {
   return GI_OK;
 }
 
-size_t pb_gather_smem(int Ks) { return (kPbC + 4) * sizeof(float) + ((Ks + 2) & ~1) * 4 + (size_t)Ks * 8; }
+size_t pb_gather_smem(int Ks) { return 2 * (kPbB + 4) * sizeof(uint32_t) + ((Ks + 2) & ~1) * 4 + (size_t)Ks * 8; }
 
 }  // namespace
 

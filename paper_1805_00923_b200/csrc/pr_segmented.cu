@@ -102,6 +102,10 @@ constexpr int64_t kBlockEdges = (1ll << 31) - (1ll << 20);  // and fewer edges t
 #define GI_SEG_DAMP 1.0  // fraction of the way each re-balance moves a boundary
 #endif
 constexpr int kCalibPasses = GI_SEG_CALIB;
+#ifndef GI_SEG_WAVES_DEFAULT
+#define GI_SEG_WAVES_DEFAULT 1
+#endif
+constexpr int kSegWaves = GI_SEG_WAVES_DEFAULT;
 
 struct SegArgs {
   const uint8_t* __restrict__ rec;     // kRecBytes per record
@@ -919,7 +923,10 @@ static gi_status seg_build_t(gi_graph g, int Z, int64_t DB) {
   blocks.clear();
   const auto tb1 = std::chrono::steady_clock::now();
   // ---- cost-balanced CTA ranges (every staged unit start adds kUnitCost)
-  const int ctas = sms;
+  // CTAs: one per SM, or `waves` per SM run back to back (the block scheduler then
+  // hands the last waves to whichever SMs finish first)
+  static const int waves = getenv("GI_SEG_WAVES") ? std::max(1, atoi(getenv("GI_SEG_WAVES"))) : kSegWaves;
+  const int ctas = sms * waves;
   std::vector<int32_t> h_cta(ctas + 1, (int32_t)C);
   {
     std::vector<int64_t> pre(C + 1, 0);

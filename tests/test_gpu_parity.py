@@ -463,6 +463,25 @@ def test_bfs_multi_bitparallel_batches(gi, ctx):
             assert stats[i].levels == depth.max() + 1
 
 
+@pytest.mark.parametrize("k", [8, 16, 17, 32, 33, 64])
+def test_bfs_multi_bitparallel_mask_widths(gi, ctx, k):
+    """The pull levels gather frontier masks narrowed to 16 bits (k <= 16) or 32 bits (k <= 32),
+    else the 64-bit masks: every width at its boundary, every direction policy."""
+    cfg = graphgen.CONFIGS[1]
+    s, d = cfg.edges()
+    g = gi.Graph(ctx, cfg.n, s, d)
+    go = oracle.build_graph(cfg.n, s, d)
+    sources = graphgen.pick_sources(cfg.n, s, d, k, 100 + k).tolist()
+    for policy in POLICIES:
+        par, st = g.bfs_multi(sources, batch=gi.GI_BFS_BATCH_BITPARALLEL, policy=_pol(gi, policy))
+        for i, src in enumerate(sources):
+            depth = oracle.bfs_depth(go, src)
+            ok, msg = oracle.validate_bfs(go, src, par[i], depth)
+            assert ok, f"k={k} {policy} src={src}: {msg}"
+            assert st[i].reached == int((depth >= 0).sum())
+    g.close()
+
+
 def test_bfs_multi_bitparallel_edge_cases(gi, ctx):
     """Bit-parallel passes on degenerate inputs: no edges; isolated and sink
     sources; k = 1, 64 and 65; a 100k-leaf star under every direction policy —

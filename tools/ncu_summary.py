@@ -2,6 +2,7 @@
 """Summarise an ncu --set full report: per-launch duration, DRAM bytes, throughput.
 
     python tools/ncu_summary.py gpurun_out/prof_r01.ncu-rep profiles/r01_ncu_summary.md [--json profiles/ncu_summary.json]
+                                [--config rmat-s25-ef48]   (store under configs/<name>: bench.py reads it per workload)
 """
 import csv
 import io
@@ -31,6 +32,7 @@ UNITS = {"dram_read": {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9},
 def main():
     rep, out = sys.argv[1], sys.argv[2]
     js = sys.argv[sys.argv.index("--json") + 1] if "--json" in sys.argv else None
+    cfgname = sys.argv[sys.argv.index("--config") + 1] if "--config" in sys.argv else None
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units = rows[0], rows[1]
@@ -70,7 +72,8 @@ def main():
             for key, name in (("k_pr_seg", "pr_seg"), ("k_pr_acc", "pr_acc"), ("k_pr_pull", "pr_direct"),
                               ("k_bfs_fused", "bfs_fused"), ("k_ms_pull_heavy", "ms_pull_heavy"),
                               ("k_ms_pull<", "ms_pull_light"), ("k_ms_push", "ms_push"),
-                              ("k_ms_finish", "ms_finish")):
+                              ("k_ms_finish", "ms_finish"), ("k_pb_scatter", "pb_scatter"),
+                              ("k_pb_gather", "pb_gather")):
                 if key in k:
                     a = agg.setdefault(name, {"launches": 0, "dram_bytes": 0.0, "duration_ns": 0.0})
                     a["launches"] += 1
@@ -84,18 +87,23 @@ def main():
             agg["pr_pull"] = {"dram_bytes_per_launch": agg["pr_seg"]["dram_bytes_per_launch"] +
                               agg["pr_acc"]["dram_bytes_per_launch"],
                               "note": "per PageRank iteration: k_pr_seg + k_pr_acc"}
+        if "pb_scatter" in agg and "pb_gather" in agg:  # one blocked-pull iteration = scatter + gather
+            agg["pr_pull"] = {"dram_bytes_per_launch": agg["pb_scatter"]["dram_bytes_per_launch"] +
+                              agg["pb_gather"]["dram_bytes_per_launch"],
+                              "note": "per PageRank iteration: k_pb_scatter + k_pb_gather"}
         if "ms_pull_light" in agg:  # one bit-parallel pull level = light-row kernel + heavy-row kernel
             lv = agg["ms_pull_light"]["launches"]
             tot = agg["ms_pull_light"]["dram_bytes"] + agg.get("ms_pull_heavy", {}).get("dram_bytes", 0.0)
             agg["bfs_pull"] = {"dram_bytes_per_launch": tot / lv, "levels": lv,
                                "note": "per bit-parallel pull level: k_ms_pull + k_ms_pull_heavy"}
-        old = json.load(open(js)) if os.path.exists(js) else {}
+        top = json.load(open(js)) if os.path.exists(js) else {}
+        old = top.setdefault("configs", {}).setdefault(cfgname, {}) if cfgname else top
         old.update(agg)  # merge with summaries of other captures (PR and BFS are captured separately)
         old.setdefault("sources", [])
         if rep not in old["sources"]:
             old["sources"].append(rep)
         old.pop("source", None)
-        json.dump(old, open(js, "w"), indent=1)
+        json.dump(top, open(js, "w"), indent=1)
 
 
 if __name__ == "__main__":

@@ -68,7 +68,7 @@ for ci in cfgs:
     bfs_ms = sum(x.total_ms for x in bst) / len(bst)
     trav = sum(x.edges_traversed for x in bst) / len(bst)
     line = {"config": cfg.name, "n": cfg.n, "m": g.m, "build_ms": round(build_ms, 1),
-            "pr_first_call_ms": round(first_pr_ms, 1), "pr_kernel": {0: "pull", 1: "push", 2: "direct",
+            "pr_first_call_ms": round(first_pr_ms, 1), "pr_kernel": {0: "pull", 1: "push", 2: "direct", 4: "partitioned", 5: "blocked",
                                                                     3: "segmented"}[best.kernel],
             "pr_ms_per_iter": round(best.edge_ms / best.edge_launches, 4),
             "pr_gteps": round(g.m * cfg.pr_iters / (best.total_ms * 1e-3) / 1e9, 1),
