@@ -217,7 +217,9 @@ struct gi_graph_s {
   std::vector<int32_t> seg_h_uc;   // host copy of seg_unit_c0
   std::vector<int64_t> seg_h_model;  // prefix of the per-record cost model (C + 1)
   gi::DevBuf seg_time;     // uint64[4*CTAs]: per-CTA timings of the last calibrated launch
+  gi::DevBuf seg_ht;       // uint64[CTAs]: {tail, head} of each CTA's remaining record range (work stealing)
   int seg_calib = 0;       // edge passes left that re-balance the CTA ranges from measured timings
+  int seg_steal = 0;       // CTAs steal records from each other's ranges (large layouts)
   gi::DevBuf seg_acc;      // float[2][seg_acc_stride]: per-row sums (ping-pong), L2-resident
   int64_t seg_acc_stride = 0;
   int seg_acc_cur = 0;     // buffer the next edge pass reduces into (all zero)

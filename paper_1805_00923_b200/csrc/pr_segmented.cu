@@ -102,10 +102,7 @@ constexpr int64_t kBlockEdges = (1ll << 31) - (1ll << 20);  // and fewer edges t
 #define GI_SEG_DAMP 1.0  // fraction of the way each re-balance moves a boundary
 #endif
 constexpr int kCalibPasses = GI_SEG_CALIB;
-#ifndef GI_SEG_WAVES_DEFAULT
-#define GI_SEG_WAVES_DEFAULT 1
-#endif
-constexpr int kSegWaves = GI_SEG_WAVES_DEFAULT;
+
 
 struct SegArgs {
   const uint8_t* __restrict__ rec;     // kRecBytes per record
@@ -117,6 +114,8 @@ struct SegArgs {
   int64_t n;
   int Z, S, U;
   unsigned long long* timing;  // per CTA [start, end, staging ns, units] (balance calibration, diagnostics)
+  unsigned long long* ht;      // per CTA {tail << 32 | head}: its remaining record range (work stealing)
+  int steal;                   // 1: CTAs that finish their range steal half of the largest remaining one
 };
 
 // programmatic dependent launch (the edge and vertex passes of consecutive
@@ -282,114 +281,192 @@ __device__ __forceinline__ void reduce_record(const SegArgs& A, const uint8_t* r
 }
 
 // Persistent CTA per SM over records [cta_c0[b], cta_c0[b+1]), unit by unit.
-// Warp kConsumers is the producer: one lane streams records into a
-// kStages-deep shared-memory ring with bulk copies (full[s]: bytes landed;
-// empty[s]: every consumer warp has taken its record). Consumer warp w
-// reduces record w of every stage. The unit's contrib segment is staged with
-// one more bulk copy.
-// MODE (GI_SEG_MODE diagnostics): 0 full, 1 no REDs, 2 record stream only.
+// Warp kConsumers is the producer: one lane claims records and streams them
+// into a kStages-deep shared-memory ring with bulk copies (full[s]: bytes
+// landed; empty[s]: every consumer warp has taken its record out of slot s),
+// writing a descriptor per stage (first record, count, sparse-unit flag,
+// restage flag). Consumer warp w reduces record w of every stage. A unit's
+// contrib segment is staged with one more bulk copy once every consumer has
+// left the previous segment (seg_free) and has been told by the descriptor to
+// wait for the new one (seg_bar).
+// Work stealing: a CTA's remaining range is one 64-bit word {tail, head}; the
+// owner claims a stage by adding to head, and a CTA that has exhausted its range
+// takes the upper half of the largest remaining range by lowering that range's
+// tail (CAS on the same word: a concurrent claim makes it retry). Ranges stay
+// contiguous, so records keep their RED and DRAM locality; the static cuts only
+// set where CTAs start. MODE (GI_SEG_MODE diagnostics): 0 full, 1 no REDs,
+// 2 record stream only.
+constexpr int kMinSteal = 256;  // records: below this, a steal does not pay for its segment staging
+constexpr int kClaim = 8 * kConsumers;  // records an owner claims from its range per atomic
+constexpr int kStealMinPerCta = 8192;   // records per CTA from which stealing pays (configs 4/5, not 2)
 template <int MODE, class OP>
 __global__ void __launch_bounds__(kSegThreads, 1) k_pr_seg(SegArgs A) {
   using T = typename OP::T;
   extern __shared__ __align__(128) uint8_t smem[];  // [kStages][kStageBytes] ring | Z + 4 floats of segment
-  __shared__ __align__(8) uint64_t full[kStages], empty[kStages], seg_bar;
+  __shared__ __align__(8) uint64_t full[kStages], empty[kStages], seg_bar, seg_free;
+  __shared__ int4 desc[kStages];  // first record, count (-1: end of work), sparse unit, restage
+  __shared__ unsigned long long s_units;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   uint8_t* ring = smem;
   T* scontrib = reinterpret_cast<T*>(smem + kStages * kStageBytes);
-  int c0 = A.cta_c0[blockIdx.x];
-  const int c1 = A.cta_c0[blockIdx.x + 1];
-  if (c0 >= c1) return;
-  unsigned long long t_start = 0, t_stage = 0, n_units = 0;
+  const int b = blockIdx.x;
+  unsigned long long t_start = 0, n_units = 0;
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], kConsumers);
     }
     mbar_init(&seg_bar, 1);
+    mbar_init(&seg_free, kConsumers);
   }
-  int u = __ldg(&A.cta_u[blockIdx.x]);  // unit of c0
   pdl_launch_dependents();
   __syncthreads();
   pdl_wait();  // the previous vertex pass wrote cin and cleared acc
   if (A.timing && tid == 0) t_start = globaltimer();
-  uint32_t it = 0;  // stages issued (producer) / consumed (consumers), over all units
-  uint32_t seg_phase = 0;
-  int staged_seg = -1;
-  while (c0 < c1) {
-    int uend = __ldg(&A.unit_c0[u + 1]);
-    // a sparse unit gathers from global memory instead of staging its segment;
-    // a run of consecutive sparse units streams as one span (records carry their segment)
-    const bool direct = uend - __ldg(&A.unit_c0[u]) < kDirectRecs;
-    if (direct)
-      while (uend < c1 && u + 1 < A.U && __ldg(&A.unit_c0[u + 2]) - uend < kDirectRecs) uend = __ldg(&A.unit_c0[++u + 1]);
-    const int ue = min(c1, uend);
-    const int seg = u % A.S;
-    const int nst = (ue - c0 + kConsumers - 1) / kConsumers;  // stages in this unit (span)
-    const bool restage = !direct && seg != staged_seg;
-    if (restage) {
-      __syncthreads();  // every consumer is done with the previous segment
-      if (tid == 0) {
-        const int64_t base = (int64_t)seg * A.Z;
-        const int64_t zlen = min((int64_t)A.Z, A.n - base);
-        scontrib[A.Z] = OP::id();
-        tma_load_1d(scontrib, A.cin + base, (uint32_t)(((zlen * 4) + 15) & ~15ll), &seg_bar);
-      }
-      staged_seg = seg;
-    }
-    if (warp == kConsumers) {
-      if (lane == 0) {  // producer
+  if (warp == kConsumers) {
+    if (lane == 0) {  // producer
 #if GI_SEG_EVICT_FIRST
-        uint64_t rec_policy;
-        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(rec_policy));
+      uint64_t rec_policy;
+      asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(rec_policy));
 #endif
-        for (int k = 0; k < nst; ++k, ++it) {
-          const uint32_t s = it % kStages, ph = (it / kStages) & 1u;
-          if (it >= kStages) mbar_wait(&empty[s], ph ^ 1u);  // consumers released this slot's last use
-          const int cs = c0 + k * kConsumers;
-          const int nc = min(kConsumers, ue - cs);
-#if GI_SEG_EVICT_FIRST
-          tma_load_1d_hint(ring + s * kStageBytes, A.rec + (int64_t)cs * kRecBytes, (uint32_t)(nc * kRecBytes),
-                           &full[s], rec_policy);
-#else
-          tma_load_1d(ring + s * kStageBytes, A.rec + (int64_t)cs * kRecBytes, (uint32_t)(nc * kRecBytes), &full[s]);
-#endif
+      const int c1 = __ldg(&A.cta_c0[b + 1]);
+      int h = __ldg(&A.cta_c0[b]);  // next record to issue
+      int ce = A.steal ? h : c1;    // end of the block of records claimed so far
+      if (A.steal) atomicExch(&A.ht[b], ((unsigned long long)(uint32_t)c1 << 32) | (uint32_t)h);
+      int u = __ldg(&A.cta_u[b]);  // unit of h
+      uint32_t it = 0, nrestage = 0;
+      int staged_seg = -1;
+      int span_u = -1, span_ce = -1, uend = 0, ulast = 0;
+      bool direct = false;
+      auto wait_slot = [&](uint32_t i) {
+        if (i >= kStages) mbar_wait(&empty[i % kStages], ((i / kStages) & 1u) ^ 1u);
+      };
+      for (;;) {
+        if (h >= ce) {
+          if (!A.steal) break;
+          // claim the next block of kClaim records of the own range (one atomic per
+          // kClaim / kConsumers stages); a thief may have lowered the tail meanwhile
+          const unsigned long long old = atomicAdd(&A.ht[b], (unsigned long long)kClaim);
+          const int oh = (int)(uint32_t)old, ot = (int)(old >> 32);
+          if (oh < ot) {
+            h = oh;
+            ce = min(oh + kClaim, ot);
+          } else {  // own range exhausted: steal the upper half of the largest remaining range
+            bool got = false;
+            for (int tries = 0; tries < 8 && !got; ++tries) {
+              int vbest = -1, rbest = kMinSteal - 1;
+              unsigned long long wbest = 0;
+              for (int v = 0; v < (int)gridDim.x; ++v) {
+                const unsigned long long w = *reinterpret_cast<volatile unsigned long long*>(&A.ht[v]);
+                const int rem = (int)(w >> 32) - (int)(uint32_t)w;
+                if (rem > rbest) {
+                  rbest = rem;
+                  vbest = v;
+                  wbest = w;
+                }
+              }
+              if (vbest < 0) break;
+              const int vh = (int)(uint32_t)wbest, vt = (int)(wbest >> 32);
+              const int nt = vh + (vt - vh) / 2;
+              const unsigned long long nw = ((unsigned long long)(uint32_t)nt << 32) | (uint32_t)vh;
+              if (atomicCAS(&A.ht[vbest], wbest, nw) == wbest) {  // [nt, vt) is ours now
+                atomicExch(&A.ht[b], ((unsigned long long)(uint32_t)vt << 32) | (uint32_t)nt);
+                h = ce = nt;  // the next pass claims from it
+                int lo = 0, hi = A.U - 1;  // the unit of nt: last u with unit_c0[u] <= nt
+                while (lo < hi) {
+                  const int mid = (lo + hi + 1) >> 1;
+                  if (__ldg(&A.unit_c0[mid]) <= nt) lo = mid;
+                  else hi = mid - 1;
+                }
+                u = lo;
+                got = true;
+              }
+            }
+            if (!got) break;
+          }
+          continue;
         }
-      }
-      it = __shfl_sync(0xffffffffu, it, 0);
-    } else {
-      if (restage) {
-        const unsigned long long t0 = A.timing && tid == 0 ? globaltimer() : 0;
-        mbar_wait(&seg_bar, seg_phase);
-        if (A.timing && tid == 0) t_stage += globaltimer() - t0;
-      }
-      for (int k = 0; k < nst; ++k, ++it) {
-        const uint32_t s = it % kStages, ph = (it / kStages) & 1u;
-        mbar_wait(&full[s], ph);
-        const int c = c0 + k * kConsumers + warp;
-        const uint8_t* r = ring + s * kStageBytes + warp * kRecBytes;
-        if (c < ue) {
+        // the span of the unit holding h (a run of consecutive sparse units is one span:
+        // their records carry their segment), looked up once per unit (and after a steal)
+        if (u != span_u || ce != span_ce) {
+          span_u = u;
+          span_ce = ce;
+          uend = __ldg(&A.unit_c0[u + 1]);
+          direct = uend - __ldg(&A.unit_c0[u]) < kDirectRecs;
+          ulast = u;
           if (direct)
-            reduce_record<MODE, true, OP>(
-                A, r, reinterpret_cast<const T*>(A.cin) + (int64_t)*reinterpret_cast<const int32_t*>(r + 12) * A.Z,
-                lane, &empty[s]);
-          else reduce_record<MODE, false, OP>(A, r, scontrib, lane, &empty[s]);
+            while (uend < ce && ulast + 1 < A.U && __ldg(&A.unit_c0[ulast + 2]) - uend < kDirectRecs)
+              uend = __ldg(&A.unit_c0[++ulast + 1]);
         }
-        else if (lane == 0) {
-          mbar_arrive(&empty[s]);  // nothing to take from this slot
+        const int seg = u % A.S;
+        const int cnt = min(kConsumers, min(uend, ce) - h);
+        const bool restage = !direct && seg != staged_seg;
+        wait_slot(it);
+        const uint32_t sl = it % kStages;
+        desc[sl] = make_int4(h, cnt, direct ? 1 : 0, restage ? 1 : 0);
+#if GI_SEG_EVICT_FIRST
+        tma_load_1d_hint(ring + sl * kStageBytes, A.rec + (int64_t)h * kRecBytes, (uint32_t)(cnt * kRecBytes),
+                         &full[sl], rec_policy);
+#else
+        tma_load_1d(ring + sl * kStageBytes, A.rec + (int64_t)h * kRecBytes, (uint32_t)(cnt * kRecBytes), &full[sl]);
+#endif
+        ++it;
+        if (restage) {  // every consumer has left the old segment (it reached this stage): load the new one
+          mbar_wait(&seg_free, nrestage & 1u);
+          ++nrestage;
+          const int64_t base = (int64_t)seg * A.Z;
+          const int64_t zlen = min((int64_t)A.Z, A.n - base);
+          scontrib[A.Z] = OP::id();
+          tma_load_1d(scontrib, A.cin + base, (uint32_t)(((zlen * 4) + 15) & ~15ll), &seg_bar);
+          staged_seg = seg;
+        }
+        h += cnt;
+        if (h >= uend) {
+          u = ulast + 1;
+          ++n_units;
         }
       }
+      // end of work: one more descriptor, completed by a plain arrive
+      wait_slot(it);
+      const uint32_t sl = it % kStages;
+      desc[sl] = make_int4(0, -1, 0, 0);
+      s_units = n_units;
+      mbar_arrive(&full[sl]);
     }
-    if (restage) seg_phase ^= 1u;
-    c0 = ue;
-    ++u;
-    ++n_units;
+  } else {
+    uint32_t it = 0, seg_phase = 0;
+    for (;; ++it) {
+      const uint32_t sl = it % kStages, ph = (it / kStages) & 1u;
+      mbar_wait(&full[sl], ph);
+      const int4 d = desc[sl];
+      if (d.y < 0) break;
+      if (d.w) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&seg_free);  // done with the previous segment
+        mbar_wait(&seg_bar, seg_phase);
+        seg_phase ^= 1u;
+      }
+      const uint8_t* r = ring + sl * kStageBytes + warp * kRecBytes;
+      if (warp < d.y) {
+        if (d.z)
+          reduce_record<MODE, true, OP>(
+              A, r, reinterpret_cast<const T*>(A.cin) + (int64_t)*reinterpret_cast<const int32_t*>(r + 12) * A.Z,
+              lane, &empty[sl]);
+        else reduce_record<MODE, false, OP>(A, r, scontrib, lane, &empty[sl]);
+      } else if (lane == 0) {
+        mbar_arrive(&empty[sl]);  // nothing to take from this slot
+      }
+    }
   }
-  if (A.timing && tid == 0) {
-    unsigned long long* T = A.timing + 4 * blockIdx.x;
-    T[0] = t_start;
-    T[1] = globaltimer();
-    T[2] = t_stage;
-    T[3] = n_units;
+  if (A.timing) {
+    __syncthreads();
+    if (tid == 0) {
+      unsigned long long* Tm = A.timing + 4 * blockIdx.x;
+      Tm[0] = t_start;
+      Tm[1] = globaltimer();
+      Tm[2] = 0;
+      Tm[3] = s_units;
+    }
   }
 }
 
@@ -861,6 +938,10 @@ static gi_status seg_build_block(gi_graph g, int Z, int S, int64_t r0, int64_t r
   return GI_OK;
 }
 
+// GI_SEG_STEAL: 0 static ranges only, 1 (default) stealing on large layouts, 2 stealing on
+// every layout (tests); read at each layout build
+static int seg_steal() { return getenv("GI_SEG_STEAL") ? atoi(getenv("GI_SEG_STEAL")) : 1; }
+
 template <typename OffT>
 static gi_status seg_build_t(gi_graph g, int Z, int64_t DB) {
   gi_context ctx = g->ctx;
@@ -923,10 +1004,7 @@ static gi_status seg_build_t(gi_graph g, int Z, int64_t DB) {
   blocks.clear();
   const auto tb1 = std::chrono::steady_clock::now();
   // ---- cost-balanced CTA ranges (every staged unit start adds kUnitCost)
-  // CTAs: one per SM, or `waves` per SM run back to back (the block scheduler then
-  // hands the last waves to whichever SMs finish first)
-  static const int waves = getenv("GI_SEG_WAVES") ? std::max(1, atoi(getenv("GI_SEG_WAVES"))) : kSegWaves;
-  const int ctas = sms * waves;
+  const int ctas = sms;
   std::vector<int32_t> h_cta(ctas + 1, (int32_t)C);
   {
     std::vector<int64_t> pre(C + 1, 0);
@@ -955,6 +1033,13 @@ static gi_status seg_build_t(gi_graph g, int Z, int64_t DB) {
   g->seg_h_uc = h_uc;
   GI_TRY(seg_upload_ctas(g));
   GI_TRY(g->seg_time.alloc(4 * ctas * sizeof(unsigned long long)));
+  GI_TRY(g->seg_ht.alloc(ctas * sizeof(unsigned long long)));
+  GI_CUDA(cudaMemsetAsync(g->seg_ht.p, 0, ctas * sizeof(unsigned long long), st));  // every range empty
+  // work stealing where each CTA holds many records (a large graph), on top of the
+  // measured-time re-balancing of the static cuts (stealing only evens out the rest:
+  // a steal costs a segment staging and breaks the thief's contiguity)
+  const int steal_mode = seg_steal();
+  g->seg_steal = steal_mode == 2 || (steal_mode == 1 && C >= (int64_t)ctas * kStealMinPerCta);
   g->seg_calib = getenv("GI_SEG_NO_CALIB") ? 0 : getenv("GI_SEG_CALIB") ? atoi(getenv("GI_SEG_CALIB")) : kCalibPasses;
   g->seg_acc_stride = (n + 64) & ~31ll;  // >= n + 1: row n is the trash row of padding lanes
   GI_TRY(g->seg_acc.alloc(2 * g->seg_acc_stride * sizeof(float)));
@@ -1082,6 +1167,8 @@ gi_status seg_min_pass(gi_graph g, const int32_t* labels, int32_t* acc) {
   S.S = g->seg_S;
   S.U = g->seg_U;
   S.timing = nullptr;
+  S.ht = g->seg_ht.as<unsigned long long>();
+  S.steal = g->seg_steal;
   const size_t dyn = seg_dyn_smem(g->seg_Z);
   static size_t attr_min[64] = {};
   const int dev = g->ctx->device & 63;
@@ -1106,6 +1193,8 @@ gi_status seg_edge_pass(gi_graph g, const float* cin) {
   S.Z = g->seg_Z;
   S.S = g->seg_S;
   S.U = g->seg_U;
+  S.ht = g->seg_ht.as<unsigned long long>();
+  S.steal = g->seg_steal;
   static const int mode = getenv("GI_SEG_MODE") ? atoi(getenv("GI_SEG_MODE")) : 0;
   void (*kern)(SegArgs) = mode == 1 ? k_pr_seg<1, OpSum> : mode == 2 ? k_pr_seg<2, OpSum> : k_pr_seg<0, OpSum>;
   const size_t dyn = seg_dyn_smem(g->seg_Z);

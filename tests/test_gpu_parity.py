@@ -252,6 +252,32 @@ def test_pr_segmented_many_segments(gi, ctx, seg, dblk):
             _pr_check(got, oracle.pagerank(go, 20, 0.85, dangling), f"seg={seg} dblk={dblk} n={n}")
 
 
+@pytest.mark.parametrize("steal", ["0", "2"])
+def test_pr_segmented_work_stealing(gi, ctx, steal, monkeypatch):
+    """The segmented pull with CTAs stealing halves of each other's record ranges (forced on
+    config 2's layout, ~1150 records per CTA, by GI_SEG_STEAL=2) and without (0): PR (repeated:
+    every launch steals differently) and CC against the oracle."""
+    monkeypatch.setenv("GI_SEG_STEAL", steal)
+    cfg = graphgen.CONFIGS[2]
+    s, d = cfg.edges()
+    go = oracle.build_graph(cfg.n, s, d)
+    want = oracle.pagerank(go, 20, 0.85)
+    import torch
+
+    ts, td = torch.from_numpy(s).cuda(), torch.from_numpy(d).cuda()
+    for seg in (0, 20000):
+        g = gi.Graph(ctx, cfg.n, ts, td, gi.GI_DEFAULT_FLAGS | gi.GI_EDGES_ON_DEVICE)
+        out = torch.empty(cfg.n, dtype=torch.float32, device="cuda")
+        for _ in range(3):
+            _, st = g.pagerank(20, 0.85, out=out, direction=gi.GI_PR_PULL_SEGMENTED, segment_size=seg)
+            _pr_check(out.cpu().numpy(), want, f"steal={steal} seg={seg}")
+        if seg == 0:
+            lab = torch.empty(cfg.n, dtype=torch.int32, device="cuda")
+            g.cc(out=lab)
+            assert (lab.cpu().numpy() == oracle.cc_labels(go)).all()
+        g.close()
+
+
 @pytest.mark.parametrize("z", [1, 1000, 4096, 30000, 0])
 def test_pr_partitioned_many_partitions(gi, ctx, z):
     """Cache partitioning: the CSC split by source range
