@@ -217,10 +217,12 @@ __global__ void __launch_bounds__(kPbThreads, 1) k_pb_gather(PbArgs P, PrArgs A)
     // summed by a segmented scan; the segment's last lane adds the total
     const uint32_t kprev = __shfl_up_sync(0xffffffffu, key, 1);
     const uint32_t heads = __ballot_sync(0xffffffffu, lane == 0 || kprev != key);
+    if (heads != 0xFFFFFFFFu) {  // some lanes continue their left neighbour's run: merge (warp-uniform)
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const float y = __shfl_up_sync(0xffffffffu, X, o);
-      if (lane >= o && ((heads >> (lane - o + 1)) & ((1u << o) - 1u)) == 0u) X += y;
+      for (int o = 1; o < 32; o <<= 1) {
+        const float y = __shfl_up_sync(0xffffffffu, X, o);
+        if (lane >= o && ((heads >> (lane - o + 1)) & ((1u << o) - 1u)) == 0u) X += y;
+      }
     }
     const bool last = lane == 31 || ((heads >> (lane + 1)) & 1u);
     if (last && key != 0xFFFFFFFFu) add(key, X);
