@@ -459,7 +459,13 @@ def run_ours(args):
 
     stream = torch.cuda.Stream()
     partition = world > 1 and mode == "partition"
-    if partition:  # NCCL communicator of the library; torch.distributed only ships the unique id
+    if partition and backend != "nccl":
+        # diagnostics (GI_BENCH_DIST_BACKEND=gloo): the library's collectives staged through host memory into
+        # the gloo group (gi_context_create_hostcomm) — the partitioned path end to end on one shared GPU
+        from paper_1805_00923_b200.hostcomm import TorchDistComm
+
+        ctx = gi.Context(dev, stream.cuda_stream, hostcomm=(rank, world, TorchDistComm()))
+    elif partition:  # NCCL communicator of the library; torch.distributed only ships the unique id
         uid = torch.zeros(128, dtype=torch.uint8, device=dev)
         if rank == 0:
             uid.copy_(torch.frombuffer(bytearray(gi.gi_nccl_unique_id()), dtype=torch.uint8))
@@ -487,6 +493,7 @@ def run_ours(args):
         elig = torch.zeros(cfg.n, dtype=torch.int32, device=dev)
         keep = ts != td
         elig[ts[keep].long()] = 1
+        elig = elig.to(cdev)
         torch.distributed.all_reduce(elig)
         sources = graphgen.pick_sources_from_mask(cfg.n, elig.cpu().numpy(), cfg.bfs_sources, cfg.source_seed) \
             if cfg.source_seed else np.zeros(1, np.int32)

@@ -911,6 +911,11 @@ static gi_status bfs_dist_impl(gi_graph g, int32_t source, const gi_bfs_opts& o,
     pslice[p] = g->bounds[p] * 4;
   }
   gi_bfs_stats S{};
+  cudaEvent_t pe[2] = {nullptr, nullptr};
+  if (o.profile) {
+    for (int k = 0; k < 2; ++k) GI_CUDA(cudaEventCreate(&pe[k]));
+    GI_CUDA(cudaEventRecord(pe[0], st));
+  }
   // peer stores of the next-frontier words (GI_BFS_PEER=1, or the comm's default;
   // every rank must ask and every rank must map, agreed by allreduce): a ring of
   // three bitmaps, so the one a level writes into on every replica was zeroed
@@ -1030,6 +1035,12 @@ static gi_status bfs_dist_impl(gi_graph g, int32_t source, const gi_bfs_opts& o,
   GI_CUDA(stream_wait(st));
   S.reached = h[0];
   S.edges_traversed = h[1];
+  if (o.profile) {
+    GI_CUDA(cudaEventRecord(pe[1], st));
+    GI_CUDA(cudaEventSynchronize(pe[1]));
+    GI_CUDA(cudaEventElapsedTime(&S.total_ms, pe[0], pe[1]));
+    for (int k = 0; k < 2; ++k) cudaEventDestroy(pe[k]);
+  }
   if (stats) *stats = S;
   return GI_OK;
 }

@@ -44,7 +44,7 @@ std::mutex g_big_mu;
 std::vector<BigEntry> g_big;
 size_t g_big_total = 0;
 size_t big_cap() {
-  static const size_t v = (getenv("GI_BIGCACHE_GB") ? (size_t)atoll(getenv("GI_BIGCACHE_GB")) : 64) << 30;
+  static const size_t v = (getenv("GI_BIGCACHE_GB") ? (size_t)atoll(getenv("GI_BIGCACHE_GB")) : 120) << 30;
   return v;
 }
 }  // namespace
@@ -71,19 +71,32 @@ void* big_cache_get(size_t nbytes, cudaStream_t s, size_t* got) {
 void big_cache_put(void* p, size_t bytes, cudaStream_t s) {
   int dev = -1;
   cudaGetDevice(&dev);
+  // the device must keep kBigMinFree bytes free for everybody else (torch's allocator,
+  // other contexts): cached blocks count as used
+  size_t fr = 0, tot = 0;
+  if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) {
+    cudaGetLastError();
+    fr = 0;
+  }
+  constexpr size_t kBigMinFree = 24ull << 30;
   std::vector<void*> drop;
   {
     std::lock_guard<std::mutex> lk(g_big_mu);
     if (bytes > big_cap()) {
       drop.push_back(p);
     } else {
-      while (g_big_total + bytes > big_cap() && !g_big.empty()) {  // oldest first
+      while ((g_big_total + bytes > big_cap() || fr < kBigMinFree) && !g_big.empty()) {  // oldest first
         drop.push_back(g_big.front().p);
+        fr += g_big.front().bytes;
         g_big_total -= g_big.front().bytes;
         g_big.erase(g_big.begin());
       }
-      g_big.push_back(BigEntry{p, bytes, s, dev});
-      g_big_total += bytes;
+      if (fr < kBigMinFree) {
+        drop.push_back(p);
+      } else {
+        g_big.push_back(BigEntry{p, bytes, s, dev});
+        g_big_total += bytes;
+      }
     }
   }
   for (void* q : drop) cudaFree(q);

@@ -78,8 +78,9 @@ struct AllocScope {
 // Reuse is stream-ordered (every user of a block is on the same stream), so no
 // synchronisation is needed; cudaMalloc / cudaFree of multi-GB blocks cost
 // 10-400 ms each and stall the device (DESIGN §6 e2e). The cache holds at most
-// GI_BIGCACHE_GB (default 64) GB, is emptied when an allocation fails, and the
-// blocks of a stream are freed when its context is destroyed.
+// GI_BIGCACHE_GB (default 120) GB and never leaves less than 24 GB of the device
+// free (other allocators), is emptied when an allocation fails, and the blocks
+// of a stream are freed when its context is destroyed.
 void* big_cache_get(size_t nbytes, cudaStream_t s, size_t* got);
 void big_cache_put(void* p, size_t bytes, cudaStream_t s);
 void big_cache_flush(cudaStream_t s);  // s = nullptr: every stream of the current device

@@ -53,6 +53,13 @@ namespace {
 #define GI_MS_CS 0
 #endif
 constexpr int kMsT = 256;
+#ifndef GI_MS_LMINB
+#define GI_MS_LMINB 1  // min resident CTAs per SM requested from ptxas (register cap) for the light pull
+#endif
+#ifndef GI_MS_HMINB
+#define GI_MS_HMINB 6  // ... and for the heavy pull (40 registers: 6 CTAs per SM hide the L2 gather latency;
+                       // 13.6 vs 14.1-16.4 ms for config 4's 16-source pass)
+#endif
 #ifndef GI_MS_HEAVY
 #define GI_MS_HEAVY 32
 #endif
@@ -221,7 +228,7 @@ __device__ __forceinline__ unsigned long long ms_fget(const MsArgs& A, int32_t v
 }
 
 template <typename OffT, typename FM>
-__global__ void __launch_bounds__(kMsT) k_ms_pull(MsArgs A) {
+__global__ void __launch_bounds__(kMsT, GI_MS_LMINB) k_ms_pull(MsArgs A) {
   __shared__ int32_t s_buf[kMsT / 32][64];  // per-warp staging of the rows joining the next frontier
   int32_t* wbuf = s_buf[threadIdx.x >> 5];
   int nbuf = 0;
@@ -295,7 +302,7 @@ __device__ __forceinline__ unsigned warp_transpose32(unsigned x) {
 }
 
 template <typename OffT, typename FM>
-__global__ void __launch_bounds__(kMsT) k_ms_pull_heavy(MsArgs A, const int2* __restrict__ hch, int64_t C) {
+__global__ void __launch_bounds__(kMsT, GI_MS_HMINB) k_ms_pull_heavy(MsArgs A, const int2* __restrict__ hch, int64_t C) {
   __shared__ int32_t s_buf[kMsT / 32][32];  // per-warp staging of the rows joining the next frontier
   const OffT* __restrict__ off = static_cast<const OffT*>(A.csc_off);
   const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;

@@ -321,22 +321,30 @@ __global__ void k_pb_fill(uint16_t* __restrict__ a, int64_t n, uint16_t v) {
     a[i] = v;
 }
 
-// edges per (row, source segment of Z) piece, summed: the segmented pull's pieces
+// (row, source segment of Z) pairs holding an edge — the segmented pull's pieces —
+// counted with a warp per row: an edge starts a piece when its segment differs
+// from the previous edge's (rows are sorted by source)
 template <typename OffT>
 __global__ void k_count_pieces(const OffT* __restrict__ off, const int32_t* __restrict__ idx, int64_t nr, int Z,
                                unsigned long long* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   unsigned long long c = 0;
-  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nr; v += (int64_t)gridDim.x * blockDim.x) {
-    int prev = -1;
-    for (int64_t e = (int64_t)off[v]; e < (int64_t)off[v + 1]; ++e) {
-      const int sg = __ldg(&idx[e]) / Z;
-      c += sg != prev;
-      prev = sg;
+  for (int64_t v = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; v < nr; v += nw) {
+    const int64_t b = (int64_t)off[v], e = (int64_t)off[v + 1];
+    int prev_last = -1;  // segment of the edge before this step's first
+    for (int64_t j0 = b; j0 < e; j0 += 32) {
+      const int64_t j = j0 + lane;
+      const int sg = j < e ? __ldg(&idx[j]) / Z : -2;
+      int before = __shfl_up_sync(0xffffffffu, sg, 1);
+      if (lane == 0) before = prev_last;
+      c += (j < e && sg != before);
+      prev_last = __shfl_sync(0xffffffffu, sg, 31);
     }
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-  if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
+  if (lane == 0 && c) atomicAdd(out, c);
 }
 
 template <typename OffT>
@@ -444,7 +452,7 @@ gi_status pb_count_pieces(gi_graph g, int Z, int64_t* pieces) {
   DevBuf c;
   GI_TRY(c.alloc(sizeof(unsigned long long)));
   GI_CUDA(cudaMemsetAsync(c.p, 0, sizeof(unsigned long long), st));
-  const int grid = grid_for(g->nr, 256, g->ctx->num_sms, 16);
+  const int grid = grid_for(g->nr * 32, 256, g->ctx->num_sms, 16);
   if (g->off64)
     k_count_pieces<int64_t><<<grid, 256, 0, st>>>(g->csc_off.as<int64_t>(), g->csc_idx.as<int32_t>(), g->nr, Z,
                                                    c.as<unsigned long long>());

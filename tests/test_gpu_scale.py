@@ -86,6 +86,8 @@ def test_billion_edge_config_parity(gi, cfg_idx):
     out = torch.empty(n, dtype=torch.float32, device="cuda")
     _, st = g.pagerank(cfg.pr_iters, cfg.damping, out=out)
     assert st.bytes_alg_per_iter == 4 * g.m + ((8 if g.m >= 2**31 else 4) + 12) * n
+    # the auto pull kernel: segmented on the skewed config 4, propagation-blocked on config 5
+    assert st.kernel == (gi.GI_PR_PULL_BLOCKED if cfg_idx == 5 else gi.GI_PR_PULL_SEGMENTED)
     got = out.cpu().numpy().astype(np.float64)
     want = oracle.pagerank(go, cfg.pr_iters, cfg.damping)
     l1 = np.abs(got - want).sum()
