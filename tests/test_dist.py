@@ -257,6 +257,13 @@ def test_hostcomm_processes_end_to_end(world, peer):
         assert not bad, (rank, bad)
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("P", [2, 3])
+def test_partitioned_wide_offsets(gi, P, monkeypatch):
+    """The partitioned build, PR and BFS with int64 offsets (GI_OFFSETS64) on every rank."""
+    test_partitioned_pagerank_and_bfs(gi, P, *CASES[1], "1", monkeypatch, wide=True)
+
+
 # ---------------------------------------------------------------- simulated ranks on one GPU
 def _run_ranks(gi, P, fn):
     """Run fn(rank, ctx) on P threads, each with its own local-group context."""
@@ -302,7 +309,7 @@ CASES = [
 @pytest.mark.parametrize("peer", ["1", "0"])
 @pytest.mark.parametrize("P", [2, 3, 4])
 @pytest.mark.parametrize("name,n,make", CASES)
-def test_partitioned_pagerank_and_bfs(gi, P, name, n, make, peer, monkeypatch):
+def test_partitioned_pagerank_and_bfs(gi, P, name, n, make, peer, monkeypatch, wide=False):
     """peer=1: the vertex update stores each owned row's contrib, and the BFS level
     kernels each owned next-frontier word, into every rank's replica (peer stores,
     SURVEY §8(f) NEXT #3); peer=0: the allgathers."""
@@ -324,7 +331,7 @@ def test_partitioned_pagerank_and_bfs(gi, P, name, n, make, peer, monkeypatch):
 
     def fn(r, ctx):
         sel = owner == r
-        g = gi.Graph(ctx, n, s[sel], d[sel])
+        g = gi.Graph(ctx, n, s[sel], d[sel], gi.GI_DEFAULT_FLAGS | (gi.GI_OFFSETS64 if wide else 0))
         res = {"m": g.m, "part": g.partition()}
         for direction in (gi.GI_PR_PULL, gi.GI_PR_PULL_DIRECT, gi.GI_PR_PUSH, gi.GI_PR_PULL_BLOCKED):
             for dg in (0, 1):
