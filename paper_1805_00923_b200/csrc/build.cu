@@ -1,11 +1,12 @@
 // build.cu — device graph builder.
 //
-// edge list (int32 src, dst) -> validate -> 64-bit keys (u << b | v), self-loops
-// dropped, optional symmetrisation ("an undirected graph would be represented
-// by duplicating the directed edges", PAPER.md P:3183 [draft]) -> radix sort ->
-// unique (dedup) -> CSR offsets by binary search per vertex -> out-degrees ->
-// relabel by out-degree (descending, stable) -> CSR and CSC in internal ids ->
-// merge-path tile metadata for the pull kernel.
+// edge list (int32 src, dst) -> validate -> out-degree histogram (before dedup)
+// -> relabel by it (descending, stable) when skewed -> 64-bit keys (u' << b | v')
+// in internal ids, self-loops dropped, optional symmetrisation ("an undirected
+// graph would be represented by duplicating the directed edges", PAPER.md
+// P:3183 [draft]) -> radix sort -> unique (dedup) -> CSR (offsets by binary
+// search per vertex) and exact out-degrees -> transposed keys -> radix sort ->
+// CSC -> merge-path tile metadata for the pull kernel.
 //
 // The sort and select primitives are CUB (CUDA toolkit, header-only): library
 // primitives in the sense of a cuBLAS call; every graph-specific step is a
@@ -29,17 +30,35 @@ __global__ void k_validate(const int32_t* __restrict__ src, const int32_t* __res
   }
 }
 
+// keys of the pairs in internal ids (inv: input -> internal id, null = identity)
 __global__ void k_make_keys(const int32_t* __restrict__ src, const int32_t* __restrict__ dst, int64_t m0,
-                            int bits, int rm_self, int sym, uint64_t* __restrict__ keys) {
+                            int bits, int rm_self, int sym, uint64_t* __restrict__ keys,
+                            const int32_t* __restrict__ inv = nullptr) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m0; i += (int64_t)gridDim.x * blockDim.x) {
     uint64_t u = (uint32_t)src[i], v = (uint32_t)dst[i];
     bool drop = rm_self && u == v;
+    if (inv) {
+      u = (uint32_t)__ldg(&inv[u]);
+      v = (uint32_t)__ldg(&inv[v]);
+    }
     if (sym) {
       keys[2 * i] = drop ? kSentinel : (u << bits) | v;
       keys[2 * i + 1] = drop ? kSentinel : (v << bits) | u;
     } else {
       keys[i] = drop ? kSentinel : (u << bits) | v;
     }
+  }
+}
+
+// out-degrees before dedup (the relabelling's order and skew test; exact degrees come
+// from the CSR): one count per kept pair, both directions when symmetrising
+__global__ void k_hist_src(const int32_t* __restrict__ src, const int32_t* __restrict__ dst, int64_t m0,
+                           int rm_self, int sym, int32_t* __restrict__ deg) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m0; i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t u = src[i], v = dst[i];
+    if (rm_self && u == v) continue;
+    atomicAdd(&deg[u], 1);
+    if (sym) atomicAdd(&deg[v], 1);
   }
 }
 
@@ -174,18 +193,70 @@ gi_status build_graph(gi_context ctx, int64_t n, int64_t m0, const int32_t* d_sr
   GI_CUDA(cudaStreamSynchronize(st));
   if (h_bad) return fail(GI_ERR_VERTEX_OUT_OF_RANGE, "gi_graph_create: an edge endpoint is outside [0, n)");
 
-  // 2. keys, 3. select non-sentinel, 4. sort, 5. unique
+  // 2. relabel by out-degree (descending, stable) when the degrees are skewed:
+  // hub sources then form a dense prefix (segment 0 of the segmented pull, the
+  // staged bitmap prefix of the BFS pull). A flat degree distribution (a road
+  // grid) keeps its input order and with it its locality. The order and the
+  // skew test use the degrees before dedup (one histogram pass), so the keys are
+  // made in internal ids directly and sorted twice in all (CSR, CSC); any
+  // internal order is valid: results are reported in input ids.
   const int bits = bits_for(n > 1 ? n : 2);
   const int64_t mk = sym ? 2 * m0 : m0;
+  Temp tmp;
+  GI_TRY(g->outdeg.alloc(n * sizeof(int32_t)));
+  const int32_t* inv = nullptr;
+  if (g->relabeled && m0 > 0) {
+    GI_CUDA(cudaMemsetAsync(g->outdeg.p, 0, n * sizeof(int32_t), st));
+    k_hist_src<<<grid_for(m0, 256, sms, 16), 256, 0, st>>>(d_src, d_dst, m0, rm_self, sym, g->outdeg.as<int32_t>());
+    DevBuf mx, tot;
+    GI_TRY(mx.alloc(sizeof(int32_t)));
+    GI_TRY(tot.alloc(sizeof(int64_t)));
+    size_t b = 0;
+    GI_CUDA(cub::DeviceReduce::Max(nullptr, b, g->outdeg.as<int32_t>(), mx.as<int32_t>(), n, st));
+    GI_TRY(tmp.ensure(b));
+    GI_CUDA(cub::DeviceReduce::Max(tmp.buf.p, b, g->outdeg.as<int32_t>(), mx.as<int32_t>(), n, st));
+    b = 0;
+    GI_CUDA(cub::DeviceReduce::Sum(nullptr, b, g->outdeg.as<int32_t>(), tot.as<int64_t>(), n, st));
+    GI_TRY(tmp.ensure(b));
+    GI_CUDA(cub::DeviceReduce::Sum(tmp.buf.p, b, g->outdeg.as<int32_t>(), tot.as<int64_t>(), n, st));
+    int32_t hmax = 0;
+    int64_t htot = 0;
+    GI_CUDA(cudaMemcpyAsync(&hmax, mx.p, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    GI_CUDA(cudaMemcpyAsync(&htot, tot.p, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    GI_CUDA(cudaStreamSynchronize(st));
+    const double mean = n > 0 ? (double)htot / (double)n : 0.0;
+    g->relabeled = (double)hmax > kSkewRatio * std::max(1.0, mean);
+  } else {
+    g->relabeled = false;
+  }
+  if (g->relabeled) {
+    DevBuf rk, rk2, ids;
+    GI_TRY(rk.alloc(n * sizeof(uint32_t)));
+    GI_TRY(rk2.alloc(n * sizeof(uint32_t)));
+    GI_TRY(ids.alloc(n * sizeof(int32_t)));
+    GI_TRY(g->perm.alloc(n * sizeof(int32_t)));
+    GI_TRY(g->inv.alloc(n * sizeof(int32_t)));
+    k_relabel_keys<<<grid_for(n, 256, sms), 256, 0, st>>>(g->outdeg.as<int32_t>(), n, rk.as<uint32_t>(), ids.as<int32_t>());
+    size_t b = 0;
+    GI_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, b, rk.as<uint32_t>(), rk2.as<uint32_t>(), ids.as<int32_t>(),
+                                            g->perm.as<int32_t>(), n, 0, 32, st));
+    GI_TRY(tmp.ensure(b));
+    GI_CUDA(cub::DeviceRadixSort::SortPairs(tmp.buf.p, b, rk.as<uint32_t>(), rk2.as<uint32_t>(), ids.as<int32_t>(),
+                                            g->perm.as<int32_t>(), n, 0, 32, st));
+    k_invert<<<grid_for(n, 256, sms), 256, 0, st>>>(g->perm.as<int32_t>(), n, g->inv.as<int32_t>());
+    GI_CUDA(cudaGetLastError());
+    inv = g->inv.as<int32_t>();
+  }
+
+  // 3. keys (u' << b | v') in internal ids, 4. select non-sentinel, 5. sort, 6. unique
   DevBuf kA, kB, nsel;
   GI_TRY(kA.alloc(mk * sizeof(uint64_t)));
   GI_TRY(kB.alloc(mk * sizeof(uint64_t)));
   GI_TRY(nsel.alloc(sizeof(int64_t)));
-  Temp tmp;
   size_t tb = 0;
   int64_t m = 0;
   if (mk > 0) {
-    k_make_keys<<<grid_for(m0, 256, sms), 256, 0, st>>>(d_src, d_dst, m0, bits, rm_self, sym, kA.as<uint64_t>());
+    k_make_keys<<<grid_for(m0, 256, sms), 256, 0, st>>>(d_src, d_dst, m0, bits, rm_self, sym, kA.as<uint64_t>(), inv);
     GI_CUDA(cub::DeviceSelect::If(nullptr, tb, kA.as<uint64_t>(), kB.as<uint64_t>(), nsel.as<int64_t>(), mk,
                                   NotSentinel(), st));
     GI_TRY(tmp.ensure(tb));
@@ -224,72 +295,18 @@ gi_status build_graph(gi_context ctx, int64_t n, int64_t m0, const int32_t* d_sr
   g->nr = n;
   g->off64 = m >= (int64_t)INT32_MAX || (flags & GI_OFFSETS64);
 
-  // 6. out-degrees in input ids (from the input-id CSR)
-  DevBuf off_in;
-  GI_TRY(off_in.alloc((n + 1) * sizeof(int64_t)));
-  GI_TRY(g->outdeg.alloc(n * sizeof(int32_t)));
-  k_offsets<int64_t><<<grid_for(n + 1, 256, sms), 256, 0, st>>>(cur->as<uint64_t>(), m, n, bits, off_in.as<int64_t>());
-  k_degrees<int64_t><<<grid_for(n, 256, sms), 256, 0, st>>>(off_in.as<int64_t>(), n, g->outdeg.as<int32_t>());
-  GI_CUDA(cudaGetLastError());
-
-  // 7. relabel by out-degree (descending, stable) when the degrees are skewed:
-  // hub sources then form a dense prefix (segment 0 of the segmented pull, the
-  // staged bitmap prefix of the BFS pull). A flat degree distribution (a road
-  // grid) keeps its input order and with it its locality.
-  if (g->relabeled) {
-    DevBuf mx;
-    GI_TRY(mx.alloc(sizeof(int32_t)));
-    size_t b = 0;
-    GI_CUDA(cub::DeviceReduce::Max(nullptr, b, g->outdeg.as<int32_t>(), mx.as<int32_t>(), n, st));
-    GI_TRY(tmp.ensure(b));
-    GI_CUDA(cub::DeviceReduce::Max(tmp.buf.p, b, g->outdeg.as<int32_t>(), mx.as<int32_t>(), n, st));
-    int32_t hmax = 0;
-    GI_CUDA(cudaMemcpyAsync(&hmax, mx.p, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-    GI_CUDA(cudaStreamSynchronize(st));
-    const double mean = n > 0 ? (double)m / (double)n : 0.0;
-    g->relabeled = (double)hmax > kSkewRatio * std::max(1.0, mean);
-  }
-  const int32_t* inv = nullptr;
-  if (g->relabeled) {
-    DevBuf rk, rk2, ids;
-    GI_TRY(rk.alloc(n * sizeof(uint32_t)));
-    GI_TRY(rk2.alloc(n * sizeof(uint32_t)));
-    GI_TRY(ids.alloc(n * sizeof(int32_t)));
-    GI_TRY(g->perm.alloc(n * sizeof(int32_t)));
-    GI_TRY(g->inv.alloc(n * sizeof(int32_t)));
-    k_relabel_keys<<<grid_for(n, 256, sms), 256, 0, st>>>(g->outdeg.as<int32_t>(), n, rk.as<uint32_t>(), ids.as<int32_t>());
-    size_t b = 0;
-    GI_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, b, rk.as<uint32_t>(), rk2.as<uint32_t>(), ids.as<int32_t>(),
-                                            g->perm.as<int32_t>(), n, 0, 32, st));
-    GI_TRY(tmp.ensure(b));
-    GI_CUDA(cub::DeviceRadixSort::SortPairs(tmp.buf.p, b, rk.as<uint32_t>(), rk2.as<uint32_t>(), ids.as<int32_t>(),
-                                            g->perm.as<int32_t>(), n, 0, 32, st));
-    k_invert<<<grid_for(n, 256, sms), 256, 0, st>>>(g->perm.as<int32_t>(), n, g->inv.as<int32_t>());
-    GI_CUDA(cudaGetLastError());
-    inv = g->inv.as<int32_t>();
-  }
-
-  // 8. CSR in internal ids. Input keys are sorted by (u, v); after relabelling
-  // re-key and sort again.
-  DevBuf edges_in;  // keep the input-id sorted keys for the CSC pass
-  if (m > 0) {
-    GI_TRY(edges_in.alloc(m * sizeof(uint64_t)));
-    GI_CUDA(cudaMemcpyAsync(edges_in.p, cur->p, m * sizeof(uint64_t), cudaMemcpyDeviceToDevice, st));
-    if (inv) {
-      k_rekey<<<grid_for(m, 256, sms), 256, 0, st>>>(edges_in.as<uint64_t>(), m, bits, inv, 0, cur->as<uint64_t>());
-      GI_TRY(sort_keys(m));
-    }
-  }
+  // 7. CSR in internal ids and the exact out-degrees
   if (g->off64) GI_TRY(csr_from_sorted<int64_t>(g, cur->as<uint64_t>(), m, bits, n, g->csr_off, g->csr_idx));
   else GI_TRY(csr_from_sorted<int32_t>(g, cur->as<uint64_t>(), m, bits, n, g->csr_off, g->csr_idx));
-  if (inv) {  // out-degrees in internal ids
+  if (n > 0) {
     if (g->off64) k_degrees<int64_t><<<grid_for(n, 256, sms), 256, 0, st>>>(g->csr_off.as<int64_t>(), n, g->outdeg.as<int32_t>());
     else k_degrees<int32_t><<<grid_for(n, 256, sms), 256, 0, st>>>(g->csr_off.as<int32_t>(), n, g->outdeg.as<int32_t>());
   }
 
-  // 9. CSC in internal ids: transpose keys and sort
+  // 8. CSC in internal ids: transpose the CSR keys and sort
   if (m > 0) {
-    k_rekey<<<grid_for(m, 256, sms), 256, 0, st>>>(edges_in.as<uint64_t>(), m, bits, inv, 1, cur->as<uint64_t>());
+    k_rekey<<<grid_for(m, 256, sms), 256, 0, st>>>(cur->as<uint64_t>(), m, bits, nullptr, 1, alt->as<uint64_t>());
+    std::swap(cur, alt);
     GI_TRY(sort_keys(m));
   }
   if (g->off64) GI_TRY(csr_from_sorted<int64_t>(g, cur->as<uint64_t>(), m, bits, n, g->csc_off, g->csc_idx));

@@ -67,7 +67,7 @@ constexpr int64_t kHeavy = GI_MS_HEAVY;  // rows with at least this many in-edge
 constexpr int kMsPullDiv = 3;     // bit-parallel direction rule: pull iff |F| + sum outdeg F > m / 3 (R21)
 constexpr int kPushChunk = 256;   // push: out-edges per warp at least
 #ifndef GI_MS_BATCH
-#define GI_MS_BATCH 4
+#define GI_MS_BATCH 2
 #endif
 constexpr int kPullBatch = GI_MS_BATCH;  // in-edge gathers in flight per pull step
 #ifndef GI_MS_HCHUNK
@@ -75,7 +75,7 @@ constexpr int kPullBatch = GI_MS_BATCH;  // in-edge gathers in flight per pull s
 #endif
 constexpr int kHChunk = GI_MS_HCHUNK;  // heavy-row in-edges per pull work item
 #ifndef GI_MS_HPER
-#define GI_MS_HPER 4
+#define GI_MS_HPER 16
 #endif
 constexpr int kHeavyPer = GI_MS_HPER;  // heavy chunks per warp
 #ifndef GI_MS_LPERSM
