@@ -57,10 +57,10 @@ namespace gi {
 namespace {
 
 #ifndef GI_SEG_CONSUMERS
-#define GI_SEG_CONSUMERS 16
+#define GI_SEG_CONSUMERS 30
 #endif
 #ifndef GI_SEG_STAGES
-#define GI_SEG_STAGES 4
+#define GI_SEG_STAGES 2
 #endif
 constexpr int kConsumers = GI_SEG_CONSUMERS;        // consumer warps (one record each per stage)
 constexpr int kSegThreads = 32 * (kConsumers + 1);  // + one producer warp (TMA)
@@ -93,7 +93,7 @@ constexpr int kPieceCost = 4;
 constexpr int kDirectRecs = GI_SEG_DIRECT;  // units with fewer records gather from global memory (no staging)
 constexpr int kDirectCost = 5;              // cost factor of a record of such a unit (L2 vs shared-memory gathers)
 constexpr int64_t kUnitCost = 40 * kChunkE;         // a unit start: segment staging + pipeline refill
-constexpr int64_t kDefaultBlockRows = 8 << 20;      // 32 MB accumulator per destination block
+constexpr int64_t kDefaultBlockRows = 16 << 20;     // 64 MB accumulator per destination block (8 M: config 4 1.89-1.95 ms, 16-32 M: 1.78)
 constexpr int64_t kBlockEdges = (1ll << 31) - (1ll << 20);  // and fewer edges than the build's 32-bit sorts take
 #ifndef GI_SEG_CALIB
 #define GI_SEG_CALIB 8

@@ -28,11 +28,14 @@ g = gi.Graph(ctx, cfg.n, ts, td, flags)
 del ts, td
 torch.cuda.empty_cache()
 out = torch.empty(cfg.n, dtype=torch.float32, device="cuda")
+kw = {}
+if os.environ.get("GI_AB_DSTBLOCK"):  # segmented pull: destination rows per block (0 = auto)
+    kw = dict(direction=gi.GI_PR_PULL_SEGMENTED, dst_block=int(os.environ["GI_AB_DSTBLOCK"]))
 for _ in range(3):
-    g.pagerank(20, 0.85, out=out)
+    g.pagerank(20, 0.85, out=out, **kw)
 best, bv = 1e9, 0
 for _ in range(5):
-    _, st = g.pagerank(20, 0.85, out=out, profile=True)
+    _, st = g.pagerank(20, 0.85, out=out, profile=True, **kw)
     if st.edge_ms / st.edge_launches < best:
         best, bv = st.edge_ms / st.edge_launches, st.vertex_ms / st.edge_launches
 peak = json.load(open("MEASURED_PEAKS.json"))["hbm_gbs"] if os.path.exists("MEASURED_PEAKS.json") else 6443.2
