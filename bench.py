@@ -59,6 +59,15 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "GTEPS for PageRank iteration and BFS; achieved fraction of HBM roofline"
+# the paper's own numbers for the graphs the configs stand in for (context only: other hardware,
+# other datasets; BASELINE.md derives GTEPS from the paper's seconds and its edge counts)
+PAPER_CONTEXT = {
+    "hardware": "2x Intel Xeon E5-2695 v3 (24 cores, 48 threads), 128 GB DDR3-1600 (PAPER.md P:2194-2197)",
+    "graphit_pr_20iter_s": {"twitter_1.47B": 8.707, "livejournal_69M": 0.342, "friendster_3.6B": 32.571},
+    "graphit_pr_gteps": {"twitter_1.47B": 3.37, "livejournal_69M": 4.04, "friendster_3.6B": 2.21},
+    "graphit_bfs_s_per_source": {"twitter_1.47B": 0.298, "livejournal_69M": 0.035, "friendster_3.6B": 0.490},
+    "source": "Table 4, PAPER.md P:2291; GTEPS derived in BASELINE.md (edges x iterations / seconds)",
+}
 DEFAULT_CONFIG = 4
 
 
@@ -610,6 +619,7 @@ def run_ours(args):
             "bfs_gteps": (r["tot_bfs"] / args.steps) / (r["bfs_ms"] * 1e-3) / 1e9 if r["bfs_ms"] > 0 else None,
             "bfs_ms_per_source": r["bfs_ms"] / max(len(srcs), 1), "build_ms": build_ms,
             "pr_first_call_ms": r["first_pr_ms"], "gen_s": gen_s, "secondary": secondary,
+            "paper_context": PAPER_CONTEXT,
         }
         print(json.dumps(line), flush=True)
     ctx.close()
