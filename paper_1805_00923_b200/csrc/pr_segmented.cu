@@ -81,6 +81,9 @@ constexpr int kStageBytes = kConsumers * kRecBytes;
 // CTA balance: an initial cost model (in gather slots), then refined from
 // measured per-CTA times over the first kCalibPasses edge passes (seg_rebalance)
 constexpr int kPieceCost = 4;
+#ifndef GI_SEG_RED_EVICT_LAST
+#define GI_SEG_RED_EVICT_LAST 1  // config 4: 1.67-1.68 vs 1.70 ms per iteration
+#endif
 #ifndef GI_SEG_EVICT_FIRST
 #define GI_SEG_EVICT_FIRST 1  // the record stream carries an L2 evict_first hint (keeps acc and contrib in L2)
 #endif
@@ -184,7 +187,15 @@ struct OpSum {
   using T = float;
   static __device__ __forceinline__ T id() { return 0.f; }
   static __device__ __forceinline__ T op(T a, T b) { return a + b; }
-  static __device__ __forceinline__ void red(T* p, T v) { atomicAdd(p, v); }
+  static __device__ __forceinline__ void red(T* p, T v) {
+#if GI_SEG_RED_EVICT_LAST  // keep the accumulator's lines in L2 past the streamed records
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    asm volatile("red.global.add.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(p), "f"(v), "l"(pol) : "memory");
+#else
+    atomicAdd(p, v);
+#endif
+  }
 };
 struct OpMin {
   using T = int32_t;
