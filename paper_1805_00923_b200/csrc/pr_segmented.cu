@@ -81,6 +81,9 @@ constexpr int kStageBytes = kConsumers * kRecBytes;
 // CTA balance: an initial cost model (in gather slots), then refined from
 // measured per-CTA times over the first kCalibPasses edge passes (seg_rebalance)
 constexpr int kPieceCost = 4;
+#ifndef GI_ACC_LDCS
+#define GI_ACC_LDCS 1
+#endif
 #ifndef GI_SEG_RED_EVICT_LAST
 #define GI_SEG_RED_EVICT_LAST 1  // config 4: 1.67-1.68 vs 1.70 ms per iteration
 #endif
@@ -496,7 +499,11 @@ __global__ void __launch_bounds__(256) k_pr_acc(PrArgs A, const float* __restric
   const bool vec = (A.row0 & 3) == 0;
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < (vec ? nq : 0);
        q += (int64_t)gridDim.x * blockDim.x) {
+#if GI_ACC_LDCS
+    const float4 s4 = __ldcs(acc4 + q);  // read once: evict-first, the zeroed buffer and contrib stay
+#else
     const float4 s4 = acc4[q];
+#endif
     reinterpret_cast<float4*>(zero)[q] = make_float4(0.f, 0.f, 0.f, 0.f);
     const int64_t v0 = A.row0 + 4 * q;
     const int4 od4 = __ldg(reinterpret_cast<const int4*>(A.outdeg + v0));
