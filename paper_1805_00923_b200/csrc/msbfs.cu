@@ -13,7 +13,7 @@
 //   seen[v]    bits of the sources that have reached v (levels <= current)
 //   fr[c][v]   bits of the sources whose current frontier holds v
 //   act[c]     the vertices with fr[c][v] != 0 (push levels read it)
-// Per level (direction: pull iff |F| + sum outdeg F > m / 3 — a pull rarely
+// Per level (direction: pull iff |F| + sum outdeg F > m / 8 — a pull rarely
 // exits early here, since a vertex stops only once it has all k sources):
 //   pull (DensePull + early exit): light rows (in-degree < 32) a thread each;
 //     heavy rows cut into chunks of <= 1024 in-edges, a warp per chunk (chunks
@@ -64,7 +64,7 @@ constexpr int kMsT = 256;
 #define GI_MS_HEAVY 32
 #endif
 constexpr int64_t kHeavy = GI_MS_HEAVY;  // rows with at least this many in-edges are pulled by whole warps
-constexpr int kMsPullDiv = 3;     // bit-parallel direction rule: pull iff |F| + sum outdeg F > m / 3 (R21)
+constexpr int kMsPullDiv = 8;     // bit-parallel direction rule: pull iff |F| + sum outdeg F > m / 8 (R21)
 constexpr int kPushChunk = 256;   // push: out-edges per warp at least
 #ifndef GI_MS_BATCH
 #define GI_MS_BATCH 2
