@@ -43,6 +43,11 @@ struct BigEntry {
 std::mutex g_big_mu;
 std::vector<BigEntry> g_big;
 size_t g_big_total = 0;
+// GI_DEBUG_BIGCACHE=1: one stderr line per miss / eviction (diagnostics)
+bool big_debug() {
+  static const bool v = getenv("GI_DEBUG_BIGCACHE") && atoi(getenv("GI_DEBUG_BIGCACHE")) != 0;
+  return v;
+}
 size_t big_cap() {
   static const size_t v = (getenv("GI_BIGCACHE_GB") ? (size_t)atoll(getenv("GI_BIGCACHE_GB")) : 120) << 30;
   return v;
@@ -60,7 +65,10 @@ void* big_cache_get(size_t nbytes, cudaStream_t s, size_t* got) {
         (best < 0 || e.bytes < g_big[best].bytes))
       best = i;
   }
-  if (best < 0) return nullptr;
+  if (best < 0) {
+    if (big_debug()) fprintf(stderr, "bigcache miss %.2f GB (cached %.2f GB in %zu)\n", nbytes / 1e9, g_big_total / 1e9, g_big.size());
+    return nullptr;
+  }
   void* p = g_big[best].p;
   *got = g_big[best].bytes;
   g_big_total -= g_big[best].bytes;
@@ -99,6 +107,8 @@ void big_cache_put(void* p, size_t bytes, cudaStream_t s) {
       }
     }
   }
+  if (big_debug() && !drop.empty())
+    fprintf(stderr, "bigcache put %.2f GB: %zu blocks freed (device free %.2f GB)\n", bytes / 1e9, drop.size(), fr / 1e9);
   for (void* q : drop) cudaFree(q);
 }
 

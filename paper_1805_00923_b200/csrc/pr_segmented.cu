@@ -534,6 +534,13 @@ __global__ void __launch_bounds__(256) k_pr_acc(PrArgs A, const float* __restric
 
 
 // ---------------------------------------------------------------- layout build
+// out[i] = a[ix[i]]
+__global__ void k_gather_i64(const int64_t* __restrict__ a, const int64_t* __restrict__ ix, int64_t n,
+                             int64_t* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = a[ix[i]];
+}
+
 // row of every CSC edge (warp per row)
 template <typename OffT>
 // (rows [r0, r0 + n) of the CSC, whose edges start at e0: row[e - e0] = r0 + v)
@@ -863,15 +870,34 @@ static gi_status seg_build_block(gi_graph g, int Z, int S, int64_t r0, int64_t r
   GI_CUDA(cudaMemcpyAsync(h_cs.data(), cstart.p, (NC + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   GI_CUDA(cudaMemcpyAsync(h_up0.data(), unit_p0.p, (U + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   GI_CUDA(cudaStreamSynchronize(st));
-  for (int u = 0; u <= U; ++u)
-    GI_CUDA(cudaMemcpyAsync(&h_ao[u], aoff.as<int64_t>() + h_up0[u], sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-  GI_CUDA(cudaStreamSynchronize(st));
+  {  // h_ao[u] = aoff[unit_p0[u]]: one gather, one copy
+    DevBuf ao;
+    GI_TRY(ao.alloc((U + 1) * sizeof(int64_t)));
+    k_gather_i64<<<grid_for(U + 1, 256, sms), 256, 0, st>>>(aoff.as<int64_t>(), unit_p0.as<int64_t>(), U + 1,
+                                                           ao.as<int64_t>());
+    GI_CUDA(cudaMemcpyAsync(h_ao.data(), ao.p, (U + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    GI_CUDA(cudaStreamSynchronize(st));
+  }
   mark("bounds");
   int64_t hist_L[16] = {};  // short pieces by length (layout diagnostics)
   // ---- record layout: per unit, long records then short records by L
   std::vector<int32_t> h_uc(U + 1), h_crec0(NC, 0), h_type, h_L, h_ng;
   std::vector<int64_t> h_cost;  // per record, for the CTA balance
   int64_t C = 0, CL = 0, NS = 0;
+  {  // the record count first: the per-record vectors are filled without reallocation
+    int64_t cap = 0;
+    for (int u = 0; u < U; ++u) {
+      cap += ceil_div(h_ao[u + 1] - h_ao[u], kChunkE);
+      for (int L = 1; L < 16; ++L) {
+        const int64_t k = (int64_t)u * 16 + L;
+        cap += ceil_div(ceil_div(h_cs[k + 1] - h_cs[k], 32), short_groups(L));
+      }
+    }
+    h_type.reserve(cap);
+    h_L.reserve(cap);
+    h_ng.reserve(cap);
+    h_cost.reserve(cap);
+  }
   for (int u = 0; u < U; ++u) {
     h_uc[u] = (int32_t)C;
     const int64_t slots = h_ao[u + 1] - h_ao[u];
@@ -971,18 +997,33 @@ static gi_status seg_build_t(gi_graph g, int Z, int64_t DB) {
   const auto tb0 = std::chrono::steady_clock::now();
   // destination blocks: at most DB rows (the accumulator range kept in L2) and
   // fewer than 2^31 edges each (the build's sorts and piece ids are 32-bit)
-  std::vector<OffT> hoff(n + 1);
-  GI_CUDA(cudaMemcpyAsync(hoff.data(), g->csc_off.p, (n + 1) * sizeof(OffT), cudaMemcpyDeviceToHost, st));
-  GI_CUDA(cudaStreamSynchronize(st));
+  // (only the offsets at candidate block ends are read back; a block over emax
+  // edges reads its rows' offsets to cut it)
+  auto off_at = [&](int64_t r, int64_t* v) -> gi_status {
+    OffT x = 0;
+    GI_CUDA(cudaMemcpyAsync(&x, g->csc_off.as<OffT>() + r, sizeof(OffT), cudaMemcpyDeviceToHost, st));
+    GI_CUDA(cudaStreamSynchronize(st));
+    *v = (int64_t)x;
+    return GI_OK;
+  };
+  const auto tb_hoff = std::chrono::steady_clock::now();
   std::vector<int64_t> br{0};
   {
     static const int64_t emax = getenv("GI_SEG_BLOCK_EDGES") ? atoll(getenv("GI_SEG_BLOCK_EDGES")) : kBlockEdges;
     int64_t r = 0;
     while (r < n) {
       int64_t r1 = std::min<int64_t>(n, r + DB);
-      if ((int64_t)hoff[r1] - (int64_t)hoff[r] > emax)  // last row keeping the block under emax edges
-        r1 = std::max<int64_t>(r + 1, (int64_t)(std::upper_bound(hoff.begin() + r, hoff.begin() + r1 + 1,
-                                                                 (OffT)((int64_t)hoff[r] + emax)) - hoff.begin()) - 1);
+      int64_t er = 0, er1 = 0;
+      GI_TRY(off_at(r, &er));
+      GI_TRY(off_at(r1, &er1));
+      if (er1 - er > emax) {  // last row keeping the block under emax edges
+        std::vector<OffT> hoff(r1 - r + 1);
+        GI_CUDA(cudaMemcpyAsync(hoff.data(), g->csc_off.as<OffT>() + r, (r1 - r + 1) * sizeof(OffT),
+                                cudaMemcpyDeviceToHost, st));
+        GI_CUDA(cudaStreamSynchronize(st));
+        r1 = r + std::max<int64_t>(1, (int64_t)(std::upper_bound(hoff.begin(), hoff.end(), (OffT)(er + emax)) -
+                                                hoff.begin()) - 1);
+      }
       br.push_back(r1);
       r = r1;
     }
@@ -993,8 +1034,11 @@ static gi_status seg_build_t(gi_graph g, int Z, int64_t DB) {
   const int U = B * S;
   std::vector<SegBlock> blocks(B);
   int64_t C = 0, CL = 0, NS = 0, P = 0;
+  std::vector<double> tblk;
   for (int b = 0; b < B; ++b) {
+    const auto tq = std::chrono::steady_clock::now();
     GI_TRY(seg_build_block<OffT>(g, Z, S, br[b], br[b + 1], blocks[b]));
+    tblk.push_back(std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tq).count());
     C += blocks[b].C;
     CL += blocks[b].CL;
     NS += blocks[b].NS;
@@ -1068,6 +1112,9 @@ static gi_status seg_build_t(gi_graph g, int Z, int64_t DB) {
   if (const char* dbg = getenv("GI_DEBUG_SEG_LAYOUT")) {
     if (FILE* f = fopen(dbg, "a")) {
       const auto tb2 = std::chrono::steady_clock::now();
+      fprintf(f, "  hoff %.1f ms, per-block builds", std::chrono::duration<double, std::milli>(tb_hoff - tb0).count());
+      for (double x : tblk) fprintf(f, " %.1f", x);
+      fprintf(f, " ms\n");
       fprintf(f, "n=%lld m=%lld Z=%d S=%d B=%d U=%d records=%lld (long %lld, short %lld) bytes=%lld P=%lld "
               "(short %lld) build %.1f ms (blocks %.1f, ranges + upload %.1f)\n", (long long)n, (long long)m, Z, S, B,
               U, (long long)C, (long long)CL, (long long)(C - CL), (long long)(C * kRecBytes), (long long)P,
