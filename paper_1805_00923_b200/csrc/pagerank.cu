@@ -111,11 +111,17 @@ __global__ void __launch_bounds__(kPullThreads) k_pr_pull(PrArgs A) {
 // need no merge-path balancing: every thread sums kRowsPT rows spaced a block
 // apart (independent offset -> index -> contrib chains in flight), the
 // gathers stay local in input order, and the vertex update is fused.
-constexpr int kRowsPT = 4;
+#ifndef GI_ROWS_PT
+#define GI_ROWS_PT 4
+#endif
+constexpr int kRowsPT = GI_ROWS_PT;
 constexpr int kRowsMaxDeg = 64;
 
 template <typename OffT>
-__global__ void __launch_bounds__(256) k_pr_rows(PrArgs A) {
+#ifndef GI_ROWS_MINB
+#define GI_ROWS_MINB 4  // 64 registers: 4 CTAs per SM (96 registers, 2 CTAs: config 3 0.18-0.27 ms; 4: 0.150)
+#endif
+__global__ void __launch_bounds__(256, GI_ROWS_MINB) k_pr_rows(PrArgs A) {
   __shared__ double sred[32];
   const OffT* __restrict__ off = static_cast<const OffT*>(A.off);
   if (blockIdx.x == 0 && threadIdx.x == 0) A.dbuf[(A.it + 2) % 3] = 0.0;
