@@ -74,8 +74,15 @@ constexpr int kRecBytes = kRecHdr + kRecPayload;    // 1184, a multiple of the 1
 constexpr int kLDst = kRecHdr + 2 * kChunkE;        // long: dst[33]
 constexpr int kLMask = kLDst + 4 * kADst;           // long: mask
 static_assert(kLMask + 4 <= kRecBytes, "long record overflows");
-__host__ __device__ constexpr int short_group_bytes(int L) { return 64 * L + 128; }
-__host__ __device__ constexpr int short_groups(int L) { return kRecPayload / short_group_bytes(L); }
+// short groups: wide (type 2: int32 destination per lane) or compact (type 3: a
+// 16-bit offset per lane from an int32 group base, 0xFFFF = the trash row),
+// used when the group's 32 destinations (sorted) span < 65535 rows
+__host__ __device__ constexpr int short_group_bytes(int L, bool compact = false) {
+  return compact ? 64 * L + 80 : 64 * L + 128;
+}
+__host__ __device__ constexpr int short_groups(int L, bool compact = false) {
+  return kRecPayload / short_group_bytes(L, compact);
+}
 constexpr int kStages = GI_SEG_STAGES;              // ring depth (stages in flight per CTA)
 constexpr int kStageBytes = kConsumers * kRecBytes;
 // CTA balance: an initial cost model (in gather slots), then refined from
@@ -121,6 +128,7 @@ struct SegArgs {
   int Z, S, U;
   unsigned long long* timing;  // per CTA [start, end, staging ns, units] (balance calibration, diagnostics)
   unsigned long long* ht;      // per CTA {tail << 32 | head}: its remaining record range (work stealing)
+  int trash;                   // accumulator row of padding lanes (the owned rows' count)
   int steal;                   // 1: CTAs that finish their range steal half of the largest remaining one
 };
 
@@ -261,12 +269,19 @@ template <int MODE, bool G, class OP>
 __device__ __forceinline__ void reduce_short(const SegArgs& A, const uint8_t* r, const typename OP::T* sc, int lane,
                                              uint64_t* empty) {
   using T = typename OP::T;
+  const bool compact = *reinterpret_cast<const int32_t*>(r) == 3;
   const int L = *reinterpret_cast<const int32_t*>(r + 4);
   const int ng = *reinterpret_cast<const int32_t*>(r + 8);
-  const int gb = short_group_bytes(L);
+  const int gb = short_group_bytes(L, compact);
   for (int g = 0; g < ng; ++g) {
     const uint8_t* b = r + kRecHdr + g * gb + 2 * lane;
-    const int d = *reinterpret_cast<const int32_t*>(r + kRecHdr + g * gb + 64 * L + 4 * lane);
+    int d;
+    if (compact) {
+      const uint32_t off = *reinterpret_cast<const uint16_t*>(r + kRecHdr + g * gb + 64 * L + 2 * lane);
+      d = off == 0xFFFFu ? A.trash : *reinterpret_cast<const int32_t*>(r + kRecHdr + g * gb + 64 * L + 64) + (int)off;
+    } else {
+      d = *reinterpret_cast<const int32_t*>(r + kRecHdr + g * gb + 64 * L + 4 * lane);
+    }
     T s = OP::id();
 #pragma unroll 4
     for (int k = 0; k < L; ++k) s = OP::op(s, seg_val<G, OP>(sc, *reinterpret_cast<const uint16_t*>(b + 64 * k), A.Z));
@@ -688,10 +703,31 @@ __global__ void k_record_headers(const int32_t* __restrict__ rtype, const int32_
       if (type == 1) {
         if (o < kLDst) *w = (uint32_t)Z | ((uint32_t)Z << 16);  // idx padding (overwritten by real slots)
       } else {
-        const int L = rL[c], gb = short_group_bytes(L), g = (o - kRecHdr) / gb, go = (o - kRecHdr) % gb;
-        if (g < rng[c]) *w = go < 64 * L ? ((uint32_t)Z | ((uint32_t)Z << 16)) : (uint32_t)trash;
+        const int L = rL[c];
+        const bool compact = type == 3;
+        const int gb = short_group_bytes(L, compact), g = (o - kRecHdr) / gb, go = (o - kRecHdr) % gb;
+        if (g < rng[c]) {
+          if (go < 64 * L) *w = (uint32_t)Z | ((uint32_t)Z << 16);        // idx padding (the identity slot)
+          else if (!compact) *w = (uint32_t)trash;                          // wide: trash destination
+          else if (go < 64 * L + 64) *w = 0xFFFFFFFFu;                      // compact: trash offsets
+          else *w = 0u;                                                     // compact: base (set by placement)
+        }
       }
     }
+  }
+}
+
+// the largest destination span of any 32-piece group of each short class (pieces
+// are in ascending destination order inside a class): compact groups need < 65535
+__global__ void k_class_span(const int64_t* __restrict__ cstart, int64_t NC, const int32_t* __restrict__ spid,
+                             const int32_t* __restrict__ pdst, int32_t* __restrict__ span) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < NC; k += (int64_t)gridDim.x * blockDim.x) {
+    int32_t mx = 0;
+    for (int64_t q = cstart[k]; q < cstart[k + 1]; q += 32) {
+      const int64_t ql = min(q + 31, cstart[k + 1] - 1);
+      mx = max(mx, pdst[spid[ql]] - pdst[spid[q]]);
+    }
+    span[k] = mx;
   }
 }
 
@@ -707,13 +743,20 @@ __global__ void k_place_short(const uint32_t* __restrict__ sckey, const int32_t*
     const int L = (int)(k % 16u);
     const int64_t q = j - cstart[k];
     const int64_t grp = q / 32;
-    const int lane = (int)(q % 32), R = short_groups(L);
-    uint8_t* b = rec + (int64_t)(crec0[k] + grp / R) * kRecBytes + kRecHdr + (grp % R) * short_group_bytes(L);
+    const bool compact = *reinterpret_cast<const int32_t*>(rec + (int64_t)crec0[k] * kRecBytes) == 3;
+    const int lane = (int)(q % 32), R = short_groups(L, compact);
+    uint8_t* b = rec + (int64_t)(crec0[k] + grp / R) * kRecBytes + kRecHdr + (grp % R) * short_group_bytes(L, compact);
     const int32_t p = spid[j];
     const int64_t base = (int64_t)(skey[pstart[p]] % (uint32_t)S) * Z;
     for (int e = 0; e < L; ++e)
       *reinterpret_cast<uint16_t*>(b + 64 * e + 2 * lane) = (uint16_t)(idx[(int64_t)order[pstart[p] + e]] - base);
-    *reinterpret_cast<int32_t*>(b + 64 * L + 4 * lane) = pdst[p];
+    if (compact) {  // offset from the group's first (smallest) destination
+      const int32_t d0 = pdst[spid[cstart[k] + grp * 32]];
+      *reinterpret_cast<uint16_t*>(b + 64 * L + 2 * lane) = (uint16_t)(pdst[p] - d0);
+      if (lane == 0) *reinterpret_cast<int32_t*>(b + 64 * L + 64) = d0;
+    } else {
+      *reinterpret_cast<int32_t*>(b + 64 * L + 4 * lane) = pdst[p];
+    }
   }
 }
 
@@ -878,6 +921,18 @@ static gi_status seg_build_block(gi_graph g, int Z, int S, int64_t r0, int64_t r
     GI_CUDA(cudaMemcpyAsync(h_ao.data(), ao.p, (U + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
     GI_CUDA(cudaStreamSynchronize(st));
   }
+  // the largest destination span of a group of each short class: compact groups where it fits 16 bits
+  std::vector<int32_t> h_span(NC, 0);
+  {
+    DevBuf span;
+    GI_TRY(span.alloc(std::max<int64_t>(NC, 1) * sizeof(int32_t)));
+    k_class_span<<<grid_for(NC, 256, sms), 256, 0, st>>>(cstart.as<int64_t>(), NC, spid.as<int32_t>(),
+                                                        pdst.as<int32_t>(), span.as<int32_t>());
+    GI_CUDA(cudaMemcpyAsync(h_span.data(), span.p, NC * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    GI_CUDA(cudaStreamSynchronize(st));
+  }
+  static const bool compact_on = !getenv("GI_SEG_COMPACT") || atoi(getenv("GI_SEG_COMPACT")) != 0;
+  auto compact_k = [&](int64_t k) { return compact_on && h_span[k] < 65535; };
   mark("bounds");
   int64_t hist_L[16] = {};  // short pieces by length (layout diagnostics)
   // ---- record layout: per unit, long records then short records by L
@@ -890,7 +945,7 @@ static gi_status seg_build_block(gi_graph g, int Z, int S, int64_t r0, int64_t r
       cap += ceil_div(h_ao[u + 1] - h_ao[u], kChunkE);
       for (int L = 1; L < 16; ++L) {
         const int64_t k = (int64_t)u * 16 + L;
-        cap += ceil_div(ceil_div(h_cs[k + 1] - h_cs[k], 32), short_groups(L));
+        cap += ceil_div(ceil_div(h_cs[k + 1] - h_cs[k], 32), short_groups(L, compact_k(k)));
       }
     }
     h_type.reserve(cap);
@@ -916,10 +971,11 @@ static gi_status seg_build_block(gi_graph g, int Z, int S, int64_t r0, int64_t r
       NS += cnt;
       hist_L[L] += cnt;
       h_crec0[k] = (int32_t)C;
-      const int64_t groups = ceil_div(cnt, 32), R = short_groups(L);
+      const bool cmp = compact_k(k);
+      const int64_t groups = ceil_div(cnt, 32), R = short_groups(L, cmp);
       for (int64_t gq = 0; gq < groups; gq += R) {
         const int ng = (int)std::min<int64_t>(R, groups - gq);
-        h_type.push_back(2);
+        h_type.push_back(cmp ? 3 : 2);
         h_L.push_back(L);
         h_ng.push_back(ng);
         h_cost.push_back((int64_t)ng * 32 * (L + kPieceCost));
@@ -968,7 +1024,12 @@ static gi_status seg_build_block(gi_graph g, int Z, int S, int64_t r0, int64_t r
       fprintf(f, "block rows [%lld, %lld) edges %lld:%s\n  short pieces by L:", (long long)r0, (long long)r1,
               (long long)m, phases.c_str());
       for (int L = 1; L < 16; ++L) fprintf(f, " %d:%lld", L, (long long)hist_L[L]);
-      fprintf(f, "\n");
+      int64_t ncmp = 0, nshort = 0;
+      for (int64_t c = 0; c < C; ++c) {
+        ncmp += h_type[c] == 3;
+        nshort += h_type[c] != 1;
+      }
+      fprintf(f, "\n  short records %lld (compact %lld)\n", (long long)nshort, (long long)ncmp);
       fclose(f);
     }
   GI_CUDA(cudaGetLastError());
@@ -1233,6 +1294,7 @@ gi_status seg_min_pass(gi_graph g, const int32_t* labels, int32_t* acc) {
   S.U = g->seg_U;
   S.timing = nullptr;
   S.ht = g->seg_ht.as<unsigned long long>();
+  S.trash = (int)g->nr;
   S.steal = g->seg_steal;
   const size_t dyn = seg_dyn_smem(g->seg_Z);
   static size_t attr_min[64] = {};
@@ -1259,6 +1321,7 @@ gi_status seg_edge_pass(gi_graph g, const float* cin) {
   S.S = g->seg_S;
   S.U = g->seg_U;
   S.ht = g->seg_ht.as<unsigned long long>();
+  S.trash = (int)g->nr;
   S.steal = g->seg_steal;
   static const int mode = getenv("GI_SEG_MODE") ? atoi(getenv("GI_SEG_MODE")) : 0;
   void (*kern)(SegArgs) = mode == 1 ? k_pr_seg<1, OpSum> : mode == 2 ? k_pr_seg<2, OpSum> : k_pr_seg<0, OpSum>;
