@@ -13,6 +13,10 @@
 // kernel below.
 #include <cub/cub.cuh>
 
+#include <chrono>
+#include <cstdio>
+#include <string>
+
 #include "gi_internal.cuh"
 #include "comm.cuh"
 
@@ -142,6 +146,30 @@ __global__ void k_tile_rows(const OffT* __restrict__ off, int64_t n, int64_t m, 
   }
 }
 
+// CSR keys (u << bits | v) -> the pair (v, u) as two 32-bit arrays (the CSC's row key and value)
+__global__ void k_split_keys(const uint64_t* __restrict__ keys, int64_t m, int bits, uint32_t* __restrict__ vk,
+                             int32_t* __restrict__ uv) {
+  const uint64_t mask = (1ull << bits) - 1;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+    vk[i] = (uint32_t)(keys[i] & mask);
+    uv[i] = (int32_t)(keys[i] >> bits);
+  }
+}
+
+// off[r] = first position of row r in sorted 32-bit row keys
+template <typename OffT>
+__global__ void k_offsets32(const uint32_t* __restrict__ keys, int64_t m, int64_t n, OffT* __restrict__ off) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r <= n; r += (int64_t)gridDim.x * blockDim.x) {
+    int64_t lo = 0, hi = m;
+    while (lo < hi) {
+      const int64_t mid = lo + ((hi - lo) >> 1);
+      if ((int64_t)keys[mid] < r) lo = mid + 1;
+      else hi = mid;
+    }
+    off[r] = (OffT)lo;
+  }
+}
+
 int bits_for(int64_t n) {
   int b = 1;
   while ((1ll << b) < n) ++b;
@@ -183,6 +211,19 @@ gi_status build_graph(gi_context ctx, int64_t n, int64_t m0, const int32_t* d_sr
   const bool sym = flags & GI_SYMMETRIZE;
   g->relabeled = !(flags & GI_NO_RELABEL) && n > 1;
 
+  // diagnostics (GI_DEBUG_BUILD=file): synchronised phase times
+  static const char* bdbg = getenv("GI_DEBUG_BUILD");
+  auto tph = std::chrono::steady_clock::now();
+  std::string bphases;
+  auto bmark = [&](const char* name) {
+    if (!bdbg) return;
+    cudaStreamSynchronize(st);
+    const auto t2 = std::chrono::steady_clock::now();
+    char b[64];
+    snprintf(b, sizeof(b), " %s=%.1f", name, std::chrono::duration<double, std::milli>(t2 - tph).count());
+    bphases += b;
+    tph = t2;
+  };
   // 1. validate endpoints
   DevBuf bad;
   GI_TRY(bad.alloc(sizeof(int)));
@@ -248,6 +289,7 @@ gi_status build_graph(gi_context ctx, int64_t n, int64_t m0, const int32_t* d_sr
     inv = g->inv.as<int32_t>();
   }
 
+  bmark("validate+relabel");
   // 3. keys (u' << b | v') in internal ids, 4. select non-sentinel, 5. sort, 6. unique
   DevBuf kA, kB, nsel;
   GI_TRY(kA.alloc(mk * sizeof(uint64_t)));
@@ -278,7 +320,9 @@ gi_status build_graph(gi_context ctx, int64_t n, int64_t m0, const int32_t* d_sr
     if (db.Current() != cur->as<uint64_t>()) std::swap(cur, alt);
     return GI_OK;
   };
+  bmark("keys");
   GI_TRY(sort_keys(m));
+  bmark("sort1");
   if (dedup && m > 1) {
     size_t b = 0;
     GI_CUDA(cub::DeviceSelect::Unique(nullptr, b, cur->as<uint64_t>(), alt->as<uint64_t>(), nsel.as<int64_t>(), m, st));
@@ -295,6 +339,7 @@ gi_status build_graph(gi_context ctx, int64_t n, int64_t m0, const int32_t* d_sr
   g->nr = n;
   g->off64 = m >= (int64_t)INT32_MAX || (flags & GI_OFFSETS64);
 
+  bmark("unique");
   // 7. CSR in internal ids and the exact out-degrees
   if (g->off64) GI_TRY(csr_from_sorted<int64_t>(g, cur->as<uint64_t>(), m, bits, n, g->csr_off, g->csr_idx));
   else GI_TRY(csr_from_sorted<int32_t>(g, cur->as<uint64_t>(), m, bits, n, g->csr_off, g->csr_idx));
@@ -303,14 +348,34 @@ gi_status build_graph(gi_context ctx, int64_t n, int64_t m0, const int32_t* d_sr
     else k_degrees<int32_t><<<grid_for(n, 256, sms), 256, 0, st>>>(g->csr_off.as<int32_t>(), n, g->outdeg.as<int32_t>());
   }
 
-  // 8. CSC in internal ids: transpose the CSR keys and sort
+  bmark("csr");
+  // 8. CSC in internal ids: a stable sort of the CSR's (v, u) pairs by v alone
+  // (`bits`-bit 32-bit keys, half the passes and bytes of re-sorting 64-bit
+  // transposed keys): the CSR order already has u ascending inside each v
+  GI_TRY(g->csc_idx.alloc(std::max<int64_t>(m, 1) * sizeof(int32_t)));
+  const uint32_t* vsorted = nullptr;
   if (m > 0) {
-    k_rekey<<<grid_for(m, 256, sms), 256, 0, st>>>(cur->as<uint64_t>(), m, bits, nullptr, 1, alt->as<uint64_t>());
-    std::swap(cur, alt);
-    GI_TRY(sort_keys(m));
+    uint32_t* vk = alt->as<uint32_t>();  // alt holds 8 x mk >= 8m bytes: two 4m-byte arrays
+    int32_t* uv = reinterpret_cast<int32_t*>(vk + m);
+    k_split_keys<<<grid_for(m, 256, sms), 256, 0, st>>>(cur->as<uint64_t>(), m, bits, vk, uv);
+    uint32_t* vk2 = cur->as<uint32_t>();  // the CSR keys are consumed: cur is scratch now
+    cub::DoubleBuffer<uint32_t> dk(vk, vk2);
+    cub::DoubleBuffer<int32_t> dv(uv, g->csc_idx.as<int32_t>());
+    size_t b = 0;
+    GI_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, b, dk, dv, m, 0, bits, st));
+    GI_TRY(tmp.ensure(b));
+    GI_CUDA(cub::DeviceRadixSort::SortPairs(tmp.buf.p, b, dk, dv, m, 0, bits, st));
+    if (dv.Current() != g->csc_idx.as<int32_t>())
+      GI_CUDA(cudaMemcpyAsync(g->csc_idx.p, dv.Current(), m * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
+    vsorted = dk.Current();
   }
-  if (g->off64) GI_TRY(csr_from_sorted<int64_t>(g, cur->as<uint64_t>(), m, bits, n, g->csc_off, g->csc_idx));
-  else GI_TRY(csr_from_sorted<int32_t>(g, cur->as<uint64_t>(), m, bits, n, g->csc_off, g->csc_idx));
+  bmark("sort2");
+  GI_TRY(g->csc_off.alloc((n + 1) * (g->off64 ? sizeof(int64_t) : sizeof(int32_t))));
+  if (g->off64)
+    k_offsets32<int64_t><<<grid_for(n + 1, 256, sms), 256, 0, st>>>(vsorted, m, n, g->csc_off.as<int64_t>());
+  else
+    k_offsets32<int32_t><<<grid_for(n + 1, 256, sms), 256, 0, st>>>(vsorted, m, n, g->csc_off.as<int32_t>());
+  GI_CUDA(cudaGetLastError());
 
   // 10. pull tiling metadata
   g->ntiles = n > 0 ? ceil_div(n + m, kPullTile) : 0;
@@ -325,6 +390,12 @@ gi_status build_graph(gi_context ctx, int64_t n, int64_t m0, const int32_t* d_sr
   }
   GI_CUDA(cudaGetLastError());
   GI_CUDA(cudaStreamSynchronize(st));
+  bmark("csc+tiles");
+  if (bdbg)
+    if (FILE* f = fopen(bdbg, "a")) {
+      fprintf(f, "build n=%lld m0=%lld m=%lld:%s\n", (long long)n, (long long)m0, (long long)m, bphases.c_str());
+      fclose(f);
+    }
   return GI_OK;
 }
 
