@@ -106,6 +106,9 @@ struct MsArgs {
   uint8_t* par8;                     // light rows: par8[v * 64 + source bit] = index of the parent in v's
                                      //   in-edge list (< 32), 0xFF = v is that source itself
   const int32_t* __restrict__ hidx;  // heavy row -> its par row, -1 for a light row
+  int par_all;                       // k <= 16: every row keeps int32 parents, par[v * kp + source bit]
+                                     //   (64 bytes per row, the size of a byte row): no byte rows, no
+                                     //   read-merge-write, no in-edge scans in the push
   int64_t nact;
   unsigned long long all;            // mask of the k sources
 };
@@ -134,6 +137,30 @@ __device__ __forceinline__ void par_put(int32_t* row, unsigned long long m, int3
     } else {
       for (unsigned q = nm; q; q &= q - 1) row[8 * g + __ffs(q) - 1] = val;
     }
+    m &= ~(0xFFull << (8 * g));
+  }
+}
+
+// the par row of vertex w: its own in par_all mode, else its heavy row (-1: a byte row)
+__device__ __forceinline__ int64_t par_row(const MsArgs& A, int32_t w) {
+  return A.par_all ? (int64_t)w : (int64_t)__ldg(&A.hidx[w]);
+}
+
+// int32 parents of a row whose only writer is this thread (a pull): a sector
+// none of whose bits was known before (old) is written whole — the other
+// entries get placeholders, masked by seen at the end — so no sector is
+// partially written; other sectors one entry per new bit
+__device__ __forceinline__ void par_put_owner(int32_t* row, unsigned long long m, unsigned long long old,
+                                              int32_t val) {
+  while (m) {
+    const int g = (__ffsll((long long)m) - 1) >> 3;
+    const unsigned nm = (unsigned)(m >> (8 * g)) & 0xFFu;
+    if (((old >> (8 * g)) & 0xFFull) == 0ull) {
+      asm volatile("st.global.v8.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1};" ::"l"(row + 8 * g), "r"(val) : "memory");
+    } else {
+      for (unsigned q = nm; q; q &= q - 1) row[8 * g + __ffs(q) - 1] = val;
+    }
+    old |= (unsigned long long)nm << (8 * g);
     m &= ~(0xFFull << (8 * g));
   }
 }
@@ -255,7 +282,10 @@ __global__ void __launch_bounds__(kMsT, GI_MS_LMINB) k_ms_pull(MsArgs A) {
           for (int j = 0; j < kPullBatch; ++j) {
             const unsigned long long m = f[j] & ~s & ~found;
             if (m) {  // the parent of these bits: in-edge e + j - e0 of the row
-              if (GI_MS_OUT) par8_put(A.par8 + (int64_t)w * 64, m, (uint32_t)(e + j - e0));
+              if (GI_MS_OUT) {
+                if (A.par_all) par_put_owner(A.par + (int64_t)w * A.kp, m, s | found, in_id(A, v[j]));
+                else par8_put(A.par8 + (int64_t)w * 64, m, (uint32_t)(e + j - e0));
+              }
               found |= m;
             }
           }
@@ -322,7 +352,7 @@ __global__ void __launch_bounds__(kMsT, GI_MS_HMINB) k_ms_pull_heavy(MsArgs A, c
       const int64_t rb = (int64_t)off[w], re = (int64_t)off[w + 1];
       const int64_t e0 = rb + ch.y, e1 = min(re, e0 + kHChunk);
       const bool whole = re - rb <= kHChunk;  // the warp is the row's only writer this launch
-      int32_t* prow = A.par + (int64_t)__ldg(&A.hidx[w]) * A.kp;
+      int32_t* prow = A.par + par_row(A, w) * A.kp;
       // lane L keeps the parents of sources L (plo) and 32 + L (phi)
       int32_t plo = 0, phi = 0;
       unsigned long long found = 0;
@@ -489,9 +519,9 @@ __global__ void __launch_bounds__(kMsT) k_ms_push(MsArgs A, const long long* __r
           const unsigned long long got = m & ~atomicOr(&A.seen[w], m);  // the bits this edge claims
           if (got) {
             if (GI_MS_OUT) {
-              const int32_t h = __ldg(&A.hidx[w]);
+              const int64_t h = par_row(A, w);
               if (h >= 0) {
-                par_put(A.par + (int64_t)h * A.kp, got, in_id(A, u));
+                par_put(A.par + h * A.kp, got, in_id(A, u));
               } else {  // light row: u's position in w's in-edge list (< 32 entries, scanned 8 at a time)
                 const OffT* __restrict__ coff = static_cast<const OffT*>(A.csc_off);
                 const int64_t lo = (int64_t)coff[w], hi = (int64_t)coff[w + 1];
@@ -551,13 +581,14 @@ __global__ void __launch_bounds__(kMsT) k_ms_push(MsArgs A, const long long* __r
 __global__ void k_ms_init(const int32_t* __restrict__ src_in, int k, const int32_t* __restrict__ inv, int64_t n,
                           const int32_t* __restrict__ outdeg, unsigned long long* seen, unsigned long long* f0,
                           int32_t* act, unsigned long long* cnt, int32_t* par, int kp, uint8_t* par8,
-                          const int32_t* __restrict__ hidx) {
+                          const int32_t* __restrict__ hidx, int par_all) {
   const int i = threadIdx.x;
   if (i >= k) return;
   const int32_t si = src_in[i];
   const int32_t s = inv ? inv[si] : si;
   atomicOr(&seen[s], 1ull << i);
-  if (hidx[s] >= 0) par[(int64_t)hidx[s] * kp + i] = si;
+  const int64_t h = par_all ? (int64_t)s : (int64_t)hidx[s];
+  if (h >= 0) par[h * kp + i] = si;
   else par8[(int64_t)s * 64 + i] = 0xFF;  // the source is its own parent
   if (atomicOr(&f0[s], 1ull << i) == 0ull) {
     act[atomicAdd(&cnt[0], 1ull)] = s;
@@ -583,7 +614,7 @@ __global__ void __launch_bounds__(256) k_ms_finish_reg(const int32_t* __restrict
                                                       const int32_t* __restrict__ outdeg, int64_t n, int k,
                                                       int32_t* __restrict__ out,
                                                       unsigned long long* __restrict__ reached,
-                                                      unsigned long long* __restrict__ edges) {
+                                                      unsigned long long* __restrict__ edges, int par_all) {
   __shared__ unsigned long long r[64], d[64];
   __shared__ int32_t nbr[8][32][33];  // per warp and lane: a light row's in-neighbours in input ids
   const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
@@ -598,7 +629,7 @@ __global__ void __launch_bounds__(256) k_ms_finish_reg(const int32_t* __restrict
     const int32_t w = in ? (inv ? __ldg(&inv[v]) : (int32_t)v) : 0;
     const unsigned long long sv = in ? seen[w] : 0ull;
     const unsigned long long ov = in ? (unsigned long long)__ldg(&outdeg[w]) : 0ull;
-    const int32_t h = sv ? __ldg(&hidx[w]) : -1;
+    const int32_t h = sv ? (par_all ? w : __ldg(&hidx[w])) : -1;
     const bool light = sv && h < 0;
     uint4 p8[4] = {};
     if (light) {  // byte row (parent = an in-edge index) and the row's in-neighbours' input ids
@@ -751,7 +782,12 @@ gi_status msbfs_t(gi_graph g, int32_t k, const int32_t* sources, const gi_bfs_op
   int lkp = 3;  // par row: kp = 2^lkp >= k ints (whole 32-byte sectors, power-of-two tiles in the epilogue)
   while ((1 << lkp) < k) ++lkp;
   const int kp = 1 << lkp;
-  if (M.par.bytes < (size_t)(M.nheavy + 1) * kp * 4) GI_TRY(M.par.alloc((size_t)(M.nheavy + 1) * kp * 4));
+  // k <= 16: int32 parents for every row (64 bytes per row, like a byte row);
+  // GI_MS_PAR_ALL=0 keeps byte rows for the light rows (A/B)
+  static const bool par_all_env = !getenv("GI_MS_PAR_ALL") || atoi(getenv("GI_MS_PAR_ALL")) != 0;
+  const bool par_all = par_all_env && kp <= 16;
+  const int64_t par_rows = par_all ? n + 1 : M.nheavy + 1;
+  if (M.par.bytes < (size_t)par_rows * kp * 4) GI_TRY(M.par.alloc((size_t)par_rows * kp * 4));
   if (k <= 32 && M.fc.bytes < (size_t)(n + 1) * (k <= 16 ? 2 : 4)) GI_TRY(M.fc.alloc((size_t)(n + 1) * (k <= 16 ? 2 : 4)));
   cudaEvent_t e0 = nullptr, e1 = nullptr, pe0 = nullptr, pe1 = nullptr;
   int64_t pull_examined = 0;
@@ -776,7 +812,7 @@ gi_status msbfs_t(gi_graph g, int32_t k, const int32_t* sources, const gi_bfs_op
   k_ms_init<<<1, 64, 0, st>>>(M.src.as<int32_t>(), k, g->relabeled ? g->inv.as<int32_t>() : nullptr, n,
                               g->outdeg.as<int32_t>(), M.seen.as<unsigned long long>(), M.fr[0].as<unsigned long long>(),
                               M.act[0].as<int32_t>(), cnt, M.par.as<int32_t>(), kp, M.par8.as<uint8_t>(),
-                              M.hidx.as<int32_t>());
+                              M.hidx.as<int32_t>(), par_all ? 1 : 0);
   launches += 1;
   GI_CUDA(cudaMemcpyAsync(h, cnt, 4 * 8, cudaMemcpyDeviceToHost, st));
   GI_CUDA(stream_wait(st));
@@ -797,6 +833,7 @@ gi_status msbfs_t(gi_graph g, int32_t k, const int32_t* sources, const gi_bfs_op
   A.par8 = M.par8.as<uint8_t>();
   A.hidx = M.hidx.as<int32_t>();
   A.kp = kp;
+  A.par_all = par_all ? 1 : 0;
   A.all = k == 64 ? ~0ull : ((1ull << k) - 1ull);
   static const char* dbg = getenv("GI_DEBUG_MSBFS");  // diagnostics: per-level direction, size, time
   FILE* df = dbg ? fopen(dbg, "a") : nullptr;
@@ -880,7 +917,7 @@ gi_status msbfs_t(gi_graph g, int32_t k, const int32_t* sources, const gi_bfs_op
     fk<<<grid_for(n, 256, sms, 8), 256, 0, st>>>(
         M.par.as<int32_t>(), M.par8.as<uint8_t>(), M.hidx.as<int32_t>(), g->csc_off.as<OffT>(),
         M.csc_in.as<int32_t>(), M.seen.as<unsigned long long>(),
-        A.inv, g->outdeg.as<int32_t>(), n, k, d_out, hr, hr + 64);
+        A.inv, g->outdeg.as<int32_t>(), n, k, d_out, hr, hr + 64, A.par_all);
   }
   ++launches;
   std::vector<unsigned long long> hs(128);
