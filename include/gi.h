@@ -209,7 +209,8 @@ typedef struct {
                         block) in a streaming pass, summed per block in
                         shared memory in a second; chosen by GI_PR_PULL when
                         the segmented pull's pieces hold < 2.5 edges and
-                        contrib exceeds 64 MB, e.g. config 5) */
+                        contrib exceeds 64 MB, e.g. config 5; up to
+                        2048 x 49152 vertices, GI_ERR_UNSUPPORTED beyond) */
   int32_t dangling;  /* GI_DANGLING_UNIFORM (default) or GI_DANGLING_DROP
                         (paper-literal: no D term) */
   int32_t profile;   /* 1: fill gi_pr_stats kernel timings (CUDA events on the
