@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define GI_ABI_VERSION 1
+#define GI_ABI_VERSION 2
 
 #if defined(__GNUC__)
 #define GI_API __attribute__((visibility("default")))
@@ -295,8 +295,22 @@ typedef struct {
                             GI_BFS_BATCH_PER_SOURCE (one direction-optimising
                             traversal per source) or GI_BFS_BATCH_BITPARALLEL
                             (up to 64 sources per traversal, one bit each) */
+  int32_t pull_kernel;   /* bit-parallel passes only, their pull levels:
+                            GI_MS_PULL_AUTO (0), GI_MS_PULL_ROWS (each row scans
+                            its in-edges, gathering frontier masks, until it holds
+                            every source) or GI_MS_PULL_SEGMENTED (one OR pass of
+                            the PageRank edge kernel over the segmented layout —
+                            frontier masks staged per source segment in shared
+                            memory — then each new bit's parent by a row scan
+                            that stops once every new bit has one; passes of
+                            <= 32 sources on one GPU; builds the layout if the
+                            graph has none, else ROWS). AUTO takes the
+                            OR pass when the graph already has the layout and
+                            the rows still missing a source hold > 0.7 m
+                            (k <= 16) / 0.25 m (k <= 32) in-edges */
 } gi_bfs_opts;
 enum { GI_BFS_BATCH_AUTO = 0, GI_BFS_BATCH_PER_SOURCE = 1, GI_BFS_BATCH_BITPARALLEL = 2 };
+enum { GI_MS_PULL_AUTO = 0, GI_MS_PULL_ROWS = 1, GI_MS_PULL_SEGMENTED = 2 };
 
 typedef struct {
   int32_t levels;          /* frontier rounds executed */
@@ -314,6 +328,10 @@ typedef struct {
   int64_t pull_vertices;   /* vertex checks of the pull levels (n per level) */
   int64_t pull_edges_examined; /* the part of edges_examined read by pull levels
                                   (bit-parallel passes; 0 for per-source) */
+  int32_t pull_or_levels;  /* bit-parallel passes: pull levels run as a segmented
+                              OR pass (GI_MS_PULL_SEGMENTED); their edge reads
+                              count every in-edge */
+  int32_t reserved;
 } gi_bfs_stats;
 /* A bit-parallel pass serves up to 64 sources at once: its shared quantities
  * (total_ms, pull_ms, edges_examined, pull_vertices, pull_edges_examined) are

@@ -702,7 +702,8 @@ gi_status gi_bfs_multi(gi_graph g, int32_t k, const int32_t* sources, const gi_b
   gi_bfs_opts o{};
   if (opts) o = *opts;
   if (o.policy < GI_BFS_AUTO || o.policy > GI_BFS_PULL_ONLY || o.threshold_div < 0 ||
-      o.batch < GI_BFS_BATCH_AUTO || o.batch > GI_BFS_BATCH_BITPARALLEL)
+      o.batch < GI_BFS_BATCH_AUTO || o.batch > GI_BFS_BATCH_BITPARALLEL || o.pull_kernel < GI_MS_PULL_AUTO ||
+      o.pull_kernel > GI_MS_PULL_SEGMENTED)
     return fail(GI_ERR_INVALID_ARGUMENT, "gi_bfs_multi: bad options");
   const bool bitpar = o.batch == GI_BFS_BATCH_BITPARALLEL || (o.batch == GI_BFS_BATCH_AUTO && k >= 8);
   gi_context ctx = g->ctx;

@@ -271,6 +271,7 @@ struct gi_graph_s {
   struct {  // bit-parallel multi-source BFS (msbfs.cu)
     gi::DevBuf seen, fr[2], act[2], cnt, src, heavy, par, par8, hidx, csc_in;
     gi::DevBuf fc;       // the frontier masks narrowed to 16 / 32 bits for the pull gathers (k <= 32)
+    gi::DevBuf fc32, acc32, rlist;  // segmented OR pull: 32-bit masks, OR accumulator, heavy rows to resolve
     int64_t nheavy = 0;  // rows with in-degree >= 32 (pulled by whole warps)
     gi::DevBuf hch;      // their chunks: int2 (row, first in-edge offset)
     int64_t nhch = 0;
@@ -314,6 +315,7 @@ gi_status tile_rows_launch(const void* off, bool off64, int64_t n, int64_t m, in
 gi_status seg_edge_pass(gi_graph g, const float* cin);
 // a min pass over the segmented layout: acc[v] = min(acc[v], labels[u] over in-edges (u, v)) (CC, cc.cu)
 gi_status seg_min_pass(gi_graph g, const int32_t* labels, int32_t* acc);
+gi_status seg_or_pass(gi_graph g, const uint32_t* masks, uint32_t* acc);
 // bit-parallel BFS / CC shared state (g->ms): masks, active lists, heavy-row chunks
 gi_status ms_prepare(gi_graph g);
 // out-degree of an active vertex, as a scan input (the push levels' degree prefix

@@ -65,6 +65,12 @@ constexpr int kMsT = 256;
 #endif
 constexpr int64_t kHeavy = GI_MS_HEAVY;  // rows with at least this many in-edges are pulled by whole warps
 constexpr int kMsPullDiv = 8;     // bit-parallel direction rule: pull iff |F| + sum outdeg F > m / 8 (R21)
+// segmented OR pull iff the rows still missing a source hold > this fraction of
+// the in-edges: a row pull scans those rows to the end. With 16-bit masks the row
+// pull is cheap enough to win below ~0.6 m (config 4, 16 sources: level 2 at m
+// 3.95 vs 6.17 ms, level 3 at 0.56 m 3.8 vs 3.3 ms); 32-bit rows win nowhere
+// measured (config 2, 32 sources: every pull level faster as OR)
+constexpr double kSegOrFrac16 = 0.7, kSegOrFrac32 = 0.25;
 constexpr int kPushChunk = 256;   // push: out-edges per warp at least
 #ifndef GI_MS_BATCH
 #define GI_MS_BATCH 2
@@ -100,7 +106,8 @@ struct MsArgs {
   unsigned long long* fnext;
   const int32_t* __restrict__ acur;  // active vertices of the current level (push)
   int32_t* anext;                    // active vertices of the next level
-  unsigned long long* cnt;           // [0] |active next|, [1] sum outdeg, [2] OR of new bits, [3] edges examined
+  unsigned long long* cnt;           // [0] |active next|, [1] sum outdeg, [2] OR of new bits, [3] edges examined,
+                                     // [4] in-edges of the rows that got every source this level, [5] |rlist|
   int32_t* par;                      // heavy rows' parents (input ids): par[hidx[v] * kp + source bit]
   int kp;                            // par row stride: k rounded up to a power of two >= 8
   uint8_t* par8;                     // light rows: par8[v * 64 + source bit] = index of the parent in v's
@@ -111,6 +118,8 @@ struct MsArgs {
                                      //   read-merge-write, no in-edge scans in the push
   int64_t nact;
   unsigned long long all;            // mask of the k sources
+  const uint32_t* acc32;             // segmented OR pull: OR of each row's in-neighbours' frontier masks
+  int32_t* rlist;                    // segmented OR pull: heavy rows with new bits (parents resolved by warps)
 };
 
 __device__ __forceinline__ int32_t in_id(const MsArgs& A, int32_t v) { return A.perm ? __ldg(&A.perm[v]) : v; }
@@ -216,30 +225,35 @@ __device__ __forceinline__ void ms_warp_append(const MsArgs& A, bool act, int32_
 
 // the level's counters (cnt[1..3]), reduced over the CTA once at kernel end;
 // every thread of the CTA calls it
-__device__ __forceinline__ void ms_counters(const MsArgs& A, long long deg, unsigned long long bits, long long exam) {
-  __shared__ unsigned long long s_red[3 * (kMsT / 32)];
+__device__ __forceinline__ void ms_counters(const MsArgs& A, long long deg, unsigned long long bits, long long exam,
+                                            long long done) {
+  __shared__ unsigned long long s_red[4 * (kMsT / 32)];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   for (int o = 16; o > 0; o >>= 1) {
     deg += __shfl_xor_sync(0xffffffffu, deg, o);
     bits |= __shfl_xor_sync(0xffffffffu, bits, o);
     exam += __shfl_xor_sync(0xffffffffu, exam, o);
+    done += __shfl_xor_sync(0xffffffffu, done, o);
   }
   if (lane == 0) {
-    s_red[3 * w] = (unsigned long long)deg;
-    s_red[3 * w + 1] = bits;
-    s_red[3 * w + 2] = (unsigned long long)exam;
+    s_red[4 * w] = (unsigned long long)deg;
+    s_red[4 * w + 1] = bits;
+    s_red[4 * w + 2] = (unsigned long long)exam;
+    s_red[4 * w + 3] = (unsigned long long)done;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    unsigned long long d = 0, b = 0, x = 0;
+    unsigned long long d = 0, b = 0, x = 0, c = 0;
     for (int i = 0; i < kMsT / 32; ++i) {
-      d += s_red[3 * i];
-      b |= s_red[3 * i + 1];
-      x += s_red[3 * i + 2];
+      d += s_red[4 * i];
+      b |= s_red[4 * i + 1];
+      x += s_red[4 * i + 2];
+      c += s_red[4 * i + 3];
     }
     if (d) atomicAdd(&A.cnt[1], d);
     if (b) atomicOr(&A.cnt[2], b);
     if (x) atomicAdd(&A.cnt[3], x);
+    if (c) atomicAdd(&A.cnt[4], c);
   }
 }
 
@@ -260,7 +274,7 @@ __global__ void __launch_bounds__(kMsT, GI_MS_LMINB) k_ms_pull(MsArgs A) {
   int32_t* wbuf = s_buf[threadIdx.x >> 5];
   int nbuf = 0;
   const OffT* __restrict__ off = static_cast<const OffT*>(A.csc_off);
-  long long tdeg = 0, exam = 0;
+  long long tdeg = 0, exam = 0, tdone = 0;
   unsigned long long tbits = 0;
   for (int64_t b = blockIdx.x * (int64_t)kMsT; b < A.n; b += (int64_t)gridDim.x * kMsT) {
     const int32_t w = (int32_t)(b + threadIdx.x);
@@ -293,6 +307,7 @@ __global__ void __launch_bounds__(kMsT, GI_MS_LMINB) k_ms_pull(MsArgs A) {
         }
         if (found) {
           A.seen[w] = s | found;
+          if ((s | found) == A.all) tdone += e1 - e0;
           const int32_t deg = __ldg(&A.outdeg[w]);
           act = deg > 0;  // a sink never pushes: it stays out of the active list
           tdeg += deg;
@@ -304,7 +319,7 @@ __global__ void __launch_bounds__(kMsT, GI_MS_LMINB) k_ms_pull(MsArgs A) {
     ms_warp_append(A, act, w, wbuf, nbuf);
   }
   if (nbuf > 0) ms_warp_flush(A, wbuf, nbuf);
-  ms_counters(A, tdeg, tbits, exam);
+  ms_counters(A, tdeg, tbits, exam, tdone);
 }
 
 // pull for the heavy rows (in-degree >= kHeavy), edge-balanced: the rows are
@@ -340,7 +355,7 @@ __global__ void __launch_bounds__(kMsT, GI_MS_HMINB) k_ms_pull_heavy(MsArgs A, c
   const int64_t gw = blockIdx.x * (int64_t)(kMsT / 32) + wp;
   const int64_t per = (C + nw - 1) / nw;
   const int64_t c1 = min(C, (gw + 1) * per);
-  long long tdeg = 0, exam = 0;
+  long long tdeg = 0, exam = 0, tdone = 0;
   unsigned long long tbits = 0;
   int nbuf = 0;
   for (int64_t c = gw * per; c < c1; ++c) {
@@ -401,7 +416,8 @@ __global__ void __launch_bounds__(kMsT, GI_MS_HMINB) k_ms_pull_heavy(MsArgs A, c
         if (wh && 32 + lane < A.kp) prow[32 + lane] = phi;
       }
       if (found && lane == 0) {
-        atomicOr(&A.seen[w], found);
+        const unsigned long long old = atomicOr(&A.seen[w], found);
+        if (old != A.all && (old | found) == A.all) tdone += re - rb;  // this chunk completed the row
         tbits |= found;
         if (atomicOr(&A.fnext[w], found) == 0ull) {  // the row's first bits this level
           const int32_t d = __ldg(&A.outdeg[w]);
@@ -430,7 +446,7 @@ __global__ void __launch_bounds__(kMsT, GI_MS_HMINB) k_ms_pull_heavy(MsArgs A, c
     pos = __shfl_sync(0xffffffffu, pos, 0);
     if (lane < nbuf) A.anext[pos + lane] = s_buf[wp][lane];
   }
-  ms_counters(A, tdeg, tbits, exam);
+  ms_counters(A, tdeg, tbits, exam, tdone);
 }
 
 __global__ void k_ms_csc_in(const int32_t* __restrict__ idx, int64_t m, const int32_t* __restrict__ perm,
@@ -484,7 +500,7 @@ __global__ void __launch_bounds__(kMsT) k_ms_push(MsArgs A, const long long* __r
   int nbuf = 0;
   const int64_t nw = (int64_t)gridDim.x * (kMsT / 32);
   const int64_t gw = blockIdx.x * (int64_t)(kMsT / 32) + wp;
-  long long deg = 0, exam = 0;
+  long long deg = 0, exam = 0, done = 0;
   unsigned long long bits = 0;
   const long long E = A.nact > 0 ? __ldg(&dp[A.nact - 1]) : 0;
   const long long per = (E + nw - 1) / nw;
@@ -516,8 +532,13 @@ __global__ void __launch_bounds__(kMsT) k_ms_push(MsArgs A, const long long* __r
         ++exam;
         const unsigned long long m = A.fcur[u] & ~*(volatile unsigned long long*)&A.seen[w];
         if (m) {
-          const unsigned long long got = m & ~atomicOr(&A.seen[w], m);  // the bits this edge claims
+          const unsigned long long old = atomicOr(&A.seen[w], m);
+          const unsigned long long got = m & ~old;  // the bits this edge claims
           if (got) {
+            if ((old | got) == A.all) {  // this claim completed w: its in-edges leave the pull's scan mass
+              const OffT* __restrict__ coff = static_cast<const OffT*>(A.csc_off);
+              done += (long long)(coff[w + 1] - coff[w]);
+            }
             if (GI_MS_OUT) {
               const int64_t h = par_row(A, w);
               if (h >= 0) {
@@ -574,7 +595,147 @@ __global__ void __launch_bounds__(kMsT) k_ms_push(MsArgs A, const long long* __r
     pos = __shfl_sync(0xffffffffu, pos, 0);
     if (lane < nbuf) A.anext[pos + lane] = s_buf[wp][lane];
   }
-  ms_counters(A, deg, bits, exam);
+  ms_counters(A, deg, bits, exam, done);
+}
+
+// ---- segmented OR pull (dense pull levels of passes of <= 32 sources) ----
+// A pull level whose rows would mostly scan to the end (rows stop early only
+// once they hold every source) runs as one pass of the PageRank edge kernel over
+// the segmented layout with the reduction swapped for OR (pr_segmented.cu,
+// seg_or_pass): acc32[v] = OR over v's in-edges of the 32-bit frontier masks,
+// staged per source segment in shared memory, so every edge costs a shared-memory
+// gather instead of an L2 gather. The level's new bits are then acc32 & ~seen,
+// exactly the pull's result; each new bit's parent is found by scanning the row's
+// in-edges only until every NEW bit has a frontier in-neighbour (light rows a
+// thread each in k_ms_or_vertex, heavy rows a warp each in k_ms_resolve_heavy).
+
+// the frontier masks of an OR level: 32-bit words (staged by the OR pass) and,
+// k <= 16, the 16-bit copy the parent resolution gathers
+__global__ void k_ms_narrow_or(const unsigned long long* __restrict__ f, int64_t n, uint32_t* __restrict__ o32,
+                               uint16_t* __restrict__ o16) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned long long x = f[v];
+    o32[v] = (uint32_t)x;
+    if (o16) o16[v] = (uint16_t)x;
+  }
+}
+
+// the level's vertex pass: new = acc32 & ~seen; seen, next frontier, active list,
+// counters; a light row's parents found by its thread, a heavy row queued in rlist
+template <typename OffT, typename FM>
+__global__ void __launch_bounds__(kMsT) k_ms_or_vertex(MsArgs A) {
+  __shared__ int32_t s_buf[kMsT / 32][64];
+  int32_t* wbuf = s_buf[threadIdx.x >> 5];
+  int nbuf = 0;
+  const int lane = threadIdx.x & 31;
+  const OffT* __restrict__ off = static_cast<const OffT*>(A.csc_off);
+  long long tdeg = 0, exam = 0, tdone = 0;
+  unsigned long long tbits = 0;
+  for (int64_t b = blockIdx.x * (int64_t)kMsT; b < A.n; b += (int64_t)gridDim.x * kMsT) {
+    const int32_t w = (int32_t)(b + threadIdx.x);
+    bool act = false, heavy = false;
+    if (w < A.n) {
+      const unsigned long long s = A.seen[w];
+      const unsigned long long nb = (unsigned long long)__ldcs(&A.acc32[w]) & ~s & A.all;
+      A.fnext[w] = nb;
+      if (nb) {
+        A.seen[w] = s | nb;
+        const int64_t e0 = (int64_t)off[w], e1 = (int64_t)off[w + 1];
+        if ((s | nb) == A.all) tdone += e1 - e0;
+        const int32_t deg = __ldg(&A.outdeg[w]);
+        act = deg > 0;
+        tdeg += deg;
+        tbits |= nb;
+        if (e1 - e0 >= kHeavy) {
+          heavy = true;
+        } else {  // the parents of the new bits: the first frontier in-neighbour bringing each
+          unsigned long long rem = nb, known = s;
+          for (int64_t e = e0; rem && e < e1; e += kPullBatch) {
+            int32_t v[kPullBatch];
+            unsigned long long f[kPullBatch];
+#pragma unroll
+            for (int j = 0; j < kPullBatch; ++j) v[j] = e + j < e1 ? ms_idx(&A.csc_idx[e + j]) : -1;
+#pragma unroll
+            for (int j = 0; j < kPullBatch; ++j) f[j] = v[j] >= 0 ? ms_fget<FM>(A, v[j]) : 0ull;
+            exam += min((int64_t)kPullBatch, e1 - e);
+#pragma unroll
+            for (int j = 0; j < kPullBatch; ++j) {
+              const unsigned long long m = f[j] & rem;
+              if (m) {
+                if (GI_MS_OUT) {
+                  if (A.par_all) par_put_owner(A.par + (int64_t)w * A.kp, m, known, in_id(A, v[j]));
+                  else par8_put(A.par8 + (int64_t)w * 64, m, (uint32_t)(e + j - e0));
+                }
+                known |= m;
+                rem &= ~m;
+              }
+            }
+          }
+        }
+      }
+    }
+    const unsigned hm = __ballot_sync(0xffffffffu, heavy);
+    if (hm) {  // queue the warp's heavy rows (one atomic per warp step)
+      unsigned long long base = 0;
+      if (lane == 0) base = atomicAdd(&A.cnt[5], (unsigned long long)__popc(hm));
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (heavy) A.rlist[base + __popc(hm & ((1u << lane) - 1u))] = w;
+    }
+    ms_warp_append(A, act, w, wbuf, nbuf);
+  }
+  if (nbuf > 0) ms_warp_flush(A, wbuf, nbuf);
+  ms_counters(A, tdeg, tbits, exam, tdone);
+}
+
+// heavy rows with new bits (rlist, cnt[5] of them), a warp per row: 32 x
+// kPullBatch in-edges per step until every new bit has a parent (the lowest lane
+// bringing it: bit-matrix transpose, lane L ends up with source L's parent)
+template <typename OffT, typename FM>
+__global__ void __launch_bounds__(kMsT) k_ms_resolve_heavy(MsArgs A) {
+  const OffT* __restrict__ off = static_cast<const OffT*>(A.csc_off);
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t)gridDim.x * (kMsT / 32);
+  const int64_t R = (int64_t)*(volatile unsigned long long*)&A.cnt[5];
+  long long exam = 0;
+  for (int64_t i = blockIdx.x * (int64_t)(kMsT / 32) + (threadIdx.x >> 5); i < R; i += nw) {
+    const int32_t w = __ldg(&A.rlist[i]);
+    const unsigned long long nb = A.fnext[w];          // this level's new bits (k_ms_or_vertex)
+    const unsigned long long known = A.seen[w] & ~nb;  // bits of earlier levels
+    const int64_t e0 = (int64_t)off[w], e1 = (int64_t)off[w + 1];
+    unsigned rem = (unsigned)nb;  // k <= 32
+    int32_t plo = 0;
+    for (int64_t b = e0; rem && b < e1; b += 32 * kPullBatch) {
+      int32_t v[kPullBatch];
+      unsigned f[kPullBatch];
+#pragma unroll
+      for (int j = 0; j < kPullBatch; ++j) {
+        const int64_t e = b + 32 * j + lane;
+        v[j] = e < e1 ? ms_idx(&A.csc_idx[e]) : -1;
+      }
+#pragma unroll
+      for (int j = 0; j < kPullBatch; ++j) f[j] = v[j] >= 0 ? (unsigned)ms_fget<FM>(A, v[j]) : 0u;
+      if (lane == 0) exam += min((int64_t)32 * kPullBatch, e1 - b);
+#pragma unroll
+      for (int j = 0; j < kPullBatch; ++j) {
+        const unsigned mj = f[j] & rem;
+        const unsigned lo = __reduce_or_sync(0xffffffffu, mj);
+        if (!lo) continue;
+        const int32_t vin = mj ? in_id(A, v[j]) : 0;
+        const unsigned tl = warp_transpose32(mj);
+        const int32_t p = __shfl_sync(0xffffffffu, vin, tl ? __ffs(tl) - 1 : 0);
+        if (tl) plo = p;
+        rem &= ~lo;
+      }
+    }
+    if (GI_MS_OUT) {  // a sector without earlier bits is written whole (placeholders), else the new entries
+      int32_t* prow = A.par + par_row(A, w) * A.kp;
+      const unsigned kl = (unsigned)known, nl = (unsigned)nb;
+      const int sh = lane & ~7;
+      const bool wl = ((nl >> lane) & 1u) || (((nl >> sh) & 0xFFu) && !((kl >> sh) & 0xFFu));
+      if (wl && lane < A.kp) prow[lane] = plo;
+    }
+  }
+  ms_counters(A, 0, 0ull, exam, 0);
 }
 
 // sources: bit i at source i (internal id), its own parent in row i, active list
@@ -711,7 +872,7 @@ static gi_status ms_prepare_t(gi_graph g) {
       GI_TRY(M.fr[c].alloc((n + 1) * 8));
       GI_TRY(M.act[c].alloc((n + 1) * 4));
     }
-    GI_TRY(M.cnt.alloc(4 * 8 + 2 * 64 * 8));
+    GI_TRY(M.cnt.alloc(8 * 8 + 2 * 64 * 8));
     GI_TRY(M.src.alloc(64 * 4));
     GI_TRY(M.heavy.alloc((n + 1) * 4));
     GI_TRY(M.chunks[0].alloc((n + 1) * 8));
@@ -807,7 +968,7 @@ gi_status msbfs_t(gi_graph g, int32_t k, const int32_t* sources, const gi_bfs_op
   int launches = 0;
   GI_CUDA(cudaMemsetAsync(M.seen.p, 0, n * 8, st));
   GI_CUDA(cudaMemsetAsync(M.fr[0].p, 0, n * 8, st));
-  GI_CUDA(cudaMemsetAsync(cnt, 0, 4 * 8 + 2 * 64 * 8, st));
+  GI_CUDA(cudaMemsetAsync(cnt, 0, 8 * 8 + 2 * 64 * 8, st));
   GI_CUDA(cudaMemcpyAsync(M.src.p, sources, k * sizeof(int32_t), cudaMemcpyHostToDevice, st));
   k_ms_init<<<1, 64, 0, st>>>(M.src.as<int32_t>(), k, g->relabeled ? g->inv.as<int32_t>() : nullptr, n,
                               g->outdeg.as<int32_t>(), M.seen.as<unsigned long long>(), M.fr[0].as<unsigned long long>(),
@@ -835,6 +996,25 @@ gi_status msbfs_t(gi_graph g, int32_t k, const int32_t* sources, const gi_bfs_op
   A.kp = kp;
   A.par_all = par_all ? 1 : 0;
   A.all = k == 64 ? ~0ull : ((1ull << k) - 1ull);
+  // segmented OR pull (k <= 32, one GPU, a graph with the segmented layout):
+  // AUTO takes it for a pull level while the rows still missing sources hold more
+  // than segor_frac x m in-edges; GI_MS_PULL_SEGMENTED takes it for every pull
+  // level, building the layout if needed
+  static const char* frac_env = getenv("GI_MS_SEGOR_FRAC");
+  const double segor_frac = frac_env ? atof(frac_env) : k <= 16 ? kSegOrFrac16 : kSegOrFrac32;
+  const bool segor_ok = o.pull_kernel != GI_MS_PULL_ROWS && k <= 32 && ctx->nranks == 1 && g->ml > 0;
+  bool segor_ready = segor_ok && g->seg_Z != 0;
+  if (segor_ok && !segor_ready && o.pull_kernel == GI_MS_PULL_SEGMENTED) {
+    GI_TRY(seg_build(g, 0, 0));
+    segor_ready = true;
+  }
+  if (segor_ready) {
+    if (M.fc32.bytes < (size_t)(n + 16) * 4) GI_TRY(M.fc32.alloc((size_t)(n + 16) * 4));
+    if (M.acc32.bytes < (size_t)(n + 16) * 4) GI_TRY(M.acc32.alloc((size_t)(n + 16) * 4));
+    if (M.rlist.bytes < (size_t)(n + 1) * 4) GI_TRY(M.rlist.alloc((size_t)(n + 1) * 4));
+  }
+  int64_t inc = g->ml;  // in-edges of the rows still missing a source
+  int segor_levels = 0;
   static const char* dbg = getenv("GI_DEBUG_MSBFS");  // diagnostics: per-level direction, size, time
   FILE* df = dbg ? fopen(dbg, "a") : nullptr;
   for (int level = 0; nact > 0; ++level) {
@@ -845,11 +1025,36 @@ gi_status msbfs_t(gi_graph g, int32_t k, const int32_t* sources, const gi_bfs_op
     A.acur = M.act[c].as<int32_t>();
     A.anext = M.act[c ^ 1].as<int32_t>();
     A.nact = nact;
-    GI_CUDA(cudaMemsetAsync(cnt, 0, 4 * 8, st));
+    GI_CUDA(cudaMemsetAsync(cnt, 0, 6 * 8, st));
     const bool pull = o.policy == GI_BFS_PULL_ONLY ? level > 0
                                                    : (o.policy == GI_BFS_AUTO && nact + sdeg > mdiv);
+    const bool segor = pull && segor_ready &&
+                       (o.pull_kernel == GI_MS_PULL_SEGMENTED || (double)inc > segor_frac * (double)g->ml);
     if (pull && o.profile) GI_CUDA(cudaEventRecord(pe0, st));
-    if (pull) {
+    if (segor) {
+      const bool f16 = k <= 16;
+      k_ms_narrow_or<<<grid_for(n, 256, sms, 8), 256, 0, st>>>(A.fcur, n, M.fc32.as<uint32_t>(),
+                                                              f16 ? M.fc.as<uint16_t>() : nullptr);
+      GI_CUDA(cudaMemsetAsync(M.acc32.p, 0, (size_t)(n + 1) * 4, st));
+      GI_TRY(seg_or_pass(g, M.fc32.as<uint32_t>(), M.acc32.as<uint32_t>()));
+      A.acc32 = M.acc32.as<uint32_t>();
+      A.rlist = M.rlist.as<int32_t>();
+      const int lg = grid_for(n, kMsT, sms, kLightPerSM);
+      const unsigned rg = (unsigned)(sms * 8);
+      if (f16) {
+        A.fc = M.fc.p;
+        k_ms_or_vertex<OffT, uint16_t><<<lg, kMsT, 0, st>>>(A);
+        k_ms_resolve_heavy<OffT, uint16_t><<<rg, kMsT, 0, st>>>(A);
+      } else {
+        A.fc = M.fc32.p;
+        k_ms_or_vertex<OffT, uint32_t><<<lg, kMsT, 0, st>>>(A);
+        k_ms_resolve_heavy<OffT, uint32_t><<<rg, kMsT, 0, st>>>(A);
+      }
+      launches += 4;
+      if (o.profile) GI_CUDA(cudaEventRecord(pe1, st));
+      ++pulls;
+      ++segor_levels;
+    } else if (pull) {
       const int fw = k <= 16 ? 2 : k <= 32 ? 4 : 8;  // bytes per gathered frontier mask
       const int lg = grid_for(n, kMsT, sms, kLightPerSM);
       const int64_t hw = (M.nhch + kHeavyPer - 1) / kHeavyPer;
@@ -888,14 +1093,17 @@ gi_status msbfs_t(gi_graph g, int32_t k, const int32_t* sources, const gi_bfs_op
     }
     GI_CUDA(cudaGetLastError());
     ++launches;
-    GI_CUDA(cudaMemcpyAsync(h, cnt, 4 * 8, cudaMemcpyDeviceToHost, st));
+    GI_CUDA(cudaMemcpyAsync(h, cnt, 6 * 8, cudaMemcpyDeviceToHost, st));
     GI_CUDA(stream_wait(st));
+    if (segor) h[3] += g->ml;  // the OR pass reads every in-edge (+ the parent scans)
     if (df)
-      fprintf(df, "level=%d %s nact=%lld sdeg=%lld -> next=%lld examined=%lld us=%.1f\n", level, pull ? "pull" : "push",
-              (long long)nact, (long long)sdeg, (long long)h[0], (long long)h[3],
+      fprintf(df, "level=%d %s nact=%lld sdeg=%lld inc=%lld -> next=%lld examined=%lld us=%.1f\n", level,
+              segor ? "pull-or" : pull ? "pull" : "push", (long long)nact, (long long)sdeg, (long long)inc,
+              (long long)h[0], (long long)h[3],
               std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - tl0).count());
     nact = h[0];
     sdeg = h[1];
+    inc -= h[4];
     examined += h[3];
     if (pull) {
       pull_examined += h[3];
@@ -909,7 +1117,7 @@ gi_status msbfs_t(gi_graph g, int32_t k, const int32_t* sources, const gi_bfs_op
       if ((h[2] >> i) & 1) levels[i] = level + 2;  // source i still found vertices at this level
   }
   if (df) fclose(df);
-  unsigned long long* hr = cnt + 4;
+  unsigned long long* hr = cnt + 8;
   GI_CUDA(cudaMemsetAsync(hr, 0, 2 * 64 * 8, st));
   {  // epilogue: the k output rows + per-source counts (R16)
     auto* fk = kp == 8 ? k_ms_finish_reg<OffT, 8> : kp == 16 ? k_ms_finish_reg<OffT, 16>
@@ -944,6 +1152,7 @@ gi_status msbfs_t(gi_graph g, int32_t k, const int32_t* sources, const gi_bfs_op
       s.total_ms = ms / (float)k;
       s.pull_ms = pull_ms / (float)k;
       s.pull_edges_examined = pull_examined / k;
+      s.pull_or_levels = segor_levels;
       s.launches = i == 0 ? launches : 0;
       stats[i] = s;
     }

@@ -214,6 +214,16 @@ struct OpMin {
   static __device__ __forceinline__ T op(T a, T b) { return min(a, b); }
   static __device__ __forceinline__ void red(T* p, T v) { atomicMin(p, v); }
 };
+// the bit-parallel BFS's dense pull levels (msbfs.cu): the OR of the in-neighbours'
+// 32-bit frontier masks (RED.OR.B32)
+struct OpOr {
+  using T = uint32_t;
+  static __device__ __forceinline__ T id() { return 0u; }
+  static __device__ __forceinline__ T op(T a, T b) { return a | b; }
+  static __device__ __forceinline__ void red(T* p, T v) {
+    if (v) atomicOr(p, v);  // a piece that brings no frontier bit needs no atomic
+  }
+};
 
 // a value of the unit's segment: from the staged copy in shared memory, or (G:
 // a sparse unit, not staged) straight from global memory; offset Z is the
@@ -1304,6 +1314,37 @@ gi_status seg_min_pass(gi_graph g, const int32_t* labels, int32_t* acc) {
     attr_min[dev] = dyn;
   }
   GI_TRY(launch_pdl(k_pr_seg<0, OpMin>, g->seg_ctas, kSegThreads, dyn, st, S));
+  return GI_OK;
+}
+
+// One OR pass over the segmented layout (the bit-parallel BFS's dense pull
+// levels, msbfs.cu): acc[v] |= OR over v's in-edges (u, v) of masks[u]; masks
+// padded by >= 16 words, acc zeroed for rows 0..n (row n: padding lanes).
+gi_status seg_or_pass(gi_graph g, const uint32_t* masks, uint32_t* acc) {
+  cudaStream_t st = g->ctx->stream;
+  SegArgs S;
+  S.rec = g->seg_rec.as<uint8_t>();
+  S.unit_c0 = g->seg_unit_c0.as<int32_t>();
+  S.cta_c0 = g->seg_cta.as<int32_t>();
+  S.cta_u = g->seg_cta.as<int32_t>() + g->seg_ctas + 1;
+  S.cin = reinterpret_cast<const float*>(masks);  // raw 4-byte words: the kernel reads them as uint32
+  S.acc = reinterpret_cast<float*>(acc);
+  S.n = g->n;
+  S.Z = g->seg_Z;
+  S.S = g->seg_S;
+  S.U = g->seg_U;
+  S.timing = nullptr;
+  S.ht = g->seg_ht.as<unsigned long long>();
+  S.trash = (int)g->nr;
+  S.steal = g->seg_steal;
+  const size_t dyn = seg_dyn_smem(g->seg_Z);
+  static size_t attr_or[64] = {};
+  const int dev = g->ctx->device & 63;
+  if (attr_or[dev] < dyn) {
+    GI_CUDA(cudaFuncSetAttribute(k_pr_seg<0, OpOr>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+    attr_or[dev] = dyn;
+  }
+  GI_TRY(launch_pdl(k_pr_seg<0, OpOr>, g->seg_ctas, kSegThreads, dyn, st, S));
   return GI_OK;
 }
 

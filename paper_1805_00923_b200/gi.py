@@ -44,6 +44,7 @@ GI_DANGLING_UNIFORM, GI_DANGLING_DROP = 0, 1
 GI_BFS_AUTO, GI_BFS_PUSH_ONLY, GI_BFS_PULL_ONLY = 0, 1, 2
 GI_PRD_AUTO, GI_PRD_PUSH_ONLY, GI_PRD_PULL_ONLY = 0, 1, 2
 GI_BFS_BATCH_AUTO, GI_BFS_BATCH_PER_SOURCE, GI_BFS_BATCH_BITPARALLEL = 0, 1, 2
+GI_MS_PULL_AUTO, GI_MS_PULL_ROWS, GI_MS_PULL_SEGMENTED = 0, 1, 2
 
 
 class gi_pr_opts(ctypes.Structure):
@@ -82,7 +83,7 @@ class gi_prdelta_stats(ctypes.Structure):
 
 class gi_bfs_opts(ctypes.Structure):
     _fields_ = [("policy", ctypes.c_int32), ("threshold_div", ctypes.c_int32), ("profile", ctypes.c_int32),
-                ("batch", ctypes.c_int32)]
+                ("batch", ctypes.c_int32), ("pull_kernel", ctypes.c_int32)]
 
 
 class gi_cc_opts(ctypes.Structure):
@@ -99,7 +100,8 @@ class gi_bfs_stats(ctypes.Structure):
     _fields_ = [("levels", ctypes.c_int32), ("pull_levels", ctypes.c_int32), ("reached", ctypes.c_int64),
                 ("edges_traversed", ctypes.c_int64), ("total_ms", ctypes.c_float), ("launches", ctypes.c_int32),
                 ("pull_ms", ctypes.c_float), ("edges_examined", ctypes.c_int64), ("pull_vertices", ctypes.c_int64),
-                ("pull_edges_examined", ctypes.c_int64)]
+                ("pull_edges_examined", ctypes.c_int64), ("pull_or_levels", ctypes.c_int32),
+                ("reserved", ctypes.c_int32)]
 
 
 _vp = ctypes.c_void_p
@@ -151,6 +153,9 @@ for _name, (_args, _res) in _SIGS.items():
     _f.restype = _res
 
 EXPORTED = tuple(_SIGS)
+GI_ABI_VERSION = 2  # include/gi.h: the struct layouts above
+if _lib.gi_abi_version() != GI_ABI_VERSION:
+    raise ImportError(f"{LIB_PATH} has ABI version {_lib.gi_abi_version()}, the binding {GI_ABI_VERSION}: rebuild it")
 
 
 class GiError(RuntimeError):
@@ -441,7 +446,7 @@ def gi_sssp_weighted(g: int, source: int, weights, out=None, policy: int = GI_BF
 
 
 def gi_bfs_multi(g: int, sources, out=None, policy: int = GI_BFS_AUTO, threshold_div: int = 0,
-                 profile: bool = False, batch: int = GI_BFS_BATCH_AUTO):
+                 profile: bool = False, batch: int = GI_BFS_BATCH_AUTO, pull_kernel: int = GI_MS_PULL_AUTO):
     """k BFS runs back to back; out: int32[k, n] (host or device). Returns (out, [stats])."""
     n = gi_graph_num_vertices(g)
     src = np.ascontiguousarray(np.asarray(sources, dtype=np.int64).astype(np.int32))
@@ -449,7 +454,7 @@ def gi_bfs_multi(g: int, sources, out=None, policy: int = GI_BFS_AUTO, threshold
     if out is None:
         out = np.empty((k, n), np.int32)
     p, keep = _ptr(out, np.int32)
-    o = gi_bfs_opts(policy, threshold_div, int(profile), batch)
+    o = gi_bfs_opts(policy, threshold_div, int(profile), batch, pull_kernel)
     stats = (gi_bfs_stats * max(k, 1))()
     _check(_lib.gi_bfs_multi(g, k, src.ctypes.data if k else None, ctypes.byref(o), p or None, stats),
            "gi_bfs_multi")

@@ -508,6 +508,81 @@ def test_bfs_multi_bitparallel_mask_widths(gi, ctx, k):
     g.close()
 
 
+@pytest.mark.parametrize("k", [8, 16, 17, 32])
+def test_bfs_multi_segmented_or_pull(gi, ctx, k):
+    """Bit-parallel pull levels as an OR pass over the segmented layout (GI_MS_PULL_SEGMENTED):
+    every width it takes (16-bit parent-scan masks for k <= 16, 32-bit above), every direction
+    policy, on layouts with one, two and many source segments / destination blocks (pieces split
+    across records and CTAs, unstaged sparse units), a hub row of 100k in-edges (a heavy row
+    resolved by a warp) and a graph without relabelling.
+    Each row is validated against the oracle (exact depths, valid parents); the stats say which
+    kernel ran."""
+    cfg = graphgen.CONFIGS[1]
+    cases = [("rmat", cfg.n, *cfg.edges(), 0, 0),
+             ("rmat-small-segments", cfg.n, *cfg.edges(), 4096, 20000),
+             ("random", 70001, *graphgen.random_digraph(70001, 1000003, 5), 1000, 0),
+             ("star", 100001, *graphgen.star_bidirectional(100000), 0, 0)]
+    for name, n, s, d, seg, dblk in cases:
+        g = gi.Graph(ctx, n, s, d)
+        go = oracle.build_graph(n, s, d)
+        if seg or dblk:  # the layout PageRank builds with these parameters, reused by the BFS
+            g.pagerank(1, 0.85, direction=gi.GI_PR_PULL_SEGMENTED, segment_size=seg, dst_block=dblk)
+        sources = graphgen.pick_sources(n, s, d, k, 300 + k).tolist() if name != "star" else \
+            list(range(1, k)) + [0]
+        for policy in POLICIES:
+            par, st = g.bfs_multi(sources, batch=gi.GI_BFS_BATCH_BITPARALLEL, policy=_pol(gi, policy),
+                                  pull_kernel=gi.GI_MS_PULL_SEGMENTED)
+            assert st[0].pull_or_levels == st[0].pull_levels
+            if policy == "pull":
+                assert st[0].pull_or_levels > 0
+            for i, src in enumerate(sources):
+                depth = oracle.bfs_depth(go, src)
+                ok, msg = oracle.validate_bfs(go, src, par[i], depth)
+                assert ok, f"{name} k={k} {policy} src={src}: {msg}"
+                assert st[i].reached == int((depth >= 0).sum())
+                assert st[i].levels == depth.max() + 1
+                assert st[i].edges_traversed == oracle.reached_out_edges(go, depth)
+        g.close()
+    # no relabelling (internal ids = input ids, no permutation in the parent scans)
+    s, d = cfg.edges()
+    g = gi.Graph(ctx, cfg.n, s, d, gi.GI_DEFAULT_FLAGS | gi.GI_NO_RELABEL)
+    go = oracle.build_graph(cfg.n, s, d)
+    sources = graphgen.pick_sources(cfg.n, s, d, k, 400 + k).tolist()
+    par, st = g.bfs_multi(sources, batch=gi.GI_BFS_BATCH_BITPARALLEL, policy=gi.GI_BFS_PULL_ONLY,
+                          pull_kernel=gi.GI_MS_PULL_SEGMENTED)
+    assert st[0].pull_or_levels == st[0].pull_levels > 0
+    for i, src in enumerate(sources):
+        ok, msg = oracle.validate_bfs(go, src, par[i], oracle.bfs_depth(go, src))
+        assert ok, f"norelabel k={k} src={src}: {msg}"
+    g.close()
+
+
+def test_bfs_multi_or_pull_auto(gi, ctx):
+    """AUTO pull kernel: after a PageRank call has built the segmented layout, the dense pull
+    levels of a 16-source pass run as OR passes (rows missing sources hold > m/4 in-edges);
+    GI_MS_PULL_ROWS keeps the row pull. Both validated against the oracle."""
+    cfg = graphgen.CONFIGS[1]
+    s, d = cfg.edges()
+    g = gi.Graph(ctx, cfg.n, s, d)
+    go = oracle.build_graph(cfg.n, s, d)
+    sources = graphgen.pick_sources(cfg.n, s, d, 16, 501).tolist()
+    _, st0 = g.bfs_multi(sources, batch=gi.GI_BFS_BATCH_BITPARALLEL)
+    assert st0[0].pull_or_levels == 0  # no layout yet
+    g.pagerank(2, 0.85, direction=gi.GI_PR_PULL_SEGMENTED)
+    for pk in (gi.GI_MS_PULL_AUTO, gi.GI_MS_PULL_ROWS):
+        par, st = g.bfs_multi(sources, batch=gi.GI_BFS_BATCH_BITPARALLEL, pull_kernel=pk)
+        assert (st[0].pull_or_levels > 0) == (pk == gi.GI_MS_PULL_AUTO and st[0].pull_levels > 0)
+        for i, src in enumerate(sources):
+            depth = oracle.bfs_depth(go, src)
+            ok, msg = oracle.validate_bfs(go, src, par[i], depth)
+            assert ok, f"pull_kernel={pk} src={src}: {msg}"
+            assert st[i].edges_traversed == st0[i].edges_traversed
+    with pytest.raises(gi.GiError) as e:
+        g.bfs_multi(sources, pull_kernel=3)
+    assert e.value.status == gi.GI_ERR_INVALID_ARGUMENT
+    g.close()
+
+
 def test_bfs_multi_bitparallel_edge_cases(gi, ctx):
     """Bit-parallel passes on degenerate inputs: no edges; isolated and sink
     sources; k = 1, 64 and 65; a 100k-leaf star under every direction policy —
