@@ -43,6 +43,7 @@ struct BigEntry {
 std::mutex g_big_mu;
 std::vector<BigEntry> g_big;
 size_t g_big_total = 0;
+uint64_t g_big_mallocs = 0;  // cudaMalloc / cudaFree events of large blocks (free-memory checks)
 // GI_DEBUG_BIGCACHE=1: one stderr line per miss / eviction (diagnostics)
 bool big_debug() {
   static const bool v = getenv("GI_DEBUG_BIGCACHE") && atoi(getenv("GI_DEBUG_BIGCACHE")) != 0;
@@ -80,16 +81,25 @@ void big_cache_put(void* p, size_t bytes, cudaStream_t s) {
   int dev = -1;
   cudaGetDevice(&dev);
   // the device must keep kBigMinFree bytes free for everybody else (torch's allocator,
-  // other contexts): cached blocks count as used
-  size_t fr = 0, tot = 0;
-  if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) {
-    cudaGetLastError();
-    fr = 0;
-  }
+  // other contexts): cached blocks count as used. cudaMemGetInfo can take tens of ms,
+  // so it is asked only when a block was cudaMalloc'd since the last answer (a block
+  // moving between use and the cache does not change the device's free memory)
   constexpr size_t kBigMinFree = 24ull << 30;
   std::vector<void*> drop;
   {
     std::lock_guard<std::mutex> lk(g_big_mu);
+    static uint64_t checked = ~0ull;
+    static size_t fr_seen = 0;
+    if (checked != g_big_mallocs) {
+      size_t f = 0, tot = 0;
+      if (cudaMemGetInfo(&f, &tot) != cudaSuccess) {
+        cudaGetLastError();
+        f = 0;
+      }
+      fr_seen = f;
+      checked = g_big_mallocs;
+    }
+    size_t fr = fr_seen;
     if (bytes > big_cap()) {
       drop.push_back(p);
     } else {
@@ -107,9 +117,28 @@ void big_cache_put(void* p, size_t bytes, cudaStream_t s) {
       }
     }
   }
+  {
+    std::lock_guard<std::mutex> lk(g_big_mu);
+    for (size_t i = 0; i < drop.size(); ++i) ++g_big_mallocs;  // frees change the device's free memory too
+  }
   if (big_debug() && !drop.empty())
-    fprintf(stderr, "bigcache put %.2f GB: %zu blocks freed (device free %.2f GB)\n", bytes / 1e9, drop.size(), fr / 1e9);
+    fprintf(stderr, "bigcache put %.2f GB: %zu blocks freed\n", bytes / 1e9, drop.size());
   for (void* q : drop) cudaFree(q);
+}
+
+double slow_ms() {
+  static const double v = getenv("GI_DEBUG_SLOW_MS") ? atof(getenv("GI_DEBUG_SLOW_MS")) : 0.0;
+  return v;
+}
+
+void slow_report(const char* what, size_t bytes, std::chrono::steady_clock::time_point t0) {
+  const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  if (ms > slow_ms()) fprintf(stderr, "slow %s %.3f GB: %.1f ms\n", what, bytes / 1e9, ms);
+}
+
+void big_cache_note_malloc() {
+  std::lock_guard<std::mutex> lk(g_big_mu);
+  ++g_big_mallocs;
 }
 
 void big_cache_flush(cudaStream_t s) {

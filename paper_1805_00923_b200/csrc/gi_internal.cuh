@@ -9,6 +9,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <string>
 #include <utility>
@@ -48,11 +50,14 @@ inline uint64_t pool_keep() {  // GI_POOL_KEEP_GB overrides (A/B runs)
   static const uint64_t v = getenv("GI_POOL_KEEP_GB") ? (uint64_t)atoll(getenv("GI_POOL_KEEP_GB")) << 30 : kPoolKeepDefault;
   return v;
 }
-// larger buffers (the temporaries of a billion-edge build) use cudaMalloc: the
-// pool would release and re-map them around every synchronisation
-constexpr size_t kPoolMaxBlockDefault = 2ull << 30;
-inline size_t pool_max_block() {  // GI_POOL_MAX_GB overrides (A/B runs)
-  static const size_t v = getenv("GI_POOL_MAX_GB") ? (size_t)atoll(getenv("GI_POOL_MAX_GB")) << 30 : kPoolMaxBlockDefault;
+// larger buffers go through the per-process cache of cudaMalloc'd blocks below:
+// in steady state (the same sizes call after call) no allocation reaches the
+// driver. Pool growth alone measured 10-700 ms per cudaMallocAsync on config 4's
+// end-to-end steps (even for 24 MB, whatever the release threshold), and the
+// pool re-maps multi-GB blocks around synchronisations
+constexpr size_t kPoolMaxBlockDefault = 8ull << 20;
+inline size_t pool_max_block() {  // GI_POOL_MAX_MB overrides (A/B runs)
+  static const size_t v = getenv("GI_POOL_MAX_MB") ? (size_t)atoll(getenv("GI_POOL_MAX_MB")) << 20 : kPoolMaxBlockDefault;
   return v;
 }
 inline cudaStream_t& tl_alloc_stream() {
@@ -84,6 +89,10 @@ struct AllocScope {
 void* big_cache_get(size_t nbytes, cudaStream_t s, size_t* got);
 void big_cache_put(void* p, size_t bytes, cudaStream_t s);
 void big_cache_flush(cudaStream_t s);  // s = nullptr: every stream of the current device
+void big_cache_note_malloc();          // a large block was cudaMalloc'd (the cache re-checks free memory)
+// diagnostics: GI_DEBUG_SLOW_MS=t prints every allocation / free that takes longer than t ms
+double slow_ms();
+void slow_report(const char* what, size_t bytes, std::chrono::steady_clock::time_point t0);
 
 struct DevBuf {
   void* p = nullptr;
@@ -97,9 +106,11 @@ struct DevBuf {
   ~DevBuf() { reset(); }
   void reset() {
     if (p) {
+      const auto t0 = std::chrono::steady_clock::now();
       if (pooled) cudaFreeAsync(p, s);
       else if (cached) big_cache_put(p, cap, s);
       else cudaFree(p);
+      if (slow_ms() > 0) slow_report(pooled ? "cudaFreeAsync" : cached ? "big_cache_put" : "cudaFree", cap, t0);
     }
     p = nullptr;
     bytes = 0;
@@ -113,6 +124,7 @@ struct DevBuf {
     if (nbytes == 0) nbytes = 16;
     const cudaStream_t st = tl_alloc_stream();
     cudaError_t e = cudaSuccess;
+    const auto t0 = std::chrono::steady_clock::now();
     if (!plain && st && pool_enabled() && nbytes <= pool_max_block()) {
       e = cudaMallocAsync(&p, nbytes, st);
       pooled = e == cudaSuccess;
@@ -128,6 +140,7 @@ struct DevBuf {
           e = cudaMalloc(&p, nbytes);
         }
         got = nbytes;
+        if (e == cudaSuccess) big_cache_note_malloc();
       }
       if (e == cudaSuccess) {
         cached = true;
@@ -147,6 +160,7 @@ struct DevBuf {
     }
     bytes = nbytes;
     if (!cached) cap = nbytes;
+    if (slow_ms() > 0) slow_report(pooled ? "cudaMallocAsync" : cached ? "big alloc" : "cudaMalloc", nbytes, t0);
     return GI_OK;
   }
   size_t cap = 0;  // bytes of the underlying block (>= bytes for a reused cached block)

@@ -728,16 +728,20 @@ __global__ void k_record_headers(const int32_t* __restrict__ rtype, const int32_
 }
 
 // the largest destination span of any 32-piece group of each short class (pieces
-// are in ascending destination order inside a class): compact groups need < 65535
-__global__ void k_class_span(const int64_t* __restrict__ cstart, int64_t NC, const int32_t* __restrict__ spid,
-                             const int32_t* __restrict__ pdst, int32_t* __restrict__ span) {
-  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < NC; k += (int64_t)gridDim.x * blockDim.x) {
-    int32_t mx = 0;
-    for (int64_t q = cstart[k]; q < cstart[k + 1]; q += 32) {
-      const int64_t ql = min(q + 31, cstart[k + 1] - 1);
-      mx = max(mx, pdst[spid[ql]] - pdst[spid[q]]);
-    }
-    span[k] = mx;
+// are in ascending destination order inside a class): compact groups need < 65535.
+// A thread per short piece in class order; the first piece of each group folds its
+// group's span into span[class] (zeroed) — one class can hold millions of groups
+// (the hub segments), so a thread per class would serialise them
+__global__ void k_class_span(const uint32_t* __restrict__ sckey, int64_t NS, const int64_t* __restrict__ cstart,
+                             const int32_t* __restrict__ spid, const int32_t* __restrict__ pdst,
+                             int32_t* __restrict__ span) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < NS; j += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t k = sckey[j];
+    const int64_t c0 = cstart[k];
+    if ((j - c0) & 31) continue;
+    const int64_t ql = min(j + 31, cstart[k + 1] - 1);
+    const int32_t d = pdst[spid[ql]] - pdst[spid[j]];
+    if (d > 0) atomicMax(&span[k], d);
   }
 }
 
@@ -936,8 +940,12 @@ static gi_status seg_build_block(gi_graph g, int Z, int S, int64_t r0, int64_t r
   {
     DevBuf span;
     GI_TRY(span.alloc(std::max<int64_t>(NC, 1) * sizeof(int32_t)));
-    k_class_span<<<grid_for(NC, 256, sms), 256, 0, st>>>(cstart.as<int64_t>(), NC, spid.as<int32_t>(),
-                                                        pdst.as<int32_t>(), span.as<int32_t>());
+    GI_CUDA(cudaMemsetAsync(span.p, 0, std::max<int64_t>(NC, 1) * sizeof(int32_t), st));
+    const int64_t NSc = h_cs[NC];  // the short pieces: class keys below the long pieces' sentinel sort first
+    if (NSc > 0)
+      k_class_span<<<grid_for(NSc, 256, sms, 8), 256, 0, st>>>(sckey.as<uint32_t>(), NSc, cstart.as<int64_t>(),
+                                                               spid.as<int32_t>(), pdst.as<int32_t>(),
+                                                               span.as<int32_t>());
     GI_CUDA(cudaMemcpyAsync(h_span.data(), span.p, NC * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
     GI_CUDA(cudaStreamSynchronize(st));
   }
@@ -945,34 +953,18 @@ static gi_status seg_build_block(gi_graph g, int Z, int S, int64_t r0, int64_t r
   auto compact_k = [&](int64_t k) { return compact_on && h_span[k] < 65535; };
   mark("bounds");
   int64_t hist_L[16] = {};  // short pieces by length (layout diagnostics)
-  // ---- record layout: per unit, long records then short records by L
-  std::vector<int32_t> h_uc(U + 1), h_crec0(NC, 0), h_type, h_L, h_ng;
+  // ---- record layout: per unit, long records then short records by L. Counts
+  // first (the first record of every unit and class), then each class's run of
+  // records filled at once (millions of records: no per-record push_back)
+  // (the per-record staging vectors are kept per thread: tens of MB, first-touch
+  // page faults on every build otherwise)
+  static thread_local std::vector<int32_t> h_type, h_L, h_ng;
+  std::vector<int32_t> h_uc(U + 1), h_crec0(NC, 0);
   std::vector<int64_t> h_cost;  // per record, for the CTA balance
   int64_t C = 0, CL = 0, NS = 0;
-  {  // the record count first: the per-record vectors are filled without reallocation
-    int64_t cap = 0;
-    for (int u = 0; u < U; ++u) {
-      cap += ceil_div(h_ao[u + 1] - h_ao[u], kChunkE);
-      for (int L = 1; L < 16; ++L) {
-        const int64_t k = (int64_t)u * 16 + L;
-        cap += ceil_div(ceil_div(h_cs[k + 1] - h_cs[k], 32), short_groups(L, compact_k(k)));
-      }
-    }
-    h_type.reserve(cap);
-    h_L.reserve(cap);
-    h_ng.reserve(cap);
-    h_cost.reserve(cap);
-  }
   for (int u = 0; u < U; ++u) {
     h_uc[u] = (int32_t)C;
-    const int64_t slots = h_ao[u + 1] - h_ao[u];
-    const int64_t nl = ceil_div(slots, kChunkE);
-    for (int64_t r = 0; r < nl; ++r) {
-      h_type.push_back(1);
-      h_L.push_back(0);
-      h_ng.push_back(0);
-      h_cost.push_back(kChunkE + 2 * kPieceCost);
-    }
+    const int64_t nl = ceil_div(h_ao[u + 1] - h_ao[u], kChunkE);
     C += nl;
     CL += nl;
     for (int L = 1; L < 16; ++L) {
@@ -981,18 +973,34 @@ static gi_status seg_build_block(gi_graph g, int Z, int S, int64_t r0, int64_t r
       NS += cnt;
       hist_L[L] += cnt;
       h_crec0[k] = (int32_t)C;
-      const bool cmp = compact_k(k);
-      const int64_t groups = ceil_div(cnt, 32), R = short_groups(L, cmp);
-      for (int64_t gq = 0; gq < groups; gq += R) {
-        const int ng = (int)std::min<int64_t>(R, groups - gq);
-        h_type.push_back(cmp ? 3 : 2);
-        h_L.push_back(L);
-        h_ng.push_back(ng);
-        h_cost.push_back((int64_t)ng * 32 * (L + kPieceCost));
-        ++C;
-      }
+      C += ceil_div(ceil_div(cnt, 32), short_groups(L, compact_k(k)));
     }
     if (C >= INT32_MAX) return fail(GI_ERR_UNSUPPORTED, "segmented pull: more than 2^31 records");
+  }
+  h_type.resize(C);
+  h_L.resize(C);
+  h_ng.resize(C);
+  h_cost.resize(C);
+  for (int u = 0; u < U; ++u) {
+    const int64_t c0 = h_uc[u], nl = ceil_div(h_ao[u + 1] - h_ao[u], kChunkE);
+    std::fill_n(h_type.begin() + c0, nl, 1);
+    std::fill_n(h_L.begin() + c0, nl, 0);
+    std::fill_n(h_ng.begin() + c0, nl, 0);
+    std::fill_n(h_cost.begin() + c0, nl, (int64_t)(kChunkE + 2 * kPieceCost));
+    for (int L = 1; L < 16; ++L) {
+      const int64_t k = (int64_t)u * 16 + L;
+      const int64_t groups = ceil_div(h_cs[k + 1] - h_cs[k], 32);
+      if (groups == 0) continue;
+      const bool cmp = compact_k(k);
+      const int64_t R = short_groups(L, cmp), nr = ceil_div(groups, R), c = h_crec0[k];
+      const int ngl = (int)(groups - (nr - 1) * R);  // the last record's groups
+      std::fill_n(h_type.begin() + c, nr, cmp ? 3 : 2);
+      std::fill_n(h_L.begin() + c, nr, L);
+      std::fill_n(h_ng.begin() + c, nr - 1, (int32_t)R);
+      h_ng[c + nr - 1] = ngl;
+      std::fill_n(h_cost.begin() + c, nr - 1, R * 32 * (L + kPieceCost));
+      h_cost[c + nr - 1] = (int64_t)ngl * 32 * (L + kPieceCost);
+    }
   }
   h_uc[U] = (int32_t)C;
   mark("host_layout");
@@ -1119,14 +1127,15 @@ static gi_status seg_build_t(gi_graph g, int Z, int64_t DB) {
   // concatenate the blocks' records; unit u = b * S + segment
   std::vector<int32_t> h_uc(U + 1);
   std::vector<int64_t> h_cost;
-  h_cost.reserve(C);
+  if (B == 1) h_cost.swap(blocks[0].cost);
+  else h_cost.reserve(C);
   GI_TRY(g->seg_rec.alloc(C * kRecBytes + 16));
   GI_CUDA(cudaMemsetAsync(g->seg_rec.as<uint8_t>() + C * kRecBytes, 0, 16, st));
   int64_t cb = 0;
   for (int b = 0; b < B; ++b) {
     SegBlock& k = blocks[b];
     for (int s = 0; s < S; ++s) h_uc[b * S + s] = (int32_t)(cb + k.uc[s]);
-    h_cost.insert(h_cost.end(), k.cost.begin(), k.cost.end());
+    if (B > 1) h_cost.insert(h_cost.end(), k.cost.begin(), k.cost.end());
     if (k.C > 0)
       GI_CUDA(cudaMemcpyAsync(g->seg_rec.as<uint8_t>() + cb * kRecBytes, k.rec.p, k.C * kRecBytes,
                               cudaMemcpyDeviceToDevice, st));
