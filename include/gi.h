@@ -331,7 +331,9 @@ typedef struct {
   int32_t pull_or_levels;  /* bit-parallel passes: pull levels run as a segmented
                               OR pass (GI_MS_PULL_SEGMENTED); their edge reads
                               count every in-edge */
-  int32_t reserved;
+  int32_t pull_sparse_levels; /* bit-parallel passes: row-pull levels that pulled
+                                 only the listed rows still missing a source
+                                 (those rows' in-edges < m/64; not with ROWS) */
 } gi_bfs_stats;
 /* A bit-parallel pass serves up to 64 sources at once: its shared quantities
  * (total_ms, pull_ms, edges_examined, pull_vertices, pull_edges_examined) are

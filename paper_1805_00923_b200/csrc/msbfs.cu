@@ -71,6 +71,10 @@ constexpr int kMsPullDiv = 8;     // bit-parallel direction rule: pull iff |F| +
 // 3.95 vs 6.17 ms, level 3 at 0.56 m 3.8 vs 3.3 ms); 32-bit rows win nowhere
 // measured (config 2, 32 sources: every pull level faster as OR)
 constexpr double kSegOrFrac16 = 0.7, kSegOrFrac32 = 0.25;
+// row pull over the listed incomplete rows below this fraction of m: config 4's
+// third pull level (0.0006 m) 1.06 -> 0.67 ms; at 0.23 m (its second) listing
+// cost more than it saved (3.0 -> 3.4 ms), at 0.036 m on config 2 too (0.21 -> 0.26)
+constexpr double kSparseFrac = 1.0 / 64;
 constexpr int kPushChunk = 256;   // push: out-edges per warp at least
 #ifndef GI_MS_BATCH
 #define GI_MS_BATCH 2
@@ -119,7 +123,9 @@ struct MsArgs {
   int64_t nact;
   unsigned long long all;            // mask of the k sources
   const uint32_t* acc32;             // segmented OR pull: OR of each row's in-neighbours' frontier masks
-  int32_t* rlist;                    // segmented OR pull: heavy rows with new bits (parents resolved by warps)
+  int32_t* rlist;                    // segmented OR pull: heavy rows with new bits (parents resolved by warps);
+                                     //   sparse row pulls: the light rows still missing a source
+  int64_t nlist;                     // sparse row pulls: rows in rlist
 };
 
 __device__ __forceinline__ int32_t in_id(const MsArgs& A, int32_t v) { return A.perm ? __ldg(&A.perm[v]) : v; }
@@ -268,7 +274,9 @@ __device__ __forceinline__ unsigned long long ms_fget(const MsArgs& A, int32_t v
   return (unsigned long long)reinterpret_cast<const FM*>(A.fc)[v];
 }
 
-template <typename OffT, typename FM>
+// LIST: the level's rows are A.rlist[0, A.nlist) (the light rows still missing a
+// source, sparse pull levels) and fnext is zeroed beforehand; else every row
+template <typename OffT, typename FM, bool LIST = false>
 __global__ void __launch_bounds__(kMsT, GI_MS_LMINB) k_ms_pull(MsArgs A) {
   __shared__ int32_t s_buf[kMsT / 32][64];  // per-warp staging of the rows joining the next frontier
   int32_t* wbuf = s_buf[threadIdx.x >> 5];
@@ -276,11 +284,13 @@ __global__ void __launch_bounds__(kMsT, GI_MS_LMINB) k_ms_pull(MsArgs A) {
   const OffT* __restrict__ off = static_cast<const OffT*>(A.csc_off);
   long long tdeg = 0, exam = 0, tdone = 0;
   unsigned long long tbits = 0;
-  for (int64_t b = blockIdx.x * (int64_t)kMsT; b < A.n; b += (int64_t)gridDim.x * kMsT) {
-    const int32_t w = (int32_t)(b + threadIdx.x);
+  const int64_t N = LIST ? A.nlist : A.n;
+  for (int64_t b = blockIdx.x * (int64_t)kMsT; b < N; b += (int64_t)gridDim.x * kMsT) {
+    const int64_t i = b + threadIdx.x;
+    const int32_t w = LIST ? (i < N ? __ldg(&A.rlist[i]) : 0) : (int32_t)i;
     bool act = false;
     unsigned long long found = 0;
-    if (w < A.n) {
+    if (i < N) {
       const int64_t e0 = (int64_t)off[w], e1 = (int64_t)off[w + 1];
       const unsigned long long s = e1 - e0 >= kHeavy ? A.all : A.seen[w];  // heavy rows: k_ms_pull_heavy
       if (s != A.all) {
@@ -314,7 +324,7 @@ __global__ void __launch_bounds__(kMsT, GI_MS_LMINB) k_ms_pull(MsArgs A) {
           tbits |= found;
         }
       }
-      A.fnext[w] = found;  // heavy rows: 0 here, k_ms_pull_heavy ORs into it
+      if (!LIST || found) A.fnext[w] = found;  // heavy rows: 0 here, k_ms_pull_heavy ORs into it
     }
     ms_warp_append(A, act, w, wbuf, nbuf);
   }
@@ -596,6 +606,51 @@ __global__ void __launch_bounds__(kMsT) k_ms_push(MsArgs A, const long long* __r
     if (lane < nbuf) A.anext[pos + lane] = s_buf[wp][lane];
   }
   ms_counters(A, deg, bits, exam, done);
+}
+
+// ---- sparse row pulls: only the rows still missing a source ----
+// Late pull levels find few rows without every source (config 4: 0.9 M in-edges
+// of them at its third pull level) but a full row pull still reads every row's
+// offsets and seen word and writes its next-frontier word (1.1 ms). When the
+// rows missing a source hold < m / 64 in-edges the level zeroes the next frontier,
+// lists those rows (light ones; heavy ones by their chunks) and pulls only them.
+template <typename OffT>
+__global__ void k_ms_list_light(const OffT* __restrict__ off, const unsigned long long* __restrict__ seen, int64_t n,
+                                unsigned long long all, int32_t* __restrict__ list, unsigned long long* cnt) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t b = blockIdx.x * (int64_t)blockDim.x; b < n; b += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t w = b + threadIdx.x;  // warp-uniform loop: blockDim is a multiple of 32
+    bool in = false;
+    if (w < n && seen[w] != all) {
+      const int64_t d = (int64_t)off[w + 1] - (int64_t)off[w];
+      in = d > 0 && d < kHeavy;
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, in);
+    if (!m) continue;
+    unsigned long long base = 0;
+    if (lane == 0) base = atomicAdd(cnt, (unsigned long long)__popc(m));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (in) list[base + __popc(m & ((1u << lane) - 1u))] = (int32_t)w;
+  }
+}
+__global__ void k_ms_list_chunks(const int2* __restrict__ hch, int64_t C, const unsigned long long* __restrict__ seen,
+                                 unsigned long long all, int2* __restrict__ list, unsigned long long* cnt) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t b = blockIdx.x * (int64_t)blockDim.x; b < C; b += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = b + threadIdx.x;
+    int2 ch = make_int2(0, 0);
+    bool in = false;
+    if (c < C) {
+      ch = __ldg(&hch[c]);
+      in = seen[ch.x] != all;
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, in);
+    if (!m) continue;
+    unsigned long long base = 0;
+    if (lane == 0) base = atomicAdd(cnt, (unsigned long long)__popc(m));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (in) list[base + __popc(m & ((1u << lane) - 1u))] = ch;
+  }
 }
 
 // ---- segmented OR pull (dense pull levels of passes of <= 32 sources) ----
@@ -1014,7 +1069,8 @@ gi_status msbfs_t(gi_graph g, int32_t k, const int32_t* sources, const gi_bfs_op
     if (M.rlist.bytes < (size_t)(n + 1) * 4) GI_TRY(M.rlist.alloc((size_t)(n + 1) * 4));
   }
   int64_t inc = g->ml;  // in-edges of the rows still missing a source
-  int segor_levels = 0;
+  int segor_levels = 0, sparse_levels = 0;
+  static const double sparse_frac = getenv("GI_MS_SPARSE_FRAC") ? atof(getenv("GI_MS_SPARSE_FRAC")) : kSparseFrac;
   static const char* dbg = getenv("GI_DEBUG_MSBFS");  // diagnostics: per-level direction, size, time
   FILE* df = dbg ? fopen(dbg, "a") : nullptr;
   for (int level = 0; nact > 0; ++level) {
@@ -1030,6 +1086,7 @@ gi_status msbfs_t(gi_graph g, int32_t k, const int32_t* sources, const gi_bfs_op
                                                    : (o.policy == GI_BFS_AUTO && nact + sdeg > mdiv);
     const bool segor = pull && segor_ready &&
                        (o.pull_kernel == GI_MS_PULL_SEGMENTED || (double)inc > segor_frac * (double)g->ml);
+    bool sparse_used = false;
     if (pull && o.profile) GI_CUDA(cudaEventRecord(pe0, st));
     if (segor) {
       const bool f16 = k <= 16;
@@ -1056,28 +1113,56 @@ gi_status msbfs_t(gi_graph g, int32_t k, const int32_t* sources, const gi_bfs_op
       ++segor_levels;
     } else if (pull) {
       const int fw = k <= 16 ? 2 : k <= 32 ? 4 : 8;  // bytes per gathered frontier mask
-      const int lg = grid_for(n, kMsT, sms, kLightPerSM);
-      const int64_t hw = (M.nhch + kHeavyPer - 1) / kHeavyPer;
+      // sparse level: only the rows still missing a source (listed; fnext zeroed)
+      const bool sparse = o.pull_kernel != GI_MS_PULL_ROWS && level > 0 && (double)inc < sparse_frac * (double)g->ml;
+      int64_t nlight = n, nchunks = M.nhch;
+      const int2* chunks = M.hch.as<int2>();
+      if (sparse) {
+        if (M.rlist.bytes < (size_t)(n + 1) * 4) GI_TRY(M.rlist.alloc((size_t)(n + 1) * 4));
+        if (M.hlist.bytes < (size_t)(M.nhch + 1) * 8) GI_TRY(M.hlist.alloc((size_t)(M.nhch + 1) * 8));
+        GI_CUDA(cudaMemsetAsync(A.fnext, 0, n * 8, st));
+        GI_CUDA(cudaMemsetAsync(cnt + 6, 0, 2 * 8, st));
+        k_ms_list_light<OffT><<<grid_for(n, 256, sms, 8), 256, 0, st>>>(g->csc_off.as<OffT>(), A.seen, n, A.all,
+                                                                        M.rlist.as<int32_t>(), cnt + 6);
+        if (M.nhch > 0)
+          k_ms_list_chunks<<<grid_for(M.nhch, 256, sms, 8), 256, 0, st>>>(M.hch.as<int2>(), M.nhch, A.seen, A.all,
+                                                                         M.hlist.as<int2>(), cnt + 7);
+        GI_CUDA(cudaMemcpyAsync(h + 6, cnt + 6, 2 * 8, cudaMemcpyDeviceToHost, st));
+        GI_CUDA(stream_wait(st));
+        nlight = h[6];
+        nchunks = h[7];
+        chunks = M.hlist.as<int2>();
+        A.rlist = M.rlist.as<int32_t>();
+        A.nlist = nlight;
+        launches += 2;
+        ++sparse_levels;
+        sparse_used = true;
+      }
+      const int lg = grid_for(std::max<int64_t>(nlight, 1), kMsT, sms, kLightPerSM);
+      const int64_t hw = (nchunks + kHeavyPer - 1) / kHeavyPer;
       const unsigned hg = (unsigned)std::max<int64_t>(1, (hw + kMsT / 32 - 1) / (kMsT / 32));
       // a few chunks per warp and many CTAs: the block scheduler balances the uneven chunks
       if (fw == 8) {
         A.fc = A.fcur;
-        k_ms_pull<OffT, unsigned long long><<<lg, kMsT, 0, st>>>(A);
-        if (M.nhch > 0) k_ms_pull_heavy<OffT, unsigned long long><<<hg, kMsT, 0, st>>>(A, M.hch.as<int2>(), M.nhch);
+        if (sparse) { if (nlight > 0) k_ms_pull<OffT, unsigned long long, true><<<lg, kMsT, 0, st>>>(A); }
+        else k_ms_pull<OffT, unsigned long long><<<lg, kMsT, 0, st>>>(A);
+        if (nchunks > 0) k_ms_pull_heavy<OffT, unsigned long long><<<hg, kMsT, 0, st>>>(A, chunks, nchunks);
       } else if (fw == 4) {
         k_ms_narrow<uint32_t><<<grid_for(n, 256, sms, 8), 256, 0, st>>>(A.fcur, n, M.fc.as<uint32_t>());
         A.fc = M.fc.p;
-        k_ms_pull<OffT, uint32_t><<<lg, kMsT, 0, st>>>(A);
-        if (M.nhch > 0) k_ms_pull_heavy<OffT, uint32_t><<<hg, kMsT, 0, st>>>(A, M.hch.as<int2>(), M.nhch);
+        if (sparse) { if (nlight > 0) k_ms_pull<OffT, uint32_t, true><<<lg, kMsT, 0, st>>>(A); }
+        else k_ms_pull<OffT, uint32_t><<<lg, kMsT, 0, st>>>(A);
+        if (nchunks > 0) k_ms_pull_heavy<OffT, uint32_t><<<hg, kMsT, 0, st>>>(A, chunks, nchunks);
         ++launches;
       } else {
         k_ms_narrow<uint16_t><<<grid_for(n, 256, sms, 8), 256, 0, st>>>(A.fcur, n, M.fc.as<uint16_t>());
         A.fc = M.fc.p;
-        k_ms_pull<OffT, uint16_t><<<lg, kMsT, 0, st>>>(A);
-        if (M.nhch > 0) k_ms_pull_heavy<OffT, uint16_t><<<hg, kMsT, 0, st>>>(A, M.hch.as<int2>(), M.nhch);
+        if (sparse) { if (nlight > 0) k_ms_pull<OffT, uint16_t, true><<<lg, kMsT, 0, st>>>(A); }
+        else k_ms_pull<OffT, uint16_t><<<lg, kMsT, 0, st>>>(A);
+        if (nchunks > 0) k_ms_pull_heavy<OffT, uint16_t><<<hg, kMsT, 0, st>>>(A, chunks, nchunks);
         ++launches;
       }
-      if (M.nhch > 0) ++launches;
+      if (nchunks > 0) ++launches;
       if (o.profile) GI_CUDA(cudaEventRecord(pe1, st));
       ++pulls;
     } else {
@@ -1098,7 +1183,7 @@ gi_status msbfs_t(gi_graph g, int32_t k, const int32_t* sources, const gi_bfs_op
     if (segor) h[3] += g->ml;  // the OR pass reads every in-edge (+ the parent scans)
     if (df)
       fprintf(df, "level=%d %s nact=%lld sdeg=%lld inc=%lld -> next=%lld examined=%lld us=%.1f\n", level,
-              segor ? "pull-or" : pull ? "pull" : "push", (long long)nact, (long long)sdeg, (long long)inc,
+              segor ? "pull-or" : sparse_used ? "pull-sparse" : pull ? "pull" : "push", (long long)nact, (long long)sdeg, (long long)inc,
               (long long)h[0], (long long)h[3],
               std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - tl0).count());
     nact = h[0];
@@ -1153,6 +1238,7 @@ gi_status msbfs_t(gi_graph g, int32_t k, const int32_t* sources, const gi_bfs_op
       s.pull_ms = pull_ms / (float)k;
       s.pull_edges_examined = pull_examined / k;
       s.pull_or_levels = segor_levels;
+      s.pull_sparse_levels = sparse_levels;
       s.launches = i == 0 ? launches : 0;
       stats[i] = s;
     }

@@ -101,7 +101,7 @@ class gi_bfs_stats(ctypes.Structure):
                 ("edges_traversed", ctypes.c_int64), ("total_ms", ctypes.c_float), ("launches", ctypes.c_int32),
                 ("pull_ms", ctypes.c_float), ("edges_examined", ctypes.c_int64), ("pull_vertices", ctypes.c_int64),
                 ("pull_edges_examined", ctypes.c_int64), ("pull_or_levels", ctypes.c_int32),
-                ("reserved", ctypes.c_int32)]
+                ("pull_sparse_levels", ctypes.c_int32)]
 
 
 _vp = ctypes.c_void_p

@@ -577,6 +577,14 @@ def test_bfs_multi_or_pull_auto(gi, ctx):
             ok, msg = oracle.validate_bfs(go, src, par[i], depth)
             assert ok, f"pull_kernel={pk} src={src}: {msg}"
             assert st[i].edges_traversed == st0[i].edges_traversed
+    # pull-only: the late levels pull only the listed rows still missing a source; ROWS pulls every row
+    for pk in (gi.GI_MS_PULL_AUTO, gi.GI_MS_PULL_ROWS):
+        par, st = g.bfs_multi(sources, batch=gi.GI_BFS_BATCH_BITPARALLEL, policy=gi.GI_BFS_PULL_ONLY,
+                              pull_kernel=pk)
+        assert (st[0].pull_sparse_levels > 0) == (pk == gi.GI_MS_PULL_AUTO)
+        for i, src in enumerate(sources):
+            ok, msg = oracle.validate_bfs(go, src, par[i], oracle.bfs_depth(go, src))
+            assert ok, f"pull-only pull_kernel={pk} src={src}: {msg}"
     with pytest.raises(gi.GiError) as e:
         g.bfs_multi(sources, pull_kernel=3)
     assert e.value.status == gi.GI_ERR_INVALID_ARGUMENT
