@@ -35,12 +35,19 @@ __global__ void k_validate(const int32_t* __restrict__ src, const int32_t* __res
 }
 
 // keys of the pairs in internal ids (inv: input -> internal id, null = identity)
+// (bad != null: the endpoints are validated here — an edge outside [0, n) sets
+// *bad and becomes a sentinel — for the pipelined host-edge build)
 __global__ void k_make_keys(const int32_t* __restrict__ src, const int32_t* __restrict__ dst, int64_t m0,
                             int bits, int rm_self, int sym, uint64_t* __restrict__ keys,
-                            const int32_t* __restrict__ inv = nullptr) {
+                            const int32_t* __restrict__ inv = nullptr, int64_t n = 0, int* __restrict__ bad = nullptr) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m0; i += (int64_t)gridDim.x * blockDim.x) {
     uint64_t u = (uint32_t)src[i], v = (uint32_t)dst[i];
     bool drop = rm_self && u == v;
+    if (bad && (u >= (uint64_t)n || v >= (uint64_t)n)) {
+      atomicExch(bad, 1);
+      u = v = 0;
+      drop = true;
+    }
     if (inv) {
       u = (uint32_t)__ldg(&inv[u]);
       v = (uint32_t)__ldg(&inv[v]);
@@ -56,14 +63,82 @@ __global__ void k_make_keys(const int32_t* __restrict__ src, const int32_t* __re
 
 // out-degrees before dedup (the relabelling's order and skew test; exact degrees come
 // from the CSR): one count per kept pair, both directions when symmetrising
-__global__ void k_hist_src(const int32_t* __restrict__ src, const int32_t* __restrict__ dst, int64_t m0,
-                           int rm_self, int sym, int32_t* __restrict__ deg) {
+// the relabelling's degree: edge-list entries per source (self-loops and
+// duplicates included; with symmetrisation also per destination). A heuristic
+// order only — any internal order gives the same results in input ids — counted
+// from src alone so the pipelined host-edge build can count before dst arrives
+// (dst = null; bad != null: sources outside [0, n) set *bad and are skipped)
+__global__ void k_hist_src(const int32_t* __restrict__ src, const int32_t* __restrict__ dst, int64_t m0, int sym,
+                           int32_t* __restrict__ deg, int64_t n = 0, int* __restrict__ bad = nullptr) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m0; i += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t u = src[i], v = dst[i];
-    if (rm_self && u == v) continue;
+    const int32_t u = src[i];
+    if (bad && (u < 0 || u >= n)) {
+      atomicExch(bad, 1);
+      continue;
+    }
     atomicAdd(&deg[u], 1);
-    if (sym) atomicAdd(&deg[v], 1);
+    if (sym) atomicAdd(&deg[dst[i]], 1);
   }
+}
+
+// merge path (pairwise merge of sorted runs of 64-bit keys, the pipelined
+// build's per-chunk sorts): split[t] = elements of A among the first t * kMergeTile
+// outputs; a CTA merges one tile through shared memory
+constexpr int kMergeThreads = 256, kMergeVT = 16, kMergeTile = kMergeThreads * kMergeVT;
+__device__ __forceinline__ int64_t merge_path(const uint64_t* a, int64_t na, const uint64_t* b, int64_t nb,
+                                              int64_t diag) {
+  int64_t lo = diag > nb ? diag - nb : 0, hi = diag < na ? diag : na;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (a[mid] <= b[diag - 1 - mid]) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+__global__ void k_merge_split(const uint64_t* __restrict__ a, int64_t na, const uint64_t* __restrict__ b, int64_t nb,
+                              int64_t tiles, int64_t* __restrict__ split) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t <= tiles; t += (int64_t)gridDim.x * blockDim.x)
+    split[t] = merge_path(a, na, b, nb, t * kMergeTile < na + nb ? t * kMergeTile : na + nb);
+}
+__global__ void __launch_bounds__(kMergeThreads) k_merge(const uint64_t* __restrict__ a, int64_t na,
+                                                        const uint64_t* __restrict__ b, int64_t nb,
+                                                        const int64_t* __restrict__ split, uint64_t* __restrict__ out) {
+  __shared__ uint64_t s[kMergeTile];
+  const int64_t tot = na + nb, d0 = blockIdx.x * (int64_t)kMergeTile;
+  const int64_t d1 = d0 + kMergeTile < tot ? d0 + kMergeTile : tot;
+  const int64_t a0 = split[blockIdx.x], a1 = split[blockIdx.x + 1], b0 = d0 - a0, b1 = d1 - a1;
+  const int ta = (int)(a1 - a0), tn = (int)(d1 - d0);
+  for (int i = threadIdx.x; i < tn; i += kMergeThreads) s[i] = i < ta ? a[a0 + i] : b[b0 + i - ta];
+  __syncthreads();
+  const int diag = min((int)threadIdx.x * kMergeVT, tn);
+  int ia = (int)merge_path(s, ta, s + ta, tn - ta, diag), ib = diag - ia;
+  uint64_t r[kMergeVT];
+#pragma unroll
+  for (int k = 0; k < kMergeVT; ++k) {
+    if (diag + k < tn) {
+      const bool takea = ib >= tn - ta || (ia < ta && s[ia] <= s[ta + ib]);
+      r[k] = takea ? s[ia] : s[ta + ib];
+      if (takea) ++ia;
+      else ++ib;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < kMergeVT; ++k)
+    if (diag + k < tn) s[diag + k] = r[k];
+  __syncthreads();
+  for (int i = threadIdx.x; i < tn; i += kMergeThreads) out[d0 + i] = s[i];
+}
+
+// first index of a sentinel in sorted keys (the sentinels sort last)
+__global__ void k_count_valid(const uint64_t* __restrict__ keys, int64_t m, int64_t* __restrict__ out) {
+  int64_t lo = 0, hi = m;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (keys[mid] != kSentinel) lo = mid + 1;
+    else hi = mid;
+  }
+  *out = lo;
 }
 
 struct NotSentinel {
@@ -176,6 +251,31 @@ int bits_for(int64_t n) {
   return b;
 }
 
+// diagnostics (GI_DEBUG_BUILD=file): synchronised phase times
+struct BuildDbg {
+  const char* file = getenv("GI_DEBUG_BUILD");
+  cudaStream_t st;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  std::string s;
+  explicit BuildDbg(cudaStream_t st_) : st(st_) {}
+  void mark(const char* name) {
+    if (!file) return;
+    cudaStreamSynchronize(st);
+    const auto t2 = std::chrono::steady_clock::now();
+    char b[64];
+    snprintf(b, sizeof(b), " %s=%.1f", name, std::chrono::duration<double, std::milli>(t2 - t).count());
+    s += b;
+    t = t2;
+  }
+  void flush(const char* what, int64_t n, int64_t m0, int64_t m) {
+    if (!file) return;
+    if (FILE* f = fopen(file, "a")) {
+      fprintf(f, "%s n=%lld m0=%lld m=%lld:%s\n", what, (long long)n, (long long)m0, (long long)m, s.c_str());
+      fclose(f);
+    }
+  }
+};
+
 struct Temp {
   DevBuf buf;
   gi_status ensure(size_t bytes) {
@@ -200,6 +300,10 @@ static gi_status csr_from_sorted(gi_graph g, const uint64_t* keys, int64_t m, in
   return GI_OK;
 }
 
+static gi_status build_tail(gi_graph g, uint32_t flags, int64_t n, int64_t m, int bits, DevBuf* cur, DevBuf* alt,
+                            Temp& tmp, BuildDbg& dbg);
+static gi_status relabel_from_degrees(gi_graph g, int64_t n, Temp& tmp, const int32_t** inv);
+
 gi_status build_graph(gi_context ctx, int64_t n, int64_t m0, const int32_t* d_src, const int32_t* d_dst,
                       uint32_t flags, gi_graph g) {
   cudaStream_t st = ctx->stream;
@@ -211,19 +315,7 @@ gi_status build_graph(gi_context ctx, int64_t n, int64_t m0, const int32_t* d_sr
   const bool sym = flags & GI_SYMMETRIZE;
   g->relabeled = !(flags & GI_NO_RELABEL) && n > 1;
 
-  // diagnostics (GI_DEBUG_BUILD=file): synchronised phase times
-  static const char* bdbg = getenv("GI_DEBUG_BUILD");
-  auto tph = std::chrono::steady_clock::now();
-  std::string bphases;
-  auto bmark = [&](const char* name) {
-    if (!bdbg) return;
-    cudaStreamSynchronize(st);
-    const auto t2 = std::chrono::steady_clock::now();
-    char b[64];
-    snprintf(b, sizeof(b), " %s=%.1f", name, std::chrono::duration<double, std::milli>(t2 - tph).count());
-    bphases += b;
-    tph = t2;
-  };
+  BuildDbg dbg(st);
   // 1. validate endpoints
   DevBuf bad;
   GI_TRY(bad.alloc(sizeof(int)));
@@ -248,48 +340,12 @@ gi_status build_graph(gi_context ctx, int64_t n, int64_t m0, const int32_t* d_sr
   const int32_t* inv = nullptr;
   if (g->relabeled && m0 > 0) {
     GI_CUDA(cudaMemsetAsync(g->outdeg.p, 0, n * sizeof(int32_t), st));
-    k_hist_src<<<grid_for(m0, 256, sms, 16), 256, 0, st>>>(d_src, d_dst, m0, rm_self, sym, g->outdeg.as<int32_t>());
-    DevBuf mx, tot;
-    GI_TRY(mx.alloc(sizeof(int32_t)));
-    GI_TRY(tot.alloc(sizeof(int64_t)));
-    size_t b = 0;
-    GI_CUDA(cub::DeviceReduce::Max(nullptr, b, g->outdeg.as<int32_t>(), mx.as<int32_t>(), n, st));
-    GI_TRY(tmp.ensure(b));
-    GI_CUDA(cub::DeviceReduce::Max(tmp.buf.p, b, g->outdeg.as<int32_t>(), mx.as<int32_t>(), n, st));
-    b = 0;
-    GI_CUDA(cub::DeviceReduce::Sum(nullptr, b, g->outdeg.as<int32_t>(), tot.as<int64_t>(), n, st));
-    GI_TRY(tmp.ensure(b));
-    GI_CUDA(cub::DeviceReduce::Sum(tmp.buf.p, b, g->outdeg.as<int32_t>(), tot.as<int64_t>(), n, st));
-    int32_t hmax = 0;
-    int64_t htot = 0;
-    GI_CUDA(cudaMemcpyAsync(&hmax, mx.p, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-    GI_CUDA(cudaMemcpyAsync(&htot, tot.p, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-    GI_CUDA(cudaStreamSynchronize(st));
-    const double mean = n > 0 ? (double)htot / (double)n : 0.0;
-    g->relabeled = (double)hmax > kSkewRatio * std::max(1.0, mean);
+    k_hist_src<<<grid_for(m0, 256, sms, 16), 256, 0, st>>>(d_src, d_dst, m0, sym, g->outdeg.as<int32_t>());
+    GI_TRY(relabel_from_degrees(g, n, tmp, &inv));
   } else {
     g->relabeled = false;
   }
-  if (g->relabeled) {
-    DevBuf rk, rk2, ids;
-    GI_TRY(rk.alloc(n * sizeof(uint32_t)));
-    GI_TRY(rk2.alloc(n * sizeof(uint32_t)));
-    GI_TRY(ids.alloc(n * sizeof(int32_t)));
-    GI_TRY(g->perm.alloc(n * sizeof(int32_t)));
-    GI_TRY(g->inv.alloc(n * sizeof(int32_t)));
-    k_relabel_keys<<<grid_for(n, 256, sms), 256, 0, st>>>(g->outdeg.as<int32_t>(), n, rk.as<uint32_t>(), ids.as<int32_t>());
-    size_t b = 0;
-    GI_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, b, rk.as<uint32_t>(), rk2.as<uint32_t>(), ids.as<int32_t>(),
-                                            g->perm.as<int32_t>(), n, 0, 32, st));
-    GI_TRY(tmp.ensure(b));
-    GI_CUDA(cub::DeviceRadixSort::SortPairs(tmp.buf.p, b, rk.as<uint32_t>(), rk2.as<uint32_t>(), ids.as<int32_t>(),
-                                            g->perm.as<int32_t>(), n, 0, 32, st));
-    k_invert<<<grid_for(n, 256, sms), 256, 0, st>>>(g->perm.as<int32_t>(), n, g->inv.as<int32_t>());
-    GI_CUDA(cudaGetLastError());
-    inv = g->inv.as<int32_t>();
-  }
-
-  bmark("validate+relabel");
+  dbg.mark("validate+relabel");
   // 3. keys (u' << b | v') in internal ids, 4. select non-sentinel, 5. sort, 6. unique
   DevBuf kA, kB, nsel;
   GI_TRY(kA.alloc(mk * sizeof(uint64_t)));
@@ -320,9 +376,23 @@ gi_status build_graph(gi_context ctx, int64_t n, int64_t m0, const int32_t* d_sr
     if (db.Current() != cur->as<uint64_t>()) std::swap(cur, alt);
     return GI_OK;
   };
-  bmark("keys");
+  dbg.mark("keys");
   GI_TRY(sort_keys(m));
-  bmark("sort1");
+  dbg.mark("sort1");
+  GI_TRY(build_tail(g, flags, n, m, bits, cur, alt, tmp, dbg));
+  dbg.flush("build", n, m0, g->m);
+  return GI_OK;
+}
+
+// from the sorted keys (in *cur, m of them, sentinels removed): unique (dedup),
+// CSR and exact out-degrees, CSC, pull tiles
+static gi_status build_tail(gi_graph g, uint32_t flags, int64_t n, int64_t m, int bits, DevBuf* cur, DevBuf* alt,
+                            Temp& tmp, BuildDbg& dbg) {
+  cudaStream_t st = g->ctx->stream;
+  const int sms = g->ctx->num_sms;
+  const bool dedup = flags & GI_DEDUP;
+  DevBuf nsel;
+  GI_TRY(nsel.alloc(sizeof(int64_t)));
   if (dedup && m > 1) {
     size_t b = 0;
     GI_CUDA(cub::DeviceSelect::Unique(nullptr, b, cur->as<uint64_t>(), alt->as<uint64_t>(), nsel.as<int64_t>(), m, st));
@@ -339,7 +409,7 @@ gi_status build_graph(gi_context ctx, int64_t n, int64_t m0, const int32_t* d_sr
   g->nr = n;
   g->off64 = m >= (int64_t)INT32_MAX || (flags & GI_OFFSETS64);
 
-  bmark("unique");
+  dbg.mark("unique");
   // 7. CSR in internal ids and the exact out-degrees
   if (g->off64) GI_TRY(csr_from_sorted<int64_t>(g, cur->as<uint64_t>(), m, bits, n, g->csr_off, g->csr_idx));
   else GI_TRY(csr_from_sorted<int32_t>(g, cur->as<uint64_t>(), m, bits, n, g->csr_off, g->csr_idx));
@@ -348,7 +418,7 @@ gi_status build_graph(gi_context ctx, int64_t n, int64_t m0, const int32_t* d_sr
     else k_degrees<int32_t><<<grid_for(n, 256, sms), 256, 0, st>>>(g->csr_off.as<int32_t>(), n, g->outdeg.as<int32_t>());
   }
 
-  bmark("csr");
+  dbg.mark("csr");
   // 8. CSC in internal ids: a stable sort of the CSR's (v, u) pairs by v alone
   // (`bits`-bit 32-bit keys, half the passes and bytes of re-sorting 64-bit
   // transposed keys): the CSR order already has u ascending inside each v
@@ -369,7 +439,7 @@ gi_status build_graph(gi_context ctx, int64_t n, int64_t m0, const int32_t* d_sr
       GI_CUDA(cudaMemcpyAsync(g->csc_idx.p, dv.Current(), m * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
     vsorted = dk.Current();
   }
-  bmark("sort2");
+  dbg.mark("sort2");
   GI_TRY(g->csc_off.alloc((n + 1) * (g->off64 ? sizeof(int64_t) : sizeof(int32_t))));
   if (g->off64)
     k_offsets32<int64_t><<<grid_for(n + 1, 256, sms), 256, 0, st>>>(vsorted, m, n, g->csc_off.as<int64_t>());
@@ -390,15 +460,203 @@ gi_status build_graph(gi_context ctx, int64_t n, int64_t m0, const int32_t* d_sr
   }
   GI_CUDA(cudaGetLastError());
   GI_CUDA(cudaStreamSynchronize(st));
-  bmark("csc+tiles");
-  if (bdbg)
-    if (FILE* f = fopen(bdbg, "a")) {
-      fprintf(f, "build n=%lld m0=%lld m=%lld:%s\n", (long long)n, (long long)m0, (long long)m, bphases.c_str());
-      fclose(f);
-    }
+  dbg.mark("csc+tiles");
   return GI_OK;
 }
 
+
+// skew test on the relabelling degrees (g->outdeg, filled by k_hist_src) and, when
+// skewed, the order by them (descending, stable): perm (internal -> input), inv
+static gi_status relabel_from_degrees(gi_graph g, int64_t n, Temp& tmp, const int32_t** inv) {
+  cudaStream_t st = g->ctx->stream;
+  const int sms = g->ctx->num_sms;
+  DevBuf mx, tot;
+  GI_TRY(mx.alloc(sizeof(int32_t)));
+  GI_TRY(tot.alloc(sizeof(int64_t)));
+  size_t b = 0;
+  GI_CUDA(cub::DeviceReduce::Max(nullptr, b, g->outdeg.as<int32_t>(), mx.as<int32_t>(), n, st));
+  GI_TRY(tmp.ensure(b));
+  GI_CUDA(cub::DeviceReduce::Max(tmp.buf.p, b, g->outdeg.as<int32_t>(), mx.as<int32_t>(), n, st));
+  b = 0;
+  GI_CUDA(cub::DeviceReduce::Sum(nullptr, b, g->outdeg.as<int32_t>(), tot.as<int64_t>(), n, st));
+  GI_TRY(tmp.ensure(b));
+  GI_CUDA(cub::DeviceReduce::Sum(tmp.buf.p, b, g->outdeg.as<int32_t>(), tot.as<int64_t>(), n, st));
+  int32_t hmax = 0;
+  int64_t htot = 0;
+  GI_CUDA(cudaMemcpyAsync(&hmax, mx.p, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  GI_CUDA(cudaMemcpyAsync(&htot, tot.p, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  GI_CUDA(cudaStreamSynchronize(st));
+  const double mean = n > 0 ? (double)htot / (double)n : 0.0;
+  g->relabeled = (double)hmax > kSkewRatio * std::max(1.0, mean);
+  if (!g->relabeled) return GI_OK;
+  DevBuf rk, rk2, ids;
+  GI_TRY(rk.alloc(n * sizeof(uint32_t)));
+  GI_TRY(rk2.alloc(n * sizeof(uint32_t)));
+  GI_TRY(ids.alloc(n * sizeof(int32_t)));
+  GI_TRY(g->perm.alloc(n * sizeof(int32_t)));
+  GI_TRY(g->inv.alloc(n * sizeof(int32_t)));
+  k_relabel_keys<<<grid_for(n, 256, sms), 256, 0, st>>>(g->outdeg.as<int32_t>(), n, rk.as<uint32_t>(), ids.as<int32_t>());
+  b = 0;
+  GI_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, b, rk.as<uint32_t>(), rk2.as<uint32_t>(), ids.as<int32_t>(),
+                                          g->perm.as<int32_t>(), n, 0, 32, st));
+  GI_TRY(tmp.ensure(b));
+  GI_CUDA(cub::DeviceRadixSort::SortPairs(tmp.buf.p, b, rk.as<uint32_t>(), rk2.as<uint32_t>(), ids.as<int32_t>(),
+                                          g->perm.as<int32_t>(), n, 0, 32, st));
+  k_invert<<<grid_for(n, 256, sms), 256, 0, st>>>(g->perm.as<int32_t>(), n, g->inv.as<int32_t>());
+  GI_CUDA(cudaGetLastError());
+  *inv = g->inv.as<int32_t>();
+  return GI_OK;
+}
+
+// ---- host edges: the H2D copy overlapped with the build (gi_graph_create's
+// host-pointer path; pinned memory makes the copies asynchronous). The copy
+// stream moves src in kSrcChunks chunks, then dst in kDstChunks; the build stream
+// counts each src chunk's relabelling degrees as it lands (validating sources),
+// orders the vertices once src is complete (exactly as from device edges), then
+// per dst chunk makes its keys (validating destinations) and radix-sorts them
+// while the next chunk is in flight; pairwise merge-path rounds join the sorted
+// chunks, and the rest (dedup, CSR, CSC) is build_tail. Config 4: the 12.9 GB
+// H2D (~220 ms) used to precede a ~235 ms build.
+constexpr int kSrcChunks = 8, kDstChunks = 4;
+constexpr int64_t kPipeMinEdges = 1ll << 24;
+
+}  // namespace gi
+
+bool gi::build_host_pipelined(gi_context ctx, int64_t m0, uint32_t flags) {
+  static const bool on = !getenv("GI_BUILD_PIPELINE") || atoi(getenv("GI_BUILD_PIPELINE")) != 0;
+  return on && ctx->nranks == 1 && m0 >= kPipeMinEdges && !(flags & GI_SYMMETRIZE);
+}
+
+gi_status gi::build_graph_host(gi_context ctx, int64_t n, int64_t m0, const int32_t* h_src, const int32_t* h_dst,
+                               uint32_t flags, gi_graph g) {
+  cudaStream_t st = ctx->stream;
+  const int sms = ctx->num_sms;
+  g->ctx = ctx;
+  g->n = n;
+  const bool rm_self = flags & GI_REMOVE_SELF_LOOPS;
+  g->relabeled = !(flags & GI_NO_RELABEL) && n > 1;
+  BuildDbg dbg(st);
+  if (!ctx->copy_stream) GI_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+  cudaStream_t cs = ctx->copy_stream;
+  DevBuf ds, dd, bad;
+  GI_TRY(ds.alloc(m0 * sizeof(int32_t)));
+  GI_TRY(dd.alloc(m0 * sizeof(int32_t)));
+  GI_TRY(bad.alloc(sizeof(int)));
+  GI_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), st));
+  const int bits = bits_for(n > 1 ? n : 2);
+  Temp tmp;
+  GI_TRY(g->outdeg.alloc(n * sizeof(int32_t)));
+  GI_CUDA(cudaMemsetAsync(g->outdeg.p, 0, n * sizeof(int32_t), st));
+  DevBuf kA, kB, nsel;
+  GI_TRY(kA.alloc(m0 * sizeof(uint64_t)));
+  GI_TRY(kB.alloc(m0 * sizeof(uint64_t)));
+  GI_TRY(nsel.alloc(sizeof(int64_t)));
+  // the copy stream starts once the buffers are ready on the build stream
+  cudaEvent_t ready, ev[kSrcChunks + kDstChunks];
+  GI_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+  for (auto& e : ev) GI_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  struct Events {  // on every return: the copies are complete before ds / dd are freed
+    cudaEvent_t* e;
+    int k;
+    cudaEvent_t r;
+    cudaStream_t cs;
+    ~Events() {
+      cudaStreamSynchronize(cs);
+      for (int i = 0; i < k; ++i) cudaEventDestroy(e[i]);
+      cudaEventDestroy(r);
+    }
+  } evs{ev, kSrcChunks + kDstChunks, ready, cs};
+  GI_CUDA(cudaEventRecord(ready, st));
+  GI_CUDA(cudaStreamWaitEvent(cs, ready, 0));
+  auto cut = [&](int i, int k) { return m0 * i / k; };
+  for (int i = 0; i < kSrcChunks; ++i) {
+    const int64_t a = cut(i, kSrcChunks), b = cut(i + 1, kSrcChunks);
+    GI_CUDA(cudaMemcpyAsync(ds.as<int32_t>() + a, h_src + a, (b - a) * sizeof(int32_t), cudaMemcpyHostToDevice, cs));
+    GI_CUDA(cudaEventRecord(ev[i], cs));
+  }
+  for (int i = 0; i < kDstChunks; ++i) {
+    const int64_t a = cut(i, kDstChunks), b = cut(i + 1, kDstChunks);
+    GI_CUDA(cudaMemcpyAsync(dd.as<int32_t>() + a, h_dst + a, (b - a) * sizeof(int32_t), cudaMemcpyHostToDevice, cs));
+    GI_CUDA(cudaEventRecord(ev[kSrcChunks + i], cs));
+  }
+  // relabelling degrees per src chunk, then the order
+  const int32_t* inv = nullptr;
+  for (int i = 0; i < kSrcChunks; ++i) {
+    const int64_t a = cut(i, kSrcChunks), b = cut(i + 1, kSrcChunks);
+    GI_CUDA(cudaStreamWaitEvent(st, ev[i], 0));
+    if (g->relabeled && b > a)
+      k_hist_src<<<grid_for(b - a, 256, sms, 16), 256, 0, st>>>(ds.as<int32_t>() + a, nullptr, b - a, 0,
+                                                               g->outdeg.as<int32_t>(), n, bad.as<int>());
+  }
+  if (g->relabeled) GI_TRY(relabel_from_degrees(g, n, tmp, &inv));
+  dbg.mark("src+relabel");
+  // keys and a sort per dst chunk (validating every endpoint: an invalid edge is a
+  // sentinel and raises the flag, checked before the result is used)
+  std::vector<int64_t> run{0};
+  bool in_b = false;
+  for (int i = 0; i < kDstChunks; ++i) {
+    const int64_t a = cut(i, kDstChunks), b = cut(i + 1, kDstChunks);
+    GI_CUDA(cudaStreamWaitEvent(st, ev[kSrcChunks + i], 0));
+    if (b > a) {
+      k_make_keys<<<grid_for(b - a, 256, sms), 256, 0, st>>>(ds.as<int32_t>() + a, dd.as<int32_t>() + a, b - a, bits,
+                                                            rm_self, 0, kA.as<uint64_t>() + a, inv, n, bad.as<int>());
+      // bit 2 * bits separates the sentinels (all ones) from every key
+      cub::DoubleBuffer<uint64_t> db(kA.as<uint64_t>() + a, kB.as<uint64_t>() + a);
+      size_t tb = 0;
+      GI_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb, db, b - a, 0, 2 * bits + 1, st));
+      GI_TRY(tmp.ensure(tb));
+      GI_CUDA(cub::DeviceRadixSort::SortKeys(tmp.buf.p, tb, db, b - a, 0, 2 * bits + 1, st));
+      in_b = db.Current() != kA.as<uint64_t>() + a;  // the same pass count for every chunk
+    }
+    run.push_back(b);
+  }
+  dbg.mark("dst+keys+chunk sorts");
+  int h_bad = 0;
+  GI_CUDA(cudaMemcpyAsync(&h_bad, bad.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  GI_CUDA(cudaStreamSynchronize(st));
+  if (h_bad) return fail(GI_ERR_VERTEX_OUT_OF_RANGE, "gi_graph_create: an edge endpoint is outside [0, n)");
+  ds.reset();
+  dd.reset();
+  // pairwise merge rounds until one run is left
+  DevBuf* cur = in_b ? &kB : &kA;
+  DevBuf* alt = in_b ? &kA : &kB;
+  DevBuf split;
+  while (run.size() > 2) {
+    std::vector<int64_t> next{0};
+    for (size_t r = 0; r + 1 < run.size(); r += 2) {
+      const int64_t a0 = run[r], a1 = run[r + 1];
+      if (r + 2 >= run.size()) {  // odd run out: copied
+        GI_CUDA(cudaMemcpyAsync(alt->as<uint64_t>() + a0, cur->as<uint64_t>() + a0, (a1 - a0) * 8,
+                                cudaMemcpyDeviceToDevice, st));
+        next.push_back(a1);
+        continue;
+      }
+      const int64_t b1 = run[r + 2], na = a1 - a0, nb = b1 - a1;
+      const int64_t tiles = ceil_div(na + nb, kMergeTile);
+      if (split.bytes < (size_t)(tiles + 1) * 8) GI_TRY(split.alloc((tiles + 1) * 8));
+      k_merge_split<<<grid_for(tiles + 1, 256, sms), 256, 0, st>>>(cur->as<uint64_t>() + a0, na,
+                                                                 cur->as<uint64_t>() + a1, nb, tiles,
+                                                                 split.as<int64_t>());
+      k_merge<<<(unsigned)tiles, kMergeThreads, 0, st>>>(cur->as<uint64_t>() + a0, na, cur->as<uint64_t>() + a1, nb,
+                                                         split.as<int64_t>(), alt->as<uint64_t>() + a0);
+      next.push_back(b1);
+    }
+    run.swap(next);
+    std::swap(cur, alt);
+  }
+  GI_CUDA(cudaGetLastError());
+  // the sentinels (self-loops) sort last: m = the first sentinel's index
+  int64_t m = 0;
+  k_count_valid<<<1, 1, 0, st>>>(cur->as<uint64_t>(), m0, nsel.as<int64_t>());
+  GI_CUDA(cudaMemcpyAsync(&m, nsel.p, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  GI_CUDA(cudaStreamSynchronize(st));
+  dbg.mark("merge");
+  GI_TRY(build_tail(g, flags, n, m, bits, cur, alt, tmp, dbg));
+  dbg.flush("build (host edges, pipelined)", n, m0, g->m);
+  return GI_OK;
+}
+
+namespace gi {
 
 // ---------------------------------------------------------------------------------------------
 // Multi-GPU build: 1-D destination-range partition. Every rank

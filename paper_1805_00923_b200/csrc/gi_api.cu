@@ -306,6 +306,7 @@ gi_status gi_context_destroy(gi_context ctx) {
   if (ctx->h_scratch) cudaFreeHost(ctx->h_scratch);
   if (ctx->h_batch) cudaFreeHost(ctx->h_batch);
   if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+  if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
   delete ctx;
   return GI_OK;
 }
@@ -333,13 +334,18 @@ gi_status gi_graph_create(gi_context ctx, int64_t n, int64_t m0, const int32_t* 
   AllocScope as_(ctx->stream);
   if ((flags & GI_EDGES_ON_DEVICE) && m0 > 0 && !(is_device_ptr(src) && is_device_ptr(dst)))
     return fail(GI_ERR_INVALID_ARGUMENT, "gi_graph_create: GI_EDGES_ON_DEVICE but edges are host memory");
-  DevBuf hs, hd;
-  const int32_t *ds = nullptr, *dd = nullptr;
-  GI_TRY(to_device(ctx, src, m0, hs, &ds));
-  GI_TRY(to_device(ctx, dst, m0, hd, &dd));
   gi_graph g = new gi_graph_s();
-  gi_status s = ctx->nranks > 1 ? build_graph_dist(ctx, n, m0, ds, dd, flags, g)
-                                : build_graph(ctx, n, m0, ds, dd, flags, g);
+  gi_status s;
+  if (m0 > 0 && !is_device_ptr(src) && !is_device_ptr(dst) && build_host_pipelined(ctx, m0, flags)) {
+    s = build_graph_host(ctx, n, m0, src, dst, flags, g);  // H2D overlapped with the build
+  } else {
+    DevBuf hs, hd;
+    const int32_t *ds = nullptr, *dd = nullptr;
+    s = to_device(ctx, src, m0, hs, &ds);
+    if (s == GI_OK) s = to_device(ctx, dst, m0, hd, &dd);
+    if (s == GI_OK)
+      s = ctx->nranks > 1 ? build_graph_dist(ctx, n, m0, ds, dd, flags, g) : build_graph(ctx, n, m0, ds, dd, flags, g);
+  }
   if (s == GI_OK) s = sync(ctx);
   if (s != GI_OK) {
     delete g;

@@ -189,6 +189,7 @@ struct gi_context_s {
   int64_t* h_batch = nullptr;  // pinned per-source state slots of gi_bfs_multi
   int64_t h_batch_len = 0;
   int live_graphs = 0;  // graphs created on this context and not yet destroyed
+  cudaStream_t copy_stream = nullptr;  // host-edge H2D chunks of gi_graph_create (created on first use)
 };
 
 // Pull-PageRank tiling (merge-path over CSC rows + edges).
@@ -309,6 +310,11 @@ gi_status build_graph_dist(gi_context ctx, int64_t n, int64_t m0, const int32_t*
                            const int32_t* d_dst, uint32_t flags, gi_graph g);
 gi_status build_graph(gi_context ctx, int64_t n, int64_t m0, const int32_t* d_src,
                       const int32_t* d_dst, uint32_t flags, gi_graph g);
+// host edges (pinned for overlap): the H2D copy in chunks on the context's copy
+// stream, overlapped with the histogram, key making and per-chunk sorts
+gi_status build_graph_host(gi_context ctx, int64_t n, int64_t m0, const int32_t* h_src, const int32_t* h_dst,
+                           uint32_t flags, gi_graph g);
+bool build_host_pipelined(gi_context ctx, int64_t m0, uint32_t flags);
 // pagerank.cu
 gi_status pagerank_run(gi_graph g, int32_t iters, double damping, const gi_pr_opts& o,
                        float* d_out_input_ids, gi_pr_stats* stats);

@@ -54,7 +54,7 @@ namespace {
 #endif
 constexpr int kMsT = 256;
 #ifndef GI_MS_LMINB
-#define GI_MS_LMINB 1  // min resident CTAs per SM requested from ptxas (register cap) for the light pull
+#define GI_MS_LMINB 4  // min resident CTAs per SM requested from ptxas (register cap: 64) for the light pull
 #endif
 #ifndef GI_MS_HMINB
 #define GI_MS_HMINB 6  // ... and for the heavy pull (40 registers: 6 CTAs per SM hide the L2 gather latency;
@@ -396,7 +396,8 @@ __global__ void __launch_bounds__(kMsT, GI_MS_HMINB) k_ms_pull_heavy(MsArgs A, c
         for (int j = 0; j < kPullBatch; ++j) {
           const unsigned long long mj = f[j] & ~s & ~found;
           const unsigned lo = __reduce_or_sync(0xffffffffu, (unsigned)mj);
-          const unsigned hi = __reduce_or_sync(0xffffffffu, (unsigned)(mj >> 32));
+          // masks of <= 32 bits (k <= 32) have no upper half: one reduction per slot
+          const unsigned hi = sizeof(FM) > 4 ? __reduce_or_sync(0xffffffffu, (unsigned)(mj >> 32)) : 0u;
           if ((lo | hi) == 0u) continue;  // warp-uniform: nothing new from this batch slot
           const int32_t vin = mj ? in_id(A, v[j]) : 0;
           // each new bit's parent: the lowest lane bringing it (bit-matrix transpose of the lanes' masks)
@@ -957,11 +958,6 @@ static gi_status ms_prepare_t(gi_graph g) {
     GI_CUDA(cudaMemsetAsync(M.hidx.p, 0xFF, (n + 1) * 4, st));
     if (hn > 0) k_ms_hidx<<<grid_for(hn, 256, sms), 256, 0, st>>>(M.heavy.as<int32_t>(), hn, M.hidx.as<int32_t>());
     GI_TRY(M.par8.alloc((size_t)n * 64 + 64));
-    // the CSC's sources in input ids (the epilogue resolves light rows' parent indices through it)
-    GI_TRY(M.csc_in.alloc((size_t)(g->ml + 1) * 4));
-    k_ms_csc_in<<<grid_for(g->ml, 256, sms), 256, 0, st>>>(g->csc_idx.as<int32_t>(), g->ml,
-                                                          g->relabeled ? g->perm.as<int32_t>() : nullptr,
-                                                          M.csc_in.as<int32_t>());
     M.nhch = 0;
     if (hn > 0) {
       int32_t* cc = M.chunks[0].as<int32_t>();
@@ -1003,6 +999,13 @@ gi_status msbfs_t(gi_graph g, int32_t k, const int32_t* sources, const gi_bfs_op
   static const bool par_all_env = !getenv("GI_MS_PAR_ALL") || atoi(getenv("GI_MS_PAR_ALL")) != 0;
   const bool par_all = par_all_env && kp <= 16;
   const int64_t par_rows = par_all ? n + 1 : M.nheavy + 1;
+  if (!par_all && !M.csc_in.p) {  // byte rows: the CSC's sources in input ids (the epilogue resolves
+                                  // light rows' parent indices through it), built on first need
+    GI_TRY(M.csc_in.alloc((size_t)(g->ml + 1) * 4));
+    k_ms_csc_in<<<grid_for(g->ml, 256, sms), 256, 0, st>>>(g->csc_idx.as<int32_t>(), g->ml,
+                                                          g->relabeled ? g->perm.as<int32_t>() : nullptr,
+                                                          M.csc_in.as<int32_t>());
+  }
   if (M.par.bytes < (size_t)par_rows * kp * 4) GI_TRY(M.par.alloc((size_t)par_rows * kp * 4));
   if (k <= 32 && M.fc.bytes < (size_t)(n + 1) * (k <= 16 ? 2 : 4)) GI_TRY(M.fc.alloc((size_t)(n + 1) * (k <= 16 ? 2 : 4)));
   cudaEvent_t e0 = nullptr, e1 = nullptr, pe0 = nullptr, pe1 = nullptr;

@@ -127,6 +127,42 @@ def test_build_rmat_config1_bit_exact(gi, ctx):
     assert graphgen.edge_checksum(src_o, go.csr_idx) == graphgen.edge_checksum(src_g, idx)
 
 
+@pytest.mark.parametrize("name,kind,oflags", [fs for fs in FLAG_SETS if fs[1] != "sym"])
+def test_build_host_edges_pipelined(gi, ctx, name, kind, oflags):
+    """gi_graph_create from host edges of >= 2^24 entries takes the pipelined build (H2D in chunks
+    overlapped with the degree count, per-chunk key sorts, merge-path rounds): bit-exact CSR against
+    the oracle and the device-edge build, PageRank on it against the oracle; an endpoint outside
+    [0, n) in any chunk is an error."""
+    import torch
+
+    n = 1 << 20
+    s, d = graphgen.rmat(20, 24, 0.57, 0.19, 0.19, 777)  # 25 M entries with self-loops and duplicates
+    assert len(s) >= 1 << 24
+    flags = _flags(gi, kind)
+    g = gi.Graph(ctx, n, s, d, flags)
+    go = oracle.build_graph(n, s, d, **oflags)
+    assert g.m == go.m
+    off, idx = g.csr()
+    assert np.array_equal(off, go.csr_off) and np.array_equal(idx, go.csr_idx)
+    assert np.array_equal(g.out_degrees(), go.outdeg.astype(np.int32))
+    gd = gi.Graph(ctx, n, torch.from_numpy(s).cuda(), torch.from_numpy(d).cuda(), flags | gi.GI_EDGES_ON_DEVICE)
+    offd, idxd = gd.csr()
+    assert np.array_equal(offd, off) and np.array_equal(idxd, idx)
+    assert np.array_equal(gd.out_degrees(), g.out_degrees())
+    gd.close()
+    if kind != "raw":
+        ph, _ = g.pagerank(5, 0.85)
+        _pr_check(ph, oracle.pagerank(go, 5, 0.85), f"host-edge build {name}")
+    g.close()
+    for arr, pos, val in ((d, len(d) - 1, n), (s, len(s) // 3, -1), (d, 5, n + 7)):
+        bad = arr.copy()
+        bad[pos] = val
+        args = (s, bad) if arr is d else (bad, d)
+        with pytest.raises(gi.GiError) as e:
+            gi.Graph(ctx, n, *args, flags)
+        assert e.value.status == gi.GI_ERR_VERTEX_OUT_OF_RANGE
+
+
 def test_build_device_edges_and_errors(gi, ctx):
     import torch
 
