@@ -615,10 +615,43 @@ __global__ void __launch_bounds__(kMsT) k_ms_push(MsArgs A, const long long* __r
 // offsets and seen word and writes its next-frontier word (1.1 ms). When the
 // rows missing a source hold < m / 64 in-edges the level zeroes the next frontier,
 // lists those rows (light ones; heavy ones by their chunks) and pulls only them.
-template <typename OffT>
-__global__ void k_ms_list_light(const OffT* __restrict__ off, const unsigned long long* __restrict__ seen, int64_t n,
-                                unsigned long long all, int32_t* __restrict__ list, unsigned long long* cnt) {
+// warp-buffered list append: one atomic per 32 listed entries (buf: 64 per warp)
+template <typename T>
+__device__ __forceinline__ void list_append(bool in, T v, T* list, unsigned long long* cnt, T* buf, int& nbuf) {
   const int lane = threadIdx.x & 31;
+  const unsigned m = __ballot_sync(0xffffffffu, in);
+  if (in) buf[nbuf + __popc(m & ((1u << lane) - 1u))] = v;
+  nbuf += __popc(m);
+  if (nbuf >= 32) {
+    __syncwarp();
+    unsigned long long base = 0;
+    if (lane == 0) base = atomicAdd(cnt, 32ull);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    list[base + lane] = buf[lane];
+    __syncwarp();
+    nbuf -= 32;
+    if (lane < nbuf) buf[lane] = buf[32 + lane];
+    __syncwarp();
+  }
+}
+template <typename T>
+__device__ __forceinline__ void list_flush(T* list, unsigned long long* cnt, T* buf, int nbuf) {
+  const int lane = threadIdx.x & 31;
+  __syncwarp();
+  if (nbuf == 0) return;
+  unsigned long long base = 0;
+  if (lane == 0) base = atomicAdd(cnt, (unsigned long long)nbuf);
+  base = __shfl_sync(0xffffffffu, base, 0);
+  if (lane < nbuf) list[base + lane] = buf[lane];
+}
+
+template <typename OffT>
+__global__ void __launch_bounds__(256) k_ms_list_light(const OffT* __restrict__ off,
+                                                      const unsigned long long* __restrict__ seen, int64_t n,
+                                                      unsigned long long all, int32_t* __restrict__ list,
+                                                      unsigned long long* cnt) {
+  __shared__ int32_t s_buf[8][64];
+  int nbuf = 0;
   for (int64_t b = blockIdx.x * (int64_t)blockDim.x; b < n; b += (int64_t)gridDim.x * blockDim.x) {
     const int64_t w = b + threadIdx.x;  // warp-uniform loop: blockDim is a multiple of 32
     bool in = false;
@@ -626,17 +659,16 @@ __global__ void k_ms_list_light(const OffT* __restrict__ off, const unsigned lon
       const int64_t d = (int64_t)off[w + 1] - (int64_t)off[w];
       in = d > 0 && d < kHeavy;
     }
-    const unsigned m = __ballot_sync(0xffffffffu, in);
-    if (!m) continue;
-    unsigned long long base = 0;
-    if (lane == 0) base = atomicAdd(cnt, (unsigned long long)__popc(m));
-    base = __shfl_sync(0xffffffffu, base, 0);
-    if (in) list[base + __popc(m & ((1u << lane) - 1u))] = (int32_t)w;
+    list_append(in, (int32_t)w, list, cnt, s_buf[threadIdx.x >> 5], nbuf);
   }
+  list_flush(list, cnt, s_buf[threadIdx.x >> 5], nbuf);
 }
-__global__ void k_ms_list_chunks(const int2* __restrict__ hch, int64_t C, const unsigned long long* __restrict__ seen,
-                                 unsigned long long all, int2* __restrict__ list, unsigned long long* cnt) {
-  const int lane = threadIdx.x & 31;
+__global__ void __launch_bounds__(256) k_ms_list_chunks(const int2* __restrict__ hch, int64_t C,
+                                                       const unsigned long long* __restrict__ seen,
+                                                       unsigned long long all, int2* __restrict__ list,
+                                                       unsigned long long* cnt) {
+  __shared__ int2 s_buf[8][64];
+  int nbuf = 0;
   for (int64_t b = blockIdx.x * (int64_t)blockDim.x; b < C; b += (int64_t)gridDim.x * blockDim.x) {
     const int64_t c = b + threadIdx.x;
     int2 ch = make_int2(0, 0);
@@ -645,13 +677,9 @@ __global__ void k_ms_list_chunks(const int2* __restrict__ hch, int64_t C, const 
       ch = __ldg(&hch[c]);
       in = seen[ch.x] != all;
     }
-    const unsigned m = __ballot_sync(0xffffffffu, in);
-    if (!m) continue;
-    unsigned long long base = 0;
-    if (lane == 0) base = atomicAdd(cnt, (unsigned long long)__popc(m));
-    base = __shfl_sync(0xffffffffu, base, 0);
-    if (in) list[base + __popc(m & ((1u << lane) - 1u))] = ch;
+    list_append(in, ch, list, cnt, s_buf[threadIdx.x >> 5], nbuf);
   }
+  list_flush(list, cnt, s_buf[threadIdx.x >> 5], nbuf);
 }
 
 // ---- segmented OR pull (dense pull levels of passes of <= 32 sources) ----
@@ -680,9 +708,10 @@ __global__ void k_ms_narrow_or(const unsigned long long* __restrict__ f, int64_t
 // counters; a light row's parents found by its thread, a heavy row queued in rlist
 template <typename OffT, typename FM>
 __global__ void __launch_bounds__(kMsT) k_ms_or_vertex(MsArgs A) {
-  __shared__ int32_t s_buf[kMsT / 32][64];
+  __shared__ int32_t s_buf[kMsT / 32][64], s_hbuf[kMsT / 32][64];
   int32_t* wbuf = s_buf[threadIdx.x >> 5];
-  int nbuf = 0;
+  int32_t* hbuf = s_hbuf[threadIdx.x >> 5];
+  int nbuf = 0, nhbuf = 0;
   const int lane = threadIdx.x & 31;
   const OffT* __restrict__ off = static_cast<const OffT*>(A.csc_off);
   long long tdeg = 0, exam = 0, tdone = 0;
@@ -730,15 +759,10 @@ __global__ void __launch_bounds__(kMsT) k_ms_or_vertex(MsArgs A) {
         }
       }
     }
-    const unsigned hm = __ballot_sync(0xffffffffu, heavy);
-    if (hm) {  // queue the warp's heavy rows (one atomic per warp step)
-      unsigned long long base = 0;
-      if (lane == 0) base = atomicAdd(&A.cnt[5], (unsigned long long)__popc(hm));
-      base = __shfl_sync(0xffffffffu, base, 0);
-      if (heavy) A.rlist[base + __popc(hm & ((1u << lane) - 1u))] = w;
-    }
+    list_append(heavy, w, A.rlist, &A.cnt[5], hbuf, nhbuf);  // heavy rows: one atomic per 32
     ms_warp_append(A, act, w, wbuf, nbuf);
   }
+  list_flush(A.rlist, &A.cnt[5], hbuf, nhbuf);
   if (nbuf > 0) ms_warp_flush(A, wbuf, nbuf);
   ms_counters(A, tdeg, tbits, exam, tdone);
 }
@@ -893,6 +917,21 @@ __global__ void __launch_bounds__(256) k_ms_finish_reg(const int32_t* __restrict
       }
     }
     if (__ballot_sync(0xffffffffu, sv != 0) == 0) continue;
+    if (KP <= 32) {  // k <= 32: per source one vote and two warp sums (lane b keeps source b's counts)
+#pragma unroll
+      for (int b = 0; b < KP; ++b) {
+        if (b >= k) break;
+        const bool has = (sv >> b) & 1ull;
+        const unsigned c = __popc(__ballot_sync(0xffffffffu, has));
+        const unsigned hi = __reduce_add_sync(0xffffffffu, has ? (unsigned)(ov >> 16) : 0u);  // < 2^20 each
+        const unsigned lo = __reduce_add_sync(0xffffffffu, has ? (unsigned)(ov & 0xFFFFu) : 0u);
+        if (lane == b) {
+          r0 += c;
+          d0 += ((unsigned long long)hi << 16) + lo;
+        }
+      }
+      continue;
+    }
 #pragma unroll 4
     for (int j = 0; j < 32; ++j) {
       const unsigned long long s = __shfl_sync(0xffffffffu, sv, j);

@@ -69,9 +69,12 @@ def main():
         agg = {}
         for d in launches:
             k = d["kernel"]
-            for key, name in (("k_pr_seg", "pr_seg"), ("k_pr_acc", "pr_acc"), ("k_pr_pull", "pr_direct"),
+            for key, name in (("OpOr", "ms_or_pass"), ("OpMin", "cc_seg"), ("k_pr_seg", "pr_seg"), ("k_pr_acc", "pr_acc"), ("k_pr_pull", "pr_direct"),
                               ("k_bfs_fused", "bfs_fused"), ("k_ms_pull_heavy", "ms_pull_heavy"),
                               ("k_ms_pull<", "ms_pull_light"), ("k_ms_push", "ms_push"),
+                              ("k_ms_or_vertex", "ms_or_vertex"),
+                              ("k_ms_resolve_heavy", "ms_resolve_heavy"), ("k_ms_narrow_or", "ms_narrow_or"),
+                              ("k_ms_narrow<", "ms_narrow"), ("k_ms_list_", "ms_list"),
                               ("k_ms_finish", "ms_finish"), ("k_pb_scatter", "pb_scatter"),
                               ("k_pb_gather", "pb_gather")):
                 if key in k:
@@ -91,11 +94,19 @@ def main():
             agg["pr_pull"] = {"dram_bytes_per_launch": agg["pb_scatter"]["dram_bytes_per_launch"] +
                               agg["pb_gather"]["dram_bytes_per_launch"],
                               "note": "per PageRank iteration: k_pb_scatter + k_pb_gather"}
-        if "ms_pull_light" in agg:  # one bit-parallel pull level = light-row kernel + heavy-row kernel
+        # one bit-parallel pull level: its mask narrowing and then the row pull (light + heavy kernels,
+        # + the row lists of a sparse level) or the segmented OR pass + vertex pass + heavy parent scans
+        lv = agg.get("ms_narrow", {}).get("launches", 0) + agg.get("ms_narrow_or", {}).get("launches", 0)
+        if lv == 0 and "ms_pull_light" in agg:  # 64-bit masks: no narrowing kernel
             lv = agg["ms_pull_light"]["launches"]
-            tot = agg["ms_pull_light"]["dram_bytes"] + agg.get("ms_pull_heavy", {}).get("dram_bytes", 0.0)
+        if lv:
+            parts = ("ms_narrow", "ms_narrow_or", "ms_pull_light", "ms_pull_heavy", "ms_list", "ms_or_pass",
+                     "ms_or_vertex", "ms_resolve_heavy")
+            tot = sum(agg.get(p, {}).get("dram_bytes", 0.0) for p in parts)
             agg["bfs_pull"] = {"dram_bytes_per_launch": tot / lv, "levels": lv,
-                               "note": "per bit-parallel pull level: k_ms_pull + k_ms_pull_heavy"}
+                               "note": "per bit-parallel pull level (row pulls and segmented OR levels averaged): "
+                                       "mask narrowing + k_ms_pull + k_ms_pull_heavy (+ row lists) or "
+                                       "k_pr_seg<OpOr> + k_ms_or_vertex + k_ms_resolve_heavy"}
         top = json.load(open(js)) if os.path.exists(js) else {}
         old = top.setdefault("configs", {}).setdefault(cfgname, {}) if cfgname else top
         old.update(agg)  # merge with summaries of other captures (PR and BFS are captured separately)
