@@ -302,12 +302,12 @@ typedef struct {
                             the PageRank edge kernel over the segmented layout —
                             frontier masks staged per source segment in shared
                             memory — then each new bit's parent by a row scan
-                            that stops once every new bit has one; passes of
-                            <= 32 sources on one GPU; builds the layout if the
-                            graph has none, else ROWS). AUTO takes the
+                            that stops once every new bit has one; one GPU;
+                            32-bit OR passes: two when k > 32; builds the
+                            layout if the graph has none). AUTO takes the
                             OR pass when the graph already has the layout and
                             the rows still missing a source hold > 0.7 m
-                            (k <= 16) / 0.25 m (k <= 32) in-edges */
+                            (k <= 16) / 0.25 m (k > 16) in-edges */
 } gi_bfs_opts;
 enum { GI_BFS_BATCH_AUTO = 0, GI_BFS_BATCH_PER_SOURCE = 1, GI_BFS_BATCH_BITPARALLEL = 2 };
 enum { GI_MS_PULL_AUTO = 0, GI_MS_PULL_ROWS = 1, GI_MS_PULL_SEGMENTED = 2 };

@@ -287,6 +287,7 @@ struct gi_graph_s {
     gi::DevBuf seen, fr[2], act[2], cnt, src, heavy, par, par8, hidx, csc_in;
     gi::DevBuf fc;       // the frontier masks narrowed to 16 / 32 bits for the pull gathers (k <= 32)
     gi::DevBuf fc32, acc32, rlist;  // segmented OR pull: 32-bit masks, OR accumulator, heavy rows to resolve
+    gi::DevBuf fc32hi, acc32hi;      // segmented OR pull, k > 32: the masks' upper halves and their OR
     gi::DevBuf hlist;                // sparse row pulls: the heavy chunks of rows still missing a source
     int64_t nheavy = 0;  // rows with in-degree >= 32 (pulled by whole warps)
     gi::DevBuf hch;      // their chunks: int2 (row, first in-edge offset)

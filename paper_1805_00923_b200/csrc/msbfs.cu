@@ -123,6 +123,7 @@ struct MsArgs {
   int64_t nact;
   unsigned long long all;            // mask of the k sources
   const uint32_t* acc32;             // segmented OR pull: OR of each row's in-neighbours' frontier masks
+  const uint32_t* acc32hi;           //   ... of their upper 32 bits (k > 32; else null)
   int32_t* rlist;                    // segmented OR pull: heavy rows with new bits (parents resolved by warps);
                                      //   sparse row pulls: the light rows still missing a source
   int64_t nlist;                     // sparse row pulls: rows in rlist
@@ -682,7 +683,7 @@ __global__ void __launch_bounds__(256) k_ms_list_chunks(const int2* __restrict__
   list_flush(list, cnt, s_buf[threadIdx.x >> 5], nbuf);
 }
 
-// ---- segmented OR pull (dense pull levels of passes of <= 32 sources) ----
+// ---- segmented OR pull (dense pull levels; 32-bit OR passes: one for k <= 32, two for k <= 64) ----
 // A pull level whose rows would mostly scan to the end (rows stop early only
 // once they hold every source) runs as one pass of the PageRank edge kernel over
 // the segmented layout with the reduction swapped for OR (pr_segmented.cu,
@@ -696,11 +697,12 @@ __global__ void __launch_bounds__(256) k_ms_list_chunks(const int2* __restrict__
 // the frontier masks of an OR level: 32-bit words (staged by the OR pass) and,
 // k <= 16, the 16-bit copy the parent resolution gathers
 __global__ void k_ms_narrow_or(const unsigned long long* __restrict__ f, int64_t n, uint32_t* __restrict__ o32,
-                               uint16_t* __restrict__ o16) {
+                               uint16_t* __restrict__ o16, uint32_t* __restrict__ o32hi) {
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
     const unsigned long long x = f[v];
     o32[v] = (uint32_t)x;
     if (o16) o16[v] = (uint16_t)x;
+    if (o32hi) o32hi[v] = (uint32_t)(x >> 32);
   }
 }
 
@@ -721,7 +723,9 @@ __global__ void __launch_bounds__(kMsT) k_ms_or_vertex(MsArgs A) {
     bool act = false, heavy = false;
     if (w < A.n) {
       const unsigned long long s = A.seen[w];
-      const unsigned long long nb = (unsigned long long)__ldcs(&A.acc32[w]) & ~s & A.all;
+      unsigned long long a = (unsigned long long)__ldcs(&A.acc32[w]);
+      if (A.acc32hi) a |= (unsigned long long)__ldcs(&A.acc32hi[w]) << 32;  // k > 32: the second OR pass
+      const unsigned long long nb = a & ~s & A.all;
       A.fnext[w] = nb;
       if (nb) {
         A.seen[w] = s | nb;
@@ -782,37 +786,47 @@ __global__ void __launch_bounds__(kMsT) k_ms_resolve_heavy(MsArgs A) {
     const unsigned long long nb = A.fnext[w];          // this level's new bits (k_ms_or_vertex)
     const unsigned long long known = A.seen[w] & ~nb;  // bits of earlier levels
     const int64_t e0 = (int64_t)off[w], e1 = (int64_t)off[w + 1];
-    unsigned rem = (unsigned)nb;  // k <= 32
-    int32_t plo = 0;
+    unsigned long long rem = nb;
+    int32_t plo = 0, phi = 0;  // lane L: the parents of sources L and 32 + L
     for (int64_t b = e0; rem && b < e1; b += 32 * kPullBatch) {
       int32_t v[kPullBatch];
-      unsigned f[kPullBatch];
+      unsigned long long f[kPullBatch];
 #pragma unroll
       for (int j = 0; j < kPullBatch; ++j) {
         const int64_t e = b + 32 * j + lane;
         v[j] = e < e1 ? ms_idx(&A.csc_idx[e]) : -1;
       }
 #pragma unroll
-      for (int j = 0; j < kPullBatch; ++j) f[j] = v[j] >= 0 ? (unsigned)ms_fget<FM>(A, v[j]) : 0u;
+      for (int j = 0; j < kPullBatch; ++j) f[j] = v[j] >= 0 ? ms_fget<FM>(A, v[j]) : 0ull;
       if (lane == 0) exam += min((int64_t)32 * kPullBatch, e1 - b);
 #pragma unroll
       for (int j = 0; j < kPullBatch; ++j) {
-        const unsigned mj = f[j] & rem;
-        const unsigned lo = __reduce_or_sync(0xffffffffu, mj);
-        if (!lo) continue;
+        const unsigned long long mj = f[j] & rem;
+        const unsigned lo = __reduce_or_sync(0xffffffffu, (unsigned)mj);
+        const unsigned hi = sizeof(FM) > 4 ? __reduce_or_sync(0xffffffffu, (unsigned)(mj >> 32)) : 0u;
+        if ((lo | hi) == 0u) continue;
         const int32_t vin = mj ? in_id(A, v[j]) : 0;
-        const unsigned tl = warp_transpose32(mj);
-        const int32_t p = __shfl_sync(0xffffffffu, vin, tl ? __ffs(tl) - 1 : 0);
-        if (tl) plo = p;
-        rem &= ~lo;
+        if (lo) {
+          const unsigned tl = warp_transpose32((unsigned)mj);
+          const int32_t p = __shfl_sync(0xffffffffu, vin, tl ? __ffs(tl) - 1 : 0);
+          if (tl) plo = p;
+        }
+        if (hi) {
+          const unsigned th = warp_transpose32((unsigned)(mj >> 32));
+          const int32_t p = __shfl_sync(0xffffffffu, vin, th ? __ffs(th) - 1 : 0);
+          if (th) phi = p;
+        }
+        rem &= ~(((unsigned long long)hi << 32) | lo);
       }
     }
     if (GI_MS_OUT) {  // a sector without earlier bits is written whole (placeholders), else the new entries
       int32_t* prow = A.par + par_row(A, w) * A.kp;
-      const unsigned kl = (unsigned)known, nl = (unsigned)nb;
+      const unsigned kl = (unsigned)known, nl = (unsigned)nb, kh = (unsigned)(known >> 32), nh = (unsigned)(nb >> 32);
       const int sh = lane & ~7;
       const bool wl = ((nl >> lane) & 1u) || (((nl >> sh) & 0xFFu) && !((kl >> sh) & 0xFFu));
+      const bool wh = ((nh >> lane) & 1u) || (((nh >> sh) & 0xFFu) && !((kh >> sh) & 0xFFu));
       if (wl && lane < A.kp) prow[lane] = plo;
+      if (wh && 32 + lane < A.kp) prow[32 + lane] = phi;
     }
   }
   ms_counters(A, 0, 0ull, exam, 0);
@@ -1093,13 +1107,13 @@ gi_status msbfs_t(gi_graph g, int32_t k, const int32_t* sources, const gi_bfs_op
   A.kp = kp;
   A.par_all = par_all ? 1 : 0;
   A.all = k == 64 ? ~0ull : ((1ull << k) - 1ull);
-  // segmented OR pull (k <= 32, one GPU, a graph with the segmented layout):
+  // segmented OR pull (one GPU, a graph with the segmented layout; k > 32: two OR passes):
   // AUTO takes it for a pull level while the rows still missing sources hold more
   // than segor_frac x m in-edges; GI_MS_PULL_SEGMENTED takes it for every pull
   // level, building the layout if needed
   static const char* frac_env = getenv("GI_MS_SEGOR_FRAC");
-  const double segor_frac = frac_env ? atof(frac_env) : k <= 16 ? kSegOrFrac16 : kSegOrFrac32;
-  const bool segor_ok = o.pull_kernel != GI_MS_PULL_ROWS && k <= 32 && ctx->nranks == 1 && g->ml > 0;
+  const double segor_frac = frac_env ? atof(frac_env) : k <= 16 ? kSegOrFrac16 : kSegOrFrac32;  // k > 32 as k <= 32
+  const bool segor_ok = o.pull_kernel != GI_MS_PULL_ROWS && ctx->nranks == 1 && g->ml > 0;
   bool segor_ready = segor_ok && g->seg_Z != 0;
   if (segor_ok && !segor_ready && o.pull_kernel == GI_MS_PULL_SEGMENTED) {
     GI_TRY(seg_build(g, 0, 0));
@@ -1109,6 +1123,10 @@ gi_status msbfs_t(gi_graph g, int32_t k, const int32_t* sources, const gi_bfs_op
     if (M.fc32.bytes < (size_t)(n + 16) * 4) GI_TRY(M.fc32.alloc((size_t)(n + 16) * 4));
     if (M.acc32.bytes < (size_t)(n + 16) * 4) GI_TRY(M.acc32.alloc((size_t)(n + 16) * 4));
     if (M.rlist.bytes < (size_t)(n + 1) * 4) GI_TRY(M.rlist.alloc((size_t)(n + 1) * 4));
+    if (k > 32) {  // the upper halves: a second 32-bit OR pass
+      if (M.fc32hi.bytes < (size_t)(n + 16) * 4) GI_TRY(M.fc32hi.alloc((size_t)(n + 16) * 4));
+      if (M.acc32hi.bytes < (size_t)(n + 16) * 4) GI_TRY(M.acc32hi.alloc((size_t)(n + 16) * 4));
+    }
   }
   int64_t inc = g->ml;  // in-edges of the rows still missing a source
   int segor_levels = 0, sparse_levels = 0;
@@ -1131,12 +1149,20 @@ gi_status msbfs_t(gi_graph g, int32_t k, const int32_t* sources, const gi_bfs_op
     bool sparse_used = false;
     if (pull && o.profile) GI_CUDA(cudaEventRecord(pe0, st));
     if (segor) {
-      const bool f16 = k <= 16;
+      const bool f16 = k <= 16, wide = k > 32;
       k_ms_narrow_or<<<grid_for(n, 256, sms, 8), 256, 0, st>>>(A.fcur, n, M.fc32.as<uint32_t>(),
-                                                              f16 ? M.fc.as<uint16_t>() : nullptr);
+                                                              f16 ? M.fc.as<uint16_t>() : nullptr,
+                                                              wide ? M.fc32hi.as<uint32_t>() : nullptr);
       GI_CUDA(cudaMemsetAsync(M.acc32.p, 0, (size_t)(n + 1) * 4, st));
       GI_TRY(seg_or_pass(g, M.fc32.as<uint32_t>(), M.acc32.as<uint32_t>()));
       A.acc32 = M.acc32.as<uint32_t>();
+      A.acc32hi = nullptr;
+      if (wide) {
+        GI_CUDA(cudaMemsetAsync(M.acc32hi.p, 0, (size_t)(n + 1) * 4, st));
+        GI_TRY(seg_or_pass(g, M.fc32hi.as<uint32_t>(), M.acc32hi.as<uint32_t>()));
+        A.acc32hi = M.acc32hi.as<uint32_t>();
+        launches += 1;
+      }
       A.rlist = M.rlist.as<int32_t>();
       const int lg = grid_for(n, kMsT, sms, kLightPerSM);
       const unsigned rg = (unsigned)(sms * 8);
@@ -1144,6 +1170,10 @@ gi_status msbfs_t(gi_graph g, int32_t k, const int32_t* sources, const gi_bfs_op
         A.fc = M.fc.p;
         k_ms_or_vertex<OffT, uint16_t><<<lg, kMsT, 0, st>>>(A);
         k_ms_resolve_heavy<OffT, uint16_t><<<rg, kMsT, 0, st>>>(A);
+      } else if (wide) {  // parent scans gather the 64-bit masks
+        A.fc = A.fcur;
+        k_ms_or_vertex<OffT, unsigned long long><<<lg, kMsT, 0, st>>>(A);
+        k_ms_resolve_heavy<OffT, unsigned long long><<<rg, kMsT, 0, st>>>(A);
       } else {
         A.fc = M.fc32.p;
         k_ms_or_vertex<OffT, uint32_t><<<lg, kMsT, 0, st>>>(A);

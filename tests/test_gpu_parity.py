@@ -544,10 +544,11 @@ def test_bfs_multi_bitparallel_mask_widths(gi, ctx, k):
     g.close()
 
 
-@pytest.mark.parametrize("k", [8, 16, 17, 32])
+@pytest.mark.parametrize("k", [8, 16, 17, 32, 33, 64])
 def test_bfs_multi_segmented_or_pull(gi, ctx, k):
     """Bit-parallel pull levels as an OR pass over the segmented layout (GI_MS_PULL_SEGMENTED):
-    every width it takes (16-bit parent-scan masks for k <= 16, 32-bit above), every direction
+    every width it takes (16-bit parent-scan masks for k <= 16, 32-bit up to 32, two 32-bit OR
+    passes and 64-bit parent scans above), every direction
     policy, on layouts with one, two and many source segments / destination blocks (pieces split
     across records and CTAs, unstaged sparse units), a hub row of 100k in-edges (a heavy row
     resolved by a warp) and a graph without relabelling.
