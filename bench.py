@@ -401,8 +401,9 @@ def measure_graph(g, cfg, srcs, args, stream, dev, world, direction, gi):
         pull_edges = sum(b.pull_edges_examined for b in bsp)
         bfs_bytes = (4 * pull_edges + 20 * n * pull_levels) / pull_levels
         bfs_launch_ms = pull_ms / pull_levels
-        bfs_kernel = ("k_ms_pull + k_ms_pull_heavy (bit-parallel multi-source BFS, one pull level over "
-                      f"{len(srcs)} sources)")
+        bfs_kernel = ("bit-parallel multi-source BFS, one pull level over "
+                      f"{len(srcs)} sources (averaged over the pass's segmented-OR, row and listed-row pull levels: "
+                      "k_pr_seg<OpOr> + k_ms_or_vertex + k_ms_resolve_heavy / k_ms_pull + k_ms_pull_heavy)")
     else:
         bfs_launch_ms = bfs_pass_ms / max(len(bsp), 1)
         bfs_bytes = sum(4 * b.edges_examined + 4 * b.pull_vertices + 8 * b.reached for b in bsp) / max(len(bsp), 1)

@@ -36,6 +36,7 @@
 #include <climits>
 #include <cstdio>
 #include <cstdlib>
+#include <type_traits>
 #include <vector>
 
 #include <cub/cub.cuh>
@@ -786,24 +787,26 @@ __global__ void __launch_bounds__(kMsT) k_ms_resolve_heavy(MsArgs A) {
     const unsigned long long nb = A.fnext[w];          // this level's new bits (k_ms_or_vertex)
     const unsigned long long known = A.seen[w] & ~nb;  // bits of earlier levels
     const int64_t e0 = (int64_t)off[w], e1 = (int64_t)off[w + 1];
-    unsigned long long rem = nb;
+    using RemT = typename std::conditional<(sizeof(FM) > 4), unsigned long long, unsigned>::type;
+    RemT rem = (RemT)nb;  // k <= 32: 32-bit state (fewer registers, more resident warps)
     int32_t plo = 0, phi = 0;  // lane L: the parents of sources L and 32 + L
     for (int64_t b = e0; rem && b < e1; b += 32 * kPullBatch) {
       int32_t v[kPullBatch];
-      unsigned long long f[kPullBatch];
+      RemT f[kPullBatch];
 #pragma unroll
       for (int j = 0; j < kPullBatch; ++j) {
         const int64_t e = b + 32 * j + lane;
         v[j] = e < e1 ? ms_idx(&A.csc_idx[e]) : -1;
       }
 #pragma unroll
-      for (int j = 0; j < kPullBatch; ++j) f[j] = v[j] >= 0 ? ms_fget<FM>(A, v[j]) : 0ull;
+      for (int j = 0; j < kPullBatch; ++j) f[j] = v[j] >= 0 ? (RemT)ms_fget<FM>(A, v[j]) : (RemT)0;
       if (lane == 0) exam += min((int64_t)32 * kPullBatch, e1 - b);
 #pragma unroll
       for (int j = 0; j < kPullBatch; ++j) {
-        const unsigned long long mj = f[j] & rem;
+        const RemT mj = f[j] & rem;
         const unsigned lo = __reduce_or_sync(0xffffffffu, (unsigned)mj);
-        const unsigned hi = sizeof(FM) > 4 ? __reduce_or_sync(0xffffffffu, (unsigned)(mj >> 32)) : 0u;
+        unsigned hi = 0u;
+        if constexpr (sizeof(FM) > 4) hi = __reduce_or_sync(0xffffffffu, (unsigned)((unsigned long long)mj >> 32));
         if ((lo | hi) == 0u) continue;
         const int32_t vin = mj ? in_id(A, v[j]) : 0;
         if (lo) {
@@ -811,22 +814,29 @@ __global__ void __launch_bounds__(kMsT) k_ms_resolve_heavy(MsArgs A) {
           const int32_t p = __shfl_sync(0xffffffffu, vin, tl ? __ffs(tl) - 1 : 0);
           if (tl) plo = p;
         }
-        if (hi) {
-          const unsigned th = warp_transpose32((unsigned)(mj >> 32));
-          const int32_t p = __shfl_sync(0xffffffffu, vin, th ? __ffs(th) - 1 : 0);
-          if (th) phi = p;
+        if constexpr (sizeof(FM) > 4) {
+          if (hi) {
+            const unsigned th = warp_transpose32((unsigned)((unsigned long long)mj >> 32));
+            const int32_t p = __shfl_sync(0xffffffffu, vin, th ? __ffs(th) - 1 : 0);
+            if (th) phi = p;
+          }
+          rem &= ~(((unsigned long long)hi << 32) | lo);
+        } else {
+          rem &= ~lo;
         }
-        rem &= ~(((unsigned long long)hi << 32) | lo);
       }
     }
     if (GI_MS_OUT) {  // a sector without earlier bits is written whole (placeholders), else the new entries
       int32_t* prow = A.par + par_row(A, w) * A.kp;
-      const unsigned kl = (unsigned)known, nl = (unsigned)nb, kh = (unsigned)(known >> 32), nh = (unsigned)(nb >> 32);
+      const unsigned kl = (unsigned)known, nl = (unsigned)nb;
       const int sh = lane & ~7;
       const bool wl = ((nl >> lane) & 1u) || (((nl >> sh) & 0xFFu) && !((kl >> sh) & 0xFFu));
-      const bool wh = ((nh >> lane) & 1u) || (((nh >> sh) & 0xFFu) && !((kh >> sh) & 0xFFu));
       if (wl && lane < A.kp) prow[lane] = plo;
-      if (wh && 32 + lane < A.kp) prow[32 + lane] = phi;
+      if constexpr (sizeof(FM) > 4) {
+        const unsigned kh = (unsigned)(known >> 32), nh = (unsigned)(nb >> 32);
+        const bool wh = ((nh >> lane) & 1u) || (((nh >> sh) & 0xFFu) && !((kh >> sh) & 0xFFu));
+        if (wh && 32 + lane < A.kp) prow[32 + lane] = phi;
+      }
     }
   }
   ms_counters(A, 0, 0ull, exam, 0);

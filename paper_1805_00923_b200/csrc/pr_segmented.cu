@@ -806,6 +806,23 @@ static gi_status sort_pairs(const K* ki, K* ko, const V* vi, V* vo, int64_t n, i
 
 static gi_status seg_upload_ctas(gi_graph g);
 
+// a grow-only pinned host array, kept per thread across layout builds (its
+// previous upload has completed: every block build ends synchronised)
+struct PinnedI32 {
+  int32_t* p = nullptr;
+  size_t cap = 0;
+  gi_status resize(size_t n) {
+    if (n <= cap) return GI_OK;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    cap = 0;
+    const size_t want = n + n / 4;
+    GI_CUDA(cudaMallocHost(&p, want * sizeof(int32_t)));
+    cap = want;
+    return GI_OK;
+  }
+};
+
 // the records of one destination block (CSC rows [r0, r1), fewer than 2^31
 // edges): units (block, segment) for every segment, in segment order
 struct SegBlock {
@@ -958,7 +975,7 @@ static gi_status seg_build_block(gi_graph g, int Z, int S, int64_t r0, int64_t r
   // records filled at once (millions of records: no per-record push_back)
   // (the per-record staging vectors are kept per thread: tens of MB, first-touch
   // page faults on every build otherwise)
-  static thread_local std::vector<int32_t> h_type, h_L, h_ng;
+  static thread_local PinnedI32 h_type, h_L, h_ng;  // pinned: the uploads below run at full PCIe rate
   std::vector<int32_t> h_uc(U + 1), h_crec0(NC, 0);
   std::vector<int64_t> h_cost;  // per record, for the CTA balance
   int64_t C = 0, CL = 0, NS = 0;
@@ -977,15 +994,15 @@ static gi_status seg_build_block(gi_graph g, int Z, int S, int64_t r0, int64_t r
     }
     if (C >= INT32_MAX) return fail(GI_ERR_UNSUPPORTED, "segmented pull: more than 2^31 records");
   }
-  h_type.resize(C);
-  h_L.resize(C);
-  h_ng.resize(C);
+  GI_TRY(h_type.resize(C));
+  GI_TRY(h_L.resize(C));
+  GI_TRY(h_ng.resize(C));
   h_cost.resize(C);
   for (int u = 0; u < U; ++u) {
     const int64_t c0 = h_uc[u], nl = ceil_div(h_ao[u + 1] - h_ao[u], kChunkE);
-    std::fill_n(h_type.begin() + c0, nl, 1);
-    std::fill_n(h_L.begin() + c0, nl, 0);
-    std::fill_n(h_ng.begin() + c0, nl, 0);
+    std::fill_n(h_type.p + c0, nl, 1);
+    std::fill_n(h_L.p + c0, nl, 0);
+    std::fill_n(h_ng.p + c0, nl, 0);
     std::fill_n(h_cost.begin() + c0, nl, (int64_t)(kChunkE + 2 * kPieceCost));
     for (int L = 1; L < 16; ++L) {
       const int64_t k = (int64_t)u * 16 + L;
@@ -994,10 +1011,10 @@ static gi_status seg_build_block(gi_graph g, int Z, int S, int64_t r0, int64_t r
       const bool cmp = compact_k(k);
       const int64_t R = short_groups(L, cmp), nr = ceil_div(groups, R), c = h_crec0[k];
       const int ngl = (int)(groups - (nr - 1) * R);  // the last record's groups
-      std::fill_n(h_type.begin() + c, nr, cmp ? 3 : 2);
-      std::fill_n(h_L.begin() + c, nr, L);
-      std::fill_n(h_ng.begin() + c, nr - 1, (int32_t)R);
-      h_ng[c + nr - 1] = ngl;
+      std::fill_n(h_type.p + c, nr, cmp ? 3 : 2);
+      std::fill_n(h_L.p + c, nr, L);
+      std::fill_n(h_ng.p + c, nr - 1, (int32_t)R);
+      h_ng.p[c + nr - 1] = ngl;
       std::fill_n(h_cost.begin() + c, nr - 1, R * 32 * (L + kPieceCost));
       h_cost[c + nr - 1] = (int64_t)ngl * 32 * (L + kPieceCost);
     }
@@ -1013,9 +1030,9 @@ static gi_status seg_build_block(gi_graph g, int Z, int S, int64_t r0, int64_t r
   GI_CUDA(cudaMemcpyAsync(unit_c0.p, h_uc.data(), (U + 1) * sizeof(int32_t), cudaMemcpyHostToDevice, st));
   GI_CUDA(cudaMemcpyAsync(crec0.p, h_crec0.data(), NC * sizeof(int32_t), cudaMemcpyHostToDevice, st));
   if (C > 0) {
-    GI_CUDA(cudaMemcpyAsync(rtype.p, h_type.data(), C * sizeof(int32_t), cudaMemcpyHostToDevice, st));
-    GI_CUDA(cudaMemcpyAsync(rL.p, h_L.data(), C * sizeof(int32_t), cudaMemcpyHostToDevice, st));
-    GI_CUDA(cudaMemcpyAsync(rng.p, h_ng.data(), C * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+    GI_CUDA(cudaMemcpyAsync(rtype.p, h_type.p, C * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+    GI_CUDA(cudaMemcpyAsync(rL.p, h_L.p, C * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+    GI_CUDA(cudaMemcpyAsync(rng.p, h_ng.p, C * sizeof(int32_t), cudaMemcpyHostToDevice, st));
   }
   GI_TRY(out.rec.alloc(C * kRecBytes + 16));
   GI_CUDA(cudaMemsetAsync(out.rec.p, 0, C * kRecBytes + 16, st));
@@ -1044,8 +1061,8 @@ static gi_status seg_build_block(gi_graph g, int Z, int S, int64_t r0, int64_t r
       for (int L = 1; L < 16; ++L) fprintf(f, " %d:%lld", L, (long long)hist_L[L]);
       int64_t ncmp = 0, nshort = 0;
       for (int64_t c = 0; c < C; ++c) {
-        ncmp += h_type[c] == 3;
-        nshort += h_type[c] != 1;
+        ncmp += h_type.p[c] == 3;
+        nshort += h_type.p[c] != 1;
       }
       fprintf(f, "\n  short records %lld (compact %lld)\n", (long long)nshort, (long long)ncmp);
       fclose(f);
