@@ -322,29 +322,33 @@ __global__ void k_pb_fill(uint16_t* __restrict__ a, int64_t n, uint16_t v) {
 }
 
 // (row, source segment of Z) pairs holding an edge — the segmented pull's pieces —
-// counted with a warp per row: an edge starts a piece when its segment differs
-// from the previous edge's (rows are sorted by source)
-template <typename OffT>
-__global__ void k_count_pieces(const OffT* __restrict__ off, const int32_t* __restrict__ idx, int64_t nr, int Z,
-                               unsigned long long* __restrict__ out) {
-  const int lane = threadIdx.x & 31;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  unsigned long long c = 0;
-  for (int64_t v = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; v < nr; v += nw) {
-    const int64_t b = (int64_t)off[v], e = (int64_t)off[v + 1];
-    int prev_last = -1;  // segment of the edge before this step's first
-    for (int64_t j0 = b; j0 < e; j0 += 32) {
-      const int64_t j = j0 + lane;
-      const int sg = j < e ? __ldg(&idx[j]) / Z : -2;
-      int before = __shfl_up_sync(0xffffffffu, sg, 1);
-      if (lane == 0) before = prev_last;
-      c += (j < e && sg != before);
-      prev_last = __shfl_sync(0xffffffffu, sg, 31);
-    }
-  }
+// counted edge-parallel (rows are sorted by source): with s_j = idx[j] / Z,
+//   pieces = #{j >= 1 : s_j != s_(j-1)} + #{non-empty rows starting at b : b == 0 or s_b == s_(b-1)}
+// (every segment change inside a row starts a piece; a row's first edge starts
+// one, which the global change count already holds unless its segment equals the
+// previous row's last). Was a warp per row (15 ms on config 4).
+__device__ __forceinline__ void count_add(unsigned long long c, unsigned long long* out) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-  if (lane == 0 && c) atomicAdd(out, c);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
+}
+__global__ void k_count_changes(const int32_t* __restrict__ idx, int64_t m, int Z, unsigned long long* __restrict__ out) {
+  unsigned long long c = 0;
+  const uint32_t z = (uint32_t)Z;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x + 1; j < m; j += (int64_t)gridDim.x * blockDim.x)
+    c += (uint32_t)__ldg(&idx[j]) / z != (uint32_t)__ldg(&idx[j - 1]) / z;
+  count_add(c, out);
+}
+template <typename OffT>
+__global__ void k_count_row_starts(const OffT* __restrict__ off, const int32_t* __restrict__ idx, int64_t nr, int Z,
+                                   unsigned long long* __restrict__ out) {
+  unsigned long long c = 0;
+  const uint32_t z = (uint32_t)Z;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nr; v += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = (int64_t)off[v], e = (int64_t)off[v + 1];
+    if (e > b) c += b == 0 || (uint32_t)__ldg(&idx[b]) / z == (uint32_t)__ldg(&idx[b - 1]) / z;
+  }
+  count_add(c, out);
 }
 
 template <typename OffT>
@@ -452,13 +456,16 @@ gi_status pb_count_pieces(gi_graph g, int Z, int64_t* pieces) {
   DevBuf c;
   GI_TRY(c.alloc(sizeof(unsigned long long)));
   GI_CUDA(cudaMemsetAsync(c.p, 0, sizeof(unsigned long long), st));
-  const int grid = grid_for(g->nr * 32, 256, g->ctx->num_sms, 16);
+  const int sms = g->ctx->num_sms;
+  if (g->ml > 1)
+    k_count_changes<<<grid_for(g->ml, 256, sms, 8), 256, 0, st>>>(g->csc_idx.as<int32_t>(), g->ml, Z,
+                                                                  c.as<unsigned long long>());
   if (g->off64)
-    k_count_pieces<int64_t><<<grid, 256, 0, st>>>(g->csc_off.as<int64_t>(), g->csc_idx.as<int32_t>(), g->nr, Z,
-                                                   c.as<unsigned long long>());
+    k_count_row_starts<int64_t><<<grid_for(g->nr, 256, sms, 8), 256, 0, st>>>(
+        g->csc_off.as<int64_t>(), g->csc_idx.as<int32_t>(), g->nr, Z, c.as<unsigned long long>());
   else
-    k_count_pieces<int32_t><<<grid, 256, 0, st>>>(g->csc_off.as<int32_t>(), g->csc_idx.as<int32_t>(), g->nr, Z,
-                                                   c.as<unsigned long long>());
+    k_count_row_starts<int32_t><<<grid_for(g->nr, 256, sms, 8), 256, 0, st>>>(
+        g->csc_off.as<int32_t>(), g->csc_idx.as<int32_t>(), g->nr, Z, c.as<unsigned long long>());
   unsigned long long h = 0;
   GI_CUDA(cudaMemcpyAsync(&h, c.p, sizeof h, cudaMemcpyDeviceToHost, st));
   GI_CUDA(cudaStreamSynchronize(st));
