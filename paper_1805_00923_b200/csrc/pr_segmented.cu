@@ -47,6 +47,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cub/cub.cuh>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -977,7 +978,7 @@ static gi_status seg_build_block(gi_graph g, int Z, int S, int64_t r0, int64_t r
   // page faults on every build otherwise)
   static thread_local PinnedI32 h_type, h_L, h_ng;  // pinned: the uploads below run at full PCIe rate
   std::vector<int32_t> h_uc(U + 1), h_crec0(NC, 0);
-  std::vector<int64_t> h_cost;  // per record, for the CTA balance
+  std::vector<int64_t>& h_cost = out.cost;  // per record, for the CTA balance (capacity kept across builds)
   int64_t C = 0, CL = 0, NS = 0;
   for (int u = 0; u < U; ++u) {
     h_uc[u] = (int32_t)C;
@@ -1070,7 +1071,6 @@ static gi_status seg_build_block(gi_graph g, int Z, int S, int64_t r0, int64_t r
   GI_CUDA(cudaGetLastError());
   GI_CUDA(cudaStreamSynchronize(st));  // the temporaries are freed on return
   out.uc = std::move(h_uc);
-  out.cost = std::move(h_cost);
   out.C = C;
   out.CL = CL;
   out.NS = NS;
@@ -1128,31 +1128,38 @@ static gi_status seg_build_t(gi_graph g, int Z, int64_t DB) {
   const int B = (int)br.size() - 1;
   if ((int64_t)B * S >= INT32_MAX / 2) return fail(GI_ERR_UNSUPPORTED, "segmented pull: too many units");
   const int U = B * S;
-  std::vector<SegBlock> blocks(B);
+  // the blocks (their host vectors keep their capacity across layout builds on
+  // this thread: tens of MB, first-touch page faults on every build otherwise)
+  static thread_local std::vector<std::unique_ptr<SegBlock>> tl_blocks;
+  while ((int)tl_blocks.size() < B) tl_blocks.emplace_back(new SegBlock());
+  struct Release {  // the blocks' device records go back to the cache on every return
+    std::vector<std::unique_ptr<SegBlock>>& v;
+    int b;
+    ~Release() {
+      for (int i = 0; i < b; ++i) v[i]->rec.reset();
+    }
+  } release_{tl_blocks, B};
+  auto blocks = [&](int b) -> SegBlock& { return *tl_blocks[b]; };
   int64_t C = 0, CL = 0, NS = 0, P = 0;
   std::vector<double> tblk;
   for (int b = 0; b < B; ++b) {
     const auto tq = std::chrono::steady_clock::now();
-    GI_TRY(seg_build_block<OffT>(g, Z, S, br[b], br[b + 1], blocks[b]));
+    GI_TRY(seg_build_block<OffT>(g, Z, S, br[b], br[b + 1], blocks(b)));
     tblk.push_back(std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tq).count());
-    C += blocks[b].C;
-    CL += blocks[b].CL;
-    NS += blocks[b].NS;
-    P += blocks[b].P;
+    C += blocks(b).C;
+    CL += blocks(b).CL;
+    NS += blocks(b).NS;
+    P += blocks(b).P;
     if (C >= INT32_MAX) return fail(GI_ERR_UNSUPPORTED, "segmented pull: more than 2^31 records");
   }
   // concatenate the blocks' records; unit u = b * S + segment
   std::vector<int32_t> h_uc(U + 1);
-  std::vector<int64_t> h_cost;
-  if (B == 1) h_cost.swap(blocks[0].cost);
-  else h_cost.reserve(C);
   GI_TRY(g->seg_rec.alloc(C * kRecBytes + 16));
   GI_CUDA(cudaMemsetAsync(g->seg_rec.as<uint8_t>() + C * kRecBytes, 0, 16, st));
   int64_t cb = 0;
   for (int b = 0; b < B; ++b) {
-    SegBlock& k = blocks[b];
+    SegBlock& k = blocks(b);
     for (int s = 0; s < S; ++s) h_uc[b * S + s] = (int32_t)(cb + k.uc[s]);
-    if (B > 1) h_cost.insert(h_cost.end(), k.cost.begin(), k.cost.end());
     if (k.C > 0)
       GI_CUDA(cudaMemcpyAsync(g->seg_rec.as<uint8_t>() + cb * kRecBytes, k.rec.p, k.C * kRecBytes,
                               cudaMemcpyDeviceToDevice, st));
@@ -1160,16 +1167,18 @@ static gi_status seg_build_t(gi_graph g, int Z, int64_t DB) {
   }
   h_uc[U] = (int32_t)C;
   GI_CUDA(cudaStreamSynchronize(st));
-  blocks.clear();
+  for (int b = 0; b < B; ++b) blocks(b).rec.reset();
   const auto tb1 = std::chrono::steady_clock::now();
   // ---- cost-balanced CTA ranges (every staged unit start adds kUnitCost)
   const int ctas = sms;
   std::vector<int32_t> h_cta(ctas + 1, (int32_t)C);
   {
     std::vector<int64_t> pre(C + 1, 0);
-    int u = 0;
+    int u = 0, kb = 0;
+    int64_t kc0 = 0;  // first record of block kb
     for (int64_t c = 0; c < C; ++c) {
-      int64_t cost = h_cost[c];
+      while (c - kc0 >= blocks(kb).C) kc0 += blocks(kb++).C;
+      int64_t cost = blocks(kb).cost[c - kc0];
       while (u + 1 < U && h_uc[u + 1] <= c) ++u;  // u: the unit holding record c
       if (h_uc[u + 1] - h_uc[u] < kDirectRecs) cost *= kDirectCost;  // unstaged: L2 gathers
       else if (h_uc[u] == c) cost += kUnitCost;
