@@ -689,41 +689,48 @@ __global__ void k_long_dst(const int64_t* __restrict__ asz, const int64_t* __res
   }
 }
 
-// headers of all records; short records also get padding lanes (index Z, trash row)
+// every word of every record (a warp per record, coalesced stores; no memset
+// first): headers; long records' index padding (overwritten by the real slots)
+// and zero destinations / mask; short records' padding lanes (index Z, trash
+// row) in their groups, zeros past them
 __global__ void k_record_headers(const int32_t* __restrict__ rtype, const int32_t* __restrict__ rL,
                                  const int32_t* __restrict__ rng, int64_t C, int Z, int trash,
                                  const int32_t* __restrict__ unit_c0, int U, int S, uint8_t* __restrict__ rec) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < C * (kRecBytes / 4);
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t c = i / (kRecBytes / 4);
-    const int o = (int)(i % (kRecBytes / 4)) * 4;
-    uint32_t* w = reinterpret_cast<uint32_t*>(rec + c * kRecBytes + o);
-    const int type = rtype[c];
-    if (o == 0) *w = (uint32_t)type;
-    else if (o == 4) *w = (uint32_t)rL[c];
-    else if (o == 8) *w = (uint32_t)rng[c];
-    else if (o == 12) {  // the record's source segment (read when its unit is gathered unstaged)
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const uint32_t zz = (uint32_t)Z | ((uint32_t)Z << 16);
+  for (int64_t c = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; c < C; c += nw) {
+    const int type = __ldg(&rtype[c]), L = __ldg(&rL[c]), ng = __ldg(&rng[c]);
+    uint32_t seg = 0;
+    if (lane == 3) {  // the record's source segment (read when its unit is gathered unstaged)
       int lo = 0, hi = U - 1;  // last unit u with unit_c0[u] <= c
       while (lo < hi) {
         const int mid = (lo + hi + 1) >> 1;
-        if (unit_c0[mid] <= c) lo = mid;
+        if (__ldg(&unit_c0[mid]) <= c) lo = mid;
         else hi = mid - 1;
       }
-      *w = (uint32_t)(lo % S);
-    } else if (o >= kRecHdr) {
-      if (type == 1) {
-        if (o < kLDst) *w = (uint32_t)Z | ((uint32_t)Z << 16);  // idx padding (overwritten by real slots)
+      seg = (uint32_t)(lo % S);
+    }
+    const bool compact = type == 3;
+    const int gb = type == 1 ? 1 : short_group_bytes(L, compact);
+    uint32_t* r = reinterpret_cast<uint32_t*>(rec + c * kRecBytes);
+    for (int wi = lane; wi < kRecBytes / 4; wi += 32) {
+      const int o = 4 * wi;
+      uint32_t v = 0u;
+      if (o < kRecHdr) {
+        v = o == 0 ? (uint32_t)type : o == 4 ? (uint32_t)L : o == 8 ? (uint32_t)ng : seg;
+      } else if (type == 1) {
+        if (o < kLDst) v = zz;
       } else {
-        const int L = rL[c];
-        const bool compact = type == 3;
-        const int gb = short_group_bytes(L, compact), g = (o - kRecHdr) / gb, go = (o - kRecHdr) % gb;
-        if (g < rng[c]) {
-          if (go < 64 * L) *w = (uint32_t)Z | ((uint32_t)Z << 16);        // idx padding (the identity slot)
-          else if (!compact) *w = (uint32_t)trash;                          // wide: trash destination
-          else if (go < 64 * L + 64) *w = 0xFFFFFFFFu;                      // compact: trash offsets
-          else *w = 0u;                                                     // compact: base (set by placement)
+        const int g = (o - kRecHdr) / gb, go = (o - kRecHdr) - g * gb;
+        if (g < ng) {
+          if (go < 64 * L) v = zz;                          // idx padding (the identity slot)
+          else if (!compact) v = (uint32_t)trash;           // wide: trash destination
+          else if (go < 64 * L + 64) v = 0xFFFFFFFFu;       // compact: trash offsets
+          // compact: base 0 (set by placement)
         }
       }
+      r[wi] = v;
     }
   }
 }
@@ -1036,9 +1043,9 @@ static gi_status seg_build_block(gi_graph g, int Z, int S, int64_t r0, int64_t r
     GI_CUDA(cudaMemcpyAsync(rng.p, h_ng.p, C * sizeof(int32_t), cudaMemcpyHostToDevice, st));
   }
   GI_TRY(out.rec.alloc(C * kRecBytes + 16));
-  GI_CUDA(cudaMemsetAsync(out.rec.p, 0, C * kRecBytes + 16, st));
+  GI_CUDA(cudaMemsetAsync(out.rec.as<uint8_t>() + C * kRecBytes, 0, 16, st));  // k_record_headers writes the rest
   const int trash = (int)g->nr;  // accumulator row past the owned rows
-  k_record_headers<<<grid_for(C * (kRecBytes / 4), 256, sms), 256, 0, st>>>(
+  k_record_headers<<<grid_for(C * 32, 256, sms, 8), 256, 0, st>>>(
       rtype.as<int32_t>(), rL.as<int32_t>(), rng.as<int32_t>(), C, Z, trash, unit_c0.as<int32_t>(), (int)U, S,
       out.rec.as<uint8_t>());
   mark("headers");
