@@ -647,12 +647,14 @@ __global__ void k_place_long(const int64_t* __restrict__ asz, const int64_t* __r
                              const int32_t* __restrict__ unit_c0, const int64_t* __restrict__ pstart,
                              const uint32_t* __restrict__ skey, const OffT* __restrict__ order,
                              const int32_t* __restrict__ idx, const int32_t* __restrict__ pdst, int64_t P, int64_t m,
-                             int Z, int S, uint8_t* __restrict__ rec) {
-  // a warp per piece, its lanes striding over the piece's edges (a hub's piece
-  // holds up to ~10^5 edges: one thread per piece serialised the build on them)
+                             int Z, int S, const int32_t* __restrict__ lpid, int64_t NL, uint8_t* __restrict__ rec) {
+  // a warp per long piece (lpid: the long pieces' ids, the tail of the class
+  // order), its lanes striding over the piece's edges (a hub's piece holds up to
+  // ~10^5 edges: one thread per piece serialised the build on them)
   const int lane = threadIdx.x & 31;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t p = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; p < P; p += nw) {
+  for (int64_t q = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; q < NL; q += nw) {
+    const int64_t p = __ldg(&lpid[q]);
     if (asz[p] == 0) continue;
     const int u = punit[p];
     const int64_t s0 = (int64_t)unit_c0[u] * kChunkE + (aoff[p] - aoff[unit_p0[u]]);  // slot in record units
@@ -673,9 +675,10 @@ __global__ void k_place_long(const int64_t* __restrict__ asz, const int64_t* __r
 // dst table of the long records (after every mask is complete)
 __global__ void k_long_dst(const int64_t* __restrict__ asz, const int64_t* __restrict__ aoff,
                            const int32_t* __restrict__ punit, const int64_t* __restrict__ unit_p0,
-                           const int32_t* __restrict__ unit_c0, const int32_t* __restrict__ pdst, int64_t P,
-                           uint8_t* __restrict__ rec) {
-  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < P; p += (int64_t)gridDim.x * blockDim.x) {
+                           const int32_t* __restrict__ unit_c0, const int32_t* __restrict__ pdst,
+                           const int32_t* __restrict__ lpid, int64_t NL, uint8_t* __restrict__ rec) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < NL; q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = __ldg(&lpid[q]);
     if (asz[p] == 0) continue;
     const int u = punit[p];
     const int64_t s0 = (int64_t)unit_c0[u] * kChunkE + (aoff[p] - aoff[unit_p0[u]]), s1 = s0 + asz[p];
@@ -1049,14 +1052,17 @@ static gi_status seg_build_block(gi_graph g, int Z, int S, int64_t r0, int64_t r
       rtype.as<int32_t>(), rL.as<int32_t>(), rng.as<int32_t>(), C, Z, trash, unit_c0.as<int32_t>(), (int)U, S,
       out.rec.as<uint8_t>());
   mark("headers");
-  k_place_long<OffT><<<grid_for(P * 32, 256, sms, 16), 256, 0, st>>>(
-      asz.as<int64_t>(), aoff.as<int64_t>(), punit.as<int32_t>(), unit_p0.as<int64_t>(), unit_c0.as<int32_t>(),
-      pstart.as<int64_t>(), skey.as<uint32_t>(), order.as<OffT>(), idx, pdst.as<int32_t>(), P, m, Z, S,
-      out.rec.as<uint8_t>());
+  const int64_t NL = P - NS;  // long pieces: the tail of the class order (sentinel key)
+  if (NL > 0)
+    k_place_long<OffT><<<grid_for(NL * 32, 256, sms, 16), 256, 0, st>>>(
+        asz.as<int64_t>(), aoff.as<int64_t>(), punit.as<int32_t>(), unit_p0.as<int64_t>(), unit_c0.as<int32_t>(),
+        pstart.as<int64_t>(), skey.as<uint32_t>(), order.as<OffT>(), idx, pdst.as<int32_t>(), P, m, Z, S,
+        spid.as<int32_t>() + NS, NL, out.rec.as<uint8_t>());
   mark("place_long");
-  k_long_dst<<<grid_for(P, 256, sms), 256, 0, st>>>(asz.as<int64_t>(), aoff.as<int64_t>(), punit.as<int32_t>(),
-                                                    unit_p0.as<int64_t>(), unit_c0.as<int32_t>(), pdst.as<int32_t>(),
-                                                    P, out.rec.as<uint8_t>());
+  if (NL > 0)
+    k_long_dst<<<grid_for(NL, 256, sms), 256, 0, st>>>(asz.as<int64_t>(), aoff.as<int64_t>(), punit.as<int32_t>(),
+                                                       unit_p0.as<int64_t>(), unit_c0.as<int32_t>(), pdst.as<int32_t>(),
+                                                       spid.as<int32_t>() + NS, NL, out.rec.as<uint8_t>());
   if (NS > 0)
     k_place_short<OffT><<<grid_for(NS, 256, sms), 256, 0, st>>>(
         sckey.as<uint32_t>(), spid.as<int32_t>(), NS, cstart.as<int64_t>(), crec0.as<int32_t>(), pstart.as<int64_t>(),
