@@ -628,6 +628,32 @@ def test_bfs_multi_or_pull_auto(gi, ctx):
     g.close()
 
 
+@pytest.mark.parametrize("k", [16, 33, 64])
+def test_bfs_multi_listed_row_pull(gi, ctx, k):
+    """Late pull levels over the listed rows still missing a source (the rows' in-edges < m/64),
+    every mask width (16-bit gathers, 32/64-bit masks): a symmetrised RMAT graph under the pull-only
+    policy, where the rows of the giant component complete and the last levels turn sparse.
+    Validated against the oracle."""
+    cfg = graphgen.CONFIGS[1]
+    s, d = cfg.edges()
+    g = gi.Graph(ctx, cfg.n, s, d, gi.GI_DEFAULT_FLAGS | gi.GI_SYMMETRIZE)
+    go = oracle.build_graph(cfg.n, s, d, symmetrize=True)
+    sources = graphgen.pick_sources(cfg.n, s, d, k, 600 + k).tolist()
+    for pk in (gi.GI_MS_PULL_AUTO, gi.GI_MS_PULL_SEGMENTED):
+        par, st = g.bfs_multi(sources, batch=gi.GI_BFS_BATCH_BITPARALLEL, policy=gi.GI_BFS_PULL_ONLY,
+                              pull_kernel=pk)
+        if pk == gi.GI_MS_PULL_AUTO:  # no layout: row pulls, the late ones listed
+            assert st[0].pull_sparse_levels > 0
+        else:  # forced OR passes at every pull level (the layout built on demand)
+            assert st[0].pull_or_levels == st[0].pull_levels
+        for i, src in enumerate(sources):
+            depth = oracle.bfs_depth(go, src)
+            ok, msg = oracle.validate_bfs(go, src, par[i], depth)
+            assert ok, f"k={k} pull_kernel={pk} src={src}: {msg}"
+            assert st[i].reached == int((depth >= 0).sum())
+    g.close()
+
+
 def test_bfs_multi_bitparallel_edge_cases(gi, ctx):
     """Bit-parallel passes on degenerate inputs: no edges; isolated and sink
     sources; k = 1, 64 and 65; a 100k-leaf star under every direction policy —
