@@ -253,8 +253,13 @@ __device__ __forceinline__ void reduce_long(const SegArgs& A, const uint8_t* r, 
   T v[kLaneE];
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
-    v[2 * j] = seg_val<G, OP>(sc, w[j] & 0xFFFFu, A.Z);
-    v[2 * j + 1] = seg_val<G, OP>(sc, w[j] >> 16, A.Z);
+    if (MODE == 3) {  // diagnostics: the same gathers made bank-conflict free (wrong sums)
+      v[2 * j] = seg_val<G, OP>(sc, min(((w[j] & 0xFFFFu) & ~31u) | (uint32_t)lane, (uint32_t)A.Z), A.Z);
+      v[2 * j + 1] = seg_val<G, OP>(sc, min(((w[j] >> 16) & ~31u) | (uint32_t)lane, (uint32_t)A.Z), A.Z);
+    } else {
+      v[2 * j] = seg_val<G, OP>(sc, w[j] & 0xFFFFu, A.Z);
+      v[2 * j + 1] = seg_val<G, OP>(sc, w[j] >> 16, A.Z);
+    }
   }
 #pragma unroll
   for (int s = 1; s < kLaneE; s <<= 1)
@@ -295,7 +300,11 @@ __device__ __forceinline__ void reduce_short(const SegArgs& A, const uint8_t* r,
     }
     T s = OP::id();
 #pragma unroll 4
-    for (int k = 0; k < L; ++k) s = OP::op(s, seg_val<G, OP>(sc, *reinterpret_cast<const uint16_t*>(b + 64 * k), A.Z));
+    for (int k = 0; k < L; ++k) {
+      uint32_t o = *reinterpret_cast<const uint16_t*>(b + 64 * k);
+      if (MODE == 3) o = min((o & ~31u) | (uint32_t)lane, (uint32_t)A.Z);  // diagnostics: conflict-free
+      s = OP::op(s, seg_val<G, OP>(sc, o, A.Z));
+    }
     if (MODE == 1) {
       if (s == (T)-1) A.acc[lane] += (float)s;
     } else {
@@ -1413,7 +1422,8 @@ gi_status seg_edge_pass(gi_graph g, const float* cin) {
   S.trash = (int)g->nr;
   S.steal = g->seg_steal;
   static const int mode = getenv("GI_SEG_MODE") ? atoi(getenv("GI_SEG_MODE")) : 0;
-  void (*kern)(SegArgs) = mode == 1 ? k_pr_seg<1, OpSum> : mode == 2 ? k_pr_seg<2, OpSum> : k_pr_seg<0, OpSum>;
+  void (*kern)(SegArgs) = mode == 1 ? k_pr_seg<1, OpSum> : mode == 2 ? k_pr_seg<2, OpSum>
+                        : mode == 3 ? k_pr_seg<3, OpSum> : k_pr_seg<0, OpSum>;
   const size_t dyn = seg_dyn_smem(g->seg_Z);
   static size_t attr_set[64] = {};  // per device: largest dynamic smem size configured so far
   const int dev = g->ctx->device & 63;
@@ -1421,6 +1431,7 @@ gi_status seg_edge_pass(gi_graph g, const float* cin) {
     GI_CUDA(cudaFuncSetAttribute(k_pr_seg<0, OpSum>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
     GI_CUDA(cudaFuncSetAttribute(k_pr_seg<1, OpSum>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
     GI_CUDA(cudaFuncSetAttribute(k_pr_seg<2, OpSum>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+    GI_CUDA(cudaFuncSetAttribute(k_pr_seg<3, OpSum>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
     attr_set[dev] = dyn;
   }
   static const char* dbg = getenv("GI_DEBUG_SEG_TIMING");  // diagnostics: file to append per-CTA timings to
