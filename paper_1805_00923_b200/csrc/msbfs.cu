@@ -81,6 +81,10 @@ constexpr int kPushChunk = 256;   // push: out-edges per warp at least
 #define GI_MS_BATCH 2
 #endif
 constexpr int kPullBatch = GI_MS_BATCH;  // in-edge gathers in flight per pull step
+#ifndef GI_MS_OR_BATCH
+#define GI_MS_OR_BATCH 2
+#endif
+constexpr int kOrBatch = GI_MS_OR_BATCH;  // ... per step of a light row's parent scan (OR levels)
 #ifndef GI_MS_HCHUNK
 #define GI_MS_HCHUNK 1024
 #endif
@@ -740,16 +744,16 @@ __global__ void __launch_bounds__(kMsT) k_ms_or_vertex(MsArgs A) {
           heavy = true;
         } else {  // the parents of the new bits: the first frontier in-neighbour bringing each
           unsigned long long rem = nb, known = s;
-          for (int64_t e = e0; rem && e < e1; e += kPullBatch) {
-            int32_t v[kPullBatch];
-            unsigned long long f[kPullBatch];
+          for (int64_t e = e0; rem && e < e1; e += kOrBatch) {
+            int32_t v[kOrBatch];
+            unsigned long long f[kOrBatch];
 #pragma unroll
-            for (int j = 0; j < kPullBatch; ++j) v[j] = e + j < e1 ? ms_idx(&A.csc_idx[e + j]) : -1;
+            for (int j = 0; j < kOrBatch; ++j) v[j] = e + j < e1 ? ms_idx(&A.csc_idx[e + j]) : -1;
 #pragma unroll
-            for (int j = 0; j < kPullBatch; ++j) f[j] = v[j] >= 0 ? ms_fget<FM>(A, v[j]) : 0ull;
-            exam += min((int64_t)kPullBatch, e1 - e);
+            for (int j = 0; j < kOrBatch; ++j) f[j] = v[j] >= 0 ? ms_fget<FM>(A, v[j]) : 0ull;
+            exam += min((int64_t)kOrBatch, e1 - e);
 #pragma unroll
-            for (int j = 0; j < kPullBatch; ++j) {
+            for (int j = 0; j < kOrBatch; ++j) {
               const unsigned long long m = f[j] & rem;
               if (m) {
                 if (GI_MS_OUT) {
