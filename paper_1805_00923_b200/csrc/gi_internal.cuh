@@ -289,6 +289,7 @@ struct gi_graph_s {
     gi::DevBuf fc32, acc32, rlist;  // segmented OR pull: 32-bit masks, OR accumulator, heavy rows to resolve
     gi::DevBuf fc32hi, acc32hi;      // segmented OR pull, k > 32: the masks' upper halves and their OR
     gi::DevBuf hlist;                // sparse row pulls: the heavy chunks of rows still missing a source
+    gi::DevBuf tsum;                 // push levels: tile sums of the out-degree prefix
     int64_t nheavy = 0;  // rows with in-degree >= 32 (pulled by whole warps)
     gi::DevBuf hch;      // their chunks: int2 (row, first in-edge offset)
     int64_t nhch = 0;

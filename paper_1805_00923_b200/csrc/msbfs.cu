@@ -846,6 +846,80 @@ __global__ void __launch_bounds__(kMsT) k_ms_resolve_heavy(MsArgs A) {
   ms_counters(A, 0, 0ull, exam, 0);
 }
 
+// ---- the push levels' edge prefix: dp[i] = sum of outdeg over act[0..i] (inclusive),
+// in three passes over tiles of kScanTile active vertices: tile sums, one block
+// scanning the tile sums, then each tile's scan plus its offset
+constexpr int kScanT = 256, kScanVT = 8, kScanTile = kScanT * kScanVT;
+// block-wide exclusive scan of one value per thread (warp shuffles + one smem round)
+__device__ __forceinline__ long long block_excl_scan(long long x, long long* total) {
+  __shared__ long long s_w[32];
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5, nwp = blockDim.x >> 5;
+  long long incl = x;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const long long y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) s_w[wp] = incl;
+  __syncthreads();
+  if (wp == 0) {
+    long long w = lane < nwp ? s_w[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const long long y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += y;
+    }
+    if (lane < nwp) s_w[lane] = w;  // inclusive warp prefix
+  }
+  __syncthreads();
+  const long long before = (wp > 0 ? s_w[wp - 1] : 0) + incl - x;
+  *total = s_w[nwp - 1];
+  __syncthreads();
+  return before;
+}
+__global__ void __launch_bounds__(kScanT) k_deg_tile_sums(const int32_t* __restrict__ act, const int32_t* __restrict__ od,
+                                                         int64_t nact, long long* __restrict__ tsum) {
+  const int64_t base = blockIdx.x * (int64_t)kScanTile + threadIdx.x * kScanVT;
+  long long x = 0;
+#pragma unroll
+  for (int j = 0; j < kScanVT; ++j)
+    if (base + j < nact) x += __ldg(&od[__ldg(&act[base + j])]);
+  long long t;
+  block_excl_scan(x, &t);
+  if (threadIdx.x == 0) tsum[blockIdx.x] = t;
+}
+__global__ void __launch_bounds__(1024) k_scan_tile_sums(long long* __restrict__ tsum, int64_t nt) {
+  // one block: thread t scans its run of ceil(nt / 1024) tile sums; exclusive result in place
+  const int64_t per = (nt + 1023) / 1024, b0 = threadIdx.x * per, b1 = min(nt, b0 + per);
+  long long x = 0;
+  for (int64_t i = b0; i < b1; ++i) x += tsum[i];
+  long long t;
+  long long run = block_excl_scan(x, &t);
+  for (int64_t i = b0; i < b1; ++i) {
+    const long long v = tsum[i];
+    tsum[i] = run;
+    run += v;
+  }
+}
+__global__ void __launch_bounds__(kScanT) k_deg_scan(const int32_t* __restrict__ act, const int32_t* __restrict__ od,
+                                                    int64_t nact, const long long* __restrict__ toff,
+                                                    long long* __restrict__ dp) {
+  const int64_t base = blockIdx.x * (int64_t)kScanTile + threadIdx.x * kScanVT;
+  long long d[kScanVT], x = 0;
+#pragma unroll
+  for (int j = 0; j < kScanVT; ++j) {
+    d[j] = base + j < nact ? (long long)__ldg(&od[__ldg(&act[base + j])]) : 0;
+    x += d[j];
+  }
+  long long t;
+  long long run = block_excl_scan(x, &t) + toff[blockIdx.x];
+#pragma unroll
+  for (int j = 0; j < kScanVT; ++j) {
+    run += d[j];
+    if (base + j < nact) dp[base + j] = run;
+  }
+}
+
 // sources: bit i at source i (internal id), its own parent in row i, active list
 __global__ void k_ms_init(const int32_t* __restrict__ src_in, int k, const int32_t* __restrict__ inv, int64_t n,
                           const int32_t* __restrict__ outdeg, unsigned long long* seen, unsigned long long* f0,
@@ -1255,11 +1329,13 @@ gi_status msbfs_t(gi_graph g, int32_t k, const int32_t* sources, const gi_bfs_op
       GI_CUDA(cudaMemsetAsync(A.fnext, 0, n * 8, st));
       long long* dp = M.chunks[1].as<long long>();
 
-      size_t tb = M.scan_bytes;
-      GI_CUDA(cub::DeviceScan::InclusiveSum(
-          M.scan_tmp.p, tb, cub::TransformInputIterator<long long, OutdegOf, const int32_t*>(A.acur, OutdegOf{A.outdeg}),
-          dp, (int)nact, st));
-      launches += 2;
+      const int64_t nt = (nact + kScanTile - 1) / kScanTile;
+      if (M.tsum.bytes < (size_t)(nt + 1) * 8) GI_TRY(M.tsum.alloc((size_t)(nt + 1) * 8));
+      long long* ts = M.tsum.as<long long>();
+      k_deg_tile_sums<<<(unsigned)nt, kScanT, 0, st>>>(A.acur, A.outdeg, nact, ts);
+      k_scan_tile_sums<<<1, 1024, 0, st>>>(ts, nt);
+      k_deg_scan<<<(unsigned)nt, kScanT, 0, st>>>(A.acur, A.outdeg, nact, ts, dp);
+      launches += 3;
       k_ms_push<OffT><<<grid_for((sdeg + kPushChunk - 1) / kPushChunk * 32, kMsT, sms, 8), kMsT, 0, st>>>(A, dp);
     }
     GI_CUDA(cudaGetLastError());
