@@ -1230,8 +1230,14 @@ gi_status msbfs_t(gi_graph g, int32_t k, const int32_t* sources, const gi_bfs_op
     A.anext = M.act[c ^ 1].as<int32_t>();
     A.nact = nact;
     GI_CUDA(cudaMemsetAsync(cnt, 0, 6 * 8, st));
+    // R21, plus: a listed-row pull (the rows still missing a source hold < m/64
+    // in-edges) replaces a push whose frontier's out-edges outweigh the listing
+    // (a pass over the n rows) and the listed in-edges: config 5's fifth level,
+    // 214 M out-edges against 0.34 M listed in-edges, 4.3 ms as a push
+    const bool sparse_pull = o.pull_kernel != GI_MS_PULL_ROWS && level > 0 &&
+                             (double)inc < sparse_frac * (double)g->ml && sdeg > n / 2 + 2 * inc;
     const bool pull = o.policy == GI_BFS_PULL_ONLY ? level > 0
-                                                   : (o.policy == GI_BFS_AUTO && nact + sdeg > mdiv);
+                                                   : (o.policy == GI_BFS_AUTO && (nact + sdeg > mdiv || sparse_pull));
     const bool segor = pull && segor_ready &&
                        (o.pull_kernel == GI_MS_PULL_SEGMENTED || (double)inc > segor_frac * (double)g->ml);
     bool sparse_used = false;
