@@ -202,7 +202,9 @@ def bench_config(cfg, n, m, k, args, world, mode):
     return {"workload": f"{cfg.name} (BASELINE configs[{cfg.idx - 1}])", "n": n, "m": m,
             "pr_iters": cfg.pr_iters, "damping": cfg.damping, "bfs_sources": k,
             "pr_direction": args.pr_direction,
-            "bfs_policy": ("auto: bit-parallel pass of up to 64 sources, pull iff |F| + sum outdeg F > m/8"
+            "bfs_policy": ("auto: bit-parallel pass of up to 64 sources, pull iff |F| + sum outdeg F > m/8 "
+                           "(m/12 when 16n bytes of vertex state exceed L2) or a listed-row pull is cheaper; dense "
+                           "pulls as segmented OR passes when the graph has the layout"
                            if mode != "partition" or world == 1 else
                            "auto per source: pull iff |F| + sum outdeg F > m/20 (distributed level loop)"),
             "l2": "inputs larger than L2 (CSR+CSC ~ 8m bytes > 126 MB), no flush",

@@ -66,6 +66,7 @@ constexpr int kMsT = 256;
 #endif
 constexpr int64_t kHeavy = GI_MS_HEAVY;  // rows with at least this many in-edges are pulled by whole warps
 constexpr int kMsPullDiv = 8;     // bit-parallel direction rule: pull iff |F| + sum outdeg F > m / 8 (R21)
+constexpr int kMsPullDivBig = 12; // ... m / 12 when the vertex state the push hits at random exceeds L2
 // segmented OR pull iff the rows still missing a source hold > this fraction of
 // the in-edges: a row pull scans those rows to the end. With 16-bit masks the row
 // pull is cheap enough to win below ~0.6 m (config 4, 16 sources: level 2 at m
@@ -1161,7 +1162,13 @@ gi_status msbfs_t(gi_graph g, int32_t k, const int32_t* sources, const gi_bfs_op
   }
   unsigned long long* cnt = M.cnt.as<unsigned long long>();
   int64_t* h = ctx->h_scratch;
-  const int64_t mdiv = g->m / (o.threshold_div > 0 ? o.threshold_div : kMsPullDiv);
+  // R21's m/8, or m/12 when the push's random atomics on seen / fr_next (16 bytes
+  // per vertex) miss L2: config 5 45 ms at m/12 against 49 at m/8, config 4 neutral,
+  // config 2 (in L2) 2.44 ms at m/8 against 2.86 at m/12
+  int l2 = 0;
+  if (cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, ctx->device) != cudaSuccess) l2 = 0;
+  const int div_auto = (double)n * 16.0 > (double)l2 ? kMsPullDivBig : kMsPullDiv;
+  const int64_t mdiv = g->m / (o.threshold_div > 0 ? o.threshold_div : div_auto);
   std::vector<int32_t> levels(k, 1);
   int64_t examined = 0;
   int launches = 0;

@@ -1,7 +1,7 @@
 """One bench-like bit-parallel BFS pass on a config (after one PageRank call builds the segmented
 layout, as in the bench step): the target of an ncu capture of every kernel of a pass.
 
-usage: python tools/msbfs_one_pass.py CONFIG
+usage: [MS_DIV=d] python tools/msbfs_one_pass.py CONFIG
 """
 import os
 import sys
@@ -26,6 +26,8 @@ del ts, td
 pr = torch.empty(cfg.n, dtype=torch.float32, device="cuda")
 g.pagerank(2, 0.85, out=pr)
 out = torch.empty((len(srcs), cfg.n), dtype=torch.int32, device="cuda")
-_, st = g.bfs_multi(srcs, out=out, profile=True)
+div = int(os.environ.get("MS_DIV", "0"))  # direction threshold m / div (0: the library default)
+g.bfs_multi(srcs, out=out, threshold_div=div)
+_, st = g.bfs_multi(srcs, out=out, profile=True, threshold_div=div)
 print(f"config {ci}: k={len(srcs)} pass {sum(x.total_ms for x in st):.3f} ms, pull levels {st[0].pull_levels} "
       f"(OR {st[0].pull_or_levels}, sparse {st[0].pull_sparse_levels})")
