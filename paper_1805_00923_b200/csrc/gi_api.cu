@@ -141,6 +141,29 @@ void big_cache_note_malloc() {
   ++g_big_mallocs;
 }
 
+// frees the oldest cached block of the current device (an allocation failed):
+// false when the cache holds none; the caller retries its allocation
+bool big_cache_evict_one() {
+  int dev = -1;
+  cudaGetDevice(&dev);
+  void* p = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(g_big_mu);
+    for (size_t i = 0; i < g_big.size(); ++i)
+      if (g_big[i].dev == dev) {
+        p = g_big[i].p;
+        g_big_total -= g_big[i].bytes;
+        g_big.erase(g_big.begin() + i);
+        ++g_big_mallocs;
+        break;
+      }
+  }
+  if (!p) return false;
+  cudaDeviceSynchronize();  // a block of another stream may still be in use
+  cudaFree(p);
+  return true;
+}
+
 void big_cache_flush(cudaStream_t s) {
   int dev = -1;
   cudaGetDevice(&dev);

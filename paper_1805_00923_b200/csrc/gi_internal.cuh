@@ -84,12 +84,13 @@ struct AllocScope {
 // synchronisation is needed; cudaMalloc / cudaFree of multi-GB blocks cost
 // 10-400 ms each and stall the device (DESIGN §6 e2e). The cache holds at most
 // GI_BIGCACHE_GB (default 120) GB and never leaves less than 24 GB of the device
-// free (other allocators), is emptied when an allocation fails, and the blocks
+// free (other allocators), frees its oldest blocks one by one while an allocation fails, and the blocks
 // of a stream are freed when its context is destroyed.
 void* big_cache_get(size_t nbytes, cudaStream_t s, size_t* got);
 void big_cache_put(void* p, size_t bytes, cudaStream_t s);
 void big_cache_flush(cudaStream_t s);  // s = nullptr: every stream of the current device
 void big_cache_note_malloc();          // a large block was cudaMalloc'd (the cache re-checks free memory)
+bool big_cache_evict_one();            // frees the oldest cached block of the device (false: none left)
 // diagnostics: GI_DEBUG_SLOW_MS=t prints every allocation / free that takes longer than t ms
 double slow_ms();
 void slow_report(const char* what, size_t bytes, std::chrono::steady_clock::time_point t0);
@@ -134,9 +135,8 @@ struct DevBuf {
       p = big_cache_get(nbytes, st, &got);
       if (!p) {
         e = cudaMalloc(&p, nbytes);
-        if (e != cudaSuccess) {  // memory held by the cache: release it and retry once
-          cudaGetLastError();
-          big_cache_flush(nullptr);
+        while (e != cudaSuccess && big_cache_evict_one()) {  // memory held by the cache: free the
+          cudaGetLastError();                                // oldest blocks until the allocation fits
           e = cudaMalloc(&p, nbytes);
         }
         got = nbytes;
