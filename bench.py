@@ -107,6 +107,11 @@ def relaunch_if_needed(args):
         sys.exit(2)
 
 
+# random RED.ADD.F32 into an L2-resident 16 MB array, all SMs (tools/microbench/red_rates.cu)
+RED_PEAK_GOPS = 180.1
+RED_PEAK_SOURCE = "measured: profiles/r01_red_rates.txt (random RED.ADD.F32, 16 MB array, 148 SMs)"
+
+
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -392,6 +397,18 @@ def measure_graph(g, cfg, srcs, args, stream, dev, world, direction, gi):
                    "bytes_alg_formula": "4m + (o+12)n, o = offset bytes (SURVEY §8(d))", "launch_ms": kern_ms,
                    "vertex_ms": ps.vertex_ms / max(ps.edge_launches, 1), "peak_source": peak_src,
                    "pr_total_ms": ps.total_ms}
+    if ps.reductions_per_iter > 0:
+        # the segmented pass's second bound: one RED.ADD.F32 per piece into the L2-resident accumulator,
+        # against the measured random-RED rate of this part
+        edge_only_ms = kern_ms - roofline_pr["vertex_ms"]
+        red_gops = ps.reductions_per_iter / (edge_only_ms * 1e-3) / 1e9
+        floor_ms = ps.reductions_per_iter / (RED_PEAK_GOPS * 1e9) * 1e3 + roofline_pr["vertex_ms"]
+        roofline_pr["atomics"] = {
+            "bound": "l2_atomics", "reductions_per_launch": ps.reductions_per_iter, "edge_pass_ms": edge_only_ms,
+            "achieved": red_gops, "peak": RED_PEAK_GOPS, "unit": "Gops/s", "frac": red_gops / RED_PEAK_GOPS,
+            "peak_source": RED_PEAK_SOURCE, "iteration_floor_ms": floor_ms,
+            "hbm_frac_at_floor": ps.bytes_alg_per_iter / (floor_ms * 1e-3) / 1e9 / peak,
+            "record_bytes_per_launch": ps.stream_bytes_per_iter}
     if world > 1:
         roofline_pr["exchange"] = {0: "none", 1: "allgatherv per iteration", 2: "peer stores"}[ps.exchange]
         roofline_pr["exchange_ms_per_iter"] = ps.exchange_ms / max(ps.edge_launches, 1)

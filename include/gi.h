@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define GI_ABI_VERSION 2
+#define GI_ABI_VERSION 3
 
 #if defined(__GNUC__)
 #define GI_API __attribute__((visibility("default")))
@@ -238,6 +238,12 @@ typedef struct {
                               1 allgatherv per iteration, 2 peer stores */
   float exchange_ms;       /* profile=1: device time of the per-iteration
                               collectives (dangling allreduce + allgatherv) */
+  int64_t reductions_per_iter; /* segmented pull: global reductions (RED.ADD.F32)
+                              per edge pass = the layout's pieces, one per
+                              (source segment, destination row) pair with an
+                              edge; 0 for the other kernels */
+  int64_t stream_bytes_per_iter; /* segmented pull: record bytes streamed per
+                              edge pass; 0 for the other kernels */
 } gi_pr_stats;
 
 GI_API gi_status gi_pagerank_ex(gi_graph g, int32_t iters, double damping, const gi_pr_opts* opts,

@@ -336,6 +336,7 @@ gi_status tile_rows_launch(const void* off, bool off64, int64_t n, int64_t m, in
                            cudaStream_t st, int sms);
 // seg_acc_buf(g, cur)[v] = sum of cin over v's in-edges (the buffer is zero before the pass)
 gi_status seg_edge_pass(gi_graph g, const float* cin);
+int64_t seg_record_bytes();  // bytes per record of the segmented layout
 // a min pass over the segmented layout: acc[v] = min(acc[v], labels[u] over in-edges (u, v)) (CC, cc.cu)
 gi_status seg_min_pass(gi_graph g, const int32_t* labels, int32_t* acc);
 gi_status seg_or_pass(gi_graph g, const uint32_t* masks, uint32_t* acc);

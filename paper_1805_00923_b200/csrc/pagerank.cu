@@ -673,6 +673,10 @@ gi_status pagerank_run(gi_graph g, int32_t iters, double damping, const gi_pr_op
     for (int k = 0; k < 2; ++k) cudaEventDestroy(tot[k]);
     for (int k = 0; k < 2; ++k) cudaEventDestroy(xev[k]);
   }
+  if (kernel == GI_PR_PULL_SEGMENTED) {  // the segmented pass's per-iteration work (layout counts)
+    S.reductions_per_iter = g->seg_P;
+    S.stream_bytes_per_iter = g->seg_C * seg_record_bytes();
+  }
   if (stats) *stats = S;
   return GI_OK;
 }

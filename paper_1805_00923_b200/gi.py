@@ -55,7 +55,8 @@ class gi_pr_opts(ctypes.Structure):
 class gi_pr_stats(ctypes.Structure):
     _fields_ = [("edge_launches", ctypes.c_int32), ("aux_launches", ctypes.c_int32), ("edge_ms", ctypes.c_float),
                 ("total_ms", ctypes.c_float), ("kernel", ctypes.c_int32), ("vertex_ms", ctypes.c_float),
-                ("bytes_alg_per_iter", ctypes.c_int64), ("exchange", ctypes.c_int32), ("exchange_ms", ctypes.c_float)]
+                ("bytes_alg_per_iter", ctypes.c_int64), ("exchange", ctypes.c_int32), ("exchange_ms", ctypes.c_float),
+                ("reductions_per_iter", ctypes.c_int64), ("stream_bytes_per_iter", ctypes.c_int64)]
 
 
 GI_DT_INT32, GI_DT_INT64, GI_DT_F64 = 0, 1, 2
@@ -153,7 +154,7 @@ for _name, (_args, _res) in _SIGS.items():
     _f.restype = _res
 
 EXPORTED = tuple(_SIGS)
-GI_ABI_VERSION = 2  # include/gi.h: the struct layouts above
+GI_ABI_VERSION = 3  # include/gi.h: the struct layouts above
 if _lib.gi_abi_version() != GI_ABI_VERSION:
     raise ImportError(f"{LIB_PATH} has ABI version {_lib.gi_abi_version()}, the binding {GI_ABI_VERSION}: rebuild it")
 

@@ -50,7 +50,7 @@ def test_library_is_sm100a(gi):
 
 
 def test_status_strings_and_version(gi):
-    assert gi.gi_abi_version() == 2
+    assert gi.gi_abi_version() == 3
     for s, name in [(0, "GI_OK"), (1, "GI_ERR_INVALID_ARGUMENT"), (2, "GI_ERR_VERTEX_OUT_OF_RANGE"),
                     (4, "GI_ERR_CUDA"), (7, "GI_ERR_INTERNAL")]:
         assert gi._lib.gi_status_string(s).decode() == name

@@ -1,0 +1,8 @@
+# A/B: vertex pass (k_pr_acc) CTAs per SM and loads in flight per thread
+python -c "import __graft_entry__ as g; g.build()" > /dev/null || exit 1
+for rep in 1 2; do
+for c in 4 2; do
+for v in base acc8 accu2 accu4 acc8u2; do
+  if [ "$v" = base ]; then L=""; else L="GI_LIBGI=paper_1805_00923_b200/libgi_$v.so"; fi
+  env $L timeout 300 python tools/pr_ab.py $v $c 2>&1 | tail -1
+done; done; done
