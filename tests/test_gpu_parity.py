@@ -997,3 +997,37 @@ def test_cc_pr_share_the_segmented_layout(gi, ctx):
         assert np.abs(pr - want_pr).sum() <= 1e-5 and (np.abs(pr - want_pr) / want_pr).max() <= 1e-4, step
         par, _ = g.bfs_multi(graphgen.pick_sources(n, s, d, 8, step).tolist())  # AUTO: bit-parallel
         assert par.shape == (8, n)
+
+
+def _pieces_model(n, s, d, Z):
+    """The segmented layout's piece count from the edge list alone (test-side model, not the
+    method): vertices relabelled by descending count of edge-list entries per source (ties by id,
+    duplicates and self-loops counted), the cleaned edges' (source segment, destination) pairs."""
+    s = np.asarray(s, np.int64)
+    d = np.asarray(d, np.int64)
+    cnt = np.bincount(s, minlength=n)
+    order = np.lexsort((np.arange(n), -cnt))
+    new = np.empty(n, np.int64)
+    new[order] = np.arange(n)
+    keep = s != d
+    key = np.unique(new[d[keep]] * n + new[s[keep]])  # cleaned edges (destination, source)
+    return int(np.unique((key % n) // Z * n + key // n).size)
+
+
+def test_pr_segmented_reductions_per_iter(gi, ctx):
+    """gi_pr_stats.reductions_per_iter (the bench's atomics bound) is exactly one RED per
+    (source segment, destination row) pair with an edge, whatever the
+    destination blocking; the record stream is whole records."""
+    cfg = graphgen.CONFIGS[1]
+    s, d = cfg.edges()
+    g = gi.Graph(ctx, cfg.n, s, d)
+    m = oracle.build_graph(cfg.n, s, d).m
+    for Z, dblk in ((1000, 0), (1000, 4096), (4096, 0), (40000, 20000)):
+        _, st = g.pagerank(2, 0.85, direction=gi.GI_PR_PULL_SEGMENTED, segment_size=Z, dst_block=dblk)
+        assert st.kernel == gi.GI_PR_PULL_SEGMENTED
+        assert st.reductions_per_iter == _pieces_model(cfg.n, s, d, Z), (Z, dblk)
+        assert st.stream_bytes_per_iter > 0 and st.stream_bytes_per_iter % 1184 == 0
+        assert st.stream_bytes_per_iter >= 2 * m  # 2-byte in-segment source indices at least
+    _, st = g.pagerank(2, 0.85, direction=gi.GI_PR_PULL_DIRECT)
+    assert st.reductions_per_iter == 0 and st.stream_bytes_per_iter == 0
+    g.close()
