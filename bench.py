@@ -25,7 +25,10 @@ roofline: the pull-PageRank iteration (the north_star's >= 50% target):
          algorithmic bytes 4m + (o+12)n per iteration / its
          CUDA-event duration (edge pass + vertex pass); `traffic` = ncu DRAM
          bytes of the same kernels for this config from profiles/ncu_summary.json
-         (`traffic_source` names the capture); roofline_bfs: the bit-parallel
+         (`traffic_source` names the capture); `roofline.atomics`: the
+         segmented edge pass's second bound, its RED.ADD.F32 per piece
+         (gi_pr_stats.reductions_per_iter) against the measured random-RED
+         rate, with the iteration time that bound allows; roofline_bfs: the bit-parallel
          pull level (k_ms_pull + k_ms_pull_heavy), 4 B per in-edge read + 20 B
          per vertex.
 cpu_baseline: the oracle (oracle/, plain C, OpenMP) on a bounded sample of
