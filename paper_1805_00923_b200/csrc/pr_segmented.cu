@@ -115,8 +115,7 @@ constexpr int64_t kBlockEdges = (1ll << 31) - (1ll << 20);  // and fewer edges t
 #ifndef GI_SEG_DAMP
 #define GI_SEG_DAMP 1.0  // fraction of the way each re-balance moves a boundary
 #endif
-constexpr int kCalibPasses = GI_SEG_CALIB;        // with work stealing
-constexpr int kCalibPassesStatic = 4 * GI_SEG_CALIB;  // without (small graphs)
+constexpr int kCalibPasses = GI_SEG_CALIB;
 #ifndef GI_ACC_UNROLL
 #define GI_ACC_UNROLL 2  // config 4 vertex pass 0.113 -> 0.109 ms (1: one quad per step; 4: 0.119)
 #endif
@@ -1249,12 +1248,7 @@ static gi_status seg_build_t(gi_graph g, int Z, int64_t DB) {
   // a steal costs a segment staging and breaks the thief's contiguity)
   const int steal_mode = seg_steal();
   g->seg_steal = steal_mode == 2 || (steal_mode == 1 && C >= (int64_t)ctas * kStealMinPerCta);
-  // without stealing the static cuts alone set the balance: more calibration passes pay
-  // (config 2: 0.0867-0.0884 -> 0.0851 ms per iteration at 32, r02c_ab_config2_balance.txt)
-  g->seg_calib = getenv("GI_SEG_NO_CALIB") ? 0
-               : getenv("GI_SEG_CALIB")    ? atoi(getenv("GI_SEG_CALIB"))
-               : g->seg_steal             ? kCalibPasses
-                                           : kCalibPassesStatic;
+  g->seg_calib = getenv("GI_SEG_NO_CALIB") ? 0 : getenv("GI_SEG_CALIB") ? atoi(getenv("GI_SEG_CALIB")) : kCalibPasses;
   g->seg_acc_stride = (n + 64) & ~31ll;  // >= n + 1: row n is the trash row of padding lanes
   GI_TRY(g->seg_acc.alloc(2 * g->seg_acc_stride * sizeof(float)));
   GI_CUDA(cudaMemsetAsync(g->seg_acc.p, 0, 2 * g->seg_acc_stride * sizeof(float), st));
