@@ -57,6 +57,9 @@ constexpr int kMsT = 256;
 #ifndef GI_MS_LMINB
 #define GI_MS_LMINB 4  // min resident CTAs per SM requested from ptxas (register cap: 64) for the light pull
 #endif
+#ifndef GI_MS_OMINB
+#define GI_MS_OMINB 6  // min resident CTAs per SM for the OR level's vertex kernel (0: no cap; 6: 40 registers, config 4 1.105 -> 1.005 ms)
+#endif
 #ifndef GI_MS_HMINB
 #define GI_MS_HMINB 6  // ... and for the heavy pull (40 registers: 6 CTAs per SM hide the L2 gather latency;
                        // 13.6 vs 14.1-16.4 ms for config 4's 16-source pass)
@@ -715,7 +718,11 @@ __global__ void k_ms_narrow_or(const unsigned long long* __restrict__ f, int64_t
 // the level's vertex pass: new = acc32 & ~seen; seen, next frontier, active list,
 // counters; a light row's parents found by its thread, a heavy row queued in rlist
 template <typename OffT, typename FM>
+#if GI_MS_OMINB
+__global__ void __launch_bounds__(kMsT, GI_MS_OMINB) k_ms_or_vertex(MsArgs A) {
+#else
 __global__ void __launch_bounds__(kMsT) k_ms_or_vertex(MsArgs A) {
+#endif
   __shared__ int32_t s_buf[kMsT / 32][64], s_hbuf[kMsT / 32][64];
   int32_t* wbuf = s_buf[threadIdx.x >> 5];
   int32_t* hbuf = s_hbuf[threadIdx.x >> 5];
